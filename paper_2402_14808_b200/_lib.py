@@ -1,0 +1,93 @@
+"""ctypes binding of librelay_b200.so (the C-ABI in include/relay_b200.h).
+
+There is exactly one backend: the in-tree CUDA library.  If it is missing,
+importing this module raises -- there is no CPU fallback (the float64 CPU
+restatement under oracle/ is test infrastructure only).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ContractError, DimensionError, KernelError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librelay_b200.so")
+
+RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
+
+# every symbol include/relay_b200.h declares
+EXPORTS = (
+    "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
+    "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
+    "rb_debug_umma_probe",
+)
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -m paper_2402_14808_b200.build` "
+            "(no CPU fallback exists for the relay path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_float
+    fp = ctypes.POINTER(ctypes.c_float)
+    lib.rb_last_error.restype = ctypes.c_char_p
+    lib.rb_last_error.argtypes = []
+    lib.rb_abi_version.restype = i32
+    lib.rb_device_sm_count.argtypes = [i32, ctypes.POINTER(i32)]
+    lib.rb_sys_plan_query.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(i64),
+                                      ctypes.POINTER(ctypes.c_size_t)]
+    lib.rb_system_attention.argtypes = [
+        vp, i64, i64, i32, i32, i32, i32, vp, vp, i32, i64, i64, f32, i32, vp, vp, vp,
+        ctypes.c_size_t, vp]
+    lib.rb_context_attention.argtypes = [
+        vp, i64, i64, vp, i32, i32, i32, i32, i32,       # q .. d
+        vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
+        i32, vp, vp, i32, i64, i64,                      # causal, prefix
+        vp, vp, f32, vp, i32, vp, vp]                    # o_sys .. stream
+    lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
+    lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
+    lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+    for name in EXPORTS:
+        if name not in ("rb_last_error", "rb_abi_version"):
+            getattr(lib, name).restype = i32
+    if lib.rb_abi_version() != 1:
+        raise ImportError("librelay_b200.so ABI mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == RB_OK:
+        return
+    msg = load().rb_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if status == RB_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if status == RB_ERR_CONTRACT:
+        raise ContractError(msg)
+    raise KernelError(msg)
+
+
+def sys_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
+    """(fields dict, workspace bytes) of rb_system_attention's stream-K plan."""
+    f = (ctypes.c_longlong * 8)()
+    ws = ctypes.c_size_t(0)
+    check(load().rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, ctypes.byref(ws)),
+          "rb_sys_plan_query")
+    keys = ("nq", "n_qt", "tpu", "n_units", "total", "grid", "max_parts")
+    return dict(zip(keys, list(f)[:7])), ws.value
+
+
+def sm_count(device: int = 0) -> int:
+    out = ctypes.c_int(0)
+    check(load().rb_device_sm_count(device, ctypes.byref(out)), "rb_device_sm_count")
+    return out.value

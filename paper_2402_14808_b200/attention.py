@@ -1,0 +1,450 @@
+"""RelayAttention operator API on B200 -- a drop-in for the reference's
+`relayserve.attention` hot path (/root/reference/pkg/src/relayserve/attention.py).
+
+Same names, argument meaning and error behaviour as the reference:
+
+  TrafficCounter, LseAttentionOutput          attention.py:28-69
+  naive_causal_attention(q, k, v)             attention.py:72-93
+  attention_with_lse(q, k, v, causal)         attention.py:96-134
+  relay_fusion(o_sys, lse_sys, o_ctx, lse_ctx)  attention.py:137-157
+  relay_attention_ragged(...)                 attention.py:203-243
+  relay_attention(...)                        attention.py:246-263
+  baseline_attention_ragged / baseline_attention  attention.py:266-296
+
+Inputs may be numpy arrays (the reference's float64 convention; results
+come back as float64 numpy) or torch tensors (results stay on the GPU, fp32).
+Either way the arithmetic runs in the sm_100a kernels of librelay_b200.so:
+bf16 operands, fp32 accumulation and softmax, natural-log LSE.  Extensions
+over the reference: GQA (query heads a multiple of KV heads; the reference
+raises DimensionError, attention.py:109-110), and `return_lse` on the relay
+entry points (the fused LSE = logaddexp(lse_sys, lse_ctx)).
+
+Paged-native fast path for serving / benchmarking: RelayDecodeStep and
+NaiveDecodeStep run one decode step over a SystemKvCache + PagedKvCache
+with preallocated buffers (CUDA-graph capturable).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels
+from .errors import ContractError, DimensionError
+
+HEAD_DIM = kernels.HEAD_DIM
+
+
+@dataclass
+class TrafficCounter:
+    """Per-step element-access accounting (attention.py:28-57): one attended
+    position costs h*d elements for its K/V pair; LSE scalars are separate."""
+
+    elements_read: int = 0
+    elements_written: int = 0
+    lse_elements: int = 0
+
+    def add_load(self, n: int):
+        self.elements_read += n
+
+    def add_store(self, n: int):
+        self.elements_read += n
+        self.elements_written += n
+
+    def add_lse(self, n: int):
+        self.lse_elements += n
+
+    def reset(self):
+        self.elements_read = 0
+        self.elements_written = 0
+        self.lse_elements = 0
+
+
+@dataclass
+class LseAttentionOutput:
+    """output (b, m, h, d) and lse (b, m, h)."""
+
+    output: object
+    lse: object
+
+
+# ----------------------------------------------------------------- helpers
+
+def _is_numpy(x):
+    return isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor)
+
+
+def _device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _shape(x):
+    return tuple(x.shape) if hasattr(x, "shape") else tuple(np.shape(x))
+
+
+def _ndim(x, nd, name):
+    if len(_shape(x)) != nd:
+        raise DimensionError(f"{name}: expected {nd} dimensions, got {len(_shape(x))}")
+
+
+def _to_dev_bf16(x, device):
+    """Any array -> CUDA bf16, head_dim zero-padded to 128 (exact)."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device)
+    d = t.shape[-1]
+    if d > HEAD_DIM:
+        raise DimensionError(f"head_dim {d} > {HEAD_DIM} is not supported")
+    t = t.to(torch.bfloat16)
+    if d < HEAD_DIM:
+        t = torch.nn.functional.pad(t, (0, HEAD_DIM - d))
+    return t.contiguous()
+
+
+def _out(t, d, like_numpy):
+    t = t[..., :d] if t.shape[-1] != d else t
+    if like_numpy:
+        return t.detach().to("cpu", torch.float64).numpy()
+    return t
+
+
+def _lse_out(t, like_numpy):
+    if like_numpy:
+        return t.detach().to("cpu", torch.float64).numpy()
+    return t
+
+
+# ------------------------------------------------------------------- ops
+
+def attention_with_lse(q, k, v, causal):
+    """Scaled dot-product attention with per-query natural-log LSE.
+
+    q: (b, m, h, d); k, v: (b, n, h_kv, d).  causal=True: query t attends
+    keys 0..(n - m + t) (attention.py:120-121); causal=False: all n keys.
+    b == 1 and not causal (the shared-prefix case, attention.py:184-185)
+    runs the tcgen05 system kernel; everything else the context kernel.
+    """
+    _ndim(q, 4, "q")
+    _ndim(k, 4, "k")
+    _ndim(v, 4, "v")
+    qs, ks = _shape(q), _shape(k)
+    b, m, h, d = qs
+    if ks != _shape(v):
+        raise DimensionError(f"k/v shapes differ: {ks} vs {_shape(v)}")
+    if ks[0] != b or ks[3] != d or ks[2] < 1 or h % ks[2] != 0:
+        raise DimensionError(f"k {ks} incompatible with q {qs}")
+    n, hkv = ks[1], ks[2]
+    if n < 1:
+        raise ContractError("attention requires at least one key")
+    if causal and n < m:
+        raise ContractError(f"causal attention needs n >= m, got n={n}, m={m}")
+    like_np = _is_numpy(q)
+    dev = q.device if isinstance(q, torch.Tensor) else _device()
+    scale = 1.0 / math.sqrt(d)
+    qd = _to_dev_bf16(q, dev).reshape(b * m, h, HEAD_DIM)
+    kd = _to_dev_bf16(k, dev)
+    vd = _to_dev_bf16(v, dev)
+    if b == 1 and not causal:
+        o, lse = kernels.system_attention(qd, kd[0], vd[0], kv_layout="shd", scale=scale)
+    else:
+        q_start = torch.arange(0, b * m + 1, m, dtype=torch.int32, device=dev)
+        req_off = torch.arange(0, b * n, n, dtype=torch.int64, device=dev)
+        lens = torch.full((b,), n, dtype=torch.int32, device=dev)
+        kf = kd.reshape(b * n, hkv, HEAD_DIM)
+        vf = vd.reshape(b * n, hkv, HEAD_DIM)
+        o, lse = kernels.context_attention(
+            qd, q_start, kf, vf, lens, max_rows=m * (h // hkv), hkv=hkv, req_offset=req_off,
+            strides=(0, kf.stride(0), kf.stride(1)), causal=causal, scale=scale, out_fp32=True)
+    return LseAttentionOutput(output=_out(o.reshape(b, m, h, HEAD_DIM), d, like_np),
+                              lse=_lse_out(lse.reshape(b, m, h), like_np))
+
+
+def naive_causal_attention(q, k, v):
+    """Brute-force-equivalent causal self-attention over one sequence
+    (attention.py:72-93): q, k, v (l, h, d); position t attends 0..t."""
+    _ndim(q, 3, "q")
+    _ndim(k, 3, "k")
+    _ndim(v, 3, "v")
+    if not (_shape(q) == _shape(k) == _shape(v)):
+        raise DimensionError(f"q/k/v shapes differ: {_shape(q)}, {_shape(k)}, {_shape(v)}")
+    res = attention_with_lse(q[None], k[None], v[None], causal=True)
+    return res.output[0]
+
+
+def relay_fusion(o_sys, lse_sys, o_ctx, lse_ctx):
+    """alpha_sys = 1/(1+exp(lse_ctx - lse_sys)); o = alpha*o_sys + (1-alpha)*o_ctx
+    (attention.py:137-157), on the GPU in fp32 with max-subtracted weights."""
+    _ndim(o_sys, 4, "o_sys")
+    _ndim(o_ctx, 4, "o_ctx")
+    _ndim(lse_sys, 3, "lse_sys")
+    _ndim(lse_ctx, 3, "lse_ctx")
+    if _shape(o_sys) != _shape(o_ctx):
+        raise DimensionError(f"output shapes differ: {_shape(o_sys)} vs {_shape(o_ctx)}")
+    if _shape(lse_sys) != _shape(lse_ctx) or _shape(lse_sys) != _shape(o_sys)[:3]:
+        raise DimensionError("lse shapes must match output batch/query/head dims")
+    like_np = _is_numpy(o_sys)
+    dev = o_sys.device if isinstance(o_sys, torch.Tensor) else _device()
+
+    def f32(x):
+        if isinstance(x, torch.Tensor):
+            return x.to(device=dev, dtype=torch.float32).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+
+    out, _ = kernels.relay_fusion_fp32(f32(o_sys), f32(lse_sys), f32(o_ctx), f32(lse_ctx))
+    return out.to("cpu", torch.float64).numpy() if like_np else out
+
+
+def _count_relay(counter, m_list, c_list, s, h, d):
+    """TrafficCounter updates of attention.py:168-173, 186-192, 238-242."""
+    hd = h * d
+    for m, c in zip(m_list, c_list):
+        counter.add_load(m * hd)
+        counter.add_load(c * hd)
+        counter.add_store(m * hd)
+        counter.add_lse(m * h)
+    total_m = sum(m_list)
+    counter.add_load(total_m * hd)
+    counter.add_load(s * hd)
+    counter.add_store(total_m * hd)
+    counter.add_lse(total_m * h)
+    for m in m_list:
+        counter.add_load(2 * m * h * d)
+        counter.add_store(m * h * d)
+        counter.add_lse(2 * m * h)
+
+
+def relay_attention_ragged(q_list, sys_k, sys_v, ctx_k, ctx_v, counter=None,
+                           system_first=False, return_lse=False):
+    """Relay attention for requests with different query counts
+    (attention.py:203-243).  q_list[r]: (m_r, h, d); ctx_k[r]/ctx_v[r]:
+    (c_r, h_kv, d) including the current tokens; sys_k/sys_v: (s, h_kv, d),
+    s >= 1.  Equals causal attention over [system || context] per request.
+
+    The system segment runs once for the whole batch (tcgen05 kernel), the
+    context segment and the fusion run in one paged kernel.  Fusion is a
+    single deterministic LSE merge, so `system_first` cannot change the
+    result (the reference's bitwise order-independence, attention.py:208-212).
+    """
+    _ndim(sys_k, 3, "sys_k")
+    _ndim(sys_v, 3, "sys_v")
+    if _shape(sys_k) != _shape(sys_v):
+        raise DimensionError(f"sys_k/sys_v shapes differ: {_shape(sys_k)} vs {_shape(sys_v)}")
+    if _shape(sys_k)[0] < 1:
+        raise ContractError("relay attention requires a non-empty system segment; "
+                            "use the baseline path when there is no shared prefix")
+    if not (len(q_list) == len(ctx_k) == len(ctx_v)):
+        raise DimensionError("one context k/v pair required per request")
+    for qr in q_list:
+        _ndim(qr, 3, "q")
+    for kr in list(ctx_k) + list(ctx_v):
+        _ndim(kr, 3, "ctx_k")
+    s, hkv, d = _shape(sys_k)
+    b = len(q_list)
+    m_list = [_shape(qr)[0] for qr in q_list]
+    c_list = [_shape(kr)[0] for kr in ctx_k]
+    h = _shape(q_list[0])[1] if b else hkv
+    for qr, kr, vr in zip(q_list, ctx_k, ctx_v):
+        if _shape(qr)[1:] != (h, d) or _shape(kr)[1:] != (hkv, d) or _shape(kr) != _shape(vr):
+            raise DimensionError("q/context shapes inconsistent with the system cache")
+    if hkv < 1 or h % hkv != 0:
+        raise DimensionError(f"query heads {h} not a multiple of kv heads {hkv}")
+    for m, c in zip(m_list, c_list):
+        if c < m:
+            raise ContractError(f"causal attention needs n >= m, got n={c}, m={m}")
+    if b == 0:
+        return ([], []) if return_lse else []
+    like_np = _is_numpy(q_list[0])
+    dev = q_list[0].device if isinstance(q_list[0], torch.Tensor) else _device()
+    scale = 1.0 / math.sqrt(d)
+
+    def cat(lst):
+        if isinstance(lst[0], torch.Tensor):
+            return torch.cat([x.to(dev) for x in lst], 0)
+        return np.concatenate([np.asarray(x) for x in lst], 0)
+
+    qf = _to_dev_bf16(cat(q_list), dev)
+    skd = _to_dev_bf16(sys_k, dev)
+    svd = _to_dev_bf16(sys_v, dev)
+    ckd = _to_dev_bf16(cat(list(ctx_k)), dev)
+    cvd = _to_dev_bf16(cat(list(ctx_v)), dev)
+    q_start = torch.tensor(np.concatenate([[0], np.cumsum(m_list)]), dtype=torch.int32, device=dev)
+    req_off = torch.tensor(np.concatenate([[0], np.cumsum(c_list)[:-1]]), dtype=torch.int64,
+                           device=dev)
+    lens = torch.tensor(c_list, dtype=torch.int32, device=dev)
+
+    o_sys, lse_sys = kernels.system_attention(qf, skd, svd, kv_layout="shd", scale=scale)
+    out, lse = kernels.context_attention(
+        qf, q_start, ckd, cvd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv,
+        req_offset=req_off, strides=(0, ckd.stride(0), ckd.stride(1)), causal=True,
+        o_sys=o_sys, lse_sys=lse_sys, scale=scale, out_fp32=True)
+    if counter is not None:
+        _count_relay(counter, m_list, c_list, s, h, d)
+    outs, lses, row = [], [], 0
+    for m in m_list:
+        outs.append(_out(out[row:row + m], d, like_np))
+        lses.append(_lse_out(lse[row:row + m], like_np))
+        row += m
+    return (outs, lses) if return_lse else outs
+
+
+def relay_attention(q, sys_k, sys_v, ctx_k, ctx_v, counter=None, system_first=False,
+                    return_lse=False):
+    """Uniform-batch relay attention (attention.py:246-263).
+    q: (b, m, h, d); ctx_k[r]/ctx_v[r]: (c_r, h_kv, d)."""
+    _ndim(q, 4, "q")
+    b = _shape(q)[0]
+    if len(ctx_k) != b or len(ctx_v) != b:
+        raise DimensionError(f"expected {b} context caches, got {len(ctx_k)}/{len(ctx_v)}")
+    res = relay_attention_ragged([q[r] for r in range(b)], sys_k, sys_v, ctx_k, ctx_v,
+                                 counter=counter, system_first=system_first,
+                                 return_lse=return_lse)
+    stack = (lambda xs: np.stack(xs, 0)) if _is_numpy(q) else (lambda xs: torch.stack(xs, 0))
+    if return_lse:
+        return stack(res[0]), stack(res[1])
+    return stack(res)
+
+
+def baseline_attention_ragged(q_list, full_k, full_v, counter=None):
+    """Per-request causal attention over each request's full cache
+    (attention.py:266-288) -- the shared prefix replicated per request."""
+    if not (len(q_list) == len(full_k) == len(full_v)):
+        raise DimensionError("one k/v pair required per request")
+    outs = []
+    for qr, kr, vr in zip(q_list, full_k, full_v):
+        _ndim(qr, 3, "q")
+        _ndim(kr, 3, "k")
+        _ndim(vr, 3, "v")
+    b = len(q_list)
+    if b == 0:
+        return outs
+    m_list = [_shape(x)[0] for x in q_list]
+    n_list = [_shape(x)[0] for x in full_k]
+    h, d = _shape(q_list[0])[1:]
+    hkv = _shape(full_k[0])[1]
+    for m, n in zip(m_list, n_list):
+        if n < 1:
+            raise ContractError("attention requires at least one key")
+        if n < m:
+            raise ContractError(f"causal attention needs n >= m, got n={n}, m={m}")
+    like_np = _is_numpy(q_list[0])
+    dev = q_list[0].device if isinstance(q_list[0], torch.Tensor) else _device()
+
+    def cat(lst):
+        if isinstance(lst[0], torch.Tensor):
+            return torch.cat([x.to(dev) for x in lst], 0)
+        return np.concatenate([np.asarray(x) for x in lst], 0)
+
+    qf = _to_dev_bf16(cat(q_list), dev)
+    kd = _to_dev_bf16(cat(list(full_k)), dev)
+    vd = _to_dev_bf16(cat(list(full_v)), dev)
+    q_start = torch.tensor(np.concatenate([[0], np.cumsum(m_list)]), dtype=torch.int32, device=dev)
+    req_off = torch.tensor(np.concatenate([[0], np.cumsum(n_list)[:-1]]), dtype=torch.int64,
+                           device=dev)
+    lens = torch.tensor(n_list, dtype=torch.int32, device=dev)
+    out, _ = kernels.context_attention(
+        qf, q_start, kd, vd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv, req_offset=req_off,
+        strides=(0, kd.stride(0), kd.stride(1)), causal=True, scale=1.0 / math.sqrt(d),
+        out_fp32=True, want_lse=False)
+    if counter is not None:
+        for m, n in zip(m_list, n_list):
+            hd = h * d
+            counter.add_load(m * hd)
+            counter.add_load(n * hd)
+            counter.add_store(m * hd)
+    row = 0
+    for m in m_list:
+        outs.append(_out(out[row:row + m], d, like_np))
+        row += m
+    return outs
+
+
+def baseline_attention(q, full_k, full_v, counter=None):
+    """Uniform-batch baseline (attention.py:291-296)."""
+    _ndim(q, 4, "q")
+    outs = baseline_attention_ragged([q[r] for r in range(_shape(q)[0])], full_k, full_v,
+                                     counter=counter)
+    return np.stack(outs, 0) if _is_numpy(q) else torch.stack(outs, 0)
+
+
+# ------------------------------------------------------ paged decode steps
+
+class RelayDecodeStep:
+    """One relay decode step (m = 1 token per request) over resident caches.
+
+    q: (b, hq, 128) bf16 -> out (b, hq, 128) bf16 and fused lse (b, hq) fp32.
+    Launches exactly two kernels on the current stream: the tcgen05 system
+    kernel (shared prefix read once) and the paged context kernel with the
+    relay fusion in its epilogue.  All buffers are preallocated, so the step
+    can be captured in a CUDA graph.
+    """
+
+    def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
+                 grid=None, out_dtype=torch.bfloat16):
+        self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
+        self.block_table = block_table
+        self.ctx_lens = ctx_lens
+        self.b = ctx_lens.numel()
+        self.hq = hq
+        self.hkv = sys_cache.kv_heads
+        if hq % self.hkv != 0 or paged_cache.kv_heads != self.hkv:
+            raise DimensionError("query heads must be a multiple of the (shared) kv heads")
+        dev = block_table.device
+        self.grid = kernels.sm_count(dev) if grid is None else grid
+        from . import _lib
+        self.plan, need = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
+        self.o_sys = torch.empty((self.b, hq, HEAD_DIM), dtype=torch.float32, device=dev)
+        self.lse_sys = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
+        self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
+        self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
+        self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
+
+    def system(self, q):
+        return kernels.system_attention(
+            q, self.sys_cache.keys[self.layer], self.sys_cache.values[self.layer],
+            kv_layout="hsd", grid=self.grid, o_sys=self.o_sys, lse_sys=self.lse_sys, ws=self.ws)
+
+    def context(self, q):
+        return kernels.context_attention(
+            q, self.q_start, self.paged.k_pool[self.layer], self.paged.v_pool[self.layer],
+            self.ctx_lens, max_rows=self.hq // self.hkv, hkv=self.hkv,
+            block_table=self.block_table, block_size=self.paged.block_size,
+            strides=self.paged.strides(), causal=True, o_sys=self.o_sys, lse_sys=self.lse_sys,
+            out=self.out, lse_out=self.lse)
+
+    def __call__(self, q):
+        self.system(q)
+        return self.context(q)
+
+
+class NaiveDecodeStep:
+    """The per-request baseline step ("vLLM-PS"; reference
+    `baseline_attention`): every request re-reads the shared prefix (stored
+    once, in the SystemKvCache) and then its own paged context, in one
+    paged kernel without fusion.  Same inputs/outputs as RelayDecodeStep."""
+
+    def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
+                 out_dtype=torch.bfloat16):
+        self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
+        self.block_table, self.ctx_lens = block_table, ctx_lens
+        self.b = ctx_lens.numel()
+        self.hq, self.hkv = hq, sys_cache.kv_heads
+        dev = block_table.device
+        self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
+        self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
+        self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
+
+    def __call__(self, q):
+        pk = self.sys_cache.keys[self.layer]
+        pv = self.sys_cache.values[self.layer]
+        return kernels.context_attention(
+            q, self.q_start, self.paged.k_pool[self.layer], self.paged.v_pool[self.layer],
+            self.ctx_lens, max_rows=self.hq // self.hkv, hkv=self.hkv,
+            block_table=self.block_table, block_size=self.paged.block_size,
+            strides=self.paged.strides(), causal=True, prefix_k=pk, prefix_v=pv,
+            prefix_strides=(pk.stride(1), pk.stride(0), pk.shape[1]),
+            out=self.out, lse_out=self.lse)

@@ -1,0 +1,266 @@
+// C-ABI boundary of librelay_b200.so (declared in include/relay_b200.h).
+//
+// Replaces the reference's kernel boundary, the `relayserve.kernels` module
+// (/root/reference/pkg/src/relayserve/kernels.py:14-37), one level up: the
+// entry points take whole attention segments instead of per-head matmul /
+// softmax calls.  Conventions: plain pointers and sizes, caller-allocated
+// outputs and workspace, stream-ordered asynchronous launches, int status
+// (0 = ok) with the message in rb_last_error(); RB_ERR_DIMENSION and
+// RB_ERR_CONTRACT mirror relayserve.errors.DimensionError / ContractError
+// (errors.py:4-9).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/relay_b200.h"
+#include "rb_common.cuh"
+#include "rb_plan.h"
+#include "rb_args.cuh"
+
+namespace rb {
+cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
+                                    cudaStream_t);
+cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
+cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
+                                float*, long long, int, cudaStream_t);
+cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
+                              const __nv_bfloat16*, int, float*, float*, cudaStream_t);
+cudaError_t launch_kv_append(const __nv_bfloat16*, const __nv_bfloat16*, const int*,
+                             __nv_bfloat16*, __nv_bfloat16*, int, int, int, long long, long long,
+                             long long, cudaStream_t);
+}  // namespace rb
+
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return RB_OK;
+  return fail(RB_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+extern "C" {
+
+const char* rb_last_error(void) { return g_err.c_str(); }
+
+int rb_abi_version(void) { return RB_ABI_VERSION; }
+
+int rb_device_sm_count(int device, int* out) {
+  int v = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  *out = v;
+  return RB_OK;
+}
+
+int rb_sys_plan_query(int n_rows, int hq, int hkv, int s, int grid_cap, long long* fields,
+                      size_t* workspace_bytes) {
+  if (n_rows < 1 || hq < 1 || hkv < 1) return fail(RB_ERR_DIMENSION, "empty query set");
+  if (hq % hkv != 0) return fail(RB_ERR_DIMENSION, "hq=%d not a multiple of hkv=%d", hq, hkv);
+  if (s < 1)
+    return fail(RB_ERR_CONTRACT,
+                "relay attention requires a non-empty system segment; use the baseline path "
+                "when there is no shared prefix");
+  rb_sys_plan p;
+  rb_make_sys_plan(&p, n_rows, hq, hkv, s, grid_cap);
+  if (fields) {
+    fields[0] = p.nq;
+    fields[1] = p.n_qt;
+    fields[2] = p.tpu;
+    fields[3] = p.n_units;
+    fields[4] = p.total;
+    fields[5] = p.grid;
+    fields[6] = p.max_parts;
+  }
+  if (workspace_bytes) {
+    size_t cnt = ((size_t)p.n_units * sizeof(int) + 255) & ~(size_t)255;
+    size_t ml = p.max_parts > 1 ? (size_t)p.n_units * p.max_parts * 2 * p.nq * sizeof(float) : 0;
+    ml = (ml + 255) & ~(size_t)255;
+    size_t acc = p.max_parts > 1
+                     ? (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float)
+                     : 0;
+    *workspace_bytes = cnt + ml + acc;
+  }
+  return RB_OK;
+}
+
+// ------------------------------------------------------------ TMA maps
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static int make_kv_map(CUtensorMap* map, const void* base, int s, int hkv, long long stride_tok,
+                       long long stride_head) {
+  auto enc = get_encode();
+  if (!enc) return fail(RB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(RB_ERR_CONTRACT, "system K/V base must be 16-byte aligned");
+  if ((stride_tok * 2) % 16 != 0 || (stride_head * 2) % 16 != 0)
+    return fail(RB_ERR_CONTRACT, "system K/V strides must be multiples of 8 elements");
+  cuuint64_t dims[3] = {RB_HEAD_DIM, (cuuint64_t)s, (cuuint64_t)hkv};
+  cuuint64_t strides[2] = {(cuuint64_t)(stride_tok * 2), (cuuint64_t)(stride_head * 2)};
+  cuuint32_t box[3] = {64, RB_KEY_TILE, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RB_OK;
+}
+
+// ------------------------------------------------------ system attention
+int rb_system_attention(const void* q, long long q_row_stride, long long q_head_stride,
+                        int n_rows, int hq, int hkv, int d, const void* sys_k, const void* sys_v,
+                        int s, long long kv_stride_tok, long long kv_stride_head, float scale,
+                        int grid_cap, float* o_sys, float* lse_sys, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
+  size_t need = 0;
+  long long f[8];
+  int st = rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, &need);
+  if (st != RB_OK) return st;
+  if (workspace_bytes < need)
+    return fail(RB_ERR_CONTRACT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  if ((q_head_stride * 2) % 16 != 0 || (q_row_stride * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(q) & 15))
+    return fail(RB_ERR_CONTRACT, "q rows must be 16-byte aligned");
+  rb::SysArgs a;
+  rb_make_sys_plan(&a.plan, n_rows, hq, hkv, s, grid_cap);
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.q_row_stride = q_row_stride;
+  a.q_head_stride = q_head_stride;
+  a.scale_log2 = scale * rb::kLog2e;
+  a.o_sys = o_sys;
+  a.lse_sys = lse_sys;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  size_t cnt = ((size_t)a.plan.n_units * sizeof(int) + 255) & ~(size_t)255;
+  size_t ml = a.plan.max_parts > 1
+                  ? (size_t)a.plan.n_units * a.plan.max_parts * 2 * a.plan.nq * sizeof(float)
+                  : 0;
+  ml = (ml + 255) & ~(size_t)255;
+  a.counters = reinterpret_cast<int*>(ws);
+  a.part_ml = reinterpret_cast<float*>(ws + cnt);
+  a.part_acc = reinterpret_cast<float*>(ws + cnt + ml);
+  CUtensorMap tk, tv;
+  st = make_kv_map(&tk, sys_k, s, hkv, kv_stride_tok, kv_stride_head);
+  if (st != RB_OK) return st;
+  st = make_kv_map(&tv, sys_v, s, hkv, kv_stride_tok, kv_stride_head);
+  if (st != RB_OK) return st;
+  return cuda_status(rb::launch_system_attention(tk, tv, a, static_cast<cudaStream_t>(stream)),
+                     "system attention launch");
+}
+
+// ----------------------------------------------------- context attention
+int rb_context_attention(const void* q, long long q_row_stride, long long q_head_stride,
+                         const int* q_start, int b, int max_rows, int hq, int hkv, int d,
+                         const void* k, const void* v, const int* block_table, int bt_stride,
+                         int block_size, const long long* req_offset, long long stride_block,
+                         long long stride_tok, long long stride_head, const int* ctx_lens,
+                         int causal, const void* prefix_k, const void* prefix_v, int s_prefix,
+                         long long p_stride_tok, long long p_stride_head, const float* o_sys,
+                         const float* lse_sys, float scale, void* out, int out_fp32,
+                         float* lse_out, void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
+  if (b < 1) return RB_OK;
+  if (hq < 1 || hkv < 1 || hq % hkv != 0)
+    return fail(RB_ERR_DIMENSION, "hq=%d must be a positive multiple of hkv=%d", hq, hkv);
+  if (block_table == nullptr && req_offset == nullptr)
+    return fail(RB_ERR_CONTRACT, "either block_table (paged) or req_offset (ragged) is required");
+  if (block_table != nullptr && block_size < 1)
+    return fail(RB_ERR_CONTRACT, "block_size must be >= 1");
+  if ((o_sys == nullptr) != (lse_sys == nullptr))
+    return fail(RB_ERR_CONTRACT, "o_sys and lse_sys go together");
+  if (s_prefix > 0 && (prefix_k == nullptr || prefix_v == nullptr))
+    return fail(RB_ERR_CONTRACT, "prefix K/V required when s_prefix > 0");
+  rb::CtxArgs a;
+  a.b = b;
+  a.hq = hq;
+  a.hkv = hkv;
+  a.g = hq / hkv;
+  a.q_start = q_start;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.q_row_stride = q_row_stride;
+  a.q_head_stride = q_head_stride;
+  a.ctx.k = static_cast<const __nv_bfloat16*>(k);
+  a.ctx.v = static_cast<const __nv_bfloat16*>(v);
+  a.ctx.block_table = block_table;
+  a.ctx.bt_stride = bt_stride;
+  a.ctx.block_size = block_size;
+  a.ctx.req_offset = req_offset;
+  a.ctx.stride_block = stride_block;
+  a.ctx.stride_tok = stride_tok;
+  a.ctx.stride_head = stride_head;
+  a.ctx_lens = ctx_lens;
+  a.causal = causal;
+  a.pk = static_cast<const __nv_bfloat16*>(prefix_k);
+  a.pv = static_cast<const __nv_bfloat16*>(prefix_v);
+  a.p_stride_tok = p_stride_tok;
+  a.p_stride_head = p_stride_head;
+  a.s_prefix = s_prefix;
+  a.o_sys = o_sys;
+  a.lse_sys = lse_sys;
+  a.out = out;
+  a.out_fp32 = out_fp32;
+  a.lse_out = lse_out;
+  a.scale_log2 = scale * rb::kLog2e;
+  return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
+                     "context attention launch");
+}
+
+int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx,
+                    const float* lse_ctx, float* out, float* lse_out, long long n_vec, int d,
+                    void* stream) {
+  if (n_vec < 0 || d < 1) return fail(RB_ERR_DIMENSION, "bad fusion shape");
+  return cuda_status(rb::launch_relay_fusion(o_sys, lse_sys, o_ctx, lse_ctx, out, lse_out, n_vec,
+                                             d, static_cast<cudaStream_t>(stream)),
+                     "relay fusion launch");
+}
+
+int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, int n_tok,
+                 void* k_pool, void* v_pool, int hkv, int d, int block_size,
+                 long long stride_block, long long stride_tok, long long stride_head,
+                 void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported", d);
+  return cuda_status(
+      rb::launch_kv_append(static_cast<const __nv_bfloat16*>(k_new),
+                           static_cast<const __nv_bfloat16*>(v_new), slot_mapping,
+                           static_cast<__nv_bfloat16*>(k_pool), static_cast<__nv_bfloat16*>(v_pool),
+                           n_tok, hkv, block_size, stride_block, stride_tok, stride_head,
+                           static_cast<cudaStream_t>(stream)),
+      "kv append launch");
+}
+
+int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void* p, int nq,
+                        float* s_out, float* o_out, void* stream) {
+  return cuda_status(
+      rb::launch_umma_probe(static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(q),
+                            static_cast<const __nv_bfloat16*>(v), static_cast<const __nv_bfloat16*>(p),
+                            nq, s_out, o_out, static_cast<cudaStream_t>(stream)),
+      "umma probe launch");
+}
+
+}  // extern "C"

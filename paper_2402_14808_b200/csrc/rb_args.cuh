@@ -1,0 +1,57 @@
+// Kernel argument structs shared by the kernel translation units and the
+// C-ABI layer (capi.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include "rb_plan.h"
+
+namespace rb {
+
+struct SysArgs {
+  rb_sys_plan plan;
+  const __nv_bfloat16* q;  // row r, head h at q + r*q_row_stride + h*q_head_stride
+  long long q_row_stride;
+  long long q_head_stride;
+  float scale_log2;        // (1/sqrt(d)) * log2(e)
+  float* o_sys;            // fp32 [n_rows][hq][128], normalised
+  float* lse_sys;          // fp32 [n_rows][hq], natural log
+  float* part_acc;         // fp32 [n_units][max_parts][nq][128] (unnormalised)
+  float* part_ml;          // fp32 [n_units][max_parts][2][nq]   (m log2, l)
+  int* counters;           // int  [n_units], zero between launches
+};
+
+struct KvView {
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  const int* block_table;        // paged mode if non-null: [b][bt_stride]
+  int bt_stride;
+  int block_size;
+  const long long* req_offset;   // ragged mode: first token index of request r
+  long long stride_block;        // elements (paged)
+  long long stride_tok;          // elements
+  long long stride_head;         // elements
+};
+
+struct CtxArgs {
+  int b, hq, hkv, g;
+  const int* q_start;            // [b+1] flat row offsets (m_r = q_start[r+1]-q_start[r])
+  const __nv_bfloat16* q;
+  long long q_row_stride, q_head_stride;
+  KvView ctx;
+  const int* ctx_lens;           // [b]
+  int causal;                    // 1: row t sees keys < c_r - m_r + t + 1; 0: all c_r
+  // optional shared prefix (naive baseline), contiguous per head
+  const __nv_bfloat16* pk;
+  const __nv_bfloat16* pv;
+  long long p_stride_tok, p_stride_head;
+  int s_prefix;
+  // optional system partial (relay)
+  const float* o_sys;            // [n_rows][hq][128]
+  const float* lse_sys;          // [n_rows][hq] natural log
+  // outputs
+  void* out;                     // [n_rows][hq][128] bf16 or fp32
+  int out_fp32;
+  float* lse_out;                // [n_rows][hq] natural log (may be null)
+  float scale_log2;
+};
+
+}  // namespace rb

@@ -1,0 +1,584 @@
+// System-prompt attention on sm_100a: tcgen05 + TMA + TMEM.
+//
+// Computes, for every query row of the batch (all requests' new tokens
+// flattened, as in /root/reference/pkg/src/relayserve/attention.py:183-185)
+// and every query head, one UNMASKED attention pass over the shared prefix
+// K/V with natural-log LSE -- the reference's `_system_attention`
+// (attention.py:177-200) / `attention_with_lse(causal=False)`
+// (attention.py:96-134, kernels _kernels_cy.pyx:13-51).
+//
+// Design:
+//  * swap-AB: the MMA M dimension is the 128 keys of a tile, N is the
+//    (request x GQA-group) query rows of one KV head (nq = 16/32/64), so a
+//    batch of 32 decode rows still fills M = 128:
+//        S^T[128 keys x nq] = K_tile[128 x d] . Q^T        (both K-major)
+//        O^T[d x nq]       = V_tile^T[d x 128] . P^T       (A MN-major)
+//    accumulators in TMEM (2 S buffers + 2 O buffers = 4*nq columns).
+//  * K/V tiles (128 keys x 128 d bf16 = 32 KB each) are TMA-loaded with the
+//    128B swizzle through a STAGES-deep mbarrier ring: every shared-prefix
+//    byte crosses HBM exactly once per step.
+//  * warp roles: warp 0 TMA producer (+ Q rows), warp 1 MMA issuer (one
+//    thread) + TMEM owner, warps 2..9 softmax / O accumulation.  Thread t of
+//    a compute warp owns TMEM lane t of its quadrant = key t of the tile for
+//    S, = head-dim index t for O.
+//  * online softmax in the log2 domain: per-query max / sum across the 128
+//    key lanes via a warp reduce-scatter butterfly + a 4-warp smem combine;
+//    O accumulates in registers (acc = acc*alpha + O_tile), so the tensor
+//    core never waits for a rescale.
+//  * persistent stream-K over (kv head, query tile, key tile): one CTA per
+//    SM, contiguous equal tile ranges, per-unit semaphore merge of partial
+//    (acc, m, l) in fixed slot order -> deterministic output.
+#include "rb_common.cuh"
+#include "rb_plan.h"
+#include "rb_args.cuh"
+
+namespace rb {
+
+
+constexpr int kSysThreads = 320;  // 10 warps
+constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
+constexpr int kStageBytes = 2 * kKvTileBytes;               // K + V
+
+template <int NQ, int STAGES>
+struct SysSmem {
+  static constexpr int H = NQ / 2;                 // columns per compute warp
+  static constexpr int kQBytes = NQ * 256;         // [2 kblocks][NQ][128 B]
+  static constexpr int kOffKV = 0;
+  static constexpr int kOffQ = kOffKV + STAGES * kStageBytes;
+  static constexpr int kOffP = kOffQ + 2 * kQBytes;
+  static constexpr int kOffRedMax = kOffP + 2 * kQBytes;         // [2 halves][4][H]
+  static constexpr int kOffRedSum = kOffRedMax + 2 * 4 * H * 4;
+  static constexpr int kOffAlpha = kOffRedSum + 2 * 4 * H * 4;   // [2 par][2 halves][H]
+  static constexpr int kOffL = kOffAlpha + 2 * 2 * H * 4;        // [2 halves][H]
+  static constexpr int kOffBar = kOffL + 2 * H * 4;
+  // barriers: full[S], empty[S], s_full[2], s_empty[2], p_full[2], p_empty[2],
+  //           o_full[2], o_empty[2], q_full[2], q_empty[2]
+  static constexpr int kNumBars = 2 * STAGES + 16;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;   // tmem base + flags
+  static constexpr int kBytes = kOffMisc + 64;
+  static constexpr int kAlloc = kBytes + 1024;              // slack for 1 KB alignment
+  static constexpr int kTmemCols = (4 * NQ <= 32) ? 32 : (4 * NQ <= 64) ? 64
+                                 : (4 * NQ <= 128) ? 128 : (4 * NQ <= 256) ? 256 : 512;
+};
+
+template <int H>
+__device__ __forceinline__ int reduce_scatter_col(int lane) {
+  constexpr int S = (H == 8) ? 3 : (H == 16) ? 4 : 5;
+  return lane >> (5 - S);
+}
+
+// Reduce-scatter H per-lane values over the 32 lanes of a warp: afterwards
+// v[0] holds the reduction of column reduce_scatter_col<H>(lane) over all
+// lanes.  H - 1 + (5 - log2 H) shuffles.
+template <int H, bool IS_MAX>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[H], int lane) {
+#pragma unroll
+  for (int n = H, mask = 16; n > 1; n >>= 1, mask >>= 1) {
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = upper ? v[i] : v[i + n / 2];
+      const float keep = upper ? v[i + n / 2] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, mask);
+      v[i] = IS_MAX ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+  float r = v[0];
+  constexpr int S = (H == 8) ? 3 : (H == 16) ? 4 : 5;
+#pragma unroll
+  for (int mask = (16 >> S); mask >= 1; mask >>= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, r, mask);
+    r = IS_MAX ? fmaxf(r, o) : r + o;
+  }
+  return r;
+}
+
+template <int NQ, int STAGES>
+__global__ void __launch_bounds__(kSysThreads, 1)
+    sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                          const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
+  using L = SysSmem<NQ, STAGES>;
+  constexpr int H = L::H;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* full_bar = bars;
+  uint64_t* empty_bar = bars + STAGES;
+  uint64_t* s_full = bars + 2 * STAGES;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_full + 4;
+  uint64_t* p_empty = s_full + 6;
+  uint64_t* o_full = s_full + 8;
+  uint64_t* o_empty = s_full + 10;
+  uint64_t* q_full = s_full + 12;
+  uint64_t* q_empty = s_full + 14;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
+  float* red_max = reinterpret_cast<float*>(smem + L::kOffRedMax);
+  float* red_sum = reinterpret_cast<float*>(smem + L::kOffRedSum);
+  float* alpha_s = reinterpret_cast<float*>(smem + L::kOffAlpha);
+  float* l_s = reinterpret_cast<float*>(smem + L::kOffL);
+
+  const rb_sys_plan& P = args.plan;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long t_begin = rb_cta_begin(&P, blockIdx.x);
+  const long long t_end = rb_cta_begin(&P, blockIdx.x + 1);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 8);
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&misc[0], L::kTmemCols);
+  if (threadIdx.x < 2 * H) l_s[threadIdx.x] = 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = misc[0];
+
+  const uint32_t smem_kv = smem_u32(smem + L::kOffKV);
+  const uint32_t smem_q = smem_u32(smem + L::kOffQ);
+  const uint32_t smem_p = smem_u32(smem + L::kOffP);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    const uint64_t pol = l2_policy_evict_first();
+    int j = 0, uq = 0;
+    for (long long i = t_begin; i < t_end; ++i, ++j) {
+      const int u = static_cast<int>(i / P.tpu);
+      const int kt = static_cast<int>(i % P.tpu);
+      const int h = u / P.n_qt;
+      const int qt = u % P.n_qt;
+      if (i == t_begin || kt == 0) {
+        const int qb = uq & 1;
+        mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
+        uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
+        for (int idx = lane; idx < NQ * 16; idx += 32) {
+          const int c = idx >> 4, ch = idx & 15;
+          const int f = qt * NQ + c;
+          uint4 val = make_uint4(0, 0, 0, 0);
+          if (f < P.rows_per_head) {
+            const int row = f / P.g, jj = f % P.g;
+            const __nv_bfloat16* src = args.q + row * args.q_row_stride +
+                                       static_cast<long long>(h * P.g + jj) * args.q_head_stride +
+                                       ch * 8;
+            val = *reinterpret_cast<const uint4*>(src);
+          }
+          const int kb = ch >> 3;
+          *reinterpret_cast<uint4*>(qdst + kb * (NQ * 128) + sw128_offset(c, (ch & 7) * 8)) = val;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_full[qb]);
+        ++uq;
+      }
+      const int st = j % STAGES;
+      mbar_wait(&empty_bar[st], ((j / STAGES) & 1) ^ 1);
+      if (lane == 0) {
+        uint8_t* kdst = smem + L::kOffKV + st * kStageBytes;
+        mbar_arrive_expect_tx(&full_bar[st], kStageBytes);
+        tma_load_3d(kdst, &tmap_k, &full_bar[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(kdst + kKvTileBytes / 2, &tmap_k, &full_bar[st], 64, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(kdst + kKvTileBytes, &tmap_v, &full_bar[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(kdst + kKvTileBytes + kKvTileBytes / 2, &tmap_v, &full_bar[st], 64,
+                    kt * RB_KEY_TILE, h, pol);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+      auto issue_pv = [&](int jj) {
+        const int st = jj % STAGES, pb = jj & 1;
+        mbar_wait(&p_full[pb], (jj >> 1) & 1);
+        mbar_wait(&o_empty[pb], ((jj >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_kv + st * kStageBytes + kKvTileBytes;
+        const uint32_t p_base = smem_p + pb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + 2 * NQ + pb * NQ;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          // A = V^T (M = d, MN-major): 16 keys = two 8-row swizzle atoms.
+          const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, kKvTileBytes / 2, 1024);
+          const uint64_t b =
+              make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[pb]);
+        umma_commit(&empty_bar[st]);
+        umma_commit(&p_empty[pb]);
+      };
+      int j = 0, uq = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int kt = static_cast<int>(i % P.tpu);
+        const bool new_unit = (i == t_begin) || kt == 0;
+        const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
+        const int qb = uq & 1;
+        if (new_unit) mbar_wait(&q_full[qb], (uq >> 1) & 1);
+        const int st = j % STAGES, sb = j & 1;
+        mbar_wait(&full_bar[st], (j / STAGES) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_kv + st * kStageBytes;
+        const uint32_t q_base = smem_q + qb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + sb * NQ;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * 0 + (kk & 3) * 32;
+          const uint64_t a =
+              make_smem_desc_sw128(k_base + (kk >> 2) * (kKvTileBytes / 2) + koff, 16, 1024);
+          const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + koff, 16, 1024);
+          umma_f16_ss(d_tmem, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+        if (last_of_unit) {
+          umma_commit(&q_empty[qb]);
+          ++uq;
+        }
+        if (j > 0) issue_pv(j - 1);
+      }
+      if (j > 0) issue_pv(j - 1);
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------- softmax / O accumulation
+    const int cw = warp - 2;          // 0..7
+    const int hf = cw >> 2;           // column half
+    const int qd = warp & 3;          // TMEM lane quadrant (hardware: warp % 4)
+    const bool designated = (qd == 0) && lane < H;
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+    float m_run[H], acc[H];
+    int j = 0;
+    for (long long i = t_begin; i < t_end; ++i, ++j) {
+      const int u = static_cast<int>(i / P.tpu);
+      const int kt = static_cast<int>(i % P.tpu);
+      const bool new_unit = (i == t_begin) || kt == 0;
+      const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
+      if (new_unit) {
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          m_run[c] = -INFINITY;
+          acc[c] = 0.f;
+        }
+      }
+      const int sb = j & 1;
+      // ---- S tile -> scores (log2 domain)
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      float x[H];
+      tmem_ld_32x32b<H>(lane_addr + sb * NQ + hf * H, x);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[sb]);
+      const bool valid = kt * RB_KEY_TILE + qd * 32 + lane < P.s;
+#pragma unroll
+      for (int c = 0; c < H; ++c) x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
+      // ---- tile max across the 128 key lanes
+      float tmp[H];
+#pragma unroll
+      for (int c = 0; c < H; ++c) tmp[c] = x[c];
+      const float wmax = warp_reduce_scatter<H, true>(tmp, lane);
+      const int rcol = reduce_scatter_col<H>(lane);
+      float* rm = red_max + hf * 4 * H;
+      if ((lane & ((32 / H) - 1)) == 0) rm[qd * H + rcol] = wmax;
+      named_bar_sync(1 + hf, 128);
+      float m_new[H];
+#pragma unroll
+      for (int c4 = 0; c4 < H; c4 += 4) {
+        float4 a0 = *reinterpret_cast<const float4*>(rm + 0 * H + c4);
+        float4 a1 = *reinterpret_cast<const float4*>(rm + 1 * H + c4);
+        float4 a2 = *reinterpret_cast<const float4*>(rm + 2 * H + c4);
+        float4 a3 = *reinterpret_cast<const float4*>(rm + 3 * H + c4);
+        m_new[c4 + 0] = fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x));
+        m_new[c4 + 1] = fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y));
+        m_new[c4 + 2] = fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z));
+        m_new[c4 + 3] = fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w));
+      }
+      float* alpha_cur = alpha_s + ((j & 1) * 2 + hf) * H;
+#pragma unroll
+      for (int c = 0; c < H; ++c) {
+        const float mn = fmaxf(m_run[c], m_new[c]);
+        const float al = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
+        if (designated && lane == c) alpha_cur[c] = al;
+        m_run[c] = mn;
+        x[c] = fast_exp2(x[c] - mn);  // p, exactly 0 for masked keys
+      }
+      // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
+      mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);
+      {
+        const int key = qd * 32 + lane;
+        uint8_t* pdst = smem + L::kOffP + sb * L::kQBytes + (key >> 6) * (NQ * 128);
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          *reinterpret_cast<__nv_bfloat16*>(pdst + sw128_offset(hf * H + c, key & 63)) =
+              __float2bfloat16_rn(x[c]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[sb]);
+      // ---- row sums
+      const float wsum = warp_reduce_scatter<H, false>(x, lane);
+      float* rs = red_sum + hf * 4 * H;
+      if ((lane & ((32 / H) - 1)) == 0) rs[qd * H + rcol] = wsum;
+      named_bar_sync(1 + hf, 128);
+      if (designated) {
+        const float lt = rs[0 * H + lane] + rs[1 * H + lane] + rs[2 * H + lane] + rs[3 * H + lane];
+        l_s[hf * H + lane] = l_s[hf * H + lane] * alpha_cur[lane] + lt;
+      }
+      // ---- O accumulation (previous tile of this unit, then this one if last)
+      auto accumulate = [&](int jj) {
+        const int ob = jj & 1;
+        mbar_wait(&o_full[ob], (jj >> 1) & 1);
+        tc_fence_after();
+        float o[H];
+        tmem_ld_32x32b<H>(lane_addr + 2 * NQ + ob * NQ + hf * H, o);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[ob]);
+        const float* al = alpha_s + ((jj & 1) * 2 + hf) * H;
+#pragma unroll
+        for (int c4 = 0; c4 < H; c4 += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(al + c4);
+          acc[c4 + 0] = fmaf(acc[c4 + 0], a.x, o[c4 + 0]);
+          acc[c4 + 1] = fmaf(acc[c4 + 1], a.y, o[c4 + 1]);
+          acc[c4 + 2] = fmaf(acc[c4 + 2], a.z, o[c4 + 2]);
+          acc[c4 + 3] = fmaf(acc[c4 + 3], a.w, o[c4 + 3]);
+        }
+      };
+      if (!new_unit) accumulate(j - 1);
+      if (last_of_unit) {
+        accumulate(j);
+        // ---- finalize unit u
+        named_bar_sync(3, 256);  // l_s complete for all columns
+        const int h = u / P.n_qt, qt = u % P.n_qt;
+        const long long u_first = static_cast<long long>(u) * P.tpu;
+        const int owner0 = rb_tile_owner(&P, u_first);
+        const int nparts = rb_unit_parts(&P, u);
+        const int dcol = qd * 32 + lane;
+        float lrow[H];
+#pragma unroll
+        for (int c = 0; c < H; ++c) lrow[c] = l_s[hf * H + c];
+        if (nparts == 1) {
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int f = qt * NQ + hf * H + c;
+            if (f < P.rows_per_head) {
+              const int row = f / P.g, hh = h * P.g + f % P.g;
+              const long long o_idx = static_cast<long long>(row) * P.hq + hh;
+              args.o_sys[o_idx * RB_HEAD_DIM + dcol] = acc[c] / lrow[c];
+              if (qd == 0 && lane == 0)
+                args.lse_sys[o_idx] = (m_run[c] + __log2f(lrow[c])) * kLn2;
+            }
+          }
+        } else {
+          const int slot = blockIdx.x - owner0;
+          const long long pbase = static_cast<long long>(u) * P.max_parts + slot;
+          float* pacc = args.part_acc + pbase * NQ * RB_HEAD_DIM;
+          float* pml = args.part_ml + pbase * 2 * NQ;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int col = hf * H + c;
+            pacc[col * RB_HEAD_DIM + dcol] = acc[c];
+            if (qd == 0 && lane == 0) {
+              pml[col] = m_run[c];
+              pml[NQ + col] = lrow[c];
+            }
+          }
+          __threadfence();
+          named_bar_sync(3, 256);
+          if (threadIdx.x == 64) {
+            const int prev = atomicAdd(&args.counters[u], 1);
+            const int last = (prev == nparts - 1);
+            if (last) atomicExch(&args.counters[u], 0);
+            misc[1] = last;
+          }
+          named_bar_sync(3, 256);
+          if (misc[1]) {
+            __threadfence();
+            const float* uacc = args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
+            const float* uml = args.part_ml + static_cast<long long>(u) * P.max_parts * 2 * NQ;
+#pragma unroll 1
+            for (int c = 0; c < H; ++c) {
+              const int col = hf * H + c;
+              const int f = qt * NQ + col;
+              if (f >= P.rows_per_head) continue;
+              float M = -INFINITY;
+              for (int k = 0; k < nparts; ++k) M = fmaxf(M, __ldcg(uml + k * 2 * NQ + col));
+              float Ls = 0.f, Os = 0.f;
+              for (int k = 0; k < nparts; ++k) {
+                const float w = fast_exp2(__ldcg(uml + k * 2 * NQ + col) - M);
+                Ls = fmaf(__ldcg(uml + k * 2 * NQ + NQ + col), w, Ls);
+                Os = fmaf(__ldcg(uacc + (static_cast<long long>(k) * NQ + col) * RB_HEAD_DIM + dcol), w, Os);
+              }
+              const int row = f / P.g, hh = h * P.g + f % P.g;
+              const long long o_idx = static_cast<long long>(row) * P.hq + hh;
+              args.o_sys[o_idx * RB_HEAD_DIM + dcol] = Os / Ls;
+              if (qd == 0 && lane == 0) args.lse_sys[o_idx] = (M + __log2f(Ls)) * kLn2;
+            }
+          }
+        }
+        // reset running sums for the next unit (designated threads own l_s)
+        named_bar_sync(3, 256);
+        if (designated) l_s[hf * H + lane] = 0.f;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, L::kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------- host
+
+template <int NQ, int STAGES>
+static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, const SysArgs& a,
+                              cudaStream_t stream) {
+  using L = SysSmem<NQ, STAGES>;
+  static_assert(L::kAlloc <= 232448, "system kernel shared memory over the 227 KB limit");
+  auto kern = sys_attn_sm100_kernel<NQ, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  if (e != cudaSuccess) return e;
+  kern<<<a.plan.grid, kSysThreads, L::kAlloc, stream>>>(tk, tv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
+                                    const SysArgs& a, cudaStream_t stream) {
+  switch (a.plan.nq) {
+    case 16: return launch_sys<16, 3>(tk, tv, a, stream);
+    case 32: return launch_sys<32, 3>(tk, tv, a, stream);
+    case 64: return launch_sys<64, 2>(tk, tv, a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------ layout probe
+// One-CTA check of the exact operand layouts / descriptors the system kernel
+// uses (K, V in the TMA SW128 box layout; Q, P in the K-major SW128 layout).
+template <int NQ>
+__global__ void umma_probe_kernel(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                                  const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
+                                  float* o_out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sk = smem;
+  uint8_t* sv = smem + kKvTileBytes;
+  uint8_t* sq = smem + 2 * kKvTileBytes;
+  uint8_t* sp = sq + NQ * 256;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + NQ * 256);
+  uint32_t* tm = reinterpret_cast<uint32_t*>(bar + 2);
+  for (int idx = threadIdx.x; idx < 128 * 128; idx += blockDim.x) {
+    const int row = idx / 128, col = idx % 128;
+    const uint32_t off = (col >> 6) * (kKvTileBytes / 2) + sw128_offset(row, col & 63);
+    *reinterpret_cast<__nv_bfloat16*>(sk + off) = k[idx];
+    *reinterpret_cast<__nv_bfloat16*>(sv + off) = v[idx];
+  }
+  for (int idx = threadIdx.x; idx < NQ * 128; idx += blockDim.x) {
+    const int row = idx / 128, col = idx % 128;
+    const uint32_t off = (col >> 6) * (NQ * 128) + sw128_offset(row, col & 63);
+    *reinterpret_cast<__nv_bfloat16*>(sq + off) = q[idx];
+    *reinterpret_cast<__nv_bfloat16*>(sp + off) = p[idx];
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(tm, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tm;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
+    constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+    const uint32_t k_base = smem_u32(sk), v_base = smem_u32(sv);
+    const uint32_t q_base = smem_u32(sq), p_base = smem_u32(sp);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t a =
+          make_smem_desc_sw128(k_base + (kk >> 2) * (kKvTileBytes / 2) + (kk & 3) * 32, 16, 1024);
+      const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+      umma_f16_ss(tbase, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+    }
+    umma_commit(&bar[0]);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, kKvTileBytes / 2, 1024);
+      const uint64_t b = make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+      umma_f16_ss(tbase + 64, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+    }
+    umma_commit(&bar[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bar[0], 0);
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t laddr = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+  for (int c0 = 0; c0 < NQ; c0 += 8) {
+    float s[8], o[8];
+    tmem_ld_32x32b<8>(laddr + c0, s);
+    tmem_ld_32x32b<8>(laddr + 64 + c0, o);
+    tmem_wait_ld();
+    for (int c = 0; c < 8; ++c) {
+      s_out[(warp * 32 + lane) * NQ + c0 + c] = s[c];
+      o_out[(warp * 32 + lane) * NQ + c0 + c] = o[c];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 128);
+  }
+}
+
+template <int N>
+static cudaError_t launch_probe_n(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                                  const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
+                                  float* o_out, cudaStream_t stream) {
+  const int smem = 2 * kKvTileBytes + 2 * 64 * 256 + 64 + 1024;
+  cudaError_t e =
+      cudaFuncSetAttribute(umma_probe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  umma_probe_kernel<N><<<1, 128, smem, stream>>>(k, q, v, p, s_out, o_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_umma_probe(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                              const __nv_bfloat16* v, const __nv_bfloat16* p, int nq,
+                              float* s_out, float* o_out, cudaStream_t stream) {
+  switch (nq) {
+    case 16: return launch_probe_n<16>(k, q, v, p, s_out, o_out, stream);
+    case 32: return launch_probe_n<32>(k, q, v, p, s_out, o_out, stream);
+    case 64: return launch_probe_n<64>(k, q, v, p, s_out, o_out, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rb

@@ -1,0 +1,177 @@
+"""Segment-level launch wrappers over the C-ABI (torch tensors in, torch
+tensors out, current CUDA stream).
+
+This is the B200 replacement of the reference's kernel boundary
+`relayserve.kernels` (/root/reference/pkg/src/relayserve/kernels.py:14-37):
+instead of per-head matmul / softmax calls it launches one kernel per
+attention segment.  There is no backend selection and no fallback.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .errors import ContractError, DimensionError
+
+HEAD_DIM = 128
+BACKEND = "cuda-sm100a"
+
+_workspaces: dict = {}
+
+
+def _stream(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def sm_count(device=None) -> int:
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    return _lib.sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def workspace(nbytes: int, device, stream_key: int) -> torch.Tensor:
+    """Zero-initialised scratch for the system kernel's stream-K partials and
+    semaphores, cached per (device, stream) -- the kernel leaves the
+    semaphores zeroed, so the buffer is reusable without clearing."""
+    key = (str(device), stream_key)
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    return buf
+
+
+def _check_bf16(name, t):
+    if t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise ContractError(f"{name}: expected a CUDA bfloat16 tensor, got {t.dtype} on {t.device}")
+    if t.stride(-1) != 1:
+        raise ContractError(f"{name}: head_dim must be the contiguous dimension")
+
+
+def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
+                     o_sys=None, lse_sys=None, ws=None):
+    """Unmasked attention of every query row over the shared prefix.
+
+    q: (n_rows, hq, 128) bf16; sys_k/sys_v: (s, hkv, 128) for kv_layout
+    'shd' (the reference's layout) or (hkv, s, 128) for 'hsd' (the
+    SystemKvCache layout).  Returns (o_sys fp32 (n_rows, hq, 128),
+    lse_sys fp32 (n_rows, hq)), natural-log LSE.
+    """
+    _check_bf16("q", q)
+    _check_bf16("sys_k", sys_k)
+    _check_bf16("sys_v", sys_v)
+    if sys_k.shape != sys_v.shape or sys_k.stride() != sys_v.stride():
+        raise DimensionError(f"sys_k/sys_v shapes differ: {tuple(sys_k.shape)} vs {tuple(sys_v.shape)}")
+    n_rows, hq, d = q.shape
+    if kv_layout == "shd":
+        s, hkv, dk = sys_k.shape
+        st_tok, st_head = sys_k.stride(0), sys_k.stride(1)
+    elif kv_layout == "hsd":
+        hkv, s, dk = sys_k.shape
+        st_tok, st_head = sys_k.stride(1), sys_k.stride(0)
+    else:
+        raise ContractError(f"unknown kv_layout {kv_layout!r}")
+    if d != HEAD_DIM or dk != HEAD_DIM:
+        raise DimensionError(f"head_dim must be {HEAD_DIM} (pad smaller dims), got {d}/{dk}")
+    if hkv < 1 or hq % hkv != 0:
+        raise DimensionError(f"query heads {hq} not a multiple of kv heads {hkv}")
+    dev = q.device
+    if o_sys is None:
+        o_sys = torch.empty((n_rows, hq, HEAD_DIM), dtype=torch.float32, device=dev)
+    if lse_sys is None:
+        lse_sys = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
+    grid = sm_count(dev) if grid is None else grid
+    stream = _stream(dev)
+    if ws is None:
+        _, need = _lib.sys_plan(n_rows, hq, hkv, s, grid)
+        ws = workspace(need, dev, stream)
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
+    _lib.check(_lib.load().rb_system_attention(
+        q.data_ptr(), q.stride(0), q.stride(1), n_rows, hq, hkv, HEAD_DIM,
+        sys_k.data_ptr(), sys_v.data_ptr(), s, st_tok, st_head, float(scale), grid,
+        o_sys.data_ptr(), lse_sys.data_ptr(), ws.data_ptr(), ws.numel(), stream),
+        "rb_system_attention")
+    return o_sys, lse_sys
+
+
+def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
+                      block_table=None, block_size=0, req_offset=None,
+                      strides=None, causal=True, prefix_k=None, prefix_v=None,
+                      prefix_strides=None, o_sys=None, lse_sys=None, scale=None,
+                      out=None, out_fp32=False, lse_out=None, want_lse=True):
+    """Context (or relay, or naive-baseline) attention; see
+    include/relay_b200.h:rb_context_attention for the addressing modes.
+
+    q: (n_rows, hq, 128) bf16; q_start int32 (b+1,); ctx_lens int32 (b,).
+    strides = (stride_block, stride_tok, stride_head) in elements.
+    """
+    _check_bf16("q", q)
+    n_rows, hq, d = q.shape
+    if d != HEAD_DIM:
+        raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
+    b = ctx_lens.numel()
+    dev = q.device
+    if out is None:
+        out = torch.empty((n_rows, hq, HEAD_DIM),
+                          dtype=torch.float32 if out_fp32 else torch.bfloat16, device=dev)
+    out_fp32 = out.dtype == torch.float32
+    if lse_out is None and want_lse:
+        lse_out = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
+    s_prefix = 0
+    p_tok = p_head = 0
+    if prefix_k is not None:
+        s_prefix = prefix_strides[2]
+        p_tok, p_head = prefix_strides[0], prefix_strides[1]
+    sb, stok, sh = strides
+    bt_stride = block_table.stride(0) if block_table is not None else 0
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
+    _lib.check(_lib.load().rb_context_attention(
+        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, max_rows, hq, hkv,
+        HEAD_DIM, k.data_ptr(), v.data_ptr(), _ptr(block_table), bt_stride, block_size,
+        _ptr(req_offset), sb, stok, sh, ctx_lens.data_ptr(), 1 if causal else 0,
+        _ptr(prefix_k), _ptr(prefix_v), s_prefix, p_tok, p_head, _ptr(o_sys), _ptr(lse_sys),
+        float(scale), out.data_ptr(), 1 if out_fp32 else 0, _ptr(lse_out), _stream(dev)),
+        "rb_context_attention")
+    return out, lse_out
+
+
+def relay_fusion_fp32(o_sys, lse_sys, o_ctx, lse_ctx, out=None, lse_out=None):
+    """Standalone fusion kernel on fp32 CUDA tensors of matching shapes."""
+    tens = [o_sys, lse_sys, o_ctx, lse_ctx]
+    if any((not t.is_cuda) or t.dtype != torch.float32 or not t.is_contiguous() for t in tens):
+        raise ContractError("relay_fusion_fp32 expects contiguous fp32 CUDA tensors")
+    d = o_sys.shape[-1]
+    n_vec = lse_sys.numel()
+    out = torch.empty_like(o_sys) if out is None else out
+    lse_out = torch.empty_like(lse_sys) if lse_out is None else lse_out
+    _lib.check(_lib.load().rb_relay_fusion(
+        o_sys.data_ptr(), lse_sys.data_ptr(), o_ctx.data_ptr(), lse_ctx.data_ptr(),
+        out.data_ptr(), lse_out.data_ptr(), n_vec, d, _stream(o_sys.device)), "rb_relay_fusion")
+    return out, lse_out
+
+
+def kv_append(k_new, v_new, slot_mapping, k_pool, v_pool, block_size):
+    """Scatter (n_tok, hkv, 128) new rows into a [num_blocks][hkv][bs][128] pool."""
+    _check_bf16("k_new", k_new)
+    n_tok, hkv, d = k_new.shape
+    _lib.check(_lib.load().rb_kv_append(
+        k_new.data_ptr(), v_new.data_ptr(), slot_mapping.data_ptr(), n_tok, k_pool.data_ptr(),
+        v_pool.data_ptr(), hkv, d, block_size, k_pool.stride(0), k_pool.stride(2),
+        k_pool.stride(1), _stream(k_new.device)), "rb_kv_append")
+
+
+def umma_probe(k, q, v, p):
+    """Debug: run the system kernel's tcgen05 operand layouts on one tile."""
+    nq = q.shape[0]
+    s_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
+    o_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
+    _lib.check(_lib.load().rb_debug_umma_probe(
+        k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), nq, s_out.data_ptr(),
+        o_out.data_ptr(), _stream(k.device)), "rb_debug_umma_probe")
+    return s_out, o_out

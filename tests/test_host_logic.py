@@ -1,0 +1,86 @@
+"""Host-side logic: stream-K plan (Python mirror == C), tile coverage,
+head sharding, cost model, block pool (no GPU)."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2402_14808_b200 import _lib, costmodel, sharding
+from paper_2402_14808_b200.kvcache import BlockPool
+from paper_2402_14808_b200.plan import SysPlan
+
+
+@pytest.mark.parametrize("n_rows,hq,hkv,s,grid", [
+    (32, 52, 52, 8192, 148), (32, 52, 52, 512, 148), (4, 32, 32, 512, 148),
+    (64, 32, 32, 4096, 148), (128, 32, 8, 32768, 148), (256, 64, 8, 65536, 148),
+    (32, 7, 7, 8192, 148), (1, 1, 1, 1, 148), (32, 4, 4, 1000, 5),
+])
+def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
+    p = SysPlan(n_rows, hq, hkv, s, grid)
+    f, _ = _lib.sys_plan(n_rows, hq, hkv, s, grid)
+    assert (p.nq, p.n_qt, p.tpu, p.n_units, p.total, p.grid, p.max_parts) == \
+        (f["nq"], f["n_qt"], f["tpu"], f["n_units"], f["total"], f["grid"], f["max_parts"])
+    ranges = p.cta_ranges()
+    assert ranges[0][0] == 0 and ranges[-1][1] == p.total
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1            # balanced to one tile
+    for x in range(0, p.total, max(1, p.total // 97)):
+        c = p.owner(x)
+        assert ranges[c][0] <= x < ranges[c][1]
+    for u in range(p.n_units):
+        first = u * p.tpu
+        owners = {p.owner(x) for x in range(first, first + p.tpu)}
+        assert len(owners) == p.unit_parts(u) <= p.max_parts
+
+
+def test_head_ranges():
+    assert [b - a for a, b in sharding.head_ranges(52, 8)] == [7, 7, 7, 7, 6, 6, 6, 6]
+    assert [b - a for a, b in sharding.head_ranges(52, 4)] == [13] * 4
+    for h, w in itertools.product([1, 7, 8, 52, 64], [1, 2, 4, 8]):
+        if h < w:
+            continue
+        r = sharding.head_ranges(h, w)
+        assert r[0][0] == 0 and r[-1][1] == h
+        assert max(b - a for a, b in r) - min(b - a for a, b in r) <= 1
+    assert sharding.local_heads(8, 64, 8, 3) == (3, 4, 24, 32)
+
+
+def test_costmodel_reference_forms():
+    assert costmodel.traffic_baseline(2, 3, 1, 4) == 48
+    assert costmodel.traffic_relay(2, 3, 1, 4) == 76
+    assert abs(costmodel.theoretical_speedup(32, 2048, 128) - 2178 / 199) < 1e-9
+    g = np.load(__file__.replace("test_host_logic.py", "golden/reference_golden.npz"))
+    for b, s, c, d, nr, nb in g["traffic_tuples"]:
+        assert costmodel.traffic_relay(b, s, c, d) == nr
+        assert costmodel.traffic_baseline(b, s, c, d) == nb
+
+
+def test_byte_model_c2():
+    sh = costmodel.DecodeShape(b=32, hq=52, hkv=52, s=8192, ctx_total=32 * 128)
+    assert sh.bytes_alg == 2 * 2 * 52 * 128 * (8192 + 4096) + 2 * 2 * 32 * 52 * 128
+    assert abs(sh.bytes_alg / 1e6 - 328.0) < 1.0       # 328 MB
+    assert sh.flops_sys == 4 * 32 * 52 * 8192 * 128
+    assert 21 < sh.bytes_naive / sh.bytes_alg < 22.5   # 21.6x
+
+
+def test_block_pool_conservation():
+    rng = np.random.default_rng(808)
+    pool = BlockPool(num_blocks=64, block_size=4)
+    live, nid = [], 0
+    from paper_2402_14808_b200.errors import CapacityError
+    for _ in range(3000):
+        if live and rng.random() < 0.45:
+            pool.release(live.pop(int(rng.integers(len(live)))))
+        else:
+            rid = f"r{nid}"
+            nid += 1
+            pool.register(rid)
+            live.append(rid)
+            try:
+                pool.grow(rid, int(rng.integers(1, 10)))
+            except CapacityError:
+                pool.release(rid)
+                live.remove(rid)
+        assert pool.used_blocks + pool.free_blocks == pool.num_blocks
