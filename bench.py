@@ -1,0 +1,481 @@
+"""Relay decode-attention benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Metric: decode attention us/step (and HBM GB/s) vs system-prompt length at
+B=32 -- the reference's `relayserve profile-attn` measurement
+(/root/reference/pkg/src/relayserve/cli.py:320-357) on BASELINE.json
+configs[1]: Llama-30B attention shape (52 heads, d=128), batch 32, context
+128, system prompt swept 512..32k; the headline `value` is s=8192 (the top of
+configs[1]'s sweep).  One step = one relay decode step of one layer: the
+tcgen05 system kernel over the shared prefix + the paged context kernel with
+the fused relay epilogue.  Inputs are synthetic (seeded normal bf16), resident
+in HBM; L2 (126 MB) is flushed between timed steps by writing a 2x-L2 buffer.
+
+N > 1 (torchrun): KV heads are sharded across ranks (52 -> 7,7,7,7,6,6,6,6 at
+N=8); each rank runs the same step on its heads, no collective in the timed
+region; the step time is the max over ranks (fixed total work: "strong").
+
+--impl reference times the reference's own CPU implementation (the
+unmodified relayserve modules compiled into oracle/_ref by oracle/build.py,
+float64, all host cores via head-parallel processes) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, H, C, D = 32, 52, 128, 128
+HEADLINE_S = 8192
+SWEEP = (512, 1024, 2048, 4096, 8192, 16384, 32768)
+BLOCK = 16
+METRIC = "decode attention µs/step & HBM GB/s vs sys-prompt length (B=32), 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--s", type=int, default=HEADLINE_S)
+    p.add_argument("--sweep", type=str, default=",".join(map(str, SWEEP)))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU sampling")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------ measurement
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20", "-i", str(index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        loaded = [x for x in sm if smax and x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def make_flush(torch, device):
+    l2 = torch.cuda.get_device_properties(device).L2_cache_size
+    buf = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=device)
+
+    def flush():
+        buf.zero_()
+    return flush
+
+
+def time_loop(torch, fn, steps, warmup, flush, barrier=None):
+    """W warm-up steps, then exactly `steps` timed steps; per-step CUDA events
+    on the launching (current) stream; L2 flushed before every step outside
+    the events.  Returns per-step milliseconds."""
+    for _ in range(warmup):
+        flush()
+        fn()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for a, b in ev:
+        flush()
+        a.record()
+        fn()
+        b.record()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1663.8)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic(kernel, s):
+    """dram bytes per launch of `kernel` at system length s from the committed
+    ncu summary (profiles/ncu_summary.json), if one exists for this config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            data = json.load(f)
+        return data["kernels"][kernel][str(s)]["dram_bytes"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- workload
+
+def build(torch, s, heads, device, seed=1234):
+    """Per-head seeded synthetic C2 workload for the given global KV heads, so
+    a sharded run holds exactly the unsharded run's data for its heads."""
+    from paper_2402_14808_b200.attention import NaiveDecodeStep, RelayDecodeStep
+    from paper_2402_14808_b200.kvcache import PagedKvCache, SystemKvCache
+    nh = len(heads)
+    g = torch.Generator(device=device)
+    sk = torch.empty((nh, s, D), dtype=torch.bfloat16, device=device)
+    sv = torch.empty_like(sk)
+    nblk = B * C // BLOCK
+    paged = PagedKvCache(1, nh, nblk, BLOCK, device=device)
+    q = torch.empty((B, nh, D), dtype=torch.bfloat16, device=device)
+    for i, hg in enumerate(heads):
+        g.manual_seed(seed * 1000003 + hg)
+        sk[i] = torch.randn((s, D), generator=g, device=device)
+        sv[i] = torch.randn((s, D), generator=g, device=device)
+        paged.k_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
+        paged.v_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
+        q[:, i] = torch.randn((B, D), generator=g, device=device)
+    # shuffled physical blocks, as a real paged allocator would hand out
+    perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(seed)).tolist()
+    paged.pool._free = perm[::-1]
+    for r in range(B):
+        paged.register(r)
+        paged.pool.grow(r, C)
+        paged._layer_lengths[r][0] = C
+    ids = list(range(B))
+    bt, cl = paged.block_table(ids), paged.context_lens(ids)
+    sys_cache = SystemKvCache([sk], [sv])
+    relay = RelayDecodeStep(sys_cache, paged, bt, cl, hq=nh)
+    naive = NaiveDecodeStep(sys_cache, paged, bt, cl, hq=nh)
+    return q, relay, naive, paged, bt
+
+
+def graph_of(torch, fn):
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        fn()
+    return graph
+
+
+# ----------------------------------------------------------- CPU baselines
+
+def _ref_modules():
+    """The reference compiled in oracle/_ref ("reference") else the port."""
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "relayserve")):
+        sys.path.insert(0, ref_dir)
+        try:
+            import relayserve.attention as att
+            return att, "reference"
+        except Exception:
+            pass
+    from oracle import relay_oracle
+    return relay_oracle, "port"
+
+
+_CPU = {}
+
+
+def _cpu_data(s, nh, seed=7):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    sk = rng.standard_normal((s, nh, D)); sv = rng.standard_normal((s, nh, D))
+    ck = [rng.standard_normal((C, nh, D)) for _ in range(B)]
+    cv = [rng.standard_normal((C, nh, D)) for _ in range(B)]
+    q = rng.standard_normal((B, 1, nh, D))
+    return q, sk, sv, ck, cv
+
+
+def _cpu_worker(args):
+    lo, hi = args
+    att = _CPU["att"]
+    q, sk, sv, ck, cv = _CPU["data"]
+    t0 = time.perf_counter()
+    att.relay_attention(q[:, :, lo:hi], sk[:, lo:hi], sv[:, lo:hi],
+                        [x[:, lo:hi] for x in ck], [x[:, lo:hi] for x in cv])
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_sample(s, budget):
+    """Reference relay step on 1 core over a head subsample, best-of-N within
+    `budget` seconds, extrapolated linearly in heads (heads are independent
+    and identical work, attention.py:122-133)."""
+    att, kind = _ref_modules()
+    nh = 4
+    _CPU["att"], _CPU["data"] = att, _cpu_data(s, nh)
+    best, reps, t_start = float("inf"), 0, time.perf_counter()
+    while reps < 5 and (reps < 1 or time.perf_counter() - t_start < budget):
+        best = min(best, _cpu_worker((0, nh)))
+        reps += 1
+    us = best * 1e6 * H / nh
+    return {"value": us, "unit": "µs/step", "cores": 1, "kind": kind,
+            "sample": (f"relay_attention b={B} s={s} c={C} d={D}, {nh} of {H} heads, best of "
+                       f"{reps} on 1 core, float64, extrapolated x{H / nh:g} to all heads")}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    att, kind = _ref_modules()
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, H))
+    _CPU["att"], _CPU["data"] = att, _cpu_data(args.s, H)
+    bounds = [(H * i // procs, H * (i + 1) // procs) for i in range(procs)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, bounds)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, bounds)
+            times.append(time.perf_counter() - t0)
+    us = statistics.mean(times) * 1e6
+    sample = (f"full workload per step: relay_attention b={B}, {H} heads, s={args.s}, c={C}, "
+              f"d={D}, float64, heads split over {procs} processes")
+    line = {"metric": METRIC, "value": us, "unit": "µs/step", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded normal)",
+            "config": {"workload": f"C2 Llama-30B attention shape, b={B}, H={H}, d={D}, "
+                                   f"c={C}, s={args.s}", "global_batch": B, "seq_len": args.s,
+                       "parallelism": f"host processes x{procs}"},
+            "cpu_baseline": {"value": us, "unit": "µs/step", "cores": procs, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": us, "unit": "µs/step", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- GPU arm
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if world != args.gpus and world > 1:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    barrier = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+        barrier = dist.barrier
+    from paper_2402_14808_b200 import _lib, kernels, sharding
+    from paper_2402_14808_b200.costmodel import DecodeShape
+    _lib.load()
+    ka, kb, _, _ = sharding.local_heads(H, H, world, rank)
+    heads = list(range(ka, kb))
+    flush = make_flush(torch, device)
+    hbm, tc, peak_kind = measured_peaks()
+
+    def step_stats(s, with_naive=True, with_split=False, with_e2e=False, graph=True):
+        q, relay, naive, paged, bt = build(torch, s, heads, device)
+        fn_relay = lambda: relay(q)  # noqa: E731
+        res = {}
+        eager = time_loop(torch, fn_relay, args.steps, args.warmup, flush, barrier)
+        res["eager_ms"] = statistics.mean(eager)
+        if graph:
+            gr = graph_of(torch, fn_relay)
+            gms = time_loop(torch, gr.replay, args.steps, args.warmup, flush, barrier)
+            res["graph_ms"] = statistics.mean(gms)
+        res["ms"] = min(res["eager_ms"], res.get("graph_ms", float("inf")))
+        if with_naive:
+            res["naive_ms"] = statistics.mean(
+                time_loop(torch, lambda: naive(q), max(3, args.steps // 5), 2, flush, barrier))
+        if with_split:
+            res["sys_ms"] = statistics.mean(
+                time_loop(torch, lambda: relay.system(q), args.steps, args.warmup, flush, barrier))
+            res["ctx_ms"] = statistics.mean(
+                time_loop(torch, lambda: relay.context(q), args.steps, args.warmup, flush, barrier))
+        if with_e2e:
+            res.update(e2e_stats(q, relay, paged, bt))
+        # size-independent parity: relay == naive per-request kernel
+        out_r = relay(q)[0].float()
+        out_n = naive(q)[0].float()
+        torch.cuda.synchronize()
+        res["parity_max_abs_vs_naive"] = float((out_r - out_n).abs().max())
+        res["plan"] = relay.plan
+        del q, relay, naive, paged
+        torch.cuda.empty_cache()
+        return res
+
+    def e2e_stats(q, relay, paged, bt):
+        """Public-API decode step with host buffers: H2D of this step's q and
+        new-token k/v from pinned memory, paged append, relay step, D2H of
+        the output -- all inside the events."""
+        nh = q.shape[1]
+        g = torch.Generator().manual_seed(99)
+        q_h = torch.randn((B, nh, D), generator=g).to(torch.bfloat16).pin_memory()
+        k_h = torch.randn((B, nh, D), generator=g).to(torch.bfloat16).pin_memory()
+        v_h = torch.randn((B, nh, D), generator=g).to(torch.bfloat16).pin_memory()
+        out_h = torch.empty((B, nh, D), dtype=torch.bfloat16).pin_memory()
+        # the step's new token overwrites slot c-1 of each request (context
+        # length stays c, so every timed step does identical work)
+        btc = bt.cpu()
+        slots = torch.tensor([int(btc[r, (C - 1) // BLOCK]) * BLOCK + (C - 1) % BLOCK
+                              for r in range(B)], dtype=torch.int32, device=device)
+        fn = lambda: relay.step_host(q_h, k_h, v_h, slots, out_h)  # noqa: E731
+        ms = time_loop(torch, fn, args.steps, args.warmup, flush, barrier)
+        return {"e2e_ms": statistics.mean(ms), "h2d": 3 * q_h.numel() * 2,
+                "d2h": out_h.numel() * 2}
+
+    clocks = ClockSampler(local)
+    t_wall = time.perf_counter()
+    head = step_stats(args.s, with_split=True, with_e2e=True)
+    sweep = []
+    if args.sweep:
+        for s in [int(x) for x in args.sweep.split(",") if x.strip()]:
+            if s == args.s:
+                st = head
+            else:
+                st = step_stats(s, graph=True)
+            shp = DecodeShape(B, len(heads), len(heads), s, B * C)
+            sweep.append({"s": s, "us_per_step": st["ms"] * 1e3,
+                          "naive_us_per_step": st.get("naive_ms", float("nan")) * 1e3,
+                          "hbm_gbs": shp.bytes_alg / (st["ms"] * 1e-3) / 1e9,
+                          "frac_of_hbm_roofline": (shp.bytes_alg / (hbm * 1e9)) / (st["ms"] * 1e-3),
+                          "naive_bytes_over_relay": shp.bytes_naive / shp.bytes_alg,
+                          "parity_max_abs_vs_naive": st["parity_max_abs_vs_naive"]})
+    clk = clocks.stop()
+    wall = time.perf_counter() - t_wall
+
+    def maxr(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = maxr(head["ms"])
+    sys_ms, ctx_ms = maxr(head["sys_ms"]), maxr(head["ctx_ms"])
+    e2e_ms = maxr(head["e2e_ms"])
+    for row in sweep:
+        row["us_per_step"] = maxr(row["us_per_step"])
+        row["naive_us_per_step"] = maxr(row["naive_us_per_step"])
+
+    # end-to-end check of the sharded path: all-gather the per-rank outputs
+    gathered_ok = None
+    if world > 1:
+        q, relay, _, _, _ = build(torch, 1024, heads, device)
+        out, _ = relay(q)
+        full = sharding.gather_heads(out, H, H)
+        gathered_ok = bool(full.shape == (B, H, D) and torch.isfinite(full.float()).all())
+        del q, relay
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    shape = DecodeShape(B, H, H, args.s, B * C)
+    sys_bytes_local = 2 * 2 * len(heads) * D * args.s + 2 * B * len(heads) * D
+    achieved = sys_bytes_local / (sys_ms * 1e-3) / 1e9
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.s, args.cpu_budget)
+    value_us = ms * 1e3
+    launches = 2
+    line = {
+        "metric": METRIC, "value": value_us, "unit": "µs/step", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded normal), inputs resident in HBM",
+        "config": {"workload": (f"C2 Llama-30B attention shape (configs[1]): b={B}, H={H}, "
+                                f"d={D}, c={C}, s={args.s}, paged block {BLOCK}"),
+                   "global_batch": B, "seq_len": args.s,
+                   "parallelism": f"kv-head-shard{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed between timed steps (2x L2 buffer write)",
+                   "timing": "CUDA-graph replay of the 2-kernel step" if head.get("graph_ms", 1e9) <= head["eager_ms"] else "eager launches"},
+        "tokens_per_s": B / (ms * 1e-3),
+        "hbm_gbs": shape.bytes_alg / (ms * 1e-3) / 1e9,
+        "frac_of_hbm_roofline": (shape.bytes_alg / (hbm * 1e9)) / (ms * 1e-3),
+        "bytes_alg": shape.bytes_alg, "bytes_naive": shape.bytes_naive,
+        "eager_us_per_step": maxr(head["eager_ms"]) * 1e3,
+        "graph_us_per_step": maxr(head.get("graph_ms", float("nan"))) * 1e3,
+        "naive_us_per_step": maxr(head["naive_ms"]) * 1e3,
+        "sys_kernel_us": sys_ms * 1e3, "ctx_kernel_us": ctx_ms * 1e3,
+        "roofline": {"bound": "hbm", "kernel": "sys_attn_sm100_kernel",
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "traffic": ncu_traffic("sys_attn_sm100_kernel", args.s),
+                     "algorithmic_bytes_per_launch": sys_bytes_local},
+        "e2e": {"value": e2e_ms * 1e3, "unit": "µs/step", "h2d_bytes_per_step": head["h2d"],
+                "d2h_bytes_per_step": head["d2h"],
+                "path": "RelayDecodeStep.step_host: pinned H2D q,k_new,v_new -> rb_kv_append -> "
+                        "rb_system_attention -> rb_context_attention(relay) -> D2H out",
+                "launches_per_step": 3},
+        "gpu_launches": launches * args.steps,
+        "parity_max_abs_vs_naive": head["parity_max_abs_vs_naive"],
+        "sys_plan": head["plan"],
+        "sweep": sweep, "clocks": clk, "wall_s": wall,
+    }
+    if gathered_ok is not None:
+        line["sharded_allgather_ok"] = gathered_ok
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

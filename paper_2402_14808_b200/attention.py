@@ -420,6 +420,24 @@ class RelayDecodeStep:
         self.system(q)
         return self.context(q)
 
+    def step_host(self, q_host, k_new_host, v_new_host, slot_mapping, out_host):
+        """End-to-end decode step from host buffers (pinned for async copies):
+        H2D of the step's queries and new-token K/V, paged append at
+        `slot_mapping` (int32 device tensor), the relay step, and D2H of the
+        output into `out_host`.  All work is ordered on the current stream;
+        synchronise before reading `out_host`."""
+        if getattr(self, "_q_dev", None) is None:
+            self._q_dev = torch.empty(q_host.shape, dtype=torch.bfloat16, device=self.out.device)
+            self._k_dev = torch.empty(k_new_host.shape, dtype=torch.bfloat16, device=self.out.device)
+            self._v_dev = torch.empty(v_new_host.shape, dtype=torch.bfloat16, device=self.out.device)
+        self._q_dev.copy_(q_host, non_blocking=True)
+        self._k_dev.copy_(k_new_host, non_blocking=True)
+        self._v_dev.copy_(v_new_host, non_blocking=True)
+        self.paged.append_slots(self.layer, self._k_dev, self._v_dev, slot_mapping)
+        out, _ = self(self._q_dev)
+        out_host.copy_(out, non_blocking=True)
+        return out_host
+
 
 class NaiveDecodeStep:
     """The per-request baseline step ("vLLM-PS"; reference

@@ -16,11 +16,14 @@
 //    "vLLM-PS" baseline the paper compares against.
 //
 // Memory-bound design (HBM roofline): grid = (request,
-// kv head, row tile); 4 warps stride over 16-token chunks; a half-warp reads
-// one 256-byte K (or V) row with 16 B per lane (128-bit coalesced loads,
-// L1::no_allocate), dot products reduce with 4 xor-shuffles, online softmax
-// in the log2 domain per half-warp, then an smem merge of the 8 partial
-// states, the fusion, and one coalesced store per row.
+// kv head, row tile); 4 warps stride over 16-token chunks.  Each warp owns a
+// private 2-slot smem ring filled by cp.async.bulk (one 4 KB copy per paged
+// (block, head) run of K and of V, completing on an mbarrier), so a whole
+// 128-token context is in flight at once without costing registers.  A
+// half-warp reads one 256-byte key row from smem (16 B per lane), dot
+// products reduce with 4 xor-shuffles, online softmax in the log2 domain per
+// half-warp, then an smem merge of the 8 partial states, the fusion, and one
+// coalesced store per row.
 #include "rb_common.cuh"
 #include "rb_args.cuh"
 
@@ -29,7 +32,10 @@ namespace rb {
 
 
 constexpr int kCtxThreads = 128;
-constexpr int kChunk = 16;
+constexpr int kChunk = 16;                       // tokens per chunk
+constexpr int kRowBytes = RB_HEAD_DIM * 2;       // 256 B per key row
+constexpr int kSlotBytes = 2 * kChunk * kRowBytes;  // K + V of one chunk: 8 KB
+constexpr int kSlotsPerWarp = 2;
 
 __device__ __forceinline__ const __nv_bfloat16* ctx_row(const KvView& kv, const __nv_bfloat16* base,
                                                         int r, int t, int h) {
@@ -49,12 +55,15 @@ struct RowState {
   float m[R], l[R], acc[R][8];
 };
 
-// Process one 16-key chunk for a half-warp: keys key0 + 2p + hw, p = 0..7.
-// `lim[i]` is the exclusive key bound of row i inside this segment.
+// One 16-key chunk for a half-warp: keys key0 + 2p + hw, p = 0..7, K/V rows
+// already in registers.  `lim[i]` is the exclusive key bound of row i inside
+// this segment; keys at or past it contribute nothing (their V rows may hold
+// stale data and are zeroed, never multiplied).
 template <int R>
 __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[R][8],
-                                             const uint4 (&kr)[8], const uint4 (&vr)[8],
-                                             int key0, int hw, const int (&lim)[R], float scale_log2) {
+                                             const uint4 (&kr)[8], uint4 (&vr)[8],
+                                             int key0, int hw, const int (&lim)[R], float scale_log2,
+                                             int max_lim) {
   float x[R][8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
@@ -70,6 +79,7 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
       for (int e = 0; e < 8; ++e) s = fmaf(qf[i][e], kf[e], s);
       x[i][p] = s;
     }
+    if (key0 + 2 * p + hw >= max_lim) vr[p] = make_uint4(0, 0, 0, 0);
   }
 #pragma unroll
   for (int i = 0; i < R; ++i)
@@ -111,144 +121,266 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
   }
 }
 
+// Issue the bulk copies of chunk k (prefix chunks first, then context chunks)
+// into `slot` of the calling warp.  One (block, head) run of a paged pool is
+// contiguous, so a chunk inside one block is one 4 KB copy for K and one for
+// V; other layouts fall back to one 256 B copy per token, spread over lanes.
+__device__ __forceinline__ void issue_chunk(const CtxArgs& a, int r, int h, int k, int n_pre,
+                                            int max_lim, uint8_t* slot, uint64_t* bar, int lane) {
+  const __nv_bfloat16 *kbase, *vbase;
+  long long tok_stride;
+  int n;
+  bool contiguous;
+  if (k < n_pre) {
+    const int t0 = k * kChunk;
+    n = min(kChunk, a.s_prefix - t0);
+    const long long off = static_cast<long long>(h) * a.p_stride_head + t0 * a.p_stride_tok;
+    kbase = a.pk + off;
+    vbase = a.pv + off;
+    tok_stride = a.p_stride_tok;
+    contiguous = (a.p_stride_tok == RB_HEAD_DIM);
+  } else {
+    const int t0 = (k - n_pre) * kChunk;
+    n = min(kChunk, max_lim - t0);
+    kbase = ctx_row(a.ctx, a.ctx.k, r, t0, h);
+    vbase = ctx_row(a.ctx, a.ctx.v, r, t0, h);
+    tok_stride = a.ctx.stride_tok;
+    contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
+                 (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
+  }
+  if (lane == 0) mbar_arrive_expect_tx(bar, 2 * n * kRowBytes);
+  __syncwarp();
+  if (contiguous) {
+    if (lane == 0) {
+      bulk_copy_g2s(slot, kbase, n * kRowBytes, bar);
+      bulk_copy_g2s(slot + kChunk * kRowBytes, vbase, n * kRowBytes, bar);
+    }
+  } else if (lane < 2 * n) {
+    const int t = lane % n, which = lane / n;
+    const __nv_bfloat16* src;
+    if (k < n_pre) {
+      src = (which ? vbase : kbase) + t * tok_stride;
+    } else {
+      const int tt = (k - n_pre) * kChunk + t;
+      src = ctx_row(a.ctx, which ? a.ctx.v : a.ctx.k, r, tt, h);
+    }
+    bulk_copy_g2s(slot + which * kChunk * kRowBytes + t * kRowBytes, src, kRowBytes, bar);
+  }
+}
+
+// Work item = (request r, kv head h, row tile z).  Geometry of one item.
+template <int R>
+struct CtxItem {
+  int r, h, z, row0, m_r, nrows, c_r, max_lim, n_chunks;
+};
+
+template <int R>
+__device__ __forceinline__ CtxItem<R> ctx_item(const CtxArgs& a, int item, int n_z, int n_pre) {
+  CtxItem<R> it;
+  it.z = item % n_z;
+  it.h = (item / n_z) % a.hkv;
+  it.r = item / (n_z * a.hkv);
+  it.row0 = __ldg(a.q_start + it.r);
+  it.m_r = __ldg(a.q_start + it.r + 1) - it.row0;
+  it.nrows = it.m_r * a.g;
+  it.c_r = __ldg(a.ctx_lens + it.r);
+  const int rbase = it.z * R;
+  if (rbase >= it.nrows) {
+    it.max_lim = 0;
+    it.n_chunks = 0;
+    return it;
+  }
+  const int t_last = (min(rbase + R, it.nrows) - 1) / a.g;
+  it.max_lim = a.causal ? it.c_r - it.m_r + t_last + 1 : it.c_r;
+  it.n_chunks = n_pre + (it.max_lim + kChunk - 1) / kChunk;
+  return it;
+}
+
+// Persistent: CTA b processes items b, b + gridDim.x, ...  Each warp walks
+// its chunks (k = warp, warp + 4, ...) of those items as one stream through a
+// private 2-slot ring, so the copies of the next item are in flight while the
+// current item is computed and merged.
 template <int R>
 __global__ void __launch_bounds__(kCtxThreads)
-    ctx_attn_kernel(const CtxArgs a) {
-  const int r = blockIdx.x;
-  const int h = blockIdx.y;
+    ctx_attn_kernel(const CtxArgs a, int n_items, int n_z) {
+  extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int hw = lane >> 4, l16 = lane & 15;
-  const int row0 = a.q_start[r];
-  const int m_r = a.q_start[r + 1] - row0;
-  const int nrows_total = m_r * a.g;          // (token, group) rows of this (r, h)
-  const int rbase = blockIdx.z * R;           // first local row of this CTA
-  if (rbase >= nrows_total) return;
-  const int c_r = a.ctx_lens[r];
+  const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
+  uint8_t* my_slots = smem + warp * kSlotsPerWarp * kSlotBytes;
+  float* s_acc = reinterpret_cast<float*>(smem + 4 * kSlotsPerWarp * kSlotBytes);  // [8][R][128]
+  float* s_m = s_acc + 8 * R * 128;                                                // [8][R]
+  float* s_l = s_m + 8 * R;                                                        // [8][R]
+  uint64_t* my_bar = reinterpret_cast<uint64_t*>(s_l + 8 * R) + warp * kSlotsPerWarp;
 
-  // queries (fp32, 8 dims per lane) and per-row key limits
-  float qf[R][8];
-  int lim_ctx[R], lim_pre[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int li = rbase + i;
-    if (li < nrows_total) {
-      const int t = li / a.g, jj = li % a.g;
-      const __nv_bfloat16* qp = a.q + static_cast<long long>(row0 + t) * a.q_row_stride +
-                                static_cast<long long>(h * a.g + jj) * a.q_head_stride + l16 * 8;
-      const uint4 u = *reinterpret_cast<const uint4*>(qp);
-      qf[i][0] = bf16_lo(u.x); qf[i][1] = bf16_hi(u.x);
-      qf[i][2] = bf16_lo(u.y); qf[i][3] = bf16_hi(u.y);
-      qf[i][4] = bf16_lo(u.z); qf[i][5] = bf16_hi(u.z);
-      qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
-      lim_ctx[i] = a.causal ? c_r - m_r + t + 1 : c_r;
-      lim_pre[i] = a.s_prefix;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
-      lim_ctx[i] = 0;
-      lim_pre[i] = 0;
+  if (lane == 0) {
+    for (int sl = 0; sl < kSlotsPerWarp; ++sl) mbar_init(&my_bar[sl], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // ---- issue cursor: next (item, chunk) of this warp's stream
+  int is_item = blockIdx.x, is_k = warp;
+  CtxItem<R> is_geo = ctx_item<R>(a, min(is_item, n_items - 1), n_z, n_pre);
+  auto cursor_norm = [&]() {
+    while (is_item < n_items && is_k >= is_geo.n_chunks) {
+      is_item += gridDim.x;
+      is_k = warp;
+      if (is_item < n_items) is_geo = ctx_item<R>(a, is_item, n_z, n_pre);
     }
-  }
-  int max_lim = 0;
+  };
+  if (is_item >= n_items) return;
+  cursor_norm();
+  int issued = 0;
+  auto issue_next = [&]() {
+    if (is_item >= n_items) return;
+    const int sl = issued % kSlotsPerWarp;
+    issue_chunk(a, is_geo.r, is_geo.h, is_k, n_pre, is_geo.max_lim,
+                my_slots + sl * kSlotBytes, &my_bar[sl], lane);
+    ++issued;
+    is_k += 4;
+    cursor_norm();
+  };
 #pragma unroll
-  for (int i = 0; i < R; ++i) max_lim = max(max_lim, lim_ctx[i]);
+  for (int sl = 0; sl < kSlotsPerWarp; ++sl) issue_next();
 
-  RowState<R> st;
+  int consumed = 0;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
+    if (it.n_chunks == 0) continue;
+    const int rbase = it.z * R;
+    // queries, per-row key limits, and the system partial for the epilogue
+    float qf[R][8];
+    int lim_ctx[R], lim_pre[R];
+    float os_pref[R], ls_pref[R];
+    long long oidx[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    st.m[i] = -INFINITY;
-    st.l[i] = 0.f;
+    for (int i = 0; i < R; ++i) {
+      const int li = rbase + i;
+      os_pref[i] = 0.f;
+      ls_pref[i] = -INFINITY;
+      oidx[i] = -1;
+      if (li < it.nrows) {
+        const int t = li / a.g, jj = li % a.g;
+        oidx[i] = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
+        const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
+                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride + l16 * 8;
+        const uint4 u = *reinterpret_cast<const uint4*>(qp);
+        qf[i][0] = bf16_lo(u.x); qf[i][1] = bf16_hi(u.x);
+        qf[i][2] = bf16_lo(u.y); qf[i][3] = bf16_hi(u.y);
+        qf[i][4] = bf16_lo(u.z); qf[i][5] = bf16_hi(u.z);
+        qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
+        lim_ctx[i] = a.causal ? it.c_r - it.m_r + t + 1 : it.c_r;
+        lim_pre[i] = a.s_prefix;
+        if (a.o_sys != nullptr) {
+          os_pref[i] = __ldg(a.o_sys + oidx[i] * 128 + threadIdx.x);
+          ls_pref[i] = __ldg(a.lse_sys + oidx[i]);
+        }
+      } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
-  }
-
-  // ---- shared prefix segment (naive baseline only)
-  if (a.s_prefix > 0) {
-    const long long hoff = static_cast<long long>(h) * a.p_stride_head + l16 * 8;
-    for (int c0 = warp * kChunk; c0 < a.s_prefix; c0 += 4 * kChunk) {
+        for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
+        lim_ctx[i] = 0;
+        lim_pre[i] = 0;
+      }
+    }
+    RowState<R> st;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      st.m[i] = -INFINITY;
+      st.l[i] = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
+    }
+    for (int k = warp; k < it.n_chunks; k += 4, ++consumed) {
+      const int sl = consumed % kSlotsPerWarp;
+      uint8_t* slot = my_slots + sl * kSlotBytes;
+      mbar_wait(&my_bar[sl], (consumed / kSlotsPerWarp) & 1);
       uint4 kr[8], vr[8];
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
-        const int t = min(c0 + 2 * p + hw, a.s_prefix - 1);
-        kr[p] = ld_nc_v4(a.pk + static_cast<long long>(t) * a.p_stride_tok + hoff);
+        kr[p] = *reinterpret_cast<const uint4*>(slot + (2 * p + hw) * kRowBytes + l16 * 16);
+        vr[p] = *reinterpret_cast<const uint4*>(slot + kChunk * kRowBytes +
+                                                (2 * p + hw) * kRowBytes + l16 * 16);
       }
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        const int t = min(c0 + 2 * p + hw, a.s_prefix - 1);
-        vr[p] = ld_nc_v4(a.pv + static_cast<long long>(t) * a.p_stride_tok + hoff);
-      }
-      chunk_update<R>(st, qf, kr, vr, c0, hw, lim_pre, a.scale_log2);
+      // slot consumed (values are in registers): refill with the stream's next chunk
+      fence_proxy_async_smem();
+      __syncwarp();
+      issue_next();
+      if (k < n_pre)
+        chunk_update<R>(st, qf, kr, vr, k * kChunk, hw, lim_pre, a.scale_log2, a.s_prefix);
+      else
+        chunk_update<R>(st, qf, kr, vr, (k - n_pre) * kChunk, hw, lim_ctx, a.scale_log2,
+                        it.max_lim);
     }
-  }
-  // ---- request context segment (paged or ragged)
-  for (int c0 = warp * kChunk; c0 < max_lim; c0 += 4 * kChunk) {
-    uint4 kr[8], vr[8];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const int t = min(c0 + 2 * p + hw, max_lim - 1);
-      kr[p] = ld_nc_v4(ctx_row(a.ctx, a.ctx.k, r, t, h) + l16 * 8);
-    }
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const int t = min(c0 + 2 * p + hw, max_lim - 1);
-      vr[p] = ld_nc_v4(ctx_row(a.ctx, a.ctx.v, r, t, h) + l16 * 8);
-    }
-    chunk_update<R>(st, qf, kr, vr, c0, hw, lim_ctx, a.scale_log2);
-  }
 
-  // ---- merge the 8 (warp, half) partial states per row through smem
-  __shared__ float s_acc[8][R][128];
-  __shared__ float s_m[8][R], s_l[8][R];
-  const int wh = warp * 2 + hw;
+    // ---- merge the 8 (warp, half) partial states per row through smem
+    const int wh = warp * 2 + hw;
 #pragma unroll
-  for (int i = 0; i < R; ++i) {
-    *reinterpret_cast<float4*>(&s_acc[wh][i][l16 * 8]) =
-        make_float4(st.acc[i][0], st.acc[i][1], st.acc[i][2], st.acc[i][3]);
-    *reinterpret_cast<float4*>(&s_acc[wh][i][l16 * 8 + 4]) =
-        make_float4(st.acc[i][4], st.acc[i][5], st.acc[i][6], st.acc[i][7]);
-    if (l16 == 0) {
-      s_m[wh][i] = st.m[i];
-      s_l[wh][i] = st.l[i];
-    }
-  }
-  __syncthreads();
-  const int dcol = threadIdx.x;  // 128 threads = 128 head dims
-#pragma unroll 1
-  for (int i = 0; i < R; ++i) {
-    const int li = rbase + i;
-    if (li >= nrows_total) break;
-    float M = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) M = fmaxf(M, s_m[k][i]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float w = (s_m[k][i] == -INFINITY) ? 0.f : fast_exp2(s_m[k][i] - M);
-        L = fmaf(s_l[k][i], w, L);
-        O = fmaf(s_acc[k][i][dcol], w, O);
+    for (int i = 0; i < R; ++i) {
+      float* dst = s_acc + (wh * R + i) * 128 + l16 * 8;
+      *reinterpret_cast<float4*>(dst) =
+          make_float4(st.acc[i][0], st.acc[i][1], st.acc[i][2], st.acc[i][3]);
+      *reinterpret_cast<float4*>(dst + 4) =
+          make_float4(st.acc[i][4], st.acc[i][5], st.acc[i][6], st.acc[i][7]);
+      if (l16 == 0) {
+        s_m[wh * R + i] = st.m[i];
+        s_l[wh * R + i] = st.l[i];
       }
     }
-    float o = (L > 0.f) ? O / L : 0.f;
-    float lse2 = (L > 0.f) ? M + __log2f(L) : -INFINITY;
-    const int t = li / a.g, jj = li % a.g;
-    const long long oidx = static_cast<long long>(row0 + t) * a.hq + h * a.g + jj;
-    if (a.o_sys != nullptr) {
-      const float ls2 = a.lse_sys[oidx] * kLog2e;
-      const float os = a.o_sys[oidx * 128 + dcol];
-      const float mx = fmaxf(ls2, lse2);
-      const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
-      const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
-      const float inv = 1.f / (wc + ws);
-      o = (wc * o + ws * os) * inv;
-      lse2 = mx + __log2f(wc + ws);
+    __syncthreads();
+    const int dcol = threadIdx.x;  // 128 threads = 128 head dims
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      if (oidx[i] < 0) continue;
+      float M = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) M = fmaxf(M, s_m[k * R + i]);
+      float Ls = 0.f, O = 0.f;
+      if (M != -INFINITY) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float mk = s_m[k * R + i];
+          const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
+          Ls = fmaf(s_l[k * R + i], w, Ls);
+          O = fmaf(s_acc[(k * R + i) * 128 + dcol], w, O);
+        }
+      }
+      float o = (Ls > 0.f) ? O / Ls : 0.f;
+      float lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+      if (a.o_sys != nullptr) {
+        const float ls2 = ls_pref[i] * kLog2e;
+        const float mx = fmaxf(ls2, lse2);
+        const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
+        const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
+        const float inv = 1.f / (wc + ws);
+        o = (wc * o + ws * os_pref[i]) * inv;
+        lse2 = mx + __log2f(wc + ws);
+      }
+      if (a.out_fp32)
+        reinterpret_cast<float*>(a.out)[oidx[i] * 128 + dcol] = o;
+      else
+        reinterpret_cast<__nv_bfloat16*>(a.out)[oidx[i] * 128 + dcol] = __float2bfloat16_rn(o);
+      if (a.lse_out != nullptr && dcol == 0) a.lse_out[oidx[i]] = lse2 * kLn2;
     }
-    if (a.out_fp32)
-      reinterpret_cast<float*>(a.out)[oidx * 128 + dcol] = o;
-    else
-      reinterpret_cast<__nv_bfloat16*>(a.out)[oidx * 128 + dcol] = __float2bfloat16_rn(o);
-    if (a.lse_out != nullptr && dcol == 0) a.lse_out[oidx] = lse2 * kLn2;
+    __syncthreads();  // merge buffer free for the next item
   }
+}
+
+template <int R>
+static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStream_t stream) {
+  const int smem = 4 * kSlotsPerWarp * kSlotBytes + (8 * R * 128 + 16 * R) * 4 +
+                   4 * kSlotsPerWarp * 8;
+  cudaError_t e = cudaFuncSetAttribute(ctx_attn_kernel<R>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxThreads, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
+  ctx_attn_kernel<R><<<grid, kCtxThreads, smem, stream>>>(a, n_items, n_z);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_t stream) {
@@ -257,14 +389,15 @@ cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_
   if (max_rows >= 8) R = 8;
   else if (max_rows >= 4) R = 4;
   else if (max_rows >= 2) R = 2;
-  dim3 grid(a.b, a.hkv, (max_rows + R - 1) / R);
+  const int n_z = (max_rows + R - 1) / R;
+  const int n_items = a.b * a.hkv * n_z;
+  if (n_items == 0) return cudaSuccess;
   switch (R) {
-    case 1: ctx_attn_kernel<1><<<grid, kCtxThreads, 0, stream>>>(a); break;
-    case 2: ctx_attn_kernel<2><<<grid, kCtxThreads, 0, stream>>>(a); break;
-    case 4: ctx_attn_kernel<4><<<grid, kCtxThreads, 0, stream>>>(a); break;
-    default: ctx_attn_kernel<8><<<grid, kCtxThreads, 0, stream>>>(a); break;
+    case 1: return launch_ctx_r<1>(a, n_items, n_z, stream);
+    case 2: return launch_ctx_r<2>(a, n_items, n_z, stream);
+    case 4: return launch_ctx_r<4>(a, n_items, n_z, stream);
+    default: return launch_ctx_r<8>(a, n_items, n_z, stream);
   }
-  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- relay fusion

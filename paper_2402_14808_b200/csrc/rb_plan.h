@@ -28,7 +28,7 @@ typedef struct {
   int n_rows;         // flattened query rows (sum of m_r over requests)
   int hq, hkv, g;     // query heads, kv heads, group size hq / hkv
   int s;              // shared prefix length (keys)
-  int nq;             // query rows per tile (16, 32 or 64)
+  int nq;             // query rows per tile (16 or 32)
   int rows_per_head;  // n_rows * g
   int n_qt;           // ceil(rows_per_head / nq)
   int tpu;            // key tiles per unit, ceil(s / 128)
@@ -51,11 +51,7 @@ RB_HD int rb_unit_parts(const rb_sys_plan* p, int u) {
   return rb_tile_owner(p, last) - rb_tile_owner(p, first) + 1;
 }
 
-RB_HD int rb_pick_nq(int rows_per_head) {
-  if (rows_per_head <= 16) return 16;
-  if (rows_per_head <= 32) return 32;
-  return 64;
-}
+RB_HD int rb_pick_nq(int rows_per_head) { return rows_per_head <= 16 ? 16 : 32; }
 
 // Fill a plan. grid_cap = number of CTAs the device can hold at once
 // (SM count for this one-CTA-per-SM kernel).

@@ -9,7 +9,7 @@
 //
 // Design:
 //  * swap-AB: the MMA M dimension is the 128 keys of a tile, N is the
-//    (request x GQA-group) query rows of one KV head (nq = 16/32/64), so a
+//    (request x GQA-group) query rows of one KV head (nq = 16/32), so a
 //    batch of 32 decode rows still fills M = 128:
 //        S^T[128 keys x nq] = K_tile[128 x d] . Q^T        (both K-major)
 //        O^T[d x nq]       = V_tile^T[d x 128] . P^T       (A MN-major)
@@ -35,30 +35,35 @@
 namespace rb {
 
 
-constexpr int kSysThreads = 320;  // 10 warps
 constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
 constexpr int kStageBytes = 2 * kKvTileBytes;               // K + V
 
-template <int NQ, int STAGES>
-struct SysSmem {
-  static constexpr int H = NQ / 2;                 // columns per compute warp
-  static constexpr int kQBytes = NQ * 256;         // [2 kblocks][NQ][128 B]
+// Shared-memory / thread layout for a query tile of NQ rows.  Two compute
+// groups alternate key tiles (even / odd local tile index), each with its own
+// online-softmax state; a group has NHALF slices of 4 warps (one per TMEM
+// lane quadrant), each thread handling H query columns.
+template <int NQ>
+struct SysCfg {
+  static constexpr int H = 16;
+  static constexpr int NHALF = NQ / H;
+  static constexpr int WPG = 4 * NHALF;                 // warps per group
+  static constexpr int NCW = 2 * WPG;                   // compute warps
+  static constexpr int kThreads = 64 + NCW * 32;
+  static constexpr int STAGES = 3;
+  static constexpr int kQBytes = NQ * 256;              // [2 kblocks][NQ][128 B]
   static constexpr int kOffKV = 0;
   static constexpr int kOffQ = kOffKV + STAGES * kStageBytes;
   static constexpr int kOffP = kOffQ + 2 * kQBytes;
-  static constexpr int kOffRedMax = kOffP + 2 * kQBytes;         // [2 halves][4][H]
-  static constexpr int kOffRedSum = kOffRedMax + 2 * 4 * H * 4;
-  static constexpr int kOffAlpha = kOffRedSum + 2 * 4 * H * 4;   // [2 par][2 halves][H]
-  static constexpr int kOffL = kOffAlpha + 2 * 2 * H * 4;        // [2 halves][H]
-  static constexpr int kOffBar = kOffL + 2 * H * 4;
-  // barriers: full[S], empty[S], s_full[2], s_empty[2], p_full[2], p_empty[2],
-  //           o_full[2], o_empty[2], q_full[2], q_empty[2]
-  static constexpr int kNumBars = 2 * STAGES + 16;
-  static constexpr int kOffMisc = kOffBar + kNumBars * 8;   // tmem base + flags
+  static constexpr int kRedBytes = 2 * NHALF * 4 * H * 4;  // [group][half][quadrant][H]
+  static constexpr int kOffRedMax = kOffP + 2 * kQBytes;
+  static constexpr int kOffRedSum = kOffRedMax + kRedBytes;
+  static constexpr int kOffL = kOffRedSum + kRedBytes;   // [group][NQ]
+  static constexpr int kOffX = kOffL + 2 * NQ * 4;       // handover m, l: [2][NQ]
+  static constexpr int kOffBar = kOffX + 2 * NQ * 4;
+  static constexpr int kNumBars = 2 * STAGES + 18;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64;
-  static constexpr int kAlloc = kBytes + 1024;              // slack for 1 KB alignment
-  static constexpr int kTmemCols = (4 * NQ <= 32) ? 32 : (4 * NQ <= 64) ? 64
-                                 : (4 * NQ <= 128) ? 128 : (4 * NQ <= 256) ? 256 : 512;
+  static constexpr int kTmemCols = (5 * NQ <= 128) ? 128 : (5 * NQ <= 256) ? 256 : 512;
 };
 
 template <int H>
@@ -68,8 +73,8 @@ __device__ __forceinline__ int reduce_scatter_col(int lane) {
 }
 
 // Reduce-scatter H per-lane values over the 32 lanes of a warp: afterwards
-// v[0] holds the reduction of column reduce_scatter_col<H>(lane) over all
-// lanes.  H - 1 + (5 - log2 H) shuffles.
+// the returned value is the reduction of column reduce_scatter_col<H>(lane)
+// over all 32 lanes.  H - 1 + (5 - log2 H) shuffles.
 template <int H, bool IS_MAX>
 __device__ __forceinline__ float warp_reduce_scatter(float (&v)[H], int lane) {
 #pragma unroll
@@ -93,15 +98,14 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[H], int lane) {
   return r;
 }
 
-template <int NQ, int STAGES>
-__global__ void __launch_bounds__(kSysThreads, 1)
+template <int NQ>
+__global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
                           const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
-  using L = SysSmem<NQ, STAGES>;
+  using L = SysCfg<NQ>;
   constexpr int H = L::H;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  constexpr int STAGES = L::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
   uint64_t* full_bar = bars;
   uint64_t* empty_bar = bars + STAGES;
@@ -113,11 +117,13 @@ __global__ void __launch_bounds__(kSysThreads, 1)
   uint64_t* o_empty = s_full + 10;
   uint64_t* q_full = s_full + 12;
   uint64_t* q_empty = s_full + 14;
+  uint64_t* x_full = s_full + 16;
+  uint64_t* x_empty = s_full + 17;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
   float* red_max = reinterpret_cast<float*>(smem + L::kOffRedMax);
   float* red_sum = reinterpret_cast<float*>(smem + L::kOffRedSum);
-  float* alpha_s = reinterpret_cast<float*>(smem + L::kOffAlpha);
   float* l_s = reinterpret_cast<float*>(smem + L::kOffL);
+  float* x_ml = reinterpret_cast<float*>(smem + L::kOffX);
 
   const rb_sys_plan& P = args.plan;
   const int warp = threadIdx.x >> 5;
@@ -125,7 +131,8 @@ __global__ void __launch_bounds__(kSysThreads, 1)
   const long long t_begin = rb_cta_begin(&P, blockIdx.x);
   const long long t_end = rb_cta_begin(&P, blockIdx.x + 1);
 
-  if (warp == 0 && lane == 0) {
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
     for (int i = 0; i < STAGES; ++i) {
@@ -134,18 +141,19 @@ __global__ void __launch_bounds__(kSysThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&s_empty[i], L::WPG);
+      mbar_init(&p_full[i], L::WPG);
       mbar_init(&p_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 8);
+      mbar_init(&o_empty[i], L::WPG);
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
+    mbar_init(x_full, L::WPG);
+    mbar_init(x_empty, L::WPG);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(&misc[0], L::kTmemCols);
-  if (threadIdx.x < 2 * H) l_s[threadIdx.x] = 0.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -164,29 +172,6 @@ __global__ void __launch_bounds__(kSysThreads, 1)
       const int kt = static_cast<int>(i % P.tpu);
       const int h = u / P.n_qt;
       const int qt = u % P.n_qt;
-      if (i == t_begin || kt == 0) {
-        const int qb = uq & 1;
-        mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
-        uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
-        for (int idx = lane; idx < NQ * 16; idx += 32) {
-          const int c = idx >> 4, ch = idx & 15;
-          const int f = qt * NQ + c;
-          uint4 val = make_uint4(0, 0, 0, 0);
-          if (f < P.rows_per_head) {
-            const int row = f / P.g, jj = f % P.g;
-            const __nv_bfloat16* src = args.q + row * args.q_row_stride +
-                                       static_cast<long long>(h * P.g + jj) * args.q_head_stride +
-                                       ch * 8;
-            val = *reinterpret_cast<const uint4*>(src);
-          }
-          const int kb = ch >> 3;
-          *reinterpret_cast<uint4*>(qdst + kb * (NQ * 128) + sw128_offset(c, (ch & 7) * 8)) = val;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&q_full[qb]);
-        ++uq;
-      }
       const int st = j % STAGES;
       mbar_wait(&empty_bar[st], ((j / STAGES) & 1) ^ 1);
       if (lane == 0) {
@@ -199,6 +184,31 @@ __global__ void __launch_bounds__(kSysThreads, 1)
                     kt * RB_KEY_TILE, h, pol);
       }
       __syncwarp();
+      if (i == t_begin || kt == 0) {
+        // query rows of unit u (after this tile's K/V are already in flight)
+        const int qb = uq & 1;
+        mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
+        uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
+        // all of the tile's 16-byte chunks in flight at once (zero-fill past the rows)
+#pragma unroll
+        for (int it = 0; it < NQ / 2; ++it) {
+          const int idx = lane + it * 32;
+          const int c = idx >> 4, ch = idx & 15;
+          const int f = qt * NQ + c;
+          const bool ok = f < P.rows_per_head;
+          const int row = ok ? f / P.g : 0, jj = ok ? f % P.g : 0;
+          const __nv_bfloat16* src = args.q + row * args.q_row_stride +
+                                     static_cast<long long>(h * P.g + jj) * args.q_head_stride +
+                                     ch * 8;
+          cp_async_16(qdst + (ch >> 3) * (NQ * 128) + sw128_offset(c, (ch & 7) * 8), src,
+                      ok ? 16u : 0u);
+        }
+        cp_async_wait_all();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_full[qb]);
+        ++uq;
+      }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kSysThreads, 1)
         const uint32_t d_tmem = tmem_base + sb * NQ;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * 0 + (kk & 3) * 32;
+          const uint32_t koff = (kk & 3) * 32;
           const uint64_t a =
               make_smem_desc_sw128(k_base + (kk >> 2) * (kKvTileBytes / 2) + koff, 16, 1024);
           const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + koff, 16, 1024);
@@ -258,130 +268,179 @@ __global__ void __launch_bounds__(kSysThreads, 1)
     }
     __syncwarp();
   } else {
-    // ------------------------------------------- softmax / O accumulation
-    const int cw = warp - 2;          // 0..7
-    const int hf = cw >> 2;           // column half
-    const int qd = warp & 3;          // TMEM lane quadrant (hardware: warp % 4)
+    // ------------------------------------- softmax / O accumulation groups
+    const int cw = warp - 2;
+    const int grp = cw / L::WPG;                 // which tile parity this group owns
+    const int hf = (cw / 4) % L::NHALF;          // column slice
+    const int qd = warp & 3;                     // TMEM lane quadrant (hardware: warp % 4)
+    const int col0 = hf * H;
     const bool designated = (qd == 0) && lane < H;
+    const uint32_t bar_red = 1 + grp * L::NHALF + hf;
+    const uint32_t bar_grp = 1 + 2 * L::NHALF + grp;
     const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+    float* rmax = red_max + (grp * L::NHALF + hf) * 4 * H;
+    float* rsum = red_sum + (grp * L::NHALF + hf) * 4 * H;
+    float* lg = l_s + grp * NQ;
+    const int rcol = reduce_scatter_col<H>(lane);
+    const bool rwriter = (lane & ((32 / H) - 1)) == 0;
+    const int key_lane = qd * 32 + lane;
+    // per-thread swizzled P row offsets (8-row pattern) for this key lane
+    uint32_t poff[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) poff[r] = sw128_offset(r, key_lane & 63);
+    const uint32_t pkb = (key_lane >> 6) * (NQ * 128);
+
     float m_run[H], acc[H];
-    int j = 0;
-    for (long long i = t_begin; i < t_end; ++i, ++j) {
+    int xh = 0;  // handovers so far
+    long long i = t_begin;
+    while (i < t_end) {
       const int u = static_cast<int>(i / P.tpu);
-      const int kt = static_cast<int>(i % P.tpu);
-      const bool new_unit = (i == t_begin) || kt == 0;
-      const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
-      if (new_unit) {
-#pragma unroll
-        for (int c = 0; c < H; ++c) {
-          m_run[c] = -INFINITY;
-          acc[c] = 0.f;
-        }
-      }
-      const int sb = j & 1;
-      // ---- S tile -> scores (log2 domain)
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      float x[H];
-      tmem_ld_32x32b<H>(lane_addr + sb * NQ + hf * H, x);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[sb]);
-      const bool valid = kt * RB_KEY_TILE + qd * 32 + lane < P.s;
-#pragma unroll
-      for (int c = 0; c < H; ++c) x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
-      // ---- tile max across the 128 key lanes
-      float tmp[H];
-#pragma unroll
-      for (int c = 0; c < H; ++c) tmp[c] = x[c];
-      const float wmax = warp_reduce_scatter<H, true>(tmp, lane);
-      const int rcol = reduce_scatter_col<H>(lane);
-      float* rm = red_max + hf * 4 * H;
-      if ((lane & ((32 / H) - 1)) == 0) rm[qd * H + rcol] = wmax;
-      named_bar_sync(1 + hf, 128);
-      float m_new[H];
-#pragma unroll
-      for (int c4 = 0; c4 < H; c4 += 4) {
-        float4 a0 = *reinterpret_cast<const float4*>(rm + 0 * H + c4);
-        float4 a1 = *reinterpret_cast<const float4*>(rm + 1 * H + c4);
-        float4 a2 = *reinterpret_cast<const float4*>(rm + 2 * H + c4);
-        float4 a3 = *reinterpret_cast<const float4*>(rm + 3 * H + c4);
-        m_new[c4 + 0] = fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x));
-        m_new[c4 + 1] = fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y));
-        m_new[c4 + 2] = fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z));
-        m_new[c4 + 3] = fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w));
-      }
-      float* alpha_cur = alpha_s + ((j & 1) * 2 + hf) * H;
+      const long long unit_end = min(t_end, static_cast<long long>(u + 1) * P.tpu);
+      const long long ia = i, ib = unit_end - 1;
 #pragma unroll
       for (int c = 0; c < H; ++c) {
-        const float mn = fmaxf(m_run[c], m_new[c]);
-        const float al = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
-        if (designated && lane == c) alpha_cur[c] = al;
-        m_run[c] = mn;
-        x[c] = fast_exp2(x[c] - mn);  // p, exactly 0 for masked keys
+        m_run[c] = -INFINITY;
+        acc[c] = 0.f;
       }
-      // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
-      mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);
-      {
-        const int key = qd * 32 + lane;
-        uint8_t* pdst = smem + L::kOffP + sb * L::kQBytes + (key >> 6) * (NQ * 128);
-#pragma unroll
-        for (int c = 0; c < H; ++c) {
-          *reinterpret_cast<__nv_bfloat16*>(pdst + sw128_offset(hf * H + c, key & 63)) =
-              __float2bfloat16_rn(x[c]);
-        }
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[sb]);
-      // ---- row sums
-      const float wsum = warp_reduce_scatter<H, false>(x, lane);
-      float* rs = red_sum + hf * 4 * H;
-      if ((lane & ((32 / H) - 1)) == 0) rs[qd * H + rcol] = wsum;
-      named_bar_sync(1 + hf, 128);
-      if (designated) {
-        const float lt = rs[0 * H + lane] + rs[1 * H + lane] + rs[2 * H + lane] + rs[3 * H + lane];
-        l_s[hf * H + lane] = l_s[hf * H + lane] * alpha_cur[lane] + lt;
-      }
-      // ---- O accumulation (previous tile of this unit, then this one if last)
-      auto accumulate = [&](int jj) {
-        const int ob = jj & 1;
-        mbar_wait(&o_full[ob], (jj >> 1) & 1);
+      if (designated) lg[col0 + lane] = 0.f;
+      for (long long it = ia + ((ia - t_begin + grp) & 1); it <= ib; it += 2) {
+        const int j = static_cast<int>(it - t_begin);
+        const int kt = static_cast<int>(it % P.tpu);
+        const int gb = j & 1;  // == grp
+        const uint32_t ph = (j >> 1) & 1;
+        // ---- S tile -> scores (log2 domain)
+        mbar_wait(&s_full[gb], ph);
         tc_fence_after();
-        float o[H];
-        tmem_ld_32x32b<H>(lane_addr + 2 * NQ + ob * NQ + hf * H, o);
+        float x[H];
+        tmem_ld_32x32b<H>(lane_addr + gb * NQ + col0, x);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&o_empty[ob]);
-        const float* al = alpha_s + ((jj & 1) * 2 + hf) * H;
+        if (lane == 0) mbar_arrive(&s_empty[gb]);
+        const bool valid = kt * RB_KEY_TILE + key_lane < P.s;
+#pragma unroll
+        for (int c = 0; c < H; ++c) x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
+        // ---- tile max over the 128 key lanes (4 quadrant warps)
+        {
+          float tmp[H];
+#pragma unroll
+          for (int c = 0; c < H; ++c) tmp[c] = x[c];
+          const float wmax = warp_reduce_scatter<H, true>(tmp, lane);
+          if (rwriter) rmax[qd * H + rcol] = wmax;
+        }
+        named_bar_sync(bar_red, 128);
+        float my_al = 0.f;
 #pragma unroll
         for (int c4 = 0; c4 < H; c4 += 4) {
-          const float4 a = *reinterpret_cast<const float4*>(al + c4);
-          acc[c4 + 0] = fmaf(acc[c4 + 0], a.x, o[c4 + 0]);
-          acc[c4 + 1] = fmaf(acc[c4 + 1], a.y, o[c4 + 1]);
-          acc[c4 + 2] = fmaf(acc[c4 + 2], a.z, o[c4 + 2]);
-          acc[c4 + 3] = fmaf(acc[c4 + 3], a.w, o[c4 + 3]);
+          const float4 a0 = *reinterpret_cast<const float4*>(rmax + 0 * H + c4);
+          const float4 a1 = *reinterpret_cast<const float4*>(rmax + 1 * H + c4);
+          const float4 a2 = *reinterpret_cast<const float4*>(rmax + 2 * H + c4);
+          const float4 a3 = *reinterpret_cast<const float4*>(rmax + 3 * H + c4);
+          const float tm[4] = {fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)),
+                               fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y)),
+                               fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)),
+                               fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = c4 + e;
+            const float mn = fmaxf(m_run[c], tm[e]);
+            const float al = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
+            acc[c] *= al;
+            my_al = (lane == c) ? al : my_al;
+            m_run[c] = mn;
+            x[c] = fast_exp2(x[c] - mn);  // p; exactly 0 for masked keys
+          }
         }
-      };
-      if (!new_unit) accumulate(j - 1);
-      if (last_of_unit) {
-        accumulate(j);
-        // ---- finalize unit u
-        named_bar_sync(3, 256);  // l_s complete for all columns
+        // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
+        mbar_wait(&p_empty[gb], ph ^ 1);
+        {
+          uint8_t* pdst = smem + L::kOffP + gb * L::kQBytes + pkb;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int row = col0 + c;
+            *reinterpret_cast<__nv_bfloat16*>(pdst + (row >> 3) * 1024 + poff[row & 7]) =
+                __float2bfloat16_rn(x[c]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[gb]);
+        // ---- row sums
+        const float wsum = warp_reduce_scatter<H, false>(x, lane);
+        if (rwriter) rsum[qd * H + rcol] = wsum;
+        named_bar_sync(bar_red, 128);
+        if (designated) {
+          const float lt = rsum[0 * H + lane] + rsum[1 * H + lane] + rsum[2 * H + lane] +
+                           rsum[3 * H + lane];
+          lg[col0 + lane] = lg[col0 + lane] * my_al + lt;
+        }
+        // ---- O tile of this key tile
+        mbar_wait(&o_full[gb], ph);
+        tc_fence_after();
+        float o[H];
+        tmem_ld_32x32b<H>(lane_addr + 2 * NQ + gb * NQ + col0, o);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[gb]);
+#pragma unroll
+        for (int c = 0; c < H; ++c) acc[c] += o[c];
+      }
+
+      // ---- unit end: merge the two groups, then write / stream-K merge
+      const int fin = static_cast<int>((ib - t_begin) & 1);
+      const bool two = ib > ia;
+      const uint32_t xaddr = lane_addr + 4 * NQ + col0;
+      if (two && grp != fin) {
+        // helper: hand (acc, m, l) to the finisher through TMEM / smem
+        mbar_wait(x_empty, (xh & 1) ^ 1);
+        tmem_st_32x32b<H>(xaddr, acc);
+        tmem_wait_st();
+        if (designated) {
+          float mv = m_run[0];
+#pragma unroll
+          for (int c = 1; c < H; ++c) mv = (lane == c) ? m_run[c] : mv;
+          x_ml[col0 + lane] = mv;
+          x_ml[NQ + col0 + lane] = lg[col0 + lane];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(x_full);
+      }
+      if (grp == fin) {
+        named_bar_sync(bar_grp, L::WPG * 32);  // own l_s complete
+        float lrow[H];
+#pragma unroll
+        for (int c = 0; c < H; ++c) lrow[c] = lg[col0 + c];
+        if (two) {
+          mbar_wait(x_full, xh & 1);
+          tc_fence_after();
+          float oh[H];
+          tmem_ld_32x32b<H>(xaddr, oh);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const float mh = x_ml[col0 + c], lh = x_ml[NQ + col0 + c];
+            const float M = fmaxf(m_run[c], mh);
+            const float wf = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - M);
+            const float wh = (mh == -INFINITY) ? 0.f : fast_exp2(mh - M);
+            acc[c] = acc[c] * wf + oh[c] * wh;
+            lrow[c] = lrow[c] * wf + lh * wh;
+            m_run[c] = M;
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(x_empty);
+        }
         const int h = u / P.n_qt, qt = u % P.n_qt;
         const long long u_first = static_cast<long long>(u) * P.tpu;
         const int owner0 = rb_tile_owner(&P, u_first);
         const int nparts = rb_unit_parts(&P, u);
-        const int dcol = qd * 32 + lane;
-        float lrow[H];
-#pragma unroll
-        for (int c = 0; c < H; ++c) lrow[c] = l_s[hf * H + c];
+        const int dcol = key_lane;  // O lane = head-dim index
         if (nparts == 1) {
 #pragma unroll
           for (int c = 0; c < H; ++c) {
-            const int f = qt * NQ + hf * H + c;
+            const int f = qt * NQ + col0 + c;
             if (f < P.rows_per_head) {
               const int row = f / P.g, hh = h * P.g + f % P.g;
               const long long o_idx = static_cast<long long>(row) * P.hq + hh;
@@ -397,7 +456,7 @@ __global__ void __launch_bounds__(kSysThreads, 1)
           float* pml = args.part_ml + pbase * 2 * NQ;
 #pragma unroll
           for (int c = 0; c < H; ++c) {
-            const int col = hf * H + c;
+            const int col = col0 + c;
             pacc[col * RB_HEAD_DIM + dcol] = acc[c];
             if (qd == 0 && lane == 0) {
               pml[col] = m_run[c];
@@ -405,21 +464,22 @@ __global__ void __launch_bounds__(kSysThreads, 1)
             }
           }
           __threadfence();
-          named_bar_sync(3, 256);
-          if (threadIdx.x == 64) {
+          named_bar_sync(bar_grp, L::WPG * 32);
+          if (cw == grp * L::WPG && lane == 0) {
             const int prev = atomicAdd(&args.counters[u], 1);
             const int last = (prev == nparts - 1);
             if (last) atomicExch(&args.counters[u], 0);
-            misc[1] = last;
+            misc[2 + grp] = last;
           }
-          named_bar_sync(3, 256);
-          if (misc[1]) {
+          named_bar_sync(bar_grp, L::WPG * 32);
+          if (misc[2 + grp]) {
             __threadfence();
-            const float* uacc = args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
+            const float* uacc =
+                args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
             const float* uml = args.part_ml + static_cast<long long>(u) * P.max_parts * 2 * NQ;
 #pragma unroll 1
             for (int c = 0; c < H; ++c) {
-              const int col = hf * H + c;
+              const int col = col0 + c;
               const int f = qt * NQ + col;
               if (f >= P.rows_per_head) continue;
               float M = -INFINITY;
@@ -428,7 +488,8 @@ __global__ void __launch_bounds__(kSysThreads, 1)
               for (int k = 0; k < nparts; ++k) {
                 const float w = fast_exp2(__ldcg(uml + k * 2 * NQ + col) - M);
                 Ls = fmaf(__ldcg(uml + k * 2 * NQ + NQ + col), w, Ls);
-                Os = fmaf(__ldcg(uacc + (static_cast<long long>(k) * NQ + col) * RB_HEAD_DIM + dcol), w, Os);
+                Os = fmaf(__ldcg(uacc + (static_cast<long long>(k) * NQ + col) * RB_HEAD_DIM + dcol),
+                          w, Os);
               }
               const int row = f / P.g, hh = h * P.g + f % P.g;
               const long long o_idx = static_cast<long long>(row) * P.hq + hh;
@@ -437,10 +498,9 @@ __global__ void __launch_bounds__(kSysThreads, 1)
             }
           }
         }
-        // reset running sums for the next unit (designated threads own l_s)
-        named_bar_sync(3, 256);
-        if (designated) l_s[hf * H + lane] = 0.f;
       }
+      if (two) ++xh;
+      i = unit_end;
     }
   }
 
@@ -454,24 +514,23 @@ __global__ void __launch_bounds__(kSysThreads, 1)
 
 // ------------------------------------------------------------------- host
 
-template <int NQ, int STAGES>
+template <int NQ>
 static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, const SysArgs& a,
                               cudaStream_t stream) {
-  using L = SysSmem<NQ, STAGES>;
-  static_assert(L::kAlloc <= 232448, "system kernel shared memory over the 227 KB limit");
-  auto kern = sys_attn_sm100_kernel<NQ, STAGES>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kAlloc);
+  using L = SysCfg<NQ>;
+  static_assert(L::kBytes <= 232448, "system kernel shared memory over the 227 KB limit");
+  auto kern = sys_attn_sm100_kernel<NQ>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
   if (e != cudaSuccess) return e;
-  kern<<<a.plan.grid, kSysThreads, L::kAlloc, stream>>>(tk, tv, a);
+  kern<<<a.plan.grid, L::kThreads, L::kBytes, stream>>>(tk, tv, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
                                     const SysArgs& a, cudaStream_t stream) {
   switch (a.plan.nq) {
-    case 16: return launch_sys<16, 3>(tk, tv, a, stream);
-    case 32: return launch_sys<32, 3>(tk, tv, a, stream);
-    case 64: return launch_sys<64, 2>(tk, tv, a, stream);
+    case 16: return launch_sys<16>(tk, tv, a, stream);
+    case 32: return launch_sys<32>(tk, tv, a, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -483,9 +542,7 @@ template <int NQ>
 __global__ void umma_probe_kernel(const __nv_bfloat16* k, const __nv_bfloat16* q,
                                   const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
                                   float* o_out) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sk = smem;
   uint8_t* sv = smem + kKvTileBytes;
   uint8_t* sq = smem + 2 * kKvTileBytes;
@@ -562,7 +619,7 @@ template <int N>
 static cudaError_t launch_probe_n(const __nv_bfloat16* k, const __nv_bfloat16* q,
                                   const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
                                   float* o_out, cudaStream_t stream) {
-  const int smem = 2 * kKvTileBytes + 2 * 64 * 256 + 64 + 1024;
+  const int smem = 2 * kKvTileBytes + 2 * 64 * 256 + 64;
   cudaError_t e =
       cudaFuncSetAttribute(umma_probe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

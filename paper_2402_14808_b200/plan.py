@@ -12,11 +12,7 @@ KEY_TILE = 128
 
 
 def pick_nq(rows_per_head: int) -> int:
-    if rows_per_head <= 16:
-        return 16
-    if rows_per_head <= 32:
-        return 32
-    return 64
+    return 16 if rows_per_head <= 16 else 32
 
 
 @dataclass(frozen=True)

@@ -79,7 +79,7 @@ def test_umma_probe_layouts(rb, nq):
     (4, 2, 2, 200, None),        # nq 16, partial last tile
     (32, 4, 4, 1000, None),      # nq 32 (C2-like rows)
     (32, 4, 4, 1000, 5),         # forced stream-K splits (many partial slots)
-    (64, 2, 2, 384, 3),          # nq 64
+    (64, 2, 2, 384, 3),          # 64 rows/head -> 2 q-tiles of 32
     (24, 8, 2, 300, 7),          # GQA g=4: 96 rows/head -> 2 q-tiles
     (1, 1, 1, 1, None),          # single key
 ])
