@@ -112,6 +112,31 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
                          float* lse_out, void* stream);
 
 /*
+ * The whole relay decode step in one call -- `relay_attention_ragged`
+ * (attention.py:203-243) over a shared prefix and paged (or ragged) context:
+ * the tcgen05 system kernel writes its stream-K partial slots into
+ * `workspace` without merging them, and the context kernel (launched with
+ * programmatic dependent launch, so it streams context K/V while the system
+ * kernel drains) merges every system slot of a (row, head) with its own
+ * context state in ONE LSE-weighted combine -- the relay fusion
+ * (attention.py:137-157) -- writing `out` (bf16 or fp32) and the fused LSE.
+ * Arguments are those of rb_system_attention + rb_context_attention (causal).
+ * workspace: rb_relay_workspace_bytes(...) bytes, no initialisation needed.
+ * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
+ * (profiling: phase 2 consumes the slots a previous phase-1 call wrote).
+ */
+int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes);
+int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_stride,
+                       const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
+                       const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
+                       long long sys_stride_head, const void* k, const void* v,
+                       const int* block_table, int bt_stride, int block_size,
+                       const long long* req_offset, long long stride_block, long long stride_tok,
+                       long long stride_head, const int* ctx_lens, float scale, int grid_cap,
+                       void* out, int out_fp32, float* lse_out, void* workspace,
+                       size_t workspace_bytes, int phases, void* stream);
+
+/*
  * Standalone relay fusion (attention.py:137-157) over n_vec vectors of d
  * fp32 values: out = a*o_sys + (1-a)*o_ctx, a = 1/(1+exp(lse_ctx-lse_sys)),
  * evaluated with max-subtracted weights; lse_out (optional) = logaddexp.
@@ -137,6 +162,14 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
  */
 int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void* p, int nq,
                         float* s_out, float* o_out, void* stream);
+
+/*
+ * Debug: when `buf` (device, [grid][8] u64) is non-NULL, subsequent
+ * rb_system_attention launches record per-CTA %globaltimer stamps into it
+ * (entry, prologue done, first S tile, group-0 end, group-1 end, producer end,
+ * V-producer end, exit).  NULL disables.  For profiling only.
+ */
+int rb_debug_set_timestamps(void* buf);
 
 #ifdef __cplusplus
 }

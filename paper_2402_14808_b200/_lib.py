@@ -21,7 +21,8 @@ RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
 EXPORTS = (
     "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
     "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
-    "rb_debug_umma_probe",
+    "rb_relay_workspace_bytes", "rb_relay_attention",
+    "rb_debug_umma_probe", "rb_debug_set_timestamps",
 )
 
 _lib = None
@@ -52,9 +53,17 @@ def load():
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
         i32, vp, vp, i32, i64, i64,                      # causal, prefix
         vp, vp, f32, vp, i32, vp, vp]                    # o_sys .. stream
+    lib.rb_relay_workspace_bytes.argtypes = [i32, i32, i32, i32, i32,
+                                             ctypes.POINTER(ctypes.c_size_t)]
+    lib.rb_relay_attention.argtypes = [
+        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,   # q .. d
+        vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
+        vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,      # k .. ctx_lens
+        f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+    lib.rb_debug_set_timestamps.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("rb_last_error", "rb_abi_version"):
             getattr(lib, name).restype = i32
@@ -85,6 +94,13 @@ def sys_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
           "rb_sys_plan_query")
     keys = ("nq", "n_qt", "tpu", "n_units", "total", "grid", "max_parts")
     return dict(zip(keys, list(f)[:7])), ws.value
+
+
+def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
+          "rb_relay_workspace_bytes")
+    return out.value
 
 
 def sm_count(device: int = 0) -> int:

@@ -224,8 +224,9 @@ def relay_attention_ragged(q_list, sys_k, sys_v, ctx_k, ctx_v, counter=None,
     (c_r, h_kv, d) including the current tokens; sys_k/sys_v: (s, h_kv, d),
     s >= 1.  Equals causal attention over [system || context] per request.
 
-    The system segment runs once for the whole batch (tcgen05 kernel), the
-    context segment and the fusion run in one paged kernel.  Fusion is a
+    One rb_relay_attention call: the system segment runs once for the whole
+    batch (tcgen05 kernel), the context segment and the fusion run in one
+    kernel.  Fusion is a
     single deterministic LSE merge, so `system_first` cannot change the
     result (the reference's bitwise order-independence, attention.py:208-212).
     """
@@ -276,11 +277,10 @@ def relay_attention_ragged(q_list, sys_k, sys_v, ctx_k, ctx_v, counter=None,
                            device=dev)
     lens = torch.tensor(c_list, dtype=torch.int32, device=dev)
 
-    o_sys, lse_sys = kernels.system_attention(qf, skd, svd, kv_layout="shd", scale=scale)
-    out, lse = kernels.context_attention(
-        qf, q_start, ckd, cvd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv,
-        req_offset=req_off, strides=(0, ckd.stride(0), ckd.stride(1)), causal=True,
-        o_sys=o_sys, lse_sys=lse_sys, scale=scale, out_fp32=True)
+    out, lse = kernels.relay_attention(
+        qf, q_start, skd, svd, ckd, cvd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv,
+        sys_layout="shd", req_offset=req_off, strides=(0, ckd.stride(0), ckd.stride(1)),
+        scale=scale, out_fp32=True)
     if counter is not None:
         _count_relay(counter, m_list, c_list, s, h, d)
     outs, lses, row = [], [], 0
@@ -376,9 +376,11 @@ class RelayDecodeStep:
     """One relay decode step (m = 1 token per request) over resident caches.
 
     q: (b, hq, 128) bf16 -> out (b, hq, 128) bf16 and fused lse (b, hq) fp32.
-    Launches exactly two kernels on the current stream: the tcgen05 system
-    kernel (shared prefix read once) and the paged context kernel with the
-    relay fusion in its epilogue.  All buffers are preallocated, so the step
+    One rb_relay_attention call = two kernels on the current stream: the
+    tcgen05 system kernel (shared prefix read once, stream-K partials left
+    unmerged) and the paged context kernel, launched with programmatic
+    dependent launch, whose epilogue merges the system partials with the
+    context state (relay fusion).  All buffers are preallocated, so the step
     can be captured in a CUDA graph.
     """
 
@@ -395,30 +397,33 @@ class RelayDecodeStep:
         dev = block_table.device
         self.grid = kernels.sm_count(dev) if grid is None else grid
         from . import _lib
-        self.plan, need = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
-        self.o_sys = torch.empty((self.b, hq, HEAD_DIM), dtype=torch.float32, device=dev)
-        self.lse_sys = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
         self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
 
+    def _launch(self, q, phases):
+        return kernels.relay_attention(
+            q, self.q_start, self.sys_cache.keys[self.layer], self.sys_cache.values[self.layer],
+            self.paged.k_pool[self.layer], self.paged.v_pool[self.layer], self.ctx_lens,
+            max_rows=self.hq // self.hkv, hkv=self.hkv, sys_layout="hsd",
+            block_table=self.block_table, block_size=self.paged.block_size,
+            strides=self.paged.strides(), grid=self.grid, out=self.out, lse_out=self.lse,
+            ws=self.ws, phases=phases)
+
     def system(self, q):
-        return kernels.system_attention(
-            q, self.sys_cache.keys[self.layer], self.sys_cache.values[self.layer],
-            kv_layout="hsd", grid=self.grid, o_sys=self.o_sys, lse_sys=self.lse_sys, ws=self.ws)
+        """Only the system kernel of the step (profiling)."""
+        return self._launch(q, 1)
 
     def context(self, q):
-        return kernels.context_attention(
-            q, self.q_start, self.paged.k_pool[self.layer], self.paged.v_pool[self.layer],
-            self.ctx_lens, max_rows=self.hq // self.hkv, hkv=self.hkv,
-            block_table=self.block_table, block_size=self.paged.block_size,
-            strides=self.paged.strides(), causal=True, o_sys=self.o_sys, lse_sys=self.lse_sys,
-            out=self.out, lse_out=self.lse)
+        """Only the context + fusion kernel (profiling; consumes the system
+        partials of the last `system` call)."""
+        return self._launch(q, 2)
 
     def __call__(self, q):
-        self.system(q)
-        return self.context(q)
+        return self._launch(q, 3)
 
     def step_host(self, q_host, k_new_host, v_new_host, slot_mapping, out_host):
         """End-to-end decode step from host buffers (pinned for async copies):
@@ -437,6 +442,35 @@ class RelayDecodeStep:
         out, _ = self(self._q_dev)
         out_host.copy_(out, non_blocking=True)
         return out_host
+
+    def host_step_graph(self, qkv_host, slot_mapping, out_host):
+        """CUDA-graph version of `step_host` for a serving loop.
+
+        qkv_host: pinned bf16 (3, b, h, 128) holding this step's q, k_new,
+        v_new (one H2D copy); out_host: pinned bf16 (b, hq, 128).  Returns a
+        callable that replays H2D -> append -> relay -> D2H on the current
+        stream; refill `qkv_host` between calls.
+        """
+        dev = self.out.device
+        qkv_dev = torch.empty(qkv_host.shape, dtype=torch.bfloat16, device=dev)
+
+        def body():
+            qkv_dev.copy_(qkv_host, non_blocking=True)
+            self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
+            out, _ = self(qkv_dev[0])
+            out_host.copy_(out, non_blocking=True)
+
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            body()
+        self._host_graph = graph  # keep alive with its buffers
+        self._host_graph_bufs = (qkv_dev,)
+        return graph.replay
 
 
 class NaiveDecodeStep:

@@ -37,6 +37,7 @@ cudaError_t launch_kv_append(const __nv_bfloat16*, const __nv_bfloat16*, const i
 
 
 static thread_local std::string g_err;
+static unsigned long long* g_debug_ts = nullptr;  // test-only instrumentation
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -165,6 +166,8 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
   a.counters = reinterpret_cast<int*>(ws);
   a.part_ml = reinterpret_cast<float*>(ws + cnt);
   a.part_acc = reinterpret_cast<float*>(ws + cnt + ml);
+  a.debug_ts = g_debug_ts;
+  a.defer_merge = 0;
   CUtensorMap tk, tv;
   st = make_kv_map(&tk, sys_k, s, hkv, kv_stride_tok, kv_stride_head);
   if (st != RB_OK) return st;
@@ -221,6 +224,8 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.p_stride_tok = p_stride_tok;
   a.p_stride_head = p_stride_head;
   a.s_prefix = s_prefix;
+  a.sys_part_acc = nullptr;
+  a.sys_part_ml = nullptr;
   a.o_sys = o_sys;
   a.lse_sys = lse_sys;
   a.out = out;
@@ -229,6 +234,102 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.scale_log2 = scale * rb::kLog2e;
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
                      "context attention launch");
+}
+
+// ------------------------------------------------- fused relay decode step
+int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes) {
+  long long f[8];
+  size_t dummy = 0;
+  int st = rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, &dummy);
+  if (st != RB_OK) return st;
+  rb_sys_plan p;
+  rb_make_sys_plan(&p, n_rows, hq, hkv, s, grid_cap);
+  const size_t ml = ((size_t)p.n_units * p.max_parts * 2 * p.nq * sizeof(float) + 255) & ~(size_t)255;
+  const size_t acc = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
+  *bytes = 256 + ml + acc;
+  return RB_OK;
+}
+
+int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_stride,
+                       const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
+                       const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
+                       long long sys_stride_head, const void* k, const void* v,
+                       const int* block_table, int bt_stride, int block_size,
+                       const long long* req_offset, long long stride_block, long long stride_tok,
+                       long long stride_head, const int* ctx_lens, float scale, int grid_cap,
+                       void* out, int out_fp32, float* lse_out, void* workspace,
+                       size_t workspace_bytes, int phases, void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
+  size_t need = 0;
+  int st = rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, &need);
+  if (st != RB_OK) return st;
+  if (workspace_bytes < need)
+    return fail(RB_ERR_CONTRACT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  if (block_table == nullptr && req_offset == nullptr)
+    return fail(RB_ERR_CONTRACT, "either block_table (paged) or req_offset (ragged) is required");
+  if ((q_head_stride * 2) % 16 != 0 || (q_row_stride * 2) % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(q) & 15))
+    return fail(RB_ERR_CONTRACT, "q rows must be 16-byte aligned");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  rb::SysArgs sa;
+  rb_make_sys_plan(&sa.plan, n_rows, hq, hkv, s, grid_cap);
+  sa.q = static_cast<const __nv_bfloat16*>(q);
+  sa.q_row_stride = q_row_stride;
+  sa.q_head_stride = q_head_stride;
+  sa.scale_log2 = scale * rb::kLog2e;
+  sa.o_sys = nullptr;
+  sa.lse_sys = nullptr;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  const size_t ml = ((size_t)sa.plan.n_units * sa.plan.max_parts * 2 * sa.plan.nq * sizeof(float) +
+                     255) & ~(size_t)255;
+  sa.counters = nullptr;
+  sa.part_ml = reinterpret_cast<float*>(ws + 256);
+  sa.part_acc = reinterpret_cast<float*>(ws + 256 + ml);
+  sa.debug_ts = g_debug_ts;
+  sa.defer_merge = 1;
+  CUtensorMap tk, tv;
+  st = make_kv_map(&tk, sys_k, s, hkv, sys_stride_tok, sys_stride_head);
+  if (st != RB_OK) return st;
+  st = make_kv_map(&tv, sys_v, s, hkv, sys_stride_tok, sys_stride_head);
+  if (st != RB_OK) return st;
+  if (phases & 1) {
+    st = cuda_status(rb::launch_system_attention(tk, tv, sa, cs), "system attention launch");
+    if (st != RB_OK) return st;
+  }
+  if (b < 1 || !(phases & 2)) return RB_OK;
+  rb::CtxArgs a;
+  a.b = b;
+  a.hq = hq;
+  a.hkv = hkv;
+  a.g = hq / hkv;
+  a.q_start = q_start;
+  a.q = static_cast<const __nv_bfloat16*>(q);
+  a.q_row_stride = q_row_stride;
+  a.q_head_stride = q_head_stride;
+  a.ctx.k = static_cast<const __nv_bfloat16*>(k);
+  a.ctx.v = static_cast<const __nv_bfloat16*>(v);
+  a.ctx.block_table = block_table;
+  a.ctx.bt_stride = bt_stride;
+  a.ctx.block_size = block_size;
+  a.ctx.req_offset = req_offset;
+  a.ctx.stride_block = stride_block;
+  a.ctx.stride_tok = stride_tok;
+  a.ctx.stride_head = stride_head;
+  a.ctx_lens = ctx_lens;
+  a.causal = 1;
+  a.pk = a.pv = nullptr;
+  a.p_stride_tok = a.p_stride_head = 0;
+  a.s_prefix = 0;
+  a.sys_part_acc = sa.part_acc;
+  a.sys_part_ml = sa.part_ml;
+  a.sys_plan = sa.plan;
+  a.o_sys = nullptr;
+  a.lse_sys = nullptr;
+  a.out = out;
+  a.out_fp32 = out_fp32;
+  a.lse_out = lse_out;
+  a.scale_log2 = scale * rb::kLog2e;
+  return cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
 }
 
 int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx,
@@ -252,6 +353,11 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
                            n_tok, hkv, block_size, stride_block, stride_tok, stride_head,
                            static_cast<cudaStream_t>(stream)),
       "kv append launch");
+}
+
+int rb_debug_set_timestamps(void* buf) {
+  g_debug_ts = static_cast<unsigned long long*>(buf);
+  return RB_OK;
 }
 
 int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void* p, int nq,

@@ -31,11 +31,9 @@ namespace rb {
 
 
 
-constexpr int kCtxThreads = 128;
 constexpr int kChunk = 16;                       // tokens per chunk
 constexpr int kRowBytes = RB_HEAD_DIM * 2;       // 256 B per key row
 constexpr int kSlotBytes = 2 * kChunk * kRowBytes;  // K + V of one chunk: 8 KB
-constexpr int kSlotsPerWarp = 2;
 
 __device__ __forceinline__ const __nv_bfloat16* ctx_row(const KvView& kv, const __nv_bfloat16* base,
                                                         int r, int t, int h) {
@@ -121,53 +119,6 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
   }
 }
 
-// Issue the bulk copies of chunk k (prefix chunks first, then context chunks)
-// into `slot` of the calling warp.  One (block, head) run of a paged pool is
-// contiguous, so a chunk inside one block is one 4 KB copy for K and one for
-// V; other layouts fall back to one 256 B copy per token, spread over lanes.
-__device__ __forceinline__ void issue_chunk(const CtxArgs& a, int r, int h, int k, int n_pre,
-                                            int max_lim, uint8_t* slot, uint64_t* bar, int lane) {
-  const __nv_bfloat16 *kbase, *vbase;
-  long long tok_stride;
-  int n;
-  bool contiguous;
-  if (k < n_pre) {
-    const int t0 = k * kChunk;
-    n = min(kChunk, a.s_prefix - t0);
-    const long long off = static_cast<long long>(h) * a.p_stride_head + t0 * a.p_stride_tok;
-    kbase = a.pk + off;
-    vbase = a.pv + off;
-    tok_stride = a.p_stride_tok;
-    contiguous = (a.p_stride_tok == RB_HEAD_DIM);
-  } else {
-    const int t0 = (k - n_pre) * kChunk;
-    n = min(kChunk, max_lim - t0);
-    kbase = ctx_row(a.ctx, a.ctx.k, r, t0, h);
-    vbase = ctx_row(a.ctx, a.ctx.v, r, t0, h);
-    tok_stride = a.ctx.stride_tok;
-    contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
-                 (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
-  }
-  if (lane == 0) mbar_arrive_expect_tx(bar, 2 * n * kRowBytes);
-  __syncwarp();
-  if (contiguous) {
-    if (lane == 0) {
-      bulk_copy_g2s(slot, kbase, n * kRowBytes, bar);
-      bulk_copy_g2s(slot + kChunk * kRowBytes, vbase, n * kRowBytes, bar);
-    }
-  } else if (lane < 2 * n) {
-    const int t = lane % n, which = lane / n;
-    const __nv_bfloat16* src;
-    if (k < n_pre) {
-      src = (which ? vbase : kbase) + t * tok_stride;
-    } else {
-      const int tt = (k - n_pre) * kChunk + t;
-      src = ctx_row(a.ctx, which ? a.ctx.v : a.ctx.k, r, tt, h);
-    }
-    bulk_copy_g2s(slot + which * kChunk * kRowBytes + t * kRowBytes, src, kRowBytes, bar);
-  }
-}
-
 // Work item = (request r, kv head h, row tile z).  Geometry of one item.
 template <int R>
 struct CtxItem {
@@ -196,60 +147,108 @@ __device__ __forceinline__ CtxItem<R> ctx_item(const CtxArgs& a, int item, int n
   return it;
 }
 
-// Persistent: CTA b processes items b, b + gridDim.x, ...  Each warp walks
-// its chunks (k = warp, warp + 4, ...) of those items as one stream through a
-// private 2-slot ring, so the copies of the next item are in flight while the
-// current item is computed and merged.
+// Persistent producer/consumer kernel.  CTA b processes items b, b + grid,
+// ...; their chunks form one sequence.  Warp 0 is the producer: its lanes
+// resolve block-table entries and issue the bulk copies of up to 32 chunks
+// at once into a CTA-wide ring of kRing slots (waiting on each slot's empty
+// barrier), so the copies run far ahead of the math.  Warps 1..4 consume
+// chunk k of an item in warp 1 + (k % 4), then merge their partial states at
+// the end of the item and run the fusion epilogue (thread = head dim).
+constexpr int kRing = 12;                      // 12 x 8 KB = 96 KB of K/V in flight per CTA
+constexpr int kCtxThreadsPC = 160;             // producer + 4 consumers
+
 template <int R>
-__global__ void __launch_bounds__(kCtxThreads)
+__global__ void __launch_bounds__(kCtxThreadsPC)
     ctx_attn_kernel(const CtxArgs a, int n_items, int n_z) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hw = lane >> 4, l16 = lane & 15;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
-  uint8_t* my_slots = smem + warp * kSlotsPerWarp * kSlotBytes;
-  float* s_acc = reinterpret_cast<float*>(smem + 4 * kSlotsPerWarp * kSlotBytes);  // [8][R][128]
-  float* s_m = s_acc + 8 * R * 128;                                                // [8][R]
-  float* s_l = s_m + 8 * R;                                                        // [8][R]
-  uint64_t* my_bar = reinterpret_cast<uint64_t*>(s_l + 8 * R) + warp * kSlotsPerWarp;
+  uint8_t* ring = smem;
+  float* s_acc = reinterpret_cast<float*>(smem + kRing * kSlotBytes);  // [8][R][128]
+  float* s_m = s_acc + 8 * R * 128;                                    // [8][R]
+  float* s_l = s_m + 8 * R;                                            // [8][R]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_l + 8 * R);
+  uint64_t* empty = full + kRing;
 
-  if (lane == 0) {
-    for (int sl = 0; sl < kSlotsPerWarp; ++sl) mbar_init(&my_bar[sl], 1);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
+  pdl_launch_dependents();
 
-  // ---- issue cursor: next (item, chunk) of this warp's stream
-  int is_item = blockIdx.x, is_k = warp;
-  CtxItem<R> is_geo = ctx_item<R>(a, min(is_item, n_items - 1), n_z, n_pre);
-  auto cursor_norm = [&]() {
-    while (is_item < n_items && is_k >= is_geo.n_chunks) {
-      is_item += gridDim.x;
-      is_k = warp;
-      if (is_item < n_items) is_geo = ctx_item<R>(a, is_item, n_z, n_pre);
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    long long seq = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
+      for (int k0 = 0; k0 < it.n_chunks; k0 += 32) {
+        const int k = k0 + lane;
+        if (k < it.n_chunks) {
+          const long long sq = seq + k;
+          const int slot = static_cast<int>(sq % kRing);
+          mbar_wait(&empty[slot], static_cast<uint32_t>(((sq / kRing) & 1) ^ 1));
+          const __nv_bfloat16 *kb, *vb;
+          int n;
+          bool contiguous;
+          long long tok_stride;
+          if (k < n_pre) {
+            const int t0 = k * kChunk;
+            n = min(kChunk, a.s_prefix - t0);
+            const long long off = static_cast<long long>(it.h) * a.p_stride_head + t0 * a.p_stride_tok;
+            kb = a.pk + off;
+            vb = a.pv + off;
+            tok_stride = a.p_stride_tok;
+            contiguous = (a.p_stride_tok == RB_HEAD_DIM);
+          } else {
+            const int t0 = (k - n_pre) * kChunk;
+            n = min(kChunk, it.max_lim - t0);
+            kb = ctx_row(a.ctx, a.ctx.k, it.r, t0, it.h);
+            vb = ctx_row(a.ctx, a.ctx.v, it.r, t0, it.h);
+            tok_stride = a.ctx.stride_tok;
+            contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
+                         (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
+          }
+          uint8_t* dst = ring + slot * kSlotBytes;
+          mbar_arrive_expect_tx(&full[slot], 2 * n * kRowBytes);
+          if (contiguous) {
+            bulk_copy_g2s(dst, kb, n * kRowBytes, &full[slot]);
+            bulk_copy_g2s(dst + kChunk * kRowBytes, vb, n * kRowBytes, &full[slot]);
+          } else {
+            for (int t = 0; t < n; ++t) {
+              const __nv_bfloat16 *ks, *vs;
+              if (k < n_pre) {
+                ks = kb + t * tok_stride;
+                vs = vb + t * tok_stride;
+              } else {
+                const int tt = (k - n_pre) * kChunk + t;
+                ks = ctx_row(a.ctx, a.ctx.k, it.r, tt, it.h);
+                vs = ctx_row(a.ctx, a.ctx.v, it.r, tt, it.h);
+              }
+              bulk_copy_g2s(dst + t * kRowBytes, ks, kRowBytes, &full[slot]);
+              bulk_copy_g2s(dst + kChunk * kRowBytes + t * kRowBytes, vs, kRowBytes, &full[slot]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      seq += it.n_chunks;
     }
-  };
-  if (is_item >= n_items) return;
-  cursor_norm();
-  int issued = 0;
-  auto issue_next = [&]() {
-    if (is_item >= n_items) return;
-    const int sl = issued % kSlotsPerWarp;
-    issue_chunk(a, is_geo.r, is_geo.h, is_k, n_pre, is_geo.max_lim,
-                my_slots + sl * kSlotBytes, &my_bar[sl], lane);
-    ++issued;
-    is_k += 4;
-    cursor_norm();
-  };
-#pragma unroll
-  for (int sl = 0; sl < kSlotsPerWarp; ++sl) issue_next();
+    return;
+  }
 
-  int consumed = 0;
+  // -------------------------------------------------------------- consumers
+  const int cw = warp - 1;                      // 0..3
+  const int hw = lane >> 4, l16 = lane & 15;
+  long long seq = 0;
+  bool waited = false;
   for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
     const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
     if (it.n_chunks == 0) continue;
     const int rbase = it.z * R;
-    // queries, per-row key limits, and the system partial for the epilogue
     float qf[R][8];
     int lim_ctx[R], lim_pre[R];
     float os_pref[R], ls_pref[R];
@@ -272,10 +271,6 @@ __global__ void __launch_bounds__(kCtxThreads)
         qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
         lim_ctx[i] = a.causal ? it.c_r - it.m_r + t + 1 : it.c_r;
         lim_pre[i] = a.s_prefix;
-        if (a.o_sys != nullptr) {
-          os_pref[i] = __ldg(a.o_sys + oidx[i] * 128 + threadIdx.x);
-          ls_pref[i] = __ldg(a.lse_sys + oidx[i]);
-        }
       } else {
 #pragma unroll
         for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
@@ -291,30 +286,44 @@ __global__ void __launch_bounds__(kCtxThreads)
 #pragma unroll
       for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
     }
-    for (int k = warp; k < it.n_chunks; k += 4, ++consumed) {
-      const int sl = consumed % kSlotsPerWarp;
-      uint8_t* slot = my_slots + sl * kSlotBytes;
-      mbar_wait(&my_bar[sl], (consumed / kSlotsPerWarp) & 1);
+    for (int k = cw; k < it.n_chunks; k += 4) {
+      const long long sq = seq + k;
+      const int slot = static_cast<int>(sq % kRing);
+      mbar_wait(&full[slot], static_cast<uint32_t>((sq / kRing) & 1));
+      const uint8_t* src = ring + slot * kSlotBytes;
       uint4 kr[8], vr[8];
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
-        kr[p] = *reinterpret_cast<const uint4*>(slot + (2 * p + hw) * kRowBytes + l16 * 16);
-        vr[p] = *reinterpret_cast<const uint4*>(slot + kChunk * kRowBytes +
-                                                (2 * p + hw) * kRowBytes + l16 * 16);
+        kr[p] = *reinterpret_cast<const uint4*>(src + (2 * p + hw) * kRowBytes + l16 * 16);
+        vr[p] = *reinterpret_cast<const uint4*>(src + kChunk * kRowBytes + (2 * p + hw) * kRowBytes +
+                                                l16 * 16);
       }
-      // slot consumed (values are in registers): refill with the stream's next chunk
       fence_proxy_async_smem();
       __syncwarp();
-      issue_next();
+      if (lane == 0) mbar_arrive(&empty[slot]);
       if (k < n_pre)
         chunk_update<R>(st, qf, kr, vr, k * kChunk, hw, lim_pre, a.scale_log2, a.s_prefix);
       else
         chunk_update<R>(st, qf, kr, vr, (k - n_pre) * kChunk, hw, lim_ctx, a.scale_log2,
                         it.max_lim);
     }
+    seq += it.n_chunks;
 
+    if (!waited) {  // before the first global write / system-output read
+      pdl_wait_primary();
+      waited = true;
+    }
+    if (a.o_sys != nullptr) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        if (oidx[i] >= 0) {
+          os_pref[i] = __ldcg(a.o_sys + oidx[i] * 128 + (threadIdx.x - 32));
+          ls_pref[i] = __ldcg(a.lse_sys + oidx[i]);
+        }
+      }
+    }
     // ---- merge the 8 (warp, half) partial states per row through smem
-    const int wh = warp * 2 + hw;
+    const int wh = cw * 2 + hw;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       float* dst = s_acc + (wh * R + i) * 128 + l16 * 8;
@@ -327,8 +336,8 @@ __global__ void __launch_bounds__(kCtxThreads)
         s_l[wh * R + i] = st.l[i];
       }
     }
-    __syncthreads();
-    const int dcol = threadIdx.x;  // 128 threads = 128 head dims
+    named_bar_sync(1, 128);
+    const int dcol = threadIdx.x - 32;  // 128 consumer threads = 128 head dims
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       if (oidx[i] < 0) continue;
@@ -345,8 +354,46 @@ __global__ void __launch_bounds__(kCtxThreads)
           O = fmaf(s_acc[(k * R + i) * 128 + dcol], w, O);
         }
       }
-      float o = (Ls > 0.f) ? O / Ls : 0.f;
-      float lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+      float o, lse2;
+      if (a.sys_part_acc != nullptr) {
+        // one LSE-weighted combine of the system kernel's stream-K parts of
+        // this (row, head) and the context state (M, Ls, O): relay fusion.
+        const rb_sys_plan& SP = a.sys_plan;
+        const long long row = oidx[i] / a.hq;
+        const int hh = static_cast<int>(oidx[i] % a.hq);
+        const long long f = row * SP.g + hh % SP.g;
+        const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
+        const int u = (hh / SP.g) * SP.n_qt + qt;
+        const int np = rb_unit_parts(&SP, u);
+        const long long base = static_cast<long long>(u) * SP.max_parts;
+        float mt = M, lt = Ls, ot = O;
+        for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
+          float mk[4], lk[4], ak[4];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int k = min(k0 + kk, np - 1);
+            const float* ml = a.sys_part_ml + (base + k) * 2 * SP.nq;
+            mk[kk] = __ldcg(ml + col);
+            lk[kk] = __ldcg(ml + SP.nq + col);
+            ak[kk] = __ldcg(a.sys_part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + dcol);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (k0 + kk >= np) break;
+            const float mn = fmaxf(mt, mk[kk]);
+            const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+            const float sk = fast_exp2(mk[kk] - mn);
+            lt = lt * so + lk[kk] * sk;
+            ot = ot * so + ak[kk] * sk;
+            mt = mn;
+          }
+        }
+        o = ot / lt;
+        lse2 = mt + __log2f(lt);
+      } else {
+        o = (Ls > 0.f) ? O / Ls : 0.f;
+        lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+      }
       if (a.o_sys != nullptr) {
         const float ls2 = ls_pref[i] * kLog2e;
         const float mx = fmaxf(ls2, lse2);
@@ -362,24 +409,31 @@ __global__ void __launch_bounds__(kCtxThreads)
         reinterpret_cast<__nv_bfloat16*>(a.out)[oidx[i] * 128 + dcol] = __float2bfloat16_rn(o);
       if (a.lse_out != nullptr && dcol == 0) a.lse_out[oidx[i]] = lse2 * kLn2;
     }
-    __syncthreads();  // merge buffer free for the next item
+    named_bar_sync(1, 128);  // merge buffer free for the next item
   }
 }
 
 template <int R>
 static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStream_t stream) {
-  const int smem = 4 * kSlotsPerWarp * kSlotBytes + (8 * R * 128 + 16 * R) * 4 +
-                   4 * kSlotsPerWarp * 8;
+  const int smem = kRing * kSlotBytes + (8 * R * 128 + 16 * R) * 4 + 2 * kRing * 8;
   cudaError_t e = cudaFuncSetAttribute(ctx_attn_kernel<R>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxThreadsPC, smem);
   if (e != cudaSuccess) return e;
   const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
-  ctx_attn_kernel<R><<<grid, kCtxThreads, smem, stream>>>(a, n_items, n_z);
+  // Relay mode follows the system kernel, which triggers early: launch with
+  // PDL so this kernel streams context K/V on SMs the system kernel has
+  // already released (it waits for the system grid before reading its
+  // outputs).  Other modes are ordinary stream-ordered launches.
+  if (a.o_sys != nullptr || a.sys_part_acc != nullptr)
+    e = launch_pdl(ctx_attn_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, a, n_items, n_z);
+  else
+    ctx_attn_kernel<R><<<grid, kCtxThreadsPC, smem, stream>>>(a, n_items, n_z);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -17,6 +17,8 @@ struct SysArgs {
   float* part_acc;         // fp32 [n_units][max_parts][nq][128] (unnormalised)
   float* part_ml;          // fp32 [n_units][max_parts][2][nq]   (m log2, l)
   int* counters;           // int  [n_units], zero between launches
+  unsigned long long* debug_ts;  // optional per-CTA %globaltimer stamps [grid][8]
+  int defer_merge;         // 1: write every unit part to its slot, no merge, no o_sys
 };
 
 struct KvView {
@@ -44,6 +46,11 @@ struct CtxArgs {
   const __nv_bfloat16* pv;
   long long p_stride_tok, p_stride_head;
   int s_prefix;
+  // optional deferred system partials (relay): stream-K slots of the system
+  // kernel, merged here in the fusion epilogue
+  const float* sys_part_acc;     // [n_units][max_parts][nq][128]
+  const float* sys_part_ml;      // [n_units][max_parts][2][nq]
+  rb_sys_plan sys_plan;
   // optional system partial (relay)
   const float* o_sys;            // [n_rows][hq][128]
   const float* lse_sys;          // [n_rows][hq] natural log

@@ -14,13 +14,17 @@
 //        S^T[128 keys x nq] = K_tile[128 x d] . Q^T        (both K-major)
 //        O^T[d x nq]       = V_tile^T[d x 128] . P^T       (A MN-major)
 //    accumulators in TMEM (2 S buffers + 2 O buffers = 4*nq columns).
-//  * K/V tiles (128 keys x 128 d bf16 = 32 KB each) are TMA-loaded with the
-//    128B swizzle through a STAGES-deep mbarrier ring: every shared-prefix
-//    byte crosses HBM exactly once per step.
-//  * warp roles: warp 0 TMA producer (+ Q rows), warp 1 MMA issuer (one
-//    thread) + TMEM owner, warps 2..9 softmax / O accumulation.  Thread t of
-//    a compute warp owns TMEM lane t of its quadrant = key t of the tile for
-//    S, = head-dim index t for O.
+//  * K and V tiles (128 keys x 128 d bf16 = 32 KB each) are TMA-loaded with
+//    the 128B swizzle through two mbarrier rings: K slots are released as soon
+//    as S^T = K.Q^T completes, V slots after O^T = V^T.P^T, so the shallow K
+//    ring and the deeper V ring keep ~4 tiles of HBM reads in flight per SM.
+//    Every shared-prefix byte crosses HBM exactly once per step.
+//  * warp roles: warp 0 K producer (+ Q rows via cp.async), warp 1 QK^T
+//    issuer (one thread) + TMEM owner, warp 2 V producer, warp 3 PV issuer,
+//    then two compute groups that alternate key tiles, each with its own
+//    online-softmax state (merged at the end of a unit through TMEM).
+//    Thread t of a compute warp owns TMEM lane t of its quadrant = key t of
+//    the tile for S, = head-dim index t for O.
 //  * online softmax in the log2 domain: per-query max / sum across the 128
 //    key lanes via a warp reduce-scatter butterfly + a 4-warp smem combine;
 //    O accumulates in registers (acc = acc*alpha + O_tile), so the tensor
@@ -36,7 +40,6 @@ namespace rb {
 
 
 constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
-constexpr int kStageBytes = 2 * kKvTileBytes;               // K + V
 
 // Shared-memory / thread layout for a query tile of NQ rows.  Two compute
 // groups alternate key tiles (even / odd local tile index), each with its own
@@ -48,11 +51,15 @@ struct SysCfg {
   static constexpr int NHALF = NQ / H;
   static constexpr int WPG = 4 * NHALF;                 // warps per group
   static constexpr int NCW = 2 * WPG;                   // compute warps
-  static constexpr int kThreads = 64 + NCW * 32;
-  static constexpr int STAGES = 3;
+  static constexpr int kRoleWarps = 4;                  // K producer, QK issuer, V producer, PV issuer
+  static constexpr int kThreads = (kRoleWarps + NCW) * 32;
+  static constexpr int KS = 2;                          // K ring (freed after Q.K^T)
+  static constexpr int VS = 4;                          // V ring (freed after P.V)
+  static constexpr int kTileBytes = kKvTileBytes;       // 32 KB per K or V tile
   static constexpr int kQBytes = NQ * 256;              // [2 kblocks][NQ][128 B]
-  static constexpr int kOffKV = 0;
-  static constexpr int kOffQ = kOffKV + STAGES * kStageBytes;
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + KS * kTileBytes;
+  static constexpr int kOffQ = kOffV + VS * kTileBytes;
   static constexpr int kOffP = kOffQ + 2 * kQBytes;
   static constexpr int kRedBytes = 2 * NHALF * 4 * H * 4;  // [group][half][quadrant][H]
   static constexpr int kOffRedMax = kOffP + 2 * kQBytes;
@@ -60,7 +67,7 @@ struct SysCfg {
   static constexpr int kOffL = kOffRedSum + kRedBytes;   // [group][NQ]
   static constexpr int kOffX = kOffL + 2 * NQ * 4;       // handover m, l: [2][NQ]
   static constexpr int kOffBar = kOffX + 2 * NQ * 4;
-  static constexpr int kNumBars = 2 * STAGES + 18;
+  static constexpr int kNumBars = 2 * KS + 2 * VS + 18;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64;
   static constexpr int kTmemCols = (5 * NQ <= 128) ? 128 : (5 * NQ <= 256) ? 256 : 512;
@@ -104,12 +111,14 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
                           const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
   using L = SysCfg<NQ>;
   constexpr int H = L::H;
-  constexpr int STAGES = L::STAGES;
+  constexpr int KS = L::KS, VS = L::VS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
-  uint64_t* full_bar = bars;
-  uint64_t* empty_bar = bars + STAGES;
-  uint64_t* s_full = bars + 2 * STAGES;
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = bars + KS;
+  uint64_t* v_full = bars + 2 * KS;
+  uint64_t* v_empty = bars + 2 * KS + VS;
+  uint64_t* s_full = bars + 2 * KS + 2 * VS;
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_full + 4;
   uint64_t* p_empty = s_full + 6;
@@ -131,13 +140,19 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   const long long t_begin = rb_cta_begin(&P, blockIdx.x);
   const long long t_end = rb_cta_begin(&P, blockIdx.x + 1);
 
+  unsigned long long* dts = args.debug_ts ? args.debug_ts + blockIdx.x * 8 : nullptr;
+  if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
@@ -158,13 +173,18 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = misc[0];
+  if (dts && threadIdx.x == 0) dts[1] = global_timer_ns();
+  // the next kernel (context + fusion) may be scheduled as SMs free up; it
+  // waits for this grid's memory before it reads o_sys / lse_sys.
+  pdl_launch_dependents();
 
-  const uint32_t smem_kv = smem_u32(smem + L::kOffKV);
+  const uint32_t smem_k = smem_u32(smem + L::kOffK);
+  const uint32_t smem_v = smem_u32(smem + L::kOffV);
   const uint32_t smem_q = smem_u32(smem + L::kOffQ);
   const uint32_t smem_p = smem_u32(smem + L::kOffP);
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------- K producer (+ Q rows)
     const uint64_t pol = l2_policy_evict_first();
     int j = 0, uq = 0;
     for (long long i = t_begin; i < t_end; ++i, ++j) {
@@ -172,20 +192,19 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       const int kt = static_cast<int>(i % P.tpu);
       const int h = u / P.n_qt;
       const int qt = u % P.n_qt;
-      const int st = j % STAGES;
-      mbar_wait(&empty_bar[st], ((j / STAGES) & 1) ^ 1);
+      const int st = j % KS;
+      mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
       if (lane == 0) {
-        uint8_t* kdst = smem + L::kOffKV + st * kStageBytes;
-        mbar_arrive_expect_tx(&full_bar[st], kStageBytes);
-        tma_load_3d(kdst, &tmap_k, &full_bar[st], 0, kt * RB_KEY_TILE, h, pol);
-        tma_load_3d(kdst + kKvTileBytes / 2, &tmap_k, &full_bar[st], 64, kt * RB_KEY_TILE, h, pol);
-        tma_load_3d(kdst + kKvTileBytes, &tmap_v, &full_bar[st], 0, kt * RB_KEY_TILE, h, pol);
-        tma_load_3d(kdst + kKvTileBytes + kKvTileBytes / 2, &tmap_v, &full_bar[st], 64,
-                    kt * RB_KEY_TILE, h, pol);
+        uint8_t* dst = smem + L::kOffK + st * L::kTileBytes;
+        mbar_arrive_expect_tx(&k_full[st], L::kTileBytes);
+        tma_load_3d(dst, &tmap_k, &k_full[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(dst + L::kTileBytes / 2, &tmap_k, &k_full[st], 64, kt * RB_KEY_TILE, h, pol);
       }
       __syncwarp();
       if (i == t_begin || kt == 0) {
-        // query rows of unit u (after this tile's K/V are already in flight)
+        // query rows of unit u (after this tile's K is already in flight);
+        // q may be produced by the previous kernel in the stream.
+        if (i == t_begin) pdl_wait_primary();
         const int qb = uq & 1;
         mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
         uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
@@ -210,31 +229,28 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         ++uq;
       }
     }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ V producer
+    const uint64_t pol = l2_policy_evict_first();
+    if (lane == 0) {
+      int j = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int u = static_cast<int>(i / P.tpu);
+        const int kt = static_cast<int>(i % P.tpu);
+        const int h = u / P.n_qt;
+        const int st = j % VS;
+        mbar_wait(&v_empty[st], ((j / VS) & 1) ^ 1);
+        uint8_t* dst = smem + L::kOffV + st * L::kTileBytes;
+        mbar_arrive_expect_tx(&v_full[st], L::kTileBytes);
+        tma_load_3d(dst, &tmap_v, &v_full[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(dst + L::kTileBytes / 2, &tmap_v, &v_full[st], 64, kt * RB_KEY_TILE, h, pol);
+      }
+    }
+    __syncwarp();
   } else if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer
+    // ----------------------------------------------- S^T = K . Q^T issuer
     if (lane == 0) {
       constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
-      auto issue_pv = [&](int jj) {
-        const int st = jj % STAGES, pb = jj & 1;
-        mbar_wait(&p_full[pb], (jj >> 1) & 1);
-        mbar_wait(&o_empty[pb], ((jj >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t v_base = smem_kv + st * kStageBytes + kKvTileBytes;
-        const uint32_t p_base = smem_p + pb * L::kQBytes;
-        const uint32_t d_tmem = tmem_base + 2 * NQ + pb * NQ;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          // A = V^T (M = d, MN-major): 16 keys = two 8-row swizzle atoms.
-          const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, kKvTileBytes / 2, 1024);
-          const uint64_t b =
-              make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
-          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : 0u);
-        }
-        umma_commit(&o_full[pb]);
-        umma_commit(&empty_bar[st]);
-        umma_commit(&p_empty[pb]);
-      };
       int j = 0, uq = 0;
       for (long long i = t_begin; i < t_end; ++i, ++j) {
         const int kt = static_cast<int>(i % P.tpu);
@@ -242,34 +258,61 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
         const int qb = uq & 1;
         if (new_unit) mbar_wait(&q_full[qb], (uq >> 1) & 1);
-        const int st = j % STAGES, sb = j & 1;
-        mbar_wait(&full_bar[st], (j / STAGES) & 1);
+        const int st = j % KS, sb = j & 1;
+        mbar_wait(&k_full[st], (j / KS) & 1);
         mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k_base = smem_kv + st * kStageBytes;
+        const uint32_t k_base = smem_k + st * L::kTileBytes;
         const uint32_t q_base = smem_q + qb * L::kQBytes;
         const uint32_t d_tmem = tmem_base + sb * NQ;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t koff = (kk & 3) * 32;
           const uint64_t a =
-              make_smem_desc_sw128(k_base + (kk >> 2) * (kKvTileBytes / 2) + koff, 16, 1024);
+              make_smem_desc_sw128(k_base + (kk >> 2) * (L::kTileBytes / 2) + koff, 16, 1024);
           const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + koff, 16, 1024);
           umma_f16_ss(d_tmem, a, b, idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[st]);
         if (last_of_unit) {
           umma_commit(&q_empty[qb]);
           ++uq;
         }
-        if (j > 0) issue_pv(j - 1);
       }
-      if (j > 0) issue_pv(j - 1);
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // ------------------------------------------------- O^T = V^T . P^T issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+      int j = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int st = j % VS, pb = j & 1;
+        mbar_wait(&v_full[st], (j / VS) & 1);
+        mbar_wait(&p_full[pb], (j >> 1) & 1);
+        mbar_wait(&o_empty[pb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_v + st * L::kTileBytes;
+        const uint32_t p_base = smem_p + pb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + 2 * NQ + pb * NQ;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          // A = V^T (M = d, MN-major): 16 keys = two 8-row swizzle atoms.
+          const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, L::kTileBytes / 2, 1024);
+          const uint64_t b =
+              make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[pb]);
+        umma_commit(&v_empty[st]);
+        umma_commit(&p_empty[pb]);
+      }
     }
     __syncwarp();
   } else {
     // ------------------------------------- softmax / O accumulation groups
-    const int cw = warp - 2;
+    const int cw = warp - L::kRoleWarps;
     const int grp = cw / L::WPG;                 // which tile parity this group owns
     const int hf = (cw / 4) % L::NHALF;          // column slice
     const int qd = warp & 3;                     // TMEM lane quadrant (hardware: warp % 4)
@@ -292,6 +335,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
 
     float m_run[H], acc[H];
     int xh = 0;  // handovers so far
+    pdl_wait_primary();  // o_sys / partials may still be read by the previous kernel
     long long i = t_begin;
     while (i < t_end) {
       const int u = static_cast<int>(i / P.tpu);
@@ -310,6 +354,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const uint32_t ph = (j >> 1) & 1;
         // ---- S tile -> scores (log2 domain)
         mbar_wait(&s_full[gb], ph);
+        if (dts && j == 0 && threadIdx.x == L::kRoleWarps * 32) dts[2] = global_timer_ns();
         tc_fence_after();
         float x[H];
         tmem_ld_32x32b<H>(lane_addr + gb * NQ + col0, x);
@@ -437,7 +482,22 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const int owner0 = rb_tile_owner(&P, u_first);
         const int nparts = rb_unit_parts(&P, u);
         const int dcol = key_lane;  // O lane = head-dim index
-        if (nparts == 1) {
+        if (args.defer_merge) {
+          // relay path: hand the (unnormalised) part to the fusion epilogue
+          const int slot = blockIdx.x - owner0;
+          const long long pbase = static_cast<long long>(u) * P.max_parts + slot;
+          float* pacc = args.part_acc + pbase * NQ * RB_HEAD_DIM;
+          float* pml = args.part_ml + pbase * 2 * NQ;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int col = col0 + c;
+            pacc[col * RB_HEAD_DIM + dcol] = acc[c];
+            if (qd == 0 && lane == 0) {
+              pml[col] = m_run[c];
+              pml[NQ + col] = lrow[c];
+            }
+          }
+        } else if (nparts == 1) {
 #pragma unroll
           for (int c = 0; c < H; ++c) {
             const int f = qt * NQ + col0 + c;
@@ -473,28 +533,54 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           }
           named_bar_sync(bar_grp, L::WPG * 32);
           if (misc[2 + grp]) {
+            // last CTA of unit u: merge the slots in slot order (deterministic
+            // whoever merges); per slot all H columns' loads are in flight.
             __threadfence();
             const float* uacc =
                 args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
             const float* uml = args.part_ml + static_cast<long long>(u) * P.max_parts * 2 * NQ;
-#pragma unroll 1
+            // running merge state reuses m_run / lrow / acc (own slot is re-read
+            // from global like every other slot)
+            float* M = m_run;
+            float* Ls = lrow;
+            float* Os = acc;
+#pragma unroll
             for (int c = 0; c < H; ++c) {
-              const int col = col0 + c;
-              const int f = qt * NQ + col;
-              if (f >= P.rows_per_head) continue;
-              float M = -INFINITY;
-              for (int k = 0; k < nparts; ++k) M = fmaxf(M, __ldcg(uml + k * 2 * NQ + col));
-              float Ls = 0.f, Os = 0.f;
-              for (int k = 0; k < nparts; ++k) {
-                const float w = fast_exp2(__ldcg(uml + k * 2 * NQ + col) - M);
-                Ls = fmaf(__ldcg(uml + k * 2 * NQ + NQ + col), w, Ls);
-                Os = fmaf(__ldcg(uacc + (static_cast<long long>(k) * NQ + col) * RB_HEAD_DIM + dcol),
-                          w, Os);
+              M[c] = -INFINITY;
+              Ls[c] = 0.f;
+              Os[c] = 0.f;
+            }
+            for (int k = 0; k < nparts; ++k) {
+#pragma unroll
+              for (int c0 = 0; c0 < H; c0 += 8) {
+                float mk[8], lk[8], ak[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  mk[c] = __ldcg(uml + k * 2 * NQ + col0 + c0 + c);
+                  lk[c] = __ldcg(uml + k * 2 * NQ + NQ + col0 + c0 + c);
+                  ak[c] = __ldcg(uacc + (static_cast<long long>(k) * NQ + col0 + c0 + c) *
+                                            RB_HEAD_DIM + dcol);
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const float mn = fmaxf(M[c0 + c], mk[c]);
+                  const float so = (M[c0 + c] == -INFINITY) ? 0.f : fast_exp2(M[c0 + c] - mn);
+                  const float sk = fast_exp2(mk[c] - mn);
+                  Ls[c0 + c] = Ls[c0 + c] * so + lk[c] * sk;
+                  Os[c0 + c] = Os[c0 + c] * so + ak[c] * sk;
+                  M[c0 + c] = mn;
+                }
               }
-              const int row = f / P.g, hh = h * P.g + f % P.g;
-              const long long o_idx = static_cast<long long>(row) * P.hq + hh;
-              args.o_sys[o_idx * RB_HEAD_DIM + dcol] = Os / Ls;
-              if (qd == 0 && lane == 0) args.lse_sys[o_idx] = (M + __log2f(Ls)) * kLn2;
+            }
+#pragma unroll
+            for (int c = 0; c < H; ++c) {
+              const int f = qt * NQ + col0 + c;
+              if (f < P.rows_per_head) {
+                const int row = f / P.g, hh = h * P.g + f % P.g;
+                const long long o_idx = static_cast<long long>(row) * P.hq + hh;
+                args.o_sys[o_idx * RB_HEAD_DIM + dcol] = Os[c] / Ls[c];
+                if (qd == 0 && lane == 0) args.lse_sys[o_idx] = (M[c] + __log2f(Ls[c])) * kLn2;
+              }
             }
           }
         }
@@ -502,14 +588,19 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       if (two) ++xh;
       i = unit_end;
     }
+    if (dts && threadIdx.x == L::kRoleWarps * 32) dts[3] = global_timer_ns();
+    if (dts && threadIdx.x == (L::kRoleWarps + L::WPG) * 32) dts[4] = global_timer_ns();
   }
 
+  if (dts && threadIdx.x == 0) dts[5] = global_timer_ns();
+  if (dts && threadIdx.x == 64) dts[6] = global_timer_ns();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, L::kTmemCols);
   }
+  if (dts && threadIdx.x == 0) dts[7] = global_timer_ns();
 }
 
 // ------------------------------------------------------------------- host
@@ -519,10 +610,12 @@ static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, cons
                               cudaStream_t stream) {
   using L = SysCfg<NQ>;
   static_assert(L::kBytes <= 232448, "system kernel shared memory over the 227 KB limit");
+  static_assert(L::kThreads <= 1024, "too many warps");
   auto kern = sys_attn_sm100_kernel<NQ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
   if (e != cudaSuccess) return e;
-  kern<<<a.plan.grid, L::kThreads, L::kBytes, stream>>>(tk, tv, a);
+  e = launch_pdl(kern, dim3(a.plan.grid), dim3(L::kThreads), L::kBytes, stream, tk, tv, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -35,11 +35,12 @@ def sm_count(device=None) -> int:
     return _lib.sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
 
 
-def workspace(nbytes: int, device, stream_key: int) -> torch.Tensor:
-    """Zero-initialised scratch for the system kernel's stream-K partials and
-    semaphores, cached per (device, stream) -- the kernel leaves the
-    semaphores zeroed, so the buffer is reusable without clearing."""
-    key = (str(device), stream_key)
+def workspace(nbytes: int, device, stream_key: int, kind: str = "sys") -> torch.Tensor:
+    """Zero-initialised scratch, cached per (kind, device, stream).  kind
+    "sys": rb_system_attention's stream-K partials + semaphores (the kernel
+    leaves the semaphores zeroed, so the buffer is reusable without
+    clearing); kind "relay": rb_relay_attention's unmerged partial slots."""
+    key = (kind, str(device), stream_key)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
@@ -138,6 +139,48 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
         _ptr(prefix_k), _ptr(prefix_v), s_prefix, p_tok, p_head, _ptr(o_sys), _ptr(lse_sys),
         float(scale), out.data_ptr(), 1 if out_fp32 else 0, _ptr(lse_out), _stream(dev)),
         "rb_context_attention")
+    return out, lse_out
+
+
+def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
+                    sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
+                    strides=None, scale=None, grid=None, out=None, lse_out=None,
+                    out_fp32=False, ws=None, phases=3):
+    """The fused relay step (rb_relay_attention): system kernel (stream-K
+    partials, no merge) + context kernel whose epilogue merges the system
+    partials with the context state.  Returns (out, lse)."""
+    _check_bf16("q", q)
+    n_rows, hq, d = q.shape
+    if d != HEAD_DIM:
+        raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
+    if sys_layout == "hsd":
+        _, s, _ = sys_k.shape
+        s_tok, s_head = sys_k.stride(1), sys_k.stride(0)
+    else:
+        s, _, _ = sys_k.shape
+        s_tok, s_head = sys_k.stride(0), sys_k.stride(1)
+    dev = q.device
+    b = ctx_lens.numel()
+    if out is None:
+        out = torch.empty((n_rows, hq, HEAD_DIM),
+                          dtype=torch.float32 if out_fp32 else torch.bfloat16, device=dev)
+    if lse_out is None:
+        lse_out = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
+    grid = sm_count(dev) if grid is None else grid
+    stream = _stream(dev)
+    if ws is None:
+        need = _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid)
+        ws = workspace(need, dev, stream, kind="relay")
+    sb, stok, sh = strides
+    bt_stride = block_table.stride(0) if block_table is not None else 0
+    scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
+    _lib.check(_lib.load().rb_relay_attention(
+        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq, hkv,
+        HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
+        v.data_ptr(), _ptr(block_table), bt_stride, block_size, _ptr(req_offset), sb, stok, sh,
+        ctx_lens.data_ptr(), float(scale), grid, out.data_ptr(),
+        1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), ws.data_ptr(), ws.numel(),
+        phases, stream), "rb_relay_attention")
     return out, lse_out
 
 

@@ -192,8 +192,12 @@ class PagedKvCache:
 
     def append_slots(self, layer, k, v, slot_mapping):
         """Device-side append with a precomputed int32 slot mapping."""
-        kernels.kv_append(k.to(torch.bfloat16).contiguous(), v.to(torch.bfloat16).contiguous(),
-                          slot_mapping, self.k_pool[layer], self.v_pool[layer], self.block_size)
+        if k.dtype != torch.bfloat16 or not k.is_contiguous():
+            k = k.to(torch.bfloat16).contiguous()
+        if v.dtype != torch.bfloat16 or not v.is_contiguous():
+            v = v.to(torch.bfloat16).contiguous()
+        kernels.kv_append(k, v, slot_mapping, self.k_pool[layer], self.v_pool[layer],
+                          self.block_size)
 
     def block_table(self, request_ids, width=None):
         """int32 (b, width) block table on the device (unused entries 0)."""
