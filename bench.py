@@ -10,7 +10,8 @@ configs[1]: Llama-30B attention shape (52 heads, d=128), batch 32, context
 configs[1]'s sweep).  One step = one relay decode step of one layer: the
 tcgen05 system kernel over the shared prefix + the paged context kernel with
 the fused relay epilogue.  Inputs are synthetic (seeded normal bf16), resident
-in HBM; L2 (126 MB) is flushed between timed steps by writing a 2x-L2 buffer.
+in HBM; L2 (126 MB) is flushed between timed steps (write a 2x-L2 buffer, then
+read another so the write-back happens outside the timed region).
 
 N > 1 (torchrun): KV heads are sharded across ranks (52 -> 7,7,7,7,6,6,6,6 at
 N=8); each rank runs the same step on its heads, no collective in the timed
@@ -314,11 +315,18 @@ def run_b200(args):
     world, rank, local = dist_env()
     if world != args.gpus and world > 1:
         args.gpus = world
+    # BENCH_SAME_GPU=1 (testing only): every rank on cuda:0 with gloo, to
+    # exercise the sharded path on a single-GPU box.
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"
+    local = 0 if same_gpu else local
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     barrier = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
         barrier = dist.barrier
     from paper_2402_14808_b200 import _lib, kernels, sharding
     from paper_2402_14808_b200.costmodel import DecodeShape
@@ -404,7 +412,7 @@ def run_b200(args):
     def maxr(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if same_gpu else device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -420,7 +428,7 @@ def run_b200(args):
     if world > 1:
         q, relay, _, _, _ = build(torch, 1024, heads, device)
         out, _ = relay(q)
-        full = sharding.gather_heads(out, H, H)
+        full = sharding.gather_heads(out.cpu() if same_gpu else out, H, H)
         gathered_ok = bool(full.shape == (B, H, D) and torch.isfinite(full.float()).all())
         del q, relay
 

@@ -447,29 +447,39 @@ class RelayDecodeStep:
         """CUDA-graph version of `step_host` for a serving loop.
 
         qkv_host: pinned bf16 (3, b, h, 128) holding this step's q, k_new,
-        v_new (one H2D copy); out_host: pinned bf16 (b, hq, 128).  Returns a
-        callable that replays H2D -> append -> relay -> D2H on the current
-        stream; refill `qkv_host` between calls.
+        v_new; out_host: pinned bf16 (b, hq, 128).  Returns a callable that
+        replays the step on the current stream.  Inside the graph the q H2D
+        feeds the system kernel directly while the k/v H2D and the paged
+        append run on a forked stream; the context kernel joins both.  Refill
+        `qkv_host` between calls.
         """
         dev = self.out.device
         qkv_dev = torch.empty(qkv_host.shape, dtype=torch.bfloat16, device=dev)
+        main = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
 
         def body():
-            qkv_dev.copy_(qkv_host, non_blocking=True)
-            self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
-            out, _ = self(qkv_dev[0])
+            cur = torch.cuda.current_stream(dev)
+            side.wait_stream(cur)
+            qkv_dev[0].copy_(qkv_host[0], non_blocking=True)
+            self.system(qkv_dev[0])
+            with torch.cuda.stream(side):
+                qkv_dev[1:].copy_(qkv_host[1:], non_blocking=True)
+                self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
+            cur.wait_stream(side)
+            out, _ = self.context(qkv_dev[0])
             out_host.copy_(out, non_blocking=True)
 
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
+        warm = torch.cuda.Stream(device=dev)
+        warm.wait_stream(main)
+        with torch.cuda.stream(warm):
             body()
-        torch.cuda.current_stream(dev).wait_stream(side)
+        main.wait_stream(warm)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             body()
         self._host_graph = graph  # keep alive with its buffers
-        self._host_graph_bufs = (qkv_dev,)
+        self._host_graph_bufs = (qkv_dev, side)
         return graph.replay
 
 

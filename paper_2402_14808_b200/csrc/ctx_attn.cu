@@ -123,6 +123,7 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
 template <int R>
 struct CtxItem {
   int r, h, z, row0, m_r, nrows, c_r, max_lim, n_chunks;
+  long long roff;  // ragged mode: first token of request r
 };
 
 template <int R>
@@ -135,6 +136,7 @@ __device__ __forceinline__ CtxItem<R> ctx_item(const CtxArgs& a, int item, int n
   it.m_r = __ldg(a.q_start + it.r + 1) - it.row0;
   it.nrows = it.m_r * a.g;
   it.c_r = __ldg(a.ctx_lens + it.r);
+  it.roff = a.ctx.req_offset != nullptr ? __ldg(a.ctx.req_offset + it.r) : 0;
   const int rbase = it.z * R;
   if (rbase >= it.nrows) {
     it.max_lim = 0;
@@ -147,19 +149,364 @@ __device__ __forceinline__ CtxItem<R> ctx_item(const CtxArgs& a, int item, int n
   return it;
 }
 
-// Persistent producer/consumer kernel.  CTA b processes items b, b + grid,
-// ...; their chunks form one sequence.  Warp 0 is the producer: its lanes
-// resolve block-table entries and issue the bulk copies of up to 32 chunks
+// Everything a warp needs to start an item, loaded lane-parallel one item
+// ahead: geometry, this lane's 8 query dims per row, and (lanes j, j+32) the
+// block-table entries of context chunks j and j + 32.
+template <int R>
+struct ItemPrefetch {
+  CtxItem<R> it;
+  float qf[R][8];
+  int bt0, bt1;
+};
+
+template <int R>
+__device__ __forceinline__ void prefetch_item(const CtxArgs& a, int item, int n_z, int n_pre,
+                                              int lane, ItemPrefetch<R>& pf) {
+  pf.it = ctx_item<R>(a, item, n_z, n_pre);
+  const CtxItem<R>& it = pf.it;
+  const int l16 = lane & 15;
+  const int rbase = it.z * R;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int li = rbase + i;
+    if (li < it.nrows) {
+      const int t = li / a.g, jj = li % a.g;
+      const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
+                                static_cast<long long>(it.h * a.g + jj) * a.q_head_stride + l16 * 8;
+      const uint4 u = *reinterpret_cast<const uint4*>(qp);
+      pf.qf[i][0] = bf16_lo(u.x); pf.qf[i][1] = bf16_hi(u.x);
+      pf.qf[i][2] = bf16_lo(u.y); pf.qf[i][3] = bf16_hi(u.y);
+      pf.qf[i][4] = bf16_lo(u.z); pf.qf[i][5] = bf16_hi(u.z);
+      pf.qf[i][6] = bf16_lo(u.w); pf.qf[i][7] = bf16_hi(u.w);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pf.qf[i][e] = 0.f;
+    }
+  }
+  pf.bt0 = pf.bt1 = 0;
+  if (a.ctx.block_table != nullptr && it.n_chunks > 0) {
+    const int nb = (it.max_lim + a.ctx.block_size - 1) / a.ctx.block_size;
+    const int* row = a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride;
+    if (lane < nb) pf.bt0 = __ldg(row + lane);
+    if (lane + 32 < nb) pf.bt1 = __ldg(row + lane + 32);
+  }
+}
+
+// Issue the bulk copies of chunk k of `it` into `slot` (warp-uniform call).
+// Paged K/V of one (block, head) run is contiguous: one 4 KB copy for K and
+// one for V; other layouts use one 256-byte copy per token, spread over lanes.
+template <int R>
+__device__ __forceinline__ void issue_chunk(const CtxArgs& a, const ItemPrefetch<R>& pf, int k,
+                                            int n_pre, uint8_t* slot, uint64_t* bar, int lane) {
+  const CtxItem<R>& it = pf.it;
+  const __nv_bfloat16 *kb, *vb;
+  int n;
+  long long tok_stride;
+  bool contiguous;
+  int blk = 0;
+  if (k >= n_pre && a.ctx.block_table != nullptr) {
+    // block id of this chunk's first token: from the lane-parallel prefetch
+    const int t0 = (k - n_pre) * kChunk;
+    const int bi = t0 / a.ctx.block_size;
+    const int v0 = __shfl_sync(0xffffffffu, pf.bt0, bi & 31);
+    const int v1 = __shfl_sync(0xffffffffu, pf.bt1, bi & 31);
+    blk = bi < 32 ? v0 : bi < 64 ? v1
+                   : __ldg(a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride + bi);
+  }
+  if (k < n_pre) {
+    const int t0 = k * kChunk;
+    n = min(kChunk, a.s_prefix - t0);
+    const long long off = static_cast<long long>(it.h) * a.p_stride_head + t0 * a.p_stride_tok;
+    kb = a.pk + off;
+    vb = a.pv + off;
+    tok_stride = a.p_stride_tok;
+    contiguous = (a.p_stride_tok == RB_HEAD_DIM);
+  } else {
+    const int t0 = (k - n_pre) * kChunk;
+    n = min(kChunk, it.max_lim - t0);
+    long long off;
+    if (a.ctx.block_table != nullptr)
+      off = static_cast<long long>(blk) * a.ctx.stride_block +
+            static_cast<long long>(t0 % a.ctx.block_size) * a.ctx.stride_tok;
+    else
+      off = (it.roff + t0) * a.ctx.stride_tok;
+    off += it.h * a.ctx.stride_head;
+    kb = a.ctx.k + off;
+    vb = a.ctx.v + off;
+    tok_stride = a.ctx.stride_tok;
+    contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
+                 (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
+  }
+  if (lane == 0) mbar_arrive_expect_tx(bar, 2 * n * kRowBytes);
+  __syncwarp();
+  if (contiguous) {
+    if (lane == 0) {
+      bulk_copy_g2s(slot, kb, n * kRowBytes, bar);
+      bulk_copy_g2s(slot + kChunk * kRowBytes, vb, n * kRowBytes, bar);
+    }
+  } else if (lane < 2 * n) {
+    const int t = lane % n, which = lane / n;
+    const __nv_bfloat16* src;
+    if (k < n_pre || a.ctx.block_table == nullptr) {
+      src = (which ? vb : kb) + t * tok_stride;
+    } else {
+      const int tt = (k - n_pre) * kChunk + t;
+      const int bi = tt / a.ctx.block_size;
+      const int b2 = __ldg(a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride + bi);
+      src = (which ? a.ctx.v : a.ctx.k) + static_cast<long long>(b2) * a.ctx.stride_block +
+            static_cast<long long>(tt % a.ctx.block_size) * a.ctx.stride_tok +
+            it.h * a.ctx.stride_head;
+    }
+    bulk_copy_g2s(slot + which * kChunk * kRowBytes + t * kRowBytes, src, kRowBytes, bar);
+  }
+}
+
+// Warp-per-item persistent kernel.  Global warp gw processes items gw,
+// gw + W, ... (W = all warps of the grid).  Each warp streams its items'
+// chunks through a private ring of kWarpSlots bulk-copy slots; chunks of the
+// next item are issued while the current one finishes, and the next item's
+// metadata / queries / block-table entries are prefetched one item ahead, so
+// no global round trip sits on the per-item critical path.  Half-warp hw
+// handles keys 2p + hw of each chunk; the two half states merge with shuffles.
+constexpr int kWarpSlots = 2;
+constexpr int kCtxWarps = 4;
+
+template <int R>
+__global__ void __launch_bounds__(kCtxWarps * 32, (R <= 2) ? 3 : 1)
+    ctx_attn_kernel(const CtxArgs a, int n_items, int n_z) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int hw = lane >> 4, l16 = lane & 15;
+  const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
+  const int W = gridDim.x * kCtxWarps;
+  const int gw = blockIdx.x * kCtxWarps + warp;
+  uint8_t* slots = smem + warp * kWarpSlots * kSlotBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kCtxWarps * kWarpSlots * kSlotBytes) +
+                  warp * kWarpSlots;
+  if (lane == 0) {
+    for (int i = 0; i < kWarpSlots; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  pdl_launch_dependents();
+  if (gw >= n_items) return;
+
+  // issue cursor (item + chunk) runs up to kWarpSlots chunks ahead of compute
+  ItemPrefetch<R> iss;
+  prefetch_item<R>(a, gw, n_z, n_pre, lane, iss);
+  int iss_item = gw, iss_k = 0;
+  long long issued = 0;
+  ItemPrefetch<R> nxt;  // next item's prefetch for the issue cursor
+  bool have_nxt = false;
+  auto advance_issue = [&]() {
+    // move the issue cursor past exhausted items (warp-uniform)
+    while (iss_item < n_items && iss_k >= iss.it.n_chunks) {
+      iss_item += W;
+      iss_k = 0;
+      if (iss_item >= n_items) break;
+      if (have_nxt) {
+        iss = nxt;
+        have_nxt = false;
+      } else {
+        prefetch_item<R>(a, iss_item, n_z, n_pre, lane, iss);
+      }
+    }
+  };
+  auto issue_one = [&]() {
+    advance_issue();
+    if (iss_item >= n_items) return;
+    const int sl = static_cast<int>(issued % kWarpSlots);
+    issue_chunk<R>(a, iss, iss_k, n_pre, slots + sl * kSlotBytes, &bar[sl], lane);
+    ++issued;
+    ++iss_k;
+    // start fetching the following item's metadata as soon as this one is issued
+    if (iss_k == iss.it.n_chunks && !have_nxt && iss_item + W < n_items) {
+      prefetch_item<R>(a, iss_item + W, n_z, n_pre, lane, nxt);
+      have_nxt = true;
+    }
+  };
+
+  ItemPrefetch<R> cur = iss;  // compute cursor starts on the same item
+  for (int s = 0; s < kWarpSlots; ++s) issue_one();
+
+  long long consumed = 0;
+  bool waited = false;
+  for (int item = gw; item < n_items; item += W) {
+    if (item != gw) {
+      // the issue cursor has already prefetched this item (it runs ahead)
+      cur = (iss_item == item) ? iss : cur;
+      if (cur.it.r != item / (n_z * a.hkv) || cur.it.h != (item / n_z) % a.hkv ||
+          cur.it.z != item % n_z)
+        prefetch_item<R>(a, item, n_z, n_pre, lane, cur);
+    }
+    const CtxItem<R>& it = cur.it;
+    if (it.n_chunks == 0) continue;
+    const int rbase = it.z * R;
+    int lim_ctx[R], lim_pre[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int li = rbase + i;
+      if (li < it.nrows) {
+        const int t = li / a.g;
+        lim_ctx[i] = a.causal ? it.c_r - it.m_r + t + 1 : it.c_r;
+        lim_pre[i] = a.s_prefix;
+      } else {
+        lim_ctx[i] = 0;
+        lim_pre[i] = 0;
+      }
+    }
+    RowState<R> st;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      st.m[i] = -INFINITY;
+      st.l[i] = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
+    }
+    for (int k = 0; k < it.n_chunks; ++k, ++consumed) {
+      const int sl = static_cast<int>(consumed % kWarpSlots);
+      const uint8_t* src = slots + sl * kSlotBytes;
+      mbar_wait(&bar[sl], static_cast<uint32_t>((consumed / kWarpSlots) & 1));
+      uint4 kr[8], vr[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        kr[p] = *reinterpret_cast<const uint4*>(src + (2 * p + hw) * kRowBytes + l16 * 16);
+        vr[p] = *reinterpret_cast<const uint4*>(src + kChunk * kRowBytes + (2 * p + hw) * kRowBytes +
+                                                l16 * 16);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      issue_one();  // refill the slot just read
+      if (k < n_pre)
+        chunk_update<R>(st, cur.qf, kr, vr, k * kChunk, hw, lim_pre, a.scale_log2, a.s_prefix);
+      else
+        chunk_update<R>(st, cur.qf, kr, vr, (k - n_pre) * kChunk, hw, lim_ctx, a.scale_log2,
+                        it.max_lim);
+    }
+
+    // ---- merge the two half-warp states (keys 2p and 2p+1) with shuffles
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float mo = __shfl_xor_sync(0xffffffffu, st.m[i], 16);
+      const float lo = __shfl_xor_sync(0xffffffffu, st.l[i], 16);
+      const float M = fmaxf(st.m[i], mo);
+      const float ws = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - M);
+      const float wo = (mo == -INFINITY) ? 0.f : fast_exp2(mo - M);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float ao = __shfl_xor_sync(0xffffffffu, st.acc[i][e], 16);
+        st.acc[i][e] = st.acc[i][e] * ws + ao * wo;
+      }
+      st.l[i] = st.l[i] * ws + lo * wo;
+      st.m[i] = M;
+    }
+    if (!waited) {  // before the first global write / system-output read
+      pdl_wait_primary();
+      waited = true;
+    }
+    // ---- epilogue: half-warp 0 owns 8 head dims per lane
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int li = rbase + i;
+      if (li >= it.nrows) continue;
+      const int t = li / a.g, jj = li % a.g;
+      const long long oidx = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
+      const float M = st.m[i], Ls = st.l[i];
+      float o[8], lse2;
+      if (a.sys_part_acc != nullptr) {
+        // relay fusion: merge every system stream-K part of this (row, head)
+        const rb_sys_plan& SP = a.sys_plan;
+        const long long f = static_cast<long long>(it.row0 + t) * SP.g + jj;
+        const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
+        const int u = it.h * SP.n_qt + qt;
+        const int np = rb_unit_parts(&SP, u);
+        const long long base = static_cast<long long>(u) * SP.max_parts;
+        float mt = M, lt = Ls;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = st.acc[i][e];
+        for (int k0 = 0; k0 < np; k0 += 2) {
+          float mk[2], lk[2];
+          float4 ak[2][2];
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int k = min(k0 + kk, np - 1);
+            const float* ml = a.sys_part_ml + (base + k) * 2 * SP.nq;
+            mk[kk] = __ldcg(ml + col);
+            lk[kk] = __ldcg(ml + SP.nq + col);
+            const float4* ap = reinterpret_cast<const float4*>(
+                a.sys_part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + l16 * 8);
+            ak[kk][0] = __ldcg(ap);
+            ak[kk][1] = __ldcg(ap + 1);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            if (k0 + kk >= np) break;
+            const float mn = fmaxf(mt, mk[kk]);
+            const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+            const float sk = fast_exp2(mk[kk] - mn);
+            lt = lt * so + lk[kk] * sk;
+            const float av[8] = {ak[kk][0].x, ak[kk][0].y, ak[kk][0].z, ak[kk][0].w,
+                                 ak[kk][1].x, ak[kk][1].y, ak[kk][1].z, ak[kk][1].w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = o[e] * so + av[e] * sk;
+            mt = mn;
+          }
+        }
+        const float inv = 1.f / lt;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] *= inv;
+        lse2 = mt + __log2f(lt);
+      } else {
+        const float inv = (Ls > 0.f) ? 1.f / Ls : 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = st.acc[i][e] * inv;
+        lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+      }
+      if (a.o_sys != nullptr) {
+        const float ls2 = __ldcg(a.lse_sys + oidx) * kLog2e;
+        const float4* op = reinterpret_cast<const float4*>(a.o_sys + oidx * 128 + l16 * 8);
+        const float4 s0 = __ldcg(op), s1 = __ldcg(op + 1);
+        const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const float mx = fmaxf(ls2, lse2);
+        const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
+        const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
+        const float inv = 1.f / (wc + ws);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = (wc * o[e] + ws * sv[e]) * inv;
+        lse2 = mx + __log2f(wc + ws);
+      }
+      if (hw == 0) {
+        if (a.out_fp32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx * 128 + l16 * 8);
+          dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+          dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        } else {
+          uint4 pk;
+          pk.x = pack_bf16x2(o[0], o[1]);
+          pk.y = pack_bf16x2(o[2], o[3]);
+          pk.z = pack_bf16x2(o[4], o[5]);
+          pk.w = pack_bf16x2(o[6], o[7]);
+          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + oidx * 128 + l16 * 8) = pk;
+        }
+        if (a.lse_out != nullptr && l16 == 0) a.lse_out[oidx] = lse2 * kLn2;
+      }
+    }
+  }
+}
+
+// Long items (the naive baseline's shared prefix: hundreds of chunks per
+// request): CTA-per-item producer/consumer kernel.  CTA b processes items b,
+// b + grid, ...; their chunks form one sequence.  Warp 0 is the producer: its lanes
+// resolve block-table entries and issue the bulk copies of up to kRing chunks
 // at once into a CTA-wide ring of kRing slots (waiting on each slot's empty
 // barrier), so the copies run far ahead of the math.  Warps 1..4 consume
 // chunk k of an item in warp 1 + (k % 4), then merge their partial states at
 // the end of the item and run the fusion epilogue (thread = head dim).
 constexpr int kRing = 12;                      // 12 x 8 KB = 96 KB of K/V in flight per CTA
 constexpr int kCtxThreadsPC = 160;             // producer + 4 consumers
-
 template <int R>
 __global__ void __launch_bounds__(kCtxThreadsPC)
-    ctx_attn_kernel(const CtxArgs a, int n_items, int n_z) {
+    ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
@@ -185,9 +532,12 @@ __global__ void __launch_bounds__(kCtxThreadsPC)
     long long seq = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
-      for (int k0 = 0; k0 < it.n_chunks; k0 += 32) {
+      // a batch never spans more than one ring round, so every lane's slot was
+      // last used by a chunk issued in an earlier batch and the empty-barrier
+      // parity it waits on is unambiguous
+      for (int k0 = 0; k0 < it.n_chunks; k0 += kRing) {
         const int k = k0 + lane;
-        if (k < it.n_chunks) {
+        if (lane < kRing && k < it.n_chunks) {
           const long long sq = seq + k;
           const int slot = static_cast<int>(sq % kRing);
           mbar_wait(&empty[slot], static_cast<uint32_t>(((sq / kRing) & 1) ^ 1));
@@ -415,24 +765,36 @@ __global__ void __launch_bounds__(kCtxThreadsPC)
 
 template <int R>
 static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStream_t stream) {
-  const int smem = kRing * kSlotBytes + (8 * R * 128 + 16 * R) * 4 + 2 * kRing * 8;
-  cudaError_t e = cudaFuncSetAttribute(ctx_attn_kernel<R>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxThreadsPC, smem);
+  const bool pdl = a.o_sys != nullptr || a.sys_part_acc != nullptr;
+  cudaError_t e;
+  if (a.s_prefix > 0) {
+    // naive baseline: long per-request key sequences -> 4 consumer warps per item
+    const int smem = kRing * kSlotBytes + (8 * R * 128 + 16 * R) * 4 + 2 * kRing * 8;
+    e = cudaFuncSetAttribute(ctx_cta_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R>, kCtxThreadsPC, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
+    ctx_cta_kernel<R><<<grid, kCtxThreadsPC, smem, stream>>>(a, n_items, n_z);
+    return cudaGetLastError();
+  }
+  const int smem = kCtxWarps * kWarpSlots * kSlotBytes + kCtxWarps * kWarpSlots * 8;
+  e = cudaFuncSetAttribute(ctx_attn_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxWarps * 32, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = max(1, min((n_items + kCtxWarps - 1) / kCtxWarps, sms * max(per_sm, 1)));
   // Relay mode follows the system kernel, which triggers early: launch with
   // PDL so this kernel streams context K/V on SMs the system kernel has
   // already released (it waits for the system grid before reading its
   // outputs).  Other modes are ordinary stream-ordered launches.
-  if (a.o_sys != nullptr || a.sys_part_acc != nullptr)
-    e = launch_pdl(ctx_attn_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, a, n_items, n_z);
+  if (pdl)
+    e = launch_pdl(ctx_attn_kernel<R>, dim3(grid), dim3(kCtxWarps * 32), smem, stream, a, n_items, n_z);
   else
-    ctx_attn_kernel<R><<<grid, kCtxThreadsPC, smem, stream>>>(a, n_items, n_z);
+    ctx_attn_kernel<R><<<grid, kCtxWarps * 32, smem, stream>>>(a, n_items, n_z);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -487,22 +849,29 @@ cudaError_t launch_relay_fusion(const float* o_sys, const float* lse_sys, const 
 // ----------------------------------------------------------- paged append
 // Write n_tok new (k, v) rows [n_tok][hkv][128] into the pool at
 // slot_mapping[t] = block_id * block_size + offset (kvcache.py:207-235).
+// One thread per 16-byte chunk of K or V: fully parallel, coalesced.
 __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k_new,
                                  const __nv_bfloat16* __restrict__ v_new,
                                  const int* __restrict__ slots, __nv_bfloat16* k_pool,
                                  __nv_bfloat16* v_pool, int n_tok, int hkv, int block_size,
                                  long long stride_block, long long stride_tok,
                                  long long stride_head) {
-  const int t = blockIdx.x;
-  const int slot = slots[t];
+  const long long n_chunks = static_cast<long long>(n_tok) * hkv * 16;
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= 2 * n_chunks) return;
+  const bool is_v = idx >= n_chunks;
+  const long long ci = is_v ? idx - n_chunks : idx;
+  const int c = static_cast<int>(ci & 15);
+  const int h = static_cast<int>((ci >> 4) % hkv);
+  const int t = static_cast<int>((ci >> 4) / hkv);
+  const int slot = __ldg(slots + t);
   const int blk = slot / block_size, off = slot % block_size;
-  for (int idx = threadIdx.x; idx < hkv * 16; idx += blockDim.x) {
-    const int h = idx / 16, c = idx % 16;
-    const long long src = (static_cast<long long>(t) * hkv + h) * 128 + c * 8;
-    const long long dst = blk * stride_block + off * stride_tok + h * stride_head + c * 8;
-    *reinterpret_cast<uint4*>(k_pool + dst) = *reinterpret_cast<const uint4*>(k_new + src);
+  const long long src = (static_cast<long long>(t) * hkv + h) * 128 + c * 8;
+  const long long dst = blk * stride_block + off * stride_tok + h * stride_head + c * 8;
+  if (is_v)
     *reinterpret_cast<uint4*>(v_pool + dst) = *reinterpret_cast<const uint4*>(v_new + src);
-  }
+  else
+    *reinterpret_cast<uint4*>(k_pool + dst) = *reinterpret_cast<const uint4*>(k_new + src);
 }
 
 cudaError_t launch_kv_append(const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
@@ -510,8 +879,11 @@ cudaError_t launch_kv_append(const __nv_bfloat16* k_new, const __nv_bfloat16* v_
                              int n_tok, int hkv, int block_size, long long stride_block,
                              long long stride_tok, long long stride_head, cudaStream_t stream) {
   if (n_tok == 0) return cudaSuccess;
-  kv_append_kernel<<<n_tok, 128, 0, stream>>>(k_new, v_new, slots, k_pool, v_pool, n_tok, hkv,
-                                              block_size, stride_block, stride_tok, stride_head);
+  const long long total = 2LL * n_tok * hkv * 16;
+  const int threads = 256;
+  kv_append_kernel<<<static_cast<unsigned>((total + threads - 1) / threads), threads, 0, stream>>>(
+      k_new, v_new, slots, k_pool, v_pool, n_tok, hkv, block_size, stride_block, stride_tok,
+      stride_head);
   return cudaGetLastError();
 }
 

@@ -233,6 +233,10 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     // ------------------------------------------------------------ V producer
     const uint64_t pol = l2_policy_evict_first();
     if (lane == 0) {
+      // Start streaming V only once this CTA's first K tile has landed: at
+      // launch every SM fires its rings at once, and the first Q.K^T must not
+      // queue behind four V tiles per SM.
+      if (t_begin < t_end) mbar_wait(&k_full[0], 0);
       int j = 0;
       for (long long i = t_begin; i < t_end; ++i, ++j) {
         const int u = static_cast<int>(i / P.tpu);
