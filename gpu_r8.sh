@@ -1,0 +1,4 @@
+python -m paper_2402_14808_b200.build 2>&1 | tail -1
+timeout 300 python profiles/diag_step_timeline.py 8192 3 0 60 100 147 2>&1 | tail -14
+timeout 600 python -m pytest tests/test_relay_step.py tests/test_gpu_parity.py -m gpu -q -x 2>&1 | tail -5
+timeout 600 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/bench8.json 2> gpurun_out/bench8.err; echo "bench rc $?"; tail -3 gpurun_out/bench8.err

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 1
+#define RB_ABI_VERSION 2
 
 enum {
   RB_OK = 0,
@@ -137,6 +137,36 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        size_t workspace_bytes, int phases, void* stream);
 
 /*
+ * The relay decode step as ONE persistent kernel (relay_step_sm100.cu):
+ * system tiles (stream-K over the shared prefix, read once) and context tiles
+ * (whole (request, kv head) units over the paged pool or a ragged context
+ * buffer) run through one TMA + tcgen05 pipeline; the last contributor of
+ * each output group merges the system parts with the context partials (relay
+ * fusion, attention.py:137-157) into `out` and the fused LSE.  Same arguments
+ * as rb_relay_attention plus the context buffer extent `ctx_extent` (paged:
+ * number of pool blocks; ragged: number of context tokens).  max_rows =
+ * max_r(m_r) * (hq / hkv).  workspace: rb_relay_step_workspace_bytes(...)
+ * bytes, ZERO-FILLED before the first call (the kernel leaves its
+ * semaphores zeroed).  Context pool slots a request has not written must hold
+ * finite values (PagedKvCache zero-initialises its pool).  phases: 3 = the
+ * full step; 1 / 2 = system / context tiles only (profiling; output is then
+ * the segment's own attention).  rb_relay_step_supported() says whether a
+ * shape runs here (else use rb_relay_attention).
+ */
+int rb_relay_step_supported(int n_rows, int hq, int hkv, int b, int block_size, int paged);
+int rb_relay_step_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap,
+                                  size_t* bytes);
+int rb_relay_step(const void* q, long long q_row_stride, long long q_head_stride,
+                  const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
+                  const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
+                  long long sys_stride_head, const void* k, const void* v, long long ctx_extent,
+                  const int* block_table, int bt_stride, int block_size,
+                  const long long* req_offset, long long stride_block, long long stride_tok,
+                  long long stride_head, const int* ctx_lens, float scale, int grid_cap,
+                  void* out, int out_fp32, float* lse_out, void* workspace,
+                  size_t workspace_bytes, int phases, void* stream);
+
+/*
  * Standalone relay fusion (attention.py:137-157) over n_vec vectors of d
  * fp32 values: out = a*o_sys + (1-a)*o_ctx, a = 1/(1+exp(lse_ctx-lse_sys)),
  * evaluated with max-subtracted weights; lse_out (optional) = logaddexp.
@@ -162,6 +192,15 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
  */
 int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void* p, int nq,
                         float* s_out, float* o_out, void* stream);
+
+/*
+ * Debug probe of the paged-context operand layouts of rb_relay_step (one CTA):
+ * k, v [128 keys][128 d] bf16 are laid out as PagedKvCache blocks of
+ * block_size (16/32/64) tokens, q, p [32][128]; s_out = K.Q^T and
+ * o_out = V^T.P^T, fp32 [128][32].  For tests only.
+ */
+int rb_debug_ctx_probe(const void* k, const void* q, const void* v, const void* p, int block_size,
+                       float* s_out, float* o_out, void* stream);
 
 /*
  * Debug: when `buf` (device, [grid][8] u64) is non-NULL, subsequent

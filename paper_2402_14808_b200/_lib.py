@@ -22,7 +22,8 @@ EXPORTS = (
     "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
     "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
     "rb_relay_workspace_bytes", "rb_relay_attention",
-    "rb_debug_umma_probe", "rb_debug_set_timestamps",
+    "rb_relay_step_supported", "rb_relay_step_workspace_bytes", "rb_relay_step",
+    "rb_debug_umma_probe", "rb_debug_ctx_probe", "rb_debug_set_timestamps",
 )
 
 _lib = None
@@ -60,14 +61,23 @@ def load():
         vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,      # k .. ctx_lens
         f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
+    lib.rb_relay_step_supported.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.rb_relay_step_workspace_bytes.argtypes = [i32, i32, i32, i32, i32,
+                                                  ctypes.POINTER(ctypes.c_size_t)]
+    lib.rb_relay_step.argtypes = [
+        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,   # q .. d
+        vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
+        vp, vp, i64, vp, i32, i32, vp, i64, i64, i64, vp,  # k .. ctx_lens
+        f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
     lib.rb_debug_set_timestamps.argtypes = [vp]
+    lib.rb_debug_ctx_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("rb_last_error", "rb_abi_version"):
             getattr(lib, name).restype = i32
-    if lib.rb_abi_version() != 1:
+    if lib.rb_abi_version() != 2:
         raise ImportError("librelay_b200.so ABI mismatch; rebuild")
     _lib = lib
     return lib
@@ -100,6 +110,18 @@ def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int)
     out = ctypes.c_size_t(0)
     check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
           "rb_relay_workspace_bytes")
+    return out.value
+
+
+def relay_step_supported(n_rows: int, hq: int, hkv: int, b: int, block_size: int,
+                         paged: bool) -> bool:
+    return bool(load().rb_relay_step_supported(n_rows, hq, hkv, b, block_size, int(paged)))
+
+
+def relay_step_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().rb_relay_step_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
+          "rb_relay_step_workspace_bytes")
     return out.value
 
 

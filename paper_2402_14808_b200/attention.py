@@ -385,7 +385,7 @@ class RelayDecodeStep:
     """
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
-                 grid=None, out_dtype=torch.bfloat16):
+                 grid=None, out_dtype=torch.bfloat16, fused=None):
         self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
         self.block_table = block_table
         self.ctx_lens = ctx_lens
@@ -398,7 +398,12 @@ class RelayDecodeStep:
         self.grid = kernels.sm_count(dev) if grid is None else grid
         from . import _lib
         self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
-        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        if fused is None:
+            fused = kernels.fused_step_supported(self.b, hq, self.hkv, self.b,
+                                                 paged_cache.block_size, True)
+        self.fused = fused
+        need = kernels.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len,
+                                             self.grid, fused)
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
@@ -411,7 +416,7 @@ class RelayDecodeStep:
             max_rows=self.hq // self.hkv, hkv=self.hkv, sys_layout="hsd",
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), grid=self.grid, out=self.out, lse_out=self.lse,
-            ws=self.ws, phases=phases)
+            ws=self.ws, phases=phases, fused=self.fused)
 
     def system(self, q):
         """Only the system kernel of the step (profiling)."""
@@ -461,6 +466,13 @@ class RelayDecodeStep:
         def body():
             cur = torch.cuda.current_stream(dev)
             side.wait_stream(cur)
+            if self.fused:
+                # one kernel reads q, the prefix and the appended context
+                qkv_dev.copy_(qkv_host, non_blocking=True)
+                self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
+                out, _ = self(qkv_dev[0])
+                out_host.copy_(out, non_blocking=True)
+                return
             qkv_dev[0].copy_(qkv_host[0], non_blocking=True)
             self.system(qkv_dev[0])
             with torch.cuda.stream(side):

@@ -30,6 +30,10 @@ cudaError_t launch_relay_fusion(const float*, const float*, const float*, const 
                                 float*, long long, int, cudaStream_t);
 cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
                               const __nv_bfloat16*, int, float*, float*, cudaStream_t);
+cudaError_t launch_ctx_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
+                             const __nv_bfloat16*, int, float*, float*, cudaStream_t);
+cudaError_t launch_relay_step(const CUtensorMap*, const StepArgs&, int, cudaStream_t);
+int relay_step_max_b(int nq);
 cudaError_t launch_kv_append(const __nv_bfloat16*, const __nv_bfloat16*, const int*,
                              __nv_bfloat16*, __nv_bfloat16*, int, int, int, long long, long long,
                              long long, cudaStream_t);
@@ -332,6 +336,176 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   return cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
 }
 
+// ---------------------------------------------- one-kernel relay step
+static int tmap_encode(CUtensorMap* map, int rank, const void* base, const cuuint64_t* dims,
+                       const cuuint64_t* strides_bytes, const cuuint32_t* box, const char* what) {
+  auto enc = get_encode();
+  if (!enc) return fail(RB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(RB_ERR_CONTRACT, "%s base must be 16-byte aligned", what);
+  for (int i = 0; i < rank - 1; ++i)
+    if (strides_bytes[i] % 16 != 0)
+      return fail(RB_ERR_CONTRACT, "%s strides must be multiples of 8 elements", what);
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims,
+                   strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RB_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed (%d)", what, (int)r);
+  return RB_OK;
+}
+
+static int step_nq(int rows_per_head) { return rows_per_head <= 16 ? 16 : 32; }
+
+int rb_relay_step_supported(int n_rows, int hq, int hkv, int b, int block_size, int paged) {
+  if (n_rows < 1 || hq < 1 || hkv < 1 || hq % hkv != 0) return 0;
+  const int g = hq / hkv;
+  const int nq = step_nq(n_rows * g);
+  if (nq % g != 0) return 0;
+  if (b > rb::relay_step_max_b(nq)) return 0;
+  if (paged && (block_size < 8 || block_size > RB_KEY_TILE || RB_KEY_TILE % block_size != 0))
+    return 0;
+  return 1;
+}
+
+struct StepWs {
+  size_t cnt, sys_ml, sys_acc, ctx_ml, ctx_acc, total;
+};
+static StepWs step_ws(const rb_sys_plan& p, int n_rows, int hq) {
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  StepWs w;
+  w.cnt = 0;
+  w.sys_ml = up((size_t)p.n_units * sizeof(int));
+  w.sys_acc = w.sys_ml + up((size_t)p.n_units * p.max_parts * 2 * p.nq * sizeof(float));
+  w.ctx_ml = w.sys_acc + up((size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float));
+  w.ctx_acc = w.ctx_ml + up((size_t)n_rows * hq * 2 * sizeof(float));
+  w.total = w.ctx_acc + up((size_t)n_rows * hq * RB_HEAD_DIM * sizeof(float));
+  return w;
+}
+
+static void make_step_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s, int grid_cap) {
+  rb_make_sys_plan(p, n_rows, hq, hkv, s, grid_cap);
+  // the fused kernel picks its own query tile (and needs nq % g == 0)
+  p->nq = step_nq(p->rows_per_head);
+  p->n_qt = (p->rows_per_head + p->nq - 1) / p->nq;
+  p->n_units = hkv * p->n_qt;
+  p->total = (long long)p->n_units * p->tpu;
+  long long gcap = grid_cap < 1 ? 1 : grid_cap;
+  p->grid = (int)(p->total < gcap ? p->total : gcap);
+  int mp = 1;
+  for (int u = 0; u < p->n_units; ++u) {
+    int c = rb_unit_parts(p, u);
+    if (c > mp) mp = c;
+  }
+  p->max_parts = mp;
+}
+
+int rb_relay_step_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap,
+                                  size_t* bytes) {
+  long long f[8];
+  size_t dummy = 0;
+  int st = rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, &dummy);
+  if (st != RB_OK) return st;
+  rb_sys_plan p;
+  make_step_plan(&p, n_rows, hq, hkv, s, grid_cap);
+  *bytes = step_ws(p, n_rows, hq).total;
+  return RB_OK;
+}
+
+int rb_relay_step(const void* q, long long q_row_stride, long long q_head_stride,
+                  const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
+                  const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
+                  long long sys_stride_head, const void* k, const void* v, long long ctx_extent,
+                  const int* block_table, int bt_stride, int block_size,
+                  const long long* req_offset, long long stride_block, long long stride_tok,
+                  long long stride_head, const int* ctx_lens, float scale, int grid_cap,
+                  void* out, int out_fp32, float* lse_out, void* workspace,
+                  size_t workspace_bytes, int phases, void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
+  size_t need = 0;
+  int st = rb_relay_step_workspace_bytes(n_rows, hq, hkv, s, grid_cap, &need);
+  if (st != RB_OK) return st;
+  if (workspace_bytes < need)
+    return fail(RB_ERR_CONTRACT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  const int paged = block_table != nullptr;
+  if (!paged && req_offset == nullptr && b > 0)
+    return fail(RB_ERR_CONTRACT, "either block_table (paged) or req_offset (ragged) is required");
+  if (!rb_relay_step_supported(n_rows, hq, hkv, b, block_size, paged))
+    return fail(RB_ERR_CONTRACT, "shape not supported by the fused relay step");
+  rb::StepArgs a;
+  make_step_plan(&a.sp, n_rows, hq, hkv, s, grid_cap);
+  const int g = a.sp.g, nq = a.sp.nq;
+  a.has_sys = (phases & 1) ? 1 : 0;
+  a.has_ctx = ((phases & 2) && b > 0) ? 1 : 0;
+  a.b = b;
+  const int max_m = (max_rows + g - 1) / g;
+  a.ctx_rows_box = max_m < nq / g ? max_m : nq / g;
+  if (a.ctx_rows_box < 1) a.ctx_rows_box = 1;
+  a.paged = paged;
+  a.block_size = paged ? block_size : RB_KEY_TILE;
+  a.q_start = q_start;
+  a.ctx_lens = ctx_lens;
+  a.block_table = block_table;
+  a.bt_stride = bt_stride;
+  a.req_offset = req_offset;
+  a.scale_log2 = scale * rb::kLog2e;
+  const StepWs w = step_ws(a.sp, n_rows, hq);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  a.counters = reinterpret_cast<int*>(ws + w.cnt);
+  a.sys_ml = reinterpret_cast<float*>(ws + w.sys_ml);
+  a.sys_acc = reinterpret_cast<float*>(ws + w.sys_acc);
+  a.ctx_ml = reinterpret_cast<float*>(ws + w.ctx_ml);
+  a.ctx_acc = reinterpret_cast<float*>(ws + w.ctx_acc);
+  a.out = out;
+  a.out_fp32 = out_fp32;
+  a.lse_out = lse_out;
+  a.debug_ts = g_debug_ts;
+
+  CUtensorMap maps[6];  // q (system box), q (context box), sys k, sys v, ctx k, ctx v
+  {
+    cuuint64_t dims[4] = {RB_HEAD_DIM, (cuuint64_t)g, (cuuint64_t)hkv, (cuuint64_t)n_rows};
+    cuuint64_t str[3] = {(cuuint64_t)(q_head_stride * 2), (cuuint64_t)(g * q_head_stride * 2),
+                         (cuuint64_t)(q_row_stride * 2)};
+    cuuint32_t box_s[4] = {64, (cuuint32_t)g, 1, (cuuint32_t)(nq / g)};
+    cuuint32_t box_c[4] = {64, (cuuint32_t)g, 1, (cuuint32_t)a.ctx_rows_box};
+    if ((st = tmap_encode(&maps[0], 4, q, dims, str, box_s, "q")) != RB_OK) return st;
+    if ((st = tmap_encode(&maps[1], 4, q, dims, str, box_c, "q")) != RB_OK) return st;
+  }
+  if ((st = make_kv_map(&maps[2], sys_k, s, hkv, sys_stride_tok, sys_stride_head)) != RB_OK) return st;
+  if ((st = make_kv_map(&maps[3], sys_v, s, hkv, sys_stride_tok, sys_stride_head)) != RB_OK) return st;
+  if (a.has_ctx) {
+    if (ctx_extent < 1) return fail(RB_ERR_CONTRACT, "context extent must be >= 1");
+    for (int i = 0; i < 2; ++i) {
+      const void* base = i == 0 ? k : v;
+      if (paged) {
+        cuuint64_t dims[4] = {RB_HEAD_DIM, (cuuint64_t)block_size, (cuuint64_t)hkv,
+                              (cuuint64_t)ctx_extent};
+        cuuint64_t str[3] = {(cuuint64_t)(stride_tok * 2), (cuuint64_t)(stride_head * 2),
+                             (cuuint64_t)(stride_block * 2)};
+        cuuint32_t box[4] = {64, (cuuint32_t)block_size, 1, 1};
+        if ((st = tmap_encode(&maps[4 + i], 4, base, dims, str, box, "context K/V")) != RB_OK)
+          return st;
+      } else {
+        cuuint64_t dims[3] = {RB_HEAD_DIM, (cuuint64_t)hkv, (cuuint64_t)ctx_extent};
+        cuuint64_t str[2] = {(cuuint64_t)(stride_head * 2), (cuuint64_t)(stride_tok * 2)};
+        cuuint32_t box[3] = {64, 1, RB_KEY_TILE};
+        if ((st = tmap_encode(&maps[4 + i], 3, base, dims, str, box, "context K/V")) != RB_OK)
+          return st;
+      }
+    }
+  } else {
+    maps[4] = maps[2];
+    maps[5] = maps[3];
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = grid_cap > 0 && grid_cap < sms ? grid_cap : sms;
+  if (grid < a.sp.grid) grid = a.sp.grid;
+  return cuda_status(rb::launch_relay_step(maps, a, grid, static_cast<cudaStream_t>(stream)),
+                     "relay step launch");
+}
+
 int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx,
                     const float* lse_ctx, float* out, float* lse_out, long long n_vec, int d,
                     void* stream) {
@@ -353,6 +527,15 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
                            n_tok, hkv, block_size, stride_block, stride_tok, stride_head,
                            static_cast<cudaStream_t>(stream)),
       "kv append launch");
+}
+
+int rb_debug_ctx_probe(const void* k, const void* q, const void* v, const void* p, int block_size,
+                       float* s_out, float* o_out, void* stream) {
+  return cuda_status(
+      rb::launch_ctx_probe(static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(q),
+                           static_cast<const __nv_bfloat16*>(v), static_cast<const __nv_bfloat16*>(p),
+                           block_size, s_out, o_out, static_cast<cudaStream_t>(stream)),
+      "ctx probe launch");
 }
 
 int rb_debug_set_timestamps(void* buf) {

@@ -61,4 +61,33 @@ struct CtxArgs {
   float scale_log2;
 };
 
+// One fused relay decode step (relay_step_sm100.cu): system tiles (stream-K
+// over the shared prefix) and context tiles (whole (request, kv head, q-tile)
+// units over the paged / ragged context KV) through one TMA + tcgen05
+// pipeline; partial states merged by the last contributor of each output
+// group (= system unit) into the fused output.
+struct StepArgs {
+  rb_sys_plan sp;                // system plan: stream-K over sp.total tiles on sp.grid CTAs
+  int has_sys, has_ctx;          // segments present in this launch (profiling can drop one)
+  int b;                         // requests
+  int ctx_rows_box;              // query rows per context Q TMA box
+  int paged;                     // 1: block_table + 4-D pool map; 0: ragged req_offset + 3-D map
+  int block_size;
+  const int* q_start;            // [b+1]
+  const int* ctx_lens;           // [b]
+  const int* block_table;        // [b][bt_stride]
+  int bt_stride;
+  const long long* req_offset;   // [b] (ragged)
+  float scale_log2;
+  int* counters;                 // grid barrier {arrivals, generation}; zero-filled once
+  float* sys_acc;                // [n_units][max_parts][nq][128]
+  float* sys_ml;                 // [n_units][max_parts][2][nq]
+  float* ctx_acc;                // [n_rows][hq][128]
+  float* ctx_ml;                 // [n_rows][hq][2]
+  void* out;                     // [n_rows][hq][128] bf16 or fp32
+  int out_fp32;
+  float* lse_out;                // [n_rows][hq] natural log (may be null)
+  unsigned long long* debug_ts;  // optional per-CTA stamps [grid][64]
+};
+
 }  // namespace rb

@@ -142,13 +142,25 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
     return out, lse_out
 
 
+def fused_step_supported(n_rows, hq, hkv, b, block_size, paged) -> bool:
+    return _lib.relay_step_supported(n_rows, hq, hkv, b, block_size, paged)
+
+
+def relay_workspace_bytes(n_rows, hq, hkv, s, grid, fused) -> int:
+    if fused:
+        return _lib.relay_step_workspace_bytes(n_rows, hq, hkv, s, grid)
+    return _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid)
+
+
 def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
                     sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
                     strides=None, scale=None, grid=None, out=None, lse_out=None,
-                    out_fp32=False, ws=None, phases=3):
-    """The fused relay step (rb_relay_attention): system kernel (stream-K
-    partials, no merge) + context kernel whose epilogue merges the system
-    partials with the context state.  Returns (out, lse)."""
+                    out_fp32=False, ws=None, phases=3, fused=None):
+    """The relay decode step.  fused (default when the shape is supported):
+    rb_relay_step, ONE persistent kernel for system tiles, context tiles and
+    the fusion.  fused=False: rb_relay_attention, the two-kernel path (system
+    kernel writing stream-K partials + context kernel merging them in its
+    epilogue).  Returns (out, lse)."""
     _check_bf16("q", q)
     n_rows, hq, d = q.shape
     if d != HEAD_DIM:
@@ -168,12 +180,24 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
         lse_out = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
     grid = sm_count(dev) if grid is None else grid
     stream = _stream(dev)
+    paged = block_table is not None
+    if fused is None:
+        fused = fused_step_supported(n_rows, hq, hkv, b, block_size, paged)
     if ws is None:
-        need = _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid)
-        ws = workspace(need, dev, stream, kind="relay")
+        need = relay_workspace_bytes(n_rows, hq, hkv, s, grid, fused)
+        ws = workspace(need, dev, stream, kind="step" if fused else "relay")
     sb, stok, sh = strides
     bt_stride = block_table.stride(0) if block_table is not None else 0
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
+    if fused:
+        _lib.check(_lib.load().rb_relay_step(
+            q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq,
+            hkv, HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
+            v.data_ptr(), k.shape[0], _ptr(block_table), bt_stride, block_size,
+            _ptr(req_offset), sb, stok, sh, ctx_lens.data_ptr(), float(scale), grid,
+            out.data_ptr(), 1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(),
+            ws.data_ptr(), ws.numel(), phases, stream), "rb_relay_step")
+        return out, lse_out
     _lib.check(_lib.load().rb_relay_attention(
         q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq, hkv,
         HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
@@ -217,4 +241,14 @@ def umma_probe(k, q, v, p):
     _lib.check(_lib.load().rb_debug_umma_probe(
         k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), nq, s_out.data_ptr(),
         o_out.data_ptr(), _stream(k.device)), "rb_debug_umma_probe")
+    return s_out, o_out
+
+
+def ctx_probe(k, q, v, p, block_size):
+    """Debug: the paged-context tcgen05 operand layouts of rb_relay_step on one tile."""
+    s_out = torch.empty((128, 32), dtype=torch.float32, device=k.device)
+    o_out = torch.empty((128, 32), dtype=torch.float32, device=k.device)
+    _lib.check(_lib.load().rb_debug_ctx_probe(
+        k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), block_size, s_out.data_ptr(),
+        o_out.data_ptr(), _stream(k.device)), "rb_debug_ctx_probe")
     return s_out, o_out

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(raw, name), name
     assert set(_declared()) == set(_lib.EXPORTS)
-    assert lib.rb_abi_version() == 1
+    assert lib.rb_abi_version() == 2
 
 
 def test_error_mapping_without_gpu():

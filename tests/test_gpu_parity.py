@@ -351,7 +351,8 @@ def test_fused_relay_equals_two_kernel_path(rb, oracle, grid):
     sys_cache = SystemKvCache.from_shd([sk], [sv])
     paged, bt, cl = make_paged(rb, ck, cv, hkv)
     qd = dev_bf16(q)
-    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32,
+                           fused=False)
     out, lse = step(qd)
     o_sys, lse_sys = kernels.system_attention(qd, sys_cache.keys[0], sys_cache.values[0],
                                               kv_layout="hsd", grid=grid)
