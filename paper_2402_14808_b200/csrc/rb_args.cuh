@@ -71,8 +71,15 @@ struct StepArgs {
   int has_sys, has_ctx;          // segments present in this launch (profiling can drop one)
   int b;                         // requests
   int ctx_rows_box;              // query rows per context Q TMA box
-  int paged;                     // 1: block_table + 4-D pool map; 0: ragged req_offset + 3-D map
-  int block_size;
+  int paged;                     // 1: block_table + paged pool; 0: ragged req_offset + 3-D map
+  int block_size;                // paged: 16 / 32 / 64 tokens per block
+  int causal;                    // context rows see keys < c_r - m_r + t + 1 (else all c_r)
+  int prefix_tiles;              // naive baseline: every context unit first re-reads the
+                                 // shared prefix (ceil(s / 128) tiles), no system units
+  const unsigned char* k_pool;   // paged: one layer's K pool, blocks of [128 d][bs] (swizzled)
+  const unsigned char* v_pool;
+  long long pool_block_bytes;    // byte stride between blocks
+  long long pool_head_bytes;     // byte stride between kv heads of a block
   const int* q_start;            // [b+1]
   const int* ctx_lens;           // [b]
   const int* block_table;        // [b][bt_stride]
@@ -80,10 +87,10 @@ struct StepArgs {
   const long long* req_offset;   // [b] (ragged)
   float scale_log2;
   int* counters;                 // grid barrier {arrivals, generation}; zero-filled once
-  float* sys_acc;                // [n_units][max_parts][nq][128]
-  float* sys_ml;                 // [n_units][max_parts][2][nq]
-  float* ctx_acc;                // [n_rows][hq][128]
-  float* ctx_ml;                 // [n_rows][hq][2]
+  float* sys_acc;                // [n_units][2*max_parts][nq][128]  (slot = part*2 + group)
+  float* sys_ml;                 // [n_units][2*max_parts][2][nq]
+  float* ctx_acc;                // [2 groups][n_rows][hq][128]
+  float* ctx_ml;                 // [2 groups][n_rows][hq][2]
   void* out;                     // [n_rows][hq][128] bf16 or fp32
   int out_fp32;
   float* lse_out;                // [n_rows][hq] natural log (may be null)

@@ -19,31 +19,50 @@
 //    MMA M dimension, the unit's <= NQ query rows are N):
 //        S^T[128 x NQ] = K_tile . Q^T        (tcgen05, TMEM accumulator)
 //        O^T[128 x NQ] += V_tile^T . P^T     (tcgen05, O stays in TMEM)
-//    K, V and Q tiles arrive by TMA (3-D map of the prefix, 4-D map of the
-//    paged pool read in place through the block table, 4-D map of the
-//    queries that picks a KV head's GQA group).
-//  * Softmax: one 4-warp group, thread = key lane, NQ columns per thread,
-//    log2 domain.  Lazy rescaling: the running max of a column only moves
-//    when a tile exceeds it by more than kTau (P <= 2^kTau), so O is
-//    accumulated by the tensor core across the whole part and is rescaled in
-//    TMEM only on those rare moves; row sums stay per-lane until the part ends.
-//  * Epilogue group (4 warps, thread = head dim): drains a finished part's O
-//    from TMEM (double-buffered per part) and writes the partial (acc, m, l)
-//    -- no synchronisation per part.  When a CTA's parts are all written it
-//    joins a grid barrier (one CTA per SM, all resident); then every CTA
-//    merges its share of the output vectors: context partial + system
-//    stream-K parts, the relay fusion.  Partials live in L2 (a few MB), they
-//    never take an HBM round trip of their own.
-//  * Warp roles (12 warps): 0 K/Q TMA producer, 1 QK^T issuer (TMEM owner),
-//    2 V TMA producer, 3 metadata scan then P.V issuer, 4-7 softmax,
-//    8-11 epilogue.
+//    Operands arrive by TMA (3-D map of the prefix, 4-D map of the queries
+//    that picks a KV head's GQA group) or, for paged context, ONE 4 KB bulk
+//    copy per (block, kv head): PagedKvCache stores each block as the
+//    [128 d][bs] swizzled UMMA operand (K MN-major, V^T K-major).
+//  * Two softmax groups (4 warps each, thread = key lane, NQ columns per
+//    thread, log2 domain) take alternate tiles, so one group's tile latency
+//    overlaps the other's.  Lazy rescaling: a column's reference max only
+//    moves when a tile exceeds it by more than kTau (P <= 2^kTau), so O is
+//    accumulated by the tensor core in the group's TMEM buffer across the
+//    whole part and rescaled only on those rare moves; row sums stay per lane
+//    until the group's last tile of the part, when the group drains O from
+//    TMEM and writes its partial (acc, m, l).  No per-part synchronisation
+//    with other CTAs.
+//  * When every part of every CTA is written, a grid barrier (one CTA per SM,
+//    all resident), then every CTA merges its share of the output vectors:
+//    context partials + system stream-K parts = the relay fusion.  Partials
+//    live in L2 (a few MB); they never take an HBM round trip of their own.
+//  * Warp roles (12 warps): 0 K/Q producer, 1 QK^T issuer (TMEM owner),
+//    2 V producer, 3 metadata scan then P.V issuer, 4-7 softmax group 0,
+//    8-11 softmax group 1.
 #include "rb_common.cuh"
 #include "rb_plan.h"
 #include "rb_args.cuh"
 
 namespace rb {
 
-constexpr float kTau = 8.0f;  // lazy-rescale threshold (log2 units)
+constexpr float kTau = 8.0f;         // lazy-rescale threshold (log2 units)
+constexpr float kNegBig = -1.0e30f;  // "no key yet" reference max (exp2(-inf - kNegBig) = 0)
+
+// Per-tile %globaltimer trace -- compiled in only with -DRB_STEP_TRACE=1: the
+// stamps cost instruction-cache footprint.
+#ifndef RB_STEP_TRACE
+#define RB_STEP_TRACE 0
+#endif
+#if RB_STEP_TRACE
+#define RB_TRACE(cond, idx) \
+  do {                      \
+    if (dts && (cond)) dts[idx] = global_timer_ns(); \
+  } while (0)
+#else
+#define RB_TRACE(cond, idx) \
+  do {                      \
+  } while (0)
+#endif
 
 template <int NQ>
 struct StepCfg {
@@ -54,18 +73,18 @@ struct StepCfg {
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + KS * kTile;
   static constexpr int kOffQ = kOffV + VS * kTile;
-  static constexpr int kOffP = kOffQ + QS * kQBytes;
-  static constexpr int kOffRed = kOffP + 2 * kQBytes;   // float [2][4][NQ] tile max per quadrant
-  static constexpr int kOffRed2 = kOffRed + 2 * 4 * NQ * 4;  // float [4][NQ] row sums
-  static constexpr int kOffMu = kOffRed2 + 4 * NQ * 4;       // float [4 warps][NQ] reference max
-  static constexpr int kOffAl = kOffMu + 4 * NQ * 4;         // float [4 warps][NQ] rescale factor
-  static constexpr int kOffHand = kOffAl + 4 * NQ * 4;       // float [2][2][NQ] part (m, l)
-  static constexpr int kOffMisc = kOffHand + 2 * 2 * NQ * 4; // int [16]
-  static constexpr int kIdAhead = 4;                          // block-id lookahead (tiles)
-  static constexpr int kOffIds = kOffMisc + 64;               // int [2 producers][kIdAhead][32]
+  static constexpr int kOffP = kOffQ + QS * kQBytes;            // [2 groups] P tiles
+  static constexpr int kOffRed = kOffP + 2 * kQBytes;           // float [2 grp][2][4][NQ] tile max
+  static constexpr int kOffRed2 = kOffRed + 2 * 2 * 4 * NQ * 4;  // float [2 grp][4][NQ] row sums
+  static constexpr int kOffMu = kOffRed2 + 2 * 4 * NQ * 4;       // float [8 warps][NQ] reference max
+  static constexpr int kOffAl = kOffMu + 8 * NQ * 4;             // float [8 warps][NQ] rescale
+  static constexpr int kOffMisc = kOffAl + 8 * NQ * 4;           // int [16]
+  static constexpr int kIdAhead = 4;                             // block-id lookahead (tiles)
+  static constexpr int kOffIds = kOffMisc + 64;                  // int [2 producers][kIdAhead][32]
   static constexpr int kOffBar = kOffIds + 2 * kIdAhead * 32 * 4;
-  static constexpr int kNumBars = 2 * KS + 2 * VS + 2 * QS + 18;  // rings + s,p,o,h pairs + meta + v_go
+  static constexpr int kNumBars = 2 * KS + 2 * VS + 2 * QS + 14;  // rings + s,p,o pairs + meta + v_go
   static constexpr int kOffMeta = kOffBar + kNumBars * 8;  // int P[b+1], lens[b], qs[b+1]
+  // TMEM per group: S and O accumulators of NQ columns each
   static constexpr int kTmemCols = (4 * NQ <= 32) ? 32 : (4 * NQ <= 64) ? 64 : 128;
   static int smem_bytes(int b) { return kOffMeta + 4 * (3 * b + 2) + 16; }
 };
@@ -73,68 +92,119 @@ struct StepCfg {
 // One tile of this CTA's work sequence.
 struct Tile {
   int kind;         // 0 = system, 1 = context
-  int u;            // system unit (also the output group of a system tile)
+  int u;            // system unit
   int r, h, z;      // context unit
-  int kt;           // key tile inside the unit
+  int kt;           // key tile inside the unit (context tiles: inside the context)
+  int pre;          // naive mode: this context-unit tile re-reads the shared prefix
   int first, last;  // first / last tile of this CTA's part of the unit
+  int pidx, rem;    // index of the tile in the part / tiles left in the part (incl. this)
 };
 
 // Query tiles of request r's context units: ceil(m_r * g / NQ).
 __device__ __forceinline__ int ctx_nz(const StepArgs& a, const int* qs, int r) {
-  return ((qs[r + 1] - qs[r]) * a.sp.g + a.sp.nq - 1) / a.sp.nq;
+  const int lg = __ffs(a.sp.nq) - 1;  // nq is 16 or 32
+  return ((qs[r + 1] - qs[r]) * a.sp.g + a.sp.nq - 1) >> lg;
 }
 
-// Walks a CTA's sequence: system tiles [x0, xe) then context tiles [cx, ce).
+// Tiles of one context unit of a request with c_r context keys.
+__device__ __forceinline__ int ctx_unit_tiles(const StepArgs& a, int c_r) {
+  return a.prefix_tiles + (max(c_r, 0) + RB_KEY_TILE - 1) / RB_KEY_TILE;
+}
+
+// Walks a CTA's sequence: system tiles [xs, xe) then context tiles [cx, ce).
+// Incremental (no division per tile): every role warp runs its own copy.
 struct Walker {
-  long long x0, x, xe;
-  int cx, ce, r;
+  long long xb, xs, xe;    // system range begin / cursor / end
+  int su, skt;             // current system unit / key tile
+  int cx, ce;              // context tile cursor / end (global context tile index)
+  int r, h, z, kt;         // current context unit (request, kv head, q-tile) and tile
+  int tr, nz;              // tiles per unit / q-tiles of request r
   int ctx_ready;
   __device__ __forceinline__ void init(const StepArgs& a, int cta) {
-    x0 = x = xe = 0;
+    xb = xs = xe = 0;
+    su = skt = 0;
     if (a.has_sys && cta < a.sp.grid) {
-      x0 = x = rb_cta_begin(&a.sp, cta);
+      xb = xs = rb_cta_begin(&a.sp, cta);
       xe = rb_cta_begin(&a.sp, cta + 1);
+      su = static_cast<int>(xs / a.sp.tpu);
+      skt = static_cast<int>(xs % a.sp.tpu);
     }
-    cx = ce = r = 0;
+    cx = ce = r = h = z = kt = tr = nz = 0;
     ctx_ready = 0;
+  }
+  // first context tile: locate (request, unit, tile) of cx once
+  __device__ __forceinline__ void locate(const StepArgs& a, const int* P, const int* lens,
+                                         const int* qs, const int* misc, uint64_t* meta_bar) {
+    mbar_wait(meta_bar, 0);
+    cx = misc[2];
+    ce = misc[3];
+    ctx_ready = 1;
+    if (cx >= ce) return;
+    r = 0;
+    while (P[r + 1] <= cx) ++r;
+    tr = ctx_unit_tiles(a, lens[r]);
+    nz = ctx_nz(a, qs, r);
+    const int local = cx - P[r];
+    const int ui = local / tr;
+    kt = local % tr;
+    h = ui / nz;
+    z = ui % nz;
   }
   __device__ __forceinline__ bool next(const StepArgs& a, const int* P, const int* lens,
                                        const int* qs, const int* misc, uint64_t* meta_bar,
                                        Tile& t) {
-    if (x < xe) {
-      const rb_sys_plan& p = a.sp;
+    if (xs < xe) {
+      const long long ub = static_cast<long long>(su) * a.sp.tpu;
+      const long long pb = ub > xb ? ub : xb;
+      const long long pe = ub + a.sp.tpu < xe ? ub + a.sp.tpu : xe;
       t.kind = 0;
-      t.u = static_cast<int>(x / p.tpu);
-      t.kt = static_cast<int>(x % p.tpu);
-      t.first = (x == x0) || t.kt == 0;
-      t.last = (x == xe - 1) || t.kt == p.tpu - 1;
+      t.u = su;
+      t.kt = skt;
+      t.pidx = static_cast<int>(xs - pb);
+      t.rem = static_cast<int>(pe - xs);
+      t.first = t.pidx == 0;
+      t.last = t.rem == 1;
       t.r = t.h = t.z = 0;
-      ++x;
+      t.pre = 0;
+      ++xs;
+      if (++skt == a.sp.tpu) {
+        skt = 0;
+        ++su;
+      }
       return true;
     }
     if (!a.has_ctx) return false;
-    if (!ctx_ready) {
-      mbar_wait(meta_bar, 0);
-      cx = misc[2];
-      ce = misc[3];
-      r = 0;
-      ctx_ready = 1;
-    }
+    if (!ctx_ready) locate(a, P, lens, qs, misc, meta_bar);
     if (cx >= ce) return false;
-    while (P[r + 1] <= cx) ++r;
-    const int tr = (lens[r] + RB_KEY_TILE - 1) / RB_KEY_TILE;
-    const int local = cx - P[r];
-    const int ui = local / tr;
-    const int nz = ctx_nz(a, qs, r);
     t.kind = 1;
-    t.r = r;
-    t.h = ui / nz;
-    t.z = ui % nz;
-    t.kt = local % tr;
-    t.first = t.kt == 0;
-    t.last = t.kt == tr - 1;
     t.u = 0;
+    t.r = r;
+    t.h = h;
+    t.z = z;
+    t.pre = kt < a.prefix_tiles;
+    t.kt = t.pre ? kt : kt - a.prefix_tiles;
+    t.pidx = kt;
+    t.rem = tr - kt;
+    t.first = kt == 0;
+    t.last = kt == tr - 1;
     ++cx;
+    if (++kt == tr) {
+      kt = 0;
+      if (++z == nz) {
+        z = 0;
+        if (++h == a.sp.hkv) {
+          h = 0;
+          // next request with context units (P[r+1] > P[r])
+          do {
+            ++r;
+          } while (r < a.b && P[r + 1] == P[r]);
+          if (r < a.b) {
+            tr = ctx_unit_tiles(a, lens[r]);
+            nz = ctx_nz(a, qs, r);
+          }
+        }
+      }
+    }
     return true;
   }
 };
@@ -181,137 +251,233 @@ __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool pred) {
   return r != 0;
 }
 
-constexpr float kNegBig = -1.0e30f;  // "no key yet" reference max (exp2 of -inf - kNegBig = 0)
-
-// Shared-memory / TMEM context of the softmax group.
+// Per-thread context of a softmax group.
 struct SmxCtx {
-  float* red;       // [2][4][NQ] tile maxima per quadrant
-  float* red2;      // [4][NQ] row sums
+  float* red;       // [2][4][NQ] this group's tile maxima per quadrant
+  float* red2;      // [4][NQ] this group's row sums
   float* my_mu;     // [NQ] this warp's copy of the reference max per column
   float* my_al;     // [NQ] this warp's copy of the rescale factors
-  float* hand;      // [2][2][NQ] part (m, l) -> epilogue
-  uint8_t* pbase;   // P tile of this thread's key half (add sb * kQBytes)
+  uint8_t* pbase;   // this group's P tile, this thread's key half
   uint32_t poff[8];
-  uint32_t lane_addr;  // TMEM address of this warp's lane quadrant
+  uint32_t s_addr;  // TMEM: this group's S buffer, this warp's lane quadrant
+  uint32_t o_addr;  // TMEM: this group's O buffer, this warp's lane quadrant
+  uint32_t bar;     // named barrier of the group (128 threads)
   int qd, lane;
 };
 
-// One tile of the softmax group for HC <= NQ live columns (HC = 8 for context
-// units with few query rows, HC = NQ otherwise).  x: masked, log2-scaled
-// scores of this thread's key lane.  Lazy rescaling: the common path is one
-// OR-barrier (does any score exceed its column's reference max by > kTau?),
-// exp2, row-sum accumulation and the P store; the reference maxima and the
-// O accumulator in TMEM only change on the rare path.
-template <int HC, int NQ>
-__device__ __forceinline__ void softmax_tile(const SmxCtx& C, float (&x)[HC], float (&mr)[NQ],
-                                             float (&l_part)[NQ], bool first, int j, int n,
-                                             uint64_t* p_empty, uint64_t* p_full, int qbytes) {
-  if (first) {
+// Mask of one tile: column c of the tile sees this thread's key iff
+// cmin <= c < cmax (system / prefix tiles: cmin = -1 or NQ by key < s).
+struct TileMask {
+  int cmin, cmax;
+};
+
+// Chunk of 8 score columns [c0, c0+8) of this thread's key lane: TMEM -> masked,
+// log2-scaled registers.
+__device__ __forceinline__ void load_scores8(uint32_t s_addr, int c0, const TileMask& mk,
+                                             float scale, float (&y)[8]) {
+  float x[8];
+  tmem_ld_32x32b<8>(s_addr + c0, x);
+  tmem_wait_ld();
 #pragma unroll
-    for (int c = 0; c < NQ; ++c) {
-      mr[c] = kNegBig;
-      l_part[c] = 0.f;
-    }
-    if (reduced_writer<HC>(C.lane)) C.my_mu[reduced_col<HC>(C.lane)] = kNegBig;
+  for (int e = 0; e < 8; ++e) {
+    const int c = c0 + e;
+    y[e] = (c >= mk.cmin && c < mk.cmax) ? x[e] * scale : -INFINITY;
   }
-  bool ex = false;
-#pragma unroll
-  for (int c = 0; c < HC; ++c) ex |= x[c] > mr[c] + kTau;
-  if (bar_red_or(1, 128, ex)) {
-    // ---- rare path: per-column tile max over the 128 key lanes
-    float tmp[HC];
-#pragma unroll
-    for (int c = 0; c < HC; ++c) tmp[c] = x[c];
-    const float wmax = warp_reduce_cols<HC, true>(tmp, C.lane);
-    const int rc = reduced_col<HC>(C.lane);
-    const bool rw = reduced_writer<HC>(C.lane);
-    float* rb = C.red + (j & 1) * 4 * NQ;
-    if (rw) rb[C.qd * NQ + rc] = wmax;
-    named_bar_sync(1, 128);
-    const float tm = fmaxf(fmaxf(rb[rc], rb[NQ + rc]), fmaxf(rb[2 * NQ + rc], rb[3 * NQ + rc]));
-    const float mold = C.my_mu[rc];
-    const bool mv = tm > mold + kTau;
-    const float alpha = mv ? fast_exp2(mold - tm) : 1.f;  // 0 when mold is kNegBig
-    const bool from_finite = mv && mold > 0.5f * kNegBig;
-    __syncwarp();
-    if (rw) {
-      if (mv) C.my_mu[rc] = tm;
-      C.my_al[rc] = alpha;
-    }
-    const bool need_o = __any_sync(0xffffffffu, from_finite) && !first;
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < HC; ++c) mr[c] = C.my_mu[c];
-    if (need_o) {
-      // rescale the row sums and O (after the previous P.V has landed in TMEM)
-#pragma unroll
-      for (int c = 0; c < HC; ++c) l_part[c] *= C.my_al[c];
-      mbar_wait(&p_empty[(j - 1) & 1], ((j - 1) >> 1) & 1);
-      tc_fence_after();
-      const uint32_t oaddr = C.lane_addr + 2 * NQ + (n & 1) * NQ;
-#pragma unroll
-      for (int c0 = 0; c0 < HC; c0 += 8) {
-        float o[8];
-        tmem_ld_32x32b<8>(oaddr + c0, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) o[c] *= C.my_al[c0 + c];
-        tmem_st_32x32b<8>(oaddr + c0, o);
-      }
-      tmem_wait_st();
-    }
-  }
-  // ---- P = 2^(x - m) (bf16) into the K-major SW128 [NQ][128 keys] tile
-#pragma unroll
-  for (int c = 0; c < HC; ++c) {
-    x[c] = fast_exp2(x[c] - mr[c]);
-    l_part[c] += x[c];
-  }
-  const int sb = j & 1;
-  mbar_wait(&p_empty[sb], ((j >> 1) & 1) ^ 1);
-  uint8_t* pdst = C.pbase + sb * qbytes;
-#pragma unroll
-  for (int c = 0; c < HC; ++c)
-    *reinterpret_cast<__nv_bfloat16*>(pdst + (c >> 3) * 1024 + C.poff[c & 7]) =
-        __float2bfloat16_rn(x[c]);
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncwarp();
-  if (C.lane == 0) mbar_arrive(&p_full[sb]);
 }
 
-// Part end: row sums over the 128 key lanes and the reference maxima go to the
-// epilogue through `hand` (columns < HC).
-template <int HC, int NQ>
-__device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const float (&l_part)[NQ], int n,
-                                                 uint64_t* h_empty, uint64_t* h_full) {
-  float tmp[HC];
-#pragma unroll
-  for (int c = 0; c < HC; ++c) tmp[c] = l_part[c];
-  const float wsum = warp_reduce_cols<HC, false>(tmp, C.lane);
-  const int rc = reduced_col<HC>(C.lane);
-  const bool rw = reduced_writer<HC>(C.lane);
-  if (rw) C.red2[C.qd * NQ + rc] = wsum;
-  named_bar_sync(1, 128);
-  if (C.qd == 0) {
-    const int ob = n & 1;
-    mbar_wait(&h_empty[ob], ((n >> 1) & 1) ^ 1);
-    if (rw) {
-      C.hand[ob * 2 * NQ + rc] = C.my_mu[rc];
-      C.hand[ob * 2 * NQ + NQ + rc] =
-          C.red2[rc] + C.red2[NQ + rc] + C.red2[2 * NQ + rc] + C.red2[3 * NQ + rc];
-    }
-    __syncwarp();
-    if (C.lane == 0) mbar_arrive(&h_full[ob]);
+// Rare path of a tile: per-column tile max over the group's 128 key
+// lanes, move the reference max of every column that grew by more than kTau,
+// and rescale that column's O accumulator in TMEM; returns whether the row
+// sums must be rescaled too (factors in my_al).
+__device__ __forceinline__ bool softmax_rare(const SmxCtx& C, int ncol, int NQ, bool first,
+                                             const TileMask& mk, float scale, int k,
+                                             uint64_t* p_empty) {
+  float* rb = C.red + (k & 1) * 4 * NQ;
+#pragma unroll 1
+  for (int c0 = 0; c0 < ncol; c0 += 8) {
+    float y[8];
+    load_scores8(C.s_addr, c0, mk, scale, y);
+    const float wmax = warp_reduce_cols<8, true>(y, C.lane);  // lane l: column c0 + l / 4
+    if (reduced_writer<8>(C.lane)) rb[C.qd * NQ + c0 + reduced_col<8>(C.lane)] = wmax;
   }
+  named_bar_sync(C.bar, 128);
+  bool from_finite = false;
+  __syncwarp();
+  if (C.lane < ncol) {
+    const int c = C.lane;
+    const float tm = fmaxf(fmaxf(rb[c], rb[NQ + c]), fmaxf(rb[2 * NQ + c], rb[3 * NQ + c]));
+    const float mold = C.my_mu[c];
+    const bool mv = tm > mold + kTau;
+    C.my_al[c] = mv ? fast_exp2(mold - tm) : 1.f;  // 0 when mold is kNegBig
+    if (mv) C.my_mu[c] = tm;
+    from_finite = mv && mold > 0.5f * kNegBig;
+  }
+  const bool need_o = __any_sync(0xffffffffu, from_finite) && !first;
+  __syncwarp();
+  if (need_o) {
+    // rescale O (after this group's previous P.V landed)
+    mbar_wait(p_empty, ((k - 1) & 1));
+    tc_fence_after();
+#pragma unroll 1
+    for (int c0 = 0; c0 < ncol; c0 += 8) {
+      float o[8];
+      tmem_ld_32x32b<8>(C.o_addr + c0, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] *= C.my_al[c0 + e];
+      tmem_st_32x32b<8>(C.o_addr + c0, o);
+    }
+    tmem_wait_st();
+    tc_fence_before();
+  }
+  return need_o;
+}
+
+// One tile of a softmax group over `ncol` (8 or NQ) live columns, processed
+// in chunks of 8 read straight from TMEM (the loop bodies must stay small:
+// the instruction cache is shared by two softmax warps and a role warp per
+// SMSP, and a miss goes to L2 behind the TMA stream):
+//   pass 1: does any score exceed its column's reference max by > kTau?
+//           (one OR-barrier over the group; the rare path moves the maxima)
+//   pass 2: P = 2^(y - m) (bf16) into the K-major SW128 [NQ][128 keys] tile,
+//           fp32 row sums per key lane in l_part (reduced at the part end).
+template <int NQ>
+__device__ __forceinline__ void softmax_tile(const SmxCtx& C, float (&l_part)[NQ], int ncol,
+                                             bool first, int k, const TileMask& mk, float scale,
+                                             uint64_t* s_empty, uint64_t* p_empty,
+                                             uint64_t* p_full) {
+  if (first) {
+    __syncwarp();
+    if (C.lane < NQ) C.my_mu[C.lane] = kNegBig;
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) l_part[c] = 0.f;
+  }
+  bool ex = false;
+#pragma unroll 1
+  for (int c0 = 0; c0 < ncol; c0 += 8) {
+    float y[8];
+    load_scores8(C.s_addr, c0, mk, scale, y);
+    const float4 m0 = *reinterpret_cast<const float4*>(C.my_mu + c0);
+    const float4 m1 = *reinterpret_cast<const float4*>(C.my_mu + c0 + 4);
+    ex |= (y[0] > m0.x + kTau) | (y[1] > m0.y + kTau) | (y[2] > m0.z + kTau) |
+          (y[3] > m0.w + kTau) | (y[4] > m1.x + kTau) | (y[5] > m1.y + kTau) |
+          (y[6] > m1.z + kTau) | (y[7] > m1.w + kTau);
+  }
+  if (bar_red_or(C.bar, 128, ex)) {
+    const bool resc = softmax_rare(C, ncol, NQ, first, mk, scale, k, p_empty);
+    if (resc) {
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) l_part[c] *= C.my_al[c];
+    }
+  }
+  mbar_wait(p_empty, (k & 1) ^ 1);  // this group's previous P.V has read P
+#pragma unroll
+  for (int c0 = 0; c0 < NQ; c0 += 8) {
+    if (c0 < ncol) {
+      float y[8];
+      load_scores8(C.s_addr, c0, mk, scale, y);
+      const float4 m0 = *reinterpret_cast<const float4*>(C.my_mu + c0);
+      const float4 m1 = *reinterpret_cast<const float4*>(C.my_mu + c0 + 4);
+      const float m[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      uint8_t* row = C.pbase + (c0 >> 3) * 1024;  // 8 P rows = one SW128 atom
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float pv = fast_exp2(y[e] - m[e]);
+        l_part[c0 + e] += pv;
+        *reinterpret_cast<__nv_bfloat16*>(row + C.poff[e]) = __float2bfloat16_rn(pv);
+      }
+    }
+  }
+  tc_fence_before();
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (C.lane == 0) {
+    mbar_arrive(s_empty);  // S fully read
+    mbar_arrive(p_full);
+  }
+}
+
+// The group's last tile of a part: row sums over the 128 key lanes (lane c of
+// quadrant 0 ends up with column c), drain O from TMEM (thread = head dim) and
+// write the group's partial (acc, m, l).  sys parts: slot (CTA - first owner)
+// * 2 + group of unit u; context units: ctx partial set `grp` of each of the
+// unit's query rows.  A part with one tile in this CTA also marks the other
+// group's slot empty (m = kNegBig).
+template <int NQ>
+__device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs& a, const Tile& t,
+                                                 const int* qs, const float (&l_part)[NQ],
+                                                 int ncol, int grp, int kp, uint64_t* o_full,
+                                                 uint64_t* o_free) {
+  // row sums: per chunk of 8 columns a warp reduce-scatter, then the 4
+  // quadrants through smem
+#pragma unroll
+  for (int c0 = 0; c0 < NQ; c0 += 8) {
+    if (c0 < ncol) {
+      float v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = l_part[c0 + e];
+      const float ws = warp_reduce_cols<8, false>(v, C.lane);
+      if (reduced_writer<8>(C.lane)) C.red2[C.qd * NQ + c0 + reduced_col<8>(C.lane)] = ws;
+    }
+  }
+  named_bar_sync(C.bar, 128);
+  const int d = C.qd * 32 + C.lane;  // TMEM lane of O = head dim
+  mbar_wait(o_full, kp & 1);
+  tc_fence_after();
+  const rb_sys_plan& p = a.sp;
+  const bool single = t.pidx == 0 && t.rem == 1;
+  long long s0 = 0;
+  const long long nv = static_cast<long long>(p.n_rows) * p.hq;
+  const int g = p.g;
+  int nrow = ncol;  // columns with a real query row
+  if (t.kind == 0) {
+    const int owner0 = rb_tile_owner(&p, static_cast<long long>(t.u) * p.tpu);
+    s0 = static_cast<long long>(t.u) * 2 * p.max_parts + 2 * (blockIdx.x - owner0);
+  } else {
+    nrow = min((qs[t.r + 1] - qs[t.r]) * g - t.z * NQ, ncol);
+  }
+#pragma unroll 1
+  for (int c0 = 0; c0 < ncol; c0 += 8) {
+    float o[8];
+    tmem_ld_32x32b<8>(C.o_addr + c0, o);
+    tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = c0 + e;
+      const float lsum = C.red2[c] + C.red2[NQ + c] + C.red2[2 * NQ + c] + C.red2[3 * NQ + c];
+      if (t.kind == 0) {
+        const long long pb = s0 + grp;
+        a.sys_acc[(pb * NQ + c) * RB_HEAD_DIM + d] = o[e];
+        if (d == 0) {
+          a.sys_ml[pb * 2 * NQ + c] = C.my_mu[c];
+          a.sys_ml[pb * 2 * NQ + NQ + c] = lsum;
+          if (single) a.sys_ml[(s0 + (grp ^ 1)) * 2 * NQ + c] = kNegBig;
+        }
+      } else if (c < nrow) {
+        // local row li = z*NQ + c -> query row qs[r] + li / g, head h*g + li % g
+        const int li = t.z * NQ + c;
+        const long long oi = static_cast<long long>(qs[t.r] + li / g) * p.hq + t.h * g + li % g;
+        a.ctx_acc[(grp * nv + oi) * RB_HEAD_DIM + d] = o[e];
+        if (d == 0) {
+          reinterpret_cast<float2*>(a.ctx_ml)[grp * nv + oi] = make_float2(C.my_mu[c], lsum);
+          if (single)
+            reinterpret_cast<float2*>(a.ctx_ml)[(grp ^ 1) * nv + oi] = make_float2(kNegBig, 0.f);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncwarp();
+  if (C.lane == 0) mbar_arrive(o_free);
 }
 
 // Final merge, after the grid barrier: output vector (row t, query head hh)
-// = LSE-weighted combine of its context partial (if the request has a
-// context) and the system stream-K parts of its group u = (hh / g, f / NQ),
-// in a fixed order (context, then parts by slot): the relay fusion of
+// = LSE-weighted combine of its two context partials (if the request has a
+// context) and the system stream-K slots of its group u = (hh / g, f / NQ),
+// in a fixed order (context, then slots): the relay fusion of
 // attention.py:137-157 with max-subtracted weights.  One warp per vector,
-// lane = 4 head dims.
+// lane = 4 head dims.  Empty partials (m = kNegBig) are skipped.
 template <int NQ>
 __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, const int* lens,
                                              long long v, int lane) {
@@ -320,7 +486,7 @@ __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, c
   const int h = hh / p.g, j = hh % p.g;
   const int f = t * p.g + j;
   const int u = h * p.n_qt + f / NQ, col = f % NQ;
-  const int np = a.has_sys ? rb_unit_parts(&p, u) : 0;
+  const int ns = a.has_sys ? 2 * rb_unit_parts(&p, u) : 0;
   bool hasc = false;
   if (a.has_ctx) {
     int lo = 0, hi = a.b - 1;
@@ -330,34 +496,45 @@ __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, c
     }
     hasc = lens[lo] > 0;
   }
-  const long long ubase = static_cast<long long>(u) * p.max_parts;
-  // pass 1: the common max (context partial and every part's m)
-  float mc = -INFINITY, lc = 0.f;
-  float4 xc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (hasc) {
-    const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ctx_ml) + v);
-    mc = ml.x;
-    lc = ml.y;
-    xc = __ldcg(reinterpret_cast<const float4*>(a.ctx_acc + v * RB_HEAD_DIM) + lane);
+  const long long nv = static_cast<long long>(p.n_rows) * p.hq;
+  const long long ubase = static_cast<long long>(u) * 2 * p.max_parts;
+  // pass 1: the common max
+  float mc[2] = {kNegBig, kNegBig}, lc[2] = {0.f, 0.f};
+  float4 xc[2];
+#pragma unroll
+  for (int gg = 0; gg < 2; ++gg) {
+    xc[gg] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (hasc) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ctx_ml) + gg * nv + v);
+      mc[gg] = ml.x;
+      lc[gg] = ml.y;
+      if (ml.x > 0.5f * kNegBig)
+        xc[gg] = __ldcg(reinterpret_cast<const float4*>(a.ctx_acc + (gg * nv + v) * RB_HEAD_DIM) +
+                        lane);
+    }
   }
-  float M = mc;
+  float M = fmaxf(mc[0], mc[1]);
 #pragma unroll 4
-  for (int k = 0; k < np; ++k) M = fmaxf(M, __ldcg(a.sys_ml + (ubase + k) * 2 * NQ + col));
-  // pass 2: weighted sums in fixed order (context, then parts by slot)
+  for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(a.sys_ml + (ubase + k) * 2 * NQ + col));
+  // pass 2: weighted sums in fixed order (context, then slots)
   float L = 0.f;
   float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (mc != -INFINITY) {
-    const float w = fast_exp2(mc - M);
-    L = lc * w;
-    O = make_float4(xc.x * w, xc.y * w, xc.z * w, xc.w * w);
+#pragma unroll
+  for (int gg = 0; gg < 2; ++gg) {
+    if (mc[gg] > 0.5f * kNegBig) {
+      const float w = fast_exp2(mc[gg] - M);
+      L += lc[gg] * w;
+      O.x += xc[gg].x * w; O.y += xc[gg].y * w; O.z += xc[gg].z * w; O.w += xc[gg].w * w;
+    }
   }
 #pragma unroll 4
-  for (int k = 0; k < np; ++k) {
+  for (int k = 0; k < ns; ++k) {
     const float* ml = a.sys_ml + (ubase + k) * 2 * NQ;
-    const float mk = __ldcg(ml + col), lk = __ldcg(ml + NQ + col);
-    const float4 xk = __ldcg(reinterpret_cast<const float4*>(
-                                 a.sys_acc + ((ubase + k) * NQ + col) * RB_HEAD_DIM) + lane);
-    if (mk != -INFINITY) {
+    const float mk = __ldcg(ml + col);
+    if (mk > 0.5f * kNegBig) {
+      const float lk = __ldcg(ml + NQ + col);
+      const float4 xk = __ldcg(reinterpret_cast<const float4*>(
+                                   a.sys_acc + ((ubase + k) * NQ + col) * RB_HEAD_DIM) + lane);
       const float w = fast_exp2(mk - M);
       L += lk * w;
       O.x += xk.x * w; O.y += xk.y * w; O.z += xk.z * w; O.w += xk.w * w;
@@ -378,7 +555,7 @@ __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, c
 }
 
 // Sense-reversing grid barrier over all CTAs of the launch (all resident:
-// one CTA per SM, cooperative launch).  bar[0] = arrivals, bar[1] = generation.
+// one CTA per SM).  bar[0] = arrivals, bar[1] = generation.
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nctas) {
   unsigned int gen;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
@@ -404,10 +581,9 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
                       const __grid_constant__ CUtensorMap tm_qc,
                       const __grid_constant__ CUtensorMap tm_sk,
                       const __grid_constant__ CUtensorMap tm_sv,
-                      const __grid_constant__ CUtensorMap tm_ck,
-                      const __grid_constant__ CUtensorMap tm_cv, const StepArgs a) {
+                      const __grid_constant__ CUtensorMap tm_rk,
+                      const __grid_constant__ CUtensorMap tm_rv, const StepArgs a) {
   using L = StepCfg<NQ>;
-  constexpr int H = NQ;
   constexpr int KS = L::KS, VS = L::VS, QS = L::QS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
@@ -417,27 +593,19 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
   uint64_t* v_empty = v_full + VS;
   uint64_t* q_full = v_empty + VS;
   uint64_t* q_empty = q_full + QS;
-  uint64_t* s_full = q_empty + QS;
+  uint64_t* s_full = q_empty + QS;   // [group]
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
   uint64_t* o_full = p_empty + 2;
   uint64_t* o_free = o_full + 2;
   uint64_t* meta_bar = o_free + 2;
-  // handoff softmax -> epilogue (m, l of a finished part)
-  uint64_t* h_full = meta_bar + 1;
-  uint64_t* h_empty = h_full + 2;
-  uint64_t* v_go = h_empty + 2;  // first K tile landed: V streaming may start
-  static_assert(2 * KS + 2 * VS + 2 * QS + 18 == L::kNumBars, "barrier count");
+  uint64_t* v_go = meta_bar + 1;     // first K tile landed: V streaming may start
+  static_assert(2 * KS + 2 * VS + 2 * QS + 14 == L::kNumBars, "barrier count");
   int* misc = reinterpret_cast<int*>(smem + L::kOffMisc);
   int* P = reinterpret_cast<int*>(smem + L::kOffMeta);
   int* lens = P + (a.b + 1);
   int* qs = lens + a.b;
-  float* red = reinterpret_cast<float*>(smem + L::kOffRed);
-  float* red2 = reinterpret_cast<float*>(smem + L::kOffRed2);
-  float* mu = reinterpret_cast<float*>(smem + L::kOffMu);
-  float* al = reinterpret_cast<float*>(smem + L::kOffAl);
-  float* hand = reinterpret_cast<float*>(smem + L::kOffHand);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long* dts = a.debug_ts ? a.debug_ts + blockIdx.x * 512 : nullptr;
@@ -455,8 +623,6 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       mbar_init(&p_empty[i], 1);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_free[i], 4);
-      mbar_init(&h_full[i], 1);
-      mbar_init(&h_empty[i], 4);
     }
     mbar_init(meta_bar, 1);
     mbar_init(v_go, 1);
@@ -467,19 +633,19 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     tma_prefetch_desc(&tm_sv);
   } else if (warp == 2 && lane == 1) {
     tma_prefetch_desc(&tm_qc);
-    tma_prefetch_desc(&tm_ck);
-    tma_prefetch_desc(&tm_cv);
+    tma_prefetch_desc(&tm_rk);
+    tma_prefetch_desc(&tm_rv);
   }
   if (warp == 1) tmem_alloc(reinterpret_cast<uint32_t*>(&misc[0]), L::kTmemCols);
   if (warp >= 4) {
     // V and Q rings start zeroed: rows a partial tile never loads must be
     // finite (P is 0 there, and 0 * NaN would poison O).
     const int tid = threadIdx.x - 128;
-    uint4 z = make_uint4(0, 0, 0, 0);
+    uint4 zz = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < (VS * L::kTile) / 16; i += 256)
-      reinterpret_cast<uint4*>(smem + L::kOffV)[i] = z;
+      reinterpret_cast<uint4*>(smem + L::kOffV)[i] = zz;
     for (int i = tid; i < (QS * L::kQBytes) / 16; i += 256)
-      reinterpret_cast<uint4*>(smem + L::kOffQ)[i] = z;
+      reinterpret_cast<uint4*>(smem + L::kOffQ)[i] = zz;
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -507,7 +673,9 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     const uint64_t pol = l2_policy_evict_first();
     const uint64_t pol_q = l2_policy_evict_last();
     const CUtensorMap* sysmap = is_k ? &tm_sk : &tm_sv;
-    const CUtensorMap* ctxmap = is_k ? &tm_ck : &tm_cv;
+    const CUtensorMap* ctxmap = is_k ? &tm_rk : &tm_rv;  // ragged context
+    const unsigned char* pool = is_k ? a.k_pool : a.v_pool;
+    const uint32_t blk_bytes = a.block_size * 256;
     const int NS = is_k ? KS : VS;
     uint64_t* full = is_k ? k_full : v_full;
     uint64_t* empty = is_k ? k_empty : v_empty;
@@ -521,7 +689,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     Walker wa = w;
     Tile ta;
     auto stage_ids = [&](int slot) {
-      if (wa.next(a, P, lens, qs, misc, meta_bar, ta) && ta.kind == 1 && a.paged) {
+      if (wa.next(a, P, lens, qs, misc, meta_bar, ta) && ta.kind == 1 && !ta.pre && a.paged) {
         const int nv = min(RB_KEY_TILE, lens[ta.r] - ta.kt * RB_KEY_TILE);
         if (lane < bpt && lane * a.block_size < nv)
           cp_async_4(ids + slot * 32 + lane, a.block_table +
@@ -539,18 +707,15 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
         __syncwarp();
       }
       first_tile = false;
-      if (dts && is_k && lane == 0 && j < 32) dts[360 + j] = global_timer_ns();
       // context block ids of this tile, one lane per block
       cp_async_wait_group<L::kIdAhead - 1>();
-      if (dts && is_k && lane == 0 && j < 32) dts[392 + j] = global_timer_ns();
       int blk = 0, nvalid = 0;
-      if (t.kind == 1) {
+      if (t.kind == 1 && !t.pre) {
         nvalid = min(RB_KEY_TILE, lens[t.r] - t.kt * RB_KEY_TILE);  // keys of this tile that exist
         if (a.paged) blk = ids[(j % L::kIdAhead) * 32 + lane];
       }
       __syncwarp();
       stage_ids(j % L::kIdAhead);  // slot read above is refilled for tile j + kIdAhead
-      if (dts && is_k && lane == 0 && j < 32) dts[424 + j] = global_timer_ns();
       if (is_k && t.first) {
         const int qsl = n % QS;
         if (lane == 0) {
@@ -571,29 +736,28 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
         }
         ++n;
       }
-      if (dts && is_k && lane == 0 && j < 32) dts[456 + j] = global_timer_ns();
       const int st = j % NS;
-      if (dts && is_k && lane == 0 && j < 32) dts[168 + j] = global_timer_ns();
       if (lane == 0) mbar_wait(&empty[st], ((j / NS) & 1) ^ 1);
-      if (dts && lane == 0 && j < 32) dts[(is_k ? 136 : 232) + j] = global_timer_ns();
       __syncwarp();
       uint8_t* dst = smem + ring + st * L::kTile;
-      if (t.kind == 0) {
+      if (t.kind == 0 || t.pre) {
+        // shared prefix tile (system unit, or the naive baseline's re-read)
         if (lane == 0) {
-          const int h = t.u / a.sp.n_qt;
+          const int h = t.kind == 0 ? t.u / a.sp.n_qt : t.h;
           mbar_arrive_expect_tx(&full[st], L::kTile);
           tma_load_3d(dst, sysmap, &full[st], 0, t.kt * RB_KEY_TILE, h, pol);
           tma_load_3d(dst + L::kTile / 2, sysmap, &full[st], 64, t.kt * RB_KEY_TILE, h, pol);
         }
       } else if (a.paged) {
+        // one bulk copy per (block, kv head): the pool stores each block as
+        // the [128 d][bs] swizzled UMMA operand, so the bytes land as-is
         const int nb = (nvalid + a.block_size - 1) / a.block_size;
-        if (lane == 0) mbar_arrive_expect_tx(&full[st], nb * a.block_size * 256);
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], nb * blk_bytes);
         __syncwarp();
-        if (lane < nb) {
-          const uint32_t off = lane * a.block_size * 128;
-          tma_load_4d(dst + off, ctxmap, &full[st], 0, 0, t.h, blk, pol);
-          tma_load_4d(dst + L::kTile / 2 + off, ctxmap, &full[st], 64, 0, t.h, blk, pol);
-        }
+        if (lane < nb)
+          bulk_copy_g2s(dst + lane * blk_bytes,
+                        pool + blk * a.pool_block_bytes + t.h * a.pool_head_bytes, blk_bytes,
+                        &full[st]);
       } else {
         if (lane == 0) {
           const int tok = static_cast<int>(a.req_offset[t.r]) + t.kt * RB_KEY_TILE;
@@ -609,27 +773,31 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     // ------------------------------------------------------ S^T = K . Q^T
     int j = 0, n = 0;
     constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
+    constexpr uint32_t idesc_qk_pg = make_idesc_bf16_f32(128, NQ, 1, 0);
     while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
       if (lane == 0) {
         const int qsl = n % QS;
         if (t.first) mbar_wait(&q_full[qsl], (n / QS) & 1);
-        const int st = j % KS, sb = j & 1;
+        const int st = j % KS, gb = j & 1;  // group of this tile = S buffer
         mbar_wait(&k_full[st], (j / KS) & 1);
         if (j == 0) mbar_arrive(v_go);
-        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-        if (dts && j < 32) dts[264 + j] = global_timer_ns();
+        mbar_wait(&s_empty[gb], ((j >> 1) & 1) ^ 1);
+        RB_TRACE((j < 32), 264 + j);
         tc_fence_after();
         const uint32_t k_base = smem_k + st * L::kTile;
         const uint32_t q_base = smem_q + qsl * L::kQBytes;
-        const uint32_t d_tmem = tmem_base + sb * NQ;
-#pragma unroll
+        const uint32_t d_tmem = tmem_base + gb * NQ;
+        const bool pl = t.kind == 1 && !t.pre && a.paged;  // paged block layout (K MN-major)
+#pragma unroll 1
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t koff = (kk & 3) * 32;
-          const uint64_t ad = make_smem_desc_sw128(k_base + (kk >> 2) * (L::kTile / 2) + koff, 16, 1024);
+          const uint64_t ad =
+              pl ? ctx_k_desc(k_base, kk, a.block_size)
+                 : make_smem_desc_sw128(k_base + (kk >> 2) * (L::kTile / 2) + koff, 16, 1024);
           const uint64_t bd = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + koff, 16, 1024);
-          umma_f16_ss(d_tmem, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+          umma_f16_ss(d_tmem, ad, bd, pl ? idesc_qk_pg : idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[sb]);
+        umma_commit(&s_full[gb]);
         umma_commit(&k_empty[st]);
         if (t.last) umma_commit(&q_empty[qsl]);
       }
@@ -649,7 +817,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       for (int i = lo; i < hi; ++i) {
         const int c = __ldg(a.ctx_lens + i);
         lens[i] = c;
-        sum += a.sp.hkv * ctx_nz(a, qs, i) * ((max(c, 0) + RB_KEY_TILE - 1) / RB_KEY_TILE);
+        sum += a.sp.hkv * ctx_nz(a, qs, i) * ctx_unit_tiles(a, c);
       }
       int incl = sum;
 #pragma unroll
@@ -660,7 +828,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       int run = incl - sum;
       for (int i = lo; i < hi; ++i) {
         P[i] = run;
-        run += a.sp.hkv * ctx_nz(a, qs, i) * ((max(lens[i], 0) + RB_KEY_TILE - 1) / RB_KEY_TILE);
+        run += a.sp.hkv * ctx_nz(a, qs, i) * ctx_unit_tiles(a, lens[i]);
       }
       const int Tc = __shfl_sync(0xffffffffu, incl, 31);
       if (lane == 0) P[b] = Tc;
@@ -675,7 +843,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
             const int mid = (l2 + h2 + 1) >> 1;
             if (P[mid] <= B) l2 = mid; else h2 = mid - 1;
           }
-          const int tr = (lens[l2] + RB_KEY_TILE - 1) / RB_KEY_TILE;
+          const int tr = ctx_unit_tiles(a, lens[l2]);
           const int local = static_cast<int>(B) - P[l2];
           res = P[l2] + ((local + tr - 1) / tr) * tr;
         }
@@ -685,181 +853,106 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       if (lane == 0) mbar_arrive(meta_bar);
     }
     // ------------------------------------------------ O^T += V^T . P^T
-    int j = 0, n = 0;
+    int j = 0;
+    int kp[2] = {0, 0};  // parts each group has finished (o_full / o_free phases)
     constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+    constexpr uint32_t idesc_pv_pg = make_idesc_bf16_f32(128, NQ, 0, 0);
     while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
+      const int gb = j & 1;
+      const bool gfirst = t.pidx < 2;  // the group's first tile of this part
+      const bool glast = t.rem <= 2;   // the group's last tile of this part
       if (lane == 0) {
-        const int st = j % VS, pb = j & 1, ob = n & 1;
+        const int st = j % VS;
         mbar_wait(&v_full[st], (j / VS) & 1);
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
-        if (t.first) mbar_wait(&o_free[ob], ((n >> 1) & 1) ^ 1);
-        if (dts && j < 32) dts[296 + j] = global_timer_ns();
+        mbar_wait(&p_full[gb], (j >> 1) & 1);
+        if (gfirst) mbar_wait(&o_free[gb], (kp[gb] & 1) ^ 1);
+        RB_TRACE((j < 32), 296 + j);
         tc_fence_after();
         const uint32_t v_base = smem_v + st * L::kTile;
-        const uint32_t p_base = smem_p + pb * L::kQBytes;
-        const uint32_t d_tmem = tmem_base + 2 * NQ + ob * NQ;
-#pragma unroll
+        const uint32_t p_base = smem_p + gb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + 2 * NQ + gb * NQ;
+        const bool pl = t.kind == 1 && !t.pre && a.paged;  // paged block layout (V^T K-major)
+#pragma unroll 1
         for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t ad = make_smem_desc_sw128(v_base + kk * 2048, L::kTile / 2, 1024);
+          const uint64_t ad = pl ? ctx_v_desc(v_base, kk, a.block_size)
+                                 : make_smem_desc_sw128(v_base + kk * 2048, L::kTile / 2, 1024);
           const uint64_t bd =
               make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
-          umma_f16_ss(d_tmem, ad, bd, idesc_pv, (t.first && kk == 0) ? 0u : 1u);
+          umma_f16_ss(d_tmem, ad, bd, pl ? idesc_pv_pg : idesc_pv, (gfirst && kk == 0) ? 0u : 1u);
         }
-        umma_commit(&p_empty[pb]);
+        umma_commit(&p_empty[gb]);
         umma_commit(&v_empty[st]);
-        if (t.last) umma_commit(&o_full[ob]);
+        if (glast) umma_commit(&o_full[gb]);
       }
-      if (t.last) ++n;
+      if (glast) ++kp[gb];
       ++j;
     }
     __syncwarp();
-  } else if (warp < 8) {
-    // --------------------------------------------------------- softmax
+  } else {
+    // ------------------------------------------------- softmax groups
+    const int grp = (warp - 4) >> 2;
     SmxCtx C;
     C.qd = warp & 3;                          // TMEM lane quadrant
     C.lane = lane;
     const int kl = C.qd * 32 + lane;          // key lane of the tile
-    C.red = red;
-    C.red2 = red2;
-    C.my_mu = mu + C.qd * NQ;
-    C.my_al = al + C.qd * NQ;
-    C.hand = hand;
+    C.red = reinterpret_cast<float*>(smem + L::kOffRed) + grp * 2 * 4 * NQ;
+    C.red2 = reinterpret_cast<float*>(smem + L::kOffRed2) + grp * 4 * NQ;
+    C.my_mu = reinterpret_cast<float*>(smem + L::kOffMu) + (warp - 4) * NQ;
+    C.my_al = reinterpret_cast<float*>(smem + L::kOffAl) + (warp - 4) * NQ;
 #pragma unroll
     for (int r8 = 0; r8 < 8; ++r8) C.poff[r8] = sw128_offset(r8, kl & 63);
-    C.pbase = smem + L::kOffP + (kl >> 6) * (NQ * 128);
-    C.lane_addr = tmem_base + (static_cast<uint32_t>(C.qd * 32) << 16);
-    float l_part[NQ], mr[NQ];
-    int j = 0, n = 0, small = 0;
+    C.pbase = smem + L::kOffP + grp * L::kQBytes + (kl >> 6) * (NQ * 128);
+    const uint32_t lq = static_cast<uint32_t>(C.qd * 32) << 16;
+    C.s_addr = tmem_base + lq + grp * NQ;
+    C.o_addr = tmem_base + lq + 2 * NQ + grp * NQ;
+    C.bar = 1 + grp;
+    if (a.has_ctx) mbar_wait(meta_bar, 0);  // part ends read the request metadata
+    float l_part[NQ];
+    int j = 0, kp = 0, ncol = NQ;
     while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      if (dts && threadIdx.x == 128) {
-        if (j == 0) dts[2] = global_timer_ns();
-        if (j < 32) dts[8 + j] = global_timer_ns();
+      if ((j & 1) != grp) {
+        ++j;
+        continue;
       }
+      const int k = j >> 1;  // this group's tile count
+      const bool gfirst = t.pidx < 2;
+      const bool glast = t.rem <= 2;
+      mbar_wait(&s_full[grp], k & 1);
+      if (dts && threadIdx.x == 128 && j == 0) dts[2] = global_timer_ns();
+      RB_TRACE((threadIdx.x == 128 && j < 32), 8 + j);
       tc_fence_after();
       const int key = t.kt * RB_KEY_TILE + kl;
-      if (t.kind == 0) {
-        float x[NQ];
-        tmem_ld_32x32b<NQ>(C.lane_addr + sb * NQ, x);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[sb]);
-        const bool valid = key < a.sp.s;
-#pragma unroll
-        for (int c = 0; c < NQ; ++c) x[c] = valid ? x[c] * a.scale_log2 : -INFINITY;
-        softmax_tile<NQ, NQ>(C, x, mr, l_part, t.first, j, n, p_empty, p_full, L::kQBytes);
-        if (t.last) softmax_part_end<NQ, NQ>(C, l_part, n, h_empty, h_full);
-      } else {
-        // column c (local row li = z*NQ + c, query t = li / g) sees key iff
-        // key < c_r - m_r + t + 1 (attention.py:120-121), i.e. c >= cmin, and
-        // c < cmax (the unit's rows): two compares per column, no division.
+      // Column c of the tile sees this key iff cmin <= c < cmax.
+      //   system / prefix tile: every column, key < s;
+      //   context tile: column c = local row li = z*NQ + c of request r
+      //   (query t = li / g) sees key iff key < c_r - m_r + t + 1
+      //   (attention.py:120-121), i.e. c >= cmin, and c < cmax (unit rows).
+      TileMask mk;
+      mk.cmax = NQ;
+      if (t.kind == 1) {
         const int m_r = qs[t.r + 1] - qs[t.r];
-        const int cmax = m_r * g - t.z * NQ;
-        const int cmin = (key - (lens[t.r] - m_r)) * g - t.z * NQ;
-        if (t.first) small = cmax <= 8;
-        if (small) {
-          float x[8];
-          tmem_ld_32x32b<8>(C.lane_addr + sb * NQ, x);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[sb]);
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            x[c] = (c >= cmin && c < cmax) ? x[c] * a.scale_log2 : -INFINITY;
-          softmax_tile<8, NQ>(C, x, mr, l_part, t.first, j, n, p_empty, p_full, L::kQBytes);
-          if (t.last) softmax_part_end<8, NQ>(C, l_part, n, h_empty, h_full);
-        } else {
-          float x[NQ];
-          tmem_ld_32x32b<NQ>(C.lane_addr + sb * NQ, x);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_empty[sb]);
-#pragma unroll
-          for (int c = 0; c < NQ; ++c)
-            x[c] = (c >= cmin && c < cmax) ? x[c] * a.scale_log2 : -INFINITY;
-          softmax_tile<NQ, NQ>(C, x, mr, l_part, t.first, j, n, p_empty, p_full, L::kQBytes);
-          if (t.last) softmax_part_end<NQ, NQ>(C, l_part, n, h_empty, h_full);
-        }
+        mk.cmax = m_r * g - t.z * NQ;
+        if (gfirst) ncol = mk.cmax <= 8 ? 8 : NQ;  // decode with g <= 8: one chunk
+      } else {
+        ncol = NQ;
       }
-      if (dts && threadIdx.x == 128 && j < 32) dts[328 + j] = global_timer_ns();
-      if (t.last) ++n;
+      if (t.kind == 0 || t.pre) mk.cmin = key < a.sp.s ? -1 : NQ;
+      else if (a.causal) mk.cmin = (key - (lens[t.r] - (qs[t.r + 1] - qs[t.r]))) * g - t.z * NQ;
+      else mk.cmin = key < lens[t.r] ? -1 : NQ;
+      softmax_tile<NQ>(C, l_part, ncol, gfirst, k, mk, a.scale_log2, &s_empty[grp], &p_empty[grp],
+                       &p_full[grp]);
+      if (glast)
+        softmax_part_end<NQ>(C, a, t, qs, l_part, ncol, grp, kp, &o_full[grp], &o_free[grp]);
+      RB_TRACE((threadIdx.x == 128 && j < 32), 328 + j);
+      if (glast) ++kp;
       ++j;
     }
-    if (dts && threadIdx.x == 128) dts[3] = global_timer_ns();
-  } else {
-    // -------------------------------------------------------- epilogue
-    const int tid = threadIdx.x - 256;      // 0..127
-    const int qd = warp & 3;
-    const int d = qd * 32 + lane;           // TMEM lane = head dim
-    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
-    // group bookkeeping reads the request metadata even for system parts
-    if (a.has_ctx) mbar_wait(meta_bar, 0);
-    int n = 0;
-    while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
-      if (!t.last) continue;
-      const int ob = n & 1;
-      mbar_wait(&h_full[ob], (n >> 1) & 1);
-      mbar_wait(&o_full[ob], (n >> 1) & 1);
-      if (dts && tid == 0 && n < 32) dts[40 + n] = global_timer_ns();
-      tc_fence_after();
-      float o[H];
-      tmem_ld_32x32b<H>(lane_addr + 2 * NQ + ob * NQ, o);
-      tmem_wait_ld();
-      if (dts && tid == 0 && n < 32) {
-        float acc = 0.f;
-#pragma unroll
-        for (int c = 0; c < H; ++c) acc += o[c];
-        dts[72 + n] = global_timer_ns() + (acc == 1.2345f ? 1 : 0);
-      }
-      const float* hm = hand + ob * 2 * NQ;  // this part's (m, l), freed after the writes
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[ob]);
-      if (dts && tid == 0 && n < 32) dts[200 + n] = global_timer_ns();
-      // ---- write this part's partial state
-      const rb_sys_plan& p = a.sp;
-      if (t.kind == 0) {
-        const int owner0 = rb_tile_owner(&p, static_cast<long long>(t.u) * p.tpu);
-        const long long pb = static_cast<long long>(t.u) * p.max_parts + (blockIdx.x - owner0);
-        float* pacc = a.sys_acc + pb * NQ * RB_HEAD_DIM;
-#pragma unroll
-        for (int c = 0; c < H; ++c) pacc[c * RB_HEAD_DIM + d] = o[c];
-        if (tid < NQ) {
-          a.sys_ml[pb * 2 * NQ + tid] = hm[tid];
-          a.sys_ml[pb * 2 * NQ + NQ + tid] = hm[NQ + tid];
-        }
-      } else {
-        // valid columns c < ncol: local row li = z*NQ + c -> query row
-        // qs[r] + li / g, head h*g + li % g.  Runtime loop (compact code: this
-        // runs once per context unit and must stay i-cache resident).
-        const int ncol = min((qs[t.r + 1] - qs[t.r]) * g - t.z * NQ, NQ);
-        for (int c = 0; c < ncol; ++c) {
-          float val = o[0];
-#pragma unroll
-          for (int cc = 1; cc < H; ++cc) val = (cc == c) ? o[cc] : val;
-          const int li = t.z * NQ + c;
-          const long long oi = static_cast<long long>(qs[t.r] + li / g) * p.hq + t.h * g + li % g;
-          a.ctx_acc[oi * RB_HEAD_DIM + d] = val;
-          if (d == 0) reinterpret_cast<float2*>(a.ctx_ml)[oi] = make_float2(hm[c], hm[NQ + c]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&h_empty[ob]);
-      if (dts && tid == 0 && n < 32) dts[104 + n] = global_timer_ns();
-      ++n;
-    }
-    if (dts && threadIdx.x == 256) dts[4] = global_timer_ns();
-  }
+    if (dts && (threadIdx.x == 128 || threadIdx.x == 256)) dts[3 + grp] = global_timer_ns();
 
-  if (warp >= 4) {
     // ---- every part of every CTA written: grid barrier, then each CTA merges
     // its share of the output vectors (8 warps, one vector per warp)
     named_bar_sync(3, 256);
-    if (threadIdx.x == 256) {
+    if (threadIdx.x == 128) {
       grid_barrier(reinterpret_cast<unsigned int*>(a.counters), gridDim.x);
       if (dts) dts[6] = global_timer_ns();
     }
@@ -871,6 +964,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     const long long vb = V * blockIdx.x / gridDim.x, ve = V * (blockIdx.x + 1) / gridDim.x;
     for (long long v = vb + (warp - 4); v < ve; v += 8) merge_vector<NQ>(a, qs, lens, v, lane);
   }
+
   if (dts && threadIdx.x == 0) dts[5] = global_timer_ns();
   tc_fence_before();
   __syncthreads();

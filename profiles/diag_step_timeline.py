@@ -38,7 +38,7 @@ _lib.load().rb_debug_set_timestamps(None)
 t = ts.cpu().double()
 t0 = t[:, 0].min()
 rel = torch.where(t > 0, (t - t0) / 1e3, torch.zeros_like(t))
-print(f"s={s} phases={phases}: event {e0.elapsed_time(e1) * 1e3:.1f} us, fused={relay.fused}")
+print(f"s={s} phases={phases}: event {e0.elapsed_time(e1) * 1e3:.1f} us")
 for i, n in enumerate(["entry", "prologue", "first_S", "softmax_end", "epi_end", "exit"]):
     col = sorted(rel[:, i].tolist())
     print(f"  {n:12s} min {col[0]:7.1f} p50 {col[len(col)//2]:7.1f} p90 {col[int(len(col)*.9)]:7.1f} max {col[-1]:7.1f}")

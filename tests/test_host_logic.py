@@ -18,7 +18,7 @@ from paper_2402_14808_b200.plan import SysPlan
 ])
 def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
     p = SysPlan(n_rows, hq, hkv, s, grid)
-    f, _ = _lib.sys_plan(n_rows, hq, hkv, s, grid)
+    f, _ = _lib.step_plan(n_rows, hq, hkv, s, grid)
     assert (p.nq, p.n_qt, p.tpu, p.n_units, p.total, p.grid, p.max_parts) == \
         (f["nq"], f["n_qt"], f["tpu"], f["n_units"], f["total"], f["grid"], f["max_parts"])
     ranges = p.cta_ranges()
