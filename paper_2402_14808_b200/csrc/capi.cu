@@ -315,8 +315,7 @@ int rb_relay_step(const void* q, long long q_row_stride, long long q_head_stride
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = grid_cap > 0 && grid_cap < sms ? grid_cap : sms;
-  if (grid < a.sp.grid) grid = a.sp.grid;
+  const int grid = grid_cap > 0 && grid_cap < sms ? grid_cap : sms;
   return cuda_status(rb::launch_relay_step(maps, a, grid, static_cast<cudaStream_t>(stream)),
                      "relay step launch");
 }

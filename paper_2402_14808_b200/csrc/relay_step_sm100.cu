@@ -69,7 +69,8 @@ struct StepCfg {
   static constexpr int KS = 2, VS = 3, QS = 4;
   static constexpr int kTile = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB K or V tile
   static constexpr int kQBytes = NQ * 256;                     // [2 kblocks][NQ][128 B]
-  static constexpr int kThreads = 12 * 32;
+  static constexpr int kThreads = 13 * 32;  // 12 pipeline warps + the scheduler
+  static constexpr int IQ = 8;                // work-item ring depth
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + KS * kTile;
   static constexpr int kOffQ = kOffV + VS * kTile;
@@ -79,11 +80,12 @@ struct StepCfg {
   static constexpr int kOffMu = kOffRed2 + 2 * 4 * NQ * 4;       // float [8 warps][NQ] reference max
   static constexpr int kOffAl = kOffMu + 8 * NQ * 4;             // float [8 warps][NQ] rescale
   static constexpr int kOffMisc = kOffAl + 8 * NQ * 4;           // int [16]
+  static constexpr int kOffItems = kOffMisc + 64;                // int [IQ] work-item ring
   static constexpr int kIdAhead = 4;                             // block-id lookahead (tiles)
-  static constexpr int kOffIds = kOffMisc + 64;                  // int [2 producers][kIdAhead][32]
+  static constexpr int kOffIds = kOffItems + 64;                 // int [2 producers][kIdAhead][32]
   static constexpr int kOffBar = kOffIds + 2 * kIdAhead * 32 * 4;
-  static constexpr int kNumBars = 2 * KS + 2 * VS + 2 * QS + 14;  // rings + s,p,o pairs + meta + v_go
-  static constexpr int kOffMeta = kOffBar + kNumBars * 8;  // int P[b+1], lens[b], qs[b+1]
+  static constexpr int kNumBars = 2 * KS + 2 * VS + 2 * QS + 2 * IQ + 14;  // rings + s,p,o + meta + v_go
+  static constexpr int kOffMeta = kOffBar + kNumBars * 8;  // int U[b+1], lens[b], qs[b+1]
   // TMEM per group: S and O accumulators of NQ columns each
   static constexpr int kTmemCols = (4 * NQ <= 32) ? 32 : (4 * NQ <= 64) ? 64 : 128;
   static int smem_bytes(int b) { return kOffMeta + 4 * (3 * b + 2) + 16; }
@@ -111,100 +113,94 @@ __device__ __forceinline__ int ctx_unit_tiles(const StepArgs& a, int c_r) {
   return a.prefix_tiles + (max(c_r, 0) + RB_KEY_TILE - 1) / RB_KEY_TILE;
 }
 
-// Walks a CTA's sequence: system tiles [xs, xe) then context tiles [cx, ce).
-// Incremental (no division per tile): every role warp runs its own copy.
+// Work items of a CTA: first its static stream-K share of the system tiles
+// (item u = the part of system unit u inside the CTA's tile range, rb_plan.h),
+// then context units handed out dynamically (item n_units + v = context unit
+// v in (request, kv head, q-tile) order, decoded through the per-request unit
+// prefix U).  The scheduler warp publishes item ids in a ring every role reads
+// in the same order; a CTA whose system share ran fast simply takes more of
+// the small context units, so the step ends without a tail imbalance.
+
+// Walks this CTA's items tile by tile.  Every role warp (all lanes) runs its
+// own copy; lane 0 frees a ring slot once the warp has read it.
+template <int IQ>
 struct Walker {
-  long long xb, xs, xe;    // system range begin / cursor / end
-  int su, skt;             // current system unit / key tile
-  int cx, ce;              // context tile cursor / end (global context tile index)
-  int r, h, z, kt;         // current context unit (request, kv head, q-tile) and tile
-  int tr, nz;              // tiles per unit / q-tiles of request r
-  int ctx_ready;
+  int qi;              // items read from the ring
+  int kind;            // current item: -1 none, 0 system part, 1 context unit
+  int item;            // its id
+  int u, kb, ke;       // system part: unit, key tile range [kb, ke)
+  int r, h, z, tr;     // context unit: request, kv head, q-tile, tiles
+  int kt;              // cursor inside the item
+  long long xb, xe;    // this CTA's system tile range (stream-K)
   __device__ __forceinline__ void init(const StepArgs& a, int cta) {
-    xb = xs = xe = 0;
-    su = skt = 0;
+    qi = 0;
+    kind = -1;
+    kt = ke = tr = 0;
+    xb = xe = 0;
     if (a.has_sys && cta < a.sp.grid) {
-      xb = xs = rb_cta_begin(&a.sp, cta);
+      xb = rb_cta_begin(&a.sp, cta);
       xe = rb_cta_begin(&a.sp, cta + 1);
-      su = static_cast<int>(xs / a.sp.tpu);
-      skt = static_cast<int>(xs % a.sp.tpu);
     }
-    cx = ce = r = h = z = kt = tr = nz = 0;
-    ctx_ready = 0;
   }
-  // first context tile: locate (request, unit, tile) of cx once
-  __device__ __forceinline__ void locate(const StepArgs& a, const int* P, const int* lens,
-                                         const int* qs, const int* misc, uint64_t* meta_bar) {
-    mbar_wait(meta_bar, 0);
-    cx = misc[2];
-    ce = misc[3];
-    ctx_ready = 1;
-    if (cx >= ce) return;
-    r = 0;
-    while (P[r + 1] <= cx) ++r;
-    tr = ctx_unit_tiles(a, lens[r]);
-    nz = ctx_nz(a, qs, r);
-    const int local = cx - P[r];
-    const int ui = local / tr;
-    kt = local % tr;
-    h = ui / nz;
-    z = ui % nz;
-  }
-  __device__ __forceinline__ bool next(const StepArgs& a, const int* P, const int* lens,
-                                       const int* qs, const int* misc, uint64_t* meta_bar,
-                                       Tile& t) {
-    if (xs < xe) {
-      const long long ub = static_cast<long long>(su) * a.sp.tpu;
-      const long long pb = ub > xb ? ub : xb;
-      const long long pe = ub + a.sp.tpu < xe ? ub + a.sp.tpu : xe;
-      t.kind = 0;
-      t.u = su;
-      t.kt = skt;
-      t.pidx = static_cast<int>(xs - pb);
-      t.rem = static_cast<int>(pe - xs);
-      t.first = t.pidx == 0;
-      t.last = t.rem == 1;
+  __device__ __forceinline__ bool next(const StepArgs& a, const int* U, const int* lens,
+                                       const int* qs, const int* itq, uint64_t* itq_full,
+                                       uint64_t* itq_empty, int lane, Tile& t) {
+    if (kind < 0 || (kind == 0 && kt >= ke) || (kind == 1 && kt >= tr)) {
+      const int slot = qi % IQ;
+      mbar_wait(&itq_full[slot], (qi / IQ) & 1);
+      item = itq[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&itq_empty[slot]);
+      ++qi;
+      const int n_sc = a.has_sys ? a.sp.n_units : 0;
+      if (item < n_sc) {
+        const long long ub = static_cast<long long>(item) * a.sp.tpu;
+        kind = 0;
+        u = item;
+        kb = static_cast<int>((xb > ub ? xb : ub) - ub);
+        ke = static_cast<int>((xe < ub + a.sp.tpu ? xe : ub + a.sp.tpu) - ub);
+        kt = kb;
+      } else if (a.has_ctx && item - n_sc < U[a.b]) {
+        const int v = item - n_sc;
+        int lo = 0, hi = a.b - 1;  // request r: U[r] <= v < U[r+1]
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (U[mid] <= v) lo = mid; else hi = mid - 1;
+        }
+        r = lo;
+        const int nz = ctx_nz(a, qs, r);
+        h = (v - U[r]) / nz;
+        z = (v - U[r]) % nz;
+        tr = ctx_unit_tiles(a, lens[r]);
+        kind = 1;
+        kt = 0;
+      } else {
+        kind = 2;  // sentinel: no more work
+        kt = ke = tr = 0;
+        return false;
+      }
+    }
+    t.kind = kind;
+    if (kind == 0) {
+      t.u = u;
+      t.kt = kt;
+      t.pidx = kt - kb;
+      t.rem = ke - kt;
       t.r = t.h = t.z = 0;
       t.pre = 0;
-      ++xs;
-      if (++skt == a.sp.tpu) {
-        skt = 0;
-        ++su;
-      }
-      return true;
+    } else {
+      t.u = 0;
+      t.r = r;
+      t.h = h;
+      t.z = z;
+      t.pre = kt < a.prefix_tiles;
+      t.kt = t.pre ? kt : kt - a.prefix_tiles;
+      t.pidx = kt;
+      t.rem = tr - kt;
     }
-    if (!a.has_ctx) return false;
-    if (!ctx_ready) locate(a, P, lens, qs, misc, meta_bar);
-    if (cx >= ce) return false;
-    t.kind = 1;
-    t.u = 0;
-    t.r = r;
-    t.h = h;
-    t.z = z;
-    t.pre = kt < a.prefix_tiles;
-    t.kt = t.pre ? kt : kt - a.prefix_tiles;
-    t.pidx = kt;
-    t.rem = tr - kt;
-    t.first = kt == 0;
-    t.last = kt == tr - 1;
-    ++cx;
-    if (++kt == tr) {
-      kt = 0;
-      if (++z == nz) {
-        z = 0;
-        if (++h == a.sp.hkv) {
-          h = 0;
-          // next request with context units (P[r+1] > P[r])
-          do {
-            ++r;
-          } while (r < a.b && P[r + 1] == P[r]);
-          if (r < a.b) {
-            tr = ctx_unit_tiles(a, lens[r]);
-            nz = ctx_nz(a, qs, r);
-          }
-        }
-      }
-    }
+    t.first = t.pidx == 0;
+    t.last = t.rem == 1;
+    ++kt;
     return true;
   }
 };
@@ -345,7 +341,7 @@ template <int NQ>
 __device__ __forceinline__ void softmax_tile(const SmxCtx& C, float (&l_part)[NQ], int ncol,
                                              bool first, int k, const TileMask& mk, float scale,
                                              uint64_t* s_empty, uint64_t* p_empty,
-                                             uint64_t* p_full) {
+                                             uint64_t* p_full, unsigned long long* dts, int j) {
   if (first) {
     __syncwarp();
     if (C.lane < NQ) C.my_mu[C.lane] = kNegBig;
@@ -364,14 +360,19 @@ __device__ __forceinline__ void softmax_tile(const SmxCtx& C, float (&l_part)[NQ
           (y[3] > m0.w + kTau) | (y[4] > m1.x + kTau) | (y[5] > m1.y + kTau) |
           (y[6] > m1.z + kTau) | (y[7] > m1.w + kTau);
   }
-  if (bar_red_or(C.bar, 128, ex)) {
+  RB_TRACE((threadIdx.x == 128 && j < 32), 360 + j);
+  const bool any_ex = bar_red_or(C.bar, 128, ex);
+  RB_TRACE((threadIdx.x == 128 && j < 32), 392 + j);
+  if (any_ex) {
     const bool resc = softmax_rare(C, ncol, NQ, first, mk, scale, k, p_empty);
     if (resc) {
 #pragma unroll
       for (int c = 0; c < NQ; ++c) l_part[c] *= C.my_al[c];
     }
   }
+  RB_TRACE((threadIdx.x == 128 && j < 32), 424 + j);
   mbar_wait(p_empty, (k & 1) ^ 1);  // this group's previous P.V has read P
+  RB_TRACE((threadIdx.x == 128 && j < 32), 456 + j);
 #pragma unroll
   for (int c0 = 0; c0 < NQ; c0 += 8) {
     if (c0 < ncol) {
@@ -408,7 +409,7 @@ template <int NQ>
 __device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs& a, const Tile& t,
                                                  const int* qs, const float (&l_part)[NQ],
                                                  int ncol, int grp, int kp, uint64_t* o_full,
-                                                 uint64_t* o_free) {
+                                                 uint64_t* o_free, unsigned long long* dts, int j) {
   // row sums: per chunk of 8 columns a warp reduce-scatter, then the 4
   // quadrants through smem
 #pragma unroll
@@ -421,9 +422,12 @@ __device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs
       if (reduced_writer<8>(C.lane)) C.red2[C.qd * NQ + c0 + reduced_col<8>(C.lane)] = ws;
     }
   }
+  RB_TRACE((threadIdx.x == 128 && j < 32), 136 + j);
   named_bar_sync(C.bar, 128);
+  RB_TRACE((threadIdx.x == 128 && j < 32), 168 + j);
   const int d = C.qd * 32 + C.lane;  // TMEM lane of O = head dim
   mbar_wait(o_full, kp & 1);
+  RB_TRACE((threadIdx.x == 128 && j < 32), 200 + j);
   tc_fence_after();
   const rb_sys_plan& p = a.sp;
   const bool single = t.pidx == 0 && t.rem == 1;
@@ -431,6 +435,10 @@ __device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs
   const long long nv = static_cast<long long>(p.n_rows) * p.hq;
   const int g = p.g;
   int nrow = ncol;  // columns with a real query row
+  // the group's tiles of a part are those with pidx of this parity: its
+  // partial goes to slot `half`, whichever group (and CTA) processed it, so
+  // the merge order is independent of the dynamic schedule (deterministic)
+  const int half = t.pidx & 1;
   if (t.kind == 0) {
     const int owner0 = rb_tile_owner(&p, static_cast<long long>(t.u) * p.tpu);
     s0 = static_cast<long long>(t.u) * 2 * p.max_parts + 2 * (blockIdx.x - owner0);
@@ -447,22 +455,21 @@ __device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs
       const int c = c0 + e;
       const float lsum = C.red2[c] + C.red2[NQ + c] + C.red2[2 * NQ + c] + C.red2[3 * NQ + c];
       if (t.kind == 0) {
-        const long long pb = s0 + grp;
+        const long long pb = s0 + half;
         a.sys_acc[(pb * NQ + c) * RB_HEAD_DIM + d] = o[e];
         if (d == 0) {
           a.sys_ml[pb * 2 * NQ + c] = C.my_mu[c];
           a.sys_ml[pb * 2 * NQ + NQ + c] = lsum;
-          if (single) a.sys_ml[(s0 + (grp ^ 1)) * 2 * NQ + c] = kNegBig;
+          if (single) a.sys_ml[(s0 + 1) * 2 * NQ + c] = kNegBig;
         }
       } else if (c < nrow) {
         // local row li = z*NQ + c -> query row qs[r] + li / g, head h*g + li % g
         const int li = t.z * NQ + c;
         const long long oi = static_cast<long long>(qs[t.r] + li / g) * p.hq + t.h * g + li % g;
-        a.ctx_acc[(grp * nv + oi) * RB_HEAD_DIM + d] = o[e];
+        a.ctx_acc[(half * nv + oi) * RB_HEAD_DIM + d] = o[e];
         if (d == 0) {
-          reinterpret_cast<float2*>(a.ctx_ml)[grp * nv + oi] = make_float2(C.my_mu[c], lsum);
-          if (single)
-            reinterpret_cast<float2*>(a.ctx_ml)[(grp ^ 1) * nv + oi] = make_float2(kNegBig, 0.f);
+          reinterpret_cast<float2*>(a.ctx_ml)[half * nv + oi] = make_float2(C.my_mu[c], lsum);
+          if (single) reinterpret_cast<float2*>(a.ctx_ml)[nv + oi] = make_float2(kNegBig, 0.f);
         }
       }
     }
@@ -476,8 +483,12 @@ __device__ __forceinline__ void softmax_part_end(const SmxCtx& C, const StepArgs
 // = LSE-weighted combine of its two context partials (if the request has a
 // context) and the system stream-K slots of its group u = (hh / g, f / NQ),
 // in a fixed order (context, then slots): the relay fusion of
-// attention.py:137-157 with max-subtracted weights.  One warp per vector,
-// lane = 4 head dims.  Empty partials (m = kNegBig) are skipped.
+// attention.py:137-157 with max-subtracted weights.  One warp per vector
+// (4 head dims per lane); all loads of a vector are issued in one round (up
+// to kMergeSlots system slots in registers, more in a second loop).  Empty
+// partials (m = kNegBig) are skipped.
+constexpr int kMergeSlots = 8;
+
 template <int NQ>
 __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, const int* lens,
                                              long long v, int lane) {
@@ -498,47 +509,56 @@ __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, c
   }
   const long long nv = static_cast<long long>(p.n_rows) * p.hq;
   const long long ubase = static_cast<long long>(u) * 2 * p.max_parts;
-  // pass 1: the common max
-  float mc[2] = {kNegBig, kNegBig}, lc[2] = {0.f, 0.f};
+  // ---- one round of loads (lane = 4 head dims)
+  float2 mlc[2];
   float4 xc[2];
 #pragma unroll
   for (int gg = 0; gg < 2; ++gg) {
+    mlc[gg] = make_float2(kNegBig, 0.f);
     xc[gg] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (hasc) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ctx_ml) + gg * nv + v);
-      mc[gg] = ml.x;
-      lc[gg] = ml.y;
-      if (ml.x > 0.5f * kNegBig)
-        xc[gg] = __ldcg(reinterpret_cast<const float4*>(a.ctx_acc + (gg * nv + v) * RB_HEAD_DIM) +
-                        lane);
+      mlc[gg] = __ldcg(reinterpret_cast<const float2*>(a.ctx_ml) + gg * nv + v);
+      xc[gg] = __ldcg(reinterpret_cast<const float4*>(a.ctx_acc + (gg * nv + v) * RB_HEAD_DIM) + lane);
     }
   }
-  float M = fmaxf(mc[0], mc[1]);
-#pragma unroll 4
-  for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(a.sys_ml + (ubase + k) * 2 * NQ + col));
-  // pass 2: weighted sums in fixed order (context, then slots)
+  float ms[kMergeSlots], ls[kMergeSlots];
+  float4 xs[kMergeSlots];
+#pragma unroll
+  for (int k = 0; k < kMergeSlots; ++k) {
+    ms[k] = kNegBig;
+    ls[k] = 0.f;
+    xs[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < ns) {
+      const float* ml = a.sys_ml + (ubase + k) * 2 * NQ;
+      ms[k] = __ldcg(ml + col);
+      ls[k] = __ldcg(ml + NQ + col);
+      xs[k] = __ldcg(reinterpret_cast<const float4*>(
+                         a.sys_acc + ((ubase + k) * NQ + col) * RB_HEAD_DIM) + lane);
+    }
+  }
+  float M = fmaxf(mlc[0].x, mlc[1].x);
+#pragma unroll
+  for (int k = 0; k < kMergeSlots; ++k) M = fmaxf(M, ms[k]);
+  for (int k = kMergeSlots; k < ns; ++k) M = fmaxf(M, __ldcg(a.sys_ml + (ubase + k) * 2 * NQ + col));
+  // ---- weighted sums in fixed order (context, then slots)
   float L = 0.f;
   float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto add = [&](float m, float l, const float4& x) {
+    if (m > 0.5f * kNegBig) {
+      const float w = fast_exp2(m - M);
+      L += l * w;
+      O.x += x.x * w; O.y += x.y * w; O.z += x.z * w; O.w += x.w * w;
+    }
+  };
 #pragma unroll
-  for (int gg = 0; gg < 2; ++gg) {
-    if (mc[gg] > 0.5f * kNegBig) {
-      const float w = fast_exp2(mc[gg] - M);
-      L += lc[gg] * w;
-      O.x += xc[gg].x * w; O.y += xc[gg].y * w; O.z += xc[gg].z * w; O.w += xc[gg].w * w;
-    }
-  }
-#pragma unroll 4
-  for (int k = 0; k < ns; ++k) {
+  for (int gg = 0; gg < 2; ++gg) add(mlc[gg].x, mlc[gg].y, xc[gg]);
+#pragma unroll
+  for (int k = 0; k < kMergeSlots; ++k) add(ms[k], ls[k], xs[k]);
+  for (int k = kMergeSlots; k < ns; ++k) {
     const float* ml = a.sys_ml + (ubase + k) * 2 * NQ;
-    const float mk = __ldcg(ml + col);
-    if (mk > 0.5f * kNegBig) {
-      const float lk = __ldcg(ml + NQ + col);
-      const float4 xk = __ldcg(reinterpret_cast<const float4*>(
-                                   a.sys_acc + ((ubase + k) * NQ + col) * RB_HEAD_DIM) + lane);
-      const float w = fast_exp2(mk - M);
-      L += lk * w;
-      O.x += xk.x * w; O.y += xk.y * w; O.z += xk.z * w; O.w += xk.w * w;
-    }
+    add(__ldcg(ml + col), __ldcg(ml + NQ + col),
+        __ldcg(reinterpret_cast<const float4*>(a.sys_acc + ((ubase + k) * NQ + col) * RB_HEAD_DIM) +
+               lane));
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   O.x *= inv; O.y *= inv; O.z *= inv; O.w *= inv;
@@ -555,7 +575,8 @@ __device__ __forceinline__ void merge_vector(const StepArgs& a, const int* qs, c
 }
 
 // Sense-reversing grid barrier over all CTAs of the launch (all resident:
-// one CTA per SM).  bar[0] = arrivals, bar[1] = generation.
+// one CTA per SM).  bar[0] = arrivals, bar[1] = generation; the last arriver
+// also re-arms the scheduler's item counters bar[2], bar[3].
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nctas) {
   unsigned int gen;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
@@ -563,6 +584,8 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nct
   const unsigned int prev = atomicAdd(bar, 1u);
   if (prev == nctas - 1) {
     bar[0] = 0;
+    bar[2] = 0;  // work-item counters of the scheduler: every CTA is done grabbing
+    bar[3] = 0;
     fence_acq_rel_gpu();
     atomicAdd(bar + 1, 1u);
   } else {
@@ -601,15 +624,26 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
   uint64_t* o_free = o_full + 2;
   uint64_t* meta_bar = o_free + 2;
   uint64_t* v_go = meta_bar + 1;     // first K tile landed: V streaming may start
-  static_assert(2 * KS + 2 * VS + 2 * QS + 14 == L::kNumBars, "barrier count");
+  uint64_t* itq_full = v_go + 1;     // work-item ring
+  uint64_t* itq_empty = itq_full + L::IQ;
+  static_assert(2 * KS + 2 * VS + 2 * QS + 2 * L::IQ + 14 == L::kNumBars, "barrier count");
+  // readers of every ring slot: K and V producers (main + lookahead walkers),
+  // QK and PV issuers, the 8 softmax warps
+  constexpr int kItemReaders = 14;
   int* misc = reinterpret_cast<int*>(smem + L::kOffMisc);
-  int* P = reinterpret_cast<int*>(smem + L::kOffMeta);
-  int* lens = P + (a.b + 1);
+  int* itq = reinterpret_cast<int*>(smem + L::kOffItems);
+  int* U = reinterpret_cast<int*>(smem + L::kOffMeta);  // context units before request r
+  int* lens = U + (a.b + 1);
   int* qs = lens + a.b;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long* dts = a.debug_ts ? a.debug_ts + blockIdx.x * 512 : nullptr;
-  if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
+  if (dts && threadIdx.x == 0) {
+    dts[0] = global_timer_ns();
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    dts[480] = smid;
+  }
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
@@ -626,6 +660,10 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     }
     mbar_init(meta_bar, 1);
     mbar_init(v_go, 1);
+    for (int i = 0; i < L::IQ; ++i) {
+      mbar_init(&itq_full[i], 1);
+      mbar_init(&itq_empty[i], kItemReaders);
+    }
     fence_mbar_init();
   } else if (warp == 0 && lane == 1) {
     tma_prefetch_desc(&tm_qs);
@@ -637,7 +675,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     tma_prefetch_desc(&tm_rv);
   }
   if (warp == 1) tmem_alloc(reinterpret_cast<uint32_t*>(&misc[0]), L::kTmemCols);
-  if (warp >= 4) {
+  if (warp >= 4 && warp < 12) {
     // V and Q rings start zeroed: rows a partial tile never loads must be
     // finite (P is 0 there, and 0 * NaN would poison O).
     const int tid = threadIdx.x - 128;
@@ -663,9 +701,10 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
   const int g = a.sp.g;
   const int bpt = a.paged ? RB_KEY_TILE / a.block_size : 1;  // blocks per context tile
 
-  Walker w;
+  Walker<L::IQ> w;
   w.init(a, blockIdx.x);
   Tile t;
+#define RB_NEXT(W, T) W.next(a, U, lens, qs, itq, itq_full, itq_empty, lane, T)
 
   if (warp == 0 || warp == 2) {
     // ------------------------------------------------ TMA producers (K+Q / V)
@@ -686,10 +725,10 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     // cp.async (one lane per block) so no block-table round trip sits on the
     // issue path: a walker copy runs ahead, one commit group per tile.
     int* ids = reinterpret_cast<int*>(smem + L::kOffIds) + (is_k ? 0 : L::kIdAhead * 32);
-    Walker wa = w;
+    Walker<L::IQ> wa = w;
     Tile ta;
     auto stage_ids = [&](int slot) {
-      if (wa.next(a, P, lens, qs, misc, meta_bar, ta) && ta.kind == 1 && !ta.pre && a.paged) {
+      if (RB_NEXT(wa, ta) && ta.kind == 1 && !ta.pre && a.paged) {
         const int nv = min(RB_KEY_TILE, lens[ta.r] - ta.kt * RB_KEY_TILE);
         if (lane < bpt && lane * a.block_size < nv)
           cp_async_4(ids + slot * 32 + lane, a.block_table +
@@ -699,7 +738,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     };
 #pragma unroll 1
     for (int k = 0; k < L::kIdAhead; ++k) stage_ids(k);
-    while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
+    while (RB_NEXT(w, t)) {
       if (!is_k && first_tile) {
         // K first at start-up: every SM fires its rings at once and the first
         // Q.K^T must not queue behind the V tiles.
@@ -774,7 +813,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     int j = 0, n = 0;
     constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
     constexpr uint32_t idesc_qk_pg = make_idesc_bf16_f32(128, NQ, 1, 0);
-    while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
+    while (RB_NEXT(w, t)) {
       if (lane == 0) {
         const int qsl = n % QS;
         if (t.first) mbar_wait(&q_full[qsl], (n / QS) & 1);
@@ -806,7 +845,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 3) {
-    // -------------------------------- metadata: context tile prefix + range
+    // -------------------------------- metadata: context unit prefix U
     if (a.has_ctx) {
       const int b = a.b;
       for (int i = lane; i <= b; i += 32) qs[i] = __ldg(a.q_start + i);
@@ -817,7 +856,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       for (int i = lo; i < hi; ++i) {
         const int c = __ldg(a.ctx_lens + i);
         lens[i] = c;
-        sum += a.sp.hkv * ctx_nz(a, qs, i) * ctx_unit_tiles(a, c);
+        sum += a.sp.hkv * ctx_nz(a, qs, i);  // units of request i (none without queries)
       }
       int incl = sum;
 #pragma unroll
@@ -827,28 +866,11 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       }
       int run = incl - sum;
       for (int i = lo; i < hi; ++i) {
-        P[i] = run;
-        run += a.sp.hkv * ctx_nz(a, qs, i) * ctx_unit_tiles(a, lens[i]);
+        U[i] = run;
+        run += a.sp.hkv * ctx_nz(a, qs, i);
       }
-      const int Tc = __shfl_sync(0xffffffffu, incl, 31);
-      if (lane == 0) P[b] = Tc;
-      __syncwarp();
-      if (lane < 2) {
-        // range boundary of CTA (blockIdx.x + lane), moved to a unit start
-        const long long B = static_cast<long long>(blockIdx.x + lane) * Tc / gridDim.x;
-        int res = Tc;
-        if (B < Tc) {
-          int l2 = 0, h2 = b - 1;
-          while (l2 < h2) {
-            const int mid = (l2 + h2 + 1) >> 1;
-            if (P[mid] <= B) l2 = mid; else h2 = mid - 1;
-          }
-          const int tr = ctx_unit_tiles(a, lens[l2]);
-          const int local = static_cast<int>(B) - P[l2];
-          res = P[l2] + ((local + tr - 1) / tr) * tr;
-        }
-        misc[2 + lane] = res;
-      }
+      if (lane == 0) U[b] = __shfl_sync(0xffffffffu, incl, 31);
+      else __shfl_sync(0xffffffffu, incl, 31);
       __syncwarp();
       if (lane == 0) mbar_arrive(meta_bar);
     }
@@ -857,7 +879,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     int kp[2] = {0, 0};  // parts each group has finished (o_full / o_free phases)
     constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
     constexpr uint32_t idesc_pv_pg = make_idesc_bf16_f32(128, NQ, 0, 0);
-    while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
+    while (RB_NEXT(w, t)) {
       const int gb = j & 1;
       const bool gfirst = t.pidx < 2;  // the group's first tile of this part
       const bool glast = t.rem <= 2;   // the group's last tile of this part
@@ -888,6 +910,40 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       ++j;
     }
     __syncwarp();
+  } else if (warp == 12) {
+    // ----------------------------------------------------------- scheduler
+    // publishes this CTA's system parts (static stream-K share), then grabs
+    // context units two at a time from the global counter; a sentinel ends
+    // the walk
+    if (lane == 0) {
+      unsigned int* ctr = reinterpret_cast<unsigned int*>(a.counters);
+      const int n_sc = a.has_sys ? a.sp.n_units : 0;
+      int qi = 0;
+      auto push = [&](int item) {
+        const int slot = qi % L::IQ;
+        mbar_wait(&itq_empty[slot], ((qi / L::IQ) & 1) ^ 1);
+        itq[slot] = item;
+        mbar_arrive(&itq_full[slot]);
+        ++qi;
+      };
+      if (w.xe > w.xb) {
+        const int u0 = static_cast<int>(w.xb / a.sp.tpu);
+        const int u1 = static_cast<int>((w.xe - 1) / a.sp.tpu);
+        for (int u = u0; u <= u1; ++u) push(u);
+      }
+      // the context unit count needs the metadata (ready long before the
+      // system share has been streamed)
+      if (a.has_ctx) mbar_wait(meta_bar, 0);
+      const int n_cu = a.has_ctx ? U[a.b] : 0;
+      while (n_cu > 0) {
+        const int i = static_cast<int>(atomicAdd(ctr + 3, 2u));
+        if (i >= n_cu) break;
+        push(n_sc + i);
+        if (i + 1 < n_cu) push(n_sc + i + 1);
+      }
+      push(n_sc + n_cu);  // sentinel
+    }
+    __syncwarp();
   } else {
     // ------------------------------------------------- softmax groups
     const int grp = (warp - 4) >> 2;
@@ -909,7 +965,7 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
     if (a.has_ctx) mbar_wait(meta_bar, 0);  // part ends read the request metadata
     float l_part[NQ];
     int j = 0, kp = 0, ncol = NQ;
-    while (w.next(a, P, lens, qs, misc, meta_bar, t)) {
+    while (RB_NEXT(w, t)) {
       if ((j & 1) != grp) {
         ++j;
         continue;
@@ -940,9 +996,11 @@ __global__ void __launch_bounds__(StepCfg<NQ>::kThreads, 1)
       else if (a.causal) mk.cmin = (key - (lens[t.r] - (qs[t.r + 1] - qs[t.r]))) * g - t.z * NQ;
       else mk.cmin = key < lens[t.r] ? -1 : NQ;
       softmax_tile<NQ>(C, l_part, ncol, gfirst, k, mk, a.scale_log2, &s_empty[grp], &p_empty[grp],
-                       &p_full[grp]);
+                       &p_full[grp], dts, j);
+      RB_TRACE((threadIdx.x == 128 && j < 32), 40 + j);
       if (glast)
-        softmax_part_end<NQ>(C, a, t, qs, l_part, ncol, grp, kp, &o_full[grp], &o_free[grp]);
+        softmax_part_end<NQ>(C, a, t, qs, l_part, ncol, grp, kp, &o_full[grp], &o_free[grp], dts,
+                             j);
       RB_TRACE((threadIdx.x == 128 && j < 32), 328 + j);
       if (glast) ++kp;
       ++j;

@@ -35,6 +35,14 @@ def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
         assert len(owners) == p.unit_parts(u) <= p.max_parts
 
 
+def test_context_unit_prefix():
+    from paper_2402_14808_b200.plan import context_units
+    assert context_units([1, 1, 1], 1, 52, 32) == [0, 52, 104, 156]
+    assert context_units([6, 1], 4, 2, 32) == [0, 2, 4]       # 24 rows -> one q-tile
+    assert context_units([9, 1], 4, 2, 32) == [0, 4, 6]       # 36 rows -> two q-tiles
+    assert context_units([0, 3], 8, 1, 16) == [0, 0, 2]
+
+
 def test_head_ranges():
     assert [b - a for a, b in sharding.head_ranges(52, 8)] == [7, 7, 7, 7, 6, 6, 6, 6]
     assert [b - a for a, b in sharding.head_ranges(52, 4)] == [13] * 4
