@@ -184,8 +184,8 @@ def build(torch, s, heads, device, seed=1234):
         g.manual_seed(seed * 1000003 + hg)
         sk[i] = torch.randn((s, D), generator=g, device=device)
         sv[i] = torch.randn((s, D), generator=g, device=device)
-        paged.k_pool[0, :, i] = torch.randn((nblk, D, BLOCK), generator=g, device=device)
-        paged.v_pool[0, :, i] = torch.randn((nblk, D, BLOCK), generator=g, device=device)
+        paged.k_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
+        paged.v_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
         q[:, i] = torch.randn((B, D), generator=g, device=device)
     # shuffled physical blocks, as a real paged allocator would hand out
     perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(seed)).tolist()

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 3
+#define RB_ABI_VERSION 1
 
 enum {
   RB_OK = 0,
@@ -52,64 +52,27 @@ int rb_abi_version(void);
 int rb_device_sm_count(int device, int* out);
 
 /*
- * Work plan of the relay step's system tiles (stream-K over kv head x query
+ * Work plan of rb_system_attention (stream-K split over kv head x query
  * tile x 128-key tile; paper_2402_14808_b200/csrc/rb_plan.h).  fields[7] =
  * {nq, n_qtiles, tiles_per_unit, n_units, total_tiles, grid, max_parts};
- * *workspace_bytes = the workspace every attention entry point below needs for
- * this shape (ZERO-FILLED once before first use; the kernel leaves its grid
- * barrier in the zero state, so the buffer is reusable).  s = 0: no shared
- * prefix (context-only launches).
+ * *workspace_bytes = bytes rb_system_attention needs (zero-filled before the
+ * first use; the kernel leaves its semaphores zeroed).
  */
-int rb_step_plan_query(int n_rows, int hq, int hkv, int s, int grid_cap, long long* fields,
-                       size_t* workspace_bytes);
-
-/* 1 when the relay step supports the shape: hq/hkv divides the query tile
- * (g in 1,2,4,8,16), b small enough for the per-CTA request metadata, and a
- * paged block size of 16, 32 or 64 tokens. */
-int rb_relay_step_supported(int n_rows, int hq, int hkv, int b, int block_size, int paged);
+int rb_sys_plan_query(int n_rows, int hq, int hkv, int s, int grid_cap, long long* fields,
+                      size_t* workspace_bytes);
 
 /*
- * The relay decode step as ONE persistent kernel (relay_step_sm100.cu) --
- * `relay_attention_ragged` (attention.py:203-243): system tiles (stream-K over
- * the shared prefix, read once) and context tiles (whole (request, kv head)
- * units) run through one TMA + tcgen05 pipeline; after a grid barrier every
- * CTA merges its share of the outputs: context partial + system parts, the
- * relay fusion (attention.py:137-157).  Writes `out` ([n_rows][hq][128], fp32
- * when out_fp32 else bf16) and the fused natural-log LSE ([n_rows][hq]).
- *
- * q: bf16 row t, head h at q + t*q_row_stride + h*q_head_stride; q_start[b+1]
- *   flat row offsets (m_r = q_start[r+1] - q_start[r]); max_rows = max m_r * g.
- * sys_k/sys_v: bf16 shared prefix, token i of kv head h at i*sys_stride_tok +
- *   h*sys_stride_head (the reference's (s, h, d) or SystemKvCache (h, s, d)).
- * context, paged (block_table != NULL): k/v are one layer's PagedKvCache pool,
- *   block i of kv head h at (i*stride_block + h*stride_head) elements, each
- *   block a [128 d][block_size] operand with the UMMA swizzle applied
- *   (kvcache.py documents the layout; rb_kv_append writes it); ctx_extent =
- *   number of blocks; block_table int32 [b][bt_stride].
- * context, ragged (req_offset != NULL): token i of kv head h at
- *   i*stride_tok + h*stride_head; request r starts at token req_offset[r];
- *   ctx_extent = number of tokens.
- * ctx_lens int32 [b] (context INCLUDING the current tokens); causal: query
- *   row t of request r sees keys < c_r - m_r + t + 1 (attention.py:120-121).
- * prefix_mode 1: no system units; every context unit first re-reads the
- *   prefix (the per-request baseline, attention.py:266-296 / vLLM-PS).
- * phases: 3 = full step; 1 / 2 = system / context tiles only (profiling; the
- *   output is then that segment's own attention).
- */
-int rb_relay_step(const void* q, long long q_row_stride, long long q_head_stride,
-                  const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
-                  const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
-                  long long sys_stride_head, const void* k, const void* v, long long ctx_extent,
-                  const int* block_table, int bt_stride, int block_size,
-                  const long long* req_offset, long long stride_block, long long stride_tok,
-                  long long stride_head, const int* ctx_lens, int causal, int prefix_mode,
-                  float scale, int grid_cap, void* out, int out_fp32, float* lse_out,
-                  void* workspace, size_t workspace_bytes, int phases, void* stream);
-
-/*
- * `_system_attention` (attention.py:177-200): every query row against the
- * shared prefix, unmasked -> o_sys fp32 [n_rows][hq][128] (normalised) and
- * natural-log lse_sys [n_rows][hq].  = rb_relay_step with phases 1.
+ * System-prompt attention: every flattened query row (all requests' new
+ * tokens) against the shared prefix K/V, unmasked, with LSE.
+ * Replaces `_system_attention` (attention.py:177-200), i.e.
+ * `attention_with_lse(q_flat[None], sys_k[None], sys_v[None], causal=False)`
+ * (attention.py:183-185, 96-134).
+ *   q:      bf16, row r / head h at q + r*q_row_stride + h*q_head_stride
+ *   sys_k/v bf16, key t / kv head h at base + t*kv_stride_tok + h*kv_stride_head
+ *           ([hkv][s][d]: (d, s*d); the reference's (s, h, d): (h*d, d))
+ *   o_sys:  fp32 [n_rows][hq][128] (normalised), lse_sys: fp32 [n_rows][hq]
+ *   grid_cap: CTAs to use (normally the SM count; one CTA per SM).
+ * Errors: s < 1 -> RB_ERR_CONTRACT (attention.py:219-222); hq % hkv -> DIMENSION.
  */
 int rb_system_attention(const void* q, long long q_row_stride, long long q_head_stride,
                         int n_rows, int hq, int hkv, int d, const void* sys_k, const void* sys_v,
@@ -118,23 +81,60 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
                         size_t workspace_bytes, void* stream);
 
 /*
- * `_context_attention` / `attention_with_lse` per request (attention.py:96-174)
- * over paged or ragged context K/V (as rb_relay_step), causal or not.  With
- * s_prefix > 0, every request first attends the prefix (prefix_k/prefix_v,
- * strides as sys_k) -- the reference's `baseline_attention` over
- * [sys || ctx] (attention.py:266-296), the naive per-request baseline that
- * re-reads the shared prefix for every request.  = rb_relay_step with phases 2.
+ * Request-context attention over paged (or ragged-contiguous) KV.  With
+ * causal=1, row t of request r (m_r = q_start[r+1] - q_start[r] rows)
+ * attends context keys 0 .. ctx_lens[r] - m_r + t  -- `_context_attention`
+ * (attention.py:160-174) / `attention_with_lse(causal=True)`
+ * (attention.py:120-121); causal=0 attends all ctx_lens[r] keys.
+ *   KV addressing, key t of request r, kv head h:
+ *     paged  (block_table != NULL): base + block_table[r*bt_stride + t/block_size]*stride_block
+ *                                        + (t % block_size)*stride_tok + h*stride_head
+ *            pool layout [num_blocks][hkv][block_size][128]: (hkv*bs*128, 128, bs*128)
+ *     ragged (req_offset != NULL):  base + (req_offset[r] + t)*stride_tok + h*stride_head
+ *   max_rows: max_r m_r * (hq / hkv).
+ * Relay epilogue: when o_sys/lse_sys (rb_system_attention's outputs) are
+ *   given, the result is fused with them (`relay_fusion`, attention.py:137-157)
+ *   and lse_out receives the fused LSE = logaddexp(lse_sys, lse_ctx).
+ * Naive baseline: when s_prefix > 0, each request first attends the whole
+ *   shared prefix prefix_k/prefix_v (re-read per request, like the
+ *   reference's `baseline_attention`, attention.py:266-296).
+ * out: [n_rows][hq][128], fp32 when out_fp32 else bf16; lse_out: fp32
+ *   [n_rows][hq] or NULL.
  */
 int rb_context_attention(const void* q, long long q_row_stride, long long q_head_stride,
-                         const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv,
-                         int d, const void* k, const void* v, long long ctx_extent,
-                         const int* block_table, int bt_stride, int block_size,
-                         const long long* req_offset, long long stride_block, long long stride_tok,
-                         long long stride_head, const int* ctx_lens, int causal,
-                         const void* prefix_k, const void* prefix_v, int s_prefix,
-                         long long p_stride_tok, long long p_stride_head, float scale,
-                         int grid_cap, void* out, int out_fp32, float* lse_out, void* workspace,
-                         size_t workspace_bytes, void* stream);
+                         const int* q_start, int b, int max_rows, int hq, int hkv, int d,
+                         const void* k, const void* v, const int* block_table, int bt_stride,
+                         int block_size, const long long* req_offset, long long stride_block,
+                         long long stride_tok, long long stride_head, const int* ctx_lens,
+                         int causal, const void* prefix_k, const void* prefix_v, int s_prefix,
+                         long long p_stride_tok, long long p_stride_head, const float* o_sys,
+                         const float* lse_sys, float scale, void* out, int out_fp32,
+                         float* lse_out, void* stream);
+
+/*
+ * The whole relay decode step in one call -- `relay_attention_ragged`
+ * (attention.py:203-243) over a shared prefix and paged (or ragged) context:
+ * the tcgen05 system kernel writes its stream-K partial slots into
+ * `workspace` without merging them, and the context kernel (launched with
+ * programmatic dependent launch, so it streams context K/V while the system
+ * kernel drains) merges every system slot of a (row, head) with its own
+ * context state in ONE LSE-weighted combine -- the relay fusion
+ * (attention.py:137-157) -- writing `out` (bf16 or fp32) and the fused LSE.
+ * Arguments are those of rb_system_attention + rb_context_attention (causal).
+ * workspace: rb_relay_workspace_bytes(...) bytes, no initialisation needed.
+ * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
+ * (profiling: phase 2 consumes the slots a previous phase-1 call wrote).
+ */
+int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes);
+int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_stride,
+                       const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
+                       const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
+                       long long sys_stride_head, const void* k, const void* v,
+                       const int* block_table, int bt_stride, int block_size,
+                       const long long* req_offset, long long stride_block, long long stride_tok,
+                       long long stride_head, const int* ctx_lens, float scale, int grid_cap,
+                       void* out, int out_fp32, float* lse_out, void* workspace,
+                       size_t workspace_bytes, int phases, void* stream);
 
 /*
  * Standalone relay fusion (attention.py:137-157) over n_vec vectors of d
@@ -148,16 +148,15 @@ int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx
 /*
  * Paged KV append (PagedKvCache.append, kvcache.py:207-235): token i of
  * k_new/v_new ([n_tok][hkv][128] bf16) goes to slot slot_mapping[i] =
- * block_id*block_size + offset of one layer's pool (block stride / head
- * stride in elements), written into the swizzled [128 d][block_size] block
- * layout rb_relay_step reads.
+ * block_id*block_size + offset of the pool.
  */
 int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, int n_tok,
                  void* k_pool, void* v_pool, int hkv, int d, int block_size,
-                 long long stride_block, long long stride_head, void* stream);
+                 long long stride_block, long long stride_tok, long long stride_head,
+                 void* stream);
 
 /*
- * Debug probe of the tcgen05 operand layouts of the system tiles
+ * Debug probe of the tcgen05 operand layouts used by rb_system_attention
  * (one CTA): S^T = K.Q^T and O^T = V^T.P^T for K,V [128][128], Q [nq][128],
  * P [nq][128] bf16 -> s_out, o_out fp32 [128][nq].  For tests only.
  */
@@ -165,19 +164,10 @@ int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void*
                         float* s_out, float* o_out, void* stream);
 
 /*
- * Debug probe of the paged-context operand layouts of rb_relay_step (one CTA):
- * k, v [128 keys][128 d] bf16 are laid out as PagedKvCache blocks of
- * block_size (16/32/64) tokens, q, p [32][128]; s_out = K.Q^T and
- * o_out = V^T.P^T, fp32 [128][32].  For tests only.
- */
-int rb_debug_ctx_probe(const void* k, const void* q, const void* v, const void* p, int block_size,
-                       float* s_out, float* o_out, void* stream);
-
-/*
- * Debug: when `buf` (device) is non-NULL, subsequent
- * rb_relay_step launches record per-CTA %globaltimer stamps into it ([grid][512]
- * u64; layout in profiles/diag_step_timeline.py).  NULL disables.  For
- * profiling only.
+ * Debug: when `buf` (device, [grid][8] u64) is non-NULL, subsequent
+ * rb_system_attention launches record per-CTA %globaltimer stamps into it
+ * (entry, prologue done, first S tile, group-0 end, group-1 end, producer end,
+ * V-producer end, exit).  NULL disables.  For profiling only.
  */
 int rb_debug_set_timestamps(void* buf);
 

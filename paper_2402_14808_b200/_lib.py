@@ -19,12 +19,11 @@ RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
 
 # every symbol include/relay_b200.h declares
 EXPORTS = (
-    "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_step_plan_query",
-    "rb_relay_step_supported", "rb_relay_step", "rb_system_attention", "rb_context_attention",
-    "rb_relay_fusion", "rb_kv_append",
-    "rb_debug_umma_probe", "rb_debug_ctx_probe", "rb_debug_set_timestamps",
+    "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
+    "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
+    "rb_relay_workspace_bytes", "rb_relay_attention",
+    "rb_debug_umma_probe", "rb_debug_set_timestamps",
 )
-ABI_VERSION = 3
 
 _lib = None
 
@@ -39,35 +38,36 @@ def load():
             "(no CPU fallback exists for the relay path)")
     lib = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_float
-    sz = ctypes.c_size_t
+    fp = ctypes.POINTER(ctypes.c_float)
     lib.rb_last_error.restype = ctypes.c_char_p
     lib.rb_last_error.argtypes = []
     lib.rb_abi_version.restype = i32
     lib.rb_device_sm_count.argtypes = [i32, ctypes.POINTER(i32)]
-    lib.rb_step_plan_query.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(i64),
-                                       ctypes.POINTER(sz)]
-    lib.rb_relay_step_supported.argtypes = [i32, i32, i32, i32, i32, i32]
-    lib.rb_relay_step.argtypes = [
-        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,       # q .. d
-        vp, vp, i32, i64, i64,                                # sys_k .. sys_stride_head
-        vp, vp, i64, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
-        i32, i32, f32, i32, vp, i32, vp, vp, sz, i32, vp]     # causal .. stream
+    lib.rb_sys_plan_query.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(i64),
+                                      ctypes.POINTER(ctypes.c_size_t)]
     lib.rb_system_attention.argtypes = [
-        vp, i64, i64, i32, i32, i32, i32, vp, vp, i32, i64, i64, f32, i32, vp, vp, vp, sz, vp]
+        vp, i64, i64, i32, i32, i32, i32, vp, vp, i32, i64, i64, f32, i32, vp, vp, vp,
+        ctypes.c_size_t, vp]
     lib.rb_context_attention.argtypes = [
-        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,       # q .. d
-        vp, vp, i64, vp, i32, i32, vp, i64, i64, i64, vp, i32,  # k .. causal
-        vp, vp, i32, i64, i64,                                # prefix
-        f32, i32, vp, i32, vp, vp, sz, vp]                    # scale .. stream
+        vp, i64, i64, vp, i32, i32, i32, i32, i32,       # q .. d
+        vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
+        i32, vp, vp, i32, i64, i64,                      # causal, prefix
+        vp, vp, f32, vp, i32, vp, vp]                    # o_sys .. stream
+    lib.rb_relay_workspace_bytes.argtypes = [i32, i32, i32, i32, i32,
+                                             ctypes.POINTER(ctypes.c_size_t)]
+    lib.rb_relay_attention.argtypes = [
+        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,   # q .. d
+        vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
+        vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,      # k .. ctx_lens
+        f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
-    lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, vp]
+    lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
-    lib.rb_debug_ctx_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
     lib.rb_debug_set_timestamps.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("rb_last_error", "rb_abi_version"):
             getattr(lib, name).restype = i32
-    if lib.rb_abi_version() != ABI_VERSION:
+    if lib.rb_abi_version() != 1:
         raise ImportError("librelay_b200.so ABI mismatch; rebuild")
     _lib = lib
     return lib
@@ -86,19 +86,21 @@ def check(status: int, what: str = "") -> None:
     raise KernelError(msg)
 
 
-def step_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
-    """(fields dict, workspace bytes) of the relay step's system-tile plan."""
+def sys_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
+    """(fields dict, workspace bytes) of rb_system_attention's stream-K plan."""
     f = (ctypes.c_longlong * 8)()
     ws = ctypes.c_size_t(0)
-    check(load().rb_step_plan_query(n_rows, hq, hkv, s, grid_cap, f, ctypes.byref(ws)),
-          "rb_step_plan_query")
+    check(load().rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, ctypes.byref(ws)),
+          "rb_sys_plan_query")
     keys = ("nq", "n_qt", "tpu", "n_units", "total", "grid", "max_parts")
     return dict(zip(keys, list(f)[:7])), ws.value
 
 
-def relay_step_supported(n_rows: int, hq: int, hkv: int, b: int, block_size: int,
-                         paged: bool) -> bool:
-    return bool(load().rb_relay_step_supported(n_rows, hq, hkv, b, block_size, int(paged)))
+def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
+          "rb_relay_workspace_bytes")
+    return out.value
 
 
 def sm_count(device: int = 0) -> int:

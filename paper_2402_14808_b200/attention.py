@@ -224,9 +224,10 @@ def relay_attention_ragged(q_list, sys_k, sys_v, ctx_k, ctx_v, counter=None,
     (c_r, h_kv, d) including the current tokens; sys_k/sys_v: (s, h_kv, d),
     s >= 1.  Equals causal attention over [system || context] per request.
 
-    One rb_relay_step call (one persistent kernel): the system segment runs
-    once for the whole batch, the context segment and the fusion in the same
-    launch.  Fusion is a single deterministic LSE merge, so `system_first` cannot change the
+    One rb_relay_attention call: the system segment runs once for the whole
+    batch (tcgen05 kernel), the context segment and the fusion run in one
+    kernel.  Fusion is a
+    single deterministic LSE merge, so `system_first` cannot change the
     result (the reference's bitwise order-independence, attention.py:208-212).
     """
     _ndim(sys_k, 3, "sys_k")
@@ -375,10 +376,12 @@ class RelayDecodeStep:
     """One relay decode step (m = 1 token per request) over resident caches.
 
     q: (b, hq, 128) bf16 -> out (b, hq, 128) bf16 and fused lse (b, hq) fp32.
-    One rb_relay_step call = ONE persistent kernel on the current stream:
-    system tiles (shared prefix read once), paged context tiles and the relay
-    fusion.  All buffers are preallocated, so the step can be captured in a
-    CUDA graph (context lengths and block tables are read on the device).
+    One rb_relay_attention call = two kernels on the current stream: the
+    tcgen05 system kernel (shared prefix read once, stream-K partials left
+    unmerged) and the paged context kernel, launched with programmatic
+    dependent launch, whose epilogue merges the system partials with the
+    context state (relay fusion).  All buffers are preallocated, so the step
+    can be captured in a CUDA graph.
     """
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
@@ -394,7 +397,8 @@ class RelayDecodeStep:
         dev = block_table.device
         self.grid = kernels.sm_count(dev) if grid is None else grid
         from . import _lib
-        self.plan, need = _lib.step_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
@@ -410,11 +414,12 @@ class RelayDecodeStep:
             ws=self.ws, phases=phases)
 
     def system(self, q):
-        """Only the system tiles of the step (profiling): out = o_sys."""
+        """Only the system kernel of the step (profiling)."""
         return self._launch(q, 1)
 
     def context(self, q):
-        """Only the context tiles of the step (profiling): out = o_ctx."""
+        """Only the context + fusion kernel (profiling; consumes the system
+        partials of the last `system` call)."""
         return self._launch(q, 2)
 
     def __call__(self, q):
@@ -443,17 +448,26 @@ class RelayDecodeStep:
 
         qkv_host: pinned bf16 (3, b, h, 128) holding this step's q, k_new,
         v_new; out_host: pinned bf16 (b, hq, 128).  Returns a callable that
-        replays [one H2D, the paged append, the relay step, one D2H] on the
-        current stream.  Refill `qkv_host` between calls.
+        replays the step on the current stream.  Inside the graph the q H2D
+        feeds the system kernel directly while the k/v H2D and the paged
+        append run on a forked stream; the context kernel joins both.  Refill
+        `qkv_host` between calls.
         """
         dev = self.out.device
         qkv_dev = torch.empty(qkv_host.shape, dtype=torch.bfloat16, device=dev)
         main = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
 
         def body():
-            qkv_dev.copy_(qkv_host, non_blocking=True)
-            self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
-            out, _ = self(qkv_dev[0])
+            cur = torch.cuda.current_stream(dev)
+            side.wait_stream(cur)
+            qkv_dev[0].copy_(qkv_host[0], non_blocking=True)
+            self.system(qkv_dev[0])
+            with torch.cuda.stream(side):
+                qkv_dev[1:].copy_(qkv_host[1:], non_blocking=True)
+                self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
+            cur.wait_stream(side)
+            out, _ = self.context(qkv_dev[0])
             out_host.copy_(out, non_blocking=True)
 
         warm = torch.cuda.Stream(device=dev)
@@ -465,36 +479,34 @@ class RelayDecodeStep:
         with torch.cuda.graph(graph):
             body()
         self._host_graph = graph  # keep alive with its buffers
-        self._host_graph_bufs = (qkv_dev,)
+        self._host_graph_bufs = (qkv_dev, side)
         return graph.replay
 
 
 class NaiveDecodeStep:
     """The per-request baseline step ("vLLM-PS"; reference
     `baseline_attention`): every request re-reads the shared prefix (stored
-    once, in the SystemKvCache) and then its own paged context -- the same
-    persistent kernel in its prefix-per-request mode, no fusion.  Same
-    inputs/outputs as RelayDecodeStep."""
+    once, in the SystemKvCache) and then its own paged context, in one
+    paged kernel without fusion.  Same inputs/outputs as RelayDecodeStep."""
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
-                 grid=None, out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16):
         self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
         self.block_table, self.ctx_lens = block_table, ctx_lens
         self.b = ctx_lens.numel()
         self.hq, self.hkv = hq, sys_cache.kv_heads
         dev = block_table.device
-        self.grid = kernels.sm_count(dev) if grid is None else grid
-        need = kernels.step_workspace_bytes(self.b, hq, self.hkv, 0, self.grid)
-        self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
         self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
 
     def __call__(self, q):
+        pk = self.sys_cache.keys[self.layer]
+        pv = self.sys_cache.values[self.layer]
         return kernels.context_attention(
             q, self.q_start, self.paged.k_pool[self.layer], self.paged.v_pool[self.layer],
             self.ctx_lens, max_rows=self.hq // self.hkv, hkv=self.hkv,
             block_table=self.block_table, block_size=self.paged.block_size,
-            strides=self.paged.strides(), causal=True,
-            prefix_k=self.sys_cache.keys[self.layer], prefix_v=self.sys_cache.values[self.layer],
-            prefix_layout="hsd", grid=self.grid, out=self.out, lse_out=self.lse, ws=self.ws)
+            strides=self.paged.strides(), causal=True, prefix_k=pk, prefix_v=pv,
+            prefix_strides=(pk.stride(1), pk.stride(0), pk.shape[1]),
+            out=self.out, lse_out=self.lse)

@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librelay_b200.so")
-SOURCES = ["relay_step_sm100.cu", "aux_kernels.cu", "probe_sm100.cu", "capi.cu"]
+SOURCES = ["sys_attn_sm100.cu", "ctx_attn.cu", "capi.cu"]
 HEADERS = ["rb_common.cuh", "rb_plan.h", "rb_args.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,4 +58,4 @@ def build(force=False, verbose=False):
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose=True))

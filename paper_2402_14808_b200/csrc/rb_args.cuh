@@ -61,40 +61,4 @@ struct CtxArgs {
   float scale_log2;
 };
 
-// One fused relay decode step (relay_step_sm100.cu): system tiles (stream-K
-// over the shared prefix) and context tiles (whole (request, kv head, q-tile)
-// units over the paged / ragged context KV) through one TMA + tcgen05
-// pipeline; partial states merged by the last contributor of each output
-// group (= system unit) into the fused output.
-struct StepArgs {
-  rb_sys_plan sp;                // system plan: stream-K over sp.total tiles on sp.grid CTAs
-  int has_sys, has_ctx;          // segments present in this launch (profiling can drop one)
-  int b;                         // requests
-  int ctx_rows_box;              // query rows per context Q TMA box
-  int paged;                     // 1: block_table + paged pool; 0: ragged req_offset + 3-D map
-  int block_size;                // paged: 16 / 32 / 64 tokens per block
-  int causal;                    // context rows see keys < c_r - m_r + t + 1 (else all c_r)
-  int prefix_tiles;              // naive baseline: every context unit first re-reads the
-                                 // shared prefix (ceil(s / 128) tiles), no system units
-  const unsigned char* k_pool;   // paged: one layer's K pool, blocks of [128 d][bs] (swizzled)
-  const unsigned char* v_pool;
-  long long pool_block_bytes;    // byte stride between blocks
-  long long pool_head_bytes;     // byte stride between kv heads of a block
-  const int* q_start;            // [b+1]
-  const int* ctx_lens;           // [b]
-  const int* block_table;        // [b][bt_stride]
-  int bt_stride;
-  const long long* req_offset;   // [b] (ragged)
-  float scale_log2;
-  int* counters;                 // grid barrier {arrivals, generation}; zero-filled once
-  float* sys_acc;                // [n_units][2*max_parts][nq][128]  (slot = part*2 + group)
-  float* sys_ml;                 // [n_units][2*max_parts][2][nq]
-  float* ctx_acc;                // [2 groups][n_rows][hq][128]
-  float* ctx_ml;                 // [2 groups][n_rows][hq][2]
-  void* out;                     // [n_rows][hq][128] bf16 or fp32
-  int out_fp32;
-  float* lse_out;                // [n_rows][hq] natural log (may be null)
-  unsigned long long* debug_ts;  // optional per-CTA stamps [grid][64]
-};
-
 }  // namespace rb

@@ -48,11 +48,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   do {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(addr), "r"(parity), "r"(0x989680u)  // suspend up to 10 ms: a waiting warp
-        : "memory");                                 // sleeps instead of spinning on issue slots
+        : "r"(addr), "r"(parity)
+        : "memory");
   } while (!done);
 }
 
@@ -75,12 +75,6 @@ __device__ __forceinline__ void pdl_wait_primary() {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// GPU-scope acquire/release fence (the semaphore pattern CUTLASS's
-// GenericBarrier uses: CTA barrier, then ONE thread fences and does the
-// atomic).  Much cheaper than __threadfence() (fence.sc) in every thread.
-__device__ __forceinline__ void fence_acq_rel_gpu() {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -99,16 +93,6 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
       "l"(policy)
       : "memory");
 }
-// 4-D tiled load (paged KV pool, grouped queries), coordinates innermost first.
-__device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar,
-                                            int c0, int c1, int c2, int c3, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
-      "r"(c3), "l"(policy)
-      : "memory");
-}
 // 1-D bulk async copy global -> shared, completes on `bar` (tx bytes).
 // Sizes and addresses must be multiples of 16 bytes.
 __device__ __forceinline__ void bulk_copy_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
@@ -124,19 +108,6 @@ __device__ __forceinline__ void cp_async_16(void* smem_dst, const void* gsrc, ui
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)),
                "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(src_bytes)
                : "memory");
-}
-// 4-byte cp.async (metadata staging), commit / wait-group pipelining.
-__device__ __forceinline__ void cp_async_4(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)),
-               "l"(reinterpret_cast<uint64_t>(gsrc))
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
@@ -285,47 +256,6 @@ __device__ __forceinline__ uint64_t make_smem_desc_sw128(uint32_t saddr, uint32_
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
 }
-// Same, any layout type: 0 none, 6 SWIZZLE_32B, 4 SWIZZLE_64B, 2 SWIZZLE_128B.
-__host__ __device__ constexpr uint32_t umma_layout_for_row_bytes(int row_bytes) {
-  return row_bytes == 32 ? 6u : row_bytes == 64 ? 4u : row_bytes == 128 ? 2u : 0u;
-}
-__device__ __forceinline__ uint64_t make_smem_desc(uint32_t saddr, uint32_t lbo_bytes,
-                                                   uint32_t sbo_bytes, uint32_t layout) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
-  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // version
-  d |= static_cast<uint64_t>(layout & 7) << 61;
-  return d;
-}
-// Paged KV block layout (PagedKvCache): one (block, kv head) of K or V is
-// [128 d][bs tokens], rows of rb = 2*bs bytes (32 / 64 / 128), with the
-// matching UMMA swizzle applied to the byte offset inside the block:
-// Swizzle<log2(rb/16), 4, 3>  (16-byte chunk c of row r -> c ^ (r mod rb/16)).
-// The block is then BOTH a K-major (tokens = K) and an MN-major (tokens = MN)
-// canonical UMMA operand, copied verbatim by one bulk copy.
-__host__ __device__ __forceinline__ uint32_t paged_swizzle(uint32_t off, uint32_t row_bytes) {
-  const uint32_t mask = row_bytes / 16 - 1;  // 1, 3, 7
-  return off ^ (((off >> 7) & mask) << 4);
-}
-// Descriptors of a context K / V tile made of 128/bs paged blocks of
-// bs*256 bytes each (row_bytes = 2*bs), shared with relay_step_sm100.cu.
-__device__ __forceinline__ uint64_t ctx_k_desc(uint32_t tile, int kk, int bs) {
-  const uint32_t rb = 2 * bs;
-  // MN-major: 16 d per k-step = 2 atoms of 8 rows; atoms along MN (keys) are
-  // whole blocks apart (LBO), along K 8 rows apart (SBO)
-  return make_smem_desc(tile + kk * 16 * rb, bs * 256, 8 * rb, umma_layout_for_row_bytes(rb));
-}
-__device__ __forceinline__ uint64_t ctx_v_desc(uint32_t tile, int kk, int bs) {
-  const uint32_t rb = 2 * bs;
-  // K-major: 16 keys per k-step = 32 bytes of a row; 8-row groups of d are
-  // 8 rows apart (SBO)
-  const int key0 = kk * 16;
-  return make_smem_desc(tile + (key0 / bs) * bs * 256 + (key0 % bs) * 2, 16, 8 * rb,
-                        umma_layout_for_row_bytes(rb));
-}
-
 // Instruction descriptor, kind::f16: bf16 x bf16 -> f32.
 //   [4,6) c_format (1=F32) | [7,10) a_format (1=BF16) | [10,13) b_format |
 //   [15] a_major (0=K,1=MN) | [16] b_major | [17,23) N>>3 | [24,29) M>>4

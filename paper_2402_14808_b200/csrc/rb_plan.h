@@ -1,19 +1,17 @@
-// Work decomposition of the relay step's system tiles, shared by host and
-// device (and mirrored in Python by paper_2402_14808_b200/plan.py).
+// Work decomposition of the system-prompt attention kernel, shared by host
+// and device (and mirrored in Python by paper_2402_14808_b200/plan.py).
 //
 // Units.  One unit = (kv head h, query tile qt): the query rows of KV head h
 // are the n_rows * g (request-row, group-member) pairs, cut into tiles of
 // `nq` rows.  Each unit streams the whole shared prefix of its head in key
-// tiles of 128 keys, so the flattened system tile space is
+// tiles of 128 keys, so the flattened iteration space is
 //     global tile i  ->  unit u = i / tpu, key tile kt = i % tpu,
 //     total = n_units * tpu.
-// Stream-K split (static, balanced to one tile).  CTA c of `grid` CTAs owns
-// the system tiles [c*total/grid, (c+1)*total/grid); a unit cut by CTA
-// boundaries is finished by several CTAs (its "parts"); CTA c writes part
-// slot c - owner(first tile of u), and the merge reads the slots in order,
-// so the result is deterministic.  The context units that follow are handed
-// out dynamically by each CTA's scheduler warp (relay_step_sm100.cu), which
-// absorbs whatever imbalance the static system split leaves.
+// Stream-K split.  CTA c of `grid` CTAs owns the contiguous global tile range
+// [c*total/grid, (c+1)*total/grid).  A unit cut by CTA boundaries is
+// finished by several CTAs; CTA c writes partial slot c - owner(first tile
+// of u), and the last CTA to finish (per-unit semaphore) merges the slots in
+// slot order, so the result is deterministic.
 #pragma once
 #include <stdint.h>
 
@@ -36,8 +34,8 @@ typedef struct {
   int tpu;            // key tiles per unit, ceil(s / 128)
   int n_units;        // hkv * n_qt
   long long total;    // n_units * tpu
-  int grid;           // CTAs sharing the system tiles
-  int max_parts;      // max parts (CTAs) over all units
+  int grid;           // CTAs launched
+  int max_parts;      // max partial slots over all units
 } rb_sys_plan;
 
 RB_HD long long rb_cta_begin(const rb_sys_plan* p, int c) {
@@ -51,4 +49,31 @@ RB_HD int rb_unit_parts(const rb_sys_plan* p, int u) {
   long long first = (long long)u * p->tpu;
   long long last = first + p->tpu - 1;
   return rb_tile_owner(p, last) - rb_tile_owner(p, first) + 1;
+}
+
+RB_HD int rb_pick_nq(int rows_per_head) { return rows_per_head <= 16 ? 16 : 32; }
+
+// Fill a plan. grid_cap = number of CTAs the device can hold at once
+// (SM count for this one-CTA-per-SM kernel).
+RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
+                            int grid_cap) {
+  p->n_rows = n_rows;
+  p->hq = hq;
+  p->hkv = hkv;
+  p->g = hq / hkv;
+  p->s = s;
+  p->rows_per_head = n_rows * p->g;
+  p->nq = rb_pick_nq(p->rows_per_head);
+  p->n_qt = (p->rows_per_head + p->nq - 1) / p->nq;
+  p->tpu = (s + RB_KEY_TILE - 1) / RB_KEY_TILE;
+  p->n_units = hkv * p->n_qt;
+  p->total = (long long)p->n_units * p->tpu;
+  long long gcap = grid_cap < 1 ? 1 : grid_cap;
+  p->grid = (int)(p->total < gcap ? p->total : gcap);
+  int mp = 1;
+  for (int u = 0; u < p->n_units; ++u) {
+    int c = rb_unit_parts(p, u);
+    if (c > mp) mp = c;
+  }
+  p->max_parts = mp;
 }

@@ -1,0 +1,738 @@
+// System-prompt attention on sm_100a: tcgen05 + TMA + TMEM.
+//
+// Computes, for every query row of the batch (all requests' new tokens
+// flattened, as in /root/reference/pkg/src/relayserve/attention.py:183-185)
+// and every query head, one UNMASKED attention pass over the shared prefix
+// K/V with natural-log LSE -- the reference's `_system_attention`
+// (attention.py:177-200) / `attention_with_lse(causal=False)`
+// (attention.py:96-134, kernels _kernels_cy.pyx:13-51).
+//
+// Design:
+//  * swap-AB: the MMA M dimension is the 128 keys of a tile, N is the
+//    (request x GQA-group) query rows of one KV head (nq = 16/32), so a
+//    batch of 32 decode rows still fills M = 128:
+//        S^T[128 keys x nq] = K_tile[128 x d] . Q^T        (both K-major)
+//        O^T[d x nq]       = V_tile^T[d x 128] . P^T       (A MN-major)
+//    accumulators in TMEM (2 S buffers + 2 O buffers = 4*nq columns).
+//  * K and V tiles (128 keys x 128 d bf16 = 32 KB each) are TMA-loaded with
+//    the 128B swizzle through two mbarrier rings: K slots are released as soon
+//    as S^T = K.Q^T completes, V slots after O^T = V^T.P^T, so the shallow K
+//    ring and the deeper V ring keep ~4 tiles of HBM reads in flight per SM.
+//    Every shared-prefix byte crosses HBM exactly once per step.
+//  * warp roles: warp 0 K producer (+ Q rows via cp.async), warp 1 QK^T
+//    issuer (one thread) + TMEM owner, warp 2 V producer, warp 3 PV issuer,
+//    then two compute groups that alternate key tiles, each with its own
+//    online-softmax state (merged at the end of a unit through TMEM).
+//    Thread t of a compute warp owns TMEM lane t of its quadrant = key t of
+//    the tile for S, = head-dim index t for O.
+//  * online softmax in the log2 domain: per-query max / sum across the 128
+//    key lanes via a warp reduce-scatter butterfly + a 4-warp smem combine;
+//    O accumulates in registers (acc = acc*alpha + O_tile), so the tensor
+//    core never waits for a rescale.
+//  * persistent stream-K over (kv head, query tile, key tile): one CTA per
+//    SM, contiguous equal tile ranges, per-unit semaphore merge of partial
+//    (acc, m, l) in fixed slot order -> deterministic output.
+#include "rb_common.cuh"
+#include "rb_plan.h"
+#include "rb_args.cuh"
+
+namespace rb {
+
+
+constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
+
+// Shared-memory / thread layout for a query tile of NQ rows.  Two compute
+// groups alternate key tiles (even / odd local tile index), each with its own
+// online-softmax state; a group has NHALF slices of 4 warps (one per TMEM
+// lane quadrant), each thread handling H query columns.
+template <int NQ>
+struct SysCfg {
+  static constexpr int H = 16;
+  static constexpr int NHALF = NQ / H;
+  static constexpr int WPG = 4 * NHALF;                 // warps per group
+  static constexpr int NCW = 2 * WPG;                   // compute warps
+  static constexpr int kRoleWarps = 4;                  // K producer, QK issuer, V producer, PV issuer
+  static constexpr int kThreads = (kRoleWarps + NCW) * 32;
+  static constexpr int KS = 2;                          // K ring (freed after Q.K^T)
+  static constexpr int VS = 4;                          // V ring (freed after P.V)
+  static constexpr int kTileBytes = kKvTileBytes;       // 32 KB per K or V tile
+  static constexpr int kQBytes = NQ * 256;              // [2 kblocks][NQ][128 B]
+  static constexpr int kOffK = 0;
+  static constexpr int kOffV = kOffK + KS * kTileBytes;
+  static constexpr int kOffQ = kOffV + VS * kTileBytes;
+  static constexpr int kOffP = kOffQ + 2 * kQBytes;
+  static constexpr int kRedBytes = 2 * NHALF * 4 * H * 4;  // [group][half][quadrant][H]
+  static constexpr int kOffRedMax = kOffP + 2 * kQBytes;
+  static constexpr int kOffRedSum = kOffRedMax + kRedBytes;
+  static constexpr int kOffL = kOffRedSum + kRedBytes;   // [group][NQ]
+  static constexpr int kOffX = kOffL + 2 * NQ * 4;       // handover m, l: [2][NQ]
+  static constexpr int kOffBar = kOffX + 2 * NQ * 4;
+  static constexpr int kNumBars = 2 * KS + 2 * VS + 18;
+  static constexpr int kOffMisc = kOffBar + kNumBars * 8;
+  static constexpr int kBytes = kOffMisc + 64;
+  static constexpr int kTmemCols = (5 * NQ <= 128) ? 128 : (5 * NQ <= 256) ? 256 : 512;
+};
+
+template <int H>
+__device__ __forceinline__ int reduce_scatter_col(int lane) {
+  constexpr int S = (H == 8) ? 3 : (H == 16) ? 4 : 5;
+  return lane >> (5 - S);
+}
+
+// Reduce-scatter H per-lane values over the 32 lanes of a warp: afterwards
+// the returned value is the reduction of column reduce_scatter_col<H>(lane)
+// over all 32 lanes.  H - 1 + (5 - log2 H) shuffles.
+template <int H, bool IS_MAX>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[H], int lane) {
+#pragma unroll
+  for (int n = H, mask = 16; n > 1; n >>= 1, mask >>= 1) {
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const float send = upper ? v[i] : v[i + n / 2];
+      const float keep = upper ? v[i + n / 2] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, mask);
+      v[i] = IS_MAX ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+  float r = v[0];
+  constexpr int S = (H == 8) ? 3 : (H == 16) ? 4 : 5;
+#pragma unroll
+  for (int mask = (16 >> S); mask >= 1; mask >>= 1) {
+    const float o = __shfl_xor_sync(0xffffffffu, r, mask);
+    r = IS_MAX ? fmaxf(r, o) : r + o;
+  }
+  return r;
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
+    sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                          const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
+  using L = SysCfg<NQ>;
+  constexpr int H = L::H;
+  constexpr int KS = L::KS, VS = L::VS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = bars + KS;
+  uint64_t* v_full = bars + 2 * KS;
+  uint64_t* v_empty = bars + 2 * KS + VS;
+  uint64_t* s_full = bars + 2 * KS + 2 * VS;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_full + 4;
+  uint64_t* p_empty = s_full + 6;
+  uint64_t* o_full = s_full + 8;
+  uint64_t* o_empty = s_full + 10;
+  uint64_t* q_full = s_full + 12;
+  uint64_t* q_empty = s_full + 14;
+  uint64_t* x_full = s_full + 16;
+  uint64_t* x_empty = s_full + 17;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
+  float* red_max = reinterpret_cast<float*>(smem + L::kOffRedMax);
+  float* red_sum = reinterpret_cast<float*>(smem + L::kOffRedSum);
+  float* l_s = reinterpret_cast<float*>(smem + L::kOffL);
+  float* x_ml = reinterpret_cast<float*>(smem + L::kOffX);
+
+  const rb_sys_plan& P = args.plan;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long t_begin = rb_cta_begin(&P, blockIdx.x);
+  const long long t_end = rb_cta_begin(&P, blockIdx.x + 1);
+
+  unsigned long long* dts = args.debug_ts ? args.debug_ts + blockIdx.x * 8 : nullptr;
+  if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
+  if (threadIdx.x == 0) {
+    if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
+    tma_prefetch_desc(&tmap_k);
+    tma_prefetch_desc(&tmap_v);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], L::WPG);
+      mbar_init(&p_full[i], L::WPG);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], L::WPG);
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(x_full, L::WPG);
+    mbar_init(x_empty, L::WPG);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&misc[0], L::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = misc[0];
+  if (dts && threadIdx.x == 0) dts[1] = global_timer_ns();
+  // the next kernel (context + fusion) may be scheduled as SMs free up; it
+  // waits for this grid's memory before it reads o_sys / lse_sys.
+  pdl_launch_dependents();
+
+  const uint32_t smem_k = smem_u32(smem + L::kOffK);
+  const uint32_t smem_v = smem_u32(smem + L::kOffV);
+  const uint32_t smem_q = smem_u32(smem + L::kOffQ);
+  const uint32_t smem_p = smem_u32(smem + L::kOffP);
+
+  if (warp == 0) {
+    // ------------------------------------------------- K producer (+ Q rows)
+    const uint64_t pol = l2_policy_evict_first();
+    int j = 0, uq = 0;
+    for (long long i = t_begin; i < t_end; ++i, ++j) {
+      const int u = static_cast<int>(i / P.tpu);
+      const int kt = static_cast<int>(i % P.tpu);
+      const int h = u / P.n_qt;
+      const int qt = u % P.n_qt;
+      const int st = j % KS;
+      mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
+      if (lane == 0) {
+        uint8_t* dst = smem + L::kOffK + st * L::kTileBytes;
+        mbar_arrive_expect_tx(&k_full[st], L::kTileBytes);
+        tma_load_3d(dst, &tmap_k, &k_full[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(dst + L::kTileBytes / 2, &tmap_k, &k_full[st], 64, kt * RB_KEY_TILE, h, pol);
+      }
+      __syncwarp();
+      if (i == t_begin || kt == 0) {
+        // query rows of unit u (after this tile's K is already in flight);
+        // q may be produced by the previous kernel in the stream.
+        if (i == t_begin) pdl_wait_primary();
+        const int qb = uq & 1;
+        mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
+        uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
+        // all of the tile's 16-byte chunks in flight at once (zero-fill past the rows)
+#pragma unroll
+        for (int it = 0; it < NQ / 2; ++it) {
+          const int idx = lane + it * 32;
+          const int c = idx >> 4, ch = idx & 15;
+          const int f = qt * NQ + c;
+          const bool ok = f < P.rows_per_head;
+          const int row = ok ? f / P.g : 0, jj = ok ? f % P.g : 0;
+          const __nv_bfloat16* src = args.q + row * args.q_row_stride +
+                                     static_cast<long long>(h * P.g + jj) * args.q_head_stride +
+                                     ch * 8;
+          cp_async_16(qdst + (ch >> 3) * (NQ * 128) + sw128_offset(c, (ch & 7) * 8), src,
+                      ok ? 16u : 0u);
+        }
+        cp_async_wait_all();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_full[qb]);
+        ++uq;
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ V producer
+    const uint64_t pol = l2_policy_evict_first();
+    if (lane == 0) {
+      // Start streaming V only once this CTA's first K tile has landed: at
+      // launch every SM fires its rings at once, and the first Q.K^T must not
+      // queue behind four V tiles per SM.
+      if (t_begin < t_end) mbar_wait(&k_full[0], 0);
+      int j = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int u = static_cast<int>(i / P.tpu);
+        const int kt = static_cast<int>(i % P.tpu);
+        const int h = u / P.n_qt;
+        const int st = j % VS;
+        mbar_wait(&v_empty[st], ((j / VS) & 1) ^ 1);
+        uint8_t* dst = smem + L::kOffV + st * L::kTileBytes;
+        mbar_arrive_expect_tx(&v_full[st], L::kTileBytes);
+        tma_load_3d(dst, &tmap_v, &v_full[st], 0, kt * RB_KEY_TILE, h, pol);
+        tma_load_3d(dst + L::kTileBytes / 2, &tmap_v, &v_full[st], 64, kt * RB_KEY_TILE, h, pol);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ----------------------------------------------- S^T = K . Q^T issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
+      int j = 0, uq = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int kt = static_cast<int>(i % P.tpu);
+        const bool new_unit = (i == t_begin) || kt == 0;
+        const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
+        const int qb = uq & 1;
+        if (new_unit) mbar_wait(&q_full[qb], (uq >> 1) & 1);
+        const int st = j % KS, sb = j & 1;
+        mbar_wait(&k_full[st], (j / KS) & 1);
+        mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_k + st * L::kTileBytes;
+        const uint32_t q_base = smem_q + qb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + sb * NQ;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk & 3) * 32;
+          const uint64_t a =
+              make_smem_desc_sw128(k_base + (kk >> 2) * (L::kTileBytes / 2) + koff, 16, 1024);
+          const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + koff, 16, 1024);
+          umma_f16_ss(d_tmem, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[sb]);
+        umma_commit(&k_empty[st]);
+        if (last_of_unit) {
+          umma_commit(&q_empty[qb]);
+          ++uq;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    // ------------------------------------------------- O^T = V^T . P^T issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+      int j = 0;
+      for (long long i = t_begin; i < t_end; ++i, ++j) {
+        const int st = j % VS, pb = j & 1;
+        mbar_wait(&v_full[st], (j / VS) & 1);
+        mbar_wait(&p_full[pb], (j >> 1) & 1);
+        mbar_wait(&o_empty[pb], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_v + st * L::kTileBytes;
+        const uint32_t p_base = smem_p + pb * L::kQBytes;
+        const uint32_t d_tmem = tmem_base + 2 * NQ + pb * NQ;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          // A = V^T (M = d, MN-major): 16 keys = two 8-row swizzle atoms.
+          const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, L::kTileBytes / 2, 1024);
+          const uint64_t b =
+              make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[pb]);
+        umma_commit(&v_empty[st]);
+        umma_commit(&p_empty[pb]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------- softmax / O accumulation groups
+    const int cw = warp - L::kRoleWarps;
+    const int grp = cw / L::WPG;                 // which tile parity this group owns
+    const int hf = (cw / 4) % L::NHALF;          // column slice
+    const int qd = warp & 3;                     // TMEM lane quadrant (hardware: warp % 4)
+    const int col0 = hf * H;
+    const bool designated = (qd == 0) && lane < H;
+    const uint32_t bar_red = 1 + grp * L::NHALF + hf;
+    const uint32_t bar_grp = 1 + 2 * L::NHALF + grp;
+    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
+    float* rmax = red_max + (grp * L::NHALF + hf) * 4 * H;
+    float* rsum = red_sum + (grp * L::NHALF + hf) * 4 * H;
+    float* lg = l_s + grp * NQ;
+    const int rcol = reduce_scatter_col<H>(lane);
+    const bool rwriter = (lane & ((32 / H) - 1)) == 0;
+    const int key_lane = qd * 32 + lane;
+    // per-thread swizzled P row offsets (8-row pattern) for this key lane
+    uint32_t poff[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) poff[r] = sw128_offset(r, key_lane & 63);
+    const uint32_t pkb = (key_lane >> 6) * (NQ * 128);
+
+    float m_run[H], acc[H];
+    int xh = 0;  // handovers so far
+    pdl_wait_primary();  // o_sys / partials may still be read by the previous kernel
+    long long i = t_begin;
+    while (i < t_end) {
+      const int u = static_cast<int>(i / P.tpu);
+      const long long unit_end = min(t_end, static_cast<long long>(u + 1) * P.tpu);
+      const long long ia = i, ib = unit_end - 1;
+#pragma unroll
+      for (int c = 0; c < H; ++c) {
+        m_run[c] = -INFINITY;
+        acc[c] = 0.f;
+      }
+      if (designated) lg[col0 + lane] = 0.f;
+      for (long long it = ia + ((ia - t_begin + grp) & 1); it <= ib; it += 2) {
+        const int j = static_cast<int>(it - t_begin);
+        const int kt = static_cast<int>(it % P.tpu);
+        const int gb = j & 1;  // == grp
+        const uint32_t ph = (j >> 1) & 1;
+        // ---- S tile -> scores (log2 domain)
+        mbar_wait(&s_full[gb], ph);
+        if (dts && j == 0 && threadIdx.x == L::kRoleWarps * 32) dts[2] = global_timer_ns();
+        tc_fence_after();
+        float x[H];
+        tmem_ld_32x32b<H>(lane_addr + gb * NQ + col0, x);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[gb]);
+        const bool valid = kt * RB_KEY_TILE + key_lane < P.s;
+#pragma unroll
+        for (int c = 0; c < H; ++c) x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
+        // ---- tile max over the 128 key lanes (4 quadrant warps)
+        {
+          float tmp[H];
+#pragma unroll
+          for (int c = 0; c < H; ++c) tmp[c] = x[c];
+          const float wmax = warp_reduce_scatter<H, true>(tmp, lane);
+          if (rwriter) rmax[qd * H + rcol] = wmax;
+        }
+        named_bar_sync(bar_red, 128);
+        float my_al = 0.f;
+#pragma unroll
+        for (int c4 = 0; c4 < H; c4 += 4) {
+          const float4 a0 = *reinterpret_cast<const float4*>(rmax + 0 * H + c4);
+          const float4 a1 = *reinterpret_cast<const float4*>(rmax + 1 * H + c4);
+          const float4 a2 = *reinterpret_cast<const float4*>(rmax + 2 * H + c4);
+          const float4 a3 = *reinterpret_cast<const float4*>(rmax + 3 * H + c4);
+          const float tm[4] = {fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)),
+                               fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y)),
+                               fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)),
+                               fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = c4 + e;
+            const float mn = fmaxf(m_run[c], tm[e]);
+            const float al = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
+            acc[c] *= al;
+            my_al = (lane == c) ? al : my_al;
+            m_run[c] = mn;
+            x[c] = fast_exp2(x[c] - mn);  // p; exactly 0 for masked keys
+          }
+        }
+        // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
+        mbar_wait(&p_empty[gb], ph ^ 1);
+        {
+          uint8_t* pdst = smem + L::kOffP + gb * L::kQBytes + pkb;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int row = col0 + c;
+            *reinterpret_cast<__nv_bfloat16*>(pdst + (row >> 3) * 1024 + poff[row & 7]) =
+                __float2bfloat16_rn(x[c]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[gb]);
+        // ---- row sums
+        const float wsum = warp_reduce_scatter<H, false>(x, lane);
+        if (rwriter) rsum[qd * H + rcol] = wsum;
+        named_bar_sync(bar_red, 128);
+        if (designated) {
+          const float lt = rsum[0 * H + lane] + rsum[1 * H + lane] + rsum[2 * H + lane] +
+                           rsum[3 * H + lane];
+          lg[col0 + lane] = lg[col0 + lane] * my_al + lt;
+        }
+        // ---- O tile of this key tile
+        mbar_wait(&o_full[gb], ph);
+        tc_fence_after();
+        float o[H];
+        tmem_ld_32x32b<H>(lane_addr + 2 * NQ + gb * NQ + col0, o);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[gb]);
+#pragma unroll
+        for (int c = 0; c < H; ++c) acc[c] += o[c];
+      }
+
+      // ---- unit end: merge the two groups, then write / stream-K merge
+      const int fin = static_cast<int>((ib - t_begin) & 1);
+      const bool two = ib > ia;
+      const uint32_t xaddr = lane_addr + 4 * NQ + col0;
+      if (two && grp != fin) {
+        // helper: hand (acc, m, l) to the finisher through TMEM / smem
+        mbar_wait(x_empty, (xh & 1) ^ 1);
+        tmem_st_32x32b<H>(xaddr, acc);
+        tmem_wait_st();
+        if (designated) {
+          float mv = m_run[0];
+#pragma unroll
+          for (int c = 1; c < H; ++c) mv = (lane == c) ? m_run[c] : mv;
+          x_ml[col0 + lane] = mv;
+          x_ml[NQ + col0 + lane] = lg[col0 + lane];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(x_full);
+      }
+      if (grp == fin) {
+        named_bar_sync(bar_grp, L::WPG * 32);  // own l_s complete
+        float lrow[H];
+#pragma unroll
+        for (int c = 0; c < H; ++c) lrow[c] = lg[col0 + c];
+        if (two) {
+          mbar_wait(x_full, xh & 1);
+          tc_fence_after();
+          float oh[H];
+          tmem_ld_32x32b<H>(xaddr, oh);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const float mh = x_ml[col0 + c], lh = x_ml[NQ + col0 + c];
+            const float M = fmaxf(m_run[c], mh);
+            const float wf = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - M);
+            const float wh = (mh == -INFINITY) ? 0.f : fast_exp2(mh - M);
+            acc[c] = acc[c] * wf + oh[c] * wh;
+            lrow[c] = lrow[c] * wf + lh * wh;
+            m_run[c] = M;
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(x_empty);
+        }
+        const int h = u / P.n_qt, qt = u % P.n_qt;
+        const long long u_first = static_cast<long long>(u) * P.tpu;
+        const int owner0 = rb_tile_owner(&P, u_first);
+        const int nparts = rb_unit_parts(&P, u);
+        const int dcol = key_lane;  // O lane = head-dim index
+        if (args.defer_merge) {
+          // relay path: hand the (unnormalised) part to the fusion epilogue
+          const int slot = blockIdx.x - owner0;
+          const long long pbase = static_cast<long long>(u) * P.max_parts + slot;
+          float* pacc = args.part_acc + pbase * NQ * RB_HEAD_DIM;
+          float* pml = args.part_ml + pbase * 2 * NQ;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int col = col0 + c;
+            pacc[col * RB_HEAD_DIM + dcol] = acc[c];
+            if (qd == 0 && lane == 0) {
+              pml[col] = m_run[c];
+              pml[NQ + col] = lrow[c];
+            }
+          }
+        } else if (nparts == 1) {
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int f = qt * NQ + col0 + c;
+            if (f < P.rows_per_head) {
+              const int row = f / P.g, hh = h * P.g + f % P.g;
+              const long long o_idx = static_cast<long long>(row) * P.hq + hh;
+              args.o_sys[o_idx * RB_HEAD_DIM + dcol] = acc[c] / lrow[c];
+              if (qd == 0 && lane == 0)
+                args.lse_sys[o_idx] = (m_run[c] + __log2f(lrow[c])) * kLn2;
+            }
+          }
+        } else {
+          const int slot = blockIdx.x - owner0;
+          const long long pbase = static_cast<long long>(u) * P.max_parts + slot;
+          float* pacc = args.part_acc + pbase * NQ * RB_HEAD_DIM;
+          float* pml = args.part_ml + pbase * 2 * NQ;
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const int col = col0 + c;
+            pacc[col * RB_HEAD_DIM + dcol] = acc[c];
+            if (qd == 0 && lane == 0) {
+              pml[col] = m_run[c];
+              pml[NQ + col] = lrow[c];
+            }
+          }
+          __threadfence();
+          named_bar_sync(bar_grp, L::WPG * 32);
+          if (cw == grp * L::WPG && lane == 0) {
+            const int prev = atomicAdd(&args.counters[u], 1);
+            const int last = (prev == nparts - 1);
+            if (last) atomicExch(&args.counters[u], 0);
+            misc[2 + grp] = last;
+          }
+          named_bar_sync(bar_grp, L::WPG * 32);
+          if (misc[2 + grp]) {
+            // last CTA of unit u: merge the slots in slot order (deterministic
+            // whoever merges); per slot all H columns' loads are in flight.
+            __threadfence();
+            const float* uacc =
+                args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
+            const float* uml = args.part_ml + static_cast<long long>(u) * P.max_parts * 2 * NQ;
+            // running merge state reuses m_run / lrow / acc (own slot is re-read
+            // from global like every other slot)
+            float* M = m_run;
+            float* Ls = lrow;
+            float* Os = acc;
+#pragma unroll
+            for (int c = 0; c < H; ++c) {
+              M[c] = -INFINITY;
+              Ls[c] = 0.f;
+              Os[c] = 0.f;
+            }
+            for (int k = 0; k < nparts; ++k) {
+#pragma unroll
+              for (int c0 = 0; c0 < H; c0 += 8) {
+                float mk[8], lk[8], ak[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  mk[c] = __ldcg(uml + k * 2 * NQ + col0 + c0 + c);
+                  lk[c] = __ldcg(uml + k * 2 * NQ + NQ + col0 + c0 + c);
+                  ak[c] = __ldcg(uacc + (static_cast<long long>(k) * NQ + col0 + c0 + c) *
+                                            RB_HEAD_DIM + dcol);
+                }
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const float mn = fmaxf(M[c0 + c], mk[c]);
+                  const float so = (M[c0 + c] == -INFINITY) ? 0.f : fast_exp2(M[c0 + c] - mn);
+                  const float sk = fast_exp2(mk[c] - mn);
+                  Ls[c0 + c] = Ls[c0 + c] * so + lk[c] * sk;
+                  Os[c0 + c] = Os[c0 + c] * so + ak[c] * sk;
+                  M[c0 + c] = mn;
+                }
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < H; ++c) {
+              const int f = qt * NQ + col0 + c;
+              if (f < P.rows_per_head) {
+                const int row = f / P.g, hh = h * P.g + f % P.g;
+                const long long o_idx = static_cast<long long>(row) * P.hq + hh;
+                args.o_sys[o_idx * RB_HEAD_DIM + dcol] = Os[c] / Ls[c];
+                if (qd == 0 && lane == 0) args.lse_sys[o_idx] = (M[c] + __log2f(Ls[c])) * kLn2;
+              }
+            }
+          }
+        }
+      }
+      if (two) ++xh;
+      i = unit_end;
+    }
+    if (dts && threadIdx.x == L::kRoleWarps * 32) dts[3] = global_timer_ns();
+    if (dts && threadIdx.x == (L::kRoleWarps + L::WPG) * 32) dts[4] = global_timer_ns();
+  }
+
+  if (dts && threadIdx.x == 0) dts[5] = global_timer_ns();
+  if (dts && threadIdx.x == 64) dts[6] = global_timer_ns();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, L::kTmemCols);
+  }
+  if (dts && threadIdx.x == 0) dts[7] = global_timer_ns();
+}
+
+// ------------------------------------------------------------------- host
+
+template <int NQ>
+static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, const SysArgs& a,
+                              cudaStream_t stream) {
+  using L = SysCfg<NQ>;
+  static_assert(L::kBytes <= 232448, "system kernel shared memory over the 227 KB limit");
+  static_assert(L::kThreads <= 1024, "too many warps");
+  auto kern = sys_attn_sm100_kernel<NQ>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kern, dim3(a.plan.grid), dim3(L::kThreads), L::kBytes, stream, tk, tv, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
+                                    const SysArgs& a, cudaStream_t stream) {
+  switch (a.plan.nq) {
+    case 16: return launch_sys<16>(tk, tv, a, stream);
+    case 32: return launch_sys<32>(tk, tv, a, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------ layout probe
+// One-CTA check of the exact operand layouts / descriptors the system kernel
+// uses (K, V in the TMA SW128 box layout; Q, P in the K-major SW128 layout).
+template <int NQ>
+__global__ void umma_probe_kernel(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                                  const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
+                                  float* o_out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sk = smem;
+  uint8_t* sv = smem + kKvTileBytes;
+  uint8_t* sq = smem + 2 * kKvTileBytes;
+  uint8_t* sp = sq + NQ * 256;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sp + NQ * 256);
+  uint32_t* tm = reinterpret_cast<uint32_t*>(bar + 2);
+  for (int idx = threadIdx.x; idx < 128 * 128; idx += blockDim.x) {
+    const int row = idx / 128, col = idx % 128;
+    const uint32_t off = (col >> 6) * (kKvTileBytes / 2) + sw128_offset(row, col & 63);
+    *reinterpret_cast<__nv_bfloat16*>(sk + off) = k[idx];
+    *reinterpret_cast<__nv_bfloat16*>(sv + off) = v[idx];
+  }
+  for (int idx = threadIdx.x; idx < NQ * 128; idx += blockDim.x) {
+    const int row = idx / 128, col = idx % 128;
+    const uint32_t off = (col >> 6) * (NQ * 128) + sw128_offset(row, col & 63);
+    *reinterpret_cast<__nv_bfloat16*>(sq + off) = q[idx];
+    *reinterpret_cast<__nv_bfloat16*>(sp + off) = p[idx];
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (threadIdx.x < 32) tmem_alloc(tm, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tm;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
+    constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
+    const uint32_t k_base = smem_u32(sk), v_base = smem_u32(sv);
+    const uint32_t q_base = smem_u32(sq), p_base = smem_u32(sp);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t a =
+          make_smem_desc_sw128(k_base + (kk >> 2) * (kKvTileBytes / 2) + (kk & 3) * 32, 16, 1024);
+      const uint64_t b = make_smem_desc_sw128(q_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+      umma_f16_ss(tbase, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+    }
+    umma_commit(&bar[0]);
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, kKvTileBytes / 2, 1024);
+      const uint64_t b = make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
+      umma_f16_ss(tbase + 64, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+    }
+    umma_commit(&bar[1]);
+  }
+  __syncwarp();
+  mbar_wait(&bar[0], 0);
+  mbar_wait(&bar[1], 0);
+  tc_fence_after();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t laddr = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+  for (int c0 = 0; c0 < NQ; c0 += 8) {
+    float s[8], o[8];
+    tmem_ld_32x32b<8>(laddr + c0, s);
+    tmem_ld_32x32b<8>(laddr + 64 + c0, o);
+    tmem_wait_ld();
+    for (int c = 0; c < 8; ++c) {
+      s_out[(warp * 32 + lane) * NQ + c0 + c] = s[c];
+      o_out[(warp * 32 + lane) * NQ + c0 + c] = o[c];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 128);
+  }
+}
+
+template <int N>
+static cudaError_t launch_probe_n(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                                  const __nv_bfloat16* v, const __nv_bfloat16* p, float* s_out,
+                                  float* o_out, cudaStream_t stream) {
+  const int smem = 2 * kKvTileBytes + 2 * 64 * 256 + 64;
+  cudaError_t e =
+      cudaFuncSetAttribute(umma_probe_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  umma_probe_kernel<N><<<1, 128, smem, stream>>>(k, q, v, p, s_out, o_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_umma_probe(const __nv_bfloat16* k, const __nv_bfloat16* q,
+                              const __nv_bfloat16* v, const __nv_bfloat16* p, int nq,
+                              float* s_out, float* o_out, cudaStream_t stream) {
+  switch (nq) {
+    case 16: return launch_probe_n<16>(k, q, v, p, s_out, o_out, stream);
+    case 32: return launch_probe_n<32>(k, q, v, p, s_out, o_out, stream);
+    case 64: return launch_probe_n<64>(k, q, v, p, s_out, o_out, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rb

@@ -35,20 +35,17 @@ def sm_count(device=None) -> int:
     return _lib.sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
 
 
-def workspace(nbytes: int, device, stream_key: int) -> torch.Tensor:
-    """Zero-initialised relay-step workspace (partials + grid barrier), cached
-    per (device, stream).  The kernel leaves its barrier zeroed, so the buffer
-    is reused without clearing."""
-    key = (str(device), stream_key)
+def workspace(nbytes: int, device, stream_key: int, kind: str = "sys") -> torch.Tensor:
+    """Zero-initialised scratch, cached per (kind, device, stream).  kind
+    "sys": rb_system_attention's stream-K partials + semaphores (the kernel
+    leaves the semaphores zeroed, so the buffer is reusable without
+    clearing); kind "relay": rb_relay_attention's unmerged partial slots."""
+    key = (kind, str(device), stream_key)
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
         _workspaces[key] = buf
     return buf
-
-
-def step_workspace_bytes(n_rows, hq, hkv, s, grid) -> int:
-    return _lib.step_plan(n_rows, hq, hkv, s, grid)[1]
 
 
 def _check_bf16(name, t):
@@ -58,27 +55,9 @@ def _check_bf16(name, t):
         raise ContractError(f"{name}: head_dim must be the contiguous dimension")
 
 
-def _kv_strides(t, layout):
-    """(tokens, stride_tok, stride_head, hkv) of a shared-prefix K/V tensor:
-    'shd' = (s, hkv, 128) (the reference's layout), 'hsd' = (hkv, s, 128)."""
-    if layout == "shd":
-        return t.shape[0], t.stride(0), t.stride(1), t.shape[1]
-    if layout == "hsd":
-        return t.shape[1], t.stride(1), t.stride(0), t.shape[0]
-    raise ContractError(f"unknown kv layout {layout!r}")
-
-
-def _ws(ws, n_rows, hq, hkv, s, grid, dev):
-    if ws is None:
-        ws = workspace(step_workspace_bytes(n_rows, hq, hkv, s, grid), dev, _stream(dev))
-    return ws
-
-
 def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
                      o_sys=None, lse_sys=None, ws=None):
-    """Unmasked attention of every query row over the shared prefix
-    (`_system_attention`, attention.py:177-200): the relay step's system
-    tiles only.
+    """Unmasked attention of every query row over the shared prefix.
 
     q: (n_rows, hq, 128) bf16; sys_k/sys_v: (s, hkv, 128) for kv_layout
     'shd' (the reference's layout) or (hkv, s, 128) for 'hsd' (the
@@ -91,9 +70,16 @@ def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
     if sys_k.shape != sys_v.shape or sys_k.stride() != sys_v.stride():
         raise DimensionError(f"sys_k/sys_v shapes differ: {tuple(sys_k.shape)} vs {tuple(sys_v.shape)}")
     n_rows, hq, d = q.shape
-    s, st_tok, st_head, hkv = _kv_strides(sys_k, kv_layout)
-    if d != HEAD_DIM or sys_k.shape[-1] != HEAD_DIM:
-        raise DimensionError(f"head_dim must be {HEAD_DIM} (pad smaller dims), got {d}")
+    if kv_layout == "shd":
+        s, hkv, dk = sys_k.shape
+        st_tok, st_head = sys_k.stride(0), sys_k.stride(1)
+    elif kv_layout == "hsd":
+        hkv, s, dk = sys_k.shape
+        st_tok, st_head = sys_k.stride(1), sys_k.stride(0)
+    else:
+        raise ContractError(f"unknown kv_layout {kv_layout!r}")
+    if d != HEAD_DIM or dk != HEAD_DIM:
+        raise DimensionError(f"head_dim must be {HEAD_DIM} (pad smaller dims), got {d}/{dk}")
     if hkv < 1 or hq % hkv != 0:
         raise DimensionError(f"query heads {hq} not a multiple of kv heads {hkv}")
     dev = q.device
@@ -102,12 +88,15 @@ def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
     if lse_sys is None:
         lse_sys = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
     grid = sm_count(dev) if grid is None else grid
-    ws = _ws(ws, n_rows, hq, hkv, s, grid, dev)
+    stream = _stream(dev)
+    if ws is None:
+        _, need = _lib.sys_plan(n_rows, hq, hkv, s, grid)
+        ws = workspace(need, dev, stream)
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
     _lib.check(_lib.load().rb_system_attention(
         q.data_ptr(), q.stride(0), q.stride(1), n_rows, hq, hkv, HEAD_DIM,
         sys_k.data_ptr(), sys_v.data_ptr(), s, st_tok, st_head, float(scale), grid,
-        o_sys.data_ptr(), lse_sys.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev)),
+        o_sys.data_ptr(), lse_sys.data_ptr(), ws.data_ptr(), ws.numel(), stream),
         "rb_system_attention")
     return o_sys, lse_sys
 
@@ -115,15 +104,12 @@ def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
 def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
                       block_table=None, block_size=0, req_offset=None,
                       strides=None, causal=True, prefix_k=None, prefix_v=None,
-                      prefix_layout="hsd", scale=None, grid=None, out=None, out_fp32=False,
-                      lse_out=None, want_lse=True, ws=None):
-    """Per-request (context) attention, or with prefix_k/prefix_v the naive
-    baseline that re-reads the shared prefix per request; see
-    include/relay_b200.h:rb_context_attention.
+                      prefix_strides=None, o_sys=None, lse_sys=None, scale=None,
+                      out=None, out_fp32=False, lse_out=None, want_lse=True):
+    """Context (or relay, or naive-baseline) attention; see
+    include/relay_b200.h:rb_context_attention for the addressing modes.
 
     q: (n_rows, hq, 128) bf16; q_start int32 (b+1,); ctx_lens int32 (b,).
-    paged: k/v = one layer's pool (num_blocks, hkv, 128, bs), block_table
-    (b, width) int32; ragged: k/v (tokens, hkv, 128), req_offset int64 (b,).
     strides = (stride_block, stride_tok, stride_head) in elements.
     """
     _check_bf16("q", q)
@@ -135,23 +121,24 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
     if out is None:
         out = torch.empty((n_rows, hq, HEAD_DIM),
                           dtype=torch.float32 if out_fp32 else torch.bfloat16, device=dev)
+    out_fp32 = out.dtype == torch.float32
     if lse_out is None and want_lse:
         lse_out = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
-    s_prefix, p_tok, p_head = 0, 0, 0
+    s_prefix = 0
+    p_tok = p_head = 0
     if prefix_k is not None:
-        s_prefix, p_tok, p_head, _ = _kv_strides(prefix_k, prefix_layout)
+        s_prefix = prefix_strides[2]
+        p_tok, p_head = prefix_strides[0], prefix_strides[1]
     sb, stok, sh = strides
     bt_stride = block_table.stride(0) if block_table is not None else 0
-    grid = sm_count(dev) if grid is None else grid
-    ws = _ws(ws, n_rows, hq, hkv, 0, grid, dev)
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
     _lib.check(_lib.load().rb_context_attention(
-        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq,
-        hkv, HEAD_DIM, k.data_ptr(), v.data_ptr(), k.shape[0], _ptr(block_table), bt_stride,
-        block_size, _ptr(req_offset), sb, stok, sh, ctx_lens.data_ptr(), 1 if causal else 0,
-        _ptr(prefix_k), _ptr(prefix_v), s_prefix, p_tok, p_head, float(scale), grid,
-        out.data_ptr(), 1 if out.dtype == torch.float32 else 0, _ptr(lse_out), ws.data_ptr(),
-        ws.numel(), _stream(dev)), "rb_context_attention")
+        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, max_rows, hq, hkv,
+        HEAD_DIM, k.data_ptr(), v.data_ptr(), _ptr(block_table), bt_stride, block_size,
+        _ptr(req_offset), sb, stok, sh, ctx_lens.data_ptr(), 1 if causal else 0,
+        _ptr(prefix_k), _ptr(prefix_v), s_prefix, p_tok, p_head, _ptr(o_sys), _ptr(lse_sys),
+        float(scale), out.data_ptr(), 1 if out_fp32 else 0, _ptr(lse_out), _stream(dev)),
+        "rb_context_attention")
     return out, lse_out
 
 
@@ -159,13 +146,19 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
                     sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
                     strides=None, scale=None, grid=None, out=None, lse_out=None,
                     out_fp32=False, ws=None, phases=3):
-    """The relay decode step, rb_relay_step: ONE persistent kernel for the
-    system tiles, the context tiles and the fusion.  Returns (out, lse)."""
+    """The fused relay step (rb_relay_attention): system kernel (stream-K
+    partials, no merge) + context kernel whose epilogue merges the system
+    partials with the context state.  Returns (out, lse)."""
     _check_bf16("q", q)
     n_rows, hq, d = q.shape
     if d != HEAD_DIM:
         raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
-    s, s_tok, s_head, _ = _kv_strides(sys_k, sys_layout)
+    if sys_layout == "hsd":
+        _, s, _ = sys_k.shape
+        s_tok, s_head = sys_k.stride(1), sys_k.stride(0)
+    else:
+        s, _, _ = sys_k.shape
+        s_tok, s_head = sys_k.stride(0), sys_k.stride(1)
     dev = q.device
     b = ctx_lens.numel()
     if out is None:
@@ -174,17 +167,20 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
     if lse_out is None:
         lse_out = torch.empty((n_rows, hq), dtype=torch.float32, device=dev)
     grid = sm_count(dev) if grid is None else grid
-    ws = _ws(ws, n_rows, hq, hkv, s, grid, dev)
+    stream = _stream(dev)
+    if ws is None:
+        need = _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid)
+        ws = workspace(need, dev, stream, kind="relay")
     sb, stok, sh = strides
     bt_stride = block_table.stride(0) if block_table is not None else 0
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
-    _lib.check(_lib.load().rb_relay_step(
-        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq,
-        hkv, HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
-        v.data_ptr(), k.shape[0], _ptr(block_table), bt_stride, block_size, _ptr(req_offset),
-        sb, stok, sh, ctx_lens.data_ptr(), 1, 0, float(scale), grid, out.data_ptr(),
+    _lib.check(_lib.load().rb_relay_attention(
+        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq, hkv,
+        HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
+        v.data_ptr(), _ptr(block_table), bt_stride, block_size, _ptr(req_offset), sb, stok, sh,
+        ctx_lens.data_ptr(), float(scale), grid, out.data_ptr(),
         1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), ws.data_ptr(), ws.numel(),
-        phases, _stream(dev)), "rb_relay_step")
+        phases, stream), "rb_relay_attention")
     return out, lse_out
 
 
@@ -204,32 +200,21 @@ def relay_fusion_fp32(o_sys, lse_sys, o_ctx, lse_ctx, out=None, lse_out=None):
 
 
 def kv_append(k_new, v_new, slot_mapping, k_pool, v_pool, block_size):
-    """Scatter (n_tok, hkv, 128) new rows into one layer's pool
-    (num_blocks, hkv, 128, bs) in the swizzled block layout."""
+    """Scatter (n_tok, hkv, 128) new rows into a [num_blocks][hkv][bs][128] pool."""
     _check_bf16("k_new", k_new)
     n_tok, hkv, d = k_new.shape
     _lib.check(_lib.load().rb_kv_append(
         k_new.data_ptr(), v_new.data_ptr(), slot_mapping.data_ptr(), n_tok, k_pool.data_ptr(),
-        v_pool.data_ptr(), hkv, d, block_size, k_pool.stride(0), k_pool.stride(1),
-        _stream(k_new.device)), "rb_kv_append")
+        v_pool.data_ptr(), hkv, d, block_size, k_pool.stride(0), k_pool.stride(2),
+        k_pool.stride(1), _stream(k_new.device)), "rb_kv_append")
 
 
 def umma_probe(k, q, v, p):
-    """Debug: the system tiles' tcgen05 operand layouts on one tile."""
+    """Debug: run the system kernel's tcgen05 operand layouts on one tile."""
     nq = q.shape[0]
     s_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
     o_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
     _lib.check(_lib.load().rb_debug_umma_probe(
         k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), nq, s_out.data_ptr(),
         o_out.data_ptr(), _stream(k.device)), "rb_debug_umma_probe")
-    return s_out, o_out
-
-
-def ctx_probe(k, q, v, p, block_size):
-    """Debug: the paged-context tcgen05 operand layouts of rb_relay_step on one tile."""
-    s_out = torch.empty((128, 32), dtype=torch.float32, device=k.device)
-    o_out = torch.empty((128, 32), dtype=torch.float32, device=k.device)
-    _lib.check(_lib.load().rb_debug_ctx_probe(
-        k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), block_size, s_out.data_ptr(),
-        o_out.data_ptr(), _stream(k.device)), "rb_debug_ctx_probe")
     return s_out, o_out

@@ -7,21 +7,13 @@ SystemKvCache  <- /root/reference/pkg/src/relayserve/kvcache.py:36-63
     are dense and every byte is read exactly once per decode step.
 
 PagedKvCache   <- kvcache.py:113-271 (BlockPool + PagedKvCache)
-    Per-request context K/V in fixed-size blocks (16, 32 or 64 tokens).  Pool
-    layout per layer is bf16 [num_blocks][hkv][128][block_size]: one
-    (block, kv head) pair is a contiguous 128 x block_size tile (4 KB at
-    block_size 16) holding the block TRANSPOSED (tokens contiguous) with the
-    UMMA swizzle of its row width applied (paged_swizzle in rb_common.cuh:
-    16-byte chunk c of row d goes to chunk c ^ (d mod (2*bs/16))).  That tile
-    is at once the MN-major K operand and the K-major V^T operand of the
-    relay step's tensor-core MMAs, so the kernel moves it with ONE 4 KB bulk
-    copy and never re-lays it out (a [bs][128] layout needs two 2 KB TMA boxes
-    per block, and the TMA unit's ~70 ns per-op cost caps 2 KB boxes at ~27
-    GB/s per SM -- profiles/microbench_tma.cu).  Read in place through an
-    int32 block table -- no gather copy (the reference copies to contiguous
-    scratch, kvcache.py:237-262).  Block accounting (register / grow /
-    release, CapacityError) follows BlockPool exactly; it is host
-    bookkeeping, not device work.
+    Per-request context K/V in fixed-size blocks.  Pool layout per layer is
+    bf16 [num_blocks][hkv][block_size][128]: one (block, head) pair is a
+    contiguous block_size x 256 B run (4 KB at block_size 16), read in place
+    by the context kernel through an int32 block table -- no gather copy
+    (the reference copies to contiguous scratch, kvcache.py:237-262).
+    Block accounting (register / grow / release, CapacityError) follows
+    BlockPool exactly; it is host bookkeeping, not device work.
 """
 
 from __future__ import annotations
@@ -145,36 +137,18 @@ class BlockPool:
         return len(table)
 
 
-def block_permutation(block_size):
-    """Element index inside a pool block (flattened (128, bs) storage) of the
-    logical element (d, token): the paged_swizzle of rb_common.cuh."""
-    rb = 2 * block_size
-    mask = rb // 16 - 1
-    d = torch.arange(HEAD_DIM).view(-1, 1)
-    t = torch.arange(block_size).view(1, -1)
-    off = d * rb + t * 2
-    sw = off ^ (((off >> 7) & mask) << 4)
-    return (sw // 2).reshape(-1)
-
-
 class PagedKvCache:
     """Block-paged context K/V for all layers, resident in HBM.
 
-    k_pool / v_pool: bf16 (layers, num_blocks, hkv, 128, block_size), each
-    (block, head) tile swizzled (module docstring); use append / gather, not
-    raw indexing, to move tokens in and out.
+    k_pool / v_pool: bf16 (layers, num_blocks, hkv, block_size, 128).
     """
-
-    SUPPORTED_BLOCK_SIZES = (16, 32, 64)
 
     def __init__(self, layers, kv_heads, num_blocks, block_size=DEFAULT_BLOCK_SIZE,
                  device="cuda"):
-        if block_size not in self.SUPPORTED_BLOCK_SIZES:
-            raise ContractError(f"block_size must be one of {self.SUPPORTED_BLOCK_SIZES}")
         self.pool = BlockPool(num_blocks, block_size)
         self.layers = layers
         self.kv_heads = kv_heads
-        shape = (layers, num_blocks, kv_heads, HEAD_DIM, block_size)
+        shape = (layers, num_blocks, kv_heads, block_size, HEAD_DIM)
         self.k_pool = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.v_pool = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self._layer_lengths: dict = {}
@@ -239,25 +213,19 @@ class PagedKvCache:
                             dtype=torch.int32, device=self.device)
 
     def strides(self):
-        """(stride_block, stride_tok, stride_head) of one layer's pool, in
-        elements (stride_tok is 0: tokens live inside the swizzled block)."""
+        """(stride_block, stride_tok, stride_head) of one layer's pool."""
         p = self.k_pool[0]
-        return p.stride(0), 0, p.stride(1)
-
-    def _unswizzle(self, blocks):
-        """(n, hkv, 128, bs) swizzled tiles -> logical (n, bs, hkv, 128)."""
-        bs = self.block_size
-        perm = block_permutation(bs).to(blocks.device)
-        flat = blocks.reshape(blocks.shape[0], blocks.shape[1], HEAD_DIM * bs)[:, :, perm]
-        return flat.reshape(blocks.shape[0], blocks.shape[1], HEAD_DIM, bs).permute(0, 3, 1, 2)
+        return p.stride(0), p.stride(2), p.stride(1)
 
     def gather(self, request_id, layer):
         """Contiguous (c, hkv, 128) copy of a request's K/V (tests/debug)."""
         c = self._layer_lengths[request_id][layer]
         table = self.pool.tables[request_id]
         bs = self.block_size
-        nb = -(-c // bs)
-        idx = torch.tensor(table[:nb], dtype=torch.long, device=self.k_pool.device)
-        k = self._unswizzle(self.k_pool[layer, idx]).reshape(nb * bs, self.kv_heads, HEAD_DIM)
-        v = self._unswizzle(self.v_pool[layer, idx]).reshape(nb * bs, self.kv_heads, HEAD_DIM)
-        return k[:c], v[:c]
+        ks, vs = [], []
+        for i in range(0, c, bs):
+            blk = table[i // bs]
+            take = min(bs, c - i)
+            ks.append(self.k_pool[layer, blk, :, :take].transpose(0, 1))
+            vs.append(self.v_pool[layer, blk, :, :take].transpose(0, 1))
+        return torch.cat(ks), torch.cat(vs)

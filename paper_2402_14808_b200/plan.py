@@ -1,5 +1,4 @@
-"""Python mirror of the relay step's stream-K plan of the system tiles
-(csrc/rb_plan.h) and of its context-unit numbering.
+"""Python mirror of the system kernel's stream-K work plan (csrc/rb_plan.h).
 
 Used by host-logic tests (no GPU needed) and by DESIGN.md's worked
 examples; the kernels compute the same integers on the device.
@@ -72,14 +71,3 @@ class SysPlan:
 
     def cta_ranges(self):
         return [(self.cta_begin(c), self.cta_begin(c + 1)) for c in range(self.grid)]
-
-
-def context_units(q_rows, g, hkv, nq):
-    """Per-request unit prefix U (U[r] = context units before request r) for
-    query counts q_rows[r]: hkv * ceil(m_r * g / nq) units per request.
-    Context unit v of the relay step is (request r, kv head, q-tile) with
-    U[r] <= v < U[r+1]; each CTA's scheduler hands them out dynamically."""
-    U = [0]
-    for m in q_rows:
-        U.append(U[-1] + hkv * (-(-m * g // nq)))
-    return U

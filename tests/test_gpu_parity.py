@@ -330,3 +330,46 @@ def test_c2_full_size_relay_vs_naive_and_oracle_heads(rb, oracle):
     ref, ref_lse = oracle.relay_attention(qn, sk, sv, ck, cv, return_lse=True)
     assert_close(out.float().cpu().numpy()[:, heads], ref[:, 0], "C2 relay vs oracle (3 heads)")
     assert_close(lse.cpu().numpy()[:, heads], ref_lse[:, 0], "C2 lse vs oracle", lse=True)
+
+
+@pytest.mark.parametrize("grid", [None, 5, 37])
+def test_fused_relay_equals_two_kernel_path(rb, oracle, grid):
+    """rb_relay_attention (unmerged system partials merged in the context
+    epilogue) vs rb_system_attention + rb_context_attention(o_sys): same math,
+    different merge order -> agree to fp32 rounding; both vs the oracle."""
+    from paper_2402_14808_b200 import kernels
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    rng = np.random.default_rng(77)
+    b, hq, hkv, s = 9, 12, 3, 1500
+    lens = [int(x) for x in rng.integers(1, 200, size=b)]
+    q = bf16(rng.standard_normal((b, hq, 128)))
+    sk = bf16(rng.standard_normal((s, hkv, 128)))
+    sv = bf16(rng.standard_normal((s, hkv, 128)))
+    ck = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    cv = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    sys_cache = SystemKvCache.from_shd([sk], [sv])
+    paged, bt, cl = make_paged(rb, ck, cv, hkv)
+    qd = dev_bf16(q)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32)
+    out, lse = step(qd)
+    o_sys, lse_sys = kernels.system_attention(qd, sys_cache.keys[0], sys_cache.values[0],
+                                              kv_layout="hsd", grid=grid)
+    out2, lse2 = kernels.context_attention(
+        qd, step.q_start, paged.k_pool[0], paged.v_pool[0], cl, max_rows=hq // hkv, hkv=hkv,
+        block_table=bt, block_size=16, strides=paged.strides(), o_sys=o_sys, lse_sys=lse_sys,
+        out_fp32=True)
+    torch.cuda.synchronize()
+    assert (out - out2).abs().max().item() < 1e-5
+    assert (lse - lse2).abs().max().item() < 1e-5
+    g = hq // hkv
+    ref, ref_lse = oracle.relay_attention(
+        q[:, None], oracle.expand_kv(sk, g), oracle.expand_kv(sv, g),
+        [oracle.expand_kv(x, g) for x in ck], [oracle.expand_kv(x, g) for x in cv],
+        return_lse=True)
+    assert_close(out.cpu().numpy(), ref[:, 0], f"fused relay grid={grid}")
+    assert_close(lse.cpu().numpy(), ref_lse[:, 0], "fused relay lse", lse=True)
+    # deterministic run to run
+    out3, _ = step(qd)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out3)

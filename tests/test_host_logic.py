@@ -18,7 +18,7 @@ from paper_2402_14808_b200.plan import SysPlan
 ])
 def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
     p = SysPlan(n_rows, hq, hkv, s, grid)
-    f, _ = _lib.step_plan(n_rows, hq, hkv, s, grid)
+    f, _ = _lib.sys_plan(n_rows, hq, hkv, s, grid)
     assert (p.nq, p.n_qt, p.tpu, p.n_units, p.total, p.grid, p.max_parts) == \
         (f["nq"], f["n_qt"], f["tpu"], f["n_units"], f["total"], f["grid"], f["max_parts"])
     ranges = p.cta_ranges()
@@ -33,14 +33,6 @@ def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
         first = u * p.tpu
         owners = {p.owner(x) for x in range(first, first + p.tpu)}
         assert len(owners) == p.unit_parts(u) <= p.max_parts
-
-
-def test_context_unit_prefix():
-    from paper_2402_14808_b200.plan import context_units
-    assert context_units([1, 1, 1], 1, 52, 32) == [0, 52, 104, 156]
-    assert context_units([6, 1], 4, 2, 32) == [0, 2, 4]       # 24 rows -> one q-tile
-    assert context_units([9, 1], 4, 2, 32) == [0, 4, 6]       # 36 rows -> two q-tiles
-    assert context_units([0, 3], 8, 1, 16) == [0, 0, 2]
 
 
 def test_head_ranges():
