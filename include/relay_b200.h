@@ -114,18 +114,30 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
 /*
  * The whole relay decode step in one call -- `relay_attention_ragged`
  * (attention.py:203-243) over a shared prefix and paged (or ragged) context:
- * the tcgen05 system kernel writes its stream-K partial slots into
- * `workspace` without merging them, and the context kernel (launched with
- * programmatic dependent launch, so it streams context K/V while the system
- * kernel drains) merges every system slot of a (row, head) with its own
- * context state in ONE LSE-weighted combine -- the relay fusion
- * (attention.py:137-157) -- writing `out` (bf16 or fp32) and the fused LSE.
+ * the tcgen05 system kernel (grid_cap CTAs, see rb_relay_sys_grid) writes
+ * its stream-K partial slots into `workspace` without merging them and
+ * publishes each unit on a counter; the context kernel (programmatic
+ * dependent launch: it starts right away on the SMs the system kernel does
+ * not use and streams context K/V concurrently) merges every system slot of
+ * a (row, head) with its own context state, once that unit is published, in
+ * ONE LSE-weighted combine -- the relay fusion (attention.py:137-157) --
+ * writing `out` (bf16 or fp32) and the fused LSE.
  * Arguments are those of rb_system_attention + rb_context_attention (causal).
- * workspace: rb_relay_workspace_bytes(...) bytes, no initialisation needed.
+ * workspace: rb_relay_workspace_bytes(...) bytes, zero-filled before first use;
+ * the kernels leave it zeroed (its header holds the context kernel's work
+ * counters), so one buffer serves every step on a stream.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
  * (profiling: phase 2 consumes the slots a previous phase-1 call wrote).
  */
 int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes);
+/*
+ * System-kernel CTA count for rb_relay_attention's grid_cap: the two kernels
+ * run concurrently, the system kernel on a share of the SMs proportional to
+ * its HBM bytes (ctx_tokens = total context tokens of the batch), the
+ * context kernel on the rest and on every SM the system kernel releases.
+ */
+int rb_relay_sys_grid(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sm_count,
+                      int* grid);
 int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_stride,
                        const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
                        const void* sys_k, const void* sys_v, int s, long long sys_stride_tok,
@@ -170,6 +182,8 @@ int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void*
  * V-producer end, exit).  NULL disables.  For profiling only.
  */
 int rb_debug_set_timestamps(void* buf);
+/* Diagnostics: set tuning knob `id` (0..7) for later launches (A/B runs). */
+int rb_debug_set_knob(int id, int value);
 
 #ifdef __cplusplus
 }

@@ -21,8 +21,8 @@ RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
 EXPORTS = (
     "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
     "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
-    "rb_relay_workspace_bytes", "rb_relay_attention",
-    "rb_debug_umma_probe", "rb_debug_set_timestamps",
+    "rb_relay_workspace_bytes", "rb_relay_sys_grid", "rb_relay_attention",
+    "rb_debug_umma_probe", "rb_debug_set_timestamps", "rb_debug_set_knob",
 )
 
 _lib = None
@@ -53,6 +53,7 @@ def load():
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
         i32, vp, vp, i32, i64, i64,                      # causal, prefix
         vp, vp, f32, vp, i32, vp, vp]                    # o_sys .. stream
+    lib.rb_relay_sys_grid.argtypes = [i32, i32, i32, i32, i64, i32, ctypes.POINTER(i32)]
     lib.rb_relay_workspace_bytes.argtypes = [i32, i32, i32, i32, i32,
                                              ctypes.POINTER(ctypes.c_size_t)]
     lib.rb_relay_attention.argtypes = [
@@ -64,11 +65,16 @@ def load():
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
     lib.rb_debug_set_timestamps.argtypes = [vp]
+    lib.rb_debug_set_knob.argtypes = [ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:
         if name not in ("rb_last_error", "rb_abi_version"):
             getattr(lib, name).restype = i32
     if lib.rb_abi_version() != 1:
         raise ImportError("librelay_b200.so ABI mismatch; rebuild")
+    # diagnostics: RB_KNOBS="0=1,2=5" sets tuning knobs (rb_debug_set_knob)
+    for kv in filter(None, os.environ.get("RB_KNOBS", "").split(",")):
+        k, v = kv.split("=")
+        lib.rb_debug_set_knob(int(k), int(v))
     _lib = lib
     return lib
 
@@ -100,6 +106,14 @@ def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int)
     out = ctypes.c_size_t(0)
     check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
           "rb_relay_workspace_bytes")
+    return out.value
+
+
+def relay_sys_grid(n_rows: int, hq: int, hkv: int, s: int, ctx_tokens: int, sm_count: int) -> int:
+    """System-kernel CTA count of the concurrent relay step (rb_relay_sys_grid)."""
+    out = ctypes.c_int(0)
+    check(load().rb_relay_sys_grid(n_rows, hq, hkv, s, ctx_tokens, sm_count, ctypes.byref(out)),
+          "rb_relay_sys_grid")
     return out.value
 
 

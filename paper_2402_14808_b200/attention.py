@@ -378,9 +378,11 @@ class RelayDecodeStep:
     q: (b, hq, 128) bf16 -> out (b, hq, 128) bf16 and fused lse (b, hq) fp32.
     One rb_relay_attention call = two kernels on the current stream: the
     tcgen05 system kernel (shared prefix read once, stream-K partials left
-    unmerged) and the paged context kernel, launched with programmatic
-    dependent launch, whose epilogue merges the system partials with the
-    context state (relay fusion).  All buffers are preallocated, so the step
+    unmerged, each unit published on a counter) on a byte-proportional share
+    of the SMs, and the paged context kernel, launched with programmatic
+    dependent launch so it streams concurrently on the other SMs, whose
+    epilogue merges the system partials with the context state (relay
+    fusion).  All buffers are preallocated, so the step
     can be captured in a CUDA graph.
     """
 
@@ -395,8 +397,12 @@ class RelayDecodeStep:
         if hq % self.hkv != 0 or paged_cache.kv_heads != self.hkv:
             raise DimensionError("query heads must be a multiple of the (shared) kv heads")
         dev = block_table.device
-        self.grid = kernels.sm_count(dev) if grid is None else grid
         from . import _lib
+        if grid is None:
+            # concurrent split: system CTAs by their share of the step's HBM bytes
+            grid = _lib.relay_sys_grid(self.b, hq, self.hkv, sys_cache.system_len,
+                                       int(ctx_lens.sum().item()), kernels.sm_count(dev))
+        self.grid = grid
         self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
@@ -448,26 +454,21 @@ class RelayDecodeStep:
 
         qkv_host: pinned bf16 (3, b, h, 128) holding this step's q, k_new,
         v_new; out_host: pinned bf16 (b, hq, 128).  Returns a callable that
-        replays the step on the current stream.  Inside the graph the q H2D
-        feeds the system kernel directly while the k/v H2D and the paged
-        append run on a forked stream; the context kernel joins both.  Refill
-        `qkv_host` between calls.
+        replays the step on the current stream: one H2D of the inputs, the
+        paged append of the new tokens, the relay step, the D2H of the output.
+        Refill `qkv_host` between calls.
         """
         dev = self.out.device
         qkv_dev = torch.empty(qkv_host.shape, dtype=torch.bfloat16, device=dev)
         main = torch.cuda.current_stream(dev)
-        side = torch.cuda.Stream(device=dev)
 
         def body():
-            cur = torch.cuda.current_stream(dev)
-            side.wait_stream(cur)
-            qkv_dev[0].copy_(qkv_host[0], non_blocking=True)
-            self.system(qkv_dev[0])
-            with torch.cuda.stream(side):
-                qkv_dev[1:].copy_(qkv_host[1:], non_blocking=True)
-                self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
-            cur.wait_stream(side)
-            out, _ = self.context(qkv_dev[0])
+            # one H2D of [q|k_new|v_new], the paged append, then the relay step
+            # (system + context kernels run concurrently; the append is the
+            # system kernel's PDL primary, so its prologue overlaps it)
+            qkv_dev.copy_(qkv_host, non_blocking=True)
+            self.paged.append_slots(self.layer, qkv_dev[1], qkv_dev[2], slot_mapping)
+            out, _ = self(qkv_dev[0])
             out_host.copy_(out, non_blocking=True)
 
         warm = torch.cuda.Stream(device=dev)
@@ -479,7 +480,7 @@ class RelayDecodeStep:
         with torch.cuda.graph(graph):
             body()
         self._host_graph = graph  # keep alive with its buffers
-        self._host_graph_bufs = (qkv_dev, side)
+        self._host_graph_bufs = (qkv_dev,)
         return graph.replay
 
 

@@ -26,6 +26,8 @@ namespace rb {
 cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
                                     cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
+cudaError_t launch_relay_fuse(const rb_sys_plan&, int, int, const float*, const float*, int*,
+                              const float*, void*, int, float*, int*, cudaStream_t);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
                                 float*, long long, int, cudaStream_t);
 cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
@@ -38,6 +40,11 @@ cudaError_t launch_kv_append(const __nv_bfloat16*, const __nv_bfloat16*, const i
 
 static thread_local std::string g_err;
 static unsigned long long* g_debug_ts = nullptr;  // test-only instrumentation
+// context-kernel stamps start after 1024 system CTAs x 8 slots
+static constexpr long long kCtxTsOffset = 1024 * 8;
+namespace rb {
+int g_knobs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+}
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -224,19 +231,31 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.p_stride_tok = p_stride_tok;
   a.p_stride_head = p_stride_head;
   a.s_prefix = s_prefix;
-  a.sys_part_acc = nullptr;
-  a.sys_part_ml = nullptr;
+  a.ctx_part = nullptr;
   a.o_sys = o_sys;
   a.lse_sys = lse_sys;
   a.out = out;
   a.out_fp32 = out_fp32;
   a.lse_out = lse_out;
   a.scale_log2 = scale * rb::kLog2e;
+  a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
+  a.sched = nullptr;  // no workspace: static item order
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
                      "context attention launch");
 }
 
 // ------------------------------------------------- fused relay decode step
+// Relay workspace: [256 B header: context claim / exit counters, fuse exit
+// counter][n_units system-unit publication counters, 256-aligned][context
+// partials, n_rows * hq * 132 floats][part m/l][part acc].
+static void relay_ws_layout(const rb_sys_plan& p, size_t* cnt_bytes, size_t* cpart_bytes,
+                            size_t* ml_bytes, size_t* acc_bytes) {
+  *cnt_bytes = ((size_t)p.n_units * sizeof(int) + 255) & ~(size_t)255;
+  *cpart_bytes = ((size_t)p.n_rows * p.hq * 132 * sizeof(float) + 255) & ~(size_t)255;
+  *ml_bytes = ((size_t)p.n_units * p.max_parts * 2 * p.nq * sizeof(float) + 255) & ~(size_t)255;
+  *acc_bytes = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
+}
+
 int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes) {
   long long f[8];
   size_t dummy = 0;
@@ -244,9 +263,17 @@ int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, s
   if (st != RB_OK) return st;
   rb_sys_plan p;
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, grid_cap);
-  const size_t ml = ((size_t)p.n_units * p.max_parts * 2 * p.nq * sizeof(float) + 255) & ~(size_t)255;
-  const size_t acc = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
-  *bytes = 256 + ml + acc;
+  size_t cnt, cpart, ml, acc;
+  relay_ws_layout(p, &cnt, &cpart, &ml, &acc);
+  *bytes = 256 + cnt + cpart + ml + acc;
+  return RB_OK;
+}
+
+int rb_relay_sys_grid(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sm_count,
+                      int* grid) {
+  if (n_rows < 1 || hq < 1 || hkv < 1 || hq % hkv != 0 || s < 1 || sm_count < 1 || ctx_tokens < 0)
+    return fail(RB_ERR_DIMENSION, "bad relay split arguments");
+  *grid = rb_relay_split(n_rows, hq, hkv, s, ctx_tokens, sm_count);
   return RB_OK;
 }
 
@@ -280,11 +307,13 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   sa.o_sys = nullptr;
   sa.lse_sys = nullptr;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  const size_t ml = ((size_t)sa.plan.n_units * sa.plan.max_parts * 2 * sa.plan.nq * sizeof(float) +
-                     255) & ~(size_t)255;
-  sa.counters = nullptr;
-  sa.part_ml = reinterpret_cast<float*>(ws + 256);
-  sa.part_acc = reinterpret_cast<float*>(ws + 256 + ml);
+  size_t cnt, cpart, ml, acc_b;
+  relay_ws_layout(sa.plan, &cnt, &cpart, &ml, &acc_b);
+  int* header = reinterpret_cast<int*>(ws);
+  float* ctx_part = reinterpret_cast<float*>(ws + 256 + cnt);
+  sa.counters = reinterpret_cast<int*>(ws + 256);
+  sa.part_ml = reinterpret_cast<float*>(ws + 256 + cnt + cpart);
+  sa.part_acc = reinterpret_cast<float*>(ws + 256 + cnt + cpart + ml);
   sa.debug_ts = g_debug_ts;
   sa.defer_merge = 1;
   CUtensorMap tk, tv;
@@ -320,16 +349,26 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.pk = a.pv = nullptr;
   a.p_stride_tok = a.p_stride_head = 0;
   a.s_prefix = 0;
-  a.sys_part_acc = sa.part_acc;
-  a.sys_part_ml = sa.part_ml;
-  a.sys_plan = sa.plan;
+  a.ctx_part = ctx_part;
   a.o_sys = nullptr;
   a.lse_sys = nullptr;
   a.out = out;
   a.out_fp32 = out_fp32;
   a.lse_out = lse_out;
   a.scale_log2 = scale * rb::kLog2e;
-  return cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
+  a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
+  a.sched = header;  // workspace header: dynamic item counters
+  if (!(phases & 1)) {
+    // context phase alone (profiling): the slots of an earlier phase-1 call
+    // are complete; mark every unit published (the fuse kernel rearms them)
+    cudaError_t me = cudaMemsetAsync(sa.counters, 0x3f, (size_t)sa.plan.n_units * sizeof(int), cs);
+    if (me != cudaSuccess) return cuda_status(me, "relay counters");
+  }
+  st = cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
+  if (st != RB_OK) return st;
+  return cuda_status(rb::launch_relay_fuse(sa.plan, n_rows, hq, sa.part_acc, sa.part_ml, sa.counters,
+                                           ctx_part, out, out_fp32, lse_out, header + 2, cs),
+                     "relay fuse launch");
 }
 
 int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx,
@@ -353,6 +392,12 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
                            n_tok, hkv, block_size, stride_block, stride_tok, stride_head,
                            static_cast<cudaStream_t>(stream)),
       "kv append launch");
+}
+
+int rb_debug_set_knob(int id, int value) {
+  if (id < 0 || id >= 8) return fail(RB_ERR_CONTRACT, "knob %d out of range", id);
+  rb::g_knobs[id] = value;
+  return RB_OK;
 }
 
 int rb_debug_set_timestamps(void* buf) {

@@ -1,35 +1,35 @@
-// Request-context attention over paged KV, with the relay fusion fused into
-// the epilogue; plus the standalone relay-fusion kernel and the paged KV
-// append used by the decode step.
+// Request-context attention over paged KV (the context segment of the relay
+// decode step), the relay fusion, and the paged KV append.
 //
-// One kernel, three roles (selected by the arguments, not by a backend):
+// One kernel (ctx_cta_kernel), three roles selected by the arguments:
 //  * context attention  -- `_context_attention` / causal `attention_with_lse`
 //    (/root/reference/pkg/src/relayserve/attention.py:96-134,160-174):
-//    query row t of request r attends context keys 0 .. c_r - m_r + t.
-//  * relay              -- the same plus, in the epilogue, the LSE merge with
-//    the system partial (o_sys, lse_sys) of the same (row, head)
-//    (`relay_fusion`, attention.py:137-157), writing the fused output and
-//    the fused LSE: the two partial outputs never make an extra HBM trip.
+//    query row t of request r attends context keys 0 .. c_r - m_r + t;
+//    optionally fused with a given system partial (o_sys, lse_sys):
+//    `relay_fusion` (attention.py:137-157) in the epilogue.
+//  * relay partials     -- inside rb_relay_attention: the unnormalised
+//    context state (O, m, l) of every (row, head) goes to the workspace and
+//    relay_fuse_kernel merges it with the system kernel's stream-K parts;
+//    the system and context kernels run concurrently on disjoint SMs.
 //  * naive baseline     -- a shared prefix segment (the system K/V, shared in
 //    storage) read again by every request before its context: the
 //    per-request `baseline_attention` (attention.py:266-296), i.e. the
 //    "vLLM-PS" baseline the paper compares against.
 //
-// Memory-bound design (HBM roofline): grid = (request,
-// kv head, row tile); 4 warps stride over 16-token chunks.  Each warp owns a
-// private 2-slot smem ring filled by cp.async.bulk (one 4 KB copy per paged
-// (block, head) run of K and of V, completing on an mbarrier), so a whole
-// 128-token context is in flight at once without costing registers.  A
-// half-warp reads one 256-byte key row from smem (16 B per lane), dot
-// products reduce with 4 xor-shuffles, online softmax in the log2 domain per
-// half-warp, then an smem merge of the 8 partial states, the fusion, and one
-// coalesced store per row.
+// Memory-bound design (HBM roofline).  Work item =
+// (request, kv head, row tile of up to R query rows); items are claimed
+// dynamically by persistent CTAs (2 per SM).  Per CTA: a scheduler warp
+// publishes items (geometry, block-table entries, query rows) in a smem
+// queue; 4 worker warps split each item's 16-token chunks (K 4 KB + V 4 KB
+// per chunk, streamed with cp.async through per-warp 3-slot rings -- the LSU
+// path sustains HBM rate on scattered 4 KB paged blocks where the bulk-copy
+// engine manages ~19 GB/s per SM, profiles/microbench_scatter.cu) and run
+// QK^T / PV on the tensor cores with mma.sync (16 query rows x 16 keys per
+// chunk); a merger warp combines the 4 partial states and writes the result.
 #include "rb_common.cuh"
 #include "rb_args.cuh"
 
 namespace rb {
-
-
 
 constexpr int kChunk = 16;                       // tokens per chunk
 constexpr int kRowBytes = RB_HEAD_DIM * 2;       // 256 B per key row
@@ -48,76 +48,6 @@ __device__ __forceinline__ const __nv_bfloat16* ctx_row(const KvView& kv, const 
   return base + off + h * kv.stride_head;
 }
 
-template <int R>
-struct RowState {
-  float m[R], l[R], acc[R][8];
-};
-
-// One 16-key chunk for a half-warp: keys key0 + 2p + hw, p = 0..7, K/V rows
-// already in registers.  `lim[i]` is the exclusive key bound of row i inside
-// this segment; keys at or past it contribute nothing (their V rows may hold
-// stale data and are zeroed, never multiplied).
-template <int R>
-__device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[R][8],
-                                             const uint4 (&kr)[8], uint4 (&vr)[8],
-                                             int key0, int hw, const int (&lim)[R], float scale_log2,
-                                             int max_lim) {
-  float x[R][8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    float kf[8];
-    kf[0] = bf16_lo(kr[p].x); kf[1] = bf16_hi(kr[p].x);
-    kf[2] = bf16_lo(kr[p].y); kf[3] = bf16_hi(kr[p].y);
-    kf[4] = bf16_lo(kr[p].z); kf[5] = bf16_hi(kr[p].z);
-    kf[6] = bf16_lo(kr[p].w); kf[7] = bf16_hi(kr[p].w);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      float s = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s = fmaf(qf[i][e], kf[e], s);
-      x[i][p] = s;
-    }
-    if (key0 + 2 * p + hw >= max_lim) vr[p] = make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      float s = x[i][p];
-      s += __shfl_xor_sync(0xffffffffu, s, 8);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      const int key = key0 + 2 * p + hw;
-      x[i][p] = key < lim[i] ? s * scale_log2 : -INFINITY;
-    }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    float cm = x[i][0];
-#pragma unroll
-    for (int p = 1; p < 8; ++p) cm = fmaxf(cm, x[i][p]);
-    if (cm == -INFINITY) continue;  // no valid key of this row in this chunk half
-    const float mn = fmaxf(st.m[i], cm);
-    const float al = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - mn);
-    st.m[i] = mn;
-    float ps = 0.f;
-    float a[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] = st.acc[i][e] * al;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const float pr = fast_exp2(x[i][p] - mn);
-      ps += pr;
-      a[0] = fmaf(pr, bf16_lo(vr[p].x), a[0]); a[1] = fmaf(pr, bf16_hi(vr[p].x), a[1]);
-      a[2] = fmaf(pr, bf16_lo(vr[p].y), a[2]); a[3] = fmaf(pr, bf16_hi(vr[p].y), a[3]);
-      a[4] = fmaf(pr, bf16_lo(vr[p].z), a[4]); a[5] = fmaf(pr, bf16_hi(vr[p].z), a[5]);
-      a[6] = fmaf(pr, bf16_lo(vr[p].w), a[6]); a[7] = fmaf(pr, bf16_hi(vr[p].w), a[7]);
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) st.acc[i][e] = a[e];
-    st.l[i] = st.l[i] * al + ps;
-  }
-}
 
 // Work item = (request r, kv head h, row tile z).  Geometry of one item.
 template <int R>
@@ -126,675 +56,645 @@ struct CtxItem {
   long long roff;  // ragged mode: first token of request r
 };
 
-template <int R>
-__device__ __forceinline__ CtxItem<R> ctx_item(const CtxArgs& a, int item, int n_z, int n_pre) {
-  CtxItem<R> it;
-  it.z = item % n_z;
-  it.h = (item / n_z) % a.hkv;
-  it.r = item / (n_z * a.hkv);
-  it.row0 = __ldg(a.q_start + it.r);
-  it.m_r = __ldg(a.q_start + it.r + 1) - it.row0;
-  it.nrows = it.m_r * a.g;
-  it.c_r = __ldg(a.ctx_lens + it.r);
-  it.roff = a.ctx.req_offset != nullptr ? __ldg(a.ctx.req_offset + it.r) : 0;
-  const int rbase = it.z * R;
-  if (rbase >= it.nrows) {
-    it.max_lim = 0;
-    it.n_chunks = 0;
-    return it;
+// Issue the cp.async copies of one 16-token chunk (rows 0 .. n-1 of K at kb
+// and V at vb, row stride tok_stride elements) into an 8 KB slot [K|V][16
+// rows][256 B] whose 16-byte columns are XOR-swizzled by (row & 7), so the
+// ldmatrix reads of the MMA path are bank-conflict free.  Lane (row0 = lane
+// / 16, c16 = lane % 16) copies 16 B of rows row0 + 2i; rows >= n are
+// zero-filled (never stale: their probabilities are 0 but 0 * NaN is not).
+__device__ __forceinline__ uint32_t slot_off(int row, int c16) {
+  return static_cast<uint32_t>(row * kRowBytes + ((c16 ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ void chunk_cp_async(uint8_t* slot, const __nv_bfloat16* kb,
+                                               const __nv_bfloat16* vb, long long tok_stride, int n,
+                                               int lane) {
+  const int row0 = lane >> 4, c16 = lane & 15;
+  // row = row0 + 2i, (row & 7) = row0 | (2i & 6): swizzled column c16 ^ row0 ^ (2i & 6)
+  const int cx = c16 ^ row0;
+  uint8_t* d = slot + row0 * kRowBytes;
+  const char* ks = reinterpret_cast<const char*>(kb + row0 * tok_stride + c16 * 8);
+  const char* vs = reinterpret_cast<const char*>(vb + row0 * tok_stride + c16 * 8);
+  const long long st2 = 4 * tok_stride;  // bytes between rows row and row + 2
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool ok = row0 + 2 * i < n;
+    const uint32_t off = i * 2 * kRowBytes + ((cx ^ ((2 * i) & 6)) << 4);
+    cp_async_16(d + off, ok ? ks + i * st2 : ks, ok ? 16u : 0u);
+    cp_async_16(d + kChunk * kRowBytes + off, ok ? vs + i * st2 : vs, ok ? 16u : 0u);
   }
-  const int t_last = (min(rbase + R, it.nrows) - 1) / a.g;
-  it.max_lim = a.causal ? it.c_r - it.m_r + t_last + 1 : it.c_r;
-  it.n_chunks = n_pre + (it.max_lim + kChunk - 1) / kChunk;
-  return it;
 }
 
-// Everything a warp needs to start an item, loaded lane-parallel one item
-// ahead: geometry, this lane's 8 query dims per row, and (lanes j, j+32) the
-// block-table entries of context chunks j and j + 32.
+// Cold path of the chunk copy (blocks not a multiple of 16 tokens, or other
+// row layouts): per-row addresses through the block table.  Out of line so
+// the hot loop stays small (instruction-cache resident).
+__device__ __noinline__ void chunk_cp_async_rows(uint8_t* dst, KvView kv, int r, int t0, int h, int n,
+                                                 int lane) {
+  const int row0 = lane >> 4, c16 = lane & 15;
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + 2 * i;
+    const bool ok = row < n;
+    const __nv_bfloat16* ks = ok ? ctx_row(kv, kv.k, r, t0 + row, h) : kv.k;
+    const __nv_bfloat16* vs = ok ? ctx_row(kv, kv.v, r, t0 + row, h) : kv.v;
+    const uint32_t so = slot_off(row, c16);
+    cp_async_16(dst + so, ks + c16 * 8, ok ? 16u : 0u);
+    cp_async_16(dst + kChunk * kRowBytes + so, vs + c16 * 8, ok ? 16u : 0u);
+  }
+}
+
+// Tensor-core (mma.sync m16n8k16) update of one 16-key chunk for up to 16
+// query rows: S = Q K^T (2 n-tiles x 8 k-steps), online softmax in the log2
+// domain on the accumulator fragments, O += P V (16 n-tiles).  Lane (g =
+// lane / 4, t = lane % 4) holds rows g and g + 8.  lim0 / lim1: exclusive key
+// bounds (segment-relative) of those rows; key0: this chunk's first key.
+// mask = false: every key of the chunk is valid for every valid row (rows
+// past the item's rows compute harmless values that are never written).
+// Lazy rescale: the running max moves only when a score exceeds it by more
+// than kCtxTau (log2 units), so O is rescaled rarely; p <= 2^kCtxTau.
+constexpr float kCtxTau = 8.f;
+struct MmaRowState {
+  float o[16][4];
+  float m[2], l[2];
+};
+
+__device__ __forceinline__ void chunk_mma(MmaRowState& st, const uint32_t (&qa)[8][4], uint32_t slot,
+                                          int lane, int key0, int lim0, int lim1, float scale_log2,
+                                          bool mask) {
+  const int mi = lane >> 3, rr = lane & 7, t = lane & 3;
+  float s[2][4];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[nt][e] = 0.f;
+  {
+    const int key = (mi >> 1) * 8 + rr;
+    const uint32_t kaddr = slot + key * kRowBytes;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t b[4];
+      ldsm_x4(b, kaddr + (((ks * 2 + (mi & 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816(s[0], qa[ks], b[0], b[1]);
+      mma_bf16_16816(s[1], qa[ks], b[2], b[3]);
+    }
+  }
+  float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int key = key0 + nt * 8 + 2 * t + e;
+      s[nt][e] = (!mask || key < lim0) ? s[nt][e] * scale_log2 : -INFINITY;
+      s[nt][2 + e] = (!mask || key < lim1) ? s[nt][2 + e] * scale_log2 : -INFINITY;
+      mx0 = fmaxf(mx0, s[nt][e]);
+      mx1 = fmaxf(mx1, s[nt][2 + e]);
+    }
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+  // lazy max: keep the reference unless the chunk exceeds it by > kCtxTau
+  const float mn0 = (mx0 > st.m[0] + kCtxTau) ? mx0 : st.m[0];
+  const float mn1 = (mx1 > st.m[1] + kCtxTau) ? mx1 : st.m[1];
+  const float b0 = (mn0 == -INFINITY) ? 0.f : mn0, b1 = (mn1 == -INFINITY) ? 0.f : mn1;
+  float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      s[nt][e] = fast_exp2(s[nt][e] - b0);
+      s[nt][2 + e] = fast_exp2(s[nt][2 + e] - b1);
+      sum0 += s[nt][e];
+      sum1 += s[nt][2 + e];
+    }
+  sum0 += __shfl_xor_sync(0xffffffffu, sum0, 1);
+  sum1 += __shfl_xor_sync(0xffffffffu, sum1, 1);
+  sum0 += __shfl_xor_sync(0xffffffffu, sum0, 2);
+  sum1 += __shfl_xor_sync(0xffffffffu, sum1, 2);
+  if (mn0 != st.m[0] || mn1 != st.m[1]) {
+    const float al0 = (st.m[0] == -INFINITY) ? 0.f : fast_exp2(st.m[0] - mn0);
+    const float al1 = (st.m[1] == -INFINITY) ? 0.f : fast_exp2(st.m[1] - mn1);
+    st.l[0] *= al0;
+    st.l[1] *= al1;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      st.o[nt][0] *= al0;
+      st.o[nt][1] *= al0;
+      st.o[nt][2] *= al1;
+      st.o[nt][3] *= al1;
+    }
+    st.m[0] = mn0;
+    st.m[1] = mn1;
+  }
+  st.l[0] += sum0;
+  st.l[1] += sum1;
+  const uint32_t pa[4] = {pack_bf16x2(s[0][0], s[0][1]), pack_bf16x2(s[0][2], s[0][3]),
+                          pack_bf16x2(s[1][0], s[1][1]), pack_bf16x2(s[1][2], s[1][3])};
+  {
+    const int key = (mi & 1) * 8 + rr;
+    const uint32_t vaddr = slot + kChunk * kRowBytes + key * kRowBytes;
+#pragma unroll
+    for (int dp = 0; dp < 8; ++dp) {
+      uint32_t b[4];
+      ldsm_x4_trans(b, vaddr + (((dp * 2 + (mi >> 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816(st.o[2 * dp], pa, b[0], b[1]);
+      mma_bf16_16816(st.o[2 * dp + 1], pa, b[2], b[3]);
+    }
+  }
+}
+
+constexpr int kWorkers = 4;
+constexpr int kDepth = 3;                      // chunks in flight per worker
+static_assert(kDepth == 3, "wait_group ladder in ctx_cta_kernel assumes 3");
+constexpr int kIQ = 3;                         // item queue depth (claim-ahead bound)
+constexpr int kNB = 3;                         // merge buffers
+constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
+constexpr int kMergerWarp = 1 + kWorkers;
+constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
+
 template <int R>
-struct ItemPrefetch {
+struct ItemSlot {
   CtxItem<R> it;
-  float qf[R][8];
-  int bt0, bt1;
+  int item;                                    // -1: no more work
+  int bt[32];                                  // block ids of context blocks 0..31
 };
 
 template <int R>
-__device__ __forceinline__ void prefetch_item(const CtxArgs& a, int item, int n_z, int n_pre,
-                                              int lane, ItemPrefetch<R>& pf) {
-  pf.it = ctx_item<R>(a, item, n_z, n_pre);
-  const CtxItem<R>& it = pf.it;
-  const int l16 = lane & 15;
-  const int rbase = it.z * R;
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    const int li = rbase + i;
-    if (li < it.nrows) {
-      const int t = li / a.g, jj = li % a.g;
-      const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
-                                static_cast<long long>(it.h * a.g + jj) * a.q_head_stride + l16 * 8;
-      const uint4 u = *reinterpret_cast<const uint4*>(qp);
-      pf.qf[i][0] = bf16_lo(u.x); pf.qf[i][1] = bf16_hi(u.x);
-      pf.qf[i][2] = bf16_lo(u.y); pf.qf[i][3] = bf16_hi(u.y);
-      pf.qf[i][4] = bf16_lo(u.z); pf.qf[i][5] = bf16_hi(u.z);
-      pf.qf[i][6] = bf16_lo(u.w); pf.qf[i][7] = bf16_hi(u.w);
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) pf.qf[i][e] = 0.f;
-    }
-  }
-  pf.bt0 = pf.bt1 = 0;
-  if (a.ctx.block_table != nullptr && it.n_chunks > 0) {
-    const int nb = (it.max_lim + a.ctx.block_size - 1) / a.ctx.block_size;
-    const int* row = a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride;
-    if (lane < nb) pf.bt0 = __ldg(row + lane);
-    if (lane + 32 < nb) pf.bt1 = __ldg(row + lane + 32);
-  }
-}
-
-// Issue the bulk copies of chunk k of `it` into `slot` (warp-uniform call).
-// Paged K/V of one (block, head) run is contiguous: one 4 KB copy for K and
-// one for V; other layouts use one 256-byte copy per token, spread over lanes.
-template <int R>
-__device__ __forceinline__ void issue_chunk(const CtxArgs& a, const ItemPrefetch<R>& pf, int k,
-                                            int n_pre, uint8_t* slot, uint64_t* bar, int lane) {
-  const CtxItem<R>& it = pf.it;
-  const __nv_bfloat16 *kb, *vb;
-  int n;
-  long long tok_stride;
-  bool contiguous;
-  int blk = 0;
-  if (k >= n_pre && a.ctx.block_table != nullptr) {
-    // block id of this chunk's first token: from the lane-parallel prefetch
-    const int t0 = (k - n_pre) * kChunk;
-    const int bi = t0 / a.ctx.block_size;
-    const int v0 = __shfl_sync(0xffffffffu, pf.bt0, bi & 31);
-    const int v1 = __shfl_sync(0xffffffffu, pf.bt1, bi & 31);
-    blk = bi < 32 ? v0 : bi < 64 ? v1
-                   : __ldg(a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride + bi);
-  }
-  if (k < n_pre) {
-    const int t0 = k * kChunk;
-    n = min(kChunk, a.s_prefix - t0);
-    const long long off = static_cast<long long>(it.h) * a.p_stride_head + t0 * a.p_stride_tok;
-    kb = a.pk + off;
-    vb = a.pv + off;
-    tok_stride = a.p_stride_tok;
-    contiguous = (a.p_stride_tok == RB_HEAD_DIM);
-  } else {
-    const int t0 = (k - n_pre) * kChunk;
-    n = min(kChunk, it.max_lim - t0);
-    long long off;
-    if (a.ctx.block_table != nullptr)
-      off = static_cast<long long>(blk) * a.ctx.stride_block +
-            static_cast<long long>(t0 % a.ctx.block_size) * a.ctx.stride_tok;
-    else
-      off = (it.roff + t0) * a.ctx.stride_tok;
-    off += it.h * a.ctx.stride_head;
-    kb = a.ctx.k + off;
-    vb = a.ctx.v + off;
-    tok_stride = a.ctx.stride_tok;
-    contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
-                 (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
-  }
-  if (lane == 0) mbar_arrive_expect_tx(bar, 2 * n * kRowBytes);
-  __syncwarp();
-  if (contiguous) {
-    if (lane == 0) {
-      bulk_copy_g2s(slot, kb, n * kRowBytes, bar);
-      bulk_copy_g2s(slot + kChunk * kRowBytes, vb, n * kRowBytes, bar);
-    }
-  } else if (lane < 2 * n) {
-    const int t = lane % n, which = lane / n;
-    const __nv_bfloat16* src;
-    if (k < n_pre || a.ctx.block_table == nullptr) {
-      src = (which ? vb : kb) + t * tok_stride;
-    } else {
-      const int tt = (k - n_pre) * kChunk + t;
-      const int bi = tt / a.ctx.block_size;
-      const int b2 = __ldg(a.ctx.block_table + static_cast<long long>(it.r) * a.ctx.bt_stride + bi);
-      src = (which ? a.ctx.v : a.ctx.k) + static_cast<long long>(b2) * a.ctx.stride_block +
-            static_cast<long long>(tt % a.ctx.block_size) * a.ctx.stride_tok +
-            it.h * a.ctx.stride_head;
-    }
-    bulk_copy_g2s(slot + which * kChunk * kRowBytes + t * kRowBytes, src, kRowBytes, bar);
-  }
-}
-
-// Warp-per-item persistent kernel.  Global warp gw processes items gw,
-// gw + W, ... (W = all warps of the grid).  Each warp streams its items'
-// chunks through a private ring of kWarpSlots bulk-copy slots; chunks of the
-// next item are issued while the current one finishes, and the next item's
-// metadata / queries / block-table entries are prefetched one item ahead, so
-// no global round trip sits on the per-item critical path.  Half-warp hw
-// handles keys 2p + hw of each chunk; the two half states merge with shuffles.
-constexpr int kWarpSlots = 2;
-constexpr int kCtxWarps = 4;
+struct CtaSmem {
+  // [kIQ][R][128] bf16 query rows, then one zero row (MMA rows past R)
+  static constexpr int kOffQ = kWorkers * kDepth * kSlotBytes;
+  static constexpr int kOffQZero = kOffQ + kIQ * R * kRowBytes;
+  static constexpr int kOffAcc = kOffQZero + kRowBytes;                  // [kNB][kWorkers][R][128] f32
+  static constexpr int kOffML = kOffAcc + kNB * kWorkers * R * 128 * 4;  // [kNB][kWorkers][R][2]
+  static constexpr int kOffMIt = (kOffML + kNB * kWorkers * R * 8 + 15) & ~15;  // [kNB] CtxItem
+  static constexpr int kOffItems =
+      (kOffMIt + kNB * static_cast<int>(sizeof(CtxItem<R>)) + 15) & ~15;  // [kIQ] ItemSlot
+  static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
+  static constexpr int kBytes = kOffBar + (3 * kIQ + 2 * kNB) * 8;
+};
 
 template <int R>
-__global__ void __launch_bounds__(kCtxWarps * 32, (R <= 2) ? 3 : 1)
-    ctx_attn_kernel(const CtxArgs a, int n_items, int n_z) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int hw = lane >> 4, l16 = lane & 15;
-  const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
-  const int W = gridDim.x * kCtxWarps;
-  const int gw = blockIdx.x * kCtxWarps + warp;
-  uint8_t* slots = smem + warp * kWarpSlots * kSlotBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kCtxWarps * kWarpSlots * kSlotBytes) +
-                  warp * kWarpSlots;
-  if (lane == 0) {
-    for (int i = 0; i < kWarpSlots; ++i) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  pdl_launch_dependents();
-  if (gw >= n_items) return;
-
-  // issue cursor (item + chunk) runs up to kWarpSlots chunks ahead of compute
-  ItemPrefetch<R> iss;
-  prefetch_item<R>(a, gw, n_z, n_pre, lane, iss);
-  int iss_item = gw, iss_k = 0;
-  long long issued = 0;
-  ItemPrefetch<R> nxt;  // next item's prefetch for the issue cursor
-  bool have_nxt = false;
-  auto advance_issue = [&]() {
-    // move the issue cursor past exhausted items (warp-uniform)
-    while (iss_item < n_items && iss_k >= iss.it.n_chunks) {
-      iss_item += W;
-      iss_k = 0;
-      if (iss_item >= n_items) break;
-      if (have_nxt) {
-        iss = nxt;
-        have_nxt = false;
-      } else {
-        prefetch_item<R>(a, iss_item, n_z, n_pre, lane, iss);
-      }
-    }
-  };
-  auto issue_one = [&]() {
-    advance_issue();
-    if (iss_item >= n_items) return;
-    const int sl = static_cast<int>(issued % kWarpSlots);
-    issue_chunk<R>(a, iss, iss_k, n_pre, slots + sl * kSlotBytes, &bar[sl], lane);
-    ++issued;
-    ++iss_k;
-    // start fetching the following item's metadata as soon as this one is issued
-    if (iss_k == iss.it.n_chunks && !have_nxt && iss_item + W < n_items) {
-      prefetch_item<R>(a, iss_item + W, n_z, n_pre, lane, nxt);
-      have_nxt = true;
-    }
-  };
-
-  ItemPrefetch<R> cur = iss;  // compute cursor starts on the same item
-  for (int s = 0; s < kWarpSlots; ++s) issue_one();
-
-  long long consumed = 0;
-  bool waited = false;
-  for (int item = gw; item < n_items; item += W) {
-    if (item != gw) {
-      // the issue cursor has already prefetched this item (it runs ahead)
-      cur = (iss_item == item) ? iss : cur;
-      if (cur.it.r != item / (n_z * a.hkv) || cur.it.h != (item / n_z) % a.hkv ||
-          cur.it.z != item % n_z)
-        prefetch_item<R>(a, item, n_z, n_pre, lane, cur);
-    }
-    const CtxItem<R>& it = cur.it;
-    if (it.n_chunks == 0) continue;
-    const int rbase = it.z * R;
-    int lim_ctx[R], lim_pre[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int li = rbase + i;
-      if (li < it.nrows) {
-        const int t = li / a.g;
-        lim_ctx[i] = a.causal ? it.c_r - it.m_r + t + 1 : it.c_r;
-        lim_pre[i] = a.s_prefix;
-      } else {
-        lim_ctx[i] = 0;
-        lim_pre[i] = 0;
-      }
-    }
-    RowState<R> st;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      st.m[i] = -INFINITY;
-      st.l[i] = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
-    }
-    for (int k = 0; k < it.n_chunks; ++k, ++consumed) {
-      const int sl = static_cast<int>(consumed % kWarpSlots);
-      const uint8_t* src = slots + sl * kSlotBytes;
-      mbar_wait(&bar[sl], static_cast<uint32_t>((consumed / kWarpSlots) & 1));
-      uint4 kr[8], vr[8];
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        kr[p] = *reinterpret_cast<const uint4*>(src + (2 * p + hw) * kRowBytes + l16 * 16);
-        vr[p] = *reinterpret_cast<const uint4*>(src + kChunk * kRowBytes + (2 * p + hw) * kRowBytes +
-                                                l16 * 16);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      issue_one();  // refill the slot just read
-      if (k < n_pre)
-        chunk_update<R>(st, cur.qf, kr, vr, k * kChunk, hw, lim_pre, a.scale_log2, a.s_prefix);
-      else
-        chunk_update<R>(st, cur.qf, kr, vr, (k - n_pre) * kChunk, hw, lim_ctx, a.scale_log2,
-                        it.max_lim);
-    }
-
-    // ---- merge the two half-warp states (keys 2p and 2p+1) with shuffles
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const float mo = __shfl_xor_sync(0xffffffffu, st.m[i], 16);
-      const float lo = __shfl_xor_sync(0xffffffffu, st.l[i], 16);
-      const float M = fmaxf(st.m[i], mo);
-      const float ws = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - M);
-      const float wo = (mo == -INFINITY) ? 0.f : fast_exp2(mo - M);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float ao = __shfl_xor_sync(0xffffffffu, st.acc[i][e], 16);
-        st.acc[i][e] = st.acc[i][e] * ws + ao * wo;
-      }
-      st.l[i] = st.l[i] * ws + lo * wo;
-      st.m[i] = M;
-    }
-    if (!waited) {  // before the first global write / system-output read
-      pdl_wait_primary();
-      waited = true;
-    }
-    // ---- epilogue: half-warp 0 owns 8 head dims per lane
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int li = rbase + i;
-      if (li >= it.nrows) continue;
-      const int t = li / a.g, jj = li % a.g;
-      const long long oidx = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
-      const float M = st.m[i], Ls = st.l[i];
-      float o[8], lse2;
-      if (a.sys_part_acc != nullptr) {
-        // relay fusion: merge every system stream-K part of this (row, head)
-        const rb_sys_plan& SP = a.sys_plan;
-        const long long f = static_cast<long long>(it.row0 + t) * SP.g + jj;
-        const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
-        const int u = it.h * SP.n_qt + qt;
-        const int np = rb_unit_parts(&SP, u);
-        const long long base = static_cast<long long>(u) * SP.max_parts;
-        float mt = M, lt = Ls;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = st.acc[i][e];
-        for (int k0 = 0; k0 < np; k0 += 2) {
-          float mk[2], lk[2];
-          float4 ak[2][2];
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            const int k = min(k0 + kk, np - 1);
-            const float* ml = a.sys_part_ml + (base + k) * 2 * SP.nq;
-            mk[kk] = __ldcg(ml + col);
-            lk[kk] = __ldcg(ml + SP.nq + col);
-            const float4* ap = reinterpret_cast<const float4*>(
-                a.sys_part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + l16 * 8);
-            ak[kk][0] = __ldcg(ap);
-            ak[kk][1] = __ldcg(ap + 1);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {
-            if (k0 + kk >= np) break;
-            const float mn = fmaxf(mt, mk[kk]);
-            const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
-            const float sk = fast_exp2(mk[kk] - mn);
-            lt = lt * so + lk[kk] * sk;
-            const float av[8] = {ak[kk][0].x, ak[kk][0].y, ak[kk][0].z, ak[kk][0].w,
-                                 ak[kk][1].x, ak[kk][1].y, ak[kk][1].z, ak[kk][1].w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = o[e] * so + av[e] * sk;
-            mt = mn;
-          }
-        }
-        const float inv = 1.f / lt;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] *= inv;
-        lse2 = mt + __log2f(lt);
-      } else {
-        const float inv = (Ls > 0.f) ? 1.f / Ls : 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = st.acc[i][e] * inv;
-        lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
-      }
-      if (a.o_sys != nullptr) {
-        const float ls2 = __ldcg(a.lse_sys + oidx) * kLog2e;
-        const float4* op = reinterpret_cast<const float4*>(a.o_sys + oidx * 128 + l16 * 8);
-        const float4 s0 = __ldcg(op), s1 = __ldcg(op + 1);
-        const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-        const float mx = fmaxf(ls2, lse2);
-        const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
-        const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
-        const float inv = 1.f / (wc + ws);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (wc * o[e] + ws * sv[e]) * inv;
-        lse2 = mx + __log2f(wc + ws);
-      }
-      if (hw == 0) {
-        if (a.out_fp32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx * 128 + l16 * 8);
-          dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-          dst[1] = make_float4(o[4], o[5], o[6], o[7]);
-        } else {
-          uint4 pk;
-          pk.x = pack_bf16x2(o[0], o[1]);
-          pk.y = pack_bf16x2(o[2], o[3]);
-          pk.z = pack_bf16x2(o[4], o[5]);
-          pk.w = pack_bf16x2(o[6], o[7]);
-          *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + oidx * 128 + l16 * 8) = pk;
-        }
-        if (a.lse_out != nullptr && l16 == 0) a.lse_out[oidx] = lse2 * kLn2;
-      }
-    }
-  }
-}
-
-// Long items (the naive baseline's shared prefix: hundreds of chunks per
-// request): CTA-per-item producer/consumer kernel.  CTA b processes items b,
-// b + grid, ...; their chunks form one sequence.  Warp 0 is the producer: its lanes
-// resolve block-table entries and issue the bulk copies of up to kRing chunks
-// at once into a CTA-wide ring of kRing slots (waiting on each slot's empty
-// barrier), so the copies run far ahead of the math.  Warps 1..4 consume
-// chunk k of an item in warp 1 + (k % 4), then merge their partial states at
-// the end of the item and run the fusion epilogue (thread = head dim).
-constexpr int kRing = 12;                      // 12 x 8 KB = 96 KB of K/V in flight per CTA
-constexpr int kCtxThreadsPC = 160;             // producer + 4 consumers
-template <int R>
-__global__ void __launch_bounds__(kCtxThreadsPC)
+__global__ void __launch_bounds__(kCtxThreadsPC, 2)
     ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
+  using SM = CtaSmem<R>;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
-  uint8_t* ring = smem;
-  float* s_acc = reinterpret_cast<float*>(smem + kRing * kSlotBytes);  // [8][R][128]
-  float* s_m = s_acc + 8 * R * 128;                                    // [8][R]
-  float* s_l = s_m + 8 * R;                                            // [8][R]
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_l + 8 * R);
-  uint64_t* empty = full + kRing;
+  float* s_acc = reinterpret_cast<float*>(smem + SM::kOffAcc);
+  float* s_ml = reinterpret_cast<float*>(smem + SM::kOffML);
+  ItemSlot<R>* iq = reinterpret_cast<ItemSlot<R>*>(smem + SM::kOffItems);
+  uint64_t* i_meta = reinterpret_cast<uint64_t*>(smem + SM::kOffBar);
+  uint64_t* i_full = i_meta + kIQ;
+  uint64_t* i_empty = i_full + kIQ;
+  uint64_t* m_full = i_empty + kIQ;
+  uint64_t* m_empty = m_full + kNB;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kRing; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < kIQ; ++i) {
+      mbar_init(&i_meta[i], 1);
+      mbar_init(&i_full[i], 1);
+      mbar_init(&i_empty[i], kWorkers + 1);  // workers + merger
+    }
+    for (int i = 0; i < kNB; ++i) {
+      mbar_init(&m_full[i], kWorkers);
+      mbar_init(&m_empty[i], 1);
     }
     fence_mbar_init();
   }
+  // the zero query row stands in for MMA rows past R (16-row tiles)
+  if (threadIdx.x < kRowBytes / 16)
+    reinterpret_cast<uint4*>(smem + SM::kOffQZero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   pdl_launch_dependents();
+  unsigned long long* dts = a.debug_ts ? a.debug_ts + blockIdx.x * 8 : nullptr;
+  if (dts && threadIdx.x == 0) {
+    dts[0] = global_timer_ns();
+    dts[1] = smid();
+  }
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    long long seq = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
-      // a batch never spans more than one ring round, so every lane's slot was
-      // last used by a chunk issued in an earlier batch and the empty-barrier
-      // parity it waits on is unambiguous
-      for (int k0 = 0; k0 < it.n_chunks; k0 += kRing) {
-        const int k = k0 + lane;
-        if (lane < kRing && k < it.n_chunks) {
-          const long long sq = seq + k;
-          const int slot = static_cast<int>(sq % kRing);
-          mbar_wait(&empty[slot], static_cast<uint32_t>(((sq / kRing) & 1) ^ 1));
-          const __nv_bfloat16 *kb, *vb;
-          int n;
-          bool contiguous;
-          long long tok_stride;
-          if (k < n_pre) {
-            const int t0 = k * kChunk;
-            n = min(kChunk, a.s_prefix - t0);
-            const long long off = static_cast<long long>(it.h) * a.p_stride_head + t0 * a.p_stride_tok;
-            kb = a.pk + off;
-            vb = a.pv + off;
-            tok_stride = a.p_stride_tok;
-            contiguous = (a.p_stride_tok == RB_HEAD_DIM);
-          } else {
-            const int t0 = (k - n_pre) * kChunk;
-            n = min(kChunk, it.max_lim - t0);
-            kb = ctx_row(a.ctx, a.ctx.k, it.r, t0, it.h);
-            vb = ctx_row(a.ctx, a.ctx.v, it.r, t0, it.h);
-            tok_stride = a.ctx.stride_tok;
-            contiguous = (a.ctx.stride_tok == RB_HEAD_DIM) &&
-                         (a.ctx.block_table == nullptr || (a.ctx.block_size % kChunk) == 0);
-          }
-          uint8_t* dst = ring + slot * kSlotBytes;
-          mbar_arrive_expect_tx(&full[slot], 2 * n * kRowBytes);
-          if (contiguous) {
-            bulk_copy_g2s(dst, kb, n * kRowBytes, &full[slot]);
-            bulk_copy_g2s(dst + kChunk * kRowBytes, vb, n * kRowBytes, &full[slot]);
-          } else {
-            for (int t = 0; t < n; ++t) {
-              const __nv_bfloat16 *ks, *vs;
-              if (k < n_pre) {
-                ks = kb + t * tok_stride;
-                vs = vb + t * tok_stride;
-              } else {
-                const int tt = (k - n_pre) * kChunk + t;
-                ks = ctx_row(a.ctx, a.ctx.k, it.r, tt, it.h);
-                vs = ctx_row(a.ctx, a.ctx.v, it.r, tt, it.h);
-              }
-              bulk_copy_g2s(dst + t * kRowBytes, ks, kRowBytes, &full[slot]);
-              bulk_copy_g2s(dst + kChunk * kRowBytes + t * kRowBytes, vs, kRowBytes, &full[slot]);
-            }
-          }
-        }
-        __syncwarp();
+    // ----------------------------------------------------------- scheduler
+    // Software pipeline: publish item j, load item j+1's metadata, claim
+    // item j+3 (the atomic resolves while the scheduler waits for a free
+    // queue slot).  With `sched` every item is claimed from the global
+    // counter (the first three in one atomic), so CTAs that start late --
+    // after the concurrent system kernel frees their SM -- still share the
+    // remaining work; without it the order is static (b + k * grid).
+    int* sched = a.sched;
+    const int bt_lanes = a.ctx.block_table != nullptr ? min(32, a.ctx.bt_stride) : 0;
+    struct Raw {
+      int item, qs0, qs1, clen, bte;
+      long long roff;
+    };
+    auto load_raw = [&](int item) {
+      Raw w;
+      w.item = item;
+      w.qs0 = w.qs1 = w.clen = w.bte = 0;
+      w.roff = 0;
+      if (item < n_items) {
+        const int r = item / (n_z * a.hkv);
+        w.qs0 = __ldg(a.q_start + r);
+        w.qs1 = __ldg(a.q_start + r + 1);
+        w.clen = __ldg(a.ctx_lens + r);
+        if (a.ctx.req_offset != nullptr) w.roff = __ldg(a.ctx.req_offset + r);
+        // rows of the table are bt_stride long: the first min(32, bt_stride) are in bounds
+        if (lane < bt_lanes)
+          w.bte = __ldg(a.ctx.block_table + static_cast<long long>(r) * a.ctx.bt_stride + lane);
       }
-      seq += it.n_chunks;
+      return w;
+    };
+    const int G = static_cast<int>(gridDim.x);
+    int id0 = blockIdx.x, id1 = blockIdx.x + G, id2 = blockIdx.x + 2 * G;
+    if (sched != nullptr) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(sched, 3);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      id0 = base;
+      id1 = base + 1;
+      id2 = base + 2;
+    }
+    Raw cur = load_raw(id0);
+    for (int j = 0;; ++j) {
+      const int item = cur.item;
+      const int qs = j % kIQ;
+      ItemSlot<R>& slot = iq[qs];
+      // claim item j+3 and load item j+1 while this one is published
+      int p = id2 + G;
+      if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
+      const Raw nxt = load_raw(id1);
+      if (a.knob & 1) mbar_wait_sleep(&i_empty[qs], ((j / kIQ) & 1) ^ 1); else mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
+      if (item >= n_items) {
+        if (lane == 0) {
+          slot.item = -1;
+          mbar_arrive(&i_meta[qs]);
+          mbar_arrive(&i_full[qs]);
+        }
+        break;
+      }
+      CtxItem<R> it;
+      it.z = item % n_z;
+      it.h = (item / n_z) % a.hkv;
+      it.r = item / (n_z * a.hkv);
+      it.row0 = cur.qs0;
+      it.m_r = cur.qs1 - cur.qs0;
+      it.nrows = it.m_r * a.g;
+      it.c_r = cur.clen;
+      it.roff = cur.roff;
+      const int rbase = it.z * R;
+      if (rbase >= it.nrows) {
+        it.max_lim = 0;
+        it.n_chunks = 0;
+      } else {
+        const int t_last = (min(rbase + R, it.nrows) - 1) / a.g;
+        it.max_lim = a.causal ? it.c_r - it.m_r + t_last + 1 : it.c_r;
+        it.n_chunks = n_pre + (it.max_lim + kChunk - 1) / kChunk;
+      }
+      const int nvalid = it.n_chunks > 0 ? max(0, min(R, it.nrows - rbase)) : 0;
+      slot.bt[lane] = cur.bte;
+      if (lane == 0) {
+        slot.it = it;
+        slot.item = item;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&i_meta[qs]);
+        mbar_arrive_expect_tx(&i_full[qs], nvalid * kRowBytes);
+      }
+      __syncwarp();
+      // query rows of the item: one 256-byte bulk copy per row
+      if (lane < nvalid) {
+        const int li = rbase + lane;
+        const int t = li / a.g, jj = li % a.g;
+        const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
+                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride;
+        bulk_copy_g2s(smem + SM::kOffQ + (qs * R + lane) * kRowBytes, qp, kRowBytes, &i_full[qs]);
+      }
+      cur = nxt;
+      id1 = id2;
+      id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;
+    }
+    if (sched != nullptr && lane == 0) {
+      // every scheduler's last claim precedes its arrival here, so the last
+      // CTA to arrive can rearm the counters for the next launch
+      if (atomicAdd(sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        atomicExch(sched, 0);
+        atomicExch(sched + 1, 0);
+      }
     }
     return;
   }
 
-  // -------------------------------------------------------------- consumers
-  const int cw = warp - 1;                      // 0..3
-  const int hw = lane >> 4, l16 = lane & 15;
-  long long seq = 0;
-  bool waited = false;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const CtxItem<R> it = ctx_item<R>(a, item, n_z, n_pre);
-    if (it.n_chunks == 0) continue;
-    const int rbase = it.z * R;
-    float qf[R][8];
-    int lim_ctx[R], lim_pre[R];
-    float os_pref[R], ls_pref[R];
-    long long oidx[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int li = rbase + i;
-      os_pref[i] = 0.f;
-      ls_pref[i] = -INFINITY;
-      oidx[i] = -1;
-      if (li < it.nrows) {
-        const int t = li / a.g, jj = li % a.g;
-        oidx[i] = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
-        const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
-                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride + l16 * 8;
-        const uint4 u = *reinterpret_cast<const uint4*>(qp);
-        qf[i][0] = bf16_lo(u.x); qf[i][1] = bf16_hi(u.x);
-        qf[i][2] = bf16_lo(u.y); qf[i][3] = bf16_hi(u.y);
-        qf[i][4] = bf16_lo(u.z); qf[i][5] = bf16_hi(u.z);
-        qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
-        lim_ctx[i] = a.causal ? it.c_r - it.m_r + t + 1 : it.c_r;
-        lim_pre[i] = a.s_prefix;
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
-        lim_ctx[i] = 0;
-        lim_pre[i] = 0;
+  if (warp == kMergerWarp) {
+    // --------------------------------------------------------------- merger
+    // Walks the item queue like the workers (metadata only), waits for the
+    // workers' states of each item (m_full), combines them (lane = 4 head
+    // dims) and writes: the relay context partial (unnormalised O, m, l) to
+    // the workspace, or the final output (+ optional fusion with a given
+    // system partial o_sys / lse_sys).
+    bool waited = false;
+    int jp = 0;  // queue cursor
+    for (int mi = 0;; ++mi) {
+      // next non-empty item off the queue
+      int item = -1;
+      CtxItem<R> it;
+      for (;;) {
+        const int qs = jp % kIQ;
+        if (a.knob & 1) mbar_wait_sleep(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1)); else mbar_wait(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1));
+        item = iq[qs].item;
+        it = iq[qs].it;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&i_empty[qs]);
+        ++jp;
+        if (item < 0 || it.n_chunks > 0) break;
       }
-    }
-    RowState<R> st;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      st.m[i] = -INFINITY;
-      st.l[i] = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
-    }
-    for (int k = cw; k < it.n_chunks; k += 4) {
-      const long long sq = seq + k;
-      const int slot = static_cast<int>(sq % kRing);
-      mbar_wait(&full[slot], static_cast<uint32_t>((sq / kRing) & 1));
-      const uint8_t* src = ring + slot * kSlotBytes;
-      uint4 kr[8], vr[8];
-#pragma unroll
-      for (int p = 0; p < 8; ++p) {
-        kr[p] = *reinterpret_cast<const uint4*>(src + (2 * p + hw) * kRowBytes + l16 * 16);
-        vr[p] = *reinterpret_cast<const uint4*>(src + kChunk * kRowBytes + (2 * p + hw) * kRowBytes +
-                                                l16 * 16);
+      if (item < 0) break;
+      if (!waited && a.ctx_part == nullptr) {
+        // before the first output write / o_sys read: the previous grid (a
+        // system kernel producing o_sys, or a reader of out) must be done
+        pdl_wait_primary();
+        waited = true;
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (k < n_pre)
-        chunk_update<R>(st, qf, kr, vr, k * kChunk, hw, lim_pre, a.scale_log2, a.s_prefix);
-      else
-        chunk_update<R>(st, qf, kr, vr, (k - n_pre) * kChunk, hw, lim_ctx, a.scale_log2,
-                        it.max_lim);
-    }
-    seq += it.n_chunks;
-
-    if (!waited) {  // before the first global write / system-output read
-      pdl_wait_primary();
-      waited = true;
-    }
-    if (a.o_sys != nullptr) {
-#pragma unroll
+      const int mb = mi % kNB;
+      const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
+      if (a.knob & 1) mbar_wait_sleep(&m_full[mb], mph); else mbar_wait(&m_full[mb], mph);
+      const float* bacc = s_acc + mb * kWorkers * R * 128;
+      const float* bml = s_ml + mb * kWorkers * R * 2;
+      const int rbase = it.z * R;
+      const int d0 = lane * 4;
+#pragma unroll 1
       for (int i = 0; i < R; ++i) {
-        if (oidx[i] >= 0) {
-          os_pref[i] = __ldcg(a.o_sys + oidx[i] * 128 + (threadIdx.x - 32));
-          ls_pref[i] = __ldcg(a.lse_sys + oidx[i]);
-        }
-      }
-    }
-    // ---- merge the 8 (warp, half) partial states per row through smem
-    const int wh = cw * 2 + hw;
+        const int li = rbase + i;
+        if (li >= it.nrows) break;
+        const int t = li / a.g, jj = li % a.g;
+        const long long oidx = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
+        float M = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      float* dst = s_acc + (wh * R + i) * 128 + l16 * 8;
-      *reinterpret_cast<float4*>(dst) =
-          make_float4(st.acc[i][0], st.acc[i][1], st.acc[i][2], st.acc[i][3]);
-      *reinterpret_cast<float4*>(dst + 4) =
-          make_float4(st.acc[i][4], st.acc[i][5], st.acc[i][6], st.acc[i][7]);
-      if (l16 == 0) {
-        s_m[wh * R + i] = st.m[i];
-        s_l[wh * R + i] = st.l[i];
-      }
-    }
-    named_bar_sync(1, 128);
-    const int dcol = threadIdx.x - 32;  // 128 consumer threads = 128 head dims
+        for (int k = 0; k < kWorkers; ++k) M = fmaxf(M, bml[(k * R + i) * 2]);
+        float Ls = 0.f, O[4] = {0.f, 0.f, 0.f, 0.f};
+        if (M != -INFINITY) {
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      if (oidx[i] < 0) continue;
-      float M = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) M = fmaxf(M, s_m[k * R + i]);
-      float Ls = 0.f, O = 0.f;
-      if (M != -INFINITY) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float mk = s_m[k * R + i];
-          const float w = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
-          Ls = fmaf(s_l[k * R + i], w, Ls);
-          O = fmaf(s_acc[(k * R + i) * 128 + dcol], w, O);
-        }
-      }
-      float o, lse2;
-      if (a.sys_part_acc != nullptr) {
-        // one LSE-weighted combine of the system kernel's stream-K parts of
-        // this (row, head) and the context state (M, Ls, O): relay fusion.
-        const rb_sys_plan& SP = a.sys_plan;
-        const long long row = oidx[i] / a.hq;
-        const int hh = static_cast<int>(oidx[i] % a.hq);
-        const long long f = row * SP.g + hh % SP.g;
-        const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
-        const int u = (hh / SP.g) * SP.n_qt + qt;
-        const int np = rb_unit_parts(&SP, u);
-        const long long base = static_cast<long long>(u) * SP.max_parts;
-        float mt = M, lt = Ls, ot = O;
-        for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
-          float mk[4], lk[4], ak[4];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int k = min(k0 + kk, np - 1);
-            const float* ml = a.sys_part_ml + (base + k) * 2 * SP.nq;
-            mk[kk] = __ldcg(ml + col);
-            lk[kk] = __ldcg(ml + SP.nq + col);
-            ak[kk] = __ldcg(a.sys_part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + dcol);
-          }
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            if (k0 + kk >= np) break;
-            const float mn = fmaxf(mt, mk[kk]);
-            const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
-            const float sk = fast_exp2(mk[kk] - mn);
-            lt = lt * so + lk[kk] * sk;
-            ot = ot * so + ak[kk] * sk;
-            mt = mn;
+          for (int k = 0; k < kWorkers; ++k) {
+            const float mk = bml[(k * R + i) * 2];
+            const float wt = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
+            Ls = fmaf(bml[(k * R + i) * 2 + 1], wt, Ls);
+            const float4 av = *reinterpret_cast<const float4*>(bacc + (k * R + i) * 128 + d0);
+            O[0] = fmaf(av.x, wt, O[0]);
+            O[1] = fmaf(av.y, wt, O[1]);
+            O[2] = fmaf(av.z, wt, O[2]);
+            O[3] = fmaf(av.w, wt, O[3]);
           }
         }
-        o = ot / lt;
-        lse2 = mt + __log2f(lt);
-      } else {
-        o = (Ls > 0.f) ? O / Ls : 0.f;
-        lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+        if (a.ctx_part != nullptr) {
+          // relay: unnormalised partial for relay_fuse_kernel
+          float* dst = a.ctx_part + oidx * kPartStride;
+          __stcg(reinterpret_cast<float4*>(dst + d0), make_float4(O[0], O[1], O[2], O[3]));
+          if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
+          continue;
+        }
+        float o[4];
+        float lse2;
+        {
+          const float inv = (Ls > 0.f) ? 1.f / Ls : 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[e] = O[e] * inv;
+          lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+        }
+        if (a.o_sys != nullptr) {
+          const float ls2 = __ldcg(a.lse_sys + oidx) * kLog2e;
+          const float4 sv = __ldcg(reinterpret_cast<const float4*>(a.o_sys + oidx * 128 + d0));
+          const float mx = fmaxf(ls2, lse2);
+          const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
+          const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
+          const float inv = 1.f / (wc + ws);
+          o[0] = (wc * o[0] + ws * sv.x) * inv;
+          o[1] = (wc * o[1] + ws * sv.y) * inv;
+          o[2] = (wc * o[2] + ws * sv.z) * inv;
+          o[3] = (wc * o[3] + ws * sv.w) * inv;
+          lse2 = mx + __log2f(wc + ws);
+        }
+        if (a.out_fp32) {
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx * 128 + d0) =
+              make_float4(o[0], o[1], o[2], o[3]);
+        } else {
+          uint2 pk;
+          pk.x = pack_bf16x2(o[0], o[1]);
+          pk.y = pack_bf16x2(o[2], o[3]);
+          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + oidx * 128 + d0) = pk;
+        }
+        if (a.lse_out != nullptr && lane == 0) a.lse_out[oidx] = lse2 * kLn2;
       }
-      if (a.o_sys != nullptr) {
-        const float ls2 = ls_pref[i] * kLog2e;
-        const float mx = fmaxf(ls2, lse2);
-        const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
-        const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
-        const float inv = 1.f / (wc + ws);
-        o = (wc * o + ws * os_pref[i]) * inv;
-        lse2 = mx + __log2f(wc + ws);
-      }
-      if (a.out_fp32)
-        reinterpret_cast<float*>(a.out)[oidx[i] * 128 + dcol] = o;
-      else
-        reinterpret_cast<__nv_bfloat16*>(a.out)[oidx[i] * 128 + dcol] = __float2bfloat16_rn(o);
-      if (a.lse_out != nullptr && dcol == 0) a.lse_out[oidx[i]] = lse2 * kLn2;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_empty[mb]);
     }
-    named_bar_sync(1, 128);  // merge buffer free for the next item
+    if (dts && lane == 0) dts[6] = global_timer_ns();
+    return;
   }
+
+  // ---------------------------------------------------------------- workers
+  const int w = warp - 1;                       // 0 .. kWorkers-1
+  const uint32_t ring = smem_u32(smem + w * kDepth * kSlotBytes);
+  uint8_t* ring_p = smem + w * kDepth * kSlotBytes;
+
+  // issue cursor: queue item ji, next chunk ki (= w mod kWorkers)
+  int ji = 0, ki = w, iss_item = 0, iss_bte = 0;
+  int iss_r = 0, iss_h = 0, iss_lim = 0, iss_nch = 0;
+  long long iss_roff = 0;
+  bool have_iss = false;
+  int issued = 0, consumed = 0, iss_sl = 0;
+
+  // Issue chunks while the ring has room.  The cursor blocks on the item
+  // queue only for items <= jc (already published); for later items it
+  // polls, so a worker never waits on an item its CTA cannot publish yet.
+  auto try_issue = [&](int jc) {
+    while (issued < consumed + kDepth) {
+      if (!have_iss) {
+        const int qs = ji % kIQ;
+        const uint32_t par = static_cast<uint32_t>((ji / kIQ) & 1);
+        if (ji <= jc)
+          mbar_wait(&i_meta[qs], par);
+        else if (!mbar_test(&i_meta[qs], par))
+          return;
+        iss_item = iq[qs].item;
+        iss_r = iq[qs].it.r;
+        iss_h = iq[qs].it.h;
+        iss_lim = iq[qs].it.max_lim;
+        iss_nch = iq[qs].it.n_chunks;
+        iss_roff = iq[qs].it.roff;
+        iss_bte = iq[qs].bt[lane];
+        have_iss = true;
+        ki = w;
+      }
+      if (iss_item < 0) return;
+      if (ki >= iss_nch) {
+        ++ji;
+        have_iss = false;
+        continue;
+      }
+      const int k = ki;
+      uint8_t* dst = ring_p + iss_sl * kSlotBytes;
+      const __nv_bfloat16 *kb = a.ctx.k, *vb = a.ctx.v;
+      long long tok_stride = a.ctx.stride_tok;
+      int n;
+      bool rows_ok = true;  // rows t0 .. t0 + 15 share one block / run
+      if (k < n_pre) {
+        const int t0 = k * kChunk;
+        const long long off = static_cast<long long>(iss_h) * a.p_stride_head + t0 * a.p_stride_tok;
+        kb = a.pk + off;
+        vb = a.pv + off;
+        tok_stride = a.p_stride_tok;
+        n = min(kChunk, a.s_prefix - t0);
+      } else {
+        const int t0 = (k - n_pre) * kChunk;
+        n = min(kChunk, iss_lim - t0);
+        long long off;
+        if (a.ctx.block_table == nullptr) {
+          off = (iss_roff + t0) * a.ctx.stride_tok;
+        } else if (a.ctx.block_size % kChunk == 0) {
+          const int bi = t0 / a.ctx.block_size;
+          const int v0 = __shfl_sync(0xffffffffu, iss_bte, bi & 31);
+          const int blk = bi < 32 ? v0
+                                  : __ldg(a.ctx.block_table +
+                                          static_cast<long long>(iss_r) * a.ctx.bt_stride + bi);
+          off = static_cast<long long>(blk) * a.ctx.stride_block +
+                static_cast<long long>(t0 % a.ctx.block_size) * a.ctx.stride_tok;
+        } else {
+          off = 0;
+          rows_ok = false;
+        }
+        off += iss_h * a.ctx.stride_head;
+        kb += off;
+        vb += off;
+        if (!rows_ok) chunk_cp_async_rows(dst, a.ctx, iss_r, t0, iss_h, n, lane);
+      }
+      if (rows_ok) chunk_cp_async(dst, kb, vb, tok_stride, n, lane);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      ++issued;
+      iss_sl = (iss_sl + 1 == kDepth) ? 0 : iss_sl + 1;
+      ki += kWorkers;
+    }
+  };
+
+  try_issue(0);
+  int mi = 0;  // items merged so far (skipped empty items excluded)
+  int con_sl = 0;
+  int qs = 0;
+  uint32_t qph = 0;
+  for (int jc = 0;; ++jc) {
+    mbar_wait(&i_full[qs], qph);
+    const int item = iq[qs].item;
+    const CtxItem<R> it = iq[qs].it;
+    const int rbase = it.z * R;
+    // Q rows as MMA A fragments (rows past R read the zero row)
+    uint32_t qa[8][4];
+    {
+      const int qrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const uint32_t qaddr = qrow < R ? smem_u32(smem + SM::kOffQ + (qs * R + qrow) * kRowBytes)
+                                      : smem_u32(smem + SM::kOffQZero);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) ldsm_x4(qa[ks], qaddr + ((ks * 2 + (lane >> 4)) << 4));
+    }
+    const int g8 = lane >> 2, tq = lane & 3;
+    int lim_ctx[2], lim_pre[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rr = g8 + 8 * hr, li = rbase + rr;
+      const bool ok = item >= 0 && it.n_chunks > 0 && rr < R && li < it.nrows;
+      lim_ctx[hr] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
+      lim_pre[hr] = ok ? a.s_prefix : 0;
+    }
+    // chunks below every valid row's bound need no mask: the smallest bound
+    // over the item's rows is that of its first row
+    const int ctx_nomask = a.causal ? it.c_r - it.m_r + rbase / a.g + 1 : it.c_r;
+    const int mb = mi % kNB;
+    const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
+    MmaRowState st;
+    // One loop, one issue site (instruction-cache footprint): the first pass
+    // lets the issue cursor read this item's slot before it is released.
+    int k = w;
+    for (bool first = true;; first = false) {
+      try_issue(jc);
+      if (first) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&i_empty[qs]);
+        if (++qs == kIQ) {
+          qs = 0;
+          qph ^= 1;
+        }
+        if (item < 0 || it.n_chunks == 0) break;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st.o[nt][e] = 0.f;
+        st.m[0] = st.m[1] = -INFINITY;
+        st.l[0] = st.l[1] = 0.f;
+      }
+      if (k >= it.n_chunks) break;
+      // chunk `consumed` is this warp's commit group number `consumed`; the
+      // groups committed after it may stay in flight
+      const int newer = issued - consumed - 1;
+      if (newer >= 2)
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
+      else if (newer == 1)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();  // every lane's copies of the chunk are visible to the warp
+      const uint32_t src = ring + con_sl * kSlotBytes;
+      const bool pre = k < n_pre;
+      const int key0 = (pre ? k : k - n_pre) * kChunk;
+      const bool mask = key0 + kChunk > (pre ? a.s_prefix : ctx_nomask);
+      chunk_mma(st, qa, src, lane, key0, pre ? lim_pre[0] : lim_ctx[0], pre ? lim_pre[1] : lim_ctx[1],
+                a.scale_log2, mask);
+      __syncwarp();  // every lane's reads precede the refill of this slot
+      ++consumed;
+      con_sl = (con_sl + 1 == kDepth) ? 0 : con_sl + 1;
+      k += kWorkers;
+    }
+    if (item < 0) break;
+    if (it.n_chunks == 0) continue;
+    if (dts && lane == 0) dts[2 + w] = global_timer_ns();
+
+    // ---- hand the warp's state (rows < R) to merge buffer mb
+    mbar_wait(&m_empty[mb], mph ^ 1);
+    float* macc = s_acc + (mb * kWorkers + w) * R * 128;
+    float* mml = s_ml + (mb * kWorkers + w) * R * 2;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rr = g8 + 8 * hr;
+      if (rr < R) {
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(macc + rr * 128 + nt * 8 + 2 * tq) =
+              make_float2(st.o[nt][2 * hr], st.o[nt][2 * hr + 1]);
+        if (tq == 0) {
+          mml[rr * 2] = st.m[hr];
+          mml[rr * 2 + 1] = st.l[hr];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&m_full[mb]);
+    ++mi;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (dts && lane == 0 && w == 0) dts[7] = global_timer_ns();
 }
 
 template <int R>
-static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStream_t stream) {
+static cudaError_t launch_ctx_r(const CtxArgs& a_in, int n_items, int n_z, cudaStream_t stream) {
+  CtxArgs a = a_in;
+  a.knob = g_knobs[3];
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool pdl = a.o_sys != nullptr || a.sys_part_acc != nullptr;
-  cudaError_t e;
-  if (a.s_prefix > 0) {
-    // naive baseline: long per-request key sequences -> 4 consumer warps per item
-    const int smem = kRing * kSlotBytes + (8 * R * 128 + 16 * R) * 4 + 2 * kRing * 8;
-    e = cudaFuncSetAttribute(ctx_cta_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R>, kCtxThreadsPC, smem);
-    if (e != cudaSuccess) return e;
-    const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
-    ctx_cta_kernel<R><<<grid, kCtxThreadsPC, smem, stream>>>(a, n_items, n_z);
-    return cudaGetLastError();
-  }
-  const int smem = kCtxWarps * kWarpSlots * kSlotBytes + kCtxWarps * kWarpSlots * 8;
-  e = cudaFuncSetAttribute(ctx_attn_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = CtaSmem<R>::kBytes;
+  cudaError_t e = cudaFuncSetAttribute(ctx_cta_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_attn_kernel<R>, kCtxWarps * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R>, kCtxThreadsPC, smem);
   if (e != cudaSuccess) return e;
-  const int grid = max(1, min((n_items + kCtxWarps - 1) / kCtxWarps, sms * max(per_sm, 1)));
-  // Relay mode follows the system kernel, which triggers early: launch with
-  // PDL so this kernel streams context K/V on SMs the system kernel has
-  // already released (it waits for the system grid before reading its
-  // outputs).  Other modes are ordinary stream-ordered launches.
-  if (pdl)
-    e = launch_pdl(ctx_attn_kernel<R>, dim3(grid), dim3(kCtxWarps * 32), smem, stream, a, n_items, n_z);
-  else
-    ctx_attn_kernel<R><<<grid, kCtxWarps * 32, smem, stream>>>(a, n_items, n_z);
+  const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
+  // PDL: the relay step's context kernel starts as soon as the system kernel
+  // has triggered (it runs on the SMs the system kernel leaves free); the
+  // other modes wait for their predecessor before the first output write.
+  e = launch_pdl(ctx_cta_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, a, n_items, n_z);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -814,6 +714,104 @@ cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_
     case 4: return launch_ctx_r<4>(a, n_items, n_z, stream);
     default: return launch_ctx_r<8>(a, n_items, n_z, stream);
   }
+}
+
+// ------------------------------------------------------- relay fuse (step)
+// Final combine of the relay step: per (row, head), the context partial of
+// ctx_cta_kernel and every stream-K part of the system kernel's unit, in
+// ONE LSE-weighted merge (`relay_fusion`, attention.py:137-157; the parts
+// are merged in slot order, so the result is deterministic).  One warp per
+// (row, head), lane = 4 head dims.  Launched with PDL after the context
+// kernel: it waits for that grid, then for the system unit's publication
+// counter (the system kernel runs concurrently and may still be running);
+// the last CTA rearms the counters for the next step.
+constexpr int kFuseWarps = 8;
+__global__ void __launch_bounds__(kFuseWarps * 32)
+    relay_fuse_kernel(const rb_sys_plan SP, int n_rows, int hq, const float* __restrict__ part_acc,
+                      const float* __restrict__ part_ml, int* ready, const float* ctx_part,
+                      void* out, int out_fp32, float* lse_out, int* exit_ctr) {
+  pdl_wait_primary();  // context partials of the previous grid
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long pair = static_cast<long long>(blockIdx.x) * kFuseWarps + warp;
+  if (pair < static_cast<long long>(n_rows) * hq) {
+    const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
+    const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
+    const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
+    const int u = (hh / SP.g) * SP.n_qt + qt;
+    const int np = rb_unit_parts(&SP, u);
+    if (lane == 0)
+      while (ld_acquire_gpu(ready + u) < np) __nanosleep(256);
+    __syncwarp();
+    const int d0 = lane * 4;
+    const float* cp = ctx_part + pair * kPartStride;
+    float4 O = __ldcg(reinterpret_cast<const float4*>(cp + d0));
+    const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
+    float mt = ml.x, lt = ml.y;
+    const long long base = static_cast<long long>(u) * SP.max_parts;
+    for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
+      float mk[4], lk[4];
+      float4 ak[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = min(k0 + kk, np - 1);
+        const float* pml = part_ml + (base + k) * 2 * SP.nq;
+        mk[kk] = __ldcg(pml + col);
+        lk[kk] = __ldcg(pml + SP.nq + col);
+        ak[kk] = __ldcg(reinterpret_cast<const float4*>(part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0));
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (k0 + kk >= np) break;
+        const float mn = fmaxf(mt, mk[kk]);
+        const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+        const float sk = fast_exp2(mk[kk] - mn);
+        lt = lt * so + lk[kk] * sk;
+        O.x = O.x * so + ak[kk].x * sk;
+        O.y = O.y * so + ak[kk].y * sk;
+        O.z = O.z * so + ak[kk].z * sk;
+        O.w = O.w * so + ak[kk].w * sk;
+        mt = mn;
+      }
+    }
+    const float inv = 1.f / lt;
+    if (out_fp32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + pair * 128 + d0) =
+          make_float4(O.x * inv, O.y * inv, O.z * inv, O.w * inv);
+    } else {
+      uint2 pk;
+      pk.x = pack_bf16x2(O.x * inv, O.y * inv);
+      pk.y = pack_bf16x2(O.z * inv, O.w * inv);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + d0) = pk;
+    }
+    if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
+  }
+  // the last CTA rearms the unit counters (every reader of them is done)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(exit_ctr, 1) == static_cast<int>(gridDim.x) - 1) {
+      for (int u = 0; u < SP.n_units; ++u) ready[u] = 0;
+      *exit_ctr = 0;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t launch_relay_fuse(const rb_sys_plan& SP, int n_rows, int hq, const float* part_acc,
+                              const float* part_ml, int* ready, const float* ctx_part, void* out,
+                              int out_fp32, float* lse_out, int* exit_ctr, cudaStream_t stream) {
+  const long long pairs = static_cast<long long>(n_rows) * hq;
+  if (pairs == 0) return cudaSuccess;
+  const int grid = static_cast<int>((pairs + kFuseWarps - 1) / kFuseWarps);
+  cudaError_t e = cudaSuccess;
+  if (g_knobs[2] == 1)
+    relay_fuse_kernel<<<grid, kFuseWarps * 32, 0, stream>>>(SP, n_rows, hq, part_acc, part_ml, ready,
+                                                            ctx_part, out, out_fp32, lse_out, exit_ctr);
+  else
+    e = launch_pdl(relay_fuse_kernel, dim3(grid), dim3(kFuseWarps * 32), 0, stream, SP, n_rows, hq,
+                   part_acc, part_ml, ready, ctx_part, out, out_fp32, lse_out, exit_ctr);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- relay fusion

@@ -46,11 +46,10 @@ struct CtxArgs {
   const __nv_bfloat16* pv;
   long long p_stride_tok, p_stride_head;
   int s_prefix;
-  // optional deferred system partials (relay): stream-K slots of the system
-  // kernel, merged here in the fusion epilogue
-  const float* sys_part_acc;     // [n_units][max_parts][nq][128]
-  const float* sys_part_ml;      // [n_units][max_parts][2][nq]
-  rb_sys_plan sys_plan;
+  // relay step: unnormalised context partial per (row, head) instead of the
+  // output, [n_rows * hq][132] floats (O[128], m log2, l); merged with the
+  // system kernel's stream-K parts by relay_fuse_kernel
+  float* ctx_part;
   // optional system partial (relay)
   const float* o_sys;            // [n_rows][hq][128]
   const float* lse_sys;          // [n_rows][hq] natural log
@@ -59,6 +58,12 @@ struct CtxArgs {
   int out_fp32;
   float* lse_out;                // [n_rows][hq] natural log (may be null)
   float scale_log2;
+  unsigned long long* debug_ts;  // optional per-CTA stamps [grid][8] (diagnostics)
+  int* sched;                    // optional [2] zeroed counters: item claims, scheduler exits
+  int knob;                      // diagnostics: g_knobs[3] at launch
 };
+
+// Host-side tuning knobs (rb_debug_set_knob; diagnostics / A-B comparisons).
+extern int g_knobs[8];
 
 }  // namespace rb

@@ -77,3 +77,22 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
   }
   p->max_parts = mp;
 }
+
+// SM split of the concurrent relay step (rb_relay_attention): the system
+// kernel gets a share of the SMs proportional to its HBM bytes weighted by
+// the per-SM streaming rates of the two kernels (each query tile of a KV
+// head streams the whole prefix), the context kernel the rest plus every SM
+// the system kernel releases, so both finish together.
+// RB_RELAY_RATE_RATIO = (system bytes/s per SM) / (context bytes/s per SM),
+// measured on B200 with profiles/sweep_split.py (best splits at s = 2k..32k).
+#define RB_RELAY_RATE_RATIO 1.6
+RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sms) {
+  rb_sys_plan p;
+  rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
+  const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
+  const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
+  int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
+  if (g < 1) g = 1;
+  if (g > sms) g = sms;
+  return g;
+}

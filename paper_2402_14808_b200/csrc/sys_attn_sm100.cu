@@ -40,6 +40,10 @@ namespace rb {
 
 
 constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
+// lazy max: the running max of a query column moves only when a score
+// exceeds it by more than kTau (log2 units), so p <= 2^kTau stays exact in
+// fp32 / bf16 and most tiles skip the cross-warp max reduction
+constexpr float kTau = 8.f;
 
 // Shared-memory / thread layout for a query tile of NQ rows.  Two compute
 // groups alternate key tiles (even / odd local tile index), each with its own
@@ -49,10 +53,11 @@ template <int NQ>
 struct SysCfg {
   static constexpr int H = 16;
   static constexpr int NHALF = NQ / H;
-  static constexpr int WPG = 4 * NHALF;                 // warps per group
-  static constexpr int NCW = 2 * WPG;                   // compute warps
+  static constexpr int WPG = 4 * NHALF;                 // compute warps (one group)
+  static constexpr int NCW = WPG;
   static constexpr int kRoleWarps = 4;                  // K producer, QK issuer, V producer, PV issuer
   static constexpr int kThreads = (kRoleWarps + NCW) * 32;
+
   static constexpr int KS = 2;                          // K ring (freed after Q.K^T)
   static constexpr int VS = 4;                          // V ring (freed after P.V)
   static constexpr int kTileBytes = kKvTileBytes;       // 32 KB per K or V tile
@@ -63,14 +68,16 @@ struct SysCfg {
   static constexpr int kOffP = kOffQ + 2 * kQBytes;
   static constexpr int kRedBytes = 2 * NHALF * 4 * H * 4;  // [group][half][quadrant][H]
   static constexpr int kOffRedMax = kOffP + 2 * kQBytes;
-  static constexpr int kOffRedSum = kOffRedMax + kRedBytes;
-  static constexpr int kOffL = kOffRedSum + kRedBytes;   // [group][NQ]
+  static constexpr int kOffRedSum = kOffRedMax;          // unit-end row sums reuse it
+  static constexpr int kOffL = kOffRedMax + kRedBytes;   // [group][NQ]
   static constexpr int kOffX = kOffL + 2 * NQ * 4;       // handover m, l: [2][NQ]
-  static constexpr int kOffBar = kOffX + 2 * NQ * 4;
+  static constexpr int kOffFlag = kOffX + 2 * NQ * 4;    // lazy-max flags [group][half][2][4]
+  static constexpr int kOffMs = kOffFlag + 2 * NHALF * 2 * 4 * 4;  // running max [grp][half][H]
+  static constexpr int kOffBar = kOffMs + 2 * NHALF * H * 4;
   static constexpr int kNumBars = 2 * KS + 2 * VS + 18;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   static constexpr int kBytes = kOffMisc + 64;
-  static constexpr int kTmemCols = (5 * NQ <= 128) ? 128 : (5 * NQ <= 256) ? 256 : 512;
+  static constexpr int kTmemCols = (3 * NQ <= 128) ? 128 : 256;  // S x2, O
 };
 
 template <int H>
@@ -133,6 +140,8 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   float* red_sum = reinterpret_cast<float*>(smem + L::kOffRedSum);
   float* l_s = reinterpret_cast<float*>(smem + L::kOffL);
   float* x_ml = reinterpret_cast<float*>(smem + L::kOffX);
+  int* rflag = reinterpret_cast<int*>(smem + L::kOffFlag);
+  float* m_sm = reinterpret_cast<float*>(smem + L::kOffMs);
 
   const rb_sys_plan& P = args.plan;
   const int warp = threadIdx.x >> 5;
@@ -173,10 +182,11 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = misc[0];
-  if (dts && threadIdx.x == 0) dts[1] = global_timer_ns();
-  // the next kernel (context + fusion) may be scheduled as SMs free up; it
-  // waits for this grid's memory before it reads o_sys / lse_sys.
-  pdl_launch_dependents();
+  if (dts && threadIdx.x == 0) dts[1] = smid();
+  // extended startup stamps (diagnostics): prologue, K issue, Q ready, K0 full,
+  // first MMA, V issue
+  unsigned long long* dtx = dts ? args.debug_ts + 2048 * 8 + blockIdx.x * 8 : nullptr;
+  if (dtx && threadIdx.x == 0) dtx[0] = global_timer_ns();
 
   const uint32_t smem_k = smem_u32(smem + L::kOffK);
   const uint32_t smem_v = smem_u32(smem + L::kOffV);
@@ -199,12 +209,19 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         mbar_arrive_expect_tx(&k_full[st], L::kTileBytes);
         tma_load_3d(dst, &tmap_k, &k_full[st], 0, kt * RB_KEY_TILE, h, pol);
         tma_load_3d(dst + L::kTileBytes / 2, &tmap_k, &k_full[st], 64, kt * RB_KEY_TILE, h, pol);
+        if (dtx && j == 0) dtx[1] = global_timer_ns();
       }
       __syncwarp();
       if (i == t_begin || kt == 0) {
         // query rows of unit u (after this tile's K is already in flight);
         // q may be produced by the previous kernel in the stream.
-        if (i == t_begin) pdl_wait_primary();
+        if (i == t_begin) {
+          pdl_wait_primary();
+          // the next kernel (context + fusion) may now be scheduled as SMs
+          // free up: everything this grid waited for is visible to it too.
+          // It waits for this grid's own memory before reading the partials.
+          pdl_launch_dependents();
+        }
         const int qb = uq & 1;
         mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
         uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
@@ -226,6 +243,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&q_full[qb]);
+        if (dtx && lane == 0 && uq == 0) dtx[2] = global_timer_ns();
         ++uq;
       }
     }
@@ -233,10 +251,13 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     // ------------------------------------------------------------ V producer
     const uint64_t pol = l2_policy_evict_first();
     if (lane == 0) {
-      // Start streaming V only once this CTA's first K tile has landed: at
-      // launch every SM fires its rings at once, and the first Q.K^T must not
-      // queue behind four V tiles per SM.
-      if (t_begin < t_end) mbar_wait(&k_full[0], 0);
+      // Start streaming V only once this CTA's first K tile and its query
+      // rows have landed: at launch every SM fires its rings at once, and the
+      // first Q.K^T must not queue behind four V tiles per SM.
+      if (t_begin < t_end) {
+        mbar_wait(&k_full[0], 0);
+        mbar_wait(&q_full[0], 0);  // Q rows must not queue behind the V burst either
+      }
       int j = 0;
       for (long long i = t_begin; i < t_end; ++i, ++j) {
         const int u = static_cast<int>(i / P.tpu);
@@ -248,6 +269,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         mbar_arrive_expect_tx(&v_full[st], L::kTileBytes);
         tma_load_3d(dst, &tmap_v, &v_full[st], 0, kt * RB_KEY_TILE, h, pol);
         tma_load_3d(dst + L::kTileBytes / 2, &tmap_v, &v_full[st], 64, kt * RB_KEY_TILE, h, pol);
+        if (dtx && j == 0) dtx[5] = global_timer_ns();
       }
     }
     __syncwarp();
@@ -264,6 +286,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         if (new_unit) mbar_wait(&q_full[qb], (uq >> 1) & 1);
         const int st = j % KS, sb = j & 1;
         mbar_wait(&k_full[st], (j / KS) & 1);
+        if (dtx && j == 0) dtx[3] = global_timer_ns();
         mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k_base = smem_k + st * L::kTileBytes;
@@ -278,6 +301,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           umma_f16_ss(d_tmem, a, b, idesc_qk, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
+        if (dtx && j == 0) dtx[4] = global_timer_ns();
         umma_commit(&k_empty[st]);
         if (last_of_unit) {
           umma_commit(&q_empty[qb]);
@@ -293,52 +317,56 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       int j = 0;
       for (long long i = t_begin; i < t_end; ++i, ++j) {
         const int st = j % VS, pb = j & 1;
+        // O accumulates over the tiles of a unit; its first tile starts fresh
+        const long long ua = max(t_begin, (i / P.tpu) * P.tpu);
+        const uint32_t acc0 = (i > ua) ? 1u : 0u;
         mbar_wait(&v_full[st], (j / VS) & 1);
         mbar_wait(&p_full[pb], (j >> 1) & 1);
-        mbar_wait(&o_empty[pb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t v_base = smem_v + st * L::kTileBytes;
         const uint32_t p_base = smem_p + pb * L::kQBytes;
-        const uint32_t d_tmem = tmem_base + 2 * NQ + pb * NQ;
+        const uint32_t d_tmem = tmem_base + 2 * NQ;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           // A = V^T (M = d, MN-major): 16 keys = two 8-row swizzle atoms.
           const uint64_t a = make_smem_desc_sw128(v_base + kk * 2048, L::kTileBytes / 2, 1024);
           const uint64_t b =
               make_smem_desc_sw128(p_base + (kk >> 2) * (NQ * 128) + (kk & 3) * 32, 16, 1024);
-          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : 0u);
+          umma_f16_ss(d_tmem, a, b, idesc_pv, kk > 0 ? 1u : acc0);
         }
-        umma_commit(&o_full[pb]);
+        umma_commit(&o_full[pb]);  // alternating by tile: see the waits below
         umma_commit(&v_empty[st]);
         umma_commit(&p_empty[pb]);
       }
     }
     __syncwarp();
   } else {
-    // ------------------------------------- softmax / O accumulation groups
+    // -------------------------------------------- softmax / O accumulation
+    // One compute group: NHALF column slices x 4 TMEM lane quadrants.  Tiles
+    // go through it in order; S and P are double-buffered so Q.K^T of tile
+    // j+1 and P.V of tile j-1 overlap the softmax of tile j, and O
+    // accumulates in TMEM across a unit (the P.V MMAs chain).
     const int cw = warp - L::kRoleWarps;
-    const int grp = cw / L::WPG;                 // which tile parity this group owns
-    const int hf = (cw / 4) % L::NHALF;          // column slice
+    const int hf = cw / 4;                       // column slice
     const int qd = warp & 3;                     // TMEM lane quadrant (hardware: warp % 4)
     const int col0 = hf * H;
     const bool designated = (qd == 0) && lane < H;
-    const uint32_t bar_red = 1 + grp * L::NHALF + hf;
-    const uint32_t bar_grp = 1 + 2 * L::NHALF + grp;
+    const uint32_t bar_red = 1 + hf;
+    const uint32_t bar_grp = 1 + L::NHALF;
     const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(qd * 32) << 16);
-    float* rmax = red_max + (grp * L::NHALF + hf) * 4 * H;
-    float* rsum = red_sum + (grp * L::NHALF + hf) * 4 * H;
-    float* lg = l_s + grp * NQ;
+    const uint32_t o_addr = lane_addr + 2 * NQ + col0;
+    float* rmax = red_max + hf * 4 * H;
+    float* rsum = rmax;  // unit-end row sums reuse the max scratch
+    float* lg = l_s;
     const int rcol = reduce_scatter_col<H>(lane);
     const bool rwriter = (lane & ((32 / H) - 1)) == 0;
     const int key_lane = qd * 32 + lane;
-    // per-thread swizzled P row offsets (8-row pattern) for this key lane
-    uint32_t poff[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) poff[r] = sw128_offset(r, key_lane & 63);
+    // swizzled P column of this key lane: chunk (key & 63) / 8, byte (key & 7) * 2
+    const uint32_t pkch = static_cast<uint32_t>((key_lane & 63) >> 3);
+    const uint32_t pkby = static_cast<uint32_t>((key_lane & 7) << 1);
     const uint32_t pkb = (key_lane >> 6) * (NQ * 128);
 
-    float m_run[H], acc[H];
-    int xh = 0;  // handovers so far
+    float m_run[H], acc[H], l_part[H];
     pdl_wait_primary();  // o_sys / partials may still be read by the previous kernel
     long long i = t_begin;
     while (i < t_end) {
@@ -348,13 +376,12 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
 #pragma unroll
       for (int c = 0; c < H; ++c) {
         m_run[c] = -INFINITY;
-        acc[c] = 0.f;
+        l_part[c] = 0.f;
       }
-      if (designated) lg[col0 + lane] = 0.f;
-      for (long long it = ia + ((ia - t_begin + grp) & 1); it <= ib; it += 2) {
+      for (long long it = ia; it <= ib; ++it) {
         const int j = static_cast<int>(it - t_begin);
         const int kt = static_cast<int>(it % P.tpu);
-        const int gb = j & 1;  // == grp
+        const int gb = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         // ---- S tile -> scores (log2 domain)
         mbar_wait(&s_full[gb], ph);
@@ -367,38 +394,68 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[gb]);
         const bool valid = kt * RB_KEY_TILE + key_lane < P.s;
+        bool over = false;
 #pragma unroll
-        for (int c = 0; c < H; ++c) x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
-        // ---- tile max over the 128 key lanes (4 quadrant warps)
-        {
+        for (int c = 0; c < H; ++c) {
+          x[c] = valid ? x[c] * args.scale_log2 : -INFINITY;
+          over |= x[c] > m_run[c] + kTau;
+        }
+        // ---- lazy max: the running max moves only when some score of the
+        // column exceeds it by more than kTau (always on a unit's first tile);
+        // the 4 quadrant warps agree through one flag exchange
+        int* fl = rflag + (hf * 2 + gb) * 4;
+        over = __any_sync(0xffffffffu, over);
+        if (lane == 0) fl[qd] = over ? 1 : 0;
+        named_bar_sync(bar_red, 128);
+        const int4 fv = *reinterpret_cast<const int4*>(fl);
+        if (fv.x | fv.y | fv.z | fv.w) {
           float tmp[H];
 #pragma unroll
           for (int c = 0; c < H; ++c) tmp[c] = x[c];
           const float wmax = warp_reduce_scatter<H, true>(tmp, lane);
           if (rwriter) rmax[qd * H + rcol] = wmax;
-        }
-        named_bar_sync(bar_red, 128);
-        float my_al = 0.f;
+          named_bar_sync(bar_red, 128);
+          float al[H];
 #pragma unroll
-        for (int c4 = 0; c4 < H; c4 += 4) {
-          const float4 a0 = *reinterpret_cast<const float4*>(rmax + 0 * H + c4);
-          const float4 a1 = *reinterpret_cast<const float4*>(rmax + 1 * H + c4);
-          const float4 a2 = *reinterpret_cast<const float4*>(rmax + 2 * H + c4);
-          const float4 a3 = *reinterpret_cast<const float4*>(rmax + 3 * H + c4);
-          const float tm[4] = {fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)),
-                               fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y)),
-                               fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)),
-                               fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))};
+          for (int c4 = 0; c4 < H; c4 += 4) {
+            const float4 a0 = *reinterpret_cast<const float4*>(rmax + 0 * H + c4);
+            const float4 a1 = *reinterpret_cast<const float4*>(rmax + 1 * H + c4);
+            const float4 a2 = *reinterpret_cast<const float4*>(rmax + 2 * H + c4);
+            const float4 a3 = *reinterpret_cast<const float4*>(rmax + 3 * H + c4);
+            const float tm[4] = {fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x)),
+                                 fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y)),
+                                 fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z)),
+                                 fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w))};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int c = c4 + e;
-            const float mn = fmaxf(m_run[c], tm[e]);
-            const float al = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
-            acc[c] *= al;
-            my_al = (lane == c) ? al : my_al;
-            m_run[c] = mn;
-            x[c] = fast_exp2(x[c] - mn);  // p; exactly 0 for masked keys
+            for (int e = 0; e < 4; ++e) {
+              const int c = c4 + e;
+              const float mn = fmaxf(m_run[c], tm[e]);
+              al[c] = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - mn);
+              m_run[c] = mn;
+              l_part[c] *= al[c];
+            }
           }
+          if (it > ia) {
+            // rescale the O accumulator once the previous P.V has landed.
+            // o_full alternates by tile, so this parity wait is unambiguous:
+            // P.V(j-3) is known complete (p_empty of tile j-1).
+            mbar_wait(&o_full[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+            tc_fence_after();
+            float o[H];
+            tmem_ld_32x32b<H>(o_addr, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < H; ++c) o[c] *= al[c];
+            tmem_st_32x32b<H>(o_addr, o);
+            tmem_wait_st();
+            tc_fence_before();
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          const float mu = (m_run[c] == -INFINITY) ? 0.f : m_run[c];
+          x[c] = fast_exp2(x[c] - mu);  // p; exactly 0 for masked keys
+          l_part[c] += x[c];
         }
         // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
         mbar_wait(&p_empty[gb], ph ^ 1);
@@ -406,81 +463,40 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           uint8_t* pdst = smem + L::kOffP + gb * L::kQBytes + pkb;
 #pragma unroll
           for (int c = 0; c < H; ++c) {
-            const int row = col0 + c;
-            *reinterpret_cast<__nv_bfloat16*>(pdst + (row >> 3) * 1024 + poff[row & 7]) =
-                __float2bfloat16_rn(x[c]);
+            const int row = col0 + c;  // row & 7 == c & 7 (col0 is a multiple of 16)
+            const uint32_t off = (row >> 3) * 1024 + (c & 7) * 128 + ((pkch ^ (c & 7)) << 4) + pkby;
+            *reinterpret_cast<__nv_bfloat16*>(pdst + off) = __float2bfloat16_rn(x[c]);
           }
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[gb]);
-        // ---- row sums
-        const float wsum = warp_reduce_scatter<H, false>(x, lane);
-        if (rwriter) rsum[qd * H + rcol] = wsum;
-        named_bar_sync(bar_red, 128);
-        if (designated) {
-          const float lt = rsum[0 * H + lane] + rsum[1 * H + lane] + rsum[2 * H + lane] +
-                           rsum[3 * H + lane];
-          lg[col0 + lane] = lg[col0 + lane] * my_al + lt;
-        }
-        // ---- O tile of this key tile
-        mbar_wait(&o_full[gb], ph);
-        tc_fence_after();
-        float o[H];
-        tmem_ld_32x32b<H>(lane_addr + 2 * NQ + gb * NQ + col0, o);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&o_empty[gb]);
-#pragma unroll
-        for (int c = 0; c < H; ++c) acc[c] += o[c];
       }
 
-      // ---- unit end: merge the two groups, then write / stream-K merge
-      const int fin = static_cast<int>((ib - t_begin) & 1);
-      const bool two = ib > ia;
-      const uint32_t xaddr = lane_addr + 4 * NQ + col0;
-      if (two && grp != fin) {
-        // helper: hand (acc, m, l) to the finisher through TMEM / smem
-        mbar_wait(x_empty, (xh & 1) ^ 1);
-        tmem_st_32x32b<H>(xaddr, acc);
-        tmem_wait_st();
-        if (designated) {
-          float mv = m_run[0];
-#pragma unroll
-          for (int c = 1; c < H; ++c) mv = (lane == c) ? m_run[c] : mv;
-          x_ml[col0 + lane] = mv;
-          x_ml[NQ + col0 + lane] = lg[col0 + lane];
-        }
+      // ---- unit end: O from TMEM (after the unit's last P.V), row sums
+      // reduced over the 128 key lanes once per unit, then write / merge
+      {
+        const int jl = static_cast<int>(ib - t_begin);
+        // P.V(jl) complete implies every earlier MMA complete
+        mbar_wait(&o_full[jl & 1], static_cast<uint32_t>((jl >> 1) & 1));
+        tc_fence_after();
+        tmem_ld_32x32b<H>(o_addr, acc);
+        tmem_wait_ld();
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(x_full);
+        const float wsum = warp_reduce_scatter<H, false>(l_part, lane);
+        named_bar_sync(bar_red, 128);  // rsum aliases rmax: last tile's max reads done
+        if (rwriter) rsum[qd * H + rcol] = wsum;
+        named_bar_sync(bar_red, 128);
+        if (designated)
+          lg[col0 + lane] = rsum[0 * H + lane] + rsum[1 * H + lane] + rsum[2 * H + lane] +
+                            rsum[3 * H + lane];
+        named_bar_sync(bar_grp, L::NCW * 32);  // lg complete; rsum reads done
       }
-      if (grp == fin) {
-        named_bar_sync(bar_grp, L::WPG * 32);  // own l_s complete
+      {
         float lrow[H];
 #pragma unroll
         for (int c = 0; c < H; ++c) lrow[c] = lg[col0 + c];
-        if (two) {
-          mbar_wait(x_full, xh & 1);
-          tc_fence_after();
-          float oh[H];
-          tmem_ld_32x32b<H>(xaddr, oh);
-          tmem_wait_ld();
-#pragma unroll
-          for (int c = 0; c < H; ++c) {
-            const float mh = x_ml[col0 + c], lh = x_ml[NQ + col0 + c];
-            const float M = fmaxf(m_run[c], mh);
-            const float wf = (m_run[c] == -INFINITY) ? 0.f : fast_exp2(m_run[c] - M);
-            const float wh = (mh == -INFINITY) ? 0.f : fast_exp2(mh - M);
-            acc[c] = acc[c] * wf + oh[c] * wh;
-            lrow[c] = lrow[c] * wf + lh * wh;
-            m_run[c] = M;
-          }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(x_empty);
-        }
+        named_bar_sync(bar_grp, L::NCW * 32);  // lg reads done before the next unit's writes
         const int h = u / P.n_qt, qt = u % P.n_qt;
         const long long u_first = static_cast<long long>(u) * P.tpu;
         const int owner0 = rb_tile_owner(&P, u_first);
@@ -499,6 +515,15 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
             if (qd == 0 && lane == 0) {
               pml[col] = m_run[c];
               pml[NQ + col] = lrow[c];
+            }
+          }
+          if (args.counters != nullptr) {
+            // publish the part: the context kernel, running concurrently,
+            // polls the unit's counter (release after the group's writes)
+            named_bar_sync(bar_grp, L::NCW * 32);
+            if (cw == 0 && lane == 0) {
+              __threadfence();
+              atomicAdd(&args.counters[u], 1);
             }
           }
         } else if (nparts == 1) {
@@ -527,16 +552,16 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
               pml[NQ + col] = lrow[c];
             }
           }
-          __threadfence();
-          named_bar_sync(bar_grp, L::WPG * 32);
-          if (cw == grp * L::WPG && lane == 0) {
+          named_bar_sync(bar_grp, L::NCW * 32);
+          if (cw == 0 && lane == 0) {
+            __threadfence();
             const int prev = atomicAdd(&args.counters[u], 1);
             const int last = (prev == nparts - 1);
             if (last) atomicExch(&args.counters[u], 0);
-            misc[2 + grp] = last;
+            misc[2] = last;
           }
-          named_bar_sync(bar_grp, L::WPG * 32);
-          if (misc[2 + grp]) {
+          named_bar_sync(bar_grp, L::NCW * 32);
+          if (misc[2]) {
             // last CTA of unit u: merge the slots in slot order (deterministic
             // whoever merges); per slot all H columns' loads are in flight.
             __threadfence();
@@ -589,11 +614,9 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           }
         }
       }
-      if (two) ++xh;
       i = unit_end;
     }
     if (dts && threadIdx.x == L::kRoleWarps * 32) dts[3] = global_timer_ns();
-    if (dts && threadIdx.x == (L::kRoleWarps + L::WPG) * 32) dts[4] = global_timer_ns();
   }
 
   if (dts && threadIdx.x == 0) dts[5] = global_timer_ns();

@@ -1,0 +1,143 @@
+"""Per-SM timeline of one relay decode step (system kernel + paged context
+kernel with the fused epilogue) from %globaltimer stamps
+(rb_debug_set_timestamps).  Diagnostics only.
+
+    python profiles/diag_relay_timeline.py [s] [phases]
+
+System CTA stamps [1024][8]: entry, smid, first_S, grp0_end, grp1_end,
+kprod_end, vprod_end, exit.  Extended system startup stamps at offset 2048*8: prologue, first K
+issue, Q ready, first K full, first MMA, first V issue.  Context CTA stamps
+start at offset 1024*8:
+entry, smid, warp0..3 compute end, after-PDL-wait, exit.
+"""
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2402_14808_b200 import _lib, kernels  # noqa: E402
+
+
+def q(col):
+    col = sorted(col)
+    n = len(col)
+    return f"min {col[0]:6.1f} p10 {col[n // 10]:6.1f} p50 {col[n // 2]:6.1f} p90 {col[int(n * .9)]:6.1f} max {col[-1]:6.1f}"
+
+
+def run(s, phases=3, b=32, h=52, c=128):
+    dev = torch.device("cuda", 0)
+    qq = torch.randn((b, h, 128), device=dev).to(torch.bfloat16)
+    k = torch.randn((h, s, 128), device=dev).to(torch.bfloat16)
+    v = torch.randn((h, s, 128), device=dev).to(torch.bfloat16)
+    nblk = c // 16
+    grid = int(os.environ.get("DIAG_GRID", "0")) or _lib.relay_sys_grid(b, h, h, s, b * c, kernels.sm_count(dev))
+    pk = torch.randn((b * nblk, h, 16, 128), device=dev).to(torch.bfloat16)
+    pv = torch.randn_like(pk)
+    pst = (pk.stride(0), pk.stride(2), pk.stride(1))
+    bt = torch.randperm(b * nblk, device=dev).to(torch.int32).reshape(b, nblk)
+    if os.environ.get("DIAG_SEQBT"):
+        bt = torch.arange(b * nblk, device=dev, dtype=torch.int32).reshape(b, nblk)
+    cl = torch.full((b,), c, dtype=torch.int32, device=dev)
+    qs = torch.arange(b + 1, dtype=torch.int32, device=dev)
+    ts = torch.zeros((8192, 8), dtype=torch.int64, device=dev)
+    import bench
+    flush_fn = bench.make_flush(torch, dev)
+    for it in range(5):
+        if not os.environ.get("DIAG_NOFLUSH"):
+            flush_fn()
+        ts.zero_()
+        _lib.load().rb_debug_set_timestamps(ts.data_ptr() if it == 4 else None)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=1, hkv=h, sys_layout="hsd",
+                                block_table=bt, block_size=16, strides=pst, grid=grid,
+                                phases=phases)
+        e1.record()
+        torch.cuda.synchronize()
+    _lib.load().rb_debug_set_timestamps(None)
+    t = ts.cpu()
+    sys_t = t[:1024][t[:1024, 0] != 0]
+    ctx_t = t[1024:2048][t[1024:2048, 0] != 0]
+    starts = []
+    if len(sys_t):
+        starts.append(int(sys_t[:, 0].min()))
+    if len(ctx_t):
+        starts.append(int(ctx_t[:, 0].min()))
+    t0 = min(starts)
+    us = lambda x: (int(x) - t0) / 1e3  # noqa: E731
+    print(f"s={s} phases={phases} sys grid {grid}: event {e0.elapsed_time(e1) * 1e3:.1f} us")
+    sys_exit = {}
+    if len(sys_t):
+        for i, n in enumerate(["entry", "first_S", "grp0_end", "grp1_end", "kprod_end", "vprod_end", "exit"]):
+            col = [us(r[i if i == 0 else i + 1]) for r in sys_t]
+            print(f"  sys {n:10s} {q(col)}")
+        ext = t[2048:][t[2048:, 0] != 0]
+        for i, n in enumerate(["prologue", "k0_issue", "q_ready", "k0_full", "mma0", "v0_issue"]):
+            col = [us(r[i]) for r in ext if r[i] != 0]
+            if col:
+                print(f"  sys {n:10s} {q(col)}")
+        for r in sys_t:
+            sys_exit[int(r[1])] = us(r[7])
+    if len(ctx_t):
+        print(f"  ctx CTAs {len(ctx_t)}")
+        print(f"  ctx entry      {q([us(r[0]) for r in ctx_t])}")
+        ce = [us(r[2 + w]) for r in ctx_t for w in range(4) if r[2 + w] != 0]
+        print(f"  ctx warp compute end {q(ce)}")
+        pw = [us(r[6]) for r in ctx_t if r[6] != 0]
+        if pw:
+            print(f"  ctx after pdl wait   {q(pw)}")
+        print(f"  ctx exit       {q([us(r[7]) for r in ctx_t])}")
+        per_sm = {}
+        for r in ctx_t:
+            per_sm.setdefault(int(r[1]), []).append(r)
+        cnt = [len(v_) for v_ in per_sm.values()]
+        print(f"  ctx CTAs per SM: {sorted(set(cnt))} (SMs used {len(per_sm)}), hist "
+              + str({k_: cnt.count(k_) for k_ in sorted(set(cnt))}))
+        last = sorted(per_sm.items(), key=lambda kv: max(us(r[7]) for r in kv[1]))
+        for sm, rows in last[-6:] + last[:3]:
+            print(f"    sm {sm:3d}: sys exit {sys_exit.get(sm, float('nan')):6.1f}; ctx entries "
+                  + ", ".join(f"{us(r[0]):.1f}" for r in rows) + "; compute ends "
+                  + ", ".join(f"{us(r[2 + w]):.1f}" for r in rows for w in range(4) if r[2 + w])
+                  + "; exits " + ", ".join(f"{us(r[7]):.1f}" for r in rows))
+        it = t[3072:].reshape(-1, 32)[:, :30].reshape(-1, 6, 5)
+        it = it[it[:, 0, 0] != 0]
+        if len(it):
+            names = ["publish", "epi_mfull", "w0_chunks_done", "w0_start", "epi_end"]
+            for j in range(6):
+                ok = it[:, j, 4] != 0
+                if ok.sum() < 10:
+                    break
+                x = it[ok, j]
+                print(f"  item {j}: " + "; ".join(
+                    f"{n} {statistics.median([us(v) for v in x[:, i].tolist()]):.1f}"
+                    for i, n in enumerate(names)))
+        ch = t[6144:].reshape(-1, 32)[:len(ctx_t)].reshape(-1, 16, 2)
+        print(f"  chunk stamps: {int((ch[:, :, 0] != 0).sum())} issue, {int((ch[:, :, 1] != 0).sum())} landed")
+        ch = ch[ch[:, 0, 0] != 0]
+        if len(ch):
+            for c in range(12):
+                ok = (ch[:, c, 0] != 0) & (ch[:, c, 1] != 0)
+                if ok.sum() < 10:
+                    break
+                iss = [us(v) for v in ch[ok, c, 0].tolist()]
+                lan = [us(v) for v in ch[ok, c, 1].tolist()]
+                print(f"  w0 chunk {c}: issued {statistics.median(iss):.1f} consumed {statistics.median(lan):.1f}")
+        mg = t[7424:].reshape(-1, 16)[:len(ctx_t)].reshape(-1, 8, 2)
+        print(f"  merge stamps: {int((mg != 0).sum())}")
+        for c in range(6):
+            ok = (mg[:, c, 0] != 0) & (mg[:, c, 1] != 0)
+            if ok.sum() < 10:
+                break
+            print(f"  merge {c}: start {statistics.median([us(v) for v in mg[ok, c, 0].tolist()]):.1f} "
+                  f"inputs ready {statistics.median([us(v) for v in mg[ok, c, 1].tolist()]):.1f}")
+        durs = [(int(r[7]) - int(r[0])) / 1e3 for r in ctx_t]
+        print(f"  ctx CTA duration p50 {statistics.median(durs):.1f} max {max(durs):.1f}")
+
+
+if __name__ == "__main__":
+    s = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+    ph = [int(sys.argv[2])] if len(sys.argv) > 2 else [3, 2]
+    for p in ph:
+        run(s, p)

@@ -8,6 +8,8 @@
 // CTA streams its own contiguous 64 MB slice of a 9.5 GB buffer (no L2 reuse).
 // mode 0: 3-D tensor box {64, rows, 1} with SWIZZLE_128B (rows * 128 B per box)
 // mode 1: 1-D cp.async.bulk of `bytes` per copy
+// mode 2: 1-D cp.async.bulk from pseudo-random `bytes`-aligned offsets of a
+//         shared 256 MB region (the paged-KV pattern: scattered blocks)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -50,8 +52,15 @@ __global__ void __launch_bounds__(32, 1)
           const long long row = (cta_off / 128) + op * rows_per_op;
           tma_load_3d(dst, &tm, &full[s], 0, static_cast<int>(row % 65536),
                       static_cast<int>(row / 65536), l2_policy_evict_first());
-        } else {
+        } else if (mode == 1) {
           bulk_copy_g2s(dst, base + cta_off + op * bytes_per_op, bytes_per_op, &full[s]);
+        } else {
+          const unsigned long long hsh =
+              (static_cast<unsigned long long>(blockIdx.x) * 0x9E3779B97F4A7C15ull +
+               static_cast<unsigned long long>(op) * 0xBF58476D1CE4E5B9ull) >> 20;
+          const long long nslots = (256ll << 20) / bytes_per_op;
+          bulk_copy_g2s(dst, base + (static_cast<long long>(hsh % nslots)) * bytes_per_op,
+                        bytes_per_op, &full[s]);
         }
       }
     }
@@ -87,7 +96,7 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("mode,bytes_per_op,ops_per_slot,GB/s_total,GB/s_per_SM,ns_per_op\n");
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 3; ++mode) {
     for (int bpo : {1024, 2048, 4096, 8192, 16384}) {
       CUtensorMap tm;
       const long long rows_total = total / 128;
@@ -113,7 +122,7 @@ int main() {
       const double bytes = static_cast<double>(slot_iters) * kSlotBytes * sms;
       const double gbs = bytes / (ms * 1e-3) / 1e9;
       const double ops = static_cast<double>(slot_iters) * ops_per_slot;
-      printf("%s,%d,%d,%.0f,%.1f,%.1f\n", mode == 0 ? "tma_tensor" : "bulk", bpo, ops_per_slot,
+      printf("%s,%d,%d,%.0f,%.1f,%.1f\n", mode == 0 ? "tma_tensor" : mode == 1 ? "bulk" : "bulk_random", bpo, ops_per_slot,
              gbs, gbs / sms, ms * 1e6 / ops);
     }
   }
