@@ -155,13 +155,14 @@ def measured_peaks():
         return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(kernel, s):
-    """dram bytes per launch of `kernel` at system length s from the committed
-    ncu summary (profiles/ncu_summary.json), if one exists for this config."""
+def ncu_traffic(kernels, s):
+    """dram bytes per step of `kernels` (summed) at system length s from the
+    committed ncu summary (profiles/ncu_summary.json), if every one of them
+    has an entry for this config."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             data = json.load(f)
-        return data["kernels"][kernel][str(s)]["dram_bytes"]
+        return sum(data["kernels"][k][str(s)]["dram_bytes"] for k in kernels)
     except Exception:
         return None
 
@@ -351,10 +352,17 @@ def run_b200(args):
             res["naive_ms"] = statistics.mean(
                 time_loop(torch, lambda: naive(q), max(3, args.steps // 5), 2, flush, barrier))
         if with_split:
+            # each kernel alone on every SM (the step runs them concurrently
+            # on a byte-proportional SM split)
+            from paper_2402_14808_b200.attention import RelayDecodeStep
+            alone = RelayDecodeStep(relay.sys_cache, paged, bt, relay.ctx_lens, len(heads),
+                                    grid=kernels.sm_count(device))
             res["sys_ms"] = statistics.mean(
-                time_loop(torch, lambda: relay.system(q), args.steps, args.warmup, flush, barrier))
+                time_loop(torch, lambda: alone.system(q), args.steps, args.warmup, flush, barrier))
             res["ctx_ms"] = statistics.mean(
-                time_loop(torch, lambda: relay.context(q), args.steps, args.warmup, flush, barrier))
+                time_loop(torch, lambda: alone.context(q), args.steps, args.warmup, flush, barrier))
+            res["sys_grid"] = relay.grid
+            del alone
         if with_e2e:
             res.update(e2e_stats(q, relay, paged, bt))
         # size-independent parity: relay == naive per-request kernel
@@ -438,12 +446,16 @@ def run_b200(args):
 
     shape = DecodeShape(B, H, H, args.s, B * C)
     sys_bytes_local = 2 * 2 * len(heads) * D * args.s + 2 * B * len(heads) * D
-    achieved = sys_bytes_local / (sys_ms * 1e-3) / 1e9
+    # roofline of the step: the system and context kernels stream
+    # concurrently on disjoint SMs, so the bound is the whole step's
+    # algorithmic bytes over the step time
+    step_bytes_local = DecodeShape(B, len(heads), len(heads), args.s, B * C).bytes_alg
+    achieved = step_bytes_local / (ms * 1e-3) / 1e9
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args.s, args.cpu_budget)
     value_us = ms * 1e3
-    launches = 2
+    launches = 3  # system, context, fuse kernels per step
     line = {
         "metric": METRIC, "value": value_us, "unit": "µs/step", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -454,7 +466,8 @@ def run_b200(args):
                    "global_batch": B, "seq_len": args.s,
                    "parallelism": f"kv-head-shard{world}" if world > 1 else "single-gpu",
                    "l2": "flushed between timed steps: write a 2x-L2 buffer, then read another 2x-L2 buffer (evicts inputs, write-back outside the timed region)",
-                   "timing": "CUDA-graph replay of the 2-kernel step" if head.get("graph_ms", 1e9) <= head["eager_ms"] else "eager launches"},
+                   "timing": "CUDA-graph replay of the 3-kernel step" if head.get("graph_ms", 1e9) <= head["eager_ms"] else "eager launches",
+                   "sys_sm_split": head["sys_grid"]},
         "tokens_per_s": B / (ms * 1e-3),
         "hbm_gbs": shape.bytes_alg / (ms * 1e-3) / 1e9,
         "frac_of_hbm_roofline": (shape.bytes_alg / (hbm * 1e9)) / (ms * 1e-3),
@@ -462,18 +475,21 @@ def run_b200(args):
         "eager_us_per_step": maxr(head["eager_ms"]) * 1e3,
         "graph_us_per_step": maxr(head.get("graph_ms", float("nan"))) * 1e3,
         "naive_us_per_step": maxr(head["naive_ms"]) * 1e3,
-        "sys_kernel_us": sys_ms * 1e3, "ctx_kernel_us": ctx_ms * 1e3,
-        "roofline": {"bound": "hbm", "kernel": "sys_attn_sm100_kernel",
+        "sys_kernel_alone_us": sys_ms * 1e3, "ctx_kernel_alone_us": ctx_ms * 1e3,
+        "sys_kernel_alone_gbs": sys_bytes_local / (sys_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm",
+                     "kernel": "relay step: sys_attn_sm100_kernel || ctx_cta_kernel (concurrent) + relay_fuse_kernel",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "traffic": ncu_traffic("sys_attn_sm100_kernel", args.s),
-                     "algorithmic_bytes_per_launch": sys_bytes_local},
+                     "traffic": ncu_traffic(("sys_attn_sm100_kernel", "ctx_cta_kernel", "relay_fuse_kernel"),
+                                            args.s),
+                     "algorithmic_bytes_per_launch": step_bytes_local},
         "e2e": {"value": e2e_ms * 1e3, "unit": "µs/step", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],
                 "path": "RelayDecodeStep.host_step_graph (CUDA graph): pinned H2D of [q|k_new|v_new] "
-                        "-> rb_kv_append -> rb_system_attention -> rb_context_attention(relay) -> D2H out",
+                        "-> rb_kv_append -> rb_relay_attention (system || context, fuse) -> D2H out",
                 "eager_us": maxr(head["e2e_eager_ms"]) * 1e3, "graph_us": maxr(head["e2e_graph_ms"]) * 1e3,
-                "launches_per_step": 3},
+                "launches_per_step": 4},
         "gpu_launches": launches * args.steps,
         "parity_max_abs_vs_naive": head["parity_max_abs_vs_naive"],
         "sys_plan": head["plan"],

@@ -3,8 +3,9 @@ markdown table.  Run here (no GPU needed):
 
     python profiles/summarize_ncu.py <tag> <kernel_key> <s> <report.ncu-rep> [...]
 
-kernel_key names the kernel in the summary (e.g. sys_attn_sm100_kernel); s is
-the system-prompt length of the bench workload the capture came from.
+kernel_key names the kernel in the summary (e.g. sys_attn_sm100_kernel), or
+"auto" to key every kernel of the report by its own name; s is the
+system-prompt length of the bench workload the capture came from.
 """
 
 import csv
@@ -63,7 +64,11 @@ def main():
             rec["dram_bytes"] = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
             rec["report"] = os.path.basename(rep)
             rec["tag"] = tag
-            data["kernels"].setdefault(key, {})[str(s)] = rec
+            k = key
+            if key == "auto":
+                name = rec["kernel"].split("(")[0].split("<")[0].strip()
+                k = name.split()[-1].split("::")[-1]
+            data["kernels"].setdefault(k, {})[str(s)] = rec
             print(json.dumps(rec, indent=1))
     json.dump(data, open(path, "w"), indent=1, sort_keys=True)
 
