@@ -17,6 +17,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librelay_b200.so")
+# diagnostics: RB_VARIANT="name:-DFOO=1 -DBAR=2" builds librelay_b200_<name>.so
+# with extra defines (select it at run time with RB_LIB=<path>)
+_VARIANT = os.environ.get("RB_VARIANT", "")
 SOURCES = ["sys_attn_sm100.cu", "ctx_attn.cu", "capi.cu"]
 HEADERS = ["rb_common.cuh", "rb_plan.h", "rb_args.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -36,25 +39,32 @@ def _stale():
 
 
 def build(force=False, verbose=False):
+    if _VARIANT:
+        name, defs = _VARIANT.split(":", 1)
+        return _build_to(os.path.join(PKG, f"librelay_b200_{name}.so"), defs.split(),
+                         os.path.join(PKG, "build", name), verbose)
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    return _build_to(LIB, [], os.path.join(PKG, "build"), verbose)
+
+
+def _build_to(lib, defs, objdir, verbose):
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or res.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}")
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -27,7 +27,8 @@ cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, cons
                                     cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
 cudaError_t launch_relay_fuse(const rb_sys_plan&, int, int, const float*, const float*, int*,
-                              const float*, void*, int, float*, int*, cudaStream_t);
+                              const float*, void*, int, float*, int*, unsigned long long*,
+                              cudaStream_t);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
                                 float*, long long, int, cudaStream_t);
 cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
@@ -42,6 +43,8 @@ static thread_local std::string g_err;
 static unsigned long long* g_debug_ts = nullptr;  // test-only instrumentation
 // context-kernel stamps start after 1024 system CTAs x 8 slots
 static constexpr long long kCtxTsOffset = 1024 * 8;
+// relay fuse kernel stamps: [CTA][4] after 7424 rows of 8
+static constexpr long long kFuseTsOffset = 7424 * 8;
 namespace rb {
 int g_knobs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 }
@@ -367,7 +370,8 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   st = cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
   if (st != RB_OK) return st;
   return cuda_status(rb::launch_relay_fuse(sa.plan, n_rows, hq, sa.part_acc, sa.part_ml, sa.counters,
-                                           ctx_part, out, out_fp32, lse_out, header + 2, cs),
+                                           ctx_part, out, out_fp32, lse_out, header + 2,
+                                           g_debug_ts ? g_debug_ts + kFuseTsOffset : nullptr, cs),
                      "relay fuse launch");
 }
 

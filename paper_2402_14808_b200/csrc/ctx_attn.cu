@@ -26,6 +26,8 @@
 // engine manages ~19 GB/s per SM, profiles/microbench_scatter.cu) and run
 // QK^T / PV on the tensor cores with mma.sync (16 query rows x 16 keys per
 // chunk); a merger warp combines the 4 partial states and writes the result.
+#include <type_traits>
+
 #include "rb_common.cuh"
 #include "rb_args.cuh"
 
@@ -200,6 +202,219 @@ __device__ __forceinline__ void chunk_mma(MmaRowState& st, const uint32_t (&qa)[
     }
   }
 }
+
+template <int R>
+struct RowState {
+  float m[R], l[R], acc[R][8];
+};
+
+// CUDA-core update of one 16-key chunk for a half-warp (R <= 2 query rows,
+// where 16-row MMA tiles would be mostly padding): keys key0 + 2p + hw,
+// p = 0..7, K/V rows already in registers; dot products reduce with 4
+// xor-shuffles, online softmax in the log2 domain.  `lim[i]` is the exclusive key bound of row i inside
+// this segment; keys at or past it contribute nothing (their V rows may hold
+// stale data and are zeroed, never multiplied).
+template <int R>
+__device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[R][8],
+                                             const uint4 (&kr)[8], uint4 (&vr)[8],
+                                             int key0, int hw, const int (&lim)[R], float scale_log2,
+                                             int max_lim) {
+  float x[R][8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    float kf[8];
+    kf[0] = bf16_lo(kr[p].x); kf[1] = bf16_hi(kr[p].x);
+    kf[2] = bf16_lo(kr[p].y); kf[3] = bf16_hi(kr[p].y);
+    kf[4] = bf16_lo(kr[p].z); kf[5] = bf16_hi(kr[p].z);
+    kf[6] = bf16_lo(kr[p].w); kf[7] = bf16_hi(kr[p].w);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      float s = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s = fmaf(qf[i][e], kf[e], s);
+      x[i][p] = s;
+    }
+    if (key0 + 2 * p + hw >= max_lim) vr[p] = make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      float s = x[i][p];
+      s += __shfl_xor_sync(0xffffffffu, s, 8);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      const int key = key0 + 2 * p + hw;
+      x[i][p] = key < lim[i] ? s * scale_log2 : -INFINITY;
+    }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    float cm = x[i][0];
+#pragma unroll
+    for (int p = 1; p < 8; ++p) cm = fmaxf(cm, x[i][p]);
+    if (cm == -INFINITY) continue;  // no valid key of this row in this chunk half
+    const float mn = fmaxf(st.m[i], cm);
+    const float al = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - mn);
+    st.m[i] = mn;
+    float ps = 0.f;
+    float a[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = st.acc[i][e] * al;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const float pr = fast_exp2(x[i][p] - mn);
+      ps += pr;
+      a[0] = fmaf(pr, bf16_lo(vr[p].x), a[0]); a[1] = fmaf(pr, bf16_hi(vr[p].x), a[1]);
+      a[2] = fmaf(pr, bf16_lo(vr[p].y), a[2]); a[3] = fmaf(pr, bf16_hi(vr[p].y), a[3]);
+      a[4] = fmaf(pr, bf16_lo(vr[p].z), a[4]); a[5] = fmaf(pr, bf16_hi(vr[p].z), a[5]);
+      a[6] = fmaf(pr, bf16_lo(vr[p].w), a[6]); a[7] = fmaf(pr, bf16_hi(vr[p].w), a[7]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) st.acc[i][e] = a[e];
+    st.l[i] = st.l[i] * al + ps;
+  }
+}
+
+
+// Per-worker compute policies of ctx_cta_kernel: same interface, chosen by
+// the rows per item.  R <= 2 (decode): CUDA cores, a half-warp per key pair
+// (no padded MMA rows).  R >= 4: mma.sync tiles of 16 query rows.
+template <int R>
+struct SimtCompute {
+  float qf[R][8];
+  int lim_ctx[R], lim_pre[R];
+  RowState<R> st;
+
+  __device__ __forceinline__ void load(const uint8_t* qrows, const uint8_t* /*qzero*/,
+                                       const CtxItem<R>& it, int item, const CtxArgs& a, int lane) {
+    const int l16 = lane & 15, rbase = it.z * R;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int li = rbase + i;
+      const bool ok = item >= 0 && it.n_chunks > 0 && li < it.nrows;
+      if (ok) {
+        const uint4 u = *reinterpret_cast<const uint4*>(qrows + i * kRowBytes + l16 * 16);
+        qf[i][0] = bf16_lo(u.x); qf[i][1] = bf16_hi(u.x);
+        qf[i][2] = bf16_lo(u.y); qf[i][3] = bf16_hi(u.y);
+        qf[i][4] = bf16_lo(u.z); qf[i][5] = bf16_hi(u.z);
+        qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
+      }
+      lim_ctx[i] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
+      lim_pre[i] = ok ? a.s_prefix : 0;
+    }
+  }
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      st.m[i] = -INFINITY;
+      st.l[i] = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
+    }
+  }
+  __device__ __forceinline__ void chunk(const uint8_t* slot, int key0, bool pre, int max_lim,
+                                        bool /*mask*/, const CtxArgs& a, int lane) {
+    const int hw = lane >> 4, l16 = lane & 15;
+    uint4 kr[8], vr[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const uint32_t off = slot_off(2 * p + hw, l16);
+      kr[p] = *reinterpret_cast<const uint4*>(slot + off);
+      vr[p] = *reinterpret_cast<const uint4*>(slot + kChunk * kRowBytes + off);
+    }
+    chunk_update<R>(st, qf, kr, vr, key0, hw, pre ? lim_pre : lim_ctx, a.scale_log2,
+                    pre ? a.s_prefix : max_lim);
+  }
+  // fold the two half-warp states, then half-warp 0 writes rows < R
+  __device__ __forceinline__ void handoff(float* macc, float* mml, int lane) {
+    const int hw = lane >> 4, l16 = lane & 15;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const float mo = __shfl_xor_sync(0xffffffffu, st.m[i], 16);
+      const float lo = __shfl_xor_sync(0xffffffffu, st.l[i], 16);
+      const float M = fmaxf(st.m[i], mo);
+      const float ws = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - M);
+      const float wo = (mo == -INFINITY) ? 0.f : fast_exp2(mo - M);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float ao = __shfl_xor_sync(0xffffffffu, st.acc[i][e], 16);
+        st.acc[i][e] = st.acc[i][e] * ws + ao * wo;
+      }
+      const float L = st.l[i] * ws + lo * wo;
+      if (hw == 0) {
+        *reinterpret_cast<float4*>(macc + i * 128 + l16 * 8) =
+            make_float4(st.acc[i][0], st.acc[i][1], st.acc[i][2], st.acc[i][3]);
+        *reinterpret_cast<float4*>(macc + i * 128 + l16 * 8 + 4) =
+            make_float4(st.acc[i][4], st.acc[i][5], st.acc[i][6], st.acc[i][7]);
+        if (l16 == 0) {
+          mml[i * 2] = M;
+          mml[i * 2 + 1] = L;
+        }
+      }
+    }
+  }
+};
+
+template <int R>
+struct MmaCompute {
+  uint32_t qa[8][4];
+  int lim_ctx[2], lim_pre[2];
+  MmaRowState st;
+
+  __device__ __forceinline__ void load(const uint8_t* qrows, const uint8_t* qzero,
+                                       const CtxItem<R>& it, int item, const CtxArgs& a, int lane) {
+    // Q rows as MMA A fragments (rows past R read the zero row)
+    const int qrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+    const uint32_t qaddr = qrow < R ? smem_u32(qrows + qrow * kRowBytes) : smem_u32(qzero);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) ldsm_x4(qa[ks], qaddr + ((ks * 2 + (lane >> 4)) << 4));
+    const int g8 = lane >> 2, rbase = it.z * R;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rr = g8 + 8 * hr, li = rbase + rr;
+      const bool ok = item >= 0 && it.n_chunks > 0 && rr < R && li < it.nrows;
+      lim_ctx[hr] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
+      lim_pre[hr] = ok ? a.s_prefix : 0;
+    }
+  }
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) st.o[nt][e] = 0.f;
+    st.m[0] = st.m[1] = -INFINITY;
+    st.l[0] = st.l[1] = 0.f;
+  }
+  __device__ __forceinline__ void chunk(const uint8_t* slot, int key0, bool pre, int /*max_lim*/,
+                                        bool mask, const CtxArgs& a, int lane) {
+    chunk_mma(st, qa, smem_u32(slot), lane, key0, pre ? lim_pre[0] : lim_ctx[0],
+              pre ? lim_pre[1] : lim_ctx[1], a.scale_log2, mask);
+  }
+  __device__ __forceinline__ void handoff(float* macc, float* mml, int lane) {
+    const int g8 = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rr = g8 + 8 * hr;
+      if (rr < R) {
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+          *reinterpret_cast<float2*>(macc + rr * 128 + nt * 8 + 2 * tq) =
+              make_float2(st.o[nt][2 * hr], st.o[nt][2 * hr + 1]);
+        if (tq == 0) {
+          mml[rr * 2] = st.m[hr];
+          mml[rr * 2 + 1] = st.l[hr];
+        }
+      }
+    }
+  }
+};
+
+template <int R>
+using CtxCompute = typename std::conditional<(R <= 2), SimtCompute<R>, MmaCompute<R>>::type;
 
 constexpr int kWorkers = 4;
 constexpr int kDepth = 3;                      // chunks in flight per worker
@@ -582,30 +797,13 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     const int item = iq[qs].item;
     const CtxItem<R> it = iq[qs].it;
     const int rbase = it.z * R;
-    // Q rows as MMA A fragments (rows past R read the zero row)
-    uint32_t qa[8][4];
-    {
-      const int qrow = (lane & 7) + ((lane >> 3) & 1) * 8;
-      const uint32_t qaddr = qrow < R ? smem_u32(smem + SM::kOffQ + (qs * R + qrow) * kRowBytes)
-                                      : smem_u32(smem + SM::kOffQZero);
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) ldsm_x4(qa[ks], qaddr + ((ks * 2 + (lane >> 4)) << 4));
-    }
-    const int g8 = lane >> 2, tq = lane & 3;
-    int lim_ctx[2], lim_pre[2];
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int rr = g8 + 8 * hr, li = rbase + rr;
-      const bool ok = item >= 0 && it.n_chunks > 0 && rr < R && li < it.nrows;
-      lim_ctx[hr] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
-      lim_pre[hr] = ok ? a.s_prefix : 0;
-    }
+    CtxCompute<R> cmp;
+    cmp.load(smem + SM::kOffQ + qs * R * kRowBytes, smem + SM::kOffQZero, it, item, a, lane);
     // chunks below every valid row's bound need no mask: the smallest bound
     // over the item's rows is that of its first row
     const int ctx_nomask = a.causal ? it.c_r - it.m_r + rbase / a.g + 1 : it.c_r;
     const int mb = mi % kNB;
     const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
-    MmaRowState st;
     // One loop, one issue site (instruction-cache footprint): the first pass
     // lets the issue cursor read this item's slot before it is released.
     int k = w;
@@ -619,12 +817,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
           qph ^= 1;
         }
         if (item < 0 || it.n_chunks == 0) break;
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) st.o[nt][e] = 0.f;
-        st.m[0] = st.m[1] = -INFINITY;
-        st.l[0] = st.l[1] = 0.f;
+        cmp.init();
       }
       if (k >= it.n_chunks) break;
       // chunk `consumed` is this warp's commit group number `consumed`; the
@@ -637,12 +830,10 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       else
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();  // every lane's copies of the chunk are visible to the warp
-      const uint32_t src = ring + con_sl * kSlotBytes;
       const bool pre = k < n_pre;
       const int key0 = (pre ? k : k - n_pre) * kChunk;
       const bool mask = key0 + kChunk > (pre ? a.s_prefix : ctx_nomask);
-      chunk_mma(st, qa, src, lane, key0, pre ? lim_pre[0] : lim_ctx[0], pre ? lim_pre[1] : lim_ctx[1],
-                a.scale_log2, mask);
+      cmp.chunk(ring_p + con_sl * kSlotBytes, key0, pre, it.max_lim, mask, a, lane);
       __syncwarp();  // every lane's reads precede the refill of this slot
       ++consumed;
       con_sl = (con_sl + 1 == kDepth) ? 0 : con_sl + 1;
@@ -656,20 +847,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     mbar_wait(&m_empty[mb], mph ^ 1);
     float* macc = s_acc + (mb * kWorkers + w) * R * 128;
     float* mml = s_ml + (mb * kWorkers + w) * R * 2;
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int rr = g8 + 8 * hr;
-      if (rr < R) {
-#pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(macc + rr * 128 + nt * 8 + 2 * tq) =
-              make_float2(st.o[nt][2 * hr], st.o[nt][2 * hr + 1]);
-        if (tq == 0) {
-          mml[rr * 2] = st.m[hr];
-          mml[rr * 2 + 1] = st.l[hr];
-        }
-      }
-    }
+    cmp.handoff(macc, mml, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&m_full[mb]);
     ++mi;
@@ -729,8 +907,11 @@ constexpr int kFuseWarps = 8;
 __global__ void __launch_bounds__(kFuseWarps * 32)
     relay_fuse_kernel(const rb_sys_plan SP, int n_rows, int hq, const float* __restrict__ part_acc,
                       const float* __restrict__ part_ml, int* ready, const float* ctx_part,
-                      void* out, int out_fp32, float* lse_out, int* exit_ctr) {
+                      void* out, int out_fp32, float* lse_out, int* exit_ctr,
+                      unsigned long long* dts) {
+  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4] = global_timer_ns();
   pdl_wait_primary();  // context partials of the previous grid
+  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4 + 1] = global_timer_ns();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long pair = static_cast<long long>(blockIdx.x) * kFuseWarps + warp;
   if (pair < static_cast<long long>(n_rows) * hq) {
@@ -785,6 +966,7 @@ __global__ void __launch_bounds__(kFuseWarps * 32)
     }
     if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
   }
+  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4 + 2] = global_timer_ns();
   // the last CTA rearms the unit counters (every reader of them is done)
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -799,17 +981,19 @@ __global__ void __launch_bounds__(kFuseWarps * 32)
 
 cudaError_t launch_relay_fuse(const rb_sys_plan& SP, int n_rows, int hq, const float* part_acc,
                               const float* part_ml, int* ready, const float* ctx_part, void* out,
-                              int out_fp32, float* lse_out, int* exit_ctr, cudaStream_t stream) {
+                              int out_fp32, float* lse_out, int* exit_ctr,
+                              unsigned long long* dts, cudaStream_t stream) {
   const long long pairs = static_cast<long long>(n_rows) * hq;
   if (pairs == 0) return cudaSuccess;
   const int grid = static_cast<int>((pairs + kFuseWarps - 1) / kFuseWarps);
   cudaError_t e = cudaSuccess;
   if (g_knobs[2] == 1)
     relay_fuse_kernel<<<grid, kFuseWarps * 32, 0, stream>>>(SP, n_rows, hq, part_acc, part_ml, ready,
-                                                            ctx_part, out, out_fp32, lse_out, exit_ctr);
+                                                            ctx_part, out, out_fp32, lse_out, exit_ctr,
+                                                            dts);
   else
     e = launch_pdl(relay_fuse_kernel, dim3(grid), dim3(kFuseWarps * 32), 0, stream, SP, n_rows, hq,
-                   part_acc, part_ml, ready, ctx_part, out, out_fp32, lse_out, exit_ctr);
+                   part_acc, part_ml, ready, ctx_part, out, out_fp32, lse_out, exit_ctr, dts);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -92,6 +92,12 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
   const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
   int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
+  // latency floor: with few key tiles per CTA the system kernel is bound by
+  // its per-CTA pipeline (prologue + ~1.5 us per tile), not by bytes; the
+  // measured optimum at s <= 2k keeps ~27% of the SMs on it
+  const int floor_g = sms * 27 / 100;
+  if (g < floor_g) g = floor_g;
+  if ((long long)g > p.total) g = (int)p.total;
   if (g < 1) g = 1;
   if (g > sms) g = sms;
   return g;

@@ -39,6 +39,9 @@
 namespace rb {
 
 
+#ifndef RB_SYS_KS
+#define RB_SYS_KS 2
+#endif
 constexpr int kKvTileBytes = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB
 // lazy max: the running max of a query column moves only when a score
 // exceeds it by more than kTau (log2 units), so p <= 2^kTau stays exact in
@@ -58,8 +61,8 @@ struct SysCfg {
   static constexpr int kRoleWarps = 4;                  // K producer, QK issuer, V producer, PV issuer
   static constexpr int kThreads = (kRoleWarps + NCW) * 32;
 
-  static constexpr int KS = 2;                          // K ring (freed after Q.K^T)
-  static constexpr int VS = 4;                          // V ring (freed after P.V)
+  static constexpr int KS = RB_SYS_KS;                 // K ring (freed after Q.K^T)
+  static constexpr int VS = 6 - RB_SYS_KS;             // V ring (freed after P.V)
   static constexpr int kTileBytes = kKvTileBytes;       // 32 KB per K or V tile
   static constexpr int kQBytes = NQ * 256;              // [2 kblocks][NQ][128 B]
   static constexpr int kOffK = 0;

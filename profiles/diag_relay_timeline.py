@@ -124,7 +124,12 @@ def run(s, phases=3, b=32, h=52, c=128):
                 iss = [us(v) for v in ch[ok, c, 0].tolist()]
                 lan = [us(v) for v in ch[ok, c, 1].tolist()]
                 print(f"  w0 chunk {c}: issued {statistics.median(iss):.1f} consumed {statistics.median(lan):.1f}")
-        mg = t[7424:].reshape(-1, 16)[:len(ctx_t)].reshape(-1, 8, 2)
+        fz = t[7424:].reshape(-1, 4)
+        fz = fz[fz[:, 0] != 0]
+        if len(fz):
+            for i, n in enumerate(["entry", "after pdl wait", "done"]):
+                print(f"  fuse {n:14s} {q([us(v) for v in fz[:, i].tolist()])}")
+        mg = t[7424:].reshape(-1, 16)[:len(ctx_t)].reshape(-1, 8, 2) * 0
         print(f"  merge stamps: {int((mg != 0).sum())}")
         for c in range(6):
             ok = (mg[:, c, 0] != 0) & (mg[:, c, 1] != 0)
