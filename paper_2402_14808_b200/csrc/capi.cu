@@ -26,9 +26,6 @@ namespace rb {
 cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
                                     cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
-cudaError_t launch_relay_fuse(const rb_sys_plan&, int, int, const float*, const float*, int*,
-                              const float*, void*, int, float*, int*, unsigned long long*,
-                              cudaStream_t);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
                                 float*, long long, int, cudaStream_t);
 cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
@@ -43,8 +40,6 @@ static thread_local std::string g_err;
 static unsigned long long* g_debug_ts = nullptr;  // test-only instrumentation
 // context-kernel stamps start after 1024 system CTAs x 8 slots
 static constexpr long long kCtxTsOffset = 1024 * 8;
-// relay fuse kernel stamps: [CTA][4] after 7424 rows of 8
-static constexpr long long kFuseTsOffset = 7424 * 8;
 namespace rb {
 int g_knobs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 }
@@ -235,6 +230,8 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.p_stride_head = p_stride_head;
   a.s_prefix = s_prefix;
   a.ctx_part = nullptr;
+  a.sys_part_acc = a.sys_part_ml = nullptr;
+  a.sys_ready = nullptr;
   a.o_sys = o_sys;
   a.lse_sys = lse_sys;
   a.out = out;
@@ -353,6 +350,10 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.p_stride_tok = a.p_stride_head = 0;
   a.s_prefix = 0;
   a.ctx_part = ctx_part;
+  a.sys_part_acc = sa.part_acc;
+  a.sys_part_ml = sa.part_ml;
+  a.sys_ready = sa.counters;
+  a.sys_plan = sa.plan;
   a.o_sys = nullptr;
   a.lse_sys = nullptr;
   a.out = out;
@@ -367,12 +368,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
     cudaError_t me = cudaMemsetAsync(sa.counters, 0x3f, (size_t)sa.plan.n_units * sizeof(int), cs);
     if (me != cudaSuccess) return cuda_status(me, "relay counters");
   }
-  st = cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
-  if (st != RB_OK) return st;
-  return cuda_status(rb::launch_relay_fuse(sa.plan, n_rows, hq, sa.part_acc, sa.part_ml, sa.counters,
-                                           ctx_part, out, out_fp32, lse_out, header + 2,
-                                           g_debug_ts ? g_debug_ts + kFuseTsOffset : nullptr, cs),
-                     "relay fuse launch");
+  return cuda_status(rb::launch_context_attention(a, max_rows, cs), "context attention launch");
 }
 
 int rb_relay_fusion(const float* o_sys, const float* lse_sys, const float* o_ctx,

@@ -7,10 +7,11 @@
 //    query row t of request r attends context keys 0 .. c_r - m_r + t;
 //    optionally fused with a given system partial (o_sys, lse_sys):
 //    `relay_fusion` (attention.py:137-157) in the epilogue.
-//  * relay partials     -- inside rb_relay_attention: the unnormalised
-//    context state (O, m, l) of every (row, head) goes to the workspace and
-//    relay_fuse_kernel merges it with the system kernel's stream-K parts;
-//    the system and context kernels run concurrently on disjoint SMs.
+//  * relay              -- inside rb_relay_attention, concurrently with the
+//    system kernel on other SMs: each (row, head) state is merged with the
+//    system kernel's stream-K parts of its unit (`relay_fusion`,
+//    attention.py:137-157) as soon as the unit is published; rows whose
+//    unit is not yet complete are fused at the end of the CTA.
 //  * naive baseline     -- a shared prefix segment (the system K/V, shared in
 //    storage) read again by every request before its context: the
 //    per-request `baseline_attention` (attention.py:266-296), i.e. the
@@ -416,6 +417,78 @@ struct MmaCompute {
 template <int R>
 using CtxCompute = typename std::conditional<(R <= 2), SimtCompute<R>, MmaCompute<R>>::type;
 
+// Relay fusion of one (row, head) pair (`relay_fusion`, attention.py:137-157):
+// the context state (O unnormalised, m log2, l) merged with every stream-K
+// part of the pair's system unit in slot order (deterministic), normalised
+// and written.  One warp, lane = 4 head dims.  The unit must be published.
+__device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, long long pair,
+                                                const float* part_acc, const float* part_ml,
+                                                float4 O, float mt, float lt, void* out, int out_fp32,
+                                                float* lse_out, int lane) {
+  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
+  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
+  const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
+  const int u = (hh / SP.g) * SP.n_qt + qt;
+  const int np = rb_unit_parts(&SP, u);
+  const int d0 = lane * 4;
+  const long long base = static_cast<long long>(u) * SP.max_parts;
+  for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
+    float mk[4], lk[4];
+    float4 ak[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = min(k0 + kk, np - 1);
+      const float* pml = part_ml + (base + k) * 2 * SP.nq;
+      mk[kk] = __ldcg(pml + col);
+      lk[kk] = __ldcg(pml + SP.nq + col);
+      ak[kk] = __ldcg(reinterpret_cast<const float4*>(part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0));
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      if (k0 + kk >= np) break;
+      const float mn = fmaxf(mt, mk[kk]);
+      const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+      const float sk = fast_exp2(mk[kk] - mn);
+      lt = lt * so + lk[kk] * sk;
+      O.x = O.x * so + ak[kk].x * sk;
+      O.y = O.y * so + ak[kk].y * sk;
+      O.z = O.z * so + ak[kk].z * sk;
+      O.w = O.w * so + ak[kk].w * sk;
+      mt = mn;
+    }
+  }
+  const float inv = 1.f / lt;
+  if (out_fp32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + pair * 128 + d0) =
+        make_float4(O.x * inv, O.y * inv, O.z * inv, O.w * inv);
+  } else {
+    uint2 pk;
+    pk.x = pack_bf16x2(O.x * inv, O.y * inv);
+    pk.y = pack_bf16x2(O.z * inv, O.w * inv);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + d0) = pk;
+  }
+  if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
+}
+
+// Is the system unit of `pair` published (all its parts written)?  Lane 0
+// probes with acquire semantics; the answer is broadcast to the warp.
+__device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, long long pair,
+                                                 const int* ready, int lane, bool block) {
+  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
+  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
+  const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+  const int np = rb_unit_parts(&SP, u);
+  int ok = 1;
+  if (lane == 0) {
+    ok = ld_acquire_gpu(ready + u) >= np;
+    while (!ok && block) {
+      __nanosleep(128);
+      ok = ld_acquire_gpu(ready + u) >= np;
+    }
+  }
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 constexpr int kWorkers = 4;
 constexpr int kDepth = 3;                      // chunks in flight per worker
 static_assert(kDepth == 3, "wait_group ladder in ctx_cta_kernel assumes 3");
@@ -424,6 +497,7 @@ constexpr int kNB = 3;                         // merge buffers
 constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
+constexpr int kMaxDefer = 62;                  // relay rows per CTA awaiting their system unit
 
 template <int R>
 struct ItemSlot {
@@ -443,7 +517,8 @@ struct CtaSmem {
   static constexpr int kOffItems =
       (kOffMIt + kNB * static_cast<int>(sizeof(CtxItem<R>)) + 15) & ~15;  // [kIQ] ItemSlot
   static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
-  static constexpr int kBytes = kOffBar + (3 * kIQ + 2 * kNB) * 8;
+  static constexpr int kOffDefer = kOffBar + (3 * kIQ + 2 * kNB) * 8;  // [1 + kMaxDefer] int
+  static constexpr int kBytes = kOffDefer + (1 + kMaxDefer) * 4;
 };
 
 template <int R>
@@ -463,6 +538,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   uint64_t* m_empty = m_full + kNB;
 
   if (threadIdx.x == 0) {
+    reinterpret_cast<int*>(smem + SM::kOffDefer)[0] = 0;
     for (int i = 0; i < kIQ; ++i) {
       mbar_init(&i_meta[i], 1);
       mbar_init(&i_full[i], 1);
@@ -658,10 +734,22 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
           }
         }
         if (a.ctx_part != nullptr) {
-          // relay: unnormalised partial for relay_fuse_kernel
-          float* dst = a.ctx_part + oidx * kPartStride;
-          __stcg(reinterpret_cast<float4*>(dst + d0), make_float4(O[0], O[1], O[2], O[3]));
-          if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
+          // relay: fuse now if the pair's system unit is published, else
+          // park the unnormalised partial and fuse it at the end of the CTA
+          int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
+          const bool full = defer[0] >= kMaxDefer;
+          if (relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
+            relay_fuse_pair(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml,
+                            make_float4(O[0], O[1], O[2], O[3]), M, Ls, a.out, a.out_fp32,
+                            a.lse_out, lane);
+          } else {
+            float* dst = a.ctx_part + oidx * kPartStride;
+            __stcg(reinterpret_cast<float4*>(dst + d0), make_float4(O[0], O[1], O[2], O[3]));
+            if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
+            __syncwarp();
+            if (lane == 0) defer[1 + defer[0]++] = static_cast<int>(oidx);
+            __syncwarp();
+          }
           continue;
         }
         float o[4];
@@ -700,9 +788,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       if (lane == 0) mbar_arrive(&m_empty[mb]);
     }
     if (dts && lane == 0) dts[6] = global_timer_ns();
-    return;
-  }
-
+  } else {
   // ---------------------------------------------------------------- workers
   const int w = warp - 1;                       // 0 .. kWorkers-1
   const uint32_t ring = smem_u32(smem + w * kDepth * kSlotBytes);
@@ -854,6 +940,37 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (dts && lane == 0 && w == 0) dts[7] = global_timer_ns();
+  }  // workers
+
+  // ------------------------------------------------ relay: deferred fusion
+  // Rows whose system unit was not yet published when they were merged:
+  // workers and merger share them once the CTA's items are done (each
+  // waits for its row's unit), then the last CTA to finish rearms the
+  // system-unit counters for the next step.
+  if (a.ctx_part != nullptr) {
+    named_bar_sync(1, 32 * (kWorkers + 1));
+    const int* defer = reinterpret_cast<const int*>(smem + SM::kOffDefer);
+    const int nd = defer[0];
+    for (int e = warp - 1; e < nd; e += kWorkers + 1) {
+      const long long pair = defer[1 + e];
+      relay_unit_ready(a.sys_plan, a.hq, pair, a.sys_ready, lane, true);
+      const float* cp = a.ctx_part + pair * kPartStride;
+      const float4 O = __ldcg(reinterpret_cast<const float4*>(cp + lane * 4));
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
+      relay_fuse_pair(a.sys_plan, a.hq, pair, a.sys_part_acc, a.sys_part_ml, O, ml.x, ml.y, a.out,
+                      a.out_fp32, a.lse_out, lane);
+    }
+    named_bar_sync(1, 32 * (kWorkers + 1));
+    if (dts && warp == kMergerWarp && lane == 0) dts[6] = global_timer_ns();  // CTA done
+    if (warp == kMergerWarp && lane == 0 && a.sched != nullptr) {
+      __threadfence();
+      if (atomicAdd(a.sched + 2, 1) == static_cast<int>(gridDim.x) - 1) {
+        for (int u = 0; u < a.sys_plan.n_units; ++u) a.sys_ready[u] = 0;
+        a.sched[2] = 0;
+        __threadfence();
+      }
+    }
+  }
 }
 
 template <int R>
@@ -892,110 +1009,6 @@ cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_
     case 4: return launch_ctx_r<4>(a, n_items, n_z, stream);
     default: return launch_ctx_r<8>(a, n_items, n_z, stream);
   }
-}
-
-// ------------------------------------------------------- relay fuse (step)
-// Final combine of the relay step: per (row, head), the context partial of
-// ctx_cta_kernel and every stream-K part of the system kernel's unit, in
-// ONE LSE-weighted merge (`relay_fusion`, attention.py:137-157; the parts
-// are merged in slot order, so the result is deterministic).  One warp per
-// (row, head), lane = 4 head dims.  Launched with PDL after the context
-// kernel: it waits for that grid, then for the system unit's publication
-// counter (the system kernel runs concurrently and may still be running);
-// the last CTA rearms the counters for the next step.
-constexpr int kFuseWarps = 8;
-__global__ void __launch_bounds__(kFuseWarps * 32)
-    relay_fuse_kernel(const rb_sys_plan SP, int n_rows, int hq, const float* __restrict__ part_acc,
-                      const float* __restrict__ part_ml, int* ready, const float* ctx_part,
-                      void* out, int out_fp32, float* lse_out, int* exit_ctr,
-                      unsigned long long* dts) {
-  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4] = global_timer_ns();
-  pdl_wait_primary();  // context partials of the previous grid
-  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4 + 1] = global_timer_ns();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long pair = static_cast<long long>(blockIdx.x) * kFuseWarps + warp;
-  if (pair < static_cast<long long>(n_rows) * hq) {
-    const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
-    const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-    const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
-    const int u = (hh / SP.g) * SP.n_qt + qt;
-    const int np = rb_unit_parts(&SP, u);
-    if (lane == 0)
-      while (ld_acquire_gpu(ready + u) < np) __nanosleep(256);
-    __syncwarp();
-    const int d0 = lane * 4;
-    const float* cp = ctx_part + pair * kPartStride;
-    float4 O = __ldcg(reinterpret_cast<const float4*>(cp + d0));
-    const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
-    float mt = ml.x, lt = ml.y;
-    const long long base = static_cast<long long>(u) * SP.max_parts;
-    for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
-      float mk[4], lk[4];
-      float4 ak[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = min(k0 + kk, np - 1);
-        const float* pml = part_ml + (base + k) * 2 * SP.nq;
-        mk[kk] = __ldcg(pml + col);
-        lk[kk] = __ldcg(pml + SP.nq + col);
-        ak[kk] = __ldcg(reinterpret_cast<const float4*>(part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0));
-      }
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        if (k0 + kk >= np) break;
-        const float mn = fmaxf(mt, mk[kk]);
-        const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
-        const float sk = fast_exp2(mk[kk] - mn);
-        lt = lt * so + lk[kk] * sk;
-        O.x = O.x * so + ak[kk].x * sk;
-        O.y = O.y * so + ak[kk].y * sk;
-        O.z = O.z * so + ak[kk].z * sk;
-        O.w = O.w * so + ak[kk].w * sk;
-        mt = mn;
-      }
-    }
-    const float inv = 1.f / lt;
-    if (out_fp32) {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + pair * 128 + d0) =
-          make_float4(O.x * inv, O.y * inv, O.z * inv, O.w * inv);
-    } else {
-      uint2 pk;
-      pk.x = pack_bf16x2(O.x * inv, O.y * inv);
-      pk.y = pack_bf16x2(O.z * inv, O.w * inv);
-      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + d0) = pk;
-    }
-    if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
-  }
-  if (dts && threadIdx.x == 0) dts[blockIdx.x * 4 + 2] = global_timer_ns();
-  // the last CTA rearms the unit counters (every reader of them is done)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(exit_ctr, 1) == static_cast<int>(gridDim.x) - 1) {
-      for (int u = 0; u < SP.n_units; ++u) ready[u] = 0;
-      *exit_ctr = 0;
-      __threadfence();
-    }
-  }
-}
-
-cudaError_t launch_relay_fuse(const rb_sys_plan& SP, int n_rows, int hq, const float* part_acc,
-                              const float* part_ml, int* ready, const float* ctx_part, void* out,
-                              int out_fp32, float* lse_out, int* exit_ctr,
-                              unsigned long long* dts, cudaStream_t stream) {
-  const long long pairs = static_cast<long long>(n_rows) * hq;
-  if (pairs == 0) return cudaSuccess;
-  const int grid = static_cast<int>((pairs + kFuseWarps - 1) / kFuseWarps);
-  cudaError_t e = cudaSuccess;
-  if (g_knobs[2] == 1)
-    relay_fuse_kernel<<<grid, kFuseWarps * 32, 0, stream>>>(SP, n_rows, hq, part_acc, part_ml, ready,
-                                                            ctx_part, out, out_fp32, lse_out, exit_ctr,
-                                                            dts);
-  else
-    e = launch_pdl(relay_fuse_kernel, dim3(grid), dim3(kFuseWarps * 32), 0, stream, SP, n_rows, hq,
-                   part_acc, part_ml, ready, ctx_part, out, out_fp32, lse_out, exit_ctr, dts);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------- relay fusion

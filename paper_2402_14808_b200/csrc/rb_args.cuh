@@ -46,10 +46,15 @@ struct CtxArgs {
   const __nv_bfloat16* pv;
   long long p_stride_tok, p_stride_head;
   int s_prefix;
-  // relay step: unnormalised context partial per (row, head) instead of the
-  // output, [n_rows * hq][132] floats (O[128], m log2, l); merged with the
-  // system kernel's stream-K parts by relay_fuse_kernel
+  // relay step: the system kernel's stream-K parts (published per unit on
+  // sys_ready) are fused here; rows whose unit is not yet published park an
+  // unnormalised context partial, [n_rows * hq][132] floats (O[128], m
+  // log2, l), and are fused at the end of the CTA
   float* ctx_part;
+  const float* sys_part_acc;     // [n_units][max_parts][nq][128]
+  const float* sys_part_ml;      // [n_units][max_parts][2][nq]
+  int* sys_ready;                // [n_units] parts published per unit
+  rb_sys_plan sys_plan;
   // optional system partial (relay)
   const float* o_sys;            // [n_rows][hq][128]
   const float* lse_sys;          // [n_rows][hq] natural log
@@ -59,7 +64,7 @@ struct CtxArgs {
   float* lse_out;                // [n_rows][hq] natural log (may be null)
   float scale_log2;
   unsigned long long* debug_ts;  // optional per-CTA stamps [grid][8] (diagnostics)
-  int* sched;                    // optional [2] zeroed counters: item claims, scheduler exits
+  int* sched;                    // optional [3] zeroed counters: item claims, scheduler / CTA exits
   int knob;                      // diagnostics: g_knobs[3] at launch
 };
 
