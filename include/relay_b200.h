@@ -53,8 +53,9 @@ int rb_device_sm_count(int device, int* out);
 
 /*
  * Work plan of rb_system_attention (stream-K split over kv head x query
- * tile x 128-key tile; paper_2402_14808_b200/csrc/rb_plan.h).  fields[7] =
- * {nq, n_qtiles, tiles_per_unit, n_units, total_tiles, grid, max_parts};
+ * tile x 128-key tile, or whole units dealt round-robin when a KV head has
+ * several query tiles; paper_2402_14808_b200/csrc/rb_plan.h).  fields[8] =
+ * {nq, n_qtiles, tiles_per_unit, n_units, total_tiles, grid, max_parts, rr};
  * *workspace_bytes = bytes rb_system_attention needs (zero-filled before the
  * first use; the kernel leaves its semaphores zeroed).
  */

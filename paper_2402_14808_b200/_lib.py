@@ -99,8 +99,8 @@ def sys_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
     ws = ctypes.c_size_t(0)
     check(load().rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, ctypes.byref(ws)),
           "rb_sys_plan_query")
-    keys = ("nq", "n_qt", "tpu", "n_units", "total", "grid", "max_parts")
-    return dict(zip(keys, list(f)[:7])), ws.value
+    keys = ("nq", "n_qt", "tpu", "n_units", "total", "grid", "max_parts", "rr")
+    return dict(zip(keys, list(f)[:8])), ws.value
 
 
 def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int) -> int:

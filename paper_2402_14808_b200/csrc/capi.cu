@@ -91,6 +91,7 @@ int rb_sys_plan_query(int n_rows, int hq, int hkv, int s, int grid_cap, long lon
     fields[4] = p.total;
     fields[5] = p.grid;
     fields[6] = p.max_parts;
+    fields[7] = p.rr;
   }
   if (workspace_bytes) {
     size_t cnt = ((size_t)p.n_units * sizeof(int) + 255) & ~(size_t)255;

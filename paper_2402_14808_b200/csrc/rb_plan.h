@@ -36,19 +36,42 @@ typedef struct {
   long long total;    // n_units * tpu
   int grid;           // CTAs launched
   int max_parts;      // max partial slots over all units
+  int rr;             // 1: whole units dealt round-robin (CTA c: units c, c+grid, ...)
 } rb_sys_plan;
 
 RB_HD long long rb_cta_begin(const rb_sys_plan* p, int c) {
   return (long long)c * p->total / p->grid;
 }
-// CTA owning global tile x.
+// CTA owning global tile x (stream-K mode).
 RB_HD int rb_tile_owner(const rb_sys_plan* p, long long x) {
   return (int)(((x + 1) * (long long)p->grid - 1) / p->total);
 }
 RB_HD int rb_unit_parts(const rb_sys_plan* p, int u) {
+  if (p->rr) return 1;
   long long first = (long long)u * p->tpu;
   long long last = first + p->tpu - 1;
   return rb_tile_owner(p, last) - rb_tile_owner(p, first) + 1;
+}
+// Tiles of CTA c, as a local index range [*b, *e): stream-K mode uses global
+// tile indices; round-robin mode numbers the CTA's own units' tiles from 0.
+// Both are unit-aligned: a unit starts wherever i % tpu == 0 (or at *b).
+RB_HD void rb_cta_range(const rb_sys_plan* p, int c, long long* b, long long* e) {
+  if (p->rr) {
+    const int mine = c < p->n_units ? (p->n_units - 1 - c) / p->grid + 1 : 0;
+    *b = 0;
+    *e = (long long)mine * p->tpu;
+  } else {
+    *b = rb_cta_begin(p, c);
+    *e = rb_cta_begin(p, c + 1);
+  }
+}
+// Unit of tile i of CTA c (i from rb_cta_range).
+RB_HD int rb_tile_unit(const rb_sys_plan* p, int c, long long i) {
+  return p->rr ? c + (int)(i / p->tpu) * p->grid : (int)(i / p->tpu);
+}
+// First CTA holding a part of unit u (its part slot is 0).
+RB_HD int rb_unit_owner0(const rb_sys_plan* p, int u) {
+  return p->rr ? u % p->grid : rb_tile_owner(p, (long long)u * p->tpu);
 }
 
 RB_HD int rb_pick_nq(int rows_per_head) { return rows_per_head <= 16 ? 16 : 32; }
@@ -69,7 +92,16 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
   p->n_units = hkv * p->n_qt;
   p->total = (long long)p->n_units * p->tpu;
   long long gcap = grid_cap < 1 ? 1 : grid_cap;
-  p->grid = (int)(p->total < gcap ? p->total : gcap);
+  // Several query tiles per KV head (large GQA batches) and enough units to
+  // occupy at least half the SMs: deal whole units round-robin, so the CTAs
+  // working on a head's query tiles at the same moment walk its key tiles in
+  // lockstep and every re-read of a tile comes from L2 instead of HBM.
+  // Otherwise stream-K over the flattened tiles.
+  p->rr = (p->n_qt >= 2 && 2LL * p->n_units >= gcap) ? 1 : 0;
+  if (p->rr)
+    p->grid = (int)(p->n_units < gcap ? p->n_units : gcap);
+  else
+    p->grid = (int)(p->total < gcap ? p->total : gcap);
   int mp = 1;
   for (int u = 0; u < p->n_units; ++u) {
     int c = rb_unit_parts(p, u);

@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   const rb_sys_plan& P = args.plan;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const long long t_begin = rb_cta_begin(&P, blockIdx.x);
-  const long long t_end = rb_cta_begin(&P, blockIdx.x + 1);
+  long long t_begin, t_end;
+  rb_cta_range(&P, blockIdx.x, &t_begin, &t_end);
 
   unsigned long long* dts = args.debug_ts ? args.debug_ts + blockIdx.x * 8 : nullptr;
   if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     const uint64_t pol = l2_policy_evict_first();
     int j = 0, uq = 0;
     for (long long i = t_begin; i < t_end; ++i, ++j) {
-      const int u = static_cast<int>(i / P.tpu);
+      const int u = rb_tile_unit(&P, blockIdx.x, i);
       const int kt = static_cast<int>(i % P.tpu);
       const int h = u / P.n_qt;
       const int qt = u % P.n_qt;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       }
       int j = 0;
       for (long long i = t_begin; i < t_end; ++i, ++j) {
-        const int u = static_cast<int>(i / P.tpu);
+        const int u = rb_tile_unit(&P, blockIdx.x, i);
         const int kt = static_cast<int>(i % P.tpu);
         const int h = u / P.n_qt;
         const int st = j % VS;
@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     pdl_wait_primary();  // o_sys / partials may still be read by the previous kernel
     long long i = t_begin;
     while (i < t_end) {
-      const int u = static_cast<int>(i / P.tpu);
-      const long long unit_end = min(t_end, static_cast<long long>(u + 1) * P.tpu);
+      const int u = rb_tile_unit(&P, blockIdx.x, i);
+      const long long unit_end = min(t_end, (i / P.tpu + 1) * P.tpu);  // local unit end
       const long long ia = i, ib = unit_end - 1;
 #pragma unroll
       for (int c = 0; c < H; ++c) {
@@ -501,8 +501,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         for (int c = 0; c < H; ++c) lrow[c] = lg[col0 + c];
         named_bar_sync(bar_grp, L::NCW * 32);  // lg reads done before the next unit's writes
         const int h = u / P.n_qt, qt = u % P.n_qt;
-        const long long u_first = static_cast<long long>(u) * P.tpu;
-        const int owner0 = rb_tile_owner(&P, u_first);
+        const int owner0 = rb_unit_owner0(&P, u);
         const int nparts = rb_unit_parts(&P, u);
         const int dcol = key_lane;  // O lane = head-dim index
         if (args.defer_merge) {

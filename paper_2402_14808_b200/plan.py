@@ -52,7 +52,16 @@ class SysPlan:
         return self.n_units * self.tpu
 
     @property
+    def rr(self):
+        """Whole units dealt round-robin (several query tiles per KV head and
+        enough units for half the SMs): CTAs on a head's query tiles walk its
+        key tiles in lockstep, so repeated tiles hit L2."""
+        return self.n_qt >= 2 and 2 * self.n_units >= max(1, self.grid_cap)
+
+    @property
     def grid(self):
+        if self.rr:
+            return max(1, min(self.n_units, self.grid_cap))
         return max(1, min(self.total, self.grid_cap))
 
     def cta_begin(self, c):
@@ -62,12 +71,18 @@ class SysPlan:
         return ((x + 1) * self.grid - 1) // self.total
 
     def unit_parts(self, u):
+        if self.rr:
+            return 1
         first = u * self.tpu
         return self.owner(first + self.tpu - 1) - self.owner(first) + 1
 
     @property
     def max_parts(self):
         return max(self.unit_parts(u) for u in range(self.n_units))
+
+    def cta_units(self, c):
+        """Round-robin mode: the units of CTA c, in processing order."""
+        return list(range(c, self.n_units, self.grid))
 
     def cta_ranges(self):
         return [(self.cta_begin(c), self.cta_begin(c + 1)) for c in range(self.grid)]

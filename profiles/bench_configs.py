@@ -18,6 +18,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
+from paper_2402_14808_b200 import kernels  # noqa: E402
 from paper_2402_14808_b200.attention import NaiveDecodeStep, RelayDecodeStep  # noqa: E402
 from paper_2402_14808_b200.costmodel import DecodeShape  # noqa: E402
 from paper_2402_14808_b200.kvcache import PagedKvCache, SystemKvCache  # noqa: E402
@@ -76,9 +77,12 @@ def main():
         cfg = CONFIGS[name]
         q, sys_cache, paged, bt, cl, lens = build(cfg, dev)
         relay = RelayDecodeStep(sys_cache, paged, bt, cl, cfg["hq"])
-        ms = statistics.mean(bench.time_loop(torch, lambda: relay(q), args.steps, args.warmup, flush))
-        sys_ms = statistics.mean(bench.time_loop(torch, lambda: relay.system(q), args.steps,
-                                                 args.warmup, flush))
+        gr = bench.graph_of(torch, lambda: relay(q))
+        ms = statistics.mean(bench.time_loop(torch, gr.replay, args.steps, args.warmup, flush))
+        # the system kernel alone on every SM (the step shares SMs with the context kernel)
+        alone = RelayDecodeStep(sys_cache, paged, bt, cl, cfg["hq"], grid=kernels.sm_count(dev))
+        gs = bench.graph_of(torch, lambda: alone.system(q))
+        sys_ms = statistics.mean(bench.time_loop(torch, gs.replay, args.steps, args.warmup, flush))
         shp = DecodeShape(cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], sum(lens))
         t_star = shp.roofline_s(hbm * 1e9, tc * 1e12)
         row = {"config": name, **cfg, "ctx_total": sum(lens), "us_per_step": ms * 1e3,
@@ -86,14 +90,14 @@ def main():
                "flops_sys": shp.flops_sys, "hbm_gbs": shp.bytes_alg / (ms * 1e-3) / 1e9,
                "roofline_us": t_star * 1e6, "frac_of_roofline": t_star / (ms * 1e-3),
                "bound": "tensor" if shp.flops_sys / (tc * 1e12) > shp.bytes_alg / (hbm * 1e9) else "hbm",
-               "plan": relay.plan}
+               "plan": relay.plan, "sys_alone_plan": alone.plan}
         if args.naive:
             naive = NaiveDecodeStep(sys_cache, paged, bt, cl, cfg["hq"])
             row["naive_us_per_step"] = statistics.mean(
                 bench.time_loop(torch, lambda: naive(q), max(3, args.steps // 4), 1, flush)) * 1e3
         print(json.dumps(row), flush=True)
         rows.append(row)
-        del q, sys_cache, paged, relay
+        del q, sys_cache, paged, relay, alone, gr, gs
         torch.cuda.empty_cache()
     out = os.path.join(ROOT, "gpurun_out", "bench_configs.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)

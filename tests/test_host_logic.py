@@ -15,12 +15,20 @@ from paper_2402_14808_b200.plan import SysPlan
     (32, 52, 52, 8192, 148), (32, 52, 52, 512, 148), (4, 32, 32, 512, 148),
     (64, 32, 32, 4096, 148), (128, 32, 8, 32768, 148), (256, 64, 8, 65536, 148),
     (32, 7, 7, 8192, 148), (1, 1, 1, 1, 148), (32, 4, 4, 1000, 5),
+    (64, 2, 2, 384, 3), (24, 8, 2, 300, 7),
 ])
 def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
     p = SysPlan(n_rows, hq, hkv, s, grid)
     f, _ = _lib.sys_plan(n_rows, hq, hkv, s, grid)
-    assert (p.nq, p.n_qt, p.tpu, p.n_units, p.total, p.grid, p.max_parts) == \
-        (f["nq"], f["n_qt"], f["tpu"], f["n_units"], f["total"], f["grid"], f["max_parts"])
+    assert (p.nq, p.n_qt, p.tpu, p.n_units, p.total, p.grid, p.max_parts, int(p.rr)) == \
+        (f["nq"], f["n_qt"], f["tpu"], f["n_units"], f["total"], f["grid"], f["max_parts"], f["rr"])
+    if p.rr:
+        # whole units dealt round-robin: every unit once, balanced to one unit
+        units = [p.cta_units(c) for c in range(p.grid)]
+        assert sorted(u for us in units for u in us) == list(range(p.n_units))
+        assert max(map(len, units)) - min(map(len, units)) <= 1
+        assert p.max_parts == 1
+        return
     ranges = p.cta_ranges()
     assert ranges[0][0] == 0 and ranges[-1][1] == p.total
     assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
