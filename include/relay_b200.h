@@ -128,6 +128,9 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * the kernels leave it zeroed (its header holds the context kernel's work
  * counters), so one buffer serves every step on a stream.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
+ * (2 | 4: the context kernel of a step whose system kernel was launched by an
+ * earlier phase-1 call, e.g. with stream work in between; the units are
+ * published by that system kernel as it runs)
  * (profiling: phase 2 consumes the slots a previous phase-1 call wrote).
  */
 int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes);

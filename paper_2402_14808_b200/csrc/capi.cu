@@ -363,9 +363,9 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = header;  // workspace header: dynamic item counters
-  if (!(phases & 1)) {
+  if (!(phases & 1) && !(phases & 4)) {
     // context phase alone (profiling): the slots of an earlier phase-1 call
-    // are complete; mark every unit published (the fuse kernel rearms them)
+    // are complete; mark every unit published (the kernel rearms them)
     cudaError_t me = cudaMemsetAsync(sa.counters, 0x3f, (size_t)sa.plan.n_units * sizeof(int), cs);
     if (me != cudaSuccess) return cuda_status(me, "relay counters");
   }
