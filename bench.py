@@ -481,8 +481,7 @@ def run_b200(args):
                      "kernel": "relay step: sys_attn_sm100_kernel || ctx_cta_kernel (concurrent) + relay_fuse_kernel",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "traffic": ncu_traffic(("sys_attn_sm100_kernel", "ctx_cta_kernel", "relay_fuse_kernel"),
-                                            args.s),
+                     "traffic": ncu_traffic(("sys_attn_sm100_kernel", "ctx_cta_kernel"), args.s),
                      "algorithmic_bytes_per_launch": step_bytes_local},
         "e2e": {"value": e2e_ms * 1e3, "unit": "µs/step", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],

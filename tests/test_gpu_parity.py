@@ -373,3 +373,39 @@ def test_fused_relay_equals_two_kernel_path(rb, oracle, grid):
     out3, _ = step(qd)
     torch.cuda.synchronize()
     assert torch.equal(out, out3)
+
+
+def test_concurrent_step_repeats_and_phases(rb):
+    """The concurrent relay step leaves its workspace rearmed: repeated steps,
+    a system-only call followed by the context kernel of the same step
+    (phases 1 then 2|4, and the profiling split 1 then 2) all reproduce the
+    one-call step bitwise; different SM splits agree to fp32 rounding."""
+    from paper_2402_14808_b200 import kernels
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    rng = np.random.default_rng(91)
+    b, hq, hkv, s = 16, 8, 4, 2000
+    lens = [int(x) for x in rng.integers(1, 300, size=b)]
+    q = bf16(rng.standard_normal((b, hq, 128)))
+    sk = bf16(rng.standard_normal((s, hkv, 128)))
+    sv = bf16(rng.standard_normal((s, hkv, 128)))
+    ck = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    cv = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    sys_cache = SystemKvCache.from_shd([sk], [sv])
+    paged, bt, cl = make_paged(rb, ck, cv, hkv)
+    qd = dev_bf16(q)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, out_dtype=torch.float32)
+    ref, ref_lse = [t.clone() for t in step(qd)]
+    for _ in range(4):
+        out, lse = step(qd)
+        assert torch.equal(out, ref) and torch.equal(lse, ref_lse)
+    for phases in (2 | 4, 2):
+        step._launch(qd, 1)
+        out, lse = step._launch(qd, phases)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref) and torch.equal(lse, ref_lse), f"phases 1 then {phases}"
+    for grid in (1, 7, kernels.sm_count(qd.device)):
+        other = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32)
+        out, lse = other(qd)
+        torch.cuda.synchronize()
+        assert (out - ref).abs().max().item() < 1e-5 and (lse - ref_lse).abs().max().item() < 1e-5

@@ -92,3 +92,18 @@ def test_block_pool_conservation():
                 pool.release(rid)
                 live.remove(rid)
         assert pool.used_blocks + pool.free_blocks == pool.num_blocks
+
+
+def test_relay_sm_split():
+    """rb_relay_sys_grid: within [1, sms], never below the latency floor, and
+    non-decreasing in the system length (more system bytes -> more SMs)."""
+    sms = 148
+    prev = 0
+    for s in (64, 512, 2048, 8192, 32768, 131072):
+        g = _lib.relay_sys_grid(32, 52, 52, s, 32 * 128, sms)
+        assert 1 <= g <= sms
+        assert g >= min(sms * 27 // 100, SysPlan(32, 52, 52, s, sms).total)
+        assert g >= prev
+        prev = g
+    # no context at all: the system kernel takes every SM
+    assert _lib.relay_sys_grid(32, 52, 52, 8192, 0, sms) == sms
