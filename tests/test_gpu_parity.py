@@ -379,7 +379,9 @@ def test_concurrent_step_repeats_and_phases(rb):
     """The concurrent relay step leaves its workspace rearmed: repeated steps,
     a system-only call followed by the context kernel of the same step
     (phases 1 then 2|4, and the profiling split 1 then 2) all reproduce the
-    one-call step bitwise; different SM splits agree to fp32 rounding."""
+    one-call step bitwise.  Other SM splits cut the stream-K units elsewhere,
+    which moves the lazy-max references and so the bf16 rounding of P: they
+    agree within the bf16 envelope."""
     from paper_2402_14808_b200 import kernels
     from paper_2402_14808_b200.attention import RelayDecodeStep
     from paper_2402_14808_b200.kvcache import SystemKvCache
@@ -408,4 +410,5 @@ def test_concurrent_step_repeats_and_phases(rb):
         other = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32)
         out, lse = other(qd)
         torch.cuda.synchronize()
-        assert (out - ref).abs().max().item() < 1e-5 and (lse - ref_lse).abs().max().item() < 1e-5
+        assert_close(out.cpu().numpy(), ref.cpu().numpy(), f"relay split grid={grid}")
+        assert_close(lse.cpu().numpy(), ref_lse.cpu().numpy(), f"relay lse grid={grid}", lse=True)
