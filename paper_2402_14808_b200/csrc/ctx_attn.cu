@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       int p = id2 + G;
       if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
       const Raw nxt = load_raw(id1);
-      if (a.knob & 1) mbar_wait_sleep(&i_empty[qs], ((j / kIQ) & 1) ^ 1); else mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
+      mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
       if (item >= n_items) {
         if (lane == 0) {
           slot.item = -1;
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       CtxItem<R> it;
       for (;;) {
         const int qs = jp % kIQ;
-        if (a.knob & 1) mbar_wait_sleep(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1)); else mbar_wait(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1));
+        mbar_wait(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1));
         item = iq[qs].item;
         it = iq[qs].it;
         __syncwarp();
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       }
       const int mb = mi % kNB;
       const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
-      if (a.knob & 1) mbar_wait_sleep(&m_full[mb], mph); else mbar_wait(&m_full[mb], mph);
+      mbar_wait(&m_full[mb], mph);
       const float* bacc = s_acc + mb * kWorkers * R * 128;
       const float* bml = s_ml + mb * kWorkers * R * 2;
       const int rbase = it.z * R;
@@ -974,9 +974,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
 }
 
 template <int R>
-static cudaError_t launch_ctx_r(const CtxArgs& a_in, int n_items, int n_z, cudaStream_t stream) {
-  CtxArgs a = a_in;
-  a.knob = g_knobs[3];
+static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStream_t stream) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

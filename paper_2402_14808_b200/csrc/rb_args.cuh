@@ -65,10 +65,10 @@ struct CtxArgs {
   float scale_log2;
   unsigned long long* debug_ts;  // optional per-CTA stamps [grid][8] (diagnostics)
   int* sched;                    // optional [3] zeroed counters: item claims, scheduler / CTA exits
-  int knob;                      // diagnostics: g_knobs[3] at launch
 };
 
-// Host-side tuning knobs (rb_debug_set_knob; diagnostics / A-B comparisons).
+// Host-side tuning knobs (rb_debug_set_knob): reserved for A/B comparisons
+// of launch-side choices; no kernel reads them in this build.
 extern int g_knobs[8];
 
 }  // namespace rb

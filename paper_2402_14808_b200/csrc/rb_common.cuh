@@ -75,13 +75,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 
-// mbar_wait for warps off the critical path (schedulers, mergers): back off
-// between probes so their spinning does not take issue slots from the warps
-// that stream and compute.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  while (!mbar_test(bar, parity)) __nanosleep(100);
-}
-
 __device__ __forceinline__ unsigned int smid() {
   unsigned int r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
