@@ -92,14 +92,16 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
   p->n_units = hkv * p->n_qt;
   p->total = (long long)p->n_units * p->tpu;
   long long gcap = grid_cap < 1 ? 1 : grid_cap;
-  // Several query tiles per KV head (large GQA batches) and enough units to
-  // occupy at least half the SMs: deal whole units round-robin, so the CTAs
-  // working on a head's query tiles at the same moment walk its key tiles in
-  // lockstep and every re-read of a tile comes from L2 instead of HBM.
-  // Otherwise stream-K over the flattened tiles.
-  p->rr = (p->n_qt >= 2 && 2LL * p->n_units >= gcap) ? 1 : 0;
+  // Several query tiles per KV head (large GQA batches): deal whole units
+  // round-robin, so the CTAs working on a head's query tiles at the same
+  // moment walk its key tiles in lockstep and every re-read of a tile comes
+  // from L2 instead of HBM.  Otherwise stream-K over the flattened tiles.
+  // Only when whole units fill the CTAs in even waves (>= 85% busy):
+  // otherwise a few CTAs would run one unit more than the rest.
+  const long long waves = (p->n_units + gcap - 1) / gcap;
+  p->rr = (p->n_qt >= 2 && 100LL * p->n_units >= 85LL * waves * gcap) ? 1 : 0;
   if (p->rr)
-    p->grid = (int)(p->n_units < gcap ? p->n_units : gcap);
+    p->grid = (int)((p->n_units + waves - 1) / waves);
   else
     p->grid = (int)(p->total < gcap ? p->total : gcap);
   int mp = 1;

@@ -53,15 +53,19 @@ class SysPlan:
 
     @property
     def rr(self):
-        """Whole units dealt round-robin (several query tiles per KV head and
-        enough units for half the SMs): CTAs on a head's query tiles walk its
-        key tiles in lockstep, so repeated tiles hit L2."""
-        return self.n_qt >= 2 and 2 * self.n_units >= max(1, self.grid_cap)
+        """Whole units dealt round-robin (several query tiles per KV head, and
+        whole units fill the CTAs in even waves, >= 85% busy): CTAs on a
+        head's query tiles walk its key tiles in lockstep, so re-reads hit L2."""
+        gcap = max(1, self.grid_cap)
+        waves = -(-self.n_units // gcap)
+        return self.n_qt >= 2 and 100 * self.n_units >= 85 * waves * gcap
 
     @property
     def grid(self):
         if self.rr:
-            return max(1, min(self.n_units, self.grid_cap))
+            gcap = max(1, self.grid_cap)
+            waves = -(-self.n_units // gcap)
+            return -(-self.n_units // waves)
         return max(1, min(self.total, self.grid_cap))
 
     def cta_begin(self, c):
