@@ -115,6 +115,26 @@ __device__ __forceinline__ float warp_reduce_scatter(float (&v)[H], int lane) {
   return r;
 }
 
+// Incremental (unit, key tile) walk over a CTA's tile range: no integer
+// division per tile (the per-tile path of every warp role is latency-bound).
+struct TileWalker {
+  int kt, u, h, qt;
+  __device__ __forceinline__ void start(const rb_sys_plan& P, int cta, long long t_begin) {
+    u = rb_tile_unit(&P, cta, t_begin);
+    kt = static_cast<int>(t_begin % P.tpu) - 1;  // the first next() lands on t_begin
+    h = u / P.n_qt;
+    qt = u % P.n_qt;
+  }
+  __device__ __forceinline__ void next(const rb_sys_plan& P) {
+    if (++kt == P.tpu) {
+      kt = 0;
+      u = P.rr ? u + P.grid : u + 1;
+      h = u / P.n_qt;
+      qt = u % P.n_qt;
+    }
+  }
+};
+
 template <int NQ>
 __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
@@ -200,11 +220,11 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     // ------------------------------------------------- K producer (+ Q rows)
     const uint64_t pol = l2_policy_evict_first();
     int j = 0, uq = 0;
+    TileWalker tw;
+    tw.start(P, blockIdx.x, t_begin);
     for (long long i = t_begin; i < t_end; ++i, ++j) {
-      const int u = rb_tile_unit(&P, blockIdx.x, i);
-      const int kt = static_cast<int>(i % P.tpu);
-      const int h = u / P.n_qt;
-      const int qt = u % P.n_qt;
+      tw.next(P);
+      const int kt = tw.kt, h = tw.h, qt = tw.qt;
       const int st = j % KS;
       mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
       if (lane == 0) {
@@ -262,10 +282,11 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         mbar_wait(&q_full[0], 0);  // Q rows must not queue behind the V burst either
       }
       int j = 0;
+      TileWalker tw;
+      tw.start(P, blockIdx.x, t_begin);
       for (long long i = t_begin; i < t_end; ++i, ++j) {
-        const int u = rb_tile_unit(&P, blockIdx.x, i);
-        const int kt = static_cast<int>(i % P.tpu);
-        const int h = u / P.n_qt;
+        tw.next(P);
+        const int kt = tw.kt, h = tw.h;
         const int st = j % VS;
         mbar_wait(&v_empty[st], ((j / VS) & 1) ^ 1);
         uint8_t* dst = smem + L::kOffV + st * L::kTileBytes;
@@ -281,8 +302,11 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, NQ, 0, 0);
       int j = 0, uq = 0;
+      TileWalker tw;
+      tw.start(P, blockIdx.x, t_begin);
       for (long long i = t_begin; i < t_end; ++i, ++j) {
-        const int kt = static_cast<int>(i % P.tpu);
+        tw.next(P);
+        const int kt = tw.kt;
         const bool new_unit = (i == t_begin) || kt == 0;
         const bool last_of_unit = (i == t_end - 1) || kt == P.tpu - 1;
         const int qb = uq & 1;
@@ -318,11 +342,13 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, NQ, 1, 0);
       int j = 0;
+      TileWalker tw;
+      tw.start(P, blockIdx.x, t_begin);
       for (long long i = t_begin; i < t_end; ++i, ++j) {
+        tw.next(P);
         const int st = j % VS, pb = j & 1;
         // O accumulates over the tiles of a unit; its first tile starts fresh
-        const long long ua = max(t_begin, (i / P.tpu) * P.tpu);
-        const uint32_t acc0 = (i > ua) ? 1u : 0u;
+        const uint32_t acc0 = (i > t_begin && tw.kt != 0) ? 1u : 0u;
         mbar_wait(&v_full[st], (j / VS) & 1);
         mbar_wait(&p_full[pb], (j >> 1) & 1);
         tc_fence_after();
@@ -381,9 +407,10 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         m_run[c] = -INFINITY;
         l_part[c] = 0.f;
       }
+      int kt = static_cast<int>(ia % P.tpu) - 1;
       for (long long it = ia; it <= ib; ++it) {
         const int j = static_cast<int>(it - t_begin);
-        const int kt = static_cast<int>(it % P.tpu);
+        ++kt;
         const int gb = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         // ---- S tile -> scores (log2 domain)
