@@ -421,39 +421,62 @@ using CtxCompute = typename std::conditional<(R <= 2), SimtCompute<R>, MmaComput
 // the context state (O unnormalised, m log2, l) merged with every stream-K
 // part of the pair's system unit in slot order (deterministic), normalised
 // and written.  One warp, lane = 4 head dims.  The unit must be published.
-__device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, long long pair,
-                                                const float* part_acc, const float* part_ml,
-                                                float4 O, float mt, float lt, void* out, int out_fp32,
-                                                float* lse_out, int lane) {
+// Split in two so the merger can issue the first parts' loads before it
+// waits for the workers (RelayParts carries them in registers).
+struct RelayParts {
+  long long base;
+  int np, col;
+  float mk[4], lk[4];
+  float4 ak[4];
+};
+
+__device__ __forceinline__ void relay_parts_load(const rb_sys_plan& SP, const float* part_acc,
+                                                 const float* part_ml, long long base, int np,
+                                                 int col, int k0, int lane, float* mk, float* lk,
+                                                 float4* ak) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int k = min(k0 + kk, np - 1);
+    const float* pml = part_ml + (base + k) * 2 * SP.nq;
+    mk[kk] = __ldcg(pml + col);
+    lk[kk] = __ldcg(pml + SP.nq + col);
+    ak[kk] = __ldcg(reinterpret_cast<const float4*>(part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + lane * 4));
+  }
+}
+
+__device__ __forceinline__ RelayParts relay_parts_begin(const rb_sys_plan& SP, int hq, long long pair,
+                                                        const float* part_acc, const float* part_ml,
+                                                        int lane) {
+  RelayParts P;
   const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
   const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-  const int qt = static_cast<int>(f / SP.nq), col = static_cast<int>(f % SP.nq);
+  const int qt = static_cast<int>(f / SP.nq);
+  P.col = static_cast<int>(f % SP.nq);
   const int u = (hh / SP.g) * SP.n_qt + qt;
-  const int np = rb_unit_parts(&SP, u);
+  P.np = rb_unit_parts(&SP, u);
+  P.base = static_cast<long long>(u) * SP.max_parts;
+  relay_parts_load(SP, part_acc, part_ml, P.base, P.np, P.col, 0, lane, P.mk, P.lk, P.ak);
+  return P;
+}
+
+__device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayParts& P, long long pair,
+                                                  const float* part_acc, const float* part_ml,
+                                                  float4 O, float mt, float lt, void* out, int out_fp32,
+                                                  float* lse_out, int lane) {
   const int d0 = lane * 4;
-  const long long base = static_cast<long long>(u) * SP.max_parts;
-  for (int k0 = 0; k0 < np; k0 += 4) {  // 4 parts' loads in flight at once
-    float mk[4], lk[4];
-    float4 ak[4];
+  for (int k0 = 0; k0 < P.np; k0 += 4) {
+    if (k0 > 0) relay_parts_load(SP, part_acc, part_ml, P.base, P.np, P.col, k0, lane, P.mk, P.lk, P.ak);
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
-      const int k = min(k0 + kk, np - 1);
-      const float* pml = part_ml + (base + k) * 2 * SP.nq;
-      mk[kk] = __ldcg(pml + col);
-      lk[kk] = __ldcg(pml + SP.nq + col);
-      ak[kk] = __ldcg(reinterpret_cast<const float4*>(part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0));
-    }
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      if (k0 + kk >= np) break;
-      const float mn = fmaxf(mt, mk[kk]);
+      if (k0 + kk >= P.np) break;
+      const float mn = fmaxf(mt, P.mk[kk]);
       const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
-      const float sk = fast_exp2(mk[kk] - mn);
-      lt = lt * so + lk[kk] * sk;
-      O.x = O.x * so + ak[kk].x * sk;
-      O.y = O.y * so + ak[kk].y * sk;
-      O.z = O.z * so + ak[kk].z * sk;
-      O.w = O.w * so + ak[kk].w * sk;
+      const float sk = fast_exp2(P.mk[kk] - mn);
+      lt = lt * so + P.lk[kk] * sk;
+      O.x = O.x * so + P.ak[kk].x * sk;
+      O.y = O.y * so + P.ak[kk].y * sk;
+      O.z = O.z * so + P.ak[kk].z * sk;
+      O.w = O.w * so + P.ak[kk].w * sk;
       mt = mn;
     }
   }
@@ -468,6 +491,14 @@ __device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, l
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + d0) = pk;
   }
   if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
+}
+
+__device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, long long pair,
+                                                const float* part_acc, const float* part_ml,
+                                                float4 O, float mt, float lt, void* out, int out_fp32,
+                                                float* lse_out, int lane) {
+  RelayParts P = relay_parts_begin(SP, hq, pair, part_acc, part_ml, lane);
+  relay_fuse_finish(SP, P, pair, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
 }
 
 // Is the system unit of `pair` published (all its parts written)?  Lane 0
@@ -489,6 +520,15 @@ __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, 
   return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
+// Is the system unit of `pair` in the merger's bitmask of published units?
+__device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int hq, long long pair,
+                                                     unsigned long long pub) {
+  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
+  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
+  const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+  return (pub >> u) & 1;
+}
+
 constexpr int kWorkers = 4;
 constexpr int kDepth = 3;                      // chunks in flight per worker
 static_assert(kDepth == 3, "wait_group ladder in ctx_cta_kernel assumes 3");
@@ -498,6 +538,77 @@ constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + mer
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
 constexpr int kMaxDefer = 62;                  // relay rows per CTA awaiting their system unit
+
+// Relay fusion of a parked pair (the end phase): 8 lanes per pair, lane
+// sub = lane & 7 owning head dims [16 sub, 16 sub + 16), so one warp fuses
+// four pairs with all their loads in flight at once.  Waits for the pair's
+// system unit; same merge order and arithmetic as relay_fuse_pair.
+__device__ __forceinline__ void relay_fuse_parked8(const rb_sys_plan& SP, int hq, long long pair,
+                                                   bool valid, const int* ready, const float* ctx_part,
+                                                   const float* part_acc, const float* part_ml,
+                                                   void* out, int out_fp32, float* lse_out, int lane) {
+  const int sub = lane & 7;
+  int u = 0, col = 0, np = 0;
+  if (valid) {
+    const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
+    const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
+    col = static_cast<int>(f % SP.nq);
+    u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+    np = rb_unit_parts(&SP, u);
+    if (sub == 0)
+      while (ld_acquire_gpu(ready + u) < np) __nanosleep(64);
+  }
+  __syncwarp();
+  if (!valid) return;
+  const int d0 = sub * 16;
+  const float* cp = ctx_part + pair * kPartStride;
+  float4 O[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) O[v] = __ldcg(reinterpret_cast<const float4*>(cp + d0 + 4 * v));
+  const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
+  float mt = ml.x, lt = ml.y;
+  const long long base = static_cast<long long>(u) * SP.max_parts;
+  for (int k = 0; k < np; ++k) {  // the first part's loads fly with the context part's
+    const float* pml = part_ml + (base + k) * 2 * SP.nq;
+    const float mk = __ldcg(pml + col), lk = __ldcg(pml + SP.nq + col);
+    const float* pa = part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0;
+    float4 ak[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) ak[v] = __ldcg(reinterpret_cast<const float4*>(pa + 4 * v));
+    const float mn = fmaxf(mt, mk);
+    const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+    const float sk = fast_exp2(mk - mn);
+    lt = lt * so + lk * sk;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      O[v].x = O[v].x * so + ak[v].x * sk;
+      O[v].y = O[v].y * so + ak[v].y * sk;
+      O[v].z = O[v].z * so + ak[v].z * sk;
+      O[v].w = O[v].w * so + ak[v].w * sk;
+    }
+    mt = mn;
+  }
+  const float inv = 1.f / lt;
+  if (out_fp32) {
+    float* o = reinterpret_cast<float*>(out) + pair * 128 + d0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+      reinterpret_cast<float4*>(o)[v] = make_float4(O[v].x * inv, O[v].y * inv, O[v].z * inv, O[v].w * inv);
+  } else {
+    uint4 pk[2];
+    uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      w[2 * v] = pack_bf16x2(O[v].x * inv, O[v].y * inv);
+      w[2 * v + 1] = pack_bf16x2(O[v].z * inv, O[v].w * inv);
+    }
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + d0);
+    o[0] = pk[0];
+    o[1] = pk[1];
+  }
+  if (lse_out != nullptr && sub == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
+}
+
 
 template <int R>
 struct ItemSlot {
@@ -682,13 +793,30 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     // system partial o_sys / lse_sys).
     bool waited = false;
     int jp = 0;  // queue cursor
+    // diagnostics (debug timestamps only): waits and work of the merger
+    unsigned long long d_mfull = 0, d_work = 0, d_imeta = 0, d_t = 0;
+    // relay with <= 64 system units: the publication counters are polled in
+    // the background (lane l: units l, l + 32; loads issued one item ahead,
+    // consumed at the next) into a bitmask of published units, so deciding
+    // fuse-or-park costs no round trip on the merger's critical path
+    const bool poll = a.ctx_part != nullptr && a.sys_plan.n_units <= 64;
+    unsigned long long pub = 0;
+    int pv0 = 0, pv1 = 0, np0 = 0x7fffffff, np1 = 0x7fffffff;
+    if (poll) {
+      if (lane < a.sys_plan.n_units) np0 = rb_unit_parts(&a.sys_plan, lane);
+      if (lane + 32 < a.sys_plan.n_units) np1 = rb_unit_parts(&a.sys_plan, lane + 32);
+      if (np0 != 0x7fffffff) pv0 = ld_acquire_gpu(a.sys_ready + lane);
+      if (np1 != 0x7fffffff) pv1 = ld_acquire_gpu(a.sys_ready + lane + 32);
+    }
     for (int mi = 0;; ++mi) {
       // next non-empty item off the queue
       int item = -1;
       CtxItem<R> it;
       for (;;) {
         const int qs = jp % kIQ;
+        if (dts) d_t = global_timer_ns();
         mbar_wait(&i_meta[qs], static_cast<uint32_t>((jp / kIQ) & 1));
+        if (dts) d_imeta += global_timer_ns() - d_t;
         item = iq[qs].item;
         it = iq[qs].it;
         __syncwarp();
@@ -697,6 +825,27 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         if (item < 0 || it.n_chunks > 0) break;
       }
       if (item < 0) break;
+      // relay: if row 0's system unit is already published, issue its
+      // parts' loads now so they land while the workers finish the item
+      bool pre = false;
+      RelayParts pp;
+      if (poll) {
+        // fold in the previous poll, then issue the next one
+        const unsigned b0 = __ballot_sync(0xffffffffu, pv0 >= np0);
+        const unsigned b1 = __ballot_sync(0xffffffffu, pv1 >= np1);
+        pub |= static_cast<unsigned long long>(b0) | (static_cast<unsigned long long>(b1) << 32);
+        __syncwarp();  // the acquiring lanes' loads precede every lane's part reads
+        if (np0 != 0x7fffffff && !((pub >> lane) & 1)) pv0 = ld_acquire_gpu(a.sys_ready + lane);
+        if (np1 != 0x7fffffff && !((pub >> (lane + 32)) & 1))
+          pv1 = ld_acquire_gpu(a.sys_ready + lane + 32);
+      }
+      if (a.ctx_part != nullptr && it.z * R < it.nrows) {
+        const long long o0 = static_cast<long long>(it.row0 + (it.z * R) / a.g) * a.hq +
+                             it.h * a.g + (it.z * R) % a.g;
+        pre = poll ? relay_unit_published(a.sys_plan, a.hq, o0, pub)
+                   : relay_unit_ready(a.sys_plan, a.hq, o0, a.sys_ready, lane, false);
+        if (pre) pp = relay_parts_begin(a.sys_plan, a.hq, o0, a.sys_part_acc, a.sys_part_ml, lane);
+      }
       if (!waited && a.ctx_part == nullptr) {
         // before the first output write / o_sys read: the previous grid (a
         // system kernel producing o_sys, or a reader of out) must be done
@@ -705,7 +854,13 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       }
       const int mb = mi % kNB;
       const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
+      if (dts) d_t = global_timer_ns();
       mbar_wait(&m_full[mb], mph);
+      if (dts) {
+        const unsigned long long t1 = global_timer_ns();
+        d_mfull += t1 - d_t;
+        d_t = t1;
+      }
       const float* bacc = s_acc + mb * kWorkers * R * 128;
       const float* bml = s_ml + mb * kWorkers * R * 2;
       const int rbase = it.z * R;
@@ -738,7 +893,13 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
           // park the unnormalised partial and fuse it at the end of the CTA
           int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
           const bool full = defer[0] >= kMaxDefer;
-          if (relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
+          if (i == 0 && pre) {
+            relay_fuse_finish(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml,
+                              make_float4(O[0], O[1], O[2], O[3]), M, Ls, a.out, a.out_fp32,
+                              a.lse_out, lane);
+          } else if (poll ? (relay_unit_published(a.sys_plan, a.hq, oidx, pub) ||
+                             (full && relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, true)))
+                          : relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
             relay_fuse_pair(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml,
                             make_float4(O[0], O[1], O[2], O[3]), M, Ls, a.out, a.out_fp32,
                             a.lse_out, lane);
@@ -786,8 +947,16 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&m_empty[mb]);
+      if (dts) d_work += global_timer_ns() - d_t;
     }
-    if (dts && lane == 0) dts[6] = global_timer_ns();
+    if (dts && lane == 0) {
+      dts[6] = global_timer_ns();
+      unsigned long long* acc = dts + 3072 * 8;
+      acc[0] = d_mfull;
+      acc[1] = static_cast<unsigned long long>(jp);
+      acc[2] = d_work;
+      acc[5] = d_imeta;
+    }
   } else {
   // ---------------------------------------------------------------- workers
   const int w = warp - 1;                       // 0 .. kWorkers-1
@@ -873,13 +1042,16 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     }
   };
 
+  unsigned long long d_ifull = 0, d_mempty = 0, d_t = 0;
   try_issue(0);
   int mi = 0;  // items merged so far (skipped empty items excluded)
   int con_sl = 0;
   int qs = 0;
   uint32_t qph = 0;
   for (int jc = 0;; ++jc) {
+    if (dts) d_t = global_timer_ns();
     mbar_wait(&i_full[qs], qph);
+    if (dts) d_ifull += global_timer_ns() - d_t;
     const int item = iq[qs].item;
     const CtxItem<R> it = iq[qs].it;
     const int rbase = it.z * R;
@@ -930,7 +1102,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     if (dts && lane == 0) dts[2 + w] = global_timer_ns();
 
     // ---- hand the warp's state (rows < R) to merge buffer mb
+    if (dts) d_t = global_timer_ns();
     mbar_wait(&m_empty[mb], mph ^ 1);
+    if (dts) d_mempty += global_timer_ns() - d_t;
     float* macc = s_acc + (mb * kWorkers + w) * R * 128;
     float* mml = s_ml + (mb * kWorkers + w) * R * 2;
     cmp.handoff(macc, mml, lane);
@@ -939,7 +1113,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     ++mi;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  if (dts && lane == 0 && w == 0) dts[7] = global_timer_ns();
+  if (dts && lane == 0 && w == 0) {
+    dts[7] = global_timer_ns();
+    dts[3072 * 8 + 3] = d_ifull;
+    dts[3072 * 8 + 4] = d_mempty;
+  }
   }  // workers
 
   // ------------------------------------------------ relay: deferred fusion
@@ -951,14 +1129,15 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     named_bar_sync(1, 32 * (kWorkers + 1));
     const int* defer = reinterpret_cast<const int*>(smem + SM::kOffDefer);
     const int nd = defer[0];
-    for (int e = warp - 1; e < nd; e += kWorkers + 1) {
-      const long long pair = defer[1 + e];
-      relay_unit_ready(a.sys_plan, a.hq, pair, a.sys_ready, lane, true);
-      const float* cp = a.ctx_part + pair * kPartStride;
-      const float4 O = __ldcg(reinterpret_cast<const float4*>(cp + lane * 4));
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
-      relay_fuse_pair(a.sys_plan, a.hq, pair, a.sys_part_acc, a.sys_part_ml, O, ml.x, ml.y, a.out,
-                      a.out_fp32, a.lse_out, lane);
+    if (dts && warp == kMergerWarp && lane == 0) {
+      dts[3072 * 8 + 6] = global_timer_ns();
+      dts[3072 * 8 + 7] = static_cast<unsigned long long>(nd);
+    }
+    for (int e0 = (warp - 1) * 4; e0 < nd; e0 += (kWorkers + 1) * 4) {
+      const int e = e0 + (lane >> 3);
+      const bool valid = e < nd;
+      relay_fuse_parked8(a.sys_plan, a.hq, valid ? defer[1 + e] : 0, valid, a.sys_ready, a.ctx_part,
+                         a.sys_part_acc, a.sys_part_ml, a.out, a.out_fp32, a.lse_out, lane);
     }
     named_bar_sync(1, 32 * (kWorkers + 1));
     if (dts && warp == kMergerWarp && lane == 0) dts[6] = global_timer_ns();  // CTA done

@@ -174,6 +174,15 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
 
   unsigned long long* dts = args.debug_ts ? args.debug_ts + blockIdx.x * 8 : nullptr;
   if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
+  if (warp == 0) {
+    // q may be produced by the previous kernel in the stream (the K/V tiles
+    // are not).  Once it is complete the next kernel (the context kernel of
+    // the relay step) may be scheduled on the SMs this grid leaves free:
+    // everything this grid waited for is visible to it too, and it polls
+    // this grid's per-unit counters before reading the partials.
+    pdl_wait_primary();
+    pdl_launch_dependents();
+  }
   if (threadIdx.x == 0) {
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
     tma_prefetch_desc(&tmap_k);
@@ -238,13 +247,6 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       if (i == t_begin || kt == 0) {
         // query rows of unit u (after this tile's K is already in flight);
         // q may be produced by the previous kernel in the stream.
-        if (i == t_begin) {
-          pdl_wait_primary();
-          // the next kernel (context + fusion) may now be scheduled as SMs
-          // free up: everything this grid waited for is visible to it too.
-          // It waits for this grid's own memory before reading the partials.
-          pdl_launch_dependents();
-        }
         const int qb = uq & 1;
         mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
         uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;

@@ -101,42 +101,15 @@ def run(s, phases=3, b=32, h=52, c=128):
                   + ", ".join(f"{us(r[0]):.1f}" for r in rows) + "; compute ends "
                   + ", ".join(f"{us(r[2 + w]):.1f}" for r in rows for w in range(4) if r[2 + w])
                   + "; exits " + ", ".join(f"{us(r[7]):.1f}" for r in rows))
-        it = t[3072:].reshape(-1, 32)[:, :30].reshape(-1, 6, 5)
-        it = it[it[:, 0, 0] != 0]
-        if len(it):
-            names = ["publish", "epi_mfull", "w0_chunks_done", "w0_start", "epi_end"]
-            for j in range(6):
-                ok = it[:, j, 4] != 0
-                if ok.sum() < 10:
-                    break
-                x = it[ok, j]
-                print(f"  item {j}: " + "; ".join(
-                    f"{n} {statistics.median([us(v) for v in x[:, i].tolist()]):.1f}"
-                    for i, n in enumerate(names)))
-        ch = t[6144:].reshape(-1, 32)[:len(ctx_t)].reshape(-1, 16, 2)
-        print(f"  chunk stamps: {int((ch[:, :, 0] != 0).sum())} issue, {int((ch[:, :, 1] != 0).sum())} landed")
-        ch = ch[ch[:, 0, 0] != 0]
-        if len(ch):
-            for c in range(12):
-                ok = (ch[:, c, 0] != 0) & (ch[:, c, 1] != 0)
-                if ok.sum() < 10:
-                    break
-                iss = [us(v) for v in ch[ok, c, 0].tolist()]
-                lan = [us(v) for v in ch[ok, c, 1].tolist()]
-                print(f"  w0 chunk {c}: issued {statistics.median(iss):.1f} consumed {statistics.median(lan):.1f}")
-        fz = t[7424:].reshape(-1, 4)
-        fz = fz[fz[:, 0] != 0]
-        if len(fz):
-            for i, n in enumerate(["entry", "after pdl wait", "done"]):
-                print(f"  fuse {n:14s} {q([us(v) for v in fz[:, i].tolist()])}")
-        mg = t[7424:].reshape(-1, 16)[:len(ctx_t)].reshape(-1, 8, 2) * 0
-        print(f"  merge stamps: {int((mg != 0).sum())}")
-        for c in range(6):
-            ok = (mg[:, c, 0] != 0) & (mg[:, c, 1] != 0)
-            if ok.sum() < 10:
-                break
-            print(f"  merge {c}: start {statistics.median([us(v) for v in mg[ok, c, 0].tolist()]):.1f} "
-                  f"inputs ready {statistics.median([us(v) for v in mg[ok, c, 1].tolist()]):.1f}")
+        acc = t[4096:4096 + 1024][t[4096:4096 + 1024, 1] != 0]
+        if len(acc):
+            names = ["merger m_full wait", "merger items", "merger work", "w0 i_full wait",
+                     "w0 m_empty wait", "merger i_meta wait"]
+            print(f"  ctx end-phase start  {q([us(v) for v in acc[:, 6].tolist()])}")
+            print(f"  ctx deferred rows    {q([float(v) for v in acc[:, 7].tolist()])}")
+            for i, n in enumerate(names):
+                col = [float(v) / (1 if i == 1 else 1e3) for v in acc[:, i].tolist()]
+                print(f"  ctx {n:20s} {q(col)}")
         durs = [(int(r[7]) - int(r[0])) / 1e3 for r in ctx_t]
         print(f"  ctx CTA duration p50 {statistics.median(durs):.1f} max {max(durs):.1f}")
 

@@ -42,7 +42,8 @@ def main():
         q, relay, _, paged, bt = bench.build(torch, s, list(range(bench.H)), dev)
         auto = _lib.relay_sys_grid(bench.B, bench.H, bench.H, s, bench.B * bench.C, sms)
         res = []
-        for g in sorted({auto, 40, 60, 70, 80, 90, 100, 110, 120, 148}):
+        grids = os.environ.get("SWEEP_GRIDS", "40,60,70,80,90,100,110,120,148")
+        for g in sorted({auto} | {int(x) for x in grids.split(",")}):
             step = RelayDecodeStep(relay.sys_cache, paged, bt, relay.ctx_lens, bench.H, grid=g)
             res.append((g, time_step(lambda: step(q), flush)))
         print(f"s={s} auto grid {auto}: " + ", ".join(f"{g}:{t:.1f}" for g, t in res), flush=True)
