@@ -14,7 +14,9 @@ from .errors import ContractError, DimensionError, KernelError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # RB_LIB: diagnostics only (a variant build of the same sources, see build.py)
-LIB_PATH = os.environ.get("RB_LIB") or os.path.join(_HERE, "librelay_b200.so")
+# RB_DIAG=1: the diagnostics build (kernels with %globaltimer stamps)
+LIB_PATH = os.environ.get("RB_LIB") or os.path.join(
+    _HERE, "librelay_b200_diag.so" if os.environ.get("RB_DIAG") == "1" else "librelay_b200.so")
 
 RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
 

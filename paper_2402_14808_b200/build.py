@@ -17,6 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librelay_b200.so")
+DIAG_LIB = os.path.join(PKG, "librelay_b200_diag.so")  # -DRB_DIAG=1: timestamp stamps
 # diagnostics: RB_VARIANT="name:-DFOO=1 -DBAR=2" builds librelay_b200_<name>.so
 # with extra defines (select it at run time with RB_LIB=<path>)
 _VARIANT = os.environ.get("RB_VARIANT", "")
@@ -45,6 +46,9 @@ def build(force=False, verbose=False):
                          os.path.join(PKG, "build", name), verbose)
     if not force and not _stale():
         return LIB
+    # the diagnostics build (per-CTA timestamps, profiles/diag_*.py) first:
+    # the staleness check keys on the production library's mtime
+    _build_to(DIAG_LIB, ["-DRB_DIAG=1"], os.path.join(PKG, "build", "diag"), verbose)
     return _build_to(LIB, [], os.path.join(PKG, "build"), verbose)
 
 

@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     reinterpret_cast<uint4*>(smem + SM::kOffQZero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   pdl_launch_dependents();
-  unsigned long long* dts = a.debug_ts ? a.debug_ts + blockIdx.x * 8 : nullptr;
+  unsigned long long* dts = (RB_DIAG && a.debug_ts) ? a.debug_ts + blockIdx.x * 8 : nullptr;
   if (dts && threadIdx.x == 0) {
     dts[0] = global_timer_ns();
     dts[1] = smid();

@@ -7,6 +7,13 @@
 // in cute/arch/mma_sm100_desc.hpp; we only write the raw bits).
 #pragma once
 
+// Diagnostics build (-DRB_DIAG=1, librelay_b200_diag.so): per-CTA
+// %globaltimer stamps (rb_debug_set_timestamps).  Compiled out otherwise, so
+// the production kernels carry no stamp code (instruction-cache footprint).
+#ifndef RB_DIAG
+#define RB_DIAG 0
+#endif
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

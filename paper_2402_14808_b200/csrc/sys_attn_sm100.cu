@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   long long t_begin, t_end;
   rb_cta_range(&P, blockIdx.x, &t_begin, &t_end);
 
-  unsigned long long* dts = args.debug_ts ? args.debug_ts + blockIdx.x * 8 : nullptr;
+  unsigned long long* dts = (RB_DIAG && args.debug_ts) ? args.debug_ts + blockIdx.x * 8 : nullptr;
   if (dts && threadIdx.x == 0) dts[0] = global_timer_ns();
   if (warp == 0) {
     // q may be produced by the previous kernel in the stream (the K/V tiles

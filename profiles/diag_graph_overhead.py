@@ -9,6 +9,8 @@ import sys
 
 import torch
 
+os.environ.setdefault("RB_DIAG", "1")  # the timestamped build of the kernels
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2402_14808_b200 import _lib  # noqa: E402

@@ -16,6 +16,8 @@ import sys
 
 import torch
 
+os.environ.setdefault("RB_DIAG", "1")  # the timestamped build of the kernels
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2402_14808_b200 import _lib, kernels  # noqa: E402
 
@@ -70,8 +72,8 @@ def run(s, phases=3, b=32, h=52, c=128):
     print(f"s={s} phases={phases} sys grid {grid}: event {e0.elapsed_time(e1) * 1e3:.1f} us")
     sys_exit = {}
     if len(sys_t):
-        for i, n in enumerate(["entry", "first_S", "grp0_end", "grp1_end", "kprod_end", "vprod_end", "exit"]):
-            col = [us(r[i if i == 0 else i + 1]) for r in sys_t]
+        for i, n in [(0, "entry"), (2, "first_S"), (3, "softmax_end"), (5, "kprod_end"), (6, "vprod_end"), (7, "exit")]:
+            col = [us(r[i]) for r in sys_t]
             print(f"  sys {n:10s} {q(col)}")
         ext = t[2048:][t[2048:, 0] != 0]
         for i, n in enumerate(["prologue", "k0_issue", "q_ready", "k0_full", "mma0", "v0_issue"]):
