@@ -172,6 +172,31 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
                  void* stream);
 
 /*
+ * Rotary position embedding of fp32 rows (the reference kernel boundary's
+ * `rope_rows(x, positions, base)`, _kernels_cy.pyx:80-102, called through
+ * numerics.rope_rows / rope_apply, numerics.py:81-108): row i's consecutive
+ * pairs (2j, 2j+1) rotated by positions[i] * base^(-2j/d), angles and
+ * rotation in fp64.  x, out: fp32 [n][d] (may alias); positions int64 [n].
+ */
+int rb_rope_rows(const float* x, float* out, const long long* positions, long long n, int d,
+                 double base, void* stream);
+
+/*
+ * Decode-step prologue in one launch: the new tokens' query and key rows
+ * rotated to their positions (model.py:292-293, rope_rows above) and K / V
+ * appended to the paged pool (PagedKvCache.append, kvcache.py:207-235).
+ *   q_in / q_out: bf16 [n_tok][hq][128] (may alias); k_new, v_new: bf16
+ *   [n_tok][hkv][128]; positions int64 [n_tok] (a context token's position
+ *   is its index in the context + s, kvcache.context_position, kvcache.py:25-33);
+ *   slot_mapping int32 [n_tok] as for rb_kv_append.  K is stored rotated.
+ */
+int rb_rope_append(const void* q_in, void* q_out, const void* k_new, const void* v_new,
+                   const long long* positions, const int* slot_mapping, int n_tok, int hq, int hkv,
+                   int d, double base, void* k_pool, void* v_pool, int block_size,
+                   long long stride_block, long long stride_tok, long long stride_head,
+                   void* stream);
+
+/*
  * Debug probe of the tcgen05 operand layouts used by rb_system_attention
  * (one CTA): S^T = K.Q^T and O^T = V^T.P^T for K,V [128][128], Q [nq][128],
  * P [nq][128] bf16 -> s_out, o_out fp32 [128][nq].  For tests only.

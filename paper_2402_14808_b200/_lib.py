@@ -26,6 +26,7 @@ EXPORTS = (
     "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
     "rb_relay_workspace_bytes", "rb_relay_sys_grid", "rb_relay_attention",
     "rb_debug_umma_probe", "rb_debug_set_timestamps", "rb_debug_set_knob",
+    "rb_rope_rows", "rb_rope_append",
 )
 
 _lib = None
@@ -67,6 +68,9 @@ def load():
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+    lib.rb_rope_rows.argtypes = [vp, vp, vp, i64, i32, ctypes.c_double, vp]
+    lib.rb_rope_append.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_double,
+                                   vp, vp, i32, i64, i64, i64, vp]
     lib.rb_debug_set_timestamps.argtypes = [vp]
     lib.rb_debug_set_knob.argtypes = [ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:

@@ -33,6 +33,12 @@ cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const 
 cudaError_t launch_kv_append(const __nv_bfloat16*, const __nv_bfloat16*, const int*,
                              __nv_bfloat16*, __nv_bfloat16*, int, int, int, long long, long long,
                              long long, cudaStream_t);
+cudaError_t launch_rope_append(const __nv_bfloat16*, __nv_bfloat16*, const __nv_bfloat16*,
+                               const __nv_bfloat16*, const long long*, const int*, int, int, int,
+                               double, __nv_bfloat16*, __nv_bfloat16*, int, long long, long long,
+                               long long, cudaStream_t);
+cudaError_t launch_rope_rows(const float*, float*, const long long*, long long, int, double,
+                             cudaStream_t);
 }  // namespace rb
 
 
@@ -393,6 +399,33 @@ int rb_kv_append(const void* k_new, const void* v_new, const int* slot_mapping, 
                            n_tok, hkv, block_size, stride_block, stride_tok, stride_head,
                            static_cast<cudaStream_t>(stream)),
       "kv append launch");
+}
+
+int rb_rope_rows(const float* x, float* out, const long long* positions, long long n, int d,
+                 double base, void* stream) {
+  if (n < 0 || d < 2 || d % 2 != 0 || d > 1024)
+    return fail(RB_ERR_DIMENSION, "rope_rows requires an even dimension <= 1024, got %d", d);
+  return cuda_status(rb::launch_rope_rows(x, out, positions, n, d, base,
+                                          static_cast<cudaStream_t>(stream)),
+                     "rope rows launch");
+}
+
+int rb_rope_append(const void* q_in, void* q_out, const void* k_new, const void* v_new,
+                   const long long* positions, const int* slot_mapping, int n_tok, int hq, int hkv,
+                   int d, double base, void* k_pool, void* v_pool, int block_size,
+                   long long stride_block, long long stride_tok, long long stride_head,
+                   void* stream) {
+  if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported", d);
+  if (n_tok < 0 || hq < 1 || hkv < 1 || hq % hkv != 0)
+    return fail(RB_ERR_DIMENSION, "bad rope/append shape (n_tok=%d hq=%d hkv=%d)", n_tok, hq, hkv);
+  return cuda_status(
+      rb::launch_rope_append(static_cast<const __nv_bfloat16*>(q_in), static_cast<__nv_bfloat16*>(q_out),
+                             static_cast<const __nv_bfloat16*>(k_new),
+                             static_cast<const __nv_bfloat16*>(v_new), positions, slot_mapping,
+                             n_tok, hq, hkv, base, static_cast<__nv_bfloat16*>(k_pool),
+                             static_cast<__nv_bfloat16*>(v_pool), block_size, stride_block,
+                             stride_tok, stride_head, static_cast<cudaStream_t>(stream)),
+      "rope append launch");
 }
 
 int rb_debug_set_knob(int id, int value) {

@@ -209,6 +209,49 @@ def kv_append(k_new, v_new, slot_mapping, k_pool, v_pool, block_size):
         k_pool.stride(1), _stream(k_new.device)), "rb_kv_append")
 
 
+ROPE_BASE = 10000.0  # numerics.ROPE_BASE / model.py:292
+
+
+def rope_rows(x, positions, base=ROPE_BASE, out=None):
+    """`kernels.rope_rows` (_kernels_cy.pyx:80-102) on the GPU: row i's
+    consecutive pairs rotated by positions[i] * base^(-2j/d).  x: fp32 CUDA
+    (n, d), d even; positions: int64 (n,); angles and rotation in fp64."""
+    if x.dim() != 2 or x.shape[1] % 2 != 0:
+        raise DimensionError(f"rope_rows requires (n, even d) rows, got {tuple(x.shape)}")
+    if x.dtype != torch.float32 or not x.is_contiguous():
+        raise ContractError("rope_rows takes contiguous fp32 rows")
+    positions = positions.to(device=x.device, dtype=torch.int64).contiguous()
+    if positions.shape != (x.shape[0],):
+        raise DimensionError("rope_rows: positions must be one per row")
+    out = torch.empty_like(x) if out is None else out
+    _lib.check(_lib.load().rb_rope_rows(x.data_ptr(), out.data_ptr(), positions.data_ptr(),
+                                        x.shape[0], x.shape[1], float(base),
+                                        _stream(x.device)), "rb_rope_rows")
+    return out
+
+
+def rope_append(q, k_new, v_new, positions, slot_mapping, k_pool, v_pool, block_size,
+                base=ROPE_BASE, q_out=None):
+    """Decode-step prologue in one launch: q (n_tok, hq, 128) and k_new
+    (n_tok, hkv, 128) rotated to `positions` (int64, one per token), the
+    rotated K and raw V scattered into a [num_blocks][hkv][bs][128] pool at
+    `slot_mapping` (int32).  Returns the rotated q (in place if q_out is q)."""
+    for name, t in (("q", q), ("k_new", k_new), ("v_new", v_new)):
+        _check_bf16(name, t)
+    n_tok, hq, d = q.shape
+    hkv = k_new.shape[1]
+    if k_new.shape != v_new.shape or k_new.shape[0] != n_tok:
+        raise DimensionError(f"rope_append: k/v {tuple(k_new.shape)} vs q {tuple(q.shape)}")
+    q_out = torch.empty_like(q) if q_out is None else q_out
+    positions = positions.to(device=q.device, dtype=torch.int64).contiguous()
+    _lib.check(_lib.load().rb_rope_append(
+        q.data_ptr(), q_out.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), positions.data_ptr(),
+        slot_mapping.data_ptr(), n_tok, hq, hkv, d, float(base), k_pool.data_ptr(),
+        v_pool.data_ptr(), block_size, k_pool.stride(0), k_pool.stride(2), k_pool.stride(1),
+        _stream(q.device)), "rb_rope_append")
+    return q_out
+
+
 def umma_probe(k, q, v, p):
     """Debug: run the system kernel's tcgen05 operand layouts on one tile."""
     nq = q.shape[0]

@@ -199,6 +199,27 @@ class PagedKvCache:
         kernels.kv_append(k, v, slot_mapping, self.k_pool[layer], self.v_pool[layer],
                           self.block_size)
 
+    def append_rotated(self, request_ids, layer, q, k, v, s, base=kernels.ROPE_BASE):
+        """Decode-step prologue for one new token per request: rotate q and k
+        to the token's absolute position context_position(c_r, s) (the token
+        lands after the request's c_r context tokens and the s-token shared
+        prefix, kvcache.py:25-33; model.py:292-293) and append the rotated K
+        and raw V (kvcache.py:207-235), in one launch.  q (b, hq, 128), k / v
+        (b, hkv, 128) bf16; returns the rotated q."""
+        if k.shape != v.shape or k.dim() != 3 or tuple(k.shape[1:]) != (self.kv_heads, HEAD_DIM):
+            raise DimensionError(f"append expects (b, {self.kv_heads}, {HEAD_DIM}) pairs, "
+                                 f"got {tuple(k.shape)} and {tuple(v.shape)}")
+        if q.shape[0] != len(request_ids) or k.shape[0] != len(request_ids):
+            raise DimensionError("append_rotated: one token per request")
+        pos = [context_position(self._layer_lengths[r][layer], s) for r in request_ids]
+        slots = [self._slots(r, layer, 1)[0] for r in request_ids]
+        dev = self.device
+        return kernels.rope_append(
+            q.to(torch.bfloat16).contiguous(), k.to(torch.bfloat16).contiguous(),
+            v.to(torch.bfloat16).contiguous(), torch.tensor(pos, dtype=torch.int64, device=dev),
+            torch.tensor(slots, dtype=torch.int32, device=dev), self.k_pool[layer],
+            self.v_pool[layer], self.block_size, base=base)
+
     def block_table(self, request_ids, width=None):
         """int32 (b, width) block table on the device (unused entries 0)."""
         tables = [self.pool.tables[r] for r in request_ids]

@@ -109,6 +109,22 @@ def main():
     out["traffic_tuples"] = np.asarray(tuples, dtype=np.int64)
     out["speedup_32_2048_128"] = np.asarray([costmodel.theoretical_speedup(32, 2048, 128)])
 
+    # RoPE (decode prologue): numerics.rope_rows / rope_apply
+    # (numerics.py:81-108 -> kernels.rope_rows, _kernels_cy.pyx:80-102) at
+    # context positions token_index + s (kvcache.context_position, kvcache.py:25-33)
+    from relayserve import kvcache  # noqa: E402
+    rng = np.random.default_rng(5)
+    xr = rng.standard_normal((12, 128))
+    pos = np.asarray([kvcache.context_position(t, s) for t, s in
+                      [(0, 0), (1, 0), (0, 1), (5, 512), (127, 8192), (3, 32768), (1023, 65536),
+                       (0, 65535), (17, 4096), (2, 7), (100, 100), (64, 131072)]], dtype=np.int64)
+    out["rope_x"] = xr
+    out["rope_pos"] = pos
+    out["rope_out"] = numerics.rope_rows(xr, pos)
+    v8 = rng.standard_normal(8)
+    out["rope_apply_v"] = v8
+    out["rope_apply_out"] = np.stack([numerics.rope_apply(v8, p) for p in (0, 1, 2, 1000)])
+
     path = os.path.join(HERE, "reference_golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {len(out)} arrays to {path} ({os.path.getsize(path)} bytes)")

@@ -412,3 +412,91 @@ def test_concurrent_step_repeats_and_phases(rb):
         torch.cuda.synchronize()
         assert_close(out.cpu().numpy(), ref.cpu().numpy(), f"relay split grid={grid}")
         assert_close(lse.cpu().numpy(), ref_lse.cpu().numpy(), f"relay lse grid={grid}", lse=True)
+
+
+# ------------------------------------------------- RoPE + KV append (8f2)
+
+def test_rope_rows_vs_oracle(rb, oracle):
+    """rb_rope_rows against the reference's rope_rows on the golden rows
+    (positions up to 131136) and random fp32 rows of several widths."""
+    from paper_2402_14808_b200 import kernels
+    g = np.load(__file__.replace("test_gpu_parity.py", "golden/reference_golden.npz"))
+    cases = [(g["rope_x"].astype(np.float32), g["rope_pos"])]
+    rng = np.random.default_rng(23)
+    for n, d in ((5, 2), (64, 16), (300, 128)):
+        cases.append((rng.standard_normal((n, d)).astype(np.float32),
+                      rng.integers(0, 140000, size=n).astype(np.int64)))
+    for x, pos in cases:
+        got = kernels.rope_rows(torch.from_numpy(x).cuda(), torch.from_numpy(pos))
+        torch.cuda.synchronize()
+        ref = oracle.rope_rows(x.astype(np.float64), pos, 10000.0)
+        err = np.abs(got.cpu().numpy().astype(np.float64) - ref).max()
+        print(f"rope rows {x.shape}: max|d| = {err:.3e}")
+        assert err <= 2e-6 * max(1.0, np.abs(ref).max())
+
+
+def test_rope_append_vs_oracle(rb, oracle):
+    """rb_rope_append: rotated q (in place) and rotated K / raw V in the
+    shuffled paged pool, against the oracle on the same bf16 inputs (output
+    rounded once to bf16: at most one bf16 ulp from the rounded oracle)."""
+    from paper_2402_14808_b200 import kernels
+    rng = np.random.default_rng(29)
+    n_tok, hq, hkv, bs, nblk = 37, 8, 2, 16, 40
+    q = bf16(rng.standard_normal((n_tok, hq, 128)))
+    k = bf16(rng.standard_normal((n_tok, hkv, 128)))
+    v = bf16(rng.standard_normal((n_tok, hkv, 128)))
+    pos = np.asarray([oracle.context_position(int(t), int(s)) for t, s in
+                      zip(rng.integers(0, 4096, size=n_tok), rng.integers(0, 65536, size=n_tok))],
+                     dtype=np.int64)
+    slots = rng.permutation(nblk * bs)[:n_tok].astype(np.int32)
+    kp = torch.zeros((nblk, hkv, bs, 128), dtype=torch.bfloat16, device="cuda")
+    vp = torch.zeros_like(kp)
+    qd = dev_bf16(q)
+    out = kernels.rope_append(qd, dev_bf16(k), dev_bf16(v), torch.from_numpy(pos),
+                              torch.from_numpy(slots).cuda(), kp, vp, bs, q_out=qd)
+    torch.cuda.synchronize()
+    assert out.data_ptr() == qd.data_ptr()
+
+    def ulps(got, ref):
+        r = oracle.round_bf16(ref)
+        ulp = np.maximum(np.abs(r), 1e-30) * 2.0 ** -7
+        return float((np.abs(got - r) / ulp).max())
+
+    q_ref = oracle.rope_rows(q.reshape(-1, 128), np.repeat(pos, hq), 10000.0).reshape(q.shape)
+    assert ulps(qd.float().cpu().numpy(), q_ref) <= 1.0
+    k_ref = oracle.rope_rows(k.reshape(-1, 128), np.repeat(pos, hkv), 10000.0).reshape(k.shape)
+    kpn, vpn = kp.float().cpu().numpy(), vp.float().cpu().numpy()
+    for t, sl in enumerate(slots):
+        blk, off = divmod(int(sl), bs)
+        assert ulps(kpn[blk, :, off], k_ref[t]) <= 1.0
+        assert (vpn[blk, :, off] == v[t]).all()
+
+
+def test_append_rotated_decode_prologue(rb, oracle):
+    """PagedKvCache.append_rotated: each request's new token lands after its
+    context at position c_r + s, K rotated in the pool, q returned rotated."""
+    from paper_2402_14808_b200.kvcache import PagedKvCache
+    rng = np.random.default_rng(31)
+    b, hq, hkv, s = 5, 4, 2, 1000
+    cache = PagedKvCache(2, hkv, 64, 16, device="cuda")
+    ids = [f"r{i}" for i in range(b)]
+    lens = [int(x) for x in rng.integers(0, 40, size=b)]
+    for r, c in zip(ids, lens):
+        cache.register(r)
+        if c:
+            cache.append(r, 1, dev_bf16(rng.standard_normal((c, hkv, 128))),
+                         dev_bf16(rng.standard_normal((c, hkv, 128))))
+    q = bf16(rng.standard_normal((b, hq, 128)))
+    k = bf16(rng.standard_normal((b, hkv, 128)))
+    v = bf16(rng.standard_normal((b, hkv, 128)))
+    qr = cache.append_rotated(ids, 1, dev_bf16(q), dev_bf16(k), dev_bf16(v), s)
+    torch.cuda.synchronize()
+    pos = np.asarray([c + s for c in lens], dtype=np.int64)
+    q_ref = oracle.round_bf16(oracle.rope_rows(q.reshape(-1, 128), np.repeat(pos, hq), 10000.0))
+    assert np.abs(qr.float().cpu().numpy().reshape(-1, 128) - q_ref).max() <= 2.0 ** -6 * np.abs(q_ref).max()
+    for i, (r, c) in enumerate(zip(ids, lens)):
+        assert cache.length(r, 1) == c + 1
+        kk, vv = cache.gather(r, 1)
+        k_ref = oracle.round_bf16(oracle.rope_rows(k[i], np.full(hkv, pos[i]), 10000.0))
+        assert np.abs(kk[c].float().cpu().numpy() - k_ref).max() <= 2.0 ** -6 * np.abs(k_ref).max()
+        assert (vv[c].float().cpu().numpy() == v[i]).all()

@@ -165,3 +165,34 @@ def test_round_bf16(oracle):
     x = np.random.default_rng(1).standard_normal(1000) * 10
     t = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
     assert (oracle.round_bf16(x) == t).all()
+
+
+def test_rope_golden_bitwise(oracle, golden):
+    """rope_rows (_kernels_cy.pyx:80-102) at context positions index + s
+    (kvcache.py:25-33) against the reference's own outputs."""
+    assert (oracle.rope_rows(golden["rope_x"], golden["rope_pos"], 10000.0)
+            == golden["rope_out"]).all()
+    v = golden["rope_apply_v"]
+    got = np.stack([oracle.rope_rows(v[None], np.asarray([p]), 10000.0)[0] for p in (0, 1, 2, 1000)])
+    assert (got == golden["rope_apply_out"]).all()
+    assert oracle.context_position(5, 512) == 517
+    with pytest.raises(oracle.ContractError):
+        oracle.context_position(-1, 3)
+
+
+def test_rope_bitwise_vs_compiled_reference(oracle):
+    _, kernels = _ref()
+    rng = np.random.default_rng(17)
+    for n, d in ((1, 2), (7, 16), (33, 128)):
+        x = rng.standard_normal((n, d))
+        pos = rng.integers(0, 200000, size=n).astype(np.int64)
+        assert (oracle.rope_rows(x, pos, 10000.0) == kernels.rope_rows(x, pos, 10000.0)).all()
+
+
+def test_rope_properties(oracle):
+    # test_numerics.py:88 (position 0 is the identity), norm preservation
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((50, 128))
+    assert (oracle.rope_rows(x, np.zeros(50, dtype=np.int64), 10000.0) == x).all()
+    y = oracle.rope_rows(x, rng.integers(0, 70000, size=50), 10000.0)
+    assert np.abs(np.linalg.norm(y, axis=1) - np.linalg.norm(x, axis=1)).max() < 1e-12
