@@ -398,6 +398,11 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     const uint32_t pkb = (key_lane >> 6) * (NQ * 128);
 
     float m_run[H], acc[H], l_part[H];
+    // diagnostics build only: epilogue time split (o_full wait, through the
+    // row-sum exchange, through the part write / publish) and unit count
+    unsigned long long d_t0 = 0, d_e1 = 0, d_e2 = 0, d_e3 = 0;
+    int d_nu = 0;
+    int pend_u = -1;  // relay: unit whose part is written but not yet published
     pdl_wait_primary();  // o_sys / partials may still be read by the previous kernel
     long long i = t_begin;
     while (i < t_end) {
@@ -503,14 +508,25 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[gb]);
+        if (pend_u >= 0 && (it > ia || it == ib)) {
+          // publish the previous unit's part now that its stores have had a
+          // tile's time to drain: the fence no longer stalls the group
+          if (cw == 0 && lane == 0) {
+            __threadfence();
+            atomicAdd(&args.counters[pend_u], 1);
+          }
+          pend_u = -1;
+        }
       }
 
       // ---- unit end: O from TMEM (after the unit's last P.V), row sums
       // reduced over the 128 key lanes once per unit, then write / merge
       {
         const int jl = static_cast<int>(ib - t_begin);
+        if (dts) d_t0 = global_timer_ns();
         // P.V(jl) complete implies every earlier MMA complete
         mbar_wait(&o_full[jl & 1], static_cast<uint32_t>((jl >> 1) & 1));
+        if (dts) d_e1 += global_timer_ns() - d_t0;
         tc_fence_after();
         tmem_ld_32x32b<H>(o_addr, acc);
         tmem_wait_ld();
@@ -529,6 +545,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < H; ++c) lrow[c] = lg[col0 + c];
         named_bar_sync(bar_grp, L::NCW * 32);  // lg reads done before the next unit's writes
+        if (dts) d_e2 += global_timer_ns() - d_t0;
         const int h = u / P.n_qt, qt = u % P.n_qt;
         const int owner0 = rb_unit_owner0(&P, u);
         const int nparts = rb_unit_parts(&P, u);
@@ -549,13 +566,12 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
             }
           }
           if (args.counters != nullptr) {
-            // publish the part: the context kernel, running concurrently,
-            // polls the unit's counter (release after the group's writes)
+            // publish the part (the context kernel, running concurrently,
+            // polls the unit's counter): the barrier orders every warp's
+            // writes before thread (0, 0)'s fence + increment, which come one
+            // tile into the next unit (or at the end of the CTA's range)
             named_bar_sync(bar_grp, L::NCW * 32);
-            if (cw == 0 && lane == 0) {
-              __threadfence();
-              atomicAdd(&args.counters[u], 1);
-            }
+            pend_u = u;
           }
         } else if (nparts == 1) {
 #pragma unroll
@@ -645,9 +661,23 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           }
         }
       }
+      if (dts) {
+        d_e3 += global_timer_ns() - d_t0;
+        ++d_nu;
+      }
       i = unit_end;
     }
-    if (dts && threadIdx.x == L::kRoleWarps * 32) dts[3] = global_timer_ns();
+    if (pend_u >= 0 && cw == 0 && lane == 0) {
+      __threadfence();
+      atomicAdd(&args.counters[pend_u], 1);
+    }
+    if (dts && threadIdx.x == L::kRoleWarps * 32) {
+      dts[3] = global_timer_ns();
+      dts[4] = d_nu;
+      dtx[6] = d_e1;
+      dtx[7] = d_e2;
+      dtx[3] = d_e3;  // replaces the k0_full stamp
+    }
   }
 
   if (dts && threadIdx.x == 0) dts[5] = global_timer_ns();

@@ -75,11 +75,15 @@ def run(s, phases=3, b=32, h=52, c=128):
         for i, n in [(0, "entry"), (2, "first_S"), (3, "softmax_end"), (5, "kprod_end"), (6, "vprod_end"), (7, "exit")]:
             col = [us(r[i]) for r in sys_t]
             print(f"  sys {n:10s} {q(col)}")
-        ext = t[2048:][t[2048:, 0] != 0]
+        ext = t[2048:3072][t[2048:3072, 0] != 0]
         for i, n in enumerate(["prologue", "k0_issue", "q_ready", "k0_full", "mma0", "v0_issue"]):
             col = [us(r[i]) for r in ext if r[i] != 0]
             if col:
                 print(f"  sys {n:10s} {q(col)}")
+        if len(ext):
+            print(f"  sys units/CTA       {q([float(v) for v in sys_t[:, 4].tolist()])}")
+            for c, n in ((6, "epi o_full wait"), (7, "epi thru row sums"), (3, "epi total")):
+                print(f"  sys {n:17s} {q([float(v) / 1e3 for v in ext[:, c].tolist()])}")
         for r in sys_t:
             sys_exit[int(r[1])] = us(r[7])
     if len(ctx_t):
