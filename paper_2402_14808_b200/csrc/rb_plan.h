@@ -74,7 +74,12 @@ RB_HD int rb_unit_owner0(const rb_sys_plan* p, int u) {
   return p->rr ? u % p->grid : rb_tile_owner(p, (long long)u * p->tpu);
 }
 
-RB_HD int rb_pick_nq(int rows_per_head) { return rows_per_head <= 16 ? 16 : 32; }
+// Query rows per tile: the swap-AB kernel takes 16 / 32 (N of the MMA); from
+// 128 rows per KV head on, the non-swapped kernel (sys_gqa_sm100.cu) takes
+// 128-row tiles (M of the MMA).
+RB_HD int rb_pick_nq(int rows_per_head) {
+  return rows_per_head <= 16 ? 16 : rows_per_head < 128 ? 32 : 128;
+}
 
 // Fill a plan. grid_cap = number of CTAs the device can hold at once
 // (SM count for this one-CTA-per-SM kernel).

@@ -707,11 +707,15 @@ static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, cons
   return cudaGetLastError();
 }
 
+cudaError_t launch_system_attention_gqa(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
+                                        cudaStream_t);
+
 cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
                                     const SysArgs& a, cudaStream_t stream) {
   switch (a.plan.nq) {
     case 16: return launch_sys<16>(tk, tv, a, stream);
     case 32: return launch_sys<32>(tk, tv, a, stream);
+    case 128: return launch_system_attention_gqa(tk, tv, a, stream);
     default: return cudaErrorInvalidValue;
   }
 }

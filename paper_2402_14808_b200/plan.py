@@ -12,7 +12,9 @@ KEY_TILE = 128
 
 
 def pick_nq(rows_per_head: int) -> int:
-    return 16 if rows_per_head <= 16 else 32
+    if rows_per_head <= 16:
+        return 16
+    return 32 if rows_per_head < 128 else 128
 
 
 @dataclass(frozen=True)

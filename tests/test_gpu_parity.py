@@ -82,6 +82,10 @@ def test_umma_probe_layouts(rb, nq):
     (64, 2, 2, 384, 3),          # 64 rows/head -> 2 q-tiles of 32
     (24, 8, 2, 300, 7),          # GQA g=4: 96 rows/head -> 2 q-tiles
     (1, 1, 1, 1, None),          # single key
+    (64, 8, 2, 700, None),       # 256 rows/head: non-swapped 128-row kernel, 2 q-tiles
+    (40, 8, 2, 300, 5),          # 160 rows/head (partial q-tile), stream-K parts
+    (128, 4, 1, 129, None),      # 512 rows/head, partial last key tile
+    (32, 32, 8, 1000, 3),        # g=4, 128 rows/head exactly, 3 CTAs
 ])
 def test_system_attention_vs_oracle(rb, oracle, n_rows, hq, hkv, s, grid):
     from paper_2402_14808_b200 import kernels
@@ -500,3 +504,35 @@ def test_append_rotated_decode_prologue(rb, oracle):
         k_ref = oracle.round_bf16(oracle.rope_rows(k[i], np.full(hkv, pos[i]), 10000.0))
         assert np.abs(kk[c].float().cpu().numpy() - k_ref).max() <= 2.0 ** -6 * np.abs(k_ref).max()
         assert (vv[c].float().cpu().numpy() == v[i]).all()
+
+
+def test_relay_step_gqa_large_vs_oracle(rb, oracle):
+    """The concurrent relay step with >= 128 rows per KV head (the non-swapped
+    system kernel's parts fused in the context kernel) against the oracle,
+    and bitwise repeatable."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    rng = np.random.default_rng(77)
+    b, hq, hkv, s = 48, 8, 2, 900
+    lens = [int(x) for x in rng.integers(1, 160, size=b)]
+    q = bf16(rng.standard_normal((b, hq, 128)))
+    sk = bf16(rng.standard_normal((s, hkv, 128)))
+    sv = bf16(rng.standard_normal((s, hkv, 128)))
+    ck = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    cv = [bf16(rng.standard_normal((c, hkv, 128))) for c in lens]
+    paged, bt, cl = make_paged(rb, ck, cv, hkv)
+    qd = dev_bf16(q)
+    for grid in (None, 3):
+        step = RelayDecodeStep(SystemKvCache.from_shd([sk], [sv]), paged, bt, cl, hq, grid=grid,
+                               out_dtype=torch.float32)
+        out, lse = [t.clone() for t in step(qd)]
+        o2, l2 = step(qd)
+        torch.cuda.synchronize()
+        assert torch.equal(out, o2) and torch.equal(lse, l2)
+        g = hq // hkv
+        for r in (0, 17, b - 1):
+            fk = oracle.expand_kv(np.concatenate([sk, ck[r]]), g)
+            fv = oracle.expand_kv(np.concatenate([sv, cv[r]]), g)
+            ref = oracle.attention_with_lse(q[r][None, None], fk[None], fv[None], causal=False)
+            assert_close(out[r].cpu().numpy(), ref.output[0, 0], f"relay gqa-large row {r} grid {grid}")
+            assert_close(lse[r].cpu().numpy(), ref.lse[0, 0], "relay gqa-large lse", lse=True)
