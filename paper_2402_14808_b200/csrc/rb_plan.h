@@ -105,10 +105,19 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
   // otherwise a few CTAs would run one unit more than the rest.
   const long long waves = (p->n_units + gcap - 1) / gcap;
   p->rr = (p->n_qt >= 2 && 100LL * p->n_units >= 85LL * waves * gcap) ? 1 : 0;
-  if (p->rr)
+  if (p->rr) {
     p->grid = (int)((p->n_units + waves - 1) / waves);
-  else
+  } else if (p->n_qt >= 2 && p->n_units <= gcap &&
+             100LL * p->n_units * (gcap / p->n_units) >= 85LL * gcap) {
+    // several query tiles per KV head, fewer units than CTAs: an equal
+    // number of CTAs per unit (if that keeps >= 85% of them), so each CTA
+    // holds one aligned key range of one unit and the CTAs on a head's query
+    // tiles stream the same key tiles at the same time (re-reads from L2)
+    p->grid = (int)(p->n_units * (gcap / p->n_units));
+    if ((long long)p->grid > p->total) p->grid = (int)p->total;
+  } else {
     p->grid = (int)(p->total < gcap ? p->total : gcap);
+  }
   int mp = 1;
   for (int u = 0; u < p->n_units; ++u) {
     int c = rb_unit_parts(p, u);

@@ -30,7 +30,10 @@ namespace gqa {
 
 constexpr int kRows = 128;                 // query rows per tile (MMA M)
 constexpr int kTile = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB K or V tile
-constexpr int KS = 2, VS = 2;
+#ifndef GQA_KS
+#define GQA_KS 2
+#endif
+constexpr int KS = GQA_KS, VS = 2;
 constexpr int kQBytes = kRows * 256;       // [2 kblocks][128 rows][128 B]
 constexpr int kOffK = 0;
 constexpr int kOffV = kOffK + KS * kTile;

@@ -64,11 +64,15 @@ class SysPlan:
 
     @property
     def grid(self):
+        gcap = max(1, self.grid_cap)
         if self.rr:
-            gcap = max(1, self.grid_cap)
             waves = -(-self.n_units // gcap)
             return -(-self.n_units // waves)
-        return max(1, min(self.total, self.grid_cap))
+        if (self.n_qt >= 2 and self.n_units <= gcap
+                and 100 * self.n_units * (gcap // self.n_units) >= 85 * gcap):
+            # aligned split: gcap // n_units CTAs per unit (L2 lockstep)
+            return min(self.n_units * (gcap // self.n_units), self.total)
+        return max(1, min(self.total, gcap))
 
     def cta_begin(self, c):
         return c * self.total // self.grid
