@@ -284,12 +284,19 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[sb]);
         const int valid = min(RB_KEY_TILE, P.s - kt * RB_KEY_TILE);
-        float mx = -INFINITY;
+        if (valid < RB_KEY_TILE) {
+          // the prefix's last, partial tile only: masked keys get p = 0
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          x[c] = c < valid ? x[c] * args.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, x[c]);
+          for (int c = 0; c < 128; ++c) x[c] = c < valid ? x[c] : -INFINITY;
         }
+        // row max on the raw scores (the scale is positive), 4 chains
+        float m4[4] = {x[0], x[1], x[2], x[3]};
+#pragma unroll
+        for (int c = 4; c < 128; c += 4) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], x[c + e]);
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * args.scale_log2;
         // P.V(j-1) complete: P may be overwritten, O may be rescaled
         mbar_wait(p_empty, (j & 1) ^ 1);
         tc_fence_after();
@@ -316,17 +323,19 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
             m_run = mn;
           }
         }
-        // P row (bf16, K-major SW128: row r, two 64-key halves)
+        // P row (bf16, K-major SW128: row r, two 64-key halves):
+        // p = exp2(s * scale - m), one FFMA + one MUFU per score
         const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-        float ls = 0.f;
+        const float sl = args.scale_log2;
+        float l4[4] = {0.f, 0.f, 0.f, 0.f};
         uint8_t* prow = smem + kOffP;
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
           float p[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            p[e] = fast_exp2(x[ch * 8 + e] - mu);
-            ls += p[e];
+            p[e] = fast_exp2(fmaf(x[ch * 8 + e], sl, -mu));
+            l4[e & 3] += p[e];
           }
           uint4 pk;
           pk.x = pack_bf16x2(p[0], p[1]);
@@ -335,6 +344,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           pk.w = pack_bf16x2(p[6], p[7]);
           *reinterpret_cast<uint4*>(prow + (ch >> 3) * (kRows * 128) + sw128_offset(r, (ch & 7) * 8)) = pk;
         }
+        const float ls = (l4[0] + l4[1]) + (l4[2] + l4[3]);
         l_run += ls;
         fence_proxy_async_smem();
         tc_fence_before();
