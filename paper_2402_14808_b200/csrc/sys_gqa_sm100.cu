@@ -326,16 +326,22 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         // P row (bf16, K-major SW128: row r, two 64-key halves):
         // p = exp2(s * scale - m), one FFMA + one MUFU per score
         const float mu = (m_run == -INFINITY) ? 0.f : m_run;
-        const float sl = args.scale_log2;
-        float l4[4] = {0.f, 0.f, 0.f, 0.f};
+        const float2 sl2 = make_float2(args.scale_log2, args.scale_log2);
+        const float2 nmu2 = make_float2(-mu, -mu);
+        float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
         uint8_t* prow = smem + kOffP;
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
           float p[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            p[e] = fast_exp2(fmaf(x[ch * 8 + e], sl, -mu));
-            l4[e & 3] += p[e];
+          for (int e = 0; e < 8; e += 2) {
+            const float2 a = ffma2(make_float2(x[ch * 8 + e], x[ch * 8 + e + 1]), sl2, nmu2);
+            p[e] = fast_exp2(a.x);
+            p[e + 1] = fast_exp2(a.y);
+            if (e & 2)
+              l2b = fadd2(l2b, make_float2(p[e], p[e + 1]));
+            else
+              l2a = fadd2(l2a, make_float2(p[e], p[e + 1]));
           }
           uint4 pk;
           pk.x = pack_bf16x2(p[0], p[1]);
@@ -344,7 +350,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           pk.w = pack_bf16x2(p[6], p[7]);
           *reinterpret_cast<uint4*>(prow + (ch >> 3) * (kRows * 128) + sw128_offset(r, (ch & 7) * 8)) = pk;
         }
-        const float ls = (l4[0] + l4[1]) + (l4[2] + l4[3]);
+        const float ls = (l2a.x + l2a.y) + (l2b.x + l2b.y);
         l_run += ls;
         fence_proxy_async_smem();
         tc_fence_before();
