@@ -140,6 +140,15 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
   const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
   int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
+  if (p.nq == 128 && p.n_units <= sms) {
+    // 128-row GQA kernel: whole multiples of the unit count, rounded down
+    // (at least one CTA per unit), so the CTAs on a head's query tiles stay
+    // aligned and share K/V in L2 (measured: C4 best at 2 CTAs per unit,
+    // C5 at 1; misaligned splits lose 10-20%)
+    const int k = g / p.n_units;
+    g = (k < 1 ? 1 : k) * p.n_units;
+    return g;
+  }
   // latency floor: with few key tiles per CTA the system kernel is bound by
   // its per-CTA pipeline (prologue + ~1.5 us per tile), not by bytes; the
   // measured optimum at s <= 2k keeps ~27% of the SMs on it

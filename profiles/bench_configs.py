@@ -68,6 +68,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--naive", action="store_true", help="also time the naive kernel")
+    ap.add_argument("--grids", default="", help="diagnostics: also time these system-kernel SM splits")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     flush = bench.make_flush(torch, dev)
@@ -91,6 +92,15 @@ def main():
                "roofline_us": t_star * 1e6, "frac_of_roofline": t_star / (ms * 1e-3),
                "bound": "tensor" if shp.flops_sys / (tc * 1e12) > shp.bytes_alg / (hbm * 1e9) else "hbm",
                "plan": relay.plan, "sys_alone_plan": alone.plan}
+        if args.grids:
+            sweep = {}
+            for gsel in (int(x) for x in args.grids.split(",")):
+                other = RelayDecodeStep(sys_cache, paged, bt, cl, cfg["hq"], grid=gsel)
+                go = bench.graph_of(torch, lambda: other(q))
+                sweep[gsel] = round(statistics.mean(
+                    bench.time_loop(torch, go.replay, args.steps, args.warmup, flush)) * 1e3, 1)
+                del other, go
+            row["split_sweep_us"] = sweep
         if args.naive:
             naive = NaiveDecodeStep(sys_cache, paged, bt, cl, cfg["hq"])
             row["naive_us_per_step"] = statistics.mean(
