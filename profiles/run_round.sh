@@ -19,3 +19,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 # one full capture of each kernel of the relay step at C2 s=8192
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sys_attn|ctx_cta" -c 2 -f \
   -o $out/${tag}_prof_step python profiles/diag_relay_timeline.py 8192 3 > $out/${tag}_ncu_step.log 2>&1; echo "ncu step rc $?"
+# one full capture of the GQA-large system kernel (C4 shape, alone on all SMs)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sys_gqa -s 3 -c 1 -f \
+  -o $out/${tag}_prof_gqa python profiles/diag_gqa_sys.py > $out/${tag}_ncu_gqa.log 2>&1; echo "ncu gqa rc $?"
