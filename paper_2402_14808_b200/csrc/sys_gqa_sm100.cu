@@ -33,14 +33,21 @@ constexpr int kTile = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB K or V tile
 #ifndef GQA_KS
 #define GQA_KS 2
 #endif
-constexpr int KS = GQA_KS, VS = 2;
+#ifndef GQA_VS
+#define GQA_VS 2
+#endif
+#ifndef GQA_NP
+#define GQA_NP 1
+#endif
+constexpr int KS = GQA_KS, VS = GQA_VS;
+constexpr int NP = GQA_NP;                 // P buffers (1: P.V(j-1) gates the softmax of tile j)
 constexpr int kQBytes = kRows * 256;       // [2 kblocks][128 rows][128 B]
 constexpr int kOffK = 0;
 constexpr int kOffV = kOffK + KS * kTile;
 constexpr int kOffQ = kOffV + VS * kTile;
 constexpr int kOffP = kOffQ + kQBytes;
-constexpr int kOffBar = kOffP + kQBytes;
-constexpr int kNumBars = 2 * KS + 2 * VS + 12;
+constexpr int kOffBar = kOffP + NP * kQBytes;
+constexpr int kNumBars = 2 * KS + 2 * VS + 10 + 2 * NP;
 constexpr int kOffMisc = kOffBar + kNumBars * 8;
 constexpr int kBytes = kOffMisc + 64;
 constexpr int kThreads = 256;
@@ -78,10 +85,10 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
   uint64_t* s_full = bars + 2 * KS + 2 * VS;  // [2]
   uint64_t* s_empty = s_full + 2;             // [2]
   uint64_t* o_full = s_full + 4;              // [2], P.V(j) -> [j & 1]
-  uint64_t* p_full = s_full + 6;
-  uint64_t* p_empty = s_full + 7;
-  uint64_t* q_full = s_full + 8;
-  uint64_t* q_empty = s_full + 9;
+  uint64_t* p_full = s_full + 6;              // [NP]
+  uint64_t* p_empty = p_full + NP;            // [NP]
+  uint64_t* q_full = p_empty + NP;
+  uint64_t* q_empty = q_full + 1;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
 
   const rb_sys_plan& P = args.plan;
@@ -111,8 +118,10 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
       mbar_init(&s_empty[i], 4);
       mbar_init(&o_full[i], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(p_empty, 1);
+    for (int i = 0; i < NP; ++i) {
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+    }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     fence_mbar_init();
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         const uint32_t acc0 = (j > 0 && wp.kt != 0) ? 1u : 0u;
         const int st = j % VS;
         mbar_wait(&v_full[st], (j / VS) & 1);
-        mbar_wait(p_full, j & 1);
+        mbar_wait(&p_full[j % NP], static_cast<uint32_t>((j / NP) & 1));
         tc_fence_after();
         const uint32_t v_base = smem_v + st * kTile;
 #pragma unroll
@@ -239,13 +248,13 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           // A = P (K-major, 16 keys); B = V tile, MN-major: 16 keys = two
           // 8-key swizzle atoms, the two 64-wide d halves kTile / 2 apart
           const uint64_t a =
-              make_smem_desc_sw128(smem_p + (kk >> 2) * (kRows * 128) + (kk & 3) * 32, 16, 1024);
+              make_smem_desc_sw128(smem_p + (j % NP) * kQBytes + (kk >> 2) * (kRows * 128) + (kk & 3) * 32, 16, 1024);
           const uint64_t b = make_smem_desc_sw128(v_base + kk * 2048, kTile / 2, 1024);
           umma_f16_ss(tmem_base + 256, a, b, idesc_pv, kk > 0 ? 1u : acc0);
         }
         umma_commit(&o_full[j & 1]);
         umma_commit(&v_empty[st]);
-        umma_commit(p_empty);
+        umma_commit(&p_empty[j % NP]);
       }
     }
     __syncwarp();
@@ -297,14 +306,22 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], x[c + e]);
         }
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * args.scale_log2;
-        // P.V(j-1) complete: P may be overwritten, O may be rescaled
-        mbar_wait(p_empty, (j & 1) ^ 1);
+        // P buffer j % NP is free once P.V(j - NP) has read it (NP = 1: P.V(j-1)
+        // has landed, so the O row may also be rescaled)
+        const int pb = j % NP;
+        mbar_wait(&p_empty[pb], static_cast<uint32_t>(((j / NP) & 1) ^ 1));
         tc_fence_after();
         const bool move = mx > m_run + kTau;
         if (__any_sync(0xffffffffu, move)) {
           const float mn = move ? mx : m_run;
           const float al = (m_run == -INFINITY) ? 0.f : fast_exp2(m_run - mn);
           if (t > 0) {
+            if (NP > 1) {
+              // rescale after P.V(j-1): o_full alternates by tile and
+              // P.V(j-3) is known complete, so the parity wait is unambiguous
+              mbar_wait(&o_full[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+              tc_fence_after();
+            }
             // O row *= al (rows that did not move use al = 1)
             const float a = move ? al : 1.f;
 #pragma unroll
@@ -329,7 +346,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         const float2 sl2 = make_float2(args.scale_log2, args.scale_log2);
         const float2 nmu2 = make_float2(-mu, -mu);
         float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
-        uint8_t* prow = smem + kOffP;
+        uint8_t* prow = smem + kOffP + pb * kQBytes;
 #pragma unroll
         for (int ch = 0; ch < 16; ++ch) {
           float p[8];
@@ -355,7 +372,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
+        if (lane == 0) mbar_arrive(&p_full[pb]);
         if (pend_u >= 0 && (t > 0 || t == nt - 1)) {
           // publish the previous unit's part once its stores have drained
           if (warp == kSmWarp0 && lane == 0) {
