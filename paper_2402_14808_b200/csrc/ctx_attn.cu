@@ -230,10 +230,12 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
     kf[6] = bf16_lo(kr[p].w); kf[7] = bf16_hi(kr[p].w);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      float s = 0.f;
+      // packed pairs: 4 FFMA2 + 1 FADD instead of 8 FFMA
+      float2 s2 = make_float2(qf[i][0] * kf[0], qf[i][1] * kf[1]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s = fmaf(qf[i][e], kf[e], s);
-      x[i][p] = s;
+      for (int e = 2; e < 8; e += 2)
+        s2 = ffma2(make_float2(qf[i][e], qf[i][e + 1]), make_float2(kf[e], kf[e + 1]), s2);
+      x[i][p] = s2.x + s2.y;
     }
     if (key0 + 2 * p + hw >= max_lim) vr[p] = make_uint4(0, 0, 0, 0);
   }
@@ -266,10 +268,13 @@ __device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[
     for (int p = 0; p < 8; ++p) {
       const float pr = fast_exp2(x[i][p] - mn);
       ps += pr;
-      a[0] = fmaf(pr, bf16_lo(vr[p].x), a[0]); a[1] = fmaf(pr, bf16_hi(vr[p].x), a[1]);
-      a[2] = fmaf(pr, bf16_lo(vr[p].y), a[2]); a[3] = fmaf(pr, bf16_hi(vr[p].y), a[3]);
-      a[4] = fmaf(pr, bf16_lo(vr[p].z), a[4]); a[5] = fmaf(pr, bf16_hi(vr[p].z), a[5]);
-      a[6] = fmaf(pr, bf16_lo(vr[p].w), a[6]); a[7] = fmaf(pr, bf16_hi(vr[p].w), a[7]);
+      const float2 pp = make_float2(pr, pr);
+      float2 a01 = ffma2(pp, make_float2(bf16_lo(vr[p].x), bf16_hi(vr[p].x)), make_float2(a[0], a[1]));
+      float2 a23 = ffma2(pp, make_float2(bf16_lo(vr[p].y), bf16_hi(vr[p].y)), make_float2(a[2], a[3]));
+      float2 a45 = ffma2(pp, make_float2(bf16_lo(vr[p].z), bf16_hi(vr[p].z)), make_float2(a[4], a[5]));
+      float2 a67 = ffma2(pp, make_float2(bf16_lo(vr[p].w), bf16_hi(vr[p].w)), make_float2(a[6], a[7]));
+      a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
+      a[4] = a45.x; a[5] = a45.y; a[6] = a67.x; a[7] = a67.y;
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) st.acc[i][e] = a[e];
