@@ -16,6 +16,7 @@ from paper_2402_14808_b200.plan import SysPlan
     (64, 32, 32, 4096, 148), (128, 32, 8, 32768, 148), (256, 64, 8, 65536, 148),
     (32, 7, 7, 8192, 148), (1, 1, 1, 1, 148), (32, 4, 4, 1000, 5),
     (64, 2, 2, 384, 3), (24, 8, 2, 300, 7),
+    (128, 32, 8, 32768, 82), (128, 32, 8, 32768, 64), (40, 8, 2, 300, 5), (64, 32, 32, 4096, 39),
 ])
 def test_plan_matches_c_and_covers_tiles(n_rows, hq, hkv, s, grid):
     p = SysPlan(n_rows, hq, hkv, s, grid)
@@ -107,3 +108,29 @@ def test_relay_sm_split():
         prev = g
     # no context at all: the system kernel takes every SM
     assert _lib.relay_sys_grid(32, 52, 52, 8192, 0, sms) == sms
+
+
+def test_plan_tile_sizes_and_aligned_split():
+    """nq: 16 / 32 for the swap-AB kernel, 128 (non-swapped kernel) from 128
+    rows per KV head; several q-tiles per head with fewer units than CTAs get
+    an equal number of CTAs per unit when that keeps >= 85% of them."""
+    assert SysPlan(16, 1, 1, 100, 148).nq == 16
+    assert SysPlan(127, 1, 1, 100, 148).nq == 32
+    assert SysPlan(128, 1, 1, 100, 148).nq == 128
+    c4 = SysPlan(128, 32, 8, 32768, 148)
+    assert (c4.nq, c4.n_qt, c4.n_units, c4.grid) == (128, 4, 32, 128)
+    ranges = c4.cta_ranges()
+    assert all((b - a) == c4.tpu // 4 and a % (c4.tpu // 4) == 0 for a, b in ranges)
+    assert SysPlan(128, 32, 8, 32768, 82).grid == 82      # 64 would drop 22% of the CTAs
+    c3 = SysPlan(64, 32, 32, 4096, 148)
+    assert (c3.nq, c3.n_qt, c3.n_units, c3.grid) == (32, 2, 64, 128)
+
+
+def test_relay_split_gqa_large_whole_units():
+    """The relay split gives the 128-row GQA kernel whole multiples of its
+    unit count (at least one CTA per unit)."""
+    sms = 148
+    g4 = _lib.relay_sys_grid(128, 32, 8, 32768, 128 * 512, sms)
+    assert g4 % 32 == 0 and 32 <= g4 <= sms
+    g5 = _lib.relay_sys_grid(256, 64, 8, 65536, 256 * 1024, sms)
+    assert g5 == 128
