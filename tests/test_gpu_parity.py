@@ -506,14 +506,15 @@ def test_append_rotated_decode_prologue(rb, oracle):
         assert (vv[c].float().cpu().numpy() == v[i]).all()
 
 
-def test_relay_step_gqa_large_vs_oracle(rb, oracle):
+@pytest.mark.parametrize("b,s", [(48, 900), (40, 100)])
+def test_relay_step_gqa_large_vs_oracle(rb, oracle, b, s):
     """The concurrent relay step with >= 128 rows per KV head (the non-swapped
     system kernel's parts fused in the context kernel) against the oracle,
-    and bitwise repeatable."""
+    and bitwise repeatable; s=100 gives one-tile units."""
     from paper_2402_14808_b200.attention import RelayDecodeStep
     from paper_2402_14808_b200.kvcache import SystemKvCache
-    rng = np.random.default_rng(77)
-    b, hq, hkv, s = 48, 8, 2, 900
+    rng = np.random.default_rng(77 + s)
+    hq, hkv = 8, 2
     lens = [int(x) for x in rng.integers(1, 160, size=b)]
     q = bf16(rng.standard_normal((b, hq, 128)))
     sk = bf16(rng.standard_normal((s, hkv, 128)))
