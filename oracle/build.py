@@ -25,7 +25,7 @@ REF_SRC = "/root/reference/pkg/src/relayserve"
 REF_MODULES = [
     ("__init__", ".py"), ("errors", ".py"), ("kernels", ".py"),
     ("numerics", ".py"), ("attention", ".py"), ("costmodel", ".py"),
-    ("_kernels_py", ".py"), ("_kernels_cy", ".pyx"),
+    ("_kernels_py", ".py"), ("_kernels_cy", ".pyx"), ("kvcache", ".py"),
 ]
 
 

@@ -76,6 +76,63 @@ class SystemKvCache:
             return t.to(device=device, dtype=torch.bfloat16).permute(1, 0, 2).contiguous()
         return cls([conv(k) for k in keys_shd], [conv(v) for v in values_shd], prompt_id)
 
+    # ---- the reference's on-disk format (RELAYKV, kvcache.py:19-20, 66-100):
+    # magic b"RELAYKV\0", little-endian uint32 version (1), layers, s, h, d,
+    # bits; then per layer the K tensor and the V tensor, (s, h, d) row-major
+    # little-endian IEEE floats of `bits` bits.
+    _MAGIC = b"RELAYKV\x00"
+    _VERSION = 1
+
+    @classmethod
+    def load(cls, path, device="cuda", prompt_id="system"):
+        """Read a file written by the reference's save_system_cache (or by
+        `save`) straight into GPU-resident bf16 [h][s][128] (head dims < 128
+        are zero-padded, which leaves attention exact)."""
+        import struct
+
+        import numpy as np
+        with open(path, "rb") as f:
+            if f.read(len(cls._MAGIC)) != cls._MAGIC:
+                raise ContractError(f"{path}: not a system KV cache file")
+            version, layers, s, h, d, bits = struct.unpack("<IIIIII", f.read(24))
+            if version != cls._VERSION:
+                raise ContractError(f"{path}: unsupported version {version}")
+            if bits not in (16, 32, 64):
+                raise ContractError(f"{path}: unsupported precision {bits} bits")
+            if d > HEAD_DIM or d < 1:
+                raise DimensionError(f"{path}: head_dim {d} unsupported (kernels take <= {HEAD_DIM})")
+            dtype = np.dtype(f"<f{bits // 8}")
+            count = s * h * d
+            keys, values = [], []
+            for _ in range(layers):
+                for out in (keys, values):
+                    raw = f.read(count * dtype.itemsize)
+                    if len(raw) != count * dtype.itemsize:
+                        raise ContractError(f"{path}: truncated")
+                    a = np.frombuffer(raw, dtype=dtype).astype(np.float32).reshape(s, h, d)
+                    t = torch.zeros((h, s, HEAD_DIM), dtype=torch.bfloat16, device=device)
+                    t[:, :, :d] = torch.from_numpy(a).to(device).permute(1, 0, 2).to(torch.bfloat16)
+                    out.append(t)
+        return cls(keys, values, prompt_id)
+
+    def save(self, path, head_dim=HEAD_DIM, bits=32):
+        """Write the reference's format (readable by its load_system_cache):
+        the first `head_dim` dims of each head, as IEEE floats of `bits` bits
+        (32 holds bf16 exactly)."""
+        import struct
+
+        import numpy as np
+        if bits not in (16, 32, 64):
+            raise ContractError(f"unsupported precision {bits} bits")
+        h, s, _ = self.keys[0].shape
+        header = self._MAGIC + struct.pack("<IIIIII", self._VERSION, self.layers, s, h, head_dim, bits)
+        with open(path, "wb") as f:
+            f.write(header)
+            for k, v in zip(self.keys, self.values):
+                for t in (k, v):
+                    a = t[:, :, :head_dim].permute(1, 0, 2).float().cpu().numpy()
+                    f.write(np.ascontiguousarray(a).astype(f"<f{bits // 8}").tobytes())
+
     @classmethod
     def random(cls, layers, kv_heads, s, device="cuda", generator=None, prompt_id="system"):
         keys = [torch.randn((kv_heads, s, HEAD_DIM), device=device, generator=generator,

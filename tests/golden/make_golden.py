@@ -125,6 +125,19 @@ def main():
     out["rope_apply_v"] = v8
     out["rope_apply_out"] = np.stack([numerics.rope_apply(v8, p) for p in (0, 1, 2, 1000)])
 
+    # RELAYKV system-cache files written by the reference (kvcache.py:66-82)
+    rng = np.random.default_rng(6)
+    ks = [rng.standard_normal((7, 3, 16)) for _ in range(2)]
+    vs = [rng.standard_normal((7, 3, 16)) for _ in range(2)]
+    for bits in (32, 16):
+        cache = kvcache.SystemKvCache(keys=tuple(k.astype(f"<f{bits // 8}") for k in ks),
+                                      values=tuple(v.astype(f"<f{bits // 8}") for v in vs),
+                                      system_len=7, prompt_id="golden")
+        kvcache.save_system_cache(cache, os.path.join(HERE, f"system_f{bits}.relaykv"))
+        back = kvcache.load_system_cache(os.path.join(HERE, f"system_f{bits}.relaykv"))
+        out[f"relaykv_f{bits}_keys"] = np.stack(back.keys)
+        out[f"relaykv_f{bits}_values"] = np.stack(back.values)
+
     path = os.path.join(HERE, "reference_golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {len(out)} arrays to {path} ({os.path.getsize(path)} bytes)")

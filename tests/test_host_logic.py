@@ -134,3 +134,70 @@ def test_relay_split_gqa_large_whole_units():
     assert g4 % 32 == 0 and 32 <= g4 <= sms
     g5 = _lib.relay_sys_grid(256, 64, 8, 65536, 256 * 1024, sms)
     assert g5 == 128
+
+
+def _bf16(x):
+    import torch
+    return torch.from_numpy(np.asarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("bits", [32, 16])
+def test_relaykv_load_reference_files(bits):
+    """SystemKvCache.load reads the reference's RELAYKV files
+    (save_system_cache, kvcache.py:66-82) into bf16 [h][s][128] (head dims
+    zero-padded past d), the same values the reference loads, bf16-rounded."""
+    import os
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    here = os.path.dirname(os.path.abspath(__file__))
+    g = np.load(os.path.join(here, "golden", "reference_golden.npz"))
+    cache = SystemKvCache.load(os.path.join(here, "golden", f"system_f{bits}.relaykv"), device="cpu")
+    assert (cache.layers, cache.kv_heads, cache.system_len) == (2, 3, 7)
+    for layer in range(2):
+        for got, ref in ((cache.keys[layer], g[f"relaykv_f{bits}_keys"][layer]),
+                         (cache.values[layer], g[f"relaykv_f{bits}_values"][layer])):
+            t = got.float().numpy()
+            assert (t[:, :, :16] == _bf16(ref).transpose(1, 0, 2)).all()
+            assert (t[:, :, 16:] == 0).all()
+
+
+def test_relaykv_round_trip_and_errors(tmp_path):
+    import torch
+    from paper_2402_14808_b200.errors import ContractError
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    g = torch.Generator().manual_seed(3)
+    cache = SystemKvCache.random(2, 4, 9, device="cpu", generator=g)
+    path = tmp_path / "c.relaykv"
+    cache.save(path)
+    back = SystemKvCache.load(path, device="cpu")
+    for a, b in zip(cache.keys + cache.values, back.keys + back.values):
+        assert torch.equal(a, b)
+    raw = path.read_bytes()
+    (tmp_path / "bad_magic").write_bytes(b"NOTRELAY" + raw[8:])
+    (tmp_path / "bad_version").write_bytes(raw[:8] + (7).to_bytes(4, "little") + raw[12:])
+    (tmp_path / "truncated").write_bytes(raw[:-4])
+    for name in ("bad_magic", "bad_version", "truncated"):
+        with pytest.raises(ContractError):
+            SystemKvCache.load(tmp_path / name, device="cpu")
+
+
+def test_relaykv_written_file_loads_in_reference(tmp_path):
+    """A file written by SystemKvCache.save is read back by the reference's
+    own load_system_cache (oracle/_ref, the compiled reference modules)."""
+    import os
+    import sys
+    import torch
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "relayserve")):
+        pytest.skip("oracle/_ref not built")
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    from relayserve import kvcache as ref_kvcache
+    g = torch.Generator().manual_seed(4)
+    cache = SystemKvCache.random(2, 3, 5, device="cpu", generator=g)
+    cache.save(tmp_path / "ours.relaykv")
+    ref = ref_kvcache.load_system_cache(tmp_path / "ours.relaykv")
+    assert ref.layers == 2 and ref.system_len == 5
+    for layer in range(2):
+        assert (ref.keys[layer] == cache.keys[layer].float().permute(1, 0, 2).numpy()).all()
+        assert (ref.values[layer] == cache.values[layer].float().permute(1, 0, 2).numpy()).all()
