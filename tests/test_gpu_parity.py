@@ -537,3 +537,28 @@ def test_relay_step_gqa_large_vs_oracle(rb, oracle, b, s):
             ref = oracle.attention_with_lse(q[r][None, None], fk[None], fv[None], causal=False)
             assert_close(out[r].cpu().numpy(), ref.output[0, 0], f"relay gqa-large row {r} grid {grid}")
             assert_close(lse[r].cpu().numpy(), ref.lse[0, 0], "relay gqa-large lse", lse=True)
+
+
+def test_relaykv_cache_feeds_system_kernel(rb, oracle):
+    """A reference-written RELAYKV file (d=16, float32) loaded straight to
+    the GPU layout drives the system kernel: zero-padded head dims keep the
+    attention exact against the oracle on the file's own values."""
+    import os
+    from paper_2402_14808_b200 import kernels
+    from paper_2402_14808_b200.kvcache import SystemKvCache
+    here = os.path.dirname(os.path.abspath(__file__))
+    cache = SystemKvCache.load(os.path.join(here, "golden", "system_f32.relaykv"))
+    g = np.load(os.path.join(here, "golden", "reference_golden.npz"))
+    rng = np.random.default_rng(12)
+    q16 = bf16(rng.standard_normal((5, 3, 16)))
+    q = np.zeros((5, 3, 128))
+    q[:, :, :16] = q16
+    o, lse = kernels.system_attention(dev_bf16(q), cache.keys[1], cache.values[1], kv_layout="hsd",
+                                      scale=16 ** -0.5)
+    torch.cuda.synchronize()
+    k = bf16(g["relaykv_f32_keys"][1])
+    v = bf16(g["relaykv_f32_values"][1])
+    ref = oracle.attention_with_lse(q16[None], k[None], v[None], causal=False)
+    assert_close(o.cpu().numpy()[:, :, :16], ref.output[0], "relaykv sys o")
+    assert np.abs(o.cpu().numpy()[:, :, 16:]).max() == 0
+    assert_close(lse.cpu().numpy(), ref.lse[0], "relaykv sys lse", lse=True)
