@@ -97,3 +97,46 @@ class DecodeShape:
     def shard(self, hkv_local, hq_local):
         return DecodeShape(self.b, hq_local, hkv_local, self.s, self.ctx_total, self.d, self.e,
                            self.m)
+
+
+# ---------------------------------------------------------------- hardware
+@dataclass(frozen=True)
+class HardwareProfile:
+    """Bandwidth / compute envelope of one accelerator (costmodel.py:21-33)."""
+
+    name: str
+    mem_bandwidth: float  # bytes / s
+    peak_flops: float     # flop / s
+    bytes_per_element: int = 2
+
+    def __post_init__(self):
+        if min(self.mem_bandwidth, self.peak_flops, self.bytes_per_element) <= 0:
+            raise ContractError(f"profile fields must be positive: {self}")
+
+
+# The reference's profiles (costmodel.py:36-40) plus B200 at the measured
+# copy bandwidth and dense bf16 throughput of this pool (MEASURED_PEAKS.json).
+HARDWARE_PROFILES = {
+    "A40": HardwareProfile("A40", 696e9, 37.4e12),
+    "A100-PCIE-40GB": HardwareProfile("A100-PCIE-40GB", 1555e9, 77.9e12),
+    "A100-SXM4-80GB": HardwareProfile("A100-SXM4-80GB", 2039e9, 77.9e12),
+    "B200": HardwareProfile("B200", 6539.9e9, 1647.2e12),
+}
+
+# Measured cost of this repository's relay decode step on one B200 (one
+# layer, CUDA-graph replay, L2 flushed; profiles/r01g/r01g_bench.json): above
+# ~2k prefix tokens the step is an affine function of its algorithmic bytes,
+# t = B200_STEP_FIXED_S + B_alg / B200_STEP_MARGINAL_BPS (fit through the
+# s = 8k and 32k points: 21.1 us + 6.9 TB/s); below, a latency floor.
+B200_STEP_FIXED_S = 21.1e-6
+B200_STEP_MARGINAL_BPS = 6.9e12
+B200_STEP_FLOOR_S = 45.0e-6
+
+
+def b200_relay_step_seconds(shape: "DecodeShape") -> float:
+    """Measured-model wall time of one HBM-bound relay decode step (for the
+    engine's step-cost hook, engine.py:77-85); tensor-bound shapes (large GQA
+    batches) are bounded below by their roofline at the measured peaks."""
+    prof = HARDWARE_PROFILES["B200"]
+    t = B200_STEP_FIXED_S + shape.bytes_alg / B200_STEP_MARGINAL_BPS
+    return max(B200_STEP_FLOOR_S, t, shape.roofline_s(prof.mem_bandwidth, prof.peak_flops))

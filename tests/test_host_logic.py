@@ -201,3 +201,16 @@ def test_relaykv_written_file_loads_in_reference(tmp_path):
     for layer in range(2):
         assert (ref.keys[layer] == cache.keys[layer].float().permute(1, 0, 2).numpy()).all()
         assert (ref.values[layer] == cache.values[layer].float().permute(1, 0, 2).numpy()).all()
+
+
+def test_b200_profile_and_step_model():
+    """B200 HardwareProfile and the measured step model reproduce the
+    round's measured C2 sweep within 10% for s >= 2k."""
+    from paper_2402_14808_b200.errors import ContractError
+    assert costmodel.HARDWARE_PROFILES["B200"].mem_bandwidth == 6539.9e9
+    with pytest.raises(ContractError):
+        costmodel.HardwareProfile("bad", 0, 1)
+    measured = {2048: 46.4e-6, 4096: 53.7e-6, 8192: 68.7e-6, 16384: 100.6e-6, 32768: 163.5e-6}
+    for s, t in measured.items():
+        sh = costmodel.DecodeShape(b=32, hq=52, hkv=52, s=s, ctx_total=32 * 128)
+        assert abs(costmodel.b200_relay_step_seconds(sh) - t) / t < 0.10
