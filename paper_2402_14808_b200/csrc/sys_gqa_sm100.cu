@@ -39,6 +39,9 @@ constexpr int kTile = RB_KEY_TILE * RB_HEAD_DIM * 2;  // 32 KB K or V tile
 #ifndef GQA_NP
 #define GQA_NP 1
 #endif
+#ifndef GQA_EXP_EARLY
+#define GQA_EXP_EARLY 1
+#endif
 constexpr int KS = GQA_KS, VS = GQA_VS;
 constexpr int NP = GQA_NP;                 // P buffers (1: P.V(j-1) gates the softmax of tile j)
 constexpr int kQBytes = kRows * 256;       // [2 kblocks][128 rows][128 B]
@@ -306,6 +309,61 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], x[c + e]);
         }
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * args.scale_log2;
+#if GQA_EXP_EARLY
+        // probabilities first (packed bf16 in registers), with the reference
+        // the row will have after this tile: the exponentials overlap the
+        // P.V(j-1) that the P buffer and the O rescale must wait for
+        const bool move = mx > m_run + kTau;
+        const float m_new = move ? mx : m_run;
+        const float al = (!move || m_run == -INFINITY) ? (move ? 0.f : 1.f) : fast_exp2(m_run - m_new);
+        const float mu = (m_new == -INFINITY) ? 0.f : m_new;
+        const float2 sl2 = make_float2(args.scale_log2, args.scale_log2);
+        const float2 nmu2 = make_float2(-mu, -mu);
+        float2 l2a = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
+        uint32_t pk32[64];
+#pragma unroll
+        for (int e = 0; e < 128; e += 2) {
+          const float2 a2 = ffma2(make_float2(x[e], x[e + 1]), sl2, nmu2);
+          const float p0 = fast_exp2(a2.x), p1 = fast_exp2(a2.y);
+          if (e & 2)
+            l2b = fadd2(l2b, make_float2(p0, p1));
+          else
+            l2a = fadd2(l2a, make_float2(p0, p1));
+          pk32[e >> 1] = pack_bf16x2(p0, p1);
+        }
+        const int pb = j % NP;
+        mbar_wait(&p_empty[pb], static_cast<uint32_t>(((j / NP) & 1) ^ 1));
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, move) && t > 0) {
+          if (NP > 1) {
+            mbar_wait(&o_full[(j - 1) & 1], static_cast<uint32_t>(((j - 1) >> 1) & 1));
+            tc_fence_after();
+          }
+          // O row *= al (al = 1 for rows that did not move)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tmem_ld_32x32b<32>(o_addr + c * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= al;
+            tmem_st_32x32b<32>(o_addr + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+        l_run *= al;
+        m_run = m_new;
+        uint8_t* prow = smem + kOffP + pb * kQBytes;
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          uint4 pk;
+          pk.x = pk32[ch * 4 + 0];
+          pk.y = pk32[ch * 4 + 1];
+          pk.z = pk32[ch * 4 + 2];
+          pk.w = pk32[ch * 4 + 3];
+          *reinterpret_cast<uint4*>(prow + (ch >> 3) * (kRows * 128) + sw128_offset(r, (ch & 7) * 8)) = pk;
+        }
+#else
         // P buffer j % NP is free once P.V(j - NP) has read it (NP = 1: P.V(j-1)
         // has landed, so the O row may also be rescaled)
         const int pb = j % NP;
@@ -367,6 +425,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           pk.w = pack_bf16x2(p[6], p[7]);
           *reinterpret_cast<uint4*>(prow + (ch >> 3) * (kRows * 128) + sw128_offset(r, (ch & 7) * 8)) = pk;
         }
+#endif
         const float ls = (l2a.x + l2a.y) + (l2b.x + l2b.y);
         l_run += ls;
         fence_proxy_async_smem();
