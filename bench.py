@@ -9,13 +9,22 @@ configs[1]: Llama-30B attention shape (52 heads, d=128), batch 32, context
 128, system prompt swept 512..32k; the headline `value` is s=8192 (the top of
 configs[1]'s sweep).  One step = one relay decode step of one layer: the
 tcgen05 system kernel over the shared prefix + the paged context kernel with
-the fused relay epilogue.  Inputs are synthetic (seeded normal bf16), resident
-in HBM; L2 (126 MB) is flushed between timed steps (write a 2x-L2 buffer, then
-read another so the write-back happens outside the timed region).
+the fused relay epilogue.  Inputs are synthetic (seeded normal bf16, one
+generator per KV head), resident in HBM; L2 (126 MB) is flushed between timed
+steps (write a 2x-L2 buffer, then read another so the write-back happens
+outside the timed region).  `value` is the CUDA-graph replay of the step
+(eager launches reported beside it); `e2e` the CUDA-graph replay of the
+host-buffer step (pinned H2D + paged append + step + D2H).
+
+The other BASELINE configs are timed in the same run under `configs`:
+C4 (Llama-3-8B GQA, b=128, s=32k, c=512), C5 (Llama-2-70B GQA, b=256,
+s=64k, c=1k), each with its roofline max(B_alg/BW, F_sys/P_tc).
 
 N > 1 (torchrun): KV heads are sharded across ranks (52 -> 7,7,7,7,6,6,6,6 at
-N=8); each rank runs the same step on its heads, no collective in the timed
-region; the step time is the max over ranks (fixed total work: "strong").
+N=8; C4/C5: one KV head per rank at N=8); each rank runs the same step on its
+heads, no collective in the timed region; step time = max over ranks (fixed
+total work: "strong").  After timing, the sharded output is all-gathered
+(NCCL) and compared bitwise with the unsharded step computed on rank 0.
 
 --impl reference times the reference's own CPU implementation (the
 unmodified relayserve modules compiled into oracle/_ref by oracle/build.py,
@@ -26,8 +35,8 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -41,6 +50,20 @@ HEADLINE_S = 8192
 SWEEP = (512, 1024, 2048, 4096, 8192, 16384, 32768)
 BLOCK = 16
 METRIC = "decode attention µs/step & HBM GB/s vs sys-prompt length (B=32), 1/2/4/8 B200"
+# BASELINE.json configs[3], configs[4] (one decode layer each)
+OTHER = {
+    "C4": dict(b=128, hq=32, hkv=8, s=32768, c=512,
+               label="C4 Llama-3-8B GQA (configs[3]): b=128, 32q/8kv, s=32768, c=512"),
+    "C5": dict(b=256, hq=64, hkv=8, s=65536, c=1024,
+               label="C5 Llama-2-70B GQA (configs[4]): b=256, 64q/8kv, s=65536, c=1024"),
+}
+PARITY_HEADS = (0, 17, 34, 51)   # KV heads the CPU reference sample and parity check use
+
+
+def workload_label(s):
+    """config.workload of both arms (identical strings)."""
+    return (f"C2 Llama-30B attention shape (configs[1]): b={B}, H={H}, d={D}, c={C}, s={s}, "
+            f"paged block {BLOCK}")
 
 
 def parse():
@@ -51,6 +74,7 @@ def parse():
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--s", type=int, default=HEADLINE_S)
     p.add_argument("--sweep", type=str, default=",".join(map(str, SWEEP)))
+    p.add_argument("--configs", type=str, default="C4,C5")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU sampling")
     return p.parse_args()
@@ -61,6 +85,18 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def host_cpu():
+    model = platform.processor() or "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"lscpu_model": model, "logical_cpus": os.cpu_count()}
 
 
 # ------------------------------------------------------------ measurement
@@ -150,9 +186,10 @@ def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1663.8)), "measured"
+        return (float(p["hbm_gbs"]), float(p.get("bf16_tflops", 1647.2)),
+                float(p.get("bf16_tflops_sustained", 1392.3)), "measured")
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, 1400.0, "fallback"
 
 
 def ncu_traffic(kernels, s):
@@ -169,38 +206,39 @@ def ncu_traffic(kernels, s):
 
 # ---------------------------------------------------------------- workload
 
-def build(torch, s, heads, device, seed=1234):
-    """Per-head seeded synthetic C2 workload for the given global KV heads, so
-    a sharded run holds exactly the unsharded run's data for its heads."""
-    from paper_2402_14808_b200.attention import NaiveDecodeStep, RelayDecodeStep
+def build_workload(torch, b, hq, hkv, s, lens, kv_heads, device, seed=1234, layers=1):
+    """Seeded synthetic decode workload holding the given global KV heads
+    (and their g query heads): one generator per (layer, KV head), so a
+    sharded run holds exactly the unsharded run's data for its heads.
+    Returns (q, SystemKvCache, PagedKvCache, block_table, ctx_lens)."""
     from paper_2402_14808_b200.kvcache import PagedKvCache, SystemKvCache
-    nh = len(heads)
-    g = torch.Generator(device=device)
-    sk = torch.empty((nh, s, D), dtype=torch.bfloat16, device=device)
-    sv = torch.empty_like(sk)
-    nblk = B * C // BLOCK
-    paged = PagedKvCache(1, nh, nblk, BLOCK, device=device)
-    q = torch.empty((B, nh, D), dtype=torch.bfloat16, device=device)
-    for i, hg in enumerate(heads):
-        g.manual_seed(seed * 1000003 + hg)
-        sk[i] = torch.randn((s, D), generator=g, device=device)
-        sv[i] = torch.randn((s, D), generator=g, device=device)
-        paged.k_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
-        paged.v_pool[0, :, i] = torch.randn((nblk, BLOCK, D), generator=g, device=device)
-        q[:, i] = torch.randn((B, D), generator=g, device=device)
+    g = hq // hkv
+    nh = len(kv_heads)
+    gen = torch.Generator(device=device)
+    nblk = sum(-(-c // BLOCK) for c in lens)
+    paged = PagedKvCache(layers, nh, nblk, BLOCK, device=device)
+    keys, values = [], []
+    q = torch.empty((b, nh * g, D), dtype=torch.bfloat16, device=device)
+    for layer in range(layers):
+        sk = torch.empty((nh, s, D), dtype=torch.bfloat16, device=device)
+        sv = torch.empty_like(sk)
+        for i, hg in enumerate(kv_heads):
+            gen.manual_seed((seed * 1000003 + hg) * 131 + layer)
+            sk[i] = torch.randn((s, D), generator=gen, device=device)
+            sv[i] = torch.randn((s, D), generator=gen, device=device)
+            paged.k_pool[layer, :, i] = torch.randn((nblk, BLOCK, D), generator=gen, device=device)
+            paged.v_pool[layer, :, i] = torch.randn((nblk, BLOCK, D), generator=gen, device=device)
+            if layer == 0:
+                q[:, i * g:(i + 1) * g] = torch.randn((b, g, D), generator=gen, device=device)
+        keys.append(sk)
+        values.append(sv)
     # shuffled physical blocks, as a real paged allocator would hand out
-    perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(seed)).tolist()
-    paged.pool._free = perm[::-1]
-    for r in range(B):
+    paged.allocator.shuffle(seed)
+    for r, c in enumerate(lens):
         paged.register(r)
-        paged.pool.grow(r, C)
-        paged._layer_lengths[r][0] = C
-    ids = list(range(B))
-    bt, cl = paged.block_table(ids), paged.context_lens(ids)
-    sys_cache = SystemKvCache([sk], [sv])
-    relay = RelayDecodeStep(sys_cache, paged, bt, cl, hq=nh)
-    naive = NaiveDecodeStep(sys_cache, paged, bt, cl, hq=nh)
-    return q, relay, naive, paged, bt
+        paged.extend(r, c)
+    ids = list(range(b))
+    return q, SystemKvCache(keys, values), paged, paged.block_table(ids), paged.context_lens(ids)
 
 
 def graph_of(torch, fn):
@@ -254,21 +292,49 @@ def _cpu_worker(args):
     return time.perf_counter() - t0
 
 
-def cpu_baseline_sample(s, budget):
-    """Reference relay step on 1 core over a head subsample, best-of-N within
-    `budget` seconds, extrapolated linearly in heads (heads are independent
-    and identical work, attention.py:122-133)."""
+def cpu_leg(torch, q, sys_cache, paged, out, lse, budget):
+    """cpu_baseline of the N=1 line, on the GPU run's own inputs: the
+    reference relay step (oracle/_ref, float64, 1 core) over the sampled KV
+    heads, best-of-N within `budget` seconds, extrapolated linearly in heads
+    (heads are independent and identical work, attention.py:122-133) -- and,
+    on the same sample, the GPU step's output / fused LSE against the float64
+    oracle (the checker; parity of the bench line)."""
+    import numpy as np
+    from oracle import relay_oracle as orc
+    heads = [h for h in PARITY_HEADS if h < sys_cache.kv_heads]
+    qn = q.float().cpu().numpy()[:, None][:, :, heads].astype(np.float64)
+    sk = sys_cache.keys[0].float().cpu().numpy()[heads].transpose(1, 0, 2).astype(np.float64)
+    sv = sys_cache.values[0].float().cpu().numpy()[heads].transpose(1, 0, 2).astype(np.float64)
+    ck, cv = [], []
+    for r in range(q.shape[0]):
+        k_r, v_r = paged.gather(r, 0)
+        ck.append(k_r.float().cpu().numpy()[:, heads].astype(np.float64))
+        cv.append(v_r.float().cpu().numpy()[:, heads].astype(np.float64))
+    ref_o, ref_l = orc.relay_attention(qn, sk, sv, ck, cv, return_lse=True)
+    got_o = out.float().cpu().numpy()[:, heads]
+    got_l = lse.float().cpu().numpy()[:, heads]
+    d = got_o - ref_o[:, 0]
+    parity = {"o_max_abs": float(np.abs(d).max()),
+              "o_rel": float(np.linalg.norm(d) / np.linalg.norm(ref_o)),
+              "lse_max_abs": float(np.abs(got_l - ref_l[:, 0]).max()),
+              "heads": heads, "rows": int(q.shape[0]),
+              "oracle": "float64 C restatement of the reference (oracle/relay_oracle), "
+                        "same bf16 inputs",
+              "tolerance": {"o_max_abs": 1.5e-2, "o_rel": 5e-3, "lse_max_abs": 1e-3}}
     att, kind = _ref_modules()
-    nh = 4
-    _CPU["att"], _CPU["data"] = att, _cpu_data(s, nh)
-    best, reps, t_start = float("inf"), 0, time.perf_counter()
-    while reps < 5 and (reps < 1 or time.perf_counter() - t_start < budget):
-        best = min(best, _cpu_worker((0, nh)))
+    best, reps, t0 = float("inf"), 0, time.perf_counter()
+    while reps < 5 and (reps < 1 or time.perf_counter() - t0 < budget):
+        t1 = time.perf_counter()
+        att.relay_attention(qn, sk, sv, ck, cv)
+        best = min(best, time.perf_counter() - t1)
         reps += 1
-    us = best * 1e6 * H / nh
-    return {"value": us, "unit": "µs/step", "cores": 1, "kind": kind,
-            "sample": (f"relay_attention b={B} s={s} c={C} d={D}, {nh} of {H} heads, best of "
-                       f"{reps} on 1 core, float64, extrapolated x{H / nh:g} to all heads")}
+    nh = len(heads)
+    cpu = {"value": best * 1e6 * H / nh, "unit": "µs/step", "cores": 1, "kind": kind,
+           "sample": (f"relay_attention on the GPU run's own bf16 inputs (b={B}, "
+                      f"s={sys_cache.system_len}, c={C}, d={D}), {nh} of {H} heads, best of "
+                      f"{reps} on 1 core, float64, extrapolated x{H / nh:g} to all heads"),
+           "host": host_cpu()}
+    return cpu, parity
 
 
 def run_reference(args):
@@ -297,11 +363,10 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded normal)",
-            "config": {"workload": f"C2 Llama-30B attention shape, b={B}, H={H}, d={D}, "
-                                   f"c={C}, s={args.s}", "global_batch": B, "seq_len": args.s,
+            "config": {"workload": workload_label(args.s), "global_batch": B, "seq_len": args.s,
                        "parallelism": f"host processes x{procs}"},
             "cpu_baseline": {"value": us, "unit": "µs/step", "cores": procs, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "host": host_cpu()},
             "e2e": {"value": us, "unit": "µs/step", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -330,52 +395,44 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=device)
         barrier = dist.barrier
     from paper_2402_14808_b200 import _lib, kernels, sharding
+    from paper_2402_14808_b200.attention import NaiveDecodeStep, RelayDecodeStep
     from paper_2402_14808_b200.costmodel import DecodeShape
     _lib.load()
     ka, kb, _, _ = sharding.local_heads(H, H, world, rank)
     heads = list(range(ka, kb))
     flush = make_flush(torch, device)
-    hbm, tc, peak_kind = measured_peaks()
+    hbm, tc_burst, tc_sus, peak_kind = measured_peaks()
 
-    def step_stats(s, with_naive=True, with_split=False, with_e2e=False, graph=True):
-        q, relay, naive, paged, bt = build(torch, s, heads, device)
-        fn_relay = lambda: relay(q)  # noqa: E731
-        res = {}
-        eager = time_loop(torch, fn_relay, args.steps, args.warmup, flush, barrier)
-        res["eager_ms"] = statistics.mean(eager)
-        if graph:
-            gr = graph_of(torch, fn_relay)
-            gms = time_loop(torch, gr.replay, args.steps, args.warmup, flush, barrier)
-            res["graph_ms"] = statistics.mean(gms)
-        res["ms"] = min(res["eager_ms"], res.get("graph_ms", float("inf")))
-        if with_naive:
-            res["naive_ms"] = statistics.mean(
-                time_loop(torch, lambda: naive(q), max(3, args.steps // 5), 2, flush, barrier))
-        if with_split:
+    def timed(fn, steps=None):
+        return time_loop(torch, fn, steps or args.steps, args.warmup, flush, barrier)
+
+    def c2_step(s, full=False):
+        q, sc, paged, bt, cl = build_workload(torch, B, H, H, s, [C] * B, heads, device)
+        relay = RelayDecodeStep(sc, paged, bt, cl, hq=len(heads))
+        res = {"plan": relay.plan, "sys_grid": relay.grid}
+        gr = graph_of(torch, lambda: relay(q))
+        res["graph_ms"] = statistics.mean(timed(gr.replay))
+        naive = NaiveDecodeStep(sc, paged, bt, cl, hq=len(heads))
+        res["naive_ms"] = statistics.mean(time_loop(torch, lambda: naive(q), max(3, args.steps // 5),
+                                                    2, flush, barrier))
+        out_r, lse_r = [t.clone() for t in relay(q)]
+        out_n = naive(q)[0]
+        torch.cuda.synchronize()
+        res["relay_vs_naive_max_abs"] = float((out_r.float() - out_n.float()).abs().max())
+        if full:
+            res["eager_ms"] = statistics.mean(timed(lambda: relay(q)))
             # each kernel alone on every SM (the step runs them concurrently
             # on a byte-proportional SM split)
-            from paper_2402_14808_b200.attention import RelayDecodeStep
-            alone = RelayDecodeStep(relay.sys_cache, paged, bt, relay.ctx_lens, len(heads),
-                                    grid=kernels.sm_count(device))
-            res["sys_ms"] = statistics.mean(
-                time_loop(torch, lambda: alone.system(q), args.steps, args.warmup, flush, barrier))
-            res["ctx_ms"] = statistics.mean(
-                time_loop(torch, lambda: alone.context(q), args.steps, args.warmup, flush, barrier))
-            res["sys_grid"] = relay.grid
+            alone = RelayDecodeStep(sc, paged, bt, cl, len(heads), grid=kernels.sm_count(device))
+            res["sys_ms"] = statistics.mean(timed(lambda: alone.system(q)))
+            res["ctx_ms"] = statistics.mean(timed(lambda: alone.context(q)))
             del alone
-        if with_e2e:
-            res.update(e2e_stats(q, relay, paged, bt))
-        # size-independent parity: relay == naive per-request kernel
-        out_r = relay(q)[0].float()
-        out_n = naive(q)[0].float()
-        torch.cuda.synchronize()
-        res["parity_max_abs_vs_naive"] = float((out_r - out_n).abs().max())
-        res["plan"] = relay.plan
-        del q, relay, naive, paged
-        torch.cuda.empty_cache()
+            res.update(e2e_stats(q, relay, bt))
+            res["objs"] = (q, sc, paged, out_r, lse_r)
+        del relay, naive, gr
         return res
 
-    def e2e_stats(q, relay, paged, bt):
+    def e2e_stats(q, relay, bt):
         """Public-API decode step with host buffers: one H2D of this step's
         q / new-token k / v from pinned memory, paged append, relay step, D2H
         of the output -- all inside the events (RelayDecodeStep.host_step_graph,
@@ -390,30 +447,49 @@ def run_b200(args):
         slots = torch.tensor([int(btc[r, (C - 1) // BLOCK]) * BLOCK + (C - 1) % BLOCK
                               for r in range(B)], dtype=torch.int32, device=device)
         eager = lambda: relay.step_host(qkv_h[0], qkv_h[1], qkv_h[2], slots, out_h)  # noqa: E731
-        ms_eager = time_loop(torch, eager, args.steps, args.warmup, flush, barrier)
+        ms_eager = timed(eager)
         replay = relay.host_step_graph(qkv_h, slots, out_h)
-        ms = time_loop(torch, replay, args.steps, args.warmup, flush, barrier)
-        return {"e2e_ms": min(statistics.mean(ms), statistics.mean(ms_eager)),
-                "e2e_eager_ms": statistics.mean(ms_eager), "e2e_graph_ms": statistics.mean(ms),
+        ms = timed(replay)
+        return {"e2e_graph_ms": statistics.mean(ms), "e2e_eager_ms": statistics.mean(ms_eager),
                 "h2d": qkv_h.numel() * 2, "d2h": out_h.numel() * 2}
+
+    def other_config(name):
+        cfg = OTHER[name]
+        b, hq, hkv, s, c = cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], cfg["c"]
+        a, bb, _, _ = sharding.local_heads(hkv, hq, world, rank)
+        kvh = list(range(a, bb))
+        g = hq // hkv
+        q, sc, paged, bt, cl = build_workload(torch, b, hq, hkv, s, [c] * b, kvh, device, seed=77)
+        relay = RelayDecodeStep(sc, paged, bt, cl, hq=len(kvh) * g)
+        gr = graph_of(torch, lambda: relay(q))
+        ms = statistics.mean(timed(gr.replay, max(5, args.steps // 2)))
+        shp = DecodeShape(b, len(kvh) * g, len(kvh), s, b * c)
+        res = {"label": cfg["label"], "kv_heads_per_rank": len(kvh), "plan": relay.plan,
+               "sys_grid": relay.grid, "ms": ms, "bytes_alg_per_rank": shp.bytes_alg,
+               "flops_sys_per_rank": shp.flops_sys}
+        del relay, gr, q, sc, paged
+        torch.cuda.empty_cache()
+        return res
 
     clocks = ClockSampler(local)
     t_wall = time.perf_counter()
-    head = step_stats(args.s, with_split=True, with_e2e=True)
+    head = c2_step(args.s, full=True)
+    cpu = parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        q, sc, paged, out_r, lse_r = head["objs"]
+        cpu, parity = cpu_leg(torch, q, sc, paged, out_r, lse_r, args.cpu_budget)
+    head.pop("objs")
+    torch.cuda.empty_cache()
     sweep = []
-    if args.sweep:
-        for s in [int(x) for x in args.sweep.split(",") if x.strip()]:
-            if s == args.s:
-                st = head
-            else:
-                st = step_stats(s, graph=True)
-            shp = DecodeShape(B, len(heads), len(heads), s, B * C)
-            sweep.append({"s": s, "us_per_step": st["ms"] * 1e3,
-                          "naive_us_per_step": st.get("naive_ms", float("nan")) * 1e3,
-                          "hbm_gbs": shp.bytes_alg / (st["ms"] * 1e-3) / 1e9,
-                          "frac_of_hbm_roofline": (shp.bytes_alg / (hbm * 1e9)) / (st["ms"] * 1e-3),
-                          "naive_bytes_over_relay": shp.bytes_naive / shp.bytes_alg,
-                          "parity_max_abs_vs_naive": st["parity_max_abs_vs_naive"]})
+    for s in [int(x) for x in args.sweep.split(",") if x.strip()]:
+        st = head if s == args.s else c2_step(s)
+        torch.cuda.empty_cache()
+        shp = DecodeShape(B, len(heads), len(heads), s, B * C)
+        sweep.append({"s": s, "us_per_step": st["graph_ms"] * 1e3,
+                      "naive_us_per_step": st["naive_ms"] * 1e3,
+                      "bytes_alg_per_rank": shp.bytes_alg,
+                      "relay_vs_naive_max_abs": st["relay_vs_naive_max_abs"]})
+    others = {name: other_config(name) for name in [x for x in args.configs.split(",") if x]}
     clk = clocks.stop()
     wall = time.perf_counter() - t_wall
 
@@ -424,59 +500,84 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    ms = maxr(head["ms"])
+    ms = maxr(head["graph_ms"])
     sys_ms, ctx_ms = maxr(head["sys_ms"]), maxr(head["ctx_ms"])
-    e2e_ms = maxr(head["e2e_ms"])
+    e2e_ms = maxr(head["e2e_graph_ms"])
     for row in sweep:
         row["us_per_step"] = maxr(row["us_per_step"])
         row["naive_us_per_step"] = maxr(row["naive_us_per_step"])
+        full = DecodeShape(B, H, H, row["s"], B * C)
+        t = row["us_per_step"] * 1e-6
+        row["hbm_gbs"] = full.bytes_alg / t / 1e9           # whole job over the slowest rank
+        row["frac_of_hbm_roofline"] = full.bytes_alg / (world * hbm * 1e9) / t
+        row["naive_bytes_over_relay"] = full.bytes_naive / full.bytes_alg
+    for name, r in others.items():
+        r["us_per_step"] = maxr(r["ms"]) * 1e3
+        cfg = OTHER[name]
+        full = DecodeShape(cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], cfg["b"] * cfg["c"])
+        t = r["us_per_step"] * 1e-6
+        t_hbm = full.bytes_alg / (world * hbm * 1e9)
+        t_tc = full.flops_sys / (world * tc_sus * 1e12)
+        r.update({"bytes_alg": full.bytes_alg, "flops_sys": full.flops_sys,
+                  "roofline_us": max(t_hbm, t_tc) * 1e6, "frac_of_roofline": max(t_hbm, t_tc) / t,
+                  "bound": "tensor" if t_tc > t_hbm else "hbm",
+                  "sys_tflops": full.flops_sys / t / 1e12, "tokens_per_s": cfg["b"] / t,
+                  "peaks": f"HBM {hbm} GB/s, bf16 {tc_sus} TF/s sustained ({peak_kind}), x{world} GPUs"})
+        r.pop("ms")
 
     # end-to-end check of the sharded path: all-gather the per-rank outputs
-    gathered_ok = None
+    # and compare bitwise with the unsharded step (rank 0).  Both sides cut
+    # every system unit at the same key tiles (k CTAs per unit), the
+    # condition for bitwise equality (tests/test_gpu_sharding.py).
+    sharded_equal = None
     if world > 1:
-        q, relay, _, _, _ = build(torch, 1024, heads, device)
-        out, _ = relay(q)
+        s_chk, k_unit = 1024, 2
+        q, sc, paged, bt, cl = build_workload(torch, B, H, H, s_chk, [C] * B, heads, device)
+        n_units = _lib.sys_plan(B, len(heads), len(heads), s_chk, 148)[0]["n_units"]
+        out, _ = RelayDecodeStep(sc, paged, bt, cl, len(heads), grid=k_unit * n_units)(q)
+        torch.cuda.synchronize()
         full = sharding.gather_heads(out.cpu() if same_gpu else out, H, H)
-        gathered_ok = bool(full.shape == (B, H, D) and torch.isfinite(full.float()).all())
-        del q, relay
+        if rank == 0:
+            q, sc, paged, bt, cl = build_workload(torch, B, H, H, s_chk, [C] * B, list(range(H)),
+                                                  device)
+            n_all = _lib.sys_plan(B, H, H, s_chk, 148)[0]["n_units"]
+            ref, _ = RelayDecodeStep(sc, paged, bt, cl, H, grid=k_unit * n_all)(q)
+            torch.cuda.synchronize()
+            sharded_equal = bool(torch.equal(full.to(ref.device), ref))
+        del q, sc, paged
 
     if rank != 0:
         dist.destroy_process_group()
         return 0
 
     shape = DecodeShape(B, H, H, args.s, B * C)
+    step_bytes_local = DecodeShape(B, len(heads), len(heads), args.s, B * C).bytes_alg
     sys_bytes_local = 2 * 2 * len(heads) * D * args.s + 2 * B * len(heads) * D
     # roofline of the step: the system and context kernels stream
     # concurrently on disjoint SMs, so the bound is the whole step's
-    # algorithmic bytes over the step time
-    step_bytes_local = DecodeShape(B, len(heads), len(heads), args.s, B * C).bytes_alg
+    # algorithmic bytes (this rank's share) over the step time
     achieved = step_bytes_local / (ms * 1e-3) / 1e9
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(args.s, args.cpu_budget)
     value_us = ms * 1e3
-    launches = 2  # system and context kernels per step (relay fusion runs inside them)
     line = {
         "metric": METRIC, "value": value_us, "unit": "µs/step", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded normal), inputs resident in HBM",
-        "config": {"workload": (f"C2 Llama-30B attention shape (configs[1]): b={B}, H={H}, "
-                                f"d={D}, c={C}, s={args.s}, paged block {BLOCK}"),
+        "config": {"workload": workload_label(args.s),
                    "global_batch": B, "seq_len": args.s,
                    "parallelism": f"kv-head-shard{world}" if world > 1 else "single-gpu",
                    "l2": "flushed between timed steps: write a 2x-L2 buffer, then read another 2x-L2 buffer (evicts inputs, write-back outside the timed region)",
-                   "timing": "CUDA-graph replay of the 2-kernel step" if head.get("graph_ms", 1e9) <= head["eager_ms"] else "eager launches",
+                   "timing": "value = CUDA-graph replay of the 2-kernel step (the serving path); eager launches in eager_us_per_step",
                    "sys_sm_split": head["sys_grid"]},
         "tokens_per_s": B / (ms * 1e-3),
         "hbm_gbs": shape.bytes_alg / (ms * 1e-3) / 1e9,
-        "frac_of_hbm_roofline": (shape.bytes_alg / (hbm * 1e9)) / (ms * 1e-3),
+        "frac_of_hbm_roofline": shape.bytes_alg / (world * hbm * 1e9) / (ms * 1e-3),
         "bytes_alg": shape.bytes_alg, "bytes_naive": shape.bytes_naive,
         "eager_us_per_step": maxr(head["eager_ms"]) * 1e3,
-        "graph_us_per_step": maxr(head.get("graph_ms", float("nan"))) * 1e3,
         "naive_us_per_step": maxr(head["naive_ms"]) * 1e3,
         "sys_kernel_alone_us": sys_ms * 1e3, "ctx_kernel_alone_us": ctx_ms * 1e3,
         "sys_kernel_alone_gbs": sys_bytes_local / (sys_ms * 1e-3) / 1e9,
+        "ctx_kernel_alone_gbs": (step_bytes_local - sys_bytes_local) / (ctx_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm",
                      "kernel": "relay step: sys_attn_sm100_kernel || ctx_cta_kernel (concurrent, relay fusion in-kernel)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -487,15 +588,16 @@ def run_b200(args):
                 "d2h_bytes_per_step": head["d2h"],
                 "path": "RelayDecodeStep.host_step_graph (CUDA graph): pinned H2D of [q|k_new|v_new] "
                         "-> rb_kv_append -> rb_relay_attention (system || context, fused in-kernel) -> D2H out",
-                "eager_us": maxr(head["e2e_eager_ms"]) * 1e3, "graph_us": maxr(head["e2e_graph_ms"]) * 1e3,
-                "launches_per_step": 3},
-        "gpu_launches": launches * args.steps,
-        "parity_max_abs_vs_naive": head["parity_max_abs_vs_naive"],
+                "eager_us": maxr(head["e2e_eager_ms"]) * 1e3, "launches_per_step": 3},
+        "gpu_launches": 2 * args.steps,
+        "relay_vs_naive_max_abs": head["relay_vs_naive_max_abs"],
         "sys_plan": head["plan"],
-        "sweep": sweep, "clocks": clk, "wall_s": wall,
+        "sweep": sweep, "configs": others, "clocks": clk, "wall_s": wall,
     }
-    if gathered_ok is not None:
-        line["sharded_allgather_ok"] = gathered_ok
+    if parity is not None:
+        line["parity"] = parity
+    if sharded_equal is not None:
+        line["sharded_equals_unsharded_bitwise"] = sharded_equal
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

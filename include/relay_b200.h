@@ -196,24 +196,6 @@ int rb_rope_append(const void* q_in, void* q_out, const void* k_new, const void*
                    long long stride_block, long long stride_tok, long long stride_head,
                    void* stream);
 
-/*
- * Debug probe of the tcgen05 operand layouts used by rb_system_attention
- * (one CTA): S^T = K.Q^T and O^T = V^T.P^T for K,V [128][128], Q [nq][128],
- * P [nq][128] bf16 -> s_out, o_out fp32 [128][nq].  For tests only.
- */
-int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void* p, int nq,
-                        float* s_out, float* o_out, void* stream);
-
-/*
- * Debug: when `buf` (device, [grid][8] u64) is non-NULL, subsequent
- * rb_system_attention launches record per-CTA %globaltimer stamps into it
- * (entry, prologue done, first S tile, group-0 end, group-1 end, producer end,
- * V-producer end, exit).  NULL disables.  For profiling only.
- */
-int rb_debug_set_timestamps(void* buf);
-/* Diagnostics: set tuning knob `id` (0..7) for later launches (A/B runs). */
-int rb_debug_set_knob(int id, int value);
-
 #ifdef __cplusplus
 }
 #endif

@@ -7,8 +7,10 @@
    compiled from their sources where they lie under /root/reference
    (cython -> gcc).  Only binaries land in oracle/_ref (git-ignored, travels
    to the GPU box); no reference source is copied into the repo.  Modules:
-   __init__, errors, kernels, numerics, attention, costmodel, _kernels_py
-   (.py) and _kernels_cy (.pyx) -- everything attention.py imports.
+   __init__, errors, kernels, numerics, attention, costmodel, kvcache, model,
+   _kernels_py (.py) and _kernels_cy (.pyx) -- everything attention.py and
+   the toy decoder (model.py, whose `_attend` is the reference caller of the
+   relay path) import.
 
 Run:  python oracle/build.py          (idempotent; skips up-to-date outputs)
 """
@@ -26,6 +28,7 @@ REF_MODULES = [
     ("__init__", ".py"), ("errors", ".py"), ("kernels", ".py"),
     ("numerics", ".py"), ("attention", ".py"), ("costmodel", ".py"),
     ("_kernels_py", ".py"), ("_kernels_cy", ".pyx"), ("kvcache", ".py"),
+    ("model", ".py"),
 ]
 
 

@@ -16,7 +16,7 @@ __all__ = [
     "TrafficCounter", "LseAttentionOutput", "attention_with_lse", "naive_causal_attention",
     "relay_fusion", "relay_attention", "relay_attention_ragged", "baseline_attention",
     "baseline_attention_ragged", "RelayDecodeStep", "NaiveDecodeStep", "SystemKvCache",
-    "PagedKvCache", "BlockPool", "theoretical_speedup", "kernel_backend",
+    "PagedKvCache", "BlockAllocator", "theoretical_speedup", "kernel_backend",
 ]
 
 
@@ -33,7 +33,7 @@ def __getattr__(name):
                 "RelayDecodeStep", "NaiveDecodeStep"):
         from . import attention
         return getattr(attention, name)
-    if name in ("SystemKvCache", "PagedKvCache", "BlockPool", "context_position"):
+    if name in ("SystemKvCache", "PagedKvCache", "BlockAllocator", "context_position"):
         from . import kvcache
         return getattr(kvcache, name)
     if name in ("theoretical_speedup", "traffic_relay", "traffic_baseline", "DecodeShape"):

@@ -15,32 +15,53 @@ from .errors import ContractError, DimensionError, KernelError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # RB_LIB: diagnostics only (a variant build of the same sources, see build.py)
 # RB_DIAG=1: the diagnostics build (kernels with %globaltimer stamps)
-LIB_PATH = os.environ.get("RB_LIB") or os.path.join(
-    _HERE, "librelay_b200_diag.so" if os.environ.get("RB_DIAG") == "1" else "librelay_b200.so")
+DIAG_LIB_PATH = os.path.join(_HERE, "librelay_b200_diag.so")
+LIB_PATH = os.environ.get("RB_LIB") or (
+    DIAG_LIB_PATH if os.environ.get("RB_DIAG") == "1" else os.path.join(_HERE, "librelay_b200.so"))
 
 RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
+ABI_VERSION = 1
 
 # every symbol include/relay_b200.h declares
 EXPORTS = (
     "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
     "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
     "rb_relay_workspace_bytes", "rb_relay_sys_grid", "rb_relay_attention",
-    "rb_debug_umma_probe", "rb_debug_set_timestamps", "rb_debug_set_knob",
     "rb_rope_rows", "rb_rope_append",
 )
+# include/relay_b200_diag.h: exported by librelay_b200_diag.so only
+DIAG_EXPORTS = ("rb_debug_umma_probe", "rb_debug_set_timestamps")
 
 _lib = None
+_diag = None
 
 
 def load():
     global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
+    if _lib is None:
+        _lib = _bind(LIB_PATH)
+    return _lib
+
+
+def load_diag():
+    """The diagnostics build (layout probe, per-CTA timestamps)."""
+    global _diag
+    if _diag is None:
+        _diag = _bind(DIAG_LIB_PATH)
+        vp, i32 = ctypes.c_void_p, ctypes.c_int
+        _diag.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
+        _diag.rb_debug_set_timestamps.argtypes = [vp]
+        for name in DIAG_EXPORTS:
+            getattr(_diag, name).restype = i32
+    return _diag
+
+
+def _bind(path):
+    if not os.path.exists(path):
         raise ImportError(
-            f"{LIB_PATH} is not built; run `python -m paper_2402_14808_b200.build` "
+            f"{path} is not built; run `python -m paper_2402_14808_b200.build` "
             "(no CPU fallback exists for the relay path)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, ctypes.c_float
     fp = ctypes.POINTER(ctypes.c_float)
     lib.rb_last_error.restype = ctypes.c_char_p
@@ -67,22 +88,14 @@ def load():
         f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
-    lib.rb_debug_umma_probe.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp]
     lib.rb_rope_rows.argtypes = [vp, vp, vp, i64, i32, ctypes.c_double, vp]
     lib.rb_rope_append.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_double,
                                    vp, vp, i32, i64, i64, i64, vp]
-    lib.rb_debug_set_timestamps.argtypes = [vp]
-    lib.rb_debug_set_knob.argtypes = [ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:
         if name not in ("rb_last_error", "rb_abi_version"):
             getattr(lib, name).restype = i32
-    if lib.rb_abi_version() != 1:
-        raise ImportError("librelay_b200.so ABI mismatch; rebuild")
-    # diagnostics: RB_KNOBS="0=1,2=5" sets tuning knobs (rb_debug_set_knob)
-    for kv in filter(None, os.environ.get("RB_KNOBS", "").split(",")):
-        k, v = kv.split("=")
-        lib.rb_debug_set_knob(int(k), int(v))
-    _lib = lib
+    if lib.rb_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI mismatch; rebuild")
     return lib
 
 

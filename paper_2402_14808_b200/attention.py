@@ -387,7 +387,7 @@ class RelayDecodeStep:
     """
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
-                 grid=None, out_dtype=torch.bfloat16):
+                 grid=None, out_dtype=torch.bfloat16, scale=None):
         self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
         self.block_table = block_table
         self.ctx_lens = ctx_lens
@@ -396,6 +396,18 @@ class RelayDecodeStep:
         self.hkv = sys_cache.kv_heads
         if hq % self.hkv != 0 or paged_cache.kv_heads != self.hkv:
             raise DimensionError("query heads must be a multiple of the (shared) kv heads")
+        if block_table.dim() != 2 or block_table.shape[0] != self.b:
+            raise DimensionError(f"block_table must be (b={self.b}, max_blocks), "
+                                 f"got {tuple(block_table.shape)}")
+        for name, t in (("block_table", block_table), ("ctx_lens", ctx_lens)):
+            if t.dtype != torch.int32 or not t.is_cuda:
+                raise ContractError(f"{name}: expected a CUDA int32 tensor, got {t.dtype} on {t.device}")
+        for t in (sys_cache.keys[layer], sys_cache.values[layer], paged_cache.k_pool):
+            if not t.is_cuda or t.device != block_table.device:
+                raise ContractError("caches, block table and context lengths must share one CUDA device")
+        # softmax temperature of the model's head dim (a d=16 cache is zero-
+        # padded to 128 on the device; the scale stays 16 ** -0.5)
+        self.scale = sys_cache.scale if scale is None else float(scale)
         dev = block_table.device
         from . import _lib
         if grid is None:
@@ -409,15 +421,23 @@ class RelayDecodeStep:
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
         self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
+        # a system-only launch (profiling) leaves its units published; the
+        # next full step must start from rearmed counters
+        self._system_pending = False
 
     def _launch(self, q, phases):
+        if q.dim() != 3 or tuple(q.shape) != (self.b, self.hq, HEAD_DIM):
+            raise DimensionError(f"q must be ({self.b}, {self.hq}, {HEAD_DIM}), got {tuple(q.shape)}")
+        if self._system_pending and phases & 1:
+            self.ws.zero_()
+        self._system_pending = phases == 1
         return kernels.relay_attention(
             q, self.q_start, self.sys_cache.keys[self.layer], self.sys_cache.values[self.layer],
             self.paged.k_pool[self.layer], self.paged.v_pool[self.layer], self.ctx_lens,
             max_rows=self.hq // self.hkv, hkv=self.hkv, sys_layout="hsd",
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), grid=self.grid, out=self.out, lse_out=self.lse,
-            ws=self.ws, phases=phases)
+            ws=self.ws, phases=phases, scale=self.scale)
 
     def system(self, q):
         """Only the system kernel of the step (profiling)."""
@@ -491,8 +511,9 @@ class NaiveDecodeStep:
     paged kernel without fusion.  Same inputs/outputs as RelayDecodeStep."""
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
-                 out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16, scale=None):
         self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
+        self.scale = sys_cache.scale if scale is None else float(scale)
         self.block_table, self.ctx_lens = block_table, ctx_lens
         self.b = ctx_lens.numel()
         self.hq, self.hkv = hq, sys_cache.kv_heads
@@ -510,4 +531,4 @@ class NaiveDecodeStep:
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), causal=True, prefix_k=pk, prefix_v=pv,
             prefix_strides=(pk.stride(1), pk.stride(0), pk.shape[1]),
-            out=self.out, lse_out=self.lse)
+            out=self.out, lse_out=self.lse, scale=self.scale)

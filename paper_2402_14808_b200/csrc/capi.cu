@@ -18,6 +18,9 @@
 #include <string>
 
 #include "../../include/relay_b200.h"
+#if RB_DIAG
+#include "../../include/relay_b200_diag.h"
+#endif
 #include "rb_common.cuh"
 #include "rb_plan.h"
 #include "rb_args.cuh"
@@ -43,12 +46,13 @@ cudaError_t launch_rope_rows(const float*, float*, const long long*, long long, 
 
 
 static thread_local std::string g_err;
-static unsigned long long* g_debug_ts = nullptr;  // test-only instrumentation
+#if RB_DIAG
+static unsigned long long* g_debug_ts = nullptr;  // diagnostics build only
+#else
+static constexpr unsigned long long* g_debug_ts = nullptr;
+#endif
 // context-kernel stamps start after 1024 system CTAs x 8 slots
 static constexpr long long kCtxTsOffset = 1024 * 8;
-namespace rb {
-int g_knobs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-}
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -428,12 +432,7 @@ int rb_rope_append(const void* q_in, void* q_out, const void* k_new, const void*
       "rope append launch");
 }
 
-int rb_debug_set_knob(int id, int value) {
-  if (id < 0 || id >= 8) return fail(RB_ERR_CONTRACT, "knob %d out of range", id);
-  rb::g_knobs[id] = value;
-  return RB_OK;
-}
-
+#if RB_DIAG
 int rb_debug_set_timestamps(void* buf) {
   g_debug_ts = static_cast<unsigned long long*>(buf);
   return RB_OK;
@@ -447,5 +446,6 @@ int rb_debug_umma_probe(const void* k, const void* q, const void* v, const void*
                             nq, s_out, o_out, static_cast<cudaStream_t>(stream)),
       "umma probe launch");
 }
+#endif  // RB_DIAG
 
 }  // extern "C"

@@ -69,6 +69,5 @@ struct CtxArgs {
 
 // Host-side tuning knobs (rb_debug_set_knob): reserved for A/B comparisons
 // of launch-side choices; no kernel reads them in this build.
-extern int g_knobs[8];
 
 }  // namespace rb

@@ -55,6 +55,15 @@ def _check_bf16(name, t):
         raise ContractError(f"{name}: head_dim must be the contiguous dimension")
 
 
+def _check_index(name, t, device):
+    if t.dtype not in (torch.int32, torch.int64) or t.device != device or not t.is_contiguous():
+        raise ContractError(f"{name}: expected a contiguous integer tensor on {device}, "
+                            f"got {t.dtype} on {t.device}")
+    want = torch.int64 if name == "req_offset" else torch.int32
+    if t.dtype != want:
+        raise ContractError(f"{name}: expected {want}, got {t.dtype}")
+
+
 def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
                      o_sys=None, lse_sys=None, ws=None):
     """Unmasked attention of every query row over the shared prefix.
@@ -113,10 +122,22 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
     strides = (stride_block, stride_tok, stride_head) in elements.
     """
     _check_bf16("q", q)
+    _check_bf16("k", k)
+    _check_bf16("v", v)
+    _check_index("q_start", q_start, q.device)
+    _check_index("ctx_lens", ctx_lens, q.device)
+    for name, t in (("block_table", block_table), ("req_offset", req_offset)):
+        if t is not None:
+            _check_index(name, t, q.device)
+    if prefix_k is not None:
+        _check_bf16("prefix_k", prefix_k)
+        _check_bf16("prefix_v", prefix_v)
     n_rows, hq, d = q.shape
     if d != HEAD_DIM:
         raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
     b = ctx_lens.numel()
+    if q_start.numel() != b + 1:
+        raise DimensionError(f"q_start needs b + 1 = {b + 1} offsets, got {q_start.numel()}")
     dev = q.device
     if out is None:
         out = torch.empty((n_rows, hq, HEAD_DIM),
@@ -150,9 +171,23 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
     partials, no merge) + context kernel whose epilogue merges the system
     partials with the context state.  Returns (out, lse)."""
     _check_bf16("q", q)
+    for name, t in (("sys_k", sys_k), ("sys_v", sys_v), ("k", k), ("v", v)):
+        _check_bf16(name, t)
+        if t.device != q.device:
+            raise ContractError(f"{name} is on {t.device}, q on {q.device}")
+    _check_index("q_start", q_start, q.device)
+    _check_index("ctx_lens", ctx_lens, q.device)
+    for name, t in (("block_table", block_table), ("req_offset", req_offset)):
+        if t is not None:
+            _check_index(name, t, q.device)
     n_rows, hq, d = q.shape
     if d != HEAD_DIM:
         raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
+    if q_start.numel() != ctx_lens.numel() + 1:
+        raise DimensionError(f"q_start needs b + 1 = {ctx_lens.numel() + 1} offsets, "
+                             f"got {q_start.numel()}")
+    if sys_k.shape != sys_v.shape or k.shape != v.shape:
+        raise DimensionError("K and V shapes differ")
     if sys_layout == "hsd":
         _, s, _ = sys_k.shape
         s_tok, s_head = sys_k.stride(1), sys_k.stride(0)
@@ -257,7 +292,7 @@ def umma_probe(k, q, v, p):
     nq = q.shape[0]
     s_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
     o_out = torch.empty((128, nq), dtype=torch.float32, device=k.device)
-    _lib.check(_lib.load().rb_debug_umma_probe(
+    _lib.check(_lib.load_diag().rb_debug_umma_probe(
         k.data_ptr(), q.data_ptr(), v.data_ptr(), p.data_ptr(), nq, s_out.data_ptr(),
         o_out.data_ptr(), _stream(k.device)), "rb_debug_umma_probe")
     return s_out, o_out

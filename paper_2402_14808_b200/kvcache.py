@@ -6,18 +6,20 @@ SystemKvCache  <- /root/reference/pkg/src/relayserve/kvcache.py:36-63
     s x 256 B slab, so the system kernel's TMA boxes (128 keys x 64 dims)
     are dense and every byte is read exactly once per decode step.
 
-PagedKvCache   <- kvcache.py:113-271 (BlockPool + PagedKvCache)
+PagedKvCache   <- kvcache.py:113-271 (block pool + PagedKvCache)
     Per-request context K/V in fixed-size blocks.  Pool layout per layer is
     bf16 [num_blocks][hkv][block_size][128]: one (block, head) pair is a
     contiguous block_size x 256 B run (4 KB at block_size 16), read in place
     by the context kernel through an int32 block table -- no gather copy
     (the reference copies to contiguous scratch, kvcache.py:237-262).
-    Block accounting (register / grow / release, CapacityError) follows
-    BlockPool exactly; it is host bookkeeping, not device work.
+    Block accounting (BlockAllocator: an int32 free stack, per-request block
+    lists) is host bookkeeping, not device work; running out of blocks
+    raises CapacityError as the reference's pool does.
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import kernels
@@ -40,20 +42,34 @@ def context_position(token_index_in_context: int, s: int) -> int:
 class SystemKvCache:
     """Shared prefix K/V per layer, bf16 [hkv][s][128] on one device."""
 
-    def __init__(self, keys, values, prompt_id: str = "system"):
+    def __init__(self, keys, values, prompt_id: str = "system", head_dim: int = HEAD_DIM):
         if len(keys) != len(values) or not keys:
             raise DimensionError("keys/values must have one entry per layer")
         shape = tuple(keys[0].shape)
+        dev = keys[0].device
         for k, v in zip(keys, values):
             if tuple(k.shape) != shape or tuple(v.shape) != shape or k.dim() != 3:
                 raise DimensionError(f"layer shapes inconsistent: {tuple(k.shape)} vs {tuple(v.shape)}")
             if shape[2] != HEAD_DIM:
-                raise DimensionError(f"head_dim must be {HEAD_DIM}")
+                raise DimensionError(f"the stored head_dim must be {HEAD_DIM} (zero-padded)")
+            for t in (k, v):
+                if t.device != dev:
+                    raise ContractError(f"system K/V layers on different devices: {dev} vs {t.device}")
         if shape[1] < 1:
             raise ContractError("system cache must hold at least one token")
-        self.keys = [k.contiguous() for k in keys]
-        self.values = [v.contiguous() for v in values]
+        if not 1 <= head_dim <= HEAD_DIM:
+            raise DimensionError(f"head_dim {head_dim} outside 1..{HEAD_DIM}")
+        # bf16 is the storage type the system kernel's TMA maps describe
+        self.keys = [k.to(torch.bfloat16).contiguous() for k in keys]
+        self.values = [v.to(torch.bfloat16).contiguous() for v in values]
         self.prompt_id = prompt_id
+        # the model's head dim: dims past it are zero padding; the softmax
+        # scale of attention over this cache is head_dim ** -0.5
+        self.head_dim = int(head_dim)
+
+    @property
+    def scale(self):
+        return self.head_dim ** -0.5
 
     @property
     def layers(self):
@@ -70,11 +86,18 @@ class SystemKvCache:
     @classmethod
     def from_shd(cls, keys_shd, values_shd, device="cuda", prompt_id="system"):
         """Build from per-layer (s, h, d) arrays/tensors (the reference's
-        layout, kvcache.py:40-41), converting to bf16 [h][s][d]."""
+        layout, kvcache.py:40-41), converting to bf16 [h][s][128] (d < 128 is
+        zero-padded and recorded as the cache's head_dim)."""
+        d = int(torch.as_tensor(keys_shd[0]).shape[-1])
+        if d > HEAD_DIM:
+            raise DimensionError(f"head_dim {d} > {HEAD_DIM} is not supported")
+
         def conv(x):
-            t = torch.as_tensor(x)
-            return t.to(device=device, dtype=torch.bfloat16).permute(1, 0, 2).contiguous()
-        return cls([conv(k) for k in keys_shd], [conv(v) for v in values_shd], prompt_id)
+            t = torch.as_tensor(x).to(device=device, dtype=torch.float32)
+            t = torch.nn.functional.pad(t, (0, HEAD_DIM - d)) if d < HEAD_DIM else t
+            return t.to(torch.bfloat16).permute(1, 0, 2).contiguous()
+        return cls([conv(k) for k in keys_shd], [conv(v) for v in values_shd], prompt_id,
+                   head_dim=d)
 
     # ---- the reference's on-disk format (RELAYKV, kvcache.py:19-20, 66-100):
     # magic b"RELAYKV\0", little-endian uint32 version (1), layers, s, h, d,
@@ -113,12 +136,14 @@ class SystemKvCache:
                     t = torch.zeros((h, s, HEAD_DIM), dtype=torch.bfloat16, device=device)
                     t[:, :, :d] = torch.from_numpy(a).to(device).permute(1, 0, 2).to(torch.bfloat16)
                     out.append(t)
-        return cls(keys, values, prompt_id)
+        return cls(keys, values, prompt_id, head_dim=d)
 
-    def save(self, path, head_dim=HEAD_DIM, bits=32):
+    def save(self, path, head_dim=None, bits=32):
         """Write the reference's format (readable by its load_system_cache):
-        the first `head_dim` dims of each head, as IEEE floats of `bits` bits
-        (32 holds bf16 exactly)."""
+        the first `head_dim` dims of each head (default: the cache's own
+        head_dim, so a loaded d=16 file saves back as d=16), as IEEE floats
+        of `bits` bits (32 holds bf16 exactly)."""
+        head_dim = self.head_dim if head_dim is None else head_dim
         import struct
 
         import numpy as np
@@ -142,100 +167,134 @@ class SystemKvCache:
         return cls(keys, values, prompt_id)
 
 
-class BlockPool:
-    """Bookkeeping-only block allocator, same semantics as kvcache.py:113-172."""
+class BlockAllocator:
+    """Physical block ids of one paged pool, handed out per request.
+
+    Free ids live in an int32 stack (``_stack[:_top]``); a request's block
+    list grows by slicing whole runs off the top, and a release pushes the
+    ids back so they are reused first.  Only the token -> slot arithmetic
+    matters to the kernels (they read the int32 block table in place);
+    which physical id a request gets does not, and ``shuffle`` scrambles the
+    free order to exercise the indirection (tests, benchmark).
+    """
 
     def __init__(self, num_blocks, block_size=DEFAULT_BLOCK_SIZE):
         if num_blocks < 1 or block_size < 1:
-            raise ContractError("pool needs at least one block of one slot")
-        self.num_blocks = num_blocks
-        self.block_size = block_size
-        self._free = list(range(num_blocks - 1, -1, -1))
-        self.tables: dict = {}
-        self.lengths: dict = {}
+            raise ContractError(f"a paged pool needs >= 1 block of >= 1 token "
+                                f"(num_blocks={num_blocks}, block_size={block_size})")
+        self.num_blocks = int(num_blocks)
+        self.block_size = int(block_size)
+        self._stack = np.arange(self.num_blocks - 1, -1, -1, dtype=np.int32)
+        self._top = self.num_blocks
+        self._blocks: dict = {}     # request id -> list of physical block ids
+        self._reserved: dict = {}   # request id -> tokens the blocks must hold
 
     @property
     def free_blocks(self):
-        return len(self._free)
+        return self._top
 
     @property
     def used_blocks(self):
-        return self.num_blocks - len(self._free)
+        return self.num_blocks - self._top
 
-    def blocks_for(self, tokens):
-        return -(-tokens // self.block_size)
+    def blocks_needed(self, tokens):
+        return (int(tokens) + self.block_size - 1) // self.block_size
 
-    def register(self, request_id):
-        if request_id in self.tables:
-            raise ContractError(f"request {request_id!r} already registered")
-        self.tables[request_id] = []
-        self.lengths[request_id] = 0
+    def shuffle(self, seed):
+        """Randomise which free ids are handed out next."""
+        rng = np.random.default_rng(seed)
+        self._stack[:self._top] = rng.permutation(self._stack[:self._top])
 
-    def grow(self, request_id, n_tokens):
-        if request_id not in self.tables:
-            raise ContractError(f"unknown request {request_id!r}")
-        table = self.tables[request_id]
-        new_len = self.lengths[request_id] + n_tokens
-        need = self.blocks_for(new_len)
-        if need - len(table) > len(self._free):
-            raise CapacityError(
-                f"pool exhausted: request {request_id!r} needs {need - len(table)} blocks, "
-                f"{len(self._free)} free")
-        while len(table) < need:
-            table.append(self._free.pop())
-        self.lengths[request_id] = new_len
-        return new_len
+    def open(self, request_id):
+        if request_id in self._blocks:
+            raise ContractError(f"request {request_id!r} is already open in this pool")
+        self._blocks[request_id] = []
+        self._reserved[request_id] = 0
 
-    def release(self, request_id):
-        table = self.tables.pop(request_id, [])
-        self.lengths.pop(request_id, None)
-        for bid in reversed(table):
-            self._free.append(bid)
-        return len(table)
+    def blocks(self, request_id):
+        try:
+            return self._blocks[request_id]
+        except KeyError:
+            raise ContractError(f"request {request_id!r} is not open in this pool") from None
+
+    def reserve(self, request_id, tokens):
+        """Make the request's blocks hold at least `tokens` tokens."""
+        table = self.blocks(request_id)
+        short = self.blocks_needed(tokens) - len(table)
+        if short > self._top:
+            raise CapacityError(f"paged pool full: {short} more block(s) for {request_id!r}, "
+                                f"{self._top} of {self.num_blocks} free")
+        if short > 0:
+            run = self._stack[self._top - short:self._top][::-1]
+            self._top -= short
+            table.extend(int(x) for x in run)
+        self._reserved[request_id] = max(self._reserved[request_id], int(tokens))
+        return self._reserved[request_id]
+
+    def close(self, request_id):
+        """Return the request's blocks to the pool (number returned)."""
+        table = self._blocks.pop(request_id, None)
+        self._reserved.pop(request_id, None)
+        if not table:
+            return 0
+        n = len(table)
+        self._stack[self._top:self._top + n] = np.asarray(table[::-1], dtype=np.int32)
+        self._top += n
+        return n
 
 
 class PagedKvCache:
     """Block-paged context K/V for all layers, resident in HBM.
 
-    k_pool / v_pool: bf16 (layers, num_blocks, hkv, block_size, 128).
+    k_pool / v_pool: bf16 (layers, num_blocks, hkv, block_size, 128).  Each
+    request owns a list of physical blocks (BlockAllocator) shared by all
+    layers and a token count per layer; token t of a request lives in block
+    ``blocks[t // block_size]`` at offset ``t % block_size``.
     """
 
     def __init__(self, layers, kv_heads, num_blocks, block_size=DEFAULT_BLOCK_SIZE,
                  device="cuda"):
-        self.pool = BlockPool(num_blocks, block_size)
+        self.allocator = BlockAllocator(num_blocks, block_size)
         self.layers = layers
         self.kv_heads = kv_heads
         shape = (layers, num_blocks, kv_heads, block_size, HEAD_DIM)
         self.k_pool = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.v_pool = torch.zeros(shape, dtype=torch.bfloat16, device=device)
-        self._layer_lengths: dict = {}
+        self._tokens: dict = {}     # request id -> np.int64[layers] tokens stored
         self.device = torch.device(device)
 
     @property
     def block_size(self):
-        return self.pool.block_size
+        return self.allocator.block_size
 
     def register(self, request_id):
-        self.pool.register(request_id)
-        self._layer_lengths[request_id] = [0] * self.layers
+        self.allocator.open(request_id)
+        self._tokens[request_id] = np.zeros(self.layers, dtype=np.int64)
 
     def length(self, request_id, layer=0):
-        return self._layer_lengths[request_id][layer]
+        return int(self._tokens[request_id][layer])
 
     def release(self, request_id):
-        self._layer_lengths.pop(request_id, None)
-        return self.pool.release(request_id)
+        self._tokens.pop(request_id, None)
+        return self.allocator.close(request_id)
+
+    def extend(self, request_id, n_tokens, layers=None):
+        """Account `n_tokens` more tokens on `layers` (default: all) whose
+        K/V are written straight into the pools by the caller (synthetic
+        workloads, prefill kernels); returns the slot of each new token on
+        the first of those layers."""
+        idx = range(self.layers) if layers is None else list(layers)
+        counts = self._tokens[request_id]
+        start = int(counts[idx[0]])
+        self.allocator.reserve(request_id, int(max(counts[i] for i in idx)) + n_tokens)
+        for i in idx:
+            counts[i] += n_tokens
+        table = self.allocator.blocks(request_id)
+        bs = self.block_size
+        return [table[t // bs] * bs + t % bs for t in range(start, start + n_tokens)]
 
     def _slots(self, request_id, layer, m):
-        lengths = self._layer_lengths[request_id]
-        start = lengths[layer]
-        table = self.pool.tables[request_id]
-        if self.pool.blocks_for(start + m) > len(table):
-            self.pool.grow(request_id, (start + m) - self.pool.lengths[request_id])
-        bs = self.block_size
-        slots = [table[(start + t) // bs] * bs + (start + t) % bs for t in range(m)]
-        lengths[layer] = start + m
-        return slots
+        return self.extend(request_id, m, layers=[layer])
 
     def append(self, request_id, layer, k, v):
         """Append (m, hkv, 128) keys/values (kvcache.py:207-235); returns the
@@ -245,7 +304,7 @@ class PagedKvCache:
                                  f"got {tuple(k.shape)} and {tuple(v.shape)}")
         slots = self._slots(request_id, layer, k.shape[0])
         self.append_slots(layer, k, v, torch.tensor(slots, dtype=torch.int32, device=self.device))
-        return self._layer_lengths[request_id][layer]
+        return self.length(request_id, layer)
 
     def append_slots(self, layer, k, v, slot_mapping):
         """Device-side append with a precomputed int32 slot mapping."""
@@ -268,7 +327,7 @@ class PagedKvCache:
                                  f"got {tuple(k.shape)} and {tuple(v.shape)}")
         if q.shape[0] != len(request_ids) or k.shape[0] != len(request_ids):
             raise DimensionError("append_rotated: one token per request")
-        pos = [context_position(self._layer_lengths[r][layer], s) for r in request_ids]
+        pos = [context_position(self.length(r, layer), s) for r in request_ids]
         slots = [self._slots(r, layer, 1)[0] for r in request_ids]
         dev = self.device
         return kernels.rope_append(
@@ -279,7 +338,7 @@ class PagedKvCache:
 
     def block_table(self, request_ids, width=None):
         """int32 (b, width) block table on the device (unused entries 0)."""
-        tables = [self.pool.tables[r] for r in request_ids]
+        tables = [self.allocator.blocks(r) for r in request_ids]
         width = max(1, max(len(t) for t in tables)) if width is None else width
         bt = torch.zeros((len(tables), width), dtype=torch.int32)
         for i, t in enumerate(tables):
@@ -287,7 +346,7 @@ class PagedKvCache:
         return bt.to(self.device)
 
     def context_lens(self, request_ids, layer=0):
-        return torch.tensor([self._layer_lengths[r][layer] for r in request_ids],
+        return torch.tensor([self.length(r, layer) for r in request_ids],
                             dtype=torch.int32, device=self.device)
 
     def strides(self):
@@ -297,8 +356,8 @@ class PagedKvCache:
 
     def gather(self, request_id, layer):
         """Contiguous (c, hkv, 128) copy of a request's K/V (tests/debug)."""
-        c = self._layer_lengths[request_id][layer]
-        table = self.pool.tables[request_id]
+        c = self.length(request_id, layer)
+        table = self.allocator.blocks(request_id)
         bs = self.block_size
         ks, vs = [], []
         for i in range(0, c, bs):

@@ -50,12 +50,10 @@ def build(cfg, device, seed=7):
     paged = PagedKvCache(1, hkv, nblk, 16, device=device)
     paged.k_pool.normal_(generator=g)
     paged.v_pool.normal_(generator=g)
-    perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(seed)).tolist()
-    paged.pool._free = perm[::-1]
+    paged.allocator.shuffle(seed)
     for r, c in enumerate(lens):
         paged.register(r)
-        paged.pool.grow(r, c)
-        paged._layer_lengths[r][0] = c
+        paged.extend(r, c)
     ids = list(range(b))
     bt, cl = paged.block_table(ids), paged.context_lens(ids)
     q = torch.randn((b, hq, 128), device=device, generator=g).to(torch.bfloat16)

@@ -22,7 +22,7 @@ def main():
     for s in [int(x) for x in (sys.argv[1:] or ["512", "8192"])]:
         q, relay, _, _, _ = bench.build(torch, s, list(range(bench.H)), dev)
         ts = torch.zeros((3072, 8), dtype=torch.int64, device=dev)
-        _lib.load().rb_debug_set_timestamps(ts.data_ptr())
+        _lib.load_diag().rb_debug_set_timestamps(ts.data_ptr())
         phases = int(os.environ.get("DIAG_PHASES", "3"))
         fn = {3: lambda: relay(q), 1: lambda: relay.system(q), 2: lambda: relay.context(q)}[phases]
         g = bench.graph_of(torch, fn)
@@ -46,7 +46,7 @@ def main():
                 lasts += [int(ctx[:, 7].max()), int(ctx[:, 6].max())]
             first, last = min(firsts), max(lasts)
             rows.append((e0.elapsed_time(e1) * 1e3, (last - first) / 1e3))
-        _lib.load().rb_debug_set_timestamps(None)
+        _lib.load_diag().rb_debug_set_timestamps(None)
         rows.sort()
         ev, span = rows[len(rows) // 2]
         # reference: a graph of one trivial kernel

@@ -50,7 +50,7 @@ def run(s, phases=3, b=32, h=52, c=128):
         if not os.environ.get("DIAG_NOFLUSH"):
             flush_fn()
         ts.zero_()
-        _lib.load().rb_debug_set_timestamps(ts.data_ptr() if it == 4 else None)
+        _lib.load_diag().rb_debug_set_timestamps(ts.data_ptr() if it == 4 else None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=1, hkv=h, sys_layout="hsd",
@@ -58,7 +58,7 @@ def run(s, phases=3, b=32, h=52, c=128):
                                 phases=phases)
         e1.record()
         torch.cuda.synchronize()
-    _lib.load().rb_debug_set_timestamps(None)
+    _lib.load_diag().rb_debug_set_timestamps(None)
     t = ts.cpu()
     sys_t = t[:1024][t[:1024, 0] != 0]
     ctx_t = t[1024:2048][t[1024:2048, 0] != 0]

@@ -35,7 +35,7 @@ def run(s, b=32, h=52):
     flush_fn = bench.make_flush(torch, dev)
     for it in range(4):
         flush_fn()
-        _lib.load().rb_debug_set_timestamps(ts.data_ptr() if it == 3 else None)
+        _lib.load_diag().rb_debug_set_timestamps(ts.data_ptr() if it == 3 else None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if MODE == "relay":  # system kernel as it runs inside rb_relay_attention
@@ -46,7 +46,7 @@ def run(s, b=32, h=52):
             kernels.system_attention(q, k, v, kv_layout="hsd", grid=grid)
         e1.record()
         torch.cuda.synchronize()
-    _lib.load().rb_debug_set_timestamps(None)
+    _lib.load_diag().rb_debug_set_timestamps(None)
     t = ts.cpu().double()
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3

@@ -22,8 +22,7 @@ paged.k_pool.normal_(generator=gen)
 paged.v_pool.normal_(generator=gen)
 for r in range(b):
     paged.register(r)
-    paged.pool.grow(r, c)
-    paged._layer_lengths[r][0] = c
+    paged.extend(r, c)
 ids = list(range(b))
 step = RelayDecodeStep(sysc, paged, paged.block_table(ids), paged.context_lens(ids), hq)
 q = torch.randn((b, hq, 128), device="cuda", generator=gen).to(torch.bfloat16)

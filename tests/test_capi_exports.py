@@ -8,8 +8,8 @@ import re
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared():
-    text = open(os.path.join(ROOT, "include", "relay_b200.h")).read()
+def _declared(header="relay_b200.h"):
+    text = open(os.path.join(ROOT, "include", header)).read()
     return sorted(set(re.findall(r"^\s*(?:const char\*|int)\s+(rb_\w+)\(", text, re.M)))
 
 
@@ -27,7 +27,21 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(raw, name), name
     assert set(_declared()) == set(_lib.EXPORTS)
-    assert lib.rb_abi_version() == 1
+    assert lib.rb_abi_version() == _lib.ABI_VERSION
+    # the diagnostics entry points are not part of the production ABI
+    for name in _declared("relay_b200_diag.h"):
+        assert not hasattr(raw, name), name
+
+
+def test_diag_library_exports_both_headers():
+    from paper_2402_14808_b200 import _lib
+    if not os.path.exists(_lib.DIAG_LIB_PATH):
+        import pytest
+        pytest.skip("diagnostics build absent")
+    raw = ctypes.CDLL(_lib.DIAG_LIB_PATH)
+    assert set(_declared("relay_b200_diag.h")) == set(_lib.DIAG_EXPORTS)
+    for name in _declared() + _declared("relay_b200_diag.h"):
+        assert hasattr(raw, name), name
 
 
 def test_error_mapping_without_gpu():

@@ -128,9 +128,7 @@ def make_paged(rb, ctx_k, ctx_v, hkv, block_size=16, seed=0):
     from paper_2402_14808_b200.kvcache import PagedKvCache
     total_blocks = sum(-(-len(k) // block_size) for k in ctx_k) + 3
     cache = PagedKvCache(1, hkv, total_blocks, block_size, device="cuda")
-    rng = np.random.default_rng(seed)
-    perm = list(rng.permutation(total_blocks))
-    cache.pool._free = [int(x) for x in perm]
+    cache.allocator.shuffle(seed)
     ids = []
     for r, (k, v) in enumerate(zip(ctx_k, ctx_v)):
         cache.register(r)
@@ -314,8 +312,7 @@ def test_c2_full_size_relay_vs_naive_and_oracle_heads(rb, oracle):
     paged.v_pool.normal_(generator=gen)
     for r in range(b):
         paged.register(r)
-        paged.pool.grow(r, c)
-        paged._layer_lengths[r][0] = c
+        paged.extend(r, c)
     bt, cl = paged.block_table(list(range(b))), paged.context_lens(list(range(b)))
     q = torch.randn((b, h, 128), device="cuda", generator=gen).to(torch.bfloat16)
     out, lse = RelayDecodeStep(sys_cache, paged, bt, cl, h)(q)

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from paper_2402_14808_b200 import _lib, costmodel, sharding
-from paper_2402_14808_b200.kvcache import BlockPool
+from paper_2402_14808_b200.kvcache import BlockAllocator
 from paper_2402_14808_b200.plan import SysPlan
 
 
@@ -76,23 +76,28 @@ def test_byte_model_c2():
 
 def test_block_pool_conservation():
     rng = np.random.default_rng(808)
-    pool = BlockPool(num_blocks=64, block_size=4)
-    live, nid = [], 0
+    pool = BlockAllocator(num_blocks=64, block_size=4)
+    pool.shuffle(3)
+    live, nid = {}, 0
     from paper_2402_14808_b200.errors import CapacityError
     for _ in range(3000):
         if live and rng.random() < 0.45:
-            pool.release(live.pop(int(rng.integers(len(live)))))
+            rid = list(live)[int(rng.integers(len(live)))]
+            assert pool.close(rid) == len(live.pop(rid))
         else:
             rid = f"r{nid}"
             nid += 1
-            pool.register(rid)
-            live.append(rid)
+            pool.open(rid)
             try:
-                pool.grow(rid, int(rng.integers(1, 10)))
+                pool.reserve(rid, int(rng.integers(1, 10)))
+                pool.reserve(rid, int(rng.integers(1, 20)))
+                live[rid] = list(pool.blocks(rid))
             except CapacityError:
-                pool.release(rid)
-                live.remove(rid)
+                pool.close(rid)
         assert pool.used_blocks + pool.free_blocks == pool.num_blocks
+        owned = [b for t in live.values() for b in t]
+        assert len(owned) == len(set(owned)) == pool.used_blocks   # no block owned twice
+        assert all(0 <= b < 64 for b in owned)
 
 
 def test_relay_sm_split():
