@@ -428,7 +428,10 @@ def run_b200(args):
             res["ctx_ms"] = statistics.mean(timed(lambda: alone.context(q)))
             del alone
             res.update(e2e_stats(q, relay, bt))
-            res["objs"] = (q, sc, paged, out_r, lse_r)
+            # e2e wrote its new tokens into the pool: the parity leg re-runs
+            # the step on the cache as it is now
+            out_p, lse_p = [t.clone() for t in relay(q)]
+            res["objs"] = (q, sc, paged, out_p, lse_p)
         del relay, naive, gr
         return res
 

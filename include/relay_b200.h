@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 1
+#define RB_ABI_VERSION 2
 
 enum {
   RB_OK = 0,
@@ -92,7 +92,7 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
  *                                        + (t % block_size)*stride_tok + h*stride_head
  *            pool layout [num_blocks][hkv][block_size][128]: (hkv*bs*128, 128, bs*128)
  *     ragged (req_offset != NULL):  base + (req_offset[r] + t)*stride_tok + h*stride_head
- *   max_rows: max_r m_r * (hq / hkv).
+ *   n_rows = q_start[b]; max_rows: max_r m_r * (hq / hkv).
  * Relay epilogue: when o_sys/lse_sys (rb_system_attention's outputs) are
  *   given, the result is fused with them (`relay_fusion`, attention.py:137-157)
  *   and lse_out receives the fused LSE = logaddexp(lse_sys, lse_ctx).
@@ -101,16 +101,25 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
  *   reference's `baseline_attention`, attention.py:266-296).
  * out: [n_rows][hq][128], fp32 when out_fp32 else bf16; lse_out: fp32
  *   [n_rows][hq] or NULL.
+ * Split-K: max_ctx_len (an upper bound of ctx_lens, <= 0: unknown) lets the
+ *   kernel cut long contexts into splits spread over the SMs (few requests x
+ *   heads, long contexts), combined in a fixed order (deterministic).  The
+ *   splits need `workspace` of rb_context_workspace_bytes(...) bytes,
+ *   zero-filled before first use (the kernel leaves it zeroed); workspace
+ *   NULL runs unsplit; a non-NULL workspace that is too small is an error.
  */
+int rb_context_workspace_bytes(int b, int n_rows, int max_rows, int hq, int hkv, int s_prefix,
+                               int max_ctx_len, int sm_count, size_t* bytes);
 int rb_context_attention(const void* q, long long q_row_stride, long long q_head_stride,
-                         const int* q_start, int b, int max_rows, int hq, int hkv, int d,
+                         const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
                          const void* k, const void* v, const int* block_table, int bt_stride,
                          int block_size, const long long* req_offset, long long stride_block,
                          long long stride_tok, long long stride_head, const int* ctx_lens,
                          int causal, const void* prefix_k, const void* prefix_v, int s_prefix,
                          long long p_stride_tok, long long p_stride_head, const float* o_sys,
                          const float* lse_sys, float scale, void* out, int out_fp32,
-                         float* lse_out, void* stream);
+                         float* lse_out, int max_ctx_len, void* workspace, size_t workspace_bytes,
+                         void* stream);
 
 /*
  * The whole relay decode step in one call -- `relay_attention_ragged`
@@ -124,16 +133,19 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * ONE LSE-weighted combine -- the relay fusion (attention.py:137-157) --
  * writing `out` (bf16 or fp32) and the fused LSE.
  * Arguments are those of rb_system_attention + rb_context_attention (causal).
- * workspace: rb_relay_workspace_bytes(...) bytes, zero-filled before first use;
- * the kernels leave it zeroed (its header holds the context kernel's work
- * counters), so one buffer serves every step on a stream.
+ * workspace: rb_relay_workspace_bytes(...) bytes (sm_count = the device's SM
+ * count), zero-filled before first use; the kernels leave it zeroed (its
+ * header holds the context kernel's work counters), so one buffer serves
+ * every step on a stream.  max_ctx_len: an upper bound of ctx_lens (e.g. the
+ * block table's width x block_size) for the context split-K.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
  * (2 | 4: the context kernel of a step whose system kernel was launched by an
  * earlier phase-1 call, e.g. with stream work in between; the units are
  * published by that system kernel as it runs)
  * (profiling: phase 2 consumes the slots a previous phase-1 call wrote).
  */
-int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes);
+int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, int b,
+                             int max_rows, int max_ctx_len, int sm_count, size_t* bytes);
 /*
  * System-kernel CTA count for rb_relay_attention's grid_cap: the two kernels
  * run concurrently, the system kernel on a share of the SMs proportional to
@@ -149,7 +161,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        const int* block_table, int bt_stride, int block_size,
                        const long long* req_offset, long long stride_block, long long stride_tok,
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
-                       void* out, int out_fp32, float* lse_out, void* workspace,
+                       void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
                        size_t workspace_bytes, int phases, void* stream);
 
 /*

@@ -20,12 +20,13 @@ LIB_PATH = os.environ.get("RB_LIB") or (
     DIAG_LIB_PATH if os.environ.get("RB_DIAG") == "1" else os.path.join(_HERE, "librelay_b200.so"))
 
 RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # every symbol include/relay_b200.h declares
 EXPORTS = (
     "rb_last_error", "rb_abi_version", "rb_device_sm_count", "rb_sys_plan_query",
-    "rb_system_attention", "rb_context_attention", "rb_relay_fusion", "rb_kv_append",
+    "rb_system_attention", "rb_context_attention", "rb_context_workspace_bytes",
+    "rb_relay_fusion", "rb_kv_append",
     "rb_relay_workspace_bytes", "rb_relay_sys_grid", "rb_relay_attention",
     "rb_rope_rows", "rb_rope_append",
 )
@@ -74,18 +75,21 @@ def _bind(path):
         vp, i64, i64, i32, i32, i32, i32, vp, vp, i32, i64, i64, f32, i32, vp, vp, vp,
         ctypes.c_size_t, vp]
     lib.rb_context_attention.argtypes = [
-        vp, i64, i64, vp, i32, i32, i32, i32, i32,       # q .. d
+        vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,  # q .. d
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,     # k .. ctx_lens
         i32, vp, vp, i32, i64, i64,                      # causal, prefix
-        vp, vp, f32, vp, i32, vp, vp]                    # o_sys .. stream
+        vp, vp, f32, vp, i32, vp,                        # o_sys .. lse_out
+        i32, vp, ctypes.c_size_t, vp]                    # max_ctx_len, workspace, stream
+    lib.rb_context_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32, i32, i32,
+                                               ctypes.POINTER(ctypes.c_size_t)]
     lib.rb_relay_sys_grid.argtypes = [i32, i32, i32, i32, i64, i32, ctypes.POINTER(i32)]
-    lib.rb_relay_workspace_bytes.argtypes = [i32, i32, i32, i32, i32,
+    lib.rb_relay_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32, i32, i32, i32,
                                              ctypes.POINTER(ctypes.c_size_t)]
     lib.rb_relay_attention.argtypes = [
         vp, i64, i64, vp, i32, i32, i32, i32, i32, i32,   # q .. d
         vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,      # k .. ctx_lens
-        f32, i32, vp, i32, vp, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
+        f32, i32, vp, i32, vp, i32, vp, ctypes.c_size_t, i32, vp]   # scale .. stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_rope_rows.argtypes = [vp, vp, vp, i64, i32, ctypes.c_double, vp]
@@ -122,10 +126,21 @@ def sys_plan(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int):
     return dict(zip(keys, list(f)[:8])), ws.value
 
 
-def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int) -> int:
+def relay_workspace_bytes(n_rows: int, hq: int, hkv: int, s: int, grid_cap: int, b: int,
+                          max_rows: int, max_ctx_len: int, sm_count: int) -> int:
     out = ctypes.c_size_t(0)
-    check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, ctypes.byref(out)),
+    check(load().rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, b, max_rows, max_ctx_len,
+                                          sm_count, ctypes.byref(out)),
           "rb_relay_workspace_bytes")
+    return out.value
+
+
+def context_workspace_bytes(b: int, n_rows: int, max_rows: int, hq: int, hkv: int, s_prefix: int,
+                            max_ctx_len: int, sm_count: int) -> int:
+    out = ctypes.c_size_t(0)
+    check(load().rb_context_workspace_bytes(b, n_rows, max_rows, hq, hkv, s_prefix, max_ctx_len,
+                                            sm_count, ctypes.byref(out)),
+          "rb_context_workspace_bytes")
     return out.value
 
 

@@ -158,7 +158,8 @@ def attention_with_lse(q, k, v, causal):
         vf = vd.reshape(b * n, hkv, HEAD_DIM)
         o, lse = kernels.context_attention(
             qd, q_start, kf, vf, lens, max_rows=m * (h // hkv), hkv=hkv, req_offset=req_off,
-            strides=(0, kf.stride(0), kf.stride(1)), causal=causal, scale=scale, out_fp32=True)
+            strides=(0, kf.stride(0), kf.stride(1)), causal=causal, scale=scale, out_fp32=True,
+            max_ctx_len=n)
     return LseAttentionOutput(output=_out(o.reshape(b, m, h, HEAD_DIM), d, like_np),
                               lse=_lse_out(lse.reshape(b, m, h), like_np))
 
@@ -280,7 +281,7 @@ def relay_attention_ragged(q_list, sys_k, sys_v, ctx_k, ctx_v, counter=None,
     out, lse = kernels.relay_attention(
         qf, q_start, skd, svd, ckd, cvd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv,
         sys_layout="shd", req_offset=req_off, strides=(0, ckd.stride(0), ckd.stride(1)),
-        scale=scale, out_fp32=True)
+        scale=scale, out_fp32=True, max_ctx_len=max(c_list))
     if counter is not None:
         _count_relay(counter, m_list, c_list, s, h, d)
     outs, lses, row = [], [], 0
@@ -348,7 +349,7 @@ def baseline_attention_ragged(q_list, full_k, full_v, counter=None):
     out, _ = kernels.context_attention(
         qf, q_start, kd, vd, lens, max_rows=max(m_list) * (h // hkv), hkv=hkv, req_offset=req_off,
         strides=(0, kd.stride(0), kd.stride(1)), causal=True, scale=1.0 / math.sqrt(d),
-        out_fp32=True, want_lse=False)
+        out_fp32=True, want_lse=False, max_ctx_len=max(n_list))
     if counter is not None:
         for m, n in zip(m_list, n_list):
             hd = h * d
@@ -416,7 +417,12 @@ class RelayDecodeStep:
                                        int(ctx_lens.sum().item()), kernels.sm_count(dev))
         self.grid = grid
         self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
-        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
+        # the block table's capacity bounds every context it can address, so
+        # the split-K plan stays valid while the contexts grow into it
+        self.max_ctx_len = block_table.shape[1] * paged_cache.block_size
+        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid,
+                                          self.b, hq // self.hkv, self.max_ctx_len,
+                                          kernels.sm_count(dev))
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
@@ -437,7 +443,7 @@ class RelayDecodeStep:
             max_rows=self.hq // self.hkv, hkv=self.hkv, sys_layout="hsd",
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), grid=self.grid, out=self.out, lse_out=self.lse,
-            ws=self.ws, phases=phases, scale=self.scale)
+            ws=self.ws, phases=phases, scale=self.scale, max_ctx_len=self.max_ctx_len)
 
     def system(self, q):
         """Only the system kernel of the step (profiling)."""
@@ -504,6 +510,12 @@ class RelayDecodeStep:
         return graph.replay
 
 
+def _lib_ctx_bytes(b, hq, hkv, s_prefix, max_ctx_len, dev):
+    from . import _lib
+    return _lib.context_workspace_bytes(b, b, hq // hkv, hq, hkv, s_prefix, max_ctx_len,
+                                        kernels.sm_count(dev))
+
+
 class NaiveDecodeStep:
     """The per-request baseline step ("vLLM-PS"; reference
     `baseline_attention`): every request re-reads the shared prefix (stored
@@ -521,6 +533,9 @@ class NaiveDecodeStep:
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
         self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
+        self.max_ctx_len = block_table.shape[1] * paged_cache.block_size
+        need = _lib_ctx_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.max_ctx_len, dev)
+        self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
 
     def __call__(self, q):
         pk = self.sys_cache.keys[self.layer]
@@ -531,4 +546,5 @@ class NaiveDecodeStep:
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), causal=True, prefix_k=pk, prefix_v=pv,
             prefix_strides=(pk.stride(1), pk.stride(0), pk.shape[1]),
-            out=self.out, lse_out=self.lse, scale=self.scale)
+            out=self.out, lse_out=self.lse, scale=self.scale, max_ctx_len=self.max_ctx_len,
+            ws=self.ws)

@@ -29,6 +29,7 @@ namespace rb {
 cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
                                     cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
+int ctx_resident_ctas(int sms);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
                                 float*, long long, int, cudaStream_t);
 cudaError_t launch_umma_probe(const __nv_bfloat16*, const __nv_bfloat16*, const __nv_bfloat16*,
@@ -194,15 +195,68 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
 }
 
 // ----------------------------------------------------- context attention
+// ------------------------------------------------------ context split-K
+static int device_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return sms;
+}
+
+static void ctx_split_plan(int b, int hkv, int max_rows, int s_prefix, int max_ctx_len, int sms,
+                           int* chunks, int* n_split) {
+  *chunks = 0;
+  *n_split = 1;
+  if (max_ctx_len <= 0 || max_rows < 1 || sms < 1) return;
+  const int R = rb_ctx_rows(max_rows);
+  const long long base = (long long)b * hkv * ((max_rows + R - 1) / R);
+  const int max_chunks = (s_prefix + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK +
+                         (max_ctx_len + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK;
+  rb_ctx_split(base, max_chunks, rb::ctx_resident_ctas(sms), chunks, n_split);
+}
+
+int rb_context_workspace_bytes(int b, int n_rows, int max_rows, int hq, int hkv, int s_prefix,
+                               int max_ctx_len, int sm_count, size_t* bytes) {
+  if (b < 0 || n_rows < 0 || hq < 1 || hkv < 1 || hq % hkv != 0)
+    return fail(RB_ERR_DIMENSION, "bad context workspace shape");
+  int L, ns;
+  ctx_split_plan(b, hkv, max_rows, s_prefix, max_ctx_len, sm_count, &L, &ns);
+  *bytes = (size_t)rb_ctx_split_bytes(b, n_rows, hq, hkv, max_rows, ns);
+  return RB_OK;
+}
+
+// split fields of `a` from the workspace section `ws` (NULL: no split)
+static int ctx_split_args(rb::CtxArgs& a, int n_rows, int max_rows, int max_ctx_len, void* ws,
+                          size_t ws_bytes) {
+  a.split_chunks = 0;
+  a.n_split = 1;
+  a.split_part = nullptr;
+  a.split_cnt = nullptr;
+  if (ws == nullptr) return RB_OK;
+  int L, ns;
+  ctx_split_plan(a.b, a.hkv, max_rows, a.s_prefix, max_ctx_len, device_sms(), &L, &ns);
+  if (ns < 2) return RB_OK;
+  const size_t need = (size_t)rb_ctx_split_bytes(a.b, n_rows, a.hq, a.hkv, max_rows, ns);
+  if (ws_bytes < need)
+    return fail(RB_ERR_CONTRACT, "context split workspace too small: %zu < %zu bytes", ws_bytes, need);
+  const size_t part = ((size_t)n_rows * a.hq * ns * 132 * 4 + 255) & ~(size_t)255;
+  a.split_chunks = L;
+  a.n_split = ns;
+  a.split_part = static_cast<float*>(ws);
+  a.split_cnt = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part);
+  return RB_OK;
+}
+
 int rb_context_attention(const void* q, long long q_row_stride, long long q_head_stride,
-                         const int* q_start, int b, int max_rows, int hq, int hkv, int d,
+                         const int* q_start, int b, int n_rows, int max_rows, int hq, int hkv, int d,
                          const void* k, const void* v, const int* block_table, int bt_stride,
                          int block_size, const long long* req_offset, long long stride_block,
                          long long stride_tok, long long stride_head, const int* ctx_lens,
                          int causal, const void* prefix_k, const void* prefix_v, int s_prefix,
                          long long p_stride_tok, long long p_stride_head, const float* o_sys,
                          const float* lse_sys, float scale, void* out, int out_fp32,
-                         float* lse_out, void* stream) {
+                         float* lse_out, int max_ctx_len, void* workspace, size_t workspace_bytes,
+                         void* stream) {
   if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
   if (b < 1) return RB_OK;
   if (hq < 1 || hkv < 1 || hq % hkv != 0)
@@ -250,7 +304,9 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.lse_out = lse_out;
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
-  a.sched = nullptr;  // no workspace: static item order
+  a.sched = nullptr;  // static item order
+  int st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, workspace, workspace_bytes);
+  if (st != RB_OK) return st;
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
                      "context attention launch");
 }
@@ -267,7 +323,8 @@ static void relay_ws_layout(const rb_sys_plan& p, size_t* cnt_bytes, size_t* cpa
   *acc_bytes = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
 }
 
-int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, size_t* bytes) {
+int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, int b,
+                             int max_rows, int max_ctx_len, int sm_count, size_t* bytes) {
   long long f[8];
   size_t dummy = 0;
   int st = rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, &dummy);
@@ -276,7 +333,10 @@ int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, s
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, grid_cap);
   size_t cnt, cpart, ml, acc;
   relay_ws_layout(p, &cnt, &cpart, &ml, &acc);
-  *bytes = 256 + cnt + cpart + ml + acc;
+  int L, ns;
+  ctx_split_plan(b, hkv, max_rows, 0, max_ctx_len, sm_count, &L, &ns);
+  const size_t split = (size_t)rb_ctx_split_bytes(b, n_rows, hq, hkv, max_rows, ns);
+  *bytes = 256 + cnt + cpart + ml + ((acc + 255) & ~(size_t)255) + split;
   return RB_OK;
 }
 
@@ -295,11 +355,13 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        const int* block_table, int bt_stride, int block_size,
                        const long long* req_offset, long long stride_block, long long stride_tok,
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
-                       void* out, int out_fp32, float* lse_out, void* workspace,
+                       void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
                        size_t workspace_bytes, int phases, void* stream) {
   if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
   size_t need = 0;
-  int st = rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, &need);
+  const int sms = device_sms();
+  int st = rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, b, max_rows, max_ctx_len, sms,
+                                    &need);
   if (st != RB_OK) return st;
   if (workspace_bytes < need)
     return fail(RB_ERR_CONTRACT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
@@ -373,6 +435,11 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = header;  // workspace header: dynamic item counters
+  {
+    const size_t split_off = 256 + cnt + cpart + ml + ((acc_b + 255) & ~(size_t)255);
+    st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, ws + split_off, workspace_bytes - split_off);
+    if (st != RB_OK) return st;
+  }
   if (!(phases & 1) && !(phases & 4)) {
     // context phase alone (profiling): the slots of an earlier phase-1 call
     // are complete; mark every unit published (the kernel rearms them)

@@ -56,7 +56,9 @@ __device__ __forceinline__ const __nv_bfloat16* ctx_row(const KvView& kv, const 
 template <int R>
 struct CtxItem {
   int r, h, z, row0, m_r, nrows, c_r, max_lim, n_chunks;
-  long long roff;  // ragged mode: first token of request r
+  int sp, grp, nsplit, k0;  // split index, (r, h, z) group, valid splits of it, first chunk
+  int bt0;                  // block-table index of the item's bt[0] window
+  long long roff;           // ragged mode: first token of request r
 };
 
 // Issue the cp.async copies of one 16-token chunk (rows 0 .. n-1 of K at kb
@@ -104,315 +106,179 @@ __device__ __noinline__ void chunk_cp_async_rows(uint8_t* dst, KvView kv, int r,
   }
 }
 
-// Tensor-core (mma.sync m16n8k16) update of one 16-key chunk for up to 16
-// query rows: S = Q K^T (2 n-tiles x 8 k-steps), online softmax in the log2
-// domain on the accumulator fragments, O += P V (16 n-tiles).  Lane (g =
-// lane / 4, t = lane % 4) holds rows g and g + 8.  lim0 / lim1: exclusive key
-// bounds (segment-relative) of those rows; key0: this chunk's first key.
-// mask = false: every key of the chunk is valid for every valid row (rows
-// past the item's rows compute harmless values that are never written).
-// Lazy rescale: the running max moves only when a score exceeds it by more
-// than kCtxTau (log2 units), so O is rescaled rarely; p <= 2^kCtxTau.
+// Per-worker compute of one item: up to R <= 8 query rows against the
+// item's 16-key chunks on the tensor cores, "swap-AB" so the keys fill the
+// MMA M dimension and the (few) query rows its N = 8 dimension:
+//
+//   S^T [16 keys x 8 rows] = K_chunk [16 x 128] . Q^T        (8 k-steps)
+//   O^T [128 d  x 8 rows] += V_chunk^T [128 x 16] . P^T      (8 m-tiles)
+//
+// with mma.sync m16n8k16 (bf16 in, fp32 accumulate).  A decode row (R = 1)
+// wastes 7/8 of N, but one 16-key chunk is still 16 MMAs + 16 ldmatrix +
+// a ~30-instruction softmax -- the CUDA-core formulation it replaces needed
+// ~1000 warp-instructions per chunk (64 bf16 converts each for K and V, 32
+// shuffles for the dot products), which made the kernel issue-bound at
+// ~0.5 of HBM (profiles/r01g).  Lane (g = lane / 4, t = lane % 4) holds
+// S^T rows (keys) g, g + 8 and columns (query rows) 2t, 2t + 1; the softmax
+// reduces over keys with 3 xor-shuffles per column, and P^T goes from the
+// accumulator layout to the B-operand layout with two movmatrix transposes.
+// Online softmax in the log2 domain with a lazy max: the reference max of a
+// row moves only when a chunk exceeds it by more than kCtxTau, so O is
+// rescaled rarely and p <= 2^kCtxTau.  Row sums stay per lane and are
+// reduced across the 8 key lanes once per item.
 constexpr float kCtxTau = 8.f;
-struct MmaRowState {
-  float o[16][4];
-  float m[2], l[2];
-};
-
-__device__ __forceinline__ void chunk_mma(MmaRowState& st, const uint32_t (&qa)[8][4], uint32_t slot,
-                                          int lane, int key0, int lim0, int lim1, float scale_log2,
-                                          bool mask) {
-  const int mi = lane >> 3, rr = lane & 7, t = lane & 3;
-  float s[2][4];
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) s[nt][e] = 0.f;
-  {
-    const int key = (mi >> 1) * 8 + rr;
-    const uint32_t kaddr = slot + key * kRowBytes;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      uint32_t b[4];
-      ldsm_x4(b, kaddr + (((ks * 2 + (mi & 1)) ^ (key & 7)) << 4));
-      mma_bf16_16816(s[0], qa[ks], b[0], b[1]);
-      mma_bf16_16816(s[1], qa[ks], b[2], b[3]);
-    }
-  }
-  float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int key = key0 + nt * 8 + 2 * t + e;
-      s[nt][e] = (!mask || key < lim0) ? s[nt][e] * scale_log2 : -INFINITY;
-      s[nt][2 + e] = (!mask || key < lim1) ? s[nt][2 + e] * scale_log2 : -INFINITY;
-      mx0 = fmaxf(mx0, s[nt][e]);
-      mx1 = fmaxf(mx1, s[nt][2 + e]);
-    }
-  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-  mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-  mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-  // lazy max: keep the reference unless the chunk exceeds it by > kCtxTau
-  const float mn0 = (mx0 > st.m[0] + kCtxTau) ? mx0 : st.m[0];
-  const float mn1 = (mx1 > st.m[1] + kCtxTau) ? mx1 : st.m[1];
-  const float b0 = (mn0 == -INFINITY) ? 0.f : mn0, b1 = (mn1 == -INFINITY) ? 0.f : mn1;
-  float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      s[nt][e] = fast_exp2(s[nt][e] - b0);
-      s[nt][2 + e] = fast_exp2(s[nt][2 + e] - b1);
-      sum0 += s[nt][e];
-      sum1 += s[nt][2 + e];
-    }
-  sum0 += __shfl_xor_sync(0xffffffffu, sum0, 1);
-  sum1 += __shfl_xor_sync(0xffffffffu, sum1, 1);
-  sum0 += __shfl_xor_sync(0xffffffffu, sum0, 2);
-  sum1 += __shfl_xor_sync(0xffffffffu, sum1, 2);
-  if (mn0 != st.m[0] || mn1 != st.m[1]) {
-    const float al0 = (st.m[0] == -INFINITY) ? 0.f : fast_exp2(st.m[0] - mn0);
-    const float al1 = (st.m[1] == -INFINITY) ? 0.f : fast_exp2(st.m[1] - mn1);
-    st.l[0] *= al0;
-    st.l[1] *= al1;
-#pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-      st.o[nt][0] *= al0;
-      st.o[nt][1] *= al0;
-      st.o[nt][2] *= al1;
-      st.o[nt][3] *= al1;
-    }
-    st.m[0] = mn0;
-    st.m[1] = mn1;
-  }
-  st.l[0] += sum0;
-  st.l[1] += sum1;
-  const uint32_t pa[4] = {pack_bf16x2(s[0][0], s[0][1]), pack_bf16x2(s[0][2], s[0][3]),
-                          pack_bf16x2(s[1][0], s[1][1]), pack_bf16x2(s[1][2], s[1][3])};
-  {
-    const int key = (mi & 1) * 8 + rr;
-    const uint32_t vaddr = slot + kChunk * kRowBytes + key * kRowBytes;
-#pragma unroll
-    for (int dp = 0; dp < 8; ++dp) {
-      uint32_t b[4];
-      ldsm_x4_trans(b, vaddr + (((dp * 2 + (mi >> 1)) ^ (key & 7)) << 4));
-      mma_bf16_16816(st.o[2 * dp], pa, b[0], b[1]);
-      mma_bf16_16816(st.o[2 * dp + 1], pa, b[2], b[3]);
-    }
-  }
-}
+constexpr int kAccStride = 132;   // floats per row of the merge buffers (bank-conflict padding)
 
 template <int R>
-struct RowState {
-  float m[R], l[R], acc[R][8];
-};
-
-// CUDA-core update of one 16-key chunk for a half-warp (R <= 2 query rows,
-// where 16-row MMA tiles would be mostly padding): keys key0 + 2p + hw,
-// p = 0..7, K/V rows already in registers; dot products reduce with 4
-// xor-shuffles, online softmax in the log2 domain.  `lim[i]` is the exclusive key bound of row i inside
-// this segment; keys at or past it contribute nothing (their V rows may hold
-// stale data and are zeroed, never multiplied).
-template <int R>
-__device__ __forceinline__ void chunk_update(RowState<R>& st, const float (&qf)[R][8],
-                                             const uint4 (&kr)[8], uint4 (&vr)[8],
-                                             int key0, int hw, const int (&lim)[R], float scale_log2,
-                                             int max_lim) {
-  float x[R][8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    float kf[8];
-    kf[0] = bf16_lo(kr[p].x); kf[1] = bf16_hi(kr[p].x);
-    kf[2] = bf16_lo(kr[p].y); kf[3] = bf16_hi(kr[p].y);
-    kf[4] = bf16_lo(kr[p].z); kf[5] = bf16_hi(kr[p].z);
-    kf[6] = bf16_lo(kr[p].w); kf[7] = bf16_hi(kr[p].w);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      // packed pairs: 4 FFMA2 + 1 FADD instead of 8 FFMA
-      float2 s2 = make_float2(qf[i][0] * kf[0], qf[i][1] * kf[1]);
-#pragma unroll
-      for (int e = 2; e < 8; e += 2)
-        s2 = ffma2(make_float2(qf[i][e], qf[i][e + 1]), make_float2(kf[e], kf[e + 1]), s2);
-      x[i][p] = s2.x + s2.y;
-    }
-    if (key0 + 2 * p + hw >= max_lim) vr[p] = make_uint4(0, 0, 0, 0);
-  }
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      float s = x[i][p];
-      s += __shfl_xor_sync(0xffffffffu, s, 8);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      const int key = key0 + 2 * p + hw;
-      x[i][p] = key < lim[i] ? s * scale_log2 : -INFINITY;
-    }
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    float cm = x[i][0];
-#pragma unroll
-    for (int p = 1; p < 8; ++p) cm = fmaxf(cm, x[i][p]);
-    if (cm == -INFINITY) continue;  // no valid key of this row in this chunk half
-    const float mn = fmaxf(st.m[i], cm);
-    const float al = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - mn);
-    st.m[i] = mn;
-    float ps = 0.f;
-    float a[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] = st.acc[i][e] * al;
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const float pr = fast_exp2(x[i][p] - mn);
-      ps += pr;
-      const float2 pp = make_float2(pr, pr);
-      float2 a01 = ffma2(pp, make_float2(bf16_lo(vr[p].x), bf16_hi(vr[p].x)), make_float2(a[0], a[1]));
-      float2 a23 = ffma2(pp, make_float2(bf16_lo(vr[p].y), bf16_hi(vr[p].y)), make_float2(a[2], a[3]));
-      float2 a45 = ffma2(pp, make_float2(bf16_lo(vr[p].z), bf16_hi(vr[p].z)), make_float2(a[4], a[5]));
-      float2 a67 = ffma2(pp, make_float2(bf16_lo(vr[p].w), bf16_hi(vr[p].w)), make_float2(a[6], a[7]));
-      a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
-      a[4] = a45.x; a[5] = a45.y; a[6] = a67.x; a[7] = a67.y;
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) st.acc[i][e] = a[e];
-    st.l[i] = st.l[i] * al + ps;
-  }
-}
-
-
-// Per-worker compute policies of ctx_cta_kernel: same interface, chosen by
-// the rows per item.  R <= 2 (decode): CUDA cores, a half-warp per key pair
-// (no padded MMA rows).  R >= 4: mma.sync tiles of 16 query rows.
-template <int R>
-struct SimtCompute {
-  float qf[R][8];
-  int lim_ctx[R], lim_pre[R];
-  RowState<R> st;
-
-  __device__ __forceinline__ void load(const uint8_t* qrows, const uint8_t* /*qzero*/,
-                                       const CtxItem<R>& it, int item, const CtxArgs& a, int lane) {
-    const int l16 = lane & 15, rbase = it.z * R;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const int li = rbase + i;
-      const bool ok = item >= 0 && it.n_chunks > 0 && li < it.nrows;
-      if (ok) {
-        const uint4 u = *reinterpret_cast<const uint4*>(qrows + i * kRowBytes + l16 * 16);
-        qf[i][0] = bf16_lo(u.x); qf[i][1] = bf16_hi(u.x);
-        qf[i][2] = bf16_lo(u.y); qf[i][3] = bf16_hi(u.y);
-        qf[i][4] = bf16_lo(u.z); qf[i][5] = bf16_hi(u.z);
-        qf[i][6] = bf16_lo(u.w); qf[i][7] = bf16_hi(u.w);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) qf[i][e] = 0.f;
-      }
-      lim_ctx[i] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
-      lim_pre[i] = ok ? a.s_prefix : 0;
-    }
-  }
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      st.m[i] = -INFINITY;
-      st.l[i] = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) st.acc[i][e] = 0.f;
-    }
-  }
-  __device__ __forceinline__ void chunk(const uint8_t* slot, int key0, bool pre, int max_lim,
-                                        bool /*mask*/, const CtxArgs& a, int lane) {
-    const int hw = lane >> 4, l16 = lane & 15;
-    uint4 kr[8], vr[8];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      const uint32_t off = slot_off(2 * p + hw, l16);
-      kr[p] = *reinterpret_cast<const uint4*>(slot + off);
-      vr[p] = *reinterpret_cast<const uint4*>(slot + kChunk * kRowBytes + off);
-    }
-    chunk_update<R>(st, qf, kr, vr, key0, hw, pre ? lim_pre : lim_ctx, a.scale_log2,
-                    pre ? a.s_prefix : max_lim);
-  }
-  // fold the two half-warp states, then half-warp 0 writes rows < R
-  __device__ __forceinline__ void handoff(float* macc, float* mml, int lane) {
-    const int hw = lane >> 4, l16 = lane & 15;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const float mo = __shfl_xor_sync(0xffffffffu, st.m[i], 16);
-      const float lo = __shfl_xor_sync(0xffffffffu, st.l[i], 16);
-      const float M = fmaxf(st.m[i], mo);
-      const float ws = (st.m[i] == -INFINITY) ? 0.f : fast_exp2(st.m[i] - M);
-      const float wo = (mo == -INFINITY) ? 0.f : fast_exp2(mo - M);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float ao = __shfl_xor_sync(0xffffffffu, st.acc[i][e], 16);
-        st.acc[i][e] = st.acc[i][e] * ws + ao * wo;
-      }
-      const float L = st.l[i] * ws + lo * wo;
-      if (hw == 0) {
-        *reinterpret_cast<float4*>(macc + i * 128 + l16 * 8) =
-            make_float4(st.acc[i][0], st.acc[i][1], st.acc[i][2], st.acc[i][3]);
-        *reinterpret_cast<float4*>(macc + i * 128 + l16 * 8 + 4) =
-            make_float4(st.acc[i][4], st.acc[i][5], st.acc[i][6], st.acc[i][7]);
-        if (l16 == 0) {
-          mml[i * 2] = M;
-          mml[i * 2 + 1] = L;
-        }
-      }
-    }
-  }
-};
-
-template <int R>
-struct MmaCompute {
-  uint32_t qa[8][4];
-  int lim_ctx[2], lim_pre[2];
-  MmaRowState st;
+struct SwapCompute {
+  static_assert(R >= 1 && R <= 8, "one N = 8 tile of query rows per item");
+  uint32_t qb[8][2];      // Q^T B fragments, 8 k-steps
+  float o[8][4];          // O^T accumulator, 8 m-tiles of 16 head dims
+  float m0, m1, l0, l1;   // columns 2t, 2t + 1: reference max (log2 units), partial row sum
+  int lim0, lim1;         // exclusive context-key bounds of columns 2t, 2t + 1
 
   __device__ __forceinline__ void load(const uint8_t* qrows, const uint8_t* qzero,
                                        const CtxItem<R>& it, int item, const CtxArgs& a, int lane) {
-    // Q rows as MMA A fragments (rows past R read the zero row)
-    const int qrow = (lane & 7) + ((lane >> 3) & 1) * 8;
-    const uint32_t qaddr = qrow < R ? smem_u32(qrows + qrow * kRowBytes) : smem_u32(qzero);
+    // B fragments of Q^T: ldmatrix (non-transposed) of the Q rows; matrix j
+    // of an x4 is k-step 2kp + (j >> 1), half (j & 1); rows >= R read zeros
+    const int qr = lane & 7, j = lane >> 3;
+    const uint32_t qaddr = qr < R ? smem_u32(qrows + qr * kRowBytes) : smem_u32(qzero);
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) ldsm_x4(qa[ks], qaddr + ((ks * 2 + (lane >> 4)) << 4));
-    const int g8 = lane >> 2, rbase = it.z * R;
-#pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int rr = g8 + 8 * hr, li = rbase + rr;
-      const bool ok = item >= 0 && it.n_chunks > 0 && rr < R && li < it.nrows;
-      lim_ctx[hr] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : 0;
-      lim_pre[hr] = ok ? a.s_prefix : 0;
+    for (int kp = 0; kp < 4; ++kp) {
+      uint32_t r[4];
+      ldsm_x4(r, qaddr + ((4 * kp + j) << 4));
+      qb[2 * kp][0] = r[0];
+      qb[2 * kp][1] = r[1];
+      qb[2 * kp + 1][0] = r[2];
+      qb[2 * kp + 1][1] = r[3];
     }
+    const int rbase = it.z * R, t = lane & 3;
+    int lim[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int rr = 2 * t + c, li = rbase + rr;
+      const bool ok = item >= 0 && it.n_chunks > 0 && rr < R && li < it.nrows;
+      // columns past the item's rows see every key (finite, never written)
+      lim[c] = ok ? (a.causal ? it.c_r - it.m_r + li / a.g + 1 : it.c_r) : it.max_lim;
+    }
+    lim0 = lim[0];
+    lim1 = lim[1];
   }
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt)
+    for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) st.o[nt][e] = 0.f;
-    st.m[0] = st.m[1] = -INFINITY;
-    st.l[0] = st.l[1] = 0.f;
+      for (int e = 0; e < 4; ++e) o[mt][e] = 0.f;
+    m0 = m1 = -INFINITY;
+    l0 = l1 = 0.f;
   }
-  __device__ __forceinline__ void chunk(const uint8_t* slot, int key0, bool pre, int /*max_lim*/,
+  // one 16-key chunk in ring slot `slot` ([K|V][16 rows][256 B], 16-byte
+  // columns XOR-swizzled by row & 7); key0: the chunk's first key inside
+  // its segment; mask: some key of the chunk is past some row's bound
+  __device__ __forceinline__ void chunk(const uint8_t* slot_p, int key0, bool pre, int /*max_lim*/,
                                         bool mask, const CtxArgs& a, int lane) {
-    chunk_mma(st, qa, smem_u32(slot), lane, key0, pre ? lim_pre[0] : lim_ctx[0],
-              pre ? lim_pre[1] : lim_ctx[1], a.scale_log2, mask);
+    const uint32_t slot = smem_u32(slot_p);
+    const int g = lane >> 2, t = lane & 3, j = lane >> 3, r8 = lane & 7;
+    // ---- S^T = K Q^T: two accumulators (even / odd k-steps) for ILP
+    float sa[4], sb[4];
+    {
+      const int key = r8 + 8 * (j & 1);
+      const uint32_t kaddr = slot + key * kRowBytes;
+      uint32_t ka[4];
+      ldsm_x4(ka, kaddr + (((0 + (j >> 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816_zero(sa, ka, qb[0][0], qb[0][1]);
+      ldsm_x4(ka, kaddr + (((2 + (j >> 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816_zero(sb, ka, qb[1][0], qb[1][1]);
+#pragma unroll
+      for (int ks = 2; ks < 8; ks += 2) {
+        ldsm_x4(ka, kaddr + (((2 * ks + (j >> 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(sa, ka, qb[ks][0], qb[ks][1]);
+        ldsm_x4(ka, kaddr + (((2 * ks + 2 + (j >> 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(sb, ka, qb[ks + 1][0], qb[ks + 1][1]);
+      }
+    }
+    // s[0], s[1]: key g, columns 2t, 2t+1; s[2], s[3]: key g + 8
+    float s[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) s[e] = (sa[e] + sb[e]) * a.scale_log2;
+    if (mask) {
+      // the shared prefix (naive baseline) is visible to every row
+      const int b0 = pre ? a.s_prefix : lim0, b1 = pre ? a.s_prefix : lim1;
+      if (key0 + g >= b0) s[0] = -INFINITY;
+      if (key0 + g >= b1) s[1] = -INFINITY;
+      if (key0 + g + 8 >= b0) s[2] = -INFINITY;
+      if (key0 + g + 8 >= b1) s[3] = -INFINITY;
+    }
+    // ---- lazy online softmax per column (reduce over the 8 key lanes)
+    float cm[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 4));
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 8));
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 16));
+    }
+    const bool up0 = cm[0] > m0 + kCtxTau, up1 = cm[1] > m1 + kCtxTau;
+    if (__any_sync(0xffffffffu, up0 || up1)) {
+      const float al0 = up0 ? ((m0 == -INFINITY) ? 0.f : fast_exp2(m0 - cm[0])) : 1.f;
+      const float al1 = up1 ? ((m1 == -INFINITY) ? 0.f : fast_exp2(m1 - cm[1])) : 1.f;
+      if (up0) m0 = cm[0];
+      if (up1) m1 = cm[1];
+      l0 *= al0;
+      l1 *= al1;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= al0;
+        o[mt][1] *= al1;
+        o[mt][2] *= al0;
+        o[mt][3] *= al1;
+      }
+    }
+    const float r0 = (m0 == -INFINITY) ? 0.f : m0, r1 = (m1 == -INFINITY) ? 0.f : m1;
+    const float p0 = fast_exp2(s[0] - r0), p1 = fast_exp2(s[1] - r1);
+    const float p2 = fast_exp2(s[2] - r0), p3 = fast_exp2(s[3] - r1);
+    // P^T (keys x rows) to the B-operand layout: the accumulator pairs
+    // (key g, rows 2t..2t+1) transpose to (keys 2t..2t+1, row g)
+    const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p0, p1));
+    const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p2, p3));
+    l0 += p0 + p2;
+    l1 += p1 + p3;
+    // ---- O^T += V^T P^T: A = V^T via transposed ldmatrix of the V rows
+    {
+      const int key = r8 + 8 * (j >> 1);
+      const uint32_t vaddr = slot + kChunk * kRowBytes + key * kRowBytes;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t va[4];
+        ldsm_x4_trans(va, vaddr + (((2 * mt + (j & 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(o[mt], va, pb0, pb1);
+      }
+    }
   }
+  // reduce the row sums over the key lanes, then write rows < R of this
+  // worker's state: macc [R][kAccStride] (unnormalised O), mml [R][2]
   __device__ __forceinline__ void handoff(float* macc, float* mml, int lane) {
-    const int g8 = lane >> 2, tq = lane & 3;
+    const int g = lane >> 2, t = lane & 3;
+    float ls[2] = {l0, l1};
+    const float ms[2] = {m0, m1};
 #pragma unroll
-    for (int hr = 0; hr < 2; ++hr) {
-      const int rr = g8 + 8 * hr;
+    for (int c = 0; c < 2; ++c) {
+      ls[c] += __shfl_xor_sync(0xffffffffu, ls[c], 4);
+      ls[c] += __shfl_xor_sync(0xffffffffu, ls[c], 8);
+      ls[c] += __shfl_xor_sync(0xffffffffu, ls[c], 16);
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int rr = 2 * t + c;
       if (rr < R) {
+        float* row = macc + rr * kAccStride;
 #pragma unroll
-        for (int nt = 0; nt < 16; ++nt)
-          *reinterpret_cast<float2*>(macc + rr * 128 + nt * 8 + 2 * tq) =
-              make_float2(st.o[nt][2 * hr], st.o[nt][2 * hr + 1]);
-        if (tq == 0) {
-          mml[rr * 2] = st.m[hr];
-          mml[rr * 2 + 1] = st.l[hr];
+        for (int mt = 0; mt < 8; ++mt) {
+          row[16 * mt + g] = o[mt][c];
+          row[16 * mt + g + 8] = o[mt][2 + c];
+        }
+        if (g == 0) {
+          mml[rr * 2] = ms[c];
+          mml[rr * 2 + 1] = ls[c];
         }
       }
     }
@@ -420,7 +286,7 @@ struct MmaCompute {
 };
 
 template <int R>
-using CtxCompute = typename std::conditional<(R <= 2), SimtCompute<R>, MmaCompute<R>>::type;
+using CtxCompute = SwapCompute<R>;
 
 // Relay fusion of one (row, head) pair (`relay_fusion`, attention.py:137-157):
 // the context state (O unnormalised, m log2, l) merged with every stream-K
@@ -513,6 +379,7 @@ __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, 
   const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
   const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
   const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+  if (u >= SP.n_units) return false;  // outside the plan (bad q_start): parked, then dropped
   const int np = rb_unit_parts(&SP, u);
   int ok = 1;
   if (lane == 0) {
@@ -531,7 +398,7 @@ __device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int 
   const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
   const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
   const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
-  return (pub >> u) & 1;
+  return u < 64 && ((pub >> u) & 1);
 }
 
 constexpr int kWorkers = 4;
@@ -559,8 +426,9 @@ __device__ __forceinline__ void relay_fuse_parked8(const rb_sys_plan& SP, int hq
     const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
     col = static_cast<int>(f % SP.nq);
     u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
-    np = rb_unit_parts(&SP, u);
-    if (sub == 0)
+    valid = u < SP.n_units;  // a row outside the plan (bad q_start) is dropped, never awaited
+    np = valid ? rb_unit_parts(&SP, u) : 0;
+    if (sub == 0 && valid)
       while (ld_acquire_gpu(ready + u) < np) __nanosleep(64);
   }
   __syncwarp();
@@ -619,7 +487,7 @@ template <int R>
 struct ItemSlot {
   CtxItem<R> it;
   int item;                                    // -1: no more work
-  int bt[32];                                  // block ids of context blocks 0..31
+  int bt[32];                                  // block ids of context blocks it.bt0 .. it.bt0 + 31
 };
 
 template <int R>
@@ -627,15 +495,28 @@ struct CtaSmem {
   // [kIQ][R][128] bf16 query rows, then one zero row (MMA rows past R)
   static constexpr int kOffQ = kWorkers * kDepth * kSlotBytes;
   static constexpr int kOffQZero = kOffQ + kIQ * R * kRowBytes;
-  static constexpr int kOffAcc = kOffQZero + kRowBytes;                  // [kNB][kWorkers][R][128] f32
-  static constexpr int kOffML = kOffAcc + kNB * kWorkers * R * 128 * 4;  // [kNB][kWorkers][R][2]
-  static constexpr int kOffMIt = (kOffML + kNB * kWorkers * R * 8 + 15) & ~15;  // [kNB] CtxItem
-  static constexpr int kOffItems =
-      (kOffMIt + kNB * static_cast<int>(sizeof(CtxItem<R>)) + 15) & ~15;  // [kIQ] ItemSlot
+  static constexpr int kOffAcc = kOffQZero + kRowBytes;  // [kNB][kWorkers][R][kAccStride] f32
+  static constexpr int kOffML = kOffAcc + kNB * kWorkers * R * kAccStride * 4;  // [kNB][kWorkers][R][2]
+  static constexpr int kOffItems = (kOffML + kNB * kWorkers * R * 8 + 15) & ~15;  // [kIQ] ItemSlot
   static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
   static constexpr int kOffDefer = kOffBar + (3 * kIQ + 2 * kNB) * 8;  // [1 + kMaxDefer] int
   static constexpr int kBytes = kOffDefer + (1 + kMaxDefer) * 4;
 };
+
+// Merge two unnormalised softmax states (O, m log2, l) -- the merge of
+// `relay_fusion` (attention.py:137-157) without the normalisation.
+__device__ __forceinline__ void merge_state(float4& O, float& m, float& l, float4 Ok, float mk, float lk) {
+  const float mn = fmaxf(m, mk);
+  if (mn == -INFINITY) return;
+  const float so = (m == -INFINITY) ? 0.f : fast_exp2(m - mn);
+  const float sk = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mn);
+  l = l * so + lk * sk;
+  O.x = O.x * so + Ok.x * sk;
+  O.y = O.y * so + Ok.y * sk;
+  O.z = O.z * so + Ok.z * sk;
+  O.w = O.w * so + Ok.w * sk;
+  m = mn;
+}
 
 template <int R>
 __global__ void __launch_bounds__(kCtxThreadsPC, 2)
@@ -644,6 +525,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
+  const int n_split = a.n_split;
   float* s_acc = reinterpret_cast<float*>(smem + SM::kOffAcc);
   float* s_ml = reinterpret_cast<float*>(smem + SM::kOffML);
   ItemSlot<R>* iq = reinterpret_cast<ItemSlot<R>*>(smem + SM::kOffItems);
@@ -666,7 +548,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     }
     fence_mbar_init();
   }
-  // the zero query row stands in for MMA rows past R (16-row tiles)
+  // the zero query row stands in for MMA rows past R
   if (threadIdx.x < kRowBytes / 16)
     reinterpret_cast<uint4*>(smem + SM::kOffQZero)[threadIdx.x] = make_uint4(0, 0, 0, 0);
   __syncthreads();
@@ -685,26 +567,36 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     // counter (the first three in one atomic), so CTAs that start late --
     // after the concurrent system kernel frees their SM -- still share the
     // remaining work; without it the order is static (b + k * grid).
+    // Item = ((request * hkv + head) * n_z + row tile) * n_split + split.
     int* sched = a.sched;
-    const int bt_lanes = a.ctx.block_table != nullptr ? min(32, a.ctx.bt_stride) : 0;
+    const bool paged = a.ctx.block_table != nullptr;
+    const int per_req = n_z * a.hkv * n_split;
     struct Raw {
-      int item, qs0, qs1, clen, bte;
+      int item, qs0, qs1, clen, bte, bt0;
       long long roff;
     };
     auto load_raw = [&](int item) {
       Raw w;
       w.item = item;
-      w.qs0 = w.qs1 = w.clen = w.bte = 0;
+      w.qs0 = w.qs1 = w.clen = w.bte = w.bt0 = 0;
       w.roff = 0;
       if (item < n_items) {
-        const int r = item / (n_z * a.hkv);
+        const int r = item / per_req;
+        const int sp = item % n_split;
         w.qs0 = __ldg(a.q_start + r);
         w.qs1 = __ldg(a.q_start + r + 1);
         w.clen = __ldg(a.ctx_lens + r);
         if (a.ctx.req_offset != nullptr) w.roff = __ldg(a.ctx.req_offset + r);
-        // rows of the table are bt_stride long: the first min(32, bt_stride) are in bounds
-        if (lane < bt_lanes)
-          w.bte = __ldg(a.ctx.block_table + static_cast<long long>(r) * a.ctx.bt_stride + lane);
+        if (paged) {
+          // the split's first context block (splits start on chunk
+          // boundaries; a chunk never straddles blocks when block_size % 16
+          // == 0, the only case the table window is used for)
+          const int c0 = max(0, sp * a.split_chunks - n_pre) * kChunk;
+          w.bt0 = c0 / a.ctx.block_size;
+          // rows of the table are bt_stride long: entries past it are never read
+          if (w.bt0 + lane < a.ctx.bt_stride)
+            w.bte = __ldg(a.ctx.block_table + static_cast<long long>(r) * a.ctx.bt_stride + w.bt0 + lane);
+        }
       }
       return w;
     };
@@ -737,22 +629,37 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         break;
       }
       CtxItem<R> it;
-      it.z = item % n_z;
-      it.h = (item / n_z) % a.hkv;
-      it.r = item / (n_z * a.hkv);
+      it.sp = item % n_split;
+      const int grp = item / n_split;
+      it.grp = grp;
+      it.z = grp % n_z;
+      it.h = (grp / n_z) % a.hkv;
+      it.r = grp / (n_z * a.hkv);
       it.row0 = cur.qs0;
       it.m_r = cur.qs1 - cur.qs0;
       it.nrows = it.m_r * a.g;
       it.c_r = cur.clen;
       it.roff = cur.roff;
+      it.bt0 = cur.bt0;
       const int rbase = it.z * R;
+      it.k0 = 0;
+      it.nsplit = 1;
       if (rbase >= it.nrows) {
         it.max_lim = 0;
         it.n_chunks = 0;
       } else {
         const int t_last = (min(rbase + R, it.nrows) - 1) / a.g;
         it.max_lim = a.causal ? it.c_r - it.m_r + t_last + 1 : it.c_r;
-        it.n_chunks = n_pre + (it.max_lim + kChunk - 1) / kChunk;
+        const int total = n_pre + (it.max_lim + kChunk - 1) / kChunk;
+        it.n_chunks = total;
+        if (n_split > 1) {
+          // split sp: chunks [sp L, (sp+1) L), the last valid split takes the rest
+          const int L = a.split_chunks;
+          it.nsplit = min(n_split, max(1, (total + L - 1) / L));
+          it.k0 = it.sp * L;
+          it.n_chunks = it.sp >= it.nsplit ? 0
+                        : (it.sp == it.nsplit - 1 ? total - it.k0 : L);
+        }
       }
       const int nvalid = it.n_chunks > 0 ? max(0, min(R, it.nrows - rbase)) : 0;
       slot.bt[lane] = cur.bte;
@@ -793,9 +700,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     // --------------------------------------------------------------- merger
     // Walks the item queue like the workers (metadata only), waits for the
     // workers' states of each item (m_full), combines them (lane = 4 head
-    // dims) and writes: the relay context partial (unnormalised O, m, l) to
-    // the workspace, or the final output (+ optional fusion with a given
-    // system partial o_sys / lse_sys).
+    // dims) and finishes each row: split items park their partial in the
+    // split workspace and the last split of the item combines all of them
+    // in split order; then either the relay fusion with the system parts
+    // (or parking the context partial until its system unit is published),
+    // or the final output (+ optional fusion with a given o_sys / lse_sys).
     bool waited = false;
     int jp = 0;  // queue cursor
     // diagnostics (debug timestamps only): waits and work of the merger
@@ -813,6 +722,64 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       if (np0 != 0x7fffffff) pv0 = ld_acquire_gpu(a.sys_ready + lane);
       if (np1 != 0x7fffffff) pv1 = ld_acquire_gpu(a.sys_ready + lane + 32);
     }
+    const int d0 = lane * 4;
+    int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
+
+    // the last step of a (row, head): relay fusion / park, or output
+    auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts& pp) {
+      if (a.ctx_part != nullptr) {
+        const bool full = defer[0] >= kMaxDefer;
+        if (use_pre) {
+          relay_fuse_finish(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
+                            a.out_fp32, a.lse_out, lane);
+        } else if (poll ? (relay_unit_published(a.sys_plan, a.hq, oidx, pub) ||
+                           (full && relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, true)))
+                        : relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
+          relay_fuse_pair(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
+                          a.out_fp32, a.lse_out, lane);
+        } else {
+          float* dst = a.ctx_part + oidx * kPartStride;
+          __stcg(reinterpret_cast<float4*>(dst + d0), O);
+          if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
+          __syncwarp();
+          if (lane == 0) defer[1 + defer[0]++] = static_cast<int>(oidx);
+          __syncwarp();
+        }
+        return;
+      }
+      float o[4] = {O.x, O.y, O.z, O.w};
+      float lse2;
+      {
+        const float inv = (Ls > 0.f) ? 1.f / Ls : 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] *= inv;
+        lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
+      }
+      if (a.o_sys != nullptr) {
+        const float ls2 = __ldcg(a.lse_sys + oidx) * kLog2e;
+        const float4 sv = __ldcg(reinterpret_cast<const float4*>(a.o_sys + oidx * 128 + d0));
+        const float mx = fmaxf(ls2, lse2);
+        const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
+        const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
+        const float inv = 1.f / (wc + ws);
+        o[0] = (wc * o[0] + ws * sv.x) * inv;
+        o[1] = (wc * o[1] + ws * sv.y) * inv;
+        o[2] = (wc * o[2] + ws * sv.z) * inv;
+        o[3] = (wc * o[3] + ws * sv.w) * inv;
+        lse2 = mx + __log2f(wc + ws);
+      }
+      if (a.out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx * 128 + d0) =
+            make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+        uint2 pk;
+        pk.x = pack_bf16x2(o[0], o[1]);
+        pk.y = pack_bf16x2(o[2], o[3]);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + oidx * 128 + d0) = pk;
+      }
+      if (a.lse_out != nullptr && lane == 0) a.lse_out[oidx] = lse2 * kLn2;
+    };
+
     for (int mi = 0;; ++mi) {
       // next non-empty item off the queue
       int item = -1;
@@ -830,6 +797,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         if (item < 0 || it.n_chunks > 0) break;
       }
       if (item < 0) break;
+      const bool split = it.nsplit > 1;
       // relay: if row 0's system unit is already published, issue its
       // parts' loads now so they land while the workers finish the item
       bool pre = false;
@@ -844,7 +812,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         if (np1 != 0x7fffffff && !((pub >> (lane + 32)) & 1))
           pv1 = ld_acquire_gpu(a.sys_ready + lane + 32);
       }
-      if (a.ctx_part != nullptr && it.z * R < it.nrows) {
+      if (a.ctx_part != nullptr && !split && it.z * R < it.nrows) {
         const long long o0 = static_cast<long long>(it.row0 + (it.z * R) / a.g) * a.hq +
                              it.h * a.g + (it.z * R) % a.g;
         pre = poll ? relay_unit_published(a.sys_plan, a.hq, o0, pub)
@@ -866,92 +834,75 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         d_mfull += t1 - d_t;
         d_t = t1;
       }
-      const float* bacc = s_acc + mb * kWorkers * R * 128;
+      const float* bacc = s_acc + mb * kWorkers * R * kAccStride;
       const float* bml = s_ml + mb * kWorkers * R * 2;
       const int rbase = it.z * R;
-      const int d0 = lane * 4;
+      const int nrow = min(R, it.nrows - rbase);
 #pragma unroll 1
-      for (int i = 0; i < R; ++i) {
+      for (int i = 0; i < nrow; ++i) {
         const int li = rbase + i;
-        if (li >= it.nrows) break;
         const int t = li / a.g, jj = li % a.g;
         const long long oidx = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
         float M = -INFINITY;
 #pragma unroll
         for (int k = 0; k < kWorkers; ++k) M = fmaxf(M, bml[(k * R + i) * 2]);
-        float Ls = 0.f, O[4] = {0.f, 0.f, 0.f, 0.f};
+        float Ls = 0.f;
+        float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
         if (M != -INFINITY) {
 #pragma unroll
           for (int k = 0; k < kWorkers; ++k) {
             const float mk = bml[(k * R + i) * 2];
             const float wt = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
             Ls = fmaf(bml[(k * R + i) * 2 + 1], wt, Ls);
-            const float4 av = *reinterpret_cast<const float4*>(bacc + (k * R + i) * 128 + d0);
-            O[0] = fmaf(av.x, wt, O[0]);
-            O[1] = fmaf(av.y, wt, O[1]);
-            O[2] = fmaf(av.z, wt, O[2]);
-            O[3] = fmaf(av.w, wt, O[3]);
+            const float4 av = *reinterpret_cast<const float4*>(bacc + (k * R + i) * kAccStride + d0);
+            O.x = fmaf(av.x, wt, O.x);
+            O.y = fmaf(av.y, wt, O.y);
+            O.z = fmaf(av.z, wt, O.z);
+            O.w = fmaf(av.w, wt, O.w);
           }
         }
-        if (a.ctx_part != nullptr) {
-          // relay: fuse now if the pair's system unit is published, else
-          // park the unnormalised partial and fuse it at the end of the CTA
-          int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
-          const bool full = defer[0] >= kMaxDefer;
-          if (i == 0 && pre) {
-            relay_fuse_finish(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml,
-                              make_float4(O[0], O[1], O[2], O[3]), M, Ls, a.out, a.out_fp32,
-                              a.lse_out, lane);
-          } else if (poll ? (relay_unit_published(a.sys_plan, a.hq, oidx, pub) ||
-                             (full && relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, true)))
-                          : relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
-            relay_fuse_pair(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml,
-                            make_float4(O[0], O[1], O[2], O[3]), M, Ls, a.out, a.out_fp32,
-                            a.lse_out, lane);
-          } else {
-            float* dst = a.ctx_part + oidx * kPartStride;
-            __stcg(reinterpret_cast<float4*>(dst + d0), make_float4(O[0], O[1], O[2], O[3]));
-            if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
-            __syncwarp();
-            if (lane == 0) defer[1 + defer[0]++] = static_cast<int>(oidx);
-            __syncwarp();
-          }
-          continue;
-        }
-        float o[4];
-        float lse2;
-        {
-          const float inv = (Ls > 0.f) ? 1.f / Ls : 0.f;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) o[e] = O[e] * inv;
-          lse2 = (Ls > 0.f) ? M + __log2f(Ls) : -INFINITY;
-        }
-        if (a.o_sys != nullptr) {
-          const float ls2 = __ldcg(a.lse_sys + oidx) * kLog2e;
-          const float4 sv = __ldcg(reinterpret_cast<const float4*>(a.o_sys + oidx * 128 + d0));
-          const float mx = fmaxf(ls2, lse2);
-          const float wc = (lse2 == -INFINITY) ? 0.f : fast_exp2(lse2 - mx);
-          const float ws = (ls2 == -INFINITY) ? 0.f : fast_exp2(ls2 - mx);
-          const float inv = 1.f / (wc + ws);
-          o[0] = (wc * o[0] + ws * sv.x) * inv;
-          o[1] = (wc * o[1] + ws * sv.y) * inv;
-          o[2] = (wc * o[2] + ws * sv.z) * inv;
-          o[3] = (wc * o[3] + ws * sv.w) * inv;
-          lse2 = mx + __log2f(wc + ws);
-        }
-        if (a.out_fp32) {
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx * 128 + d0) =
-              make_float4(o[0], o[1], o[2], o[3]);
+        if (split) {
+          float* dst = a.split_part + (oidx * n_split + it.sp) * kPartStride;
+          __stcg(reinterpret_cast<float4*>(dst + d0), O);
+          if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
         } else {
-          uint2 pk;
-          pk.x = pack_bf16x2(o[0], o[1]);
-          pk.y = pack_bf16x2(o[2], o[3]);
-          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + oidx * 128 + d0) = pk;
+          finish(O, M, Ls, oidx, i == 0 && pre, pp);
         }
-        if (a.lse_out != nullptr && lane == 0) a.lse_out[oidx] = lse2 * kLn2;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&m_empty[mb]);
+      if (split) {
+        // the last split of the item to finish combines every split's
+        // partial in split order (bitwise independent of the arrival order)
+        int last = 0;
+        if (lane == 0) {
+          __threadfence();
+          last = atomicAdd(a.split_cnt + it.grp, 1) == it.nsplit - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+#pragma unroll 1
+          for (int i = 0; i < nrow; ++i) {
+            const int li = rbase + i;
+            const int t = li / a.g, jj = li % a.g;
+            const long long oidx = static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
+            const float* src = a.split_part + oidx * n_split * kPartStride;
+            float4 O = __ldcg(reinterpret_cast<const float4*>(src + d0));
+            float2 ml = __ldcg(reinterpret_cast<const float2*>(src + 128));
+            float M = ml.x, Ls = ml.y;
+            for (int k = 1; k < it.nsplit; ++k) {
+              const float* sk = src + k * kPartStride;
+              const float4 Ok = __ldcg(reinterpret_cast<const float4*>(sk + d0));
+              const float2 mlk = __ldcg(reinterpret_cast<const float2*>(sk + 128));
+              merge_state(O, M, Ls, Ok, mlk.x, mlk.y);
+            }
+            finish(O, M, Ls, oidx, false, pp);
+          }
+          __syncwarp();
+          if (lane == 0) a.split_cnt[it.grp] = 0;  // rearm for the next launch
+        }
+      }
       if (dts) d_work += global_timer_ns() - d_t;
     }
     if (dts && lane == 0) {
@@ -965,12 +916,12 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   } else {
   // ---------------------------------------------------------------- workers
   const int w = warp - 1;                       // 0 .. kWorkers-1
-  const uint32_t ring = smem_u32(smem + w * kDepth * kSlotBytes);
   uint8_t* ring_p = smem + w * kDepth * kSlotBytes;
 
-  // issue cursor: queue item ji, next chunk ki (= w mod kWorkers)
-  int ji = 0, ki = w, iss_item = 0, iss_bte = 0;
-  int iss_r = 0, iss_h = 0, iss_lim = 0, iss_nch = 0;
+  // issue cursor: queue item ji, next chunk ki (= w mod kWorkers), local to
+  // the item's split; the global chunk index is iss_k0 + ki
+  int ji = 0, ki = w, iss_item = 0, iss_bte = 0, iss_bt0 = 0;
+  int iss_r = 0, iss_h = 0, iss_lim = 0, iss_nch = 0, iss_k0 = 0;
   long long iss_roff = 0;
   bool have_iss = false;
   int issued = 0, consumed = 0, iss_sl = 0;
@@ -992,6 +943,8 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         iss_h = iq[qs].it.h;
         iss_lim = iq[qs].it.max_lim;
         iss_nch = iq[qs].it.n_chunks;
+        iss_k0 = iq[qs].it.k0;
+        iss_bt0 = iq[qs].it.bt0;
         iss_roff = iq[qs].it.roff;
         iss_bte = iq[qs].bt[lane];
         have_iss = true;
@@ -1003,7 +956,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         have_iss = false;
         continue;
       }
-      const int k = ki;
+      const int k = iss_k0 + ki;
       uint8_t* dst = ring_p + iss_sl * kSlotBytes;
       const __nv_bfloat16 *kb = a.ctx.k, *vb = a.ctx.v;
       long long tok_stride = a.ctx.stride_tok;
@@ -1024,10 +977,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
           off = (iss_roff + t0) * a.ctx.stride_tok;
         } else if (a.ctx.block_size % kChunk == 0) {
           const int bi = t0 / a.ctx.block_size;
-          const int v0 = __shfl_sync(0xffffffffu, iss_bte, bi & 31);
-          const int blk = bi < 32 ? v0
-                                  : __ldg(a.ctx.block_table +
-                                          static_cast<long long>(iss_r) * a.ctx.bt_stride + bi);
+          const int v0 = __shfl_sync(0xffffffffu, iss_bte, (bi - iss_bt0) & 31);
+          const int blk = (bi - iss_bt0 >= 0 && bi - iss_bt0 < 32)
+                              ? v0
+                              : __ldg(a.ctx.block_table +
+                                      static_cast<long long>(iss_r) * a.ctx.bt_stride + bi);
           off = static_cast<long long>(blk) * a.ctx.stride_block +
                 static_cast<long long>(t0 % a.ctx.block_size) * a.ctx.stride_tok;
         } else {
@@ -1093,8 +1047,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       else
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();  // every lane's copies of the chunk are visible to the warp
-      const bool pre = k < n_pre;
-      const int key0 = (pre ? k : k - n_pre) * kChunk;
+      const int kg = it.k0 + k;
+      const bool pre = kg < n_pre;
+      const int key0 = (pre ? kg : kg - n_pre) * kChunk;
       const bool mask = key0 + kChunk > (pre ? a.s_prefix : ctx_nomask);
       cmp.chunk(ring_p + con_sl * kSlotBytes, key0, pre, it.max_lim, mask, a, lane);
       __syncwarp();  // every lane's reads precede the refill of this slot
@@ -1110,7 +1065,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     if (dts) d_t = global_timer_ns();
     mbar_wait(&m_empty[mb], mph ^ 1);
     if (dts) d_mempty += global_timer_ns() - d_t;
-    float* macc = s_acc + (mb * kWorkers + w) * R * 128;
+    float* macc = s_acc + (mb * kWorkers + w) * R * kAccStride;
     float* mml = s_ml + (mb * kWorkers + w) * R * 2;
     cmp.handoff(macc, mml, lane);
     __syncwarp();
@@ -1176,20 +1131,20 @@ static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStre
   return cudaGetLastError();
 }
 
+int ctx_resident_ctas(int sms) { return 2 * sms; }
+
 cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_t stream) {
   // max_rows = max over requests of m_r * g
-  int R = 1;
-  if (max_rows >= 8) R = 8;
-  else if (max_rows >= 4) R = 4;
-  else if (max_rows >= 2) R = 2;
+  const int R = rb_ctx_rows(max_rows);
   const int n_z = (max_rows + R - 1) / R;
-  const int n_items = a.b * a.hkv * n_z;
+  const long long n_items = static_cast<long long>(a.b) * a.hkv * n_z * a.n_split;
   if (n_items == 0) return cudaSuccess;
+  if (n_items > 0x7fffffffLL) return cudaErrorInvalidValue;
   switch (R) {
-    case 1: return launch_ctx_r<1>(a, n_items, n_z, stream);
-    case 2: return launch_ctx_r<2>(a, n_items, n_z, stream);
-    case 4: return launch_ctx_r<4>(a, n_items, n_z, stream);
-    default: return launch_ctx_r<8>(a, n_items, n_z, stream);
+    case 1: return launch_ctx_r<1>(a, static_cast<int>(n_items), n_z, stream);
+    case 2: return launch_ctx_r<2>(a, static_cast<int>(n_items), n_z, stream);
+    case 4: return launch_ctx_r<4>(a, static_cast<int>(n_items), n_z, stream);
+    default: return launch_ctx_r<8>(a, static_cast<int>(n_items), n_z, stream);
   }
 }
 

@@ -65,9 +65,11 @@ struct CtxArgs {
   float scale_log2;
   unsigned long long* debug_ts;  // optional per-CTA stamps [grid][8] (diagnostics)
   int* sched;                    // optional [3] zeroed counters: item claims, scheduler / CTA exits
+  // split-K over long contexts (rb_ctx_split): split_chunks 16-token chunks
+  // per split (0: no split), n_split splits per (request, kv head, row tile)
+  int split_chunks, n_split;
+  float* split_part;             // [n_rows * hq][n_split][132] f32 partials (O, m log2, l)
+  int* split_cnt;                // [b * hkv * n_z] zeroed counters, rearmed by the last split
 };
-
-// Host-side tuning knobs (rb_debug_set_knob): reserved for A/B comparisons
-// of launch-side choices; no kernel reads them in this build.
 
 }  // namespace rb

@@ -159,3 +159,45 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   if (g > sms) g = sms;
   return g;
 }
+
+// Context split-K (rb_context_attention / rb_relay_attention): the context
+// kernel's work items are (request, kv head, row tile); with few of them
+// (small batches, long contexts) one item would be streamed by one CTA while
+// most SMs idle, so each item's 16-token chunks are cut into splits of
+// `chunks` chunks (the last split of a request takes the remainder), combined
+// in split order by the last split to finish (deterministic).
+// max_chunks = prefix chunks + ceil(max context tokens / 16); resident =
+// CTAs the context kernel keeps resident (2 per SM).  chunks == 0: no split.
+#define RB_CTX_CHUNK 16
+#define RB_CTX_SPLIT_MIN_CHUNKS 8   /* >= 2 chunks per worker warp */
+RB_HD void rb_ctx_split(long long base_items, int max_chunks, int resident, int* chunks,
+                        int* n_split) {
+  *chunks = 0;
+  *n_split = 1;
+  if (base_items < 1 || max_chunks < 2 * RB_CTX_SPLIT_MIN_CHUNKS) return;
+  if (base_items >= 2LL * resident) return;
+  const long long want = (2LL * resident + base_items - 1) / base_items;   // splits per item
+  int L = (int)((max_chunks + want - 1) / want);
+  if (L < RB_CTX_SPLIT_MIN_CHUNKS) L = RB_CTX_SPLIT_MIN_CHUNKS;
+  const int ns = (max_chunks + L - 1) / L;
+  if (ns < 2) return;
+  *chunks = L;
+  *n_split = ns;
+}
+
+// rows per work item (R) and row tiles per (request, kv head) for a batch
+// whose largest request has max_rows = m_r * g query rows per kv head
+RB_HD int rb_ctx_rows(int max_rows) {
+  return max_rows >= 8 ? 8 : max_rows >= 4 ? 4 : max_rows >= 2 ? 2 : 1;
+}
+
+// workspace bytes of the context split: partials [n_rows * hq][n_split][132]
+// f32 + one counter per (request, kv head, row tile), 256-aligned sections
+RB_HD long long rb_ctx_split_bytes(int b, int n_rows, int hq, int hkv, int max_rows, int n_split) {
+  if (n_split < 2) return 0;
+  const int R = rb_ctx_rows(max_rows);
+  const long long n_z = (max_rows + R - 1) / R;
+  const long long part = ((long long)n_rows * hq * n_split * 132 * 4 + 255) & ~255LL;
+  const long long cnt = ((long long)b * hkv * n_z * 4 + 255) & ~255LL;
+  return part + cnt;
+}

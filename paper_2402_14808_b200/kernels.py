@@ -35,17 +35,24 @@ def sm_count(device=None) -> int:
     return _lib.sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
 
 
-def workspace(nbytes: int, device, stream_key: int, kind: str = "sys") -> torch.Tensor:
+def workspace(nbytes: int, device, stream_key: int, kind: str = "sys", layout=None) -> torch.Tensor:
     """Zero-initialised scratch, cached per (kind, device, stream).  kind
     "sys": rb_system_attention's stream-K partials + semaphores (the kernel
     leaves the semaphores zeroed, so the buffer is reusable without
-    clearing); kind "relay": rb_relay_attention's unmerged partial slots."""
+    clearing); kind "relay": rb_relay_attention's unmerged partial slots;
+    kind "ctx": the context split-K partials + counters.  The kernels only
+    rearm their counters, so when the layout of the buffer changes (another
+    problem shape: a former data region may now hold counters) it is
+    zero-filled again; `layout` is the shape key of the call."""
     key = (kind, str(device), stream_key)
-    buf = _workspaces.get(key)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
-        _workspaces[key] = buf
-    return buf
+    ent = _workspaces.get(key)
+    if ent is None or ent[0].numel() < nbytes:
+        ent = (torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device), layout)
+    elif ent[1] != layout:
+        ent[0].zero_()
+        ent = (ent[0], layout)
+    _workspaces[key] = ent
+    return ent[0]
 
 
 def _check_bf16(name, t):
@@ -100,7 +107,7 @@ def system_attention(q, sys_k, sys_v, *, kv_layout="shd", scale=None, grid=None,
     stream = _stream(dev)
     if ws is None:
         _, need = _lib.sys_plan(n_rows, hq, hkv, s, grid)
-        ws = workspace(need, dev, stream)
+        ws = workspace(need, dev, stream, layout=(n_rows, hq, hkv, s, grid))
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
     _lib.check(_lib.load().rb_system_attention(
         q.data_ptr(), q.stride(0), q.stride(1), n_rows, hq, hkv, HEAD_DIM,
@@ -114,12 +121,16 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
                       block_table=None, block_size=0, req_offset=None,
                       strides=None, causal=True, prefix_k=None, prefix_v=None,
                       prefix_strides=None, o_sys=None, lse_sys=None, scale=None,
-                      out=None, out_fp32=False, lse_out=None, want_lse=True):
+                      out=None, out_fp32=False, lse_out=None, want_lse=True,
+                      max_ctx_len=0, ws=None):
     """Context (or relay, or naive-baseline) attention; see
     include/relay_b200.h:rb_context_attention for the addressing modes.
 
     q: (n_rows, hq, 128) bf16; q_start int32 (b+1,); ctx_lens int32 (b,).
     strides = (stride_block, stride_tok, stride_head) in elements.
+    max_ctx_len: an upper bound of ctx_lens (0: unknown) -- enables the
+    split-K over long contexts; its workspace is cached per stream unless
+    `ws` (zero-filled, rb_context_workspace_bytes) is given.
     """
     _check_bf16("q", q)
     _check_bf16("k", k)
@@ -153,12 +164,19 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
     sb, stok, sh = strides
     bt_stride = block_table.stride(0) if block_table is not None else 0
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
+    stream = _stream(dev)
+    if ws is None and max_ctx_len > 0:
+        need = _lib.context_workspace_bytes(b, n_rows, max_rows, hq, hkv, s_prefix, max_ctx_len,
+                                            sm_count(dev))
+        ws = workspace(need, dev, stream, kind="ctx",
+                       layout=(b, n_rows, max_rows, hq, hkv, s_prefix, max_ctx_len)) if need else None
     _lib.check(_lib.load().rb_context_attention(
-        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, max_rows, hq, hkv,
+        q.data_ptr(), q.stride(0), q.stride(1), q_start.data_ptr(), b, n_rows, max_rows, hq, hkv,
         HEAD_DIM, k.data_ptr(), v.data_ptr(), _ptr(block_table), bt_stride, block_size,
         _ptr(req_offset), sb, stok, sh, ctx_lens.data_ptr(), 1 if causal else 0,
         _ptr(prefix_k), _ptr(prefix_v), s_prefix, p_tok, p_head, _ptr(o_sys), _ptr(lse_sys),
-        float(scale), out.data_ptr(), 1 if out_fp32 else 0, _ptr(lse_out), _stream(dev)),
+        float(scale), out.data_ptr(), 1 if out_fp32 else 0, _ptr(lse_out), int(max_ctx_len),
+        _ptr(ws), 0 if ws is None else ws.numel(), stream),
         "rb_context_attention")
     return out, lse_out
 
@@ -166,10 +184,12 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
 def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
                     sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
                     strides=None, scale=None, grid=None, out=None, lse_out=None,
-                    out_fp32=False, ws=None, phases=3):
+                    out_fp32=False, ws=None, phases=3, max_ctx_len=0):
     """The fused relay step (rb_relay_attention): system kernel (stream-K
     partials, no merge) + context kernel whose epilogue merges the system
-    partials with the context state.  Returns (out, lse)."""
+    partials with the context state.  Returns (out, lse).  max_ctx_len: an
+    upper bound of ctx_lens (0: unknown) for the context split-K; `ws` must
+    then hold rb_relay_workspace_bytes(..., max_ctx_len, sm_count) bytes."""
     _check_bf16("q", q)
     for name, t in (("sys_k", sys_k), ("sys_v", sys_v), ("k", k), ("v", v)):
         _check_bf16(name, t)
@@ -204,8 +224,10 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
     grid = sm_count(dev) if grid is None else grid
     stream = _stream(dev)
     if ws is None:
-        need = _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid)
-        ws = workspace(need, dev, stream, kind="relay")
+        need = _lib.relay_workspace_bytes(n_rows, hq, hkv, s, grid, b, max_rows, max_ctx_len,
+                                          sm_count(dev))
+        ws = workspace(need, dev, stream, kind="relay",
+                       layout=(n_rows, hq, hkv, s, grid, b, max_rows, max_ctx_len))
     sb, stok, sh = strides
     bt_stride = block_table.stride(0) if block_table is not None else 0
     scale = 1.0 / math.sqrt(HEAD_DIM) if scale is None else scale
@@ -214,8 +236,8 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
         HEAD_DIM, sys_k.data_ptr(), sys_v.data_ptr(), s, s_tok, s_head, k.data_ptr(),
         v.data_ptr(), _ptr(block_table), bt_stride, block_size, _ptr(req_offset), sb, stok, sh,
         ctx_lens.data_ptr(), float(scale), grid, out.data_ptr(),
-        1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), ws.data_ptr(), ws.numel(),
-        phases, stream), "rb_relay_attention")
+        1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), int(max_ctx_len),
+        ws.data_ptr(), ws.numel(), phases, stream), "rb_relay_attention")
     return out, lse_out
 
 
