@@ -16,9 +16,11 @@ outside the timed region).  `value` is the CUDA-graph replay of the step
 (eager launches reported beside it); `e2e` the CUDA-graph replay of the
 host-buffer step (pinned H2D + paged append + step + D2H).
 
-The other BASELINE configs are timed in the same run under `configs`:
-C4 (Llama-3-8B GQA, b=128, s=32k, c=512), C5 (Llama-2-70B GQA, b=256,
-s=64k, c=1k), each with its roofline max(B_alg/BW, F_sys/P_tc).
+The other BASELINE configs are timed in the same run under `configs`: C3
+(the 32-layer Llama-2-7B decode-attention stack, b=64, s=4k, c ~ U[64,768],
+one CUDA graph of 32 relay steps), C4 (Llama-3-8B GQA, b=128, s=32k, c=512),
+C5 (Llama-2-70B GQA, b=256, s=64k, c=1k), each with its roofline
+max(B_alg/BW, F_sys/P_tc).
 
 N > 1 (torchrun): KV heads are sharded across ranks (52 -> 7,7,7,7,6,6,6,6 at
 N=8; C4/C5: one KV head per rank at N=8); each rank runs the same step on its
@@ -52,6 +54,9 @@ BLOCK = 16
 METRIC = "decode attention µs/step & HBM GB/s vs sys-prompt length (B=32), 1/2/4/8 B200"
 # BASELINE.json configs[3], configs[4] (one decode layer each)
 OTHER = {
+    "C3": dict(b=64, hq=32, hkv=32, s=4096, c="U[64,768]", layers=32,
+               label="C3 Llama-2-7B decode-attention stack (configs[2]): 32 layers, b=64, H=32, "
+                     "s=4096, paged 16, c ~ U[64,768] (seeded)"),
     "C4": dict(b=128, hq=32, hkv=8, s=32768, c=512,
                label="C4 Llama-3-8B GQA (configs[3]): b=128, 32q/8kv, s=32768, c=512"),
     "C5": dict(b=256, hq=64, hkv=8, s=65536, c=1024,
@@ -74,7 +79,7 @@ def parse():
     p.add_argument("--impl", choices=["b200", "reference"], default="b200")
     p.add_argument("--s", type=int, default=HEADLINE_S)
     p.add_argument("--sweep", type=str, default=",".join(map(str, SWEEP)))
-    p.add_argument("--configs", type=str, default="C4,C5")
+    p.add_argument("--configs", type=str, default="C3,C4,C5")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU sampling")
     return p.parse_args()
@@ -456,21 +461,38 @@ def run_b200(args):
         return {"e2e_graph_ms": statistics.mean(ms), "e2e_eager_ms": statistics.mean(ms_eager),
                 "h2d": qkv_h.numel() * 2, "d2h": out_h.numel() * 2}
 
+    def other_lens(cfg):
+        if isinstance(cfg["c"], int):
+            return [cfg["c"]] * cfg["b"]
+        import numpy as np
+        return [int(x) for x in np.random.default_rng(1002).integers(64, 769, size=cfg["b"])]
+
     def other_config(name):
+        from paper_2402_14808_b200.attention import RelayDecodeStack
         cfg = OTHER[name]
-        b, hq, hkv, s, c = cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], cfg["c"]
+        b, hq, hkv, s = cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"]
+        layers = cfg.get("layers", 1)
+        lens = other_lens(cfg)
         a, bb, _, _ = sharding.local_heads(hkv, hq, world, rank)
         kvh = list(range(a, bb))
         g = hq // hkv
-        q, sc, paged, bt, cl = build_workload(torch, b, hq, hkv, s, [c] * b, kvh, device, seed=77)
-        relay = RelayDecodeStep(sc, paged, bt, cl, hq=len(kvh) * g)
-        gr = graph_of(torch, lambda: relay(q))
+        q, sc, paged, bt, cl = build_workload(torch, b, hq, hkv, s, lens, kvh, device, seed=77,
+                                              layers=layers)
+        if layers > 1:
+            qs = q[None].expand(layers, *q.shape).contiguous()
+            step = RelayDecodeStack(sc, paged, bt, cl, hq=len(kvh) * g)
+            fn = lambda: step(qs)  # noqa: E731
+        else:
+            step = RelayDecodeStep(sc, paged, bt, cl, hq=len(kvh) * g)
+            fn = lambda: step(q)  # noqa: E731
+        gr = graph_of(torch, fn)
         ms = statistics.mean(timed(gr.replay, max(5, args.steps // 2)))
-        shp = DecodeShape(b, len(kvh) * g, len(kvh), s, b * c)
-        res = {"label": cfg["label"], "kv_heads_per_rank": len(kvh), "plan": relay.plan,
-               "sys_grid": relay.grid, "ms": ms, "bytes_alg_per_rank": shp.bytes_alg,
-               "flops_sys_per_rank": shp.flops_sys}
-        del relay, gr, q, sc, paged
+        shp = DecodeShape(b, len(kvh) * g, len(kvh), s, sum(lens))
+        res = {"label": cfg["label"], "kv_heads_per_rank": len(kvh), "layers": layers,
+               "plan": step.plan, "sys_grid": step.grid, "ms": ms,
+               "bytes_alg_per_rank": layers * shp.bytes_alg,
+               "flops_sys_per_rank": layers * shp.flops_sys, "launches_per_step": 2 * layers}
+        del step, gr, q, sc, paged
         torch.cuda.empty_cache()
         return res
 
@@ -517,14 +539,15 @@ def run_b200(args):
     for name, r in others.items():
         r["us_per_step"] = maxr(r["ms"]) * 1e3
         cfg = OTHER[name]
-        full = DecodeShape(cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], cfg["b"] * cfg["c"])
+        L = cfg.get("layers", 1)
+        full = DecodeShape(cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], sum(other_lens(cfg)))
         t = r["us_per_step"] * 1e-6
-        t_hbm = full.bytes_alg / (world * hbm * 1e9)
-        t_tc = full.flops_sys / (world * tc_sus * 1e12)
-        r.update({"bytes_alg": full.bytes_alg, "flops_sys": full.flops_sys,
+        t_hbm = L * full.bytes_alg / (world * hbm * 1e9)
+        t_tc = L * full.flops_sys / (world * tc_sus * 1e12)
+        r.update({"bytes_alg": L * full.bytes_alg, "flops_sys": L * full.flops_sys,
                   "roofline_us": max(t_hbm, t_tc) * 1e6, "frac_of_roofline": max(t_hbm, t_tc) / t,
                   "bound": "tensor" if t_tc > t_hbm else "hbm",
-                  "sys_tflops": full.flops_sys / t / 1e12, "tokens_per_s": cfg["b"] / t,
+                  "sys_tflops": L * full.flops_sys / t / 1e12, "tokens_per_s": cfg["b"] / t,
                   "peaks": f"HBM {hbm} GB/s, bf16 {tc_sus} TF/s sustained ({peak_kind}), x{world} GPUs"})
         r.pop("ms")
 

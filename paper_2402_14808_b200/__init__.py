@@ -15,7 +15,8 @@ __version__ = "0.1.0"
 __all__ = [
     "TrafficCounter", "LseAttentionOutput", "attention_with_lse", "naive_causal_attention",
     "relay_fusion", "relay_attention", "relay_attention_ragged", "baseline_attention",
-    "baseline_attention_ragged", "RelayDecodeStep", "NaiveDecodeStep", "SystemKvCache",
+    "baseline_attention_ragged", "RelayDecodeStep", "RelayDecodeStack", "NaiveDecodeStep",
+    "SystemKvCache",
     "PagedKvCache", "BlockAllocator", "theoretical_speedup", "kernel_backend",
 ]
 
@@ -30,7 +31,7 @@ def __getattr__(name):
     if name in ("TrafficCounter", "LseAttentionOutput", "attention_with_lse",
                 "naive_causal_attention", "relay_fusion", "relay_attention",
                 "relay_attention_ragged", "baseline_attention", "baseline_attention_ragged",
-                "RelayDecodeStep", "NaiveDecodeStep"):
+                "RelayDecodeStep", "RelayDecodeStack", "NaiveDecodeStep"):
         from . import attention
         return getattr(attention, name)
     if name in ("SystemKvCache", "PagedKvCache", "BlockAllocator", "context_position"):

@@ -388,7 +388,7 @@ class RelayDecodeStep:
     """
 
     def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
-                 grid=None, out_dtype=torch.bfloat16, scale=None):
+                 grid=None, out_dtype=torch.bfloat16, scale=None, out=None, lse=None):
         self.sys_cache, self.paged, self.layer = sys_cache, paged_cache, layer
         self.block_table = block_table
         self.ctx_lens = ctx_lens
@@ -424,8 +424,10 @@ class RelayDecodeStep:
                                           self.b, hq // self.hkv, self.max_ctx_len,
                                           kernels.sm_count(dev))
         self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
-        self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
-        self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev)
+        self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev) if out is None else out
+        self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev) if lse is None else lse
+        if tuple(self.out.shape) != (self.b, hq, HEAD_DIM) or tuple(self.lse.shape) != (self.b, hq):
+            raise DimensionError("out / lse buffers must be (b, hq, 128) / (b, hq)")
         self.q_start = torch.arange(self.b + 1, dtype=torch.int32, device=dev)
         # a system-only launch (profiling) leaves its units published; the
         # next full step must start from rearmed counters
@@ -514,6 +516,49 @@ def _lib_ctx_bytes(b, hq, hkv, s_prefix, max_ctx_len, dev):
     from . import _lib
     return _lib.context_workspace_bytes(b, b, hq // hkv, hq, hkv, s_prefix, max_ctx_len,
                                         kernels.sm_count(dev))
+
+
+class RelayDecodeStack:
+    """The decode-attention stack of a model: one relay decode step per layer
+    (the reference model's per-layer `_attend`, model.py:261-336, relay mode)
+    over the layers of one SystemKvCache and one PagedKvCache, sharing the
+    block table and context lengths.
+
+    q: (layers, b, hq, 128) bf16 -> out (layers, b, hq, 128), fused lse
+    (layers, b, hq).  The 2 x layers kernels are launched back to back on the
+    current stream; each layer's system kernel is a programmatic dependent
+    of the previous layer's context kernel, so its prologue (barriers, TMEM,
+    descriptor prefetch) overlaps that kernel's tail while its first loads
+    wait for it to complete.  Every layer has its own workspace, so the
+    whole stack is one capturable sequence (one CUDA graph per decode step).
+    """
+
+    def __init__(self, sys_cache, paged_cache, block_table, ctx_lens, hq, grid=None,
+                 out_dtype=torch.bfloat16, scale=None):
+        if sys_cache.layers != paged_cache.layers:
+            raise DimensionError(f"system cache has {sys_cache.layers} layers, paged cache "
+                                 f"{paged_cache.layers}")
+        self.layers = sys_cache.layers
+        b = ctx_lens.numel()
+        dev = block_table.device
+        self.out = torch.empty((self.layers, b, hq, HEAD_DIM), dtype=out_dtype, device=dev)
+        self.lse = torch.empty((self.layers, b, hq), dtype=torch.float32, device=dev)
+        first = RelayDecodeStep(sys_cache, paged_cache, block_table, ctx_lens, hq, layer=0,
+                                grid=grid, out_dtype=out_dtype, scale=scale,
+                                out=self.out[0], lse=self.lse[0])
+        self.steps = [first] + [
+            RelayDecodeStep(sys_cache, paged_cache, block_table, ctx_lens, hq, layer=i,
+                            grid=first.grid, out_dtype=out_dtype, scale=scale,
+                            out=self.out[i], lse=self.lse[i])
+            for i in range(1, self.layers)]
+        self.grid, self.plan = first.grid, first.plan
+
+    def __call__(self, q):
+        if q.dim() != 4 or q.shape[0] != self.layers:
+            raise DimensionError(f"q must be (layers={self.layers}, b, hq, 128), got {tuple(q.shape)}")
+        for i, step in enumerate(self.steps):
+            step(q[i])
+        return self.out, self.lse
 
 
 class NaiveDecodeStep:

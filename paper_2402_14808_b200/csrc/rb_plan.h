@@ -132,8 +132,9 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
 // head streams the whole prefix), the context kernel the rest plus every SM
 // the system kernel releases, so both finish together.
 // RB_RELAY_RATE_RATIO = (system bytes/s per SM) / (context bytes/s per SM),
-// measured on B200 with profiles/sweep_split.py (best splits at s = 2k..32k).
-#define RB_RELAY_RATE_RATIO 1.6
+// fit on B200 with profiles/sweep_split.py to the best splits at s = 4k..32k
+// (profiles/r02/sweep_split.txt: 60 / 90 / ~106 / ~115 system CTAs).
+#define RB_RELAY_RATE_RATIO 1.3
 RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sms) {
   rb_sys_plan p;
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
@@ -151,8 +152,8 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   }
   // latency floor: with few key tiles per CTA the system kernel is bound by
   // its per-CTA pipeline (prologue + ~1.5 us per tile), not by bytes; the
-  // measured optimum at s <= 2k keeps ~27% of the SMs on it
-  const int floor_g = sms * 27 / 100;
+  // measured optimum at s <= 2k keeps ~20% of the SMs on it
+  const int floor_g = sms * 20 / 100;
   if (g < floor_g) g = floor_g;
   if ((long long)g > p.total) g = (int)p.total;
   if (g < 1) g = 1;

@@ -39,12 +39,13 @@ def main():
     flush = bench.make_flush(torch, dev)
     sms = kernels.sm_count(dev)
     for s in [int(x) for x in (sys.argv[1:] or ["2048", "8192", "32768"])]:
-        q, relay, _, paged, bt = bench.build(torch, s, list(range(bench.H)), dev)
+        q, sc, paged, bt, cl = bench.build_workload(torch, bench.B, bench.H, bench.H, s,
+                                                    [bench.C] * bench.B, list(range(bench.H)), dev)
         auto = _lib.relay_sys_grid(bench.B, bench.H, bench.H, s, bench.B * bench.C, sms)
         res = []
-        grids = os.environ.get("SWEEP_GRIDS", "40,60,70,80,90,100,110,120,148")
+        grids = os.environ.get("SWEEP_GRIDS", "10,20,30,40,50,60,70,80,90,100,110,120,148")
         for g in sorted({auto} | {int(x) for x in grids.split(",")}):
-            step = RelayDecodeStep(relay.sys_cache, paged, bt, relay.ctx_lens, bench.H, grid=g)
+            step = RelayDecodeStep(sc, paged, bt, cl, bench.H, grid=g)
             res.append((g, time_step(lambda: step(q), flush)))
         print(f"s={s} auto grid {auto}: " + ", ".join(f"{g}:{t:.1f}" for g, t in res), flush=True)
 

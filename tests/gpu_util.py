@@ -86,7 +86,7 @@ def oracle_pair(oracle, q, sys_cache, paged, layer, r, h, g):
     ck, cv = paged.gather(r, layer)
     k = np.concatenate([sk, ck[:, h].float().cpu().numpy()]).astype(np.float64)
     v = np.concatenate([sv, cv[:, h].float().cpu().numpy()]).astype(np.float64)
-    qn = q[r, h * g:(h + 1) * g].float().cpu().numpy().astype(np.float64)
+    qn = q[r, h * g:(h + 1) * g].float().cpu().numpy().astype(np.float64)   # q: (b, hq, 128)
     res = oracle.attention_with_lse(qn[None, :, None], k[None, :, None], v[None, :, None],
                                     causal=False)
     return res.output[0, :, 0], res.lse[0, :, 0]

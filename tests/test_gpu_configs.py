@@ -94,3 +94,32 @@ def test_c5_full_size(rb, oracle):
     # 2048 rows per KV head, 128 units on <= 148 SMs: whole units dealt
     # round-robin (rr = 1), the GQA kernel's one-part-per-unit path
     _run_config(rb, oracle, "C5", expect_plan={"nq": 128, "n_qt": 16, "rr": 1})
+
+
+def test_c3_32_layer_stack(rb, oracle):
+    """configs[2] as stated: the 32-layer decode-attention stack (b=64, 32
+    heads, s=4096, paged 16-token blocks, c ~ U[64, 768]) through
+    RelayDecodeStack -- one relay step per layer over per-layer caches --
+    deterministic, and against the oracle on sampled layers / pairs."""
+    from paper_2402_14808_b200.attention import RelayDecodeStack
+    cfg = CONFIGS["C3"]
+    b, hq, hkv, s, lens = cfg["b"], cfg["hq"], cfg["hkv"], cfg["s"], cfg["lens"]
+    layers = 32
+    q0, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, 3003, layers=layers)
+    gen = torch.Generator(device="cuda").manual_seed(3004)
+    q = torch.randn((layers, b, hq, 128), device="cuda", generator=gen).to(torch.bfloat16)
+    stack = RelayDecodeStack(sys_cache, paged, bt, cl, hq)
+    out, lse = [t.clone() for t in stack(q)]
+    out2, lse2 = stack(q)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and torch.equal(lse, lse2), "stack not deterministic"
+    rng = np.random.default_rng(3005)
+    worst = [0.0, 0.0, 0.0]
+    for layer in (0, 13, layers - 1):
+        pairs = [(int(r), int(h)) for r, h in zip(rng.integers(0, b, size=3), rng.integers(0, hkv, size=3))]
+        res = check_sampled_pairs(oracle, out[layer], lse[layer], q[layer], sys_cache, paged,
+                                  layer, pairs, 1, f"C3 layer {layer}")
+        worst = [max(a, b_) for a, b_ in zip(worst, res)]
+    log_parity("config C3 (32-layer stack)", kind="config", config="C3x32", layers=layers,
+               sampled_layers=[0, 13, layers - 1], o_max_abs=worst[0], o_rel=worst[1],
+               lse_max_abs=worst[2])
