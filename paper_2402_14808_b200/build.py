@@ -21,7 +21,8 @@ DIAG_LIB = os.path.join(PKG, "librelay_b200_diag.so")  # -DRB_DIAG=1: timestamp 
 # diagnostics: RB_VARIANT="name:-DFOO=1 -DBAR=2" builds librelay_b200_<name>.so
 # with extra defines (select it at run time with RB_LIB=<path>)
 _VARIANT = os.environ.get("RB_VARIANT", "")
-SOURCES = ["sys_attn_sm100.cu", "sys_gqa_sm100.cu", "ctx_attn.cu", "rope_append.cu", "capi.cu"]
+SOURCES = ["sys_attn_sm100.cu", "sys_gqa_sm100.cu", "sys_gqa2_sm100.cu", "ctx_attn.cu",
+           "rope_append.cu", "capi.cu"]
 HEADERS = ["rb_common.cuh", "rb_plan.h", "rb_args.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

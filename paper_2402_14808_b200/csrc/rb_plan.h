@@ -28,7 +28,7 @@ typedef struct {
   int n_rows;         // flattened query rows (sum of m_r over requests)
   int hq, hkv, g;     // query heads, kv heads, group size hq / hkv
   int s;              // shared prefix length (keys)
-  int nq;             // query rows per tile (16 or 32)
+  int nq;             // query rows per unit (16, 32, 128 or 256)
   int rows_per_head;  // n_rows * g
   int n_qt;           // ceil(rows_per_head / nq)
   int tpu;            // key tiles per unit, ceil(s / 128)
@@ -76,9 +76,10 @@ RB_HD int rb_unit_owner0(const rb_sys_plan* p, int u) {
 
 // Query rows per tile: the swap-AB kernel takes 16 / 32 (N of the MMA); from
 // 128 rows per KV head on, the non-swapped kernel (sys_gqa_sm100.cu) takes
-// 128-row tiles (M of the MMA).
+// 128-row tiles (M of the MMA); from 256 on, sys_gqa2_sm100.cu takes units of
+// two 128-row tiles that share each K/V tile (two softmax warpgroups).
 RB_HD int rb_pick_nq(int rows_per_head) {
-  return rows_per_head <= 16 ? 16 : rows_per_head < 128 ? 32 : 128;
+  return rows_per_head <= 16 ? 16 : rows_per_head < 128 ? 32 : rows_per_head < 256 ? 128 : 256;
 }
 
 // Fill a plan. grid_cap = number of CTAs the device can hold at once
@@ -135,13 +136,29 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
 // fit on B200 with profiles/sweep_split.py to the best splits at s = 4k..32k
 // (profiles/r02/sweep_split.txt: 60 / 90 / ~106 / ~115 system CTAs).
 #define RB_RELAY_RATE_RATIO 1.3
+#define RB_GQA2_TILE_US 2.0   /* sys_gqa2: one 128-key tile for 256 query rows */
+#define RB_CTX_SM_GBS 38.0    /* context kernel streaming rate per SM */
 RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sms) {
   rb_sys_plan p;
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
   const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
   const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
   int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
-  if (p.nq == 128 && p.n_units <= sms) {
+  if (p.nq == 256 && p.n_units <= sms) {
+    // the 256-row GQA kernel is tensor-bound: balance measured time, not
+    // bytes -- RB_GQA2_TILE_US per key tile per CTA against the context
+    // kernel's RB_CTX_SM_GBS per SM (profiles/r02), rounded to whole
+    // multiples of the unit count (CTAs on a head's units share K/V in L2;
+    // measured C4 64 / 80 CTAs within 4%, C5 128 CTAs 31% faster than 64)
+    const double sys_work = (double)p.total * RB_GQA2_TILE_US;
+    const double ctx_work = ctx_bytes / (RB_CTX_SM_GBS * 1e3);
+    const double gt = sms * sys_work / (sys_work + ctx_work);
+    int k = (int)(gt / p.n_units + 0.5);
+    if (k < 1) k = 1;
+    if (k * p.n_units > sms) k = sms / p.n_units;
+    return k * p.n_units;
+  }
+  if (p.nq >= 128 && p.n_units <= sms) {
     // 128-row GQA kernel: whole multiples of the unit count, rounded down
     // (at least one CTA per unit), so the CTAs on a head's query tiles stay
     // aligned and share K/V in L2 (measured: C4 best at 2 CTAs per unit,

@@ -14,7 +14,9 @@ KEY_TILE = 128
 def pick_nq(rows_per_head: int) -> int:
     if rows_per_head <= 16:
         return 16
-    return 32 if rows_per_head < 128 else 128
+    if rows_per_head < 128:
+        return 32
+    return 128 if rows_per_head < 256 else 256
 
 
 @dataclass(frozen=True)

@@ -70,7 +70,7 @@ def main():
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     flush = bench.make_flush(torch, dev)
-    hbm, tc, _ = bench.measured_peaks()
+    hbm, _, tc, _ = bench.measured_peaks()
     rows = []
     for name in args.configs.split(","):
         cfg = CONFIGS[name]

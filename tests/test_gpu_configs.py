@@ -86,14 +86,13 @@ def test_c3_one_layer_full_size(rb, oracle):
 
 
 def test_c4_full_size(rb, oracle):
-    # 512 query rows per KV head: the 128-row GQA kernel (nq = 128)
-    _run_config(rb, oracle, "C4", expect_plan={"nq": 128, "n_qt": 4})
+    # 512 query rows per KV head: 256-row units (two query tiles, sys_gqa2)
+    _run_config(rb, oracle, "C4", expect_plan={"nq": 256, "n_qt": 2})
 
 
 def test_c5_full_size(rb, oracle):
-    # 2048 rows per KV head, 128 units on <= 148 SMs: whole units dealt
-    # round-robin (rr = 1), the GQA kernel's one-part-per-unit path
-    _run_config(rb, oracle, "C5", expect_plan={"nq": 128, "n_qt": 16, "rr": 1})
+    # 2048 rows per KV head: 8 units of 256 rows per head, 2 CTAs per unit
+    _run_config(rb, oracle, "C5", expect_plan={"nq": 256, "n_qt": 8, "grid": 128, "rr": 0})
 
 
 def test_c3_32_layer_stack(rb, oracle):

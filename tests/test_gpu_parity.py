@@ -84,8 +84,11 @@ def test_umma_probe_layouts(rb, nq):
     (1, 1, 1, 1, None),          # single key
     (64, 8, 2, 700, None),       # 256 rows/head: non-swapped 128-row kernel, 2 q-tiles
     (40, 8, 2, 300, 5),          # 160 rows/head (partial q-tile), stream-K parts
-    (128, 4, 1, 129, None),      # 512 rows/head, partial last key tile
+    (128, 4, 1, 129, None),      # 512 rows/head: 256-row units (two query tiles), partial key tile
     (32, 32, 8, 1000, 3),        # g=4, 128 rows/head exactly, 3 CTAs
+    (75, 4, 1, 1000, 5),         # 300 rows/head: a full and a 44-row 256-row unit, stream-K parts
+    (64, 16, 4, 2000, 9),        # 256 rows/head exactly, 4 units over 9 CTAs
+    (160, 8, 1, 900, None),      # 1280 rows/head: 5 units round-robin / aligned
 ])
 def test_system_attention_vs_oracle(rb, oracle, n_rows, hq, hkv, s, grid):
     from paper_2402_14808_b200 import kernels
@@ -503,7 +506,7 @@ def test_append_rotated_decode_prologue(rb, oracle):
         assert (vv[c].float().cpu().numpy() == v[i]).all()
 
 
-@pytest.mark.parametrize("b,s", [(48, 900), (40, 100)])
+@pytest.mark.parametrize("b,s", [(48, 900), (40, 100), (80, 1300), (130, 257)])
 def test_relay_step_gqa_large_vs_oracle(rb, oracle, b, s):
     """The concurrent relay step with >= 128 rows per KV head (the non-swapped
     system kernel's parts fused in the context kernel) against the oracle,
@@ -534,6 +537,31 @@ def test_relay_step_gqa_large_vs_oracle(rb, oracle, b, s):
             ref = oracle.attention_with_lse(q[r][None, None], fk[None], fv[None], causal=False)
             assert_close(out[r].cpu().numpy(), ref.output[0, 0], f"relay gqa-large row {r} grid {grid}")
             assert_close(lse[r].cpu().numpy(), ref.lse[0, 0], "relay gqa-large lse", lse=True)
+
+
+@pytest.mark.parametrize("b,hq,hkv,s,grid,nq", [
+    (48, 32, 8, 600, 16, 128),     # 192 rows / head: 128-row kernel, 16 units round-robin
+    (128, 32, 8, 700, 16, 256),    # 512 rows / head: 256-row kernel, 16 units round-robin
+    (256, 64, 8, 300, 64, 256),    # C5's head layout at s=300: 64 units, one CTA each
+])
+def test_relay_step_round_robin_units(rb, oracle, b, hq, hkv, s, grid, nq):
+    """Whole units dealt round-robin (plan rr = 1: one part per unit, the
+    CTAs of a head's units walk its key tiles in lockstep) through the relay
+    step, for both GQA system kernels, against the oracle."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    from gpu_util import check_sampled_pairs, synth_paged_problem
+    lens = [int(x) for x in np.random.default_rng(b + s).integers(1, 200, size=b)]
+    q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, seed=b * s)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, grid=grid, out_dtype=torch.float32)
+    assert step.plan["rr"] == 1 and step.plan["nq"] == nq, step.plan
+    out, lse = [t.clone() for t in step(q)]
+    o2, l2 = step(q)
+    torch.cuda.synchronize()
+    assert torch.equal(out, o2) and torch.equal(lse, l2)
+    g = hq // hkv
+    pairs = [(0, 0), (b // 2, hkv // 2), (b - 1, hkv - 1)]
+    check_sampled_pairs(oracle, out, lse, q, sys_cache, paged, 0, pairs, g,
+                        f"rr relay nq={nq} b={b} grid={grid}")
 
 
 def test_relaykv_cache_feeds_system_kernel(rb, oracle):

@@ -117,16 +117,25 @@ def test_relay_sm_split():
 
 def test_plan_tile_sizes_and_aligned_split():
     """nq: 16 / 32 for the swap-AB kernel, 128 (non-swapped kernel) from 128
-    rows per KV head; several q-tiles per head with fewer units than CTAs get
-    an equal number of CTAs per unit when that keeps >= 85% of them."""
+    rows per KV head, 256 (two query tiles per unit) from 256; several units
+    per head with fewer units than CTAs get an equal number of CTAs per unit
+    when that keeps >= 85% of them."""
     assert SysPlan(16, 1, 1, 100, 148).nq == 16
     assert SysPlan(127, 1, 1, 100, 148).nq == 32
     assert SysPlan(128, 1, 1, 100, 148).nq == 128
+    assert SysPlan(255, 1, 1, 100, 148).nq == 128
+    assert SysPlan(256, 1, 1, 100, 148).nq == 256
     c4 = SysPlan(128, 32, 8, 32768, 148)
-    assert (c4.nq, c4.n_qt, c4.n_units, c4.grid) == (128, 4, 32, 128)
+    assert (c4.nq, c4.n_qt, c4.n_units, c4.grid) == (256, 2, 16, 144)
+    # 9 CTAs per unit: every CTA's key range lies inside one unit, and the
+    # units are cut at the same key tiles
     ranges = c4.cta_ranges()
-    assert all((b - a) == c4.tpu // 4 and a % (c4.tpu // 4) == 0 for a, b in ranges)
-    assert SysPlan(128, 32, 8, 32768, 82).grid == 82      # 64 would drop 22% of the CTAs
+    assert all(a // c4.tpu == (b - 1) // c4.tpu for a, b in ranges)
+    cuts = [[a % c4.tpu for a, _ in ranges[u * 9:(u + 1) * 9]] for u in range(16)]
+    assert all(c == cuts[0] for c in cuts)
+    assert SysPlan(128, 32, 8, 32768, 82).grid == 80      # 5 per unit (82 would misalign)
+    old = SysPlan(40, 8, 2, 300, 148)                     # 160 rows per head: 128-row kernel
+    assert (old.nq, old.n_qt) == (128, 2)
     c3 = SysPlan(64, 32, 32, 4096, 148)
     assert (c3.nq, c3.n_qt, c3.n_units, c3.grid) == (32, 2, 64, 128)
 
@@ -136,7 +145,7 @@ def test_relay_split_gqa_large_whole_units():
     unit count (at least one CTA per unit)."""
     sms = 148
     g4 = _lib.relay_sys_grid(128, 32, 8, 32768, 128 * 512, sms)
-    assert g4 % 32 == 0 and 32 <= g4 <= sms
+    assert g4 % 16 == 0 and 16 <= g4 <= sms
     g5 = _lib.relay_sys_grid(256, 64, 8, 65536, 256 * 1024, sms)
     assert g5 == 128
 
