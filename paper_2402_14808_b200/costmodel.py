@@ -1,8 +1,9 @@
 """Traffic / roofline model of the relay decode step.
 
-Reference element-count closed forms (costmodel.py:85-112), kept for API
-compatibility, plus the physical byte model the B200 roofline uses
-(SURVEY.md section 8d):
+The reference's analytic cost model (costmodel.py:21-163: element-count
+closed forms, traffic report, GEMM intensity, ridge / roofline helpers,
+speedup-curve CSV), kept for API compatibility, plus the physical byte model
+the B200 roofline uses:
 
   B_alg   = e*2*H_kv*d*(s + sum_c) + e*2*b*H_q*d    shared KV once + context KV + Q + O
   B_naive = e*2*H_kv*d*(b*s + sum_c) + e*2*b*H_q*d  shared KV re-read per request
@@ -14,9 +15,10 @@ Intermediates (fp32 system partials, LSEs, block tables) are NOT in B_alg;
 
 from __future__ import annotations
 
+import csv
 from dataclasses import dataclass
 
-from .errors import ContractError
+from .errors import ContractError, DimensionError
 
 
 def _check(b, s, c, d):
@@ -40,6 +42,50 @@ def theoretical_speedup(b, s, c):
     """costmodel.py:105-112: p = (s + c + 2) / (s/b + c + 7)."""
     _check(b, s, c, 1)
     return (s + c + 2) / (s / b + c + 7)
+
+
+@dataclass(frozen=True)
+class TrafficReport:
+    """Element traffic of one decode step on both paths (costmodel.py:43-53)."""
+
+    n_baseline: int
+    n_relay: int
+    speedup: float
+    b: int
+    s: int
+    c: int
+    d: int
+
+
+def traffic_report(b, s, c, d):
+    """costmodel.py:115-119: both closed forms and their ratio."""
+    base, relay = traffic_baseline(b, s, c, d), traffic_relay(b, s, c, d)
+    return TrafficReport(base, relay, base / relay, b, s, c, d)
+
+
+@dataclass(frozen=True)
+class GemmShape:
+    """C = A @ B.T with A (m, k), B (n, k) (numerics.py:24-33)."""
+
+    m: int
+    n: int
+    k: int
+
+    def __post_init__(self):
+        if min(self.m, self.n, self.k) < 1:
+            raise DimensionError(f"GemmShape dimensions must be >= 1, got {self}")
+
+
+def arithmetic_intensity_gemm(shape):
+    """flop per byte of a bf16 GEMM with every operand moved once
+    (costmodel.py:56-61): mnk / (mk + nk + mn)."""
+    m, n, k = shape.m, shape.n, shape.k
+    return (m * n * k) / (m * k + n * k + m * n)
+
+
+def gemm_intensity_bound(shape):
+    """min(m, n, k) bounds the GEMM intensity from above (costmodel.py:64-66)."""
+    return min(shape.m, shape.n, shape.k)
 
 
 @dataclass(frozen=True)
@@ -131,6 +177,51 @@ HARDWARE_PROFILES = {
 B200_STEP_FIXED_S = 21.1e-6
 B200_STEP_MARGINAL_BPS = 6.9e12
 B200_STEP_FLOOR_S = 45.0e-6
+
+
+def balance_ratio(profile):
+    """Ridge intensity peak_flops / bandwidth (costmodel.py:69-72)."""
+    return profile.peak_flops / profile.mem_bandwidth
+
+
+def compute_time_ratio(intensity, profile):
+    """intensity / ridge: compute time over memory time of an overlapped
+    operator (costmodel.py:75-80); below 1 it is memory-bound."""
+    return intensity / balance_ratio(profile)
+
+
+def is_memory_bound(intensity, profile):
+    return compute_time_ratio(intensity, profile) < 1.0
+
+
+def memory_time(elements, profile):
+    """Seconds to move `elements` at full bandwidth (costmodel.py:122-124)."""
+    return elements * profile.bytes_per_element / profile.mem_bandwidth
+
+
+def compute_time(flops, profile):
+    return flops / profile.peak_flops
+
+
+def roofline_time(flops, elements, profile):
+    """max(memory time, compute time) (costmodel.py:131-135)."""
+    return max(memory_time(elements, profile), compute_time(flops, profile))
+
+
+def emit_speedup_curves(path, batch_sizes=(4, 8, 16, 32), context_lens=(128, 256),
+                        s_values=(64, 128, 256, 512, 1024, 2048, 4096), measured=None):
+    """The theoretical-speedup grid as CSV rows (b, c, s, p_theoretical,
+    p_measured_traffic) -- the reference's CSV columns (costmodel.py:
+    138-163); `measured(b, c, s)`, if given, fills the last column."""
+    rows = [{"b": b, "c": c, "s": s, "p_theoretical": repr(theoretical_speedup(b, s, c)),
+             "p_measured_traffic": "" if measured is None else repr(measured(b, c, s))}
+            for b in batch_sizes for c in context_lens for s in s_values]
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=list(rows[0]) if rows else
+                           ["b", "c", "s", "p_theoretical", "p_measured_traffic"])
+        w.writeheader()
+        w.writerows(rows)
+    return rows
 
 
 def b200_relay_step_seconds(shape: "DecodeShape") -> float:

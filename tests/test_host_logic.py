@@ -228,3 +228,36 @@ def test_b200_profile_and_step_model():
     for s, t in measured.items():
         sh = costmodel.DecodeShape(b=32, hq=52, hkv=52, s=s, ctx_total=32 * 128)
         assert abs(costmodel.b200_relay_step_seconds(sh) - t) / t < 0.10
+
+
+def test_costmodel_matches_reference_module(tmp_path):
+    """The ported cost-model helpers (traffic report, GEMM intensity, ridge /
+    roofline, speedup-curve CSV) against the reference's own costmodel
+    compiled into oracle/_ref."""
+    import os
+    import sys
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "relayserve")):
+        pytest.skip("oracle/_ref not built")
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import relayserve.costmodel as ref
+    from relayserve.numerics import GemmShape as RefShape
+    for b, s, c, d in [(1, 0, 0, 1), (32, 2048, 128, 4096), (4, 64, 256, 16), (8, 8, 1, 32)]:
+        a, o = ref.traffic_report(b, s, c, d), costmodel.traffic_report(b, s, c, d)
+        assert (a.n_baseline, a.n_relay, a.speedup) == (o.n_baseline, o.n_relay, o.speedup)
+    for m, n, k in [(1, 1, 1), (32, 8192, 128), (7, 3, 5)]:
+        assert ref.arithmetic_intensity_gemm(RefShape(m, n, k)) == pytest.approx(
+            costmodel.arithmetic_intensity_gemm(costmodel.GemmShape(m, n, k)), rel=1e-14)
+        assert ref.gemm_intensity_bound(RefShape(m, n, k)) == \
+            costmodel.gemm_intensity_bound(costmodel.GemmShape(m, n, k))
+    for name, prof in ref.HARDWARE_PROFILES.items():
+        ours = costmodel.HARDWARE_PROFILES[name]
+        assert ref.balance_ratio(prof) == pytest.approx(costmodel.balance_ratio(ours), rel=1e-14)
+        for inten in (1.0, 38.2, 300.0):
+            assert ref.is_memory_bound(inten, prof) == costmodel.is_memory_bound(inten, ours)
+        assert ref.roofline_time(1e12, 10 ** 9, prof) == pytest.approx(
+            costmodel.roofline_time(1e12, 10 ** 9, ours), rel=1e-14)
+    ref.emit_speedup_curves(tmp_path / "ref.csv")
+    costmodel.emit_speedup_curves(tmp_path / "ours.csv")
+    assert (tmp_path / "ref.csv").read_text() == (tmp_path / "ours.csv").read_text()
