@@ -1051,7 +1051,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       const bool pre = kg < n_pre;
       const int key0 = (pre ? kg : kg - n_pre) * kChunk;
       const bool mask = key0 + kChunk > (pre ? a.s_prefix : ctx_nomask);
+#ifndef RB_CTX_NOCOMPUTE
       cmp.chunk(ring_p + con_sl * kSlotBytes, key0, pre, it.max_lim, mask, a, lane);
+#else
+      (void)key0;  // diagnostics variant: the data path alone (wrong results)
+#endif
       __syncwarp();  // every lane's reads precede the refill of this slot
       ++consumed;
       con_sl = (con_sl + 1 == kDepth) ? 0 : con_sl + 1;
