@@ -402,10 +402,17 @@ __device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int 
 }
 
 constexpr int kWorkers = 4;
-constexpr int kDepth = 3;                      // chunks in flight per worker
-static_assert(kDepth == 3, "wait_group ladder in ctx_cta_kernel assumes 3");
+// Per-row-count configuration.  Two CTAs must fit an SM (<= ~113 KB of
+// shared memory each) so that 8 worker warps keep their rings of K+V chunks
+// in flight per SM: the merge buffers grow with R, so R = 2 / 4 keep fewer
+// merge buffers (their items are long, the merger keeps up with one or two)
+// and R = 8 a 2-deep ring.
+template <int R>
+struct CtxCfg {
+  static constexpr int kDepth = R >= 8 ? 2 : 3;    // chunks in flight per worker
+  static constexpr int kNB = R == 1 ? 3 : R == 2 ? 2 : 1;  // merge buffers
+};
 constexpr int kIQ = 3;                         // item queue depth (claim-ahead bound)
-constexpr int kNB = 3;                         // merge buffers
 constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
@@ -492,6 +499,8 @@ struct ItemSlot {
 
 template <int R>
 struct CtaSmem {
+  static constexpr int kDepth = CtxCfg<R>::kDepth;
+  static constexpr int kNB = CtxCfg<R>::kNB;
   // [kIQ][R][128] bf16 query rows, then one zero row (MMA rows past R)
   static constexpr int kOffQ = kWorkers * kDepth * kSlotBytes;
   static constexpr int kOffQZero = kOffQ + kIQ * R * kRowBytes;
@@ -501,6 +510,7 @@ struct CtaSmem {
   static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
   static constexpr int kOffDefer = kOffBar + (3 * kIQ + 2 * kNB) * 8;  // [1 + kMaxDefer] int
   static constexpr int kBytes = kOffDefer + (1 + kMaxDefer) * 4;
+  static_assert(kBytes <= 113 * 1024, "two context CTAs must fit one SM");
 };
 
 // Merge two unnormalised softmax states (O, m log2, l) -- the merge of
@@ -522,6 +532,7 @@ template <int R>
 __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
   using SM = CtaSmem<R>;
+  constexpr int kDepth = SM::kDepth, kNB = SM::kNB;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
@@ -1040,9 +1051,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       // chunk `consumed` is this warp's commit group number `consumed`; the
       // groups committed after it may stay in flight
       const int newer = issued - consumed - 1;
-      if (newer >= 2)
+      if (kDepth >= 3 && newer >= 2)
         asm volatile("cp.async.wait_group 2;" ::: "memory");
-      else if (newer == 1)
+      else if (newer >= 1)
         asm volatile("cp.async.wait_group 1;" ::: "memory");
       else
         asm volatile("cp.async.wait_group 0;" ::: "memory");

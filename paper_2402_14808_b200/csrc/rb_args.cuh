@@ -72,4 +72,38 @@ struct CtxArgs {
   int* split_cnt;                // [b * hkv * n_z] zeroed counters, rearmed by the last split
 };
 
+#ifdef __CUDACC__
+// cp.async the query rows f0 .. f0 + ROWS - 1 of KV head h (flattened row f =
+// request f / g, group member f % g; rows past rows_per_head zero-filled)
+// into ROWS / T K-major SW128 tiles of T rows ([2 kblocks][T rows][128 B]
+// each), one warp: lane (half = lane / 16, ch = lane % 16) copies 16-byte
+// chunk ch of rows 2 it + half.  The (request, member) pair is walked
+// incrementally -- a runtime division per chunk made this loop a 10+ us
+// prologue of the 256-row kernel.
+template <int T, int ROWS>
+__device__ __forceinline__ void load_unit_q(uint8_t* dst, const SysArgs& args, int h, int f0,
+                                            int lane) {
+  const rb_sys_plan& P = args.plan;
+  const int half = lane >> 4, ch = lane & 15;
+  int f = f0 + half;
+  int row = f / P.g, jj = f % P.g;
+#pragma unroll 4
+  for (int it = 0; it < ROWS / 2; ++it) {
+    const int c = 2 * it + half;
+    const bool ok = f < P.rows_per_head;
+    const __nv_bfloat16* src = args.q + static_cast<long long>(row) * args.q_row_stride +
+                               static_cast<long long>(h * P.g + jj) * args.q_head_stride + ch * 8;
+    const int sub = c / T, rr = c % T;
+    cp_async_16(dst + sub * (T * 256) + (ch >> 3) * (T * 128) + sw128_offset(rr, (ch & 7) * 8),
+                ok ? src : args.q, ok ? 16u : 0u);
+    f += 2;
+    jj += 2;
+    while (jj >= P.g) {
+      jj -= P.g;
+      ++row;
+    }
+  }
+}
+#endif
+
 }  // namespace rb

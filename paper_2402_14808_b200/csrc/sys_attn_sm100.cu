@@ -251,19 +251,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
         uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
         // all of the tile's 16-byte chunks in flight at once (zero-fill past the rows)
-#pragma unroll
-        for (int it = 0; it < NQ / 2; ++it) {
-          const int idx = lane + it * 32;
-          const int c = idx >> 4, ch = idx & 15;
-          const int f = qt * NQ + c;
-          const bool ok = f < P.rows_per_head;
-          const int row = ok ? f / P.g : 0, jj = ok ? f % P.g : 0;
-          const __nv_bfloat16* src = args.q + row * args.q_row_stride +
-                                     static_cast<long long>(h * P.g + jj) * args.q_head_stride +
-                                     ch * 8;
-          cp_async_16(qdst + (ch >> 3) * (NQ * 128) + sw128_offset(c, (ch & 7) * 8), src,
-                      ok ? 16u : 0u);
-        }
+        load_unit_q<NQ, NQ>(qdst, args, h, qt * NQ, lane);
         cp_async_wait_all();
         fence_proxy_async_smem();
         __syncwarp();

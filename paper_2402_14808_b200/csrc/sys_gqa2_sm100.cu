@@ -115,7 +115,15 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
   // diagnostics build: CTA 0 records clock64 at 8 events x 128 tiles
   // (WG0 S ready / P done, WG1 S ready / P done, MMA: P0 seen, S0 issued,
   // P1 seen, S1 issued)
-  unsigned long long* evt = (RB_DIAG && args.debug_ts && blockIdx.x == 0) ? args.debug_ts : nullptr;
+  unsigned long long* evt =
+      (RB_DIAG && args.debug_ts && blockIdx.x == 0) ? args.debug_ts + 6144 * 8 : nullptr;
+  // per-CTA %globaltimer stamps (same slots as the other system kernels):
+  // [0] entry, [1] smid, [2] first S ready (WG0), [7] exit
+  unsigned long long* dts = (RB_DIAG && args.debug_ts) ? args.debug_ts + blockIdx.x * 8 : nullptr;
+  if (dts && threadIdx.x == 0) {
+    dts[0] = global_timer_ns();
+    dts[1] = smid();
+  }
 #define G2_EVT(e, jj) \
   do {                \
     if (evt && (jj) < 128) evt[(e) * 128 + (jj)] = clock64(); \
@@ -188,19 +196,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
       const int h = u / P.n_qt, qt = u % P.n_qt;
       mbar_wait(q_empty, (uq & 1) ^ 1);
       uint8_t* qdst = smem + kOffQ;
-#pragma unroll 4
-      for (int it = 0; it < kUnitRows / 2; ++it) {
-        const int idx = lane + it * 32;          // 16-byte chunk: row c (of 256), chunk ch
-        const int c = idx >> 4, ch = idx & 15;
-        const int f = qt * kUnitRows + c;
-        const bool ok = f < P.rows_per_head;
-        const int row = ok ? f / P.g : 0, jj = ok ? f % P.g : 0;
-        const __nv_bfloat16* src = args.q + row * args.q_row_stride +
-                                   static_cast<long long>(h * P.g + jj) * args.q_head_stride + ch * 8;
-        const int sub = c / kRows, rr = c % kRows;
-        cp_async_16(qdst + sub * kQBytes + (ch >> 3) * (kRows * 128) + sw128_offset(rr, (ch & 7) * 8),
-                    src, ok ? 16u : 0u);
-      }
+      load_unit_q<kRows, kUnitRows>(qdst, args, h, qt * kUnitRows, lane);
       cp_async_wait_all();
       fence_proxy_async_smem();
       __syncwarp();
@@ -322,6 +318,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
         mbar_wait(&s_full[sub], static_cast<uint32_t>(j & 1));
         tc_fence_after();
         if (r == 0) G2_EVT(2 * sub, j);
+        if (dts && r == 0 && sub == 0 && j == 0) dts[2] = global_timer_ns();
         if (G2_NO_SOFTMAX) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[sub]);
@@ -510,6 +507,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
+  if (dts && threadIdx.x == 0) dts[7] = global_timer_ns();
 }
 
 cudaError_t launch_system_attention_gqa2(const CUtensorMap& tk, const CUtensorMap& tv,

@@ -161,19 +161,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         // the unit's 128 query rows (zero past the last row), K-major SW128
         mbar_wait(q_empty, (uq & 1) ^ 1);
         uint8_t* qdst = smem + kOffQ;
-#pragma unroll 4
-        for (int it = 0; it < kRows / 2; ++it) {
-          const int idx = lane + it * 32;
-          const int c = idx >> 4, ch = idx & 15;
-          const int f = qt * kRows + c;
-          const bool ok = f < P.rows_per_head;
-          const int row = ok ? f / P.g : 0, jj = ok ? f % P.g : 0;
-          const __nv_bfloat16* src = args.q + row * args.q_row_stride +
-                                     static_cast<long long>(h * P.g + jj) * args.q_head_stride +
-                                     ch * 8;
-          cp_async_16(qdst + (ch >> 3) * (kRows * 128) + sw128_offset(c, (ch & 7) * 8), src,
-                      ok ? 16u : 0u);
-        }
+        load_unit_q<kRows, kRows>(qdst, args, h, qt * kRows, lane);
         cp_async_wait_all();
         fence_proxy_async_smem();
         __syncwarp();

@@ -22,7 +22,7 @@ def main():
     q = torch.randn(b, hq, 128, device="cuda", generator=g).to(torch.bfloat16)
     k = torch.randn(hkv, s, 128, device="cuda", generator=g).to(torch.bfloat16)
     v = torch.randn(hkv, s, 128, device="cuda", generator=g).to(torch.bfloat16)
-    ts = torch.zeros(10 * 128, dtype=torch.int64, device="cuda")
+    ts = torch.zeros(8192 * 8, dtype=torch.int64, device="cuda")
     lib = _lib.load_diag() if not os.environ.get("RB_LIB") else _lib._bind(os.environ["RB_LIB"])
     lib.rb_debug_set_timestamps.argtypes = [__import__("ctypes").c_void_p]
     if os.environ.get("RB_LIB"):
@@ -32,7 +32,7 @@ def main():
         kernels.system_attention(q, k, v, kv_layout="hsd")
         torch.cuda.synchronize()
     lib.rb_debug_set_timestamps(None)
-    t = ts.view(10, 128).cpu()
+    t = ts[6144 * 8:6144 * 8 + 1280].view(10, 128).cpu()
     t0 = int(t[t != 0].min())
     print("tile " + " ".join(f"{n:>13s}" for n in NAMES))
     for j in range(0, int(os.environ.get("ROWS", "14"))):

@@ -28,14 +28,15 @@ def q(col):
     return f"min {col[0]:6.1f} p10 {col[n // 10]:6.1f} p50 {col[n // 2]:6.1f} p90 {col[int(n * .9)]:6.1f} max {col[-1]:6.1f}"
 
 
-def run(s, phases=3, b=32, h=52, c=128):
+def run(s, phases=3, b=32, h=52, c=128, hkv=None):
+    hkv = h if hkv is None else hkv
     dev = torch.device("cuda", 0)
     qq = torch.randn((b, h, 128), device=dev).to(torch.bfloat16)
-    k = torch.randn((h, s, 128), device=dev).to(torch.bfloat16)
-    v = torch.randn((h, s, 128), device=dev).to(torch.bfloat16)
+    k = torch.randn((hkv, s, 128), device=dev).to(torch.bfloat16)
+    v = torch.randn((hkv, s, 128), device=dev).to(torch.bfloat16)
     nblk = c // 16
-    grid = int(os.environ.get("DIAG_GRID", "0")) or _lib.relay_sys_grid(b, h, h, s, b * c, kernels.sm_count(dev))
-    pk = torch.randn((b * nblk, h, 16, 128), device=dev).to(torch.bfloat16)
+    grid = int(os.environ.get("DIAG_GRID", "0")) or _lib.relay_sys_grid(b, h, hkv, s, b * c, kernels.sm_count(dev))
+    pk = torch.randn((b * nblk, hkv, 16, 128), device=dev).to(torch.bfloat16)
     pv = torch.randn_like(pk)
     pst = (pk.stride(0), pk.stride(2), pk.stride(1))
     bt = torch.randperm(b * nblk, device=dev).to(torch.int32).reshape(b, nblk)
@@ -53,7 +54,7 @@ def run(s, phases=3, b=32, h=52, c=128):
         _lib.load_diag().rb_debug_set_timestamps(ts.data_ptr() if it == 4 else None)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=1, hkv=h, sys_layout="hsd",
+        kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=h // hkv, hkv=hkv, sys_layout="hsd",
                                 block_table=bt, block_size=16, strides=pst, grid=grid,
                                 phases=phases)
         e1.record()
@@ -123,5 +124,7 @@ def run(s, phases=3, b=32, h=52, c=128):
 if __name__ == "__main__":
     s = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     ph = [int(sys.argv[2])] if len(sys.argv) > 2 else [3, 2]
+    # optional workload: b h hkv c (default C2: 32 52 52 128)
+    b, h, hkv, c = (int(x) for x in sys.argv[3:7]) if len(sys.argv) > 6 else (32, 52, 52, 128)
     for p in ph:
-        run(s, p)
+        run(s, p, b=b, h=h, c=c, hkv=hkv)
