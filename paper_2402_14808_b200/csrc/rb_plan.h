@@ -137,7 +137,8 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
 // (profiles/r02/sweep_split.txt: 60 / 90 / ~106 / ~115 system CTAs).
 #define RB_RELAY_RATE_RATIO 1.3
 #define RB_GQA2_TILE_US 2.0   /* sys_gqa2: one 128-key tile for 256 query rows */
-#define RB_CTX_SM_GBS 38.0    /* context kernel streaming rate per SM */
+#define RB_CTX_SM_GBS 38.0    /* context kernel streaming rate per SM (1-2 rows per item) */
+#define RB_CTX_SM_GBS_GQA 50.0 /* ... with >= 4 rows per item (C4 measured 52) */
 RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sms) {
   rb_sys_plan p;
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
@@ -147,11 +148,15 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   if (p.nq == 256 && p.n_units <= sms) {
     // the 256-row GQA kernel is tensor-bound: balance measured time, not
     // bytes -- RB_GQA2_TILE_US per key tile per CTA against the context
-    // kernel's RB_CTX_SM_GBS per SM (profiles/r02), rounded to whole
+    // kernel's RB_CTX_SM_GBS(_GQA) per SM (profiles/r02), rounded to whole
     // multiples of the unit count (CTAs on a head's units share K/V in L2;
-    // measured C4 64 / 80 CTAs within 4%, C5 128 CTAs 31% faster than 64)
+    // measured C4: 64 / 80 / 96 / 112 CTAs -> 157 / 137 / 134 / 212 us;
+    // C5: 64 / 96 / 128 / 144 -> 1091 / 878 / 728 / 726 us)
     const double sys_work = (double)p.total * RB_GQA2_TILE_US;
-    const double ctx_work = ctx_bytes / (RB_CTX_SM_GBS * 1e3);
+    // context items of >= 4 query rows (GQA groups) share each K/V chunk
+    // across the rows and stream faster per SM
+    const double ctx_rate = p.g >= 4 ? RB_CTX_SM_GBS_GQA : RB_CTX_SM_GBS;
+    const double ctx_work = ctx_bytes / (ctx_rate * 1e3);
     const double gt = sms * sys_work / (sys_work + ctx_work);
     int k = (int)(gt / p.n_units + 0.5);
     if (k < 1) k = 1;
