@@ -415,12 +415,10 @@ class RelayDecodeStep:
             # concurrent split: system CTAs by their share of the step's HBM bytes
             grid = _lib.relay_sys_grid(self.b, hq, self.hkv, sys_cache.system_len,
                                        int(ctx_lens.sum().item()), kernels.sm_count(dev))
+        if grid < 1:
+            raise ContractError(f"grid must be >= 1 system CTAs, got {grid}")
         self.grid = grid
-        # grid 0: the unified step (no system kernel; the context kernel takes
-        # the prefix as 8-row items) -- the plan then describes nothing launched
-        self.unified = grid == 0
-        self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, max(1, self.grid))
-        self.plan["unified"] = int(self.unified)
+        self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         # the block table's capacity bounds every context it can address, so
         # the split-K plan stays valid while the contexts grow into it
         self.max_ctx_len = block_table.shape[1] * paged_cache.block_size

@@ -305,7 +305,6 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = nullptr;  // static item order
-  a.sys_items = a.sys_rt = a.sys_splits = a.sys_split_chunks = 0;
   int st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, workspace, workspace_bytes);
   if (st != RB_OK) return st;
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
@@ -324,73 +323,8 @@ static void relay_ws_layout(const rb_sys_plan& p, size_t* cnt_bytes, size_t* cpa
   *acc_bytes = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
 }
 
-// Unified relay step (grid_cap == 0): no system kernel; the context kernel
-// takes the shared prefix as items of 8 flattened rows x sys_split_chunks
-// chunks (at most 4 splits per 8-row tile) next to the context items.
-// Eligible for decode batches (n_rows == b) with g | 8.
-struct UnifiedPlan {
-  int rt, splits, split_chunks, items, ctx_chunks, n_split;
-};
-static bool unified_plan(int b, int n_rows, int hq, int hkv, int s, int max_ctx_len, int sms,
-                         UnifiedPlan* u) {
-  const int g = hq / hkv;
-  if (n_rows != b || g < 1 || 8 % g != 0 || s < 1) return false;
-  const int n_pre = (s + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK;
-  u->rt = (b * g + 7) / 8;
-#ifndef RB_UNIFIED_SPLITS
-#define RB_UNIFIED_SPLITS 4
-#endif
-  int L = (n_pre + RB_UNIFIED_SPLITS - 1) / RB_UNIFIED_SPLITS;
-  if (L < RB_CTX_SPLIT_MIN_CHUNKS) L = RB_CTX_SPLIT_MIN_CHUNKS;
-  u->split_chunks = L;
-  u->splits = (n_pre + L - 1) / L;
-  u->items = hkv * u->rt * u->splits;
-  ctx_split_plan(b, hkv, g, 0, max_ctx_len, sms, &u->ctx_chunks, &u->n_split);
-  return true;
-}
-// The system units of the unified step in rb_sys_plan terms: unit = (kv
-// head, 8-row tile), one "tile" per system split, one CTA per tile, so every
-// unit has `splits` parts in split order (slot = split) -- what the relay
-// fusion in the context kernel reads.
-static void unified_sys_plan(rb_sys_plan* p, const UnifiedPlan& u, int n_rows, int hq, int hkv,
-                             int s) {
-  p->n_rows = n_rows;
-  p->hq = hq;
-  p->hkv = hkv;
-  p->g = hq / hkv;
-  p->s = s;
-  p->nq = 8;
-  p->rows_per_head = n_rows * p->g;
-  p->n_qt = u.rt;
-  p->tpu = u.splits;
-  p->n_units = hkv * u.rt;
-  p->total = (long long)p->n_units * u.splits;
-  p->grid = (int)p->total;
-  p->max_parts = u.splits;
-  p->rr = 0;
-}
-
 int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, int b,
                              int max_rows, int max_ctx_len, int sm_count, size_t* bytes) {
-  if (grid_cap == 0) {
-    UnifiedPlan u;
-    if (n_rows < 1 || hq < 1 || hkv < 1 || hq % hkv != 0)
-      return fail(RB_ERR_DIMENSION, "bad relay shape");
-    if (s < 1)
-      return fail(RB_ERR_CONTRACT,
-                  "relay attention requires a non-empty system segment; use the baseline path "
-                  "when there is no shared prefix");
-    if (!unified_plan(b, n_rows, hq, hkv, s, max_ctx_len, sm_count, &u))
-      return fail(RB_ERR_CONTRACT, "grid 0 (unified relay step) needs a decode batch (one row per "
-                                   "request) with a GQA group dividing 8");
-    rb_sys_plan p;
-    unified_sys_plan(&p, u, n_rows, hq, hkv, s);
-    size_t cnt, cpart, ml, acc;
-    relay_ws_layout(p, &cnt, &cpart, &ml, &acc);
-    const size_t split = (size_t)rb_ctx_split_bytes(b, n_rows, hq, hkv, 8, u.n_split);
-    *bytes = 256 + cnt + cpart + ml + ((acc + 255) & ~(size_t)255) + split;
-    return RB_OK;
-  }
   long long f[8];
   size_t dummy = 0;
   int st = rb_sys_plan_query(n_rows, hq, hkv, s, grid_cap, f, &dummy);
@@ -408,7 +342,6 @@ int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, i
 
 int rb_relay_sys_grid(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sm_count,
                       int* grid) {
-  // (0 = the unified step: no system kernel, see rb_relay_split)
   if (n_rows < 1 || hq < 1 || hkv < 1 || hq % hkv != 0 || s < 1 || sm_count < 1 || ctx_tokens < 0)
     return fail(RB_ERR_DIMENSION, "bad relay split arguments");
   *grid = rb_relay_split(n_rows, hq, hkv, s, ctx_tokens, sm_count);
@@ -439,14 +372,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
     return fail(RB_ERR_CONTRACT, "q rows must be 16-byte aligned");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
   rb::SysArgs sa;
-  UnifiedPlan up;
-  const bool unified = grid_cap == 0;
-  if (unified) {
-    unified_plan(b, n_rows, hq, hkv, s, max_ctx_len, sms, &up);
-    unified_sys_plan(&sa.plan, up, n_rows, hq, hkv, s);
-  } else {
-    rb_make_sys_plan(&sa.plan, n_rows, hq, hkv, s, grid_cap);
-  }
+  rb_make_sys_plan(&sa.plan, n_rows, hq, hkv, s, grid_cap);
   sa.q = static_cast<const __nv_bfloat16*>(q);
   sa.q_row_stride = q_row_stride;
   sa.q_head_stride = q_head_stride;
@@ -468,7 +394,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   if (st != RB_OK) return st;
   st = make_kv_map(&tv, sys_v, s, hkv, sys_stride_tok, sys_stride_head);
   if (st != RB_OK) return st;
-  if ((phases & 1) && !unified) {
+  if (phases & 1) {
     st = cuda_status(rb::launch_system_attention(tk, tv, sa, cs), "system attention launch");
     if (st != RB_OK) return st;
   }
@@ -509,34 +435,19 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = header;  // workspace header: dynamic item counters
-  a.sys_items = a.sys_rt = a.sys_splits = a.sys_split_chunks = 0;
   {
     // (the context split-K plan covers the context chunks only)
     const size_t split_off = 256 + cnt + cpart + ml + ((acc_b + 255) & ~(size_t)255);
     st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, ws + split_off, workspace_bytes - split_off);
     if (st != RB_OK) return st;
   }
-  if (unified) {
-    // the prefix as context-kernel items (pk / pv / s_prefix), publishing
-    // into the same unit counters / parts the system kernel would
-    a.pk = static_cast<const __nv_bfloat16*>(sys_k);
-    a.pv = static_cast<const __nv_bfloat16*>(sys_v);
-    a.p_stride_tok = sys_stride_tok;
-    a.p_stride_head = sys_stride_head;
-    a.s_prefix = s;
-    a.sys_items = up.items;
-    a.sys_rt = up.rt;
-    a.sys_splits = up.splits;
-    a.sys_split_chunks = up.split_chunks;
-  }
-  if (!(phases & 1) && !(phases & 4) && !unified) {
+  if (!(phases & 1) && !(phases & 4)) {
     // context phase alone (profiling): the slots of an earlier phase-1 call
     // are complete; mark every unit published (the kernel rearms them)
     cudaError_t me = cudaMemsetAsync(sa.counters, 0x3f, (size_t)sa.plan.n_units * sizeof(int), cs);
     if (me != cudaSuccess) return cuda_status(me, "relay counters");
   }
-  // unified: 8-row items (system tiles); decode context items have g <= 8 rows
-  return cuda_status(rb::launch_context_attention(a, unified ? 8 : max_rows, cs),
+  return cuda_status(rb::launch_context_attention(a, max_rows, cs),
                      "context attention launch");
 }
 

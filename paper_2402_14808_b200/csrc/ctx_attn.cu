@@ -58,8 +58,6 @@ struct CtxItem {
   int r, h, z, row0, m_r, nrows, c_r, max_lim, n_chunks;
   int sp, grp, nsplit, k0;  // split index, (r, h, z) group, valid splits of it, first chunk
   int bt0;                  // block-table index of the item's bt[0] window
-  int sys;                  // 1: a system-prefix item of the unified step (r = its 8-row tile)
-  int slot, ntot;           // partial slot of this item, slots its group combines (context items)
   long long roff;           // ragged mode: first token of request r
 };
 
@@ -588,7 +586,6 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     int* sched = a.sched;
     const bool paged = a.ctx.block_table != nullptr;
     const int per_req = n_z * a.hkv * n_split;
-    const int n_sys = a.sys_items;   // unified step: the prefix items come first
     struct Raw {
       int item, qs0, qs1, clen, bte, bt0;
       long long roff;
@@ -598,10 +595,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       w.item = item;
       w.qs0 = w.qs1 = w.clen = w.bte = w.bt0 = 0;
       w.roff = 0;
-      if (item < n_items && item >= n_sys) {
-        const int ci = item - n_sys;
-        const int r = ci / per_req;
-        const int sp = ci % n_split;
+      if (item < n_items) {
+        const int r = item / per_req;
+        const int sp = item % n_split;
         w.qs0 = __ldg(a.q_start + r);
         w.qs1 = __ldg(a.q_start + r + 1);
         w.clen = __ldg(a.ctx_lens + r);
@@ -610,7 +606,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
           // the split's first context block (splits start on chunk
           // boundaries; a chunk never straddles blocks when block_size % 16
           // == 0, the only case the table window is used for)
-          const int c0 = (n_sys > 0 ? sp * a.split_chunks : max(0, sp * a.split_chunks - n_pre)) * kChunk;
+          const int c0 = max(0, sp * a.split_chunks - n_pre) * kChunk;
           w.bt0 = c0 / a.ctx.block_size;
           // rows of the table are bt_stride long: entries past it are never read
           if (w.bt0 + lane < a.ctx.bt_stride)
@@ -648,33 +644,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         break;
       }
       CtxItem<R> it;
-      it.sys = 0;
       it.bt0 = cur.bt0;
       it.roff = cur.roff;
-      if (item < n_sys) {
-        // system-prefix item: head h, 8-row tile rt of the head's flattened
-        // rows (decode: row f = request f / g, member f % g), split sp
-        const int per_h = a.sys_rt * a.sys_splits;
-        it.sys = 1;
-        it.h = item / per_h;
-        it.r = (item / a.sys_splits) % a.sys_rt;
-        it.sp = item % a.sys_splits;
-        it.slot = it.sp;
-        it.ntot = 0;
-        it.grp = 0;
-        it.z = 0;
-        it.row0 = it.r * 8;
-        it.m_r = 1;
-        it.nrows = min(R, a.b * a.g - it.row0);
-        it.c_r = 0;
-        it.max_lim = a.s_prefix;
-        it.nsplit = 1;
-        it.k0 = it.sp * a.sys_split_chunks;
-        it.n_chunks = min(a.sys_split_chunks, n_pre - it.k0);
-      } else {
-        const int ci = item - n_sys;
-        it.sp = ci % n_split;
-        const int grp = ci / n_split;
+      {
+        it.sp = item % n_split;
+        const int grp = item / n_split;
         it.grp = grp;
         it.z = grp % n_z;
         it.h = (grp / n_z) % a.hkv;
@@ -683,10 +657,8 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         it.m_r = cur.qs1 - cur.qs0;
         it.nrows = it.m_r * a.g;
         it.c_r = cur.clen;
-        // unified step: the prefix belongs to the system items
-        const int pre_here = n_sys > 0 ? 0 : n_pre;
         const int rb = it.z * R;
-        it.k0 = n_pre - pre_here;
+        it.k0 = 0;
         it.nsplit = 1;
         if (rb >= it.nrows) {
           it.max_lim = 0;
@@ -694,19 +666,17 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         } else {
           const int t_last = (min(rb + R, it.nrows) - 1) / a.g;
           it.max_lim = a.causal ? it.c_r - it.m_r + t_last + 1 : it.c_r;
-          const int total = pre_here + (it.max_lim + kChunk - 1) / kChunk;
+          const int total = n_pre + (it.max_lim + kChunk - 1) / kChunk;
           it.n_chunks = total;
           if (n_split > 1) {
             // split sp: chunks [sp L, (sp+1) L), the last valid split takes the rest
             const int L = a.split_chunks;
             it.nsplit = min(n_split, max(1, (total + L - 1) / L));
-            it.k0 += it.sp * L;
+            it.k0 = it.sp * L;
             it.n_chunks = it.sp >= it.nsplit ? 0
                           : (it.sp == it.nsplit - 1 ? total - it.sp * L : L);
           }
         }
-        it.slot = it.sp;
-        it.ntot = it.nsplit;
       }
       const int rbase = it.z * R;
       const int nvalid = it.n_chunks > 0 ? max(0, min(R, it.nrows - rbase)) : 0;
@@ -721,13 +691,12 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         mbar_arrive_expect_tx(&i_full[qs], nvalid * kRowBytes);
       }
       __syncwarp();
-      // query rows of the item: one 256-byte bulk copy per row (a system
-      // item's rows come from 8 / g requests: row f = request f / g)
+      // query rows of the item: one 256-byte bulk copy per row
       if (lane < nvalid) {
         const int li = rbase + lane;
         const int t = li / a.g, jj = li % a.g;
-        const __nv_bfloat16* qp = a.q + static_cast<long long>(it.sys ? (it.row0 + li) / a.g : it.row0 + t) * a.q_row_stride +
-                                  static_cast<long long>(it.h * a.g + (it.sys ? (it.row0 + li) % a.g : jj)) * a.q_head_stride;
+        const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
+                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride;
         bulk_copy_g2s(smem + SM::kOffQ + (qs * R + lane) * kRowBytes, qp, kRowBytes, &i_full[qs]);
       }
       cur = nxt;
@@ -773,17 +742,6 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     }
     const int d0 = lane * 4;
     int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
-    // unified step: a system item's part is published one item later (its
-    // stores have drained by then, so the release fence costs little)
-    int pend_u = -1;
-    auto publish_pending = [&]() {
-      if (pend_u >= 0 && lane == 0) {
-        __threadfence();
-        atomicAdd(a.sys_ready + pend_u, 1);
-      }
-      pend_u = -1;
-    };
-
     // the last step of a (row, head): relay fusion / park, or output
     auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts& pp) {
       if (a.ctx_part != nullptr) {
@@ -855,10 +813,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         ++jp;
         if (item < 0 || it.n_chunks > 0) break;
       }
-      if (item < 0) {
-        publish_pending();
-        break;
-      }
+      if (item < 0) break;
       const bool split = it.nsplit > 1;
       const int nslots = n_split;
       // relay: if row 0's system unit is already published, issue its
@@ -875,7 +830,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         for (int k = 0; k < kPollSlots; ++k)
           if (np[k] != 0x7fffffff && !((pub >> k) & 1)) pv[k] = ld_acquire_gpu(a.sys_ready + lane + 32 * k);
       }
-      if (a.ctx_part != nullptr && !split && !it.sys && it.z * R < it.nrows) {
+      if (a.ctx_part != nullptr && !split && it.z * R < it.nrows) {
         const long long o0 = static_cast<long long>(it.row0 + (it.z * R) / a.g) * a.hq +
                              it.h * a.g + (it.z * R) % a.g;
         pre = poll ? relay_unit_published(a.sys_plan, a.hq, o0, pub)
@@ -897,19 +852,13 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         d_mfull += t1 - d_t;
         d_t = t1;
       }
-      publish_pending();
       const float* bacc = s_acc + mb * kWorkers * R * kAccStride;
       const float* bml = s_ml + mb * kWorkers * R * 2;
       const int rbase = it.z * R;
       const int nrow = min(R, it.nrows - rbase);
-      // output row of item row i: context items -- request row0 + t, group
-      // member jj; system items -- flattened row f = row0 + i of the head
+      // output row of item row i: request row0 + t, group member jj
       auto row_oidx = [&](int i) -> long long {
         const int li = rbase + i;
-        if (it.sys) {
-          const int f = it.row0 + li;
-          return static_cast<long long>(f / a.g) * a.hq + it.h * a.g + f % a.g;
-        }
         const int t = li / a.g, jj = li % a.g;
         return static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
       };
@@ -934,19 +883,8 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
             O.w = fmaf(av.w, wt, O.w);
           }
         }
-        if (it.sys) {
-          // unified step: this item is part it.sp of system unit (head,
-          // 8-row tile) -- the layout the system kernels write (rb_plan.h)
-          const long long pb = static_cast<long long>(it.h * a.sys_plan.n_qt + it.r) *
-                                   a.sys_plan.max_parts + it.sp;
-          __stcg(reinterpret_cast<float4*>(const_cast<float*>(a.sys_part_acc) + (pb * a.sys_plan.nq + i) * RB_HEAD_DIM + d0), O);
-          if (lane == 0) {
-            float* pml = const_cast<float*>(a.sys_part_ml) + pb * 2 * a.sys_plan.nq;
-            __stcg(pml + i, M);
-            __stcg(pml + a.sys_plan.nq + i, Ls);
-          }
-        } else if (split) {
-          float* dst = a.split_part + (oidx * nslots + it.slot) * kPartStride;
+        if (split) {
+          float* dst = a.split_part + (oidx * nslots + it.sp) * kPartStride;
           __stcg(reinterpret_cast<float4*>(dst + d0), O);
           if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
         } else {
@@ -955,13 +893,6 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&m_empty[mb]);
-      if (it.sys) {
-        // the part is published with the next item (or at the end): context
-        // rows of this unit fuse with it once all sys_splits parts are in
-        pend_u = it.h * a.sys_plan.n_qt + it.r;
-        if (dts) d_work += global_timer_ns() - d_t;
-        continue;
-      }
       if (split) {
         // the last split of the item to finish combines every split's
         // partial in split order (bitwise independent of the arrival order)
@@ -1230,7 +1161,7 @@ cudaError_t launch_context_attention(const CtxArgs& a, int max_rows, cudaStream_
   // max_rows = max over requests of m_r * g
   const int R = rb_ctx_rows(max_rows);
   const int n_z = (max_rows + R - 1) / R;
-  const long long n_items = static_cast<long long>(a.b) * a.hkv * n_z * a.n_split + a.sys_items;
+  const long long n_items = static_cast<long long>(a.b) * a.hkv * n_z * a.n_split;
   if (n_items == 0) return cudaSuccess;
   if (n_items > 0x7fffffffLL) return cudaErrorInvalidValue;
   switch (R) {

@@ -64,20 +64,12 @@ struct CtxArgs {
   float* lse_out;                // [n_rows][hq] natural log (may be null)
   float scale_log2;
   unsigned long long* debug_ts;  // optional per-CTA stamps [grid][8] (diagnostics)
-  int* sched;                    // optional [3] zeroed counters: item claims, scheduler / CTA exits
+  int* sched;                    // optional [2] zeroed counters: item claims, CTA exits (dynamic claims)
   // split-K over long contexts (rb_ctx_split): split_chunks 16-token chunks
   // per split (0: no split), n_split splits per (request, kv head, row tile)
   int split_chunks, n_split;
   float* split_part;             // [n_rows * hq][n_split][132] f32 partials (O, m log2, l)
   int* split_cnt;                // [b * hkv * n_z] zeroed counters, rearmed by the last split
-  // unified relay step (no system kernel; decode, g | 8): the shared prefix
-  // (pk / pv / s_prefix) is cut into sys_items = hkv * sys_rt * sys_splits
-  // items of 8 flattened query rows x sys_split_chunks 16-key chunks, claimed
-  // before the context items; each writes part sp of system unit (head,
-  // 8-row tile) -- sys_plan is then nq = 8, n_qt = sys_rt, max_parts =
-  // sys_splits -- and publishes it on sys_ready, so the context rows fuse
-  // with the system parts exactly as in the two-kernel step.  0: off.
-  int sys_items, sys_rt, sys_splits, sys_split_chunks;
 };
 
 #ifdef __CUDACC__

@@ -136,10 +136,6 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
 // fit on B200 with profiles/sweep_split.py to the best splits at s = 4k..32k
 // (profiles/r02/sweep_split.txt: 60 / 90 / ~106 / ~115 system CTAs).
 #define RB_RELAY_RATE_RATIO 1.3
-// the unified step is never picked automatically: measured on C2 it is
-// 53-67 us at s = 512-2048 against 41-49 us for the two kernels (its merger
-// warp serialises ~2 us of fusion per item; profiles/r02) -- grid 0 selects it
-#define RB_UNIFIED_MAX_RATIO 0.0   /* system bytes / context bytes of the unified step */
 #define RB_GQA2_TILE_US 2.0   /* sys_gqa2: one 128-key tile for 256 query rows */
 #define RB_CTX_SM_GBS 38.0    /* context kernel streaming rate per SM (1-2 rows per item) */
 #define RB_CTX_SM_GBS_GQA 50.0 /* ... with >= 4 rows per item (C4 measured 52) */
@@ -148,12 +144,6 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
   const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
   const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
-  // a short shared prefix next to a longer context (decode, GQA group
-  // dividing 8): no system kernel at all -- the context kernel takes the
-  // prefix as 8-row items (grid 0, the unified step), so every SM streams
-  // from the start and no prologue / SM split sits on the critical path
-  if (RB_UNIFIED_MAX_RATIO > 0 && 8 % p.g == 0 && sys_bytes <= RB_UNIFIED_MAX_RATIO * ctx_bytes)
-    return 0;
   int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
   if (p.nq == 256 && p.n_units <= sms) {
     // the 256-row GQA kernel is tensor-bound: balance measured time, not

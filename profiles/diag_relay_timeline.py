@@ -117,6 +117,12 @@ def run(s, phases=3, b=32, h=52, c=128, hkv=None):
             for i, n in enumerate(names):
                 col = [float(v) / (1 if i == 1 else 1e3) for v in acc[:, i].tolist()]
                 print(f"  ctx {n:20s} {q(col)}")
+        wst = t[6144:6144 + 1024][t[6144:6144 + 1024, 4] != 0]
+        if len(wst):
+            for i, n in enumerate(["w0 in try_issue", "w0 data wait", "w0 compute"]):
+                print(f"  ctx {n:20s} {q([float(v) / 1e3 for v in wst[:, i].tolist()])}")
+            print(f"  ctx w0 chunks        {q([float(v) for v in wst[:, 4].tolist()])}")
+            print(f"  ctx w0 waits w/ 1 in flight {q([float(v) for v in wst[:, 3].tolist()])}")
         durs = [(int(r[7]) - int(r[0])) / 1e3 for r in ctx_t]
         print(f"  ctx CTA duration p50 {statistics.median(durs):.1f} max {max(durs):.1f}")
 

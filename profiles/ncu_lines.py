@@ -46,6 +46,7 @@ def sass_lines(kernel_sub):
 def main():
     rep, ksub = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+    by_inst = len(sys.argv) > 4 and sys.argv[4] == "inst"  # rank lines by instructions executed
     csv_text = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                               capture_output=True, text=True).stdout
     rows = list(csv.reader(csv_text.splitlines()))
@@ -70,7 +71,8 @@ def main():
     tot_i, tot_s = sum(inst.values()), sum(samp.values())
     srcs = {}
     print(f"instructions {tot_i}, stall samples {tot_s}")
-    for loc, s in samp.most_common(top):
+    ranked = [(loc, samp[loc]) for loc, _ in inst.most_common(top)] if by_inst else samp.most_common(top)
+    for loc, s in ranked:
         if loc is None:
             continue
         f, ln = loc

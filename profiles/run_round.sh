@@ -14,10 +14,10 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/${tag}_
 timeout 900 python profiles/bench_configs.py --naive > $out/${tag}_configs.log 2>&1; echo "configs rc $?"
 # launch list of the bench step (kernels of this repo only; cold-cache, serialised)
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-  -k regex:"sys_attn|ctx_cta|kv_append" -c 60 --csv --log-file $out/${tag}_launches.csv \
+  -k regex:"sys_attn|ctx_|kv_append" -c 60 --csv --log-file $out/${tag}_launches.csv \
   python bench.py --steps 3 --warmup 1 --sweep "" --no-cpu-baseline > $out/${tag}_ncu_launch.log 2>&1; echo "ncu launches rc $?"
 # one full capture of each kernel of the relay step at C2 s=8192
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sys_attn|ctx_cta" -c 2 -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sys_attn|ctx_" -c 2 -f \
   -o $out/${tag}_prof_step python profiles/diag_relay_timeline.py 8192 3 > $out/${tag}_ncu_step.log 2>&1; echo "ncu step rc $?"
 # one full capture of the GQA-large system kernel (C4 shape, alone on all SMs)
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sys_gqa -s 3 -c 1 -f \

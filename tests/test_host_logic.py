@@ -102,7 +102,7 @@ def test_block_pool_conservation():
 
 def test_relay_sm_split():
     """rb_relay_sys_grid: within [1, sms], never below the latency floor,
-    non-decreasing in s (the unified step, grid 0, is opt-in)."""
+    non-decreasing in s."""
     sms = 148
     ctx = 32 * 128
     prev = 0
@@ -112,21 +112,9 @@ def test_relay_sm_split():
         assert g >= min(sms * 20 // 100, SysPlan(32, 52, 52, s, sms).total)
         assert g >= prev
         prev = g
-    # GQA groups not dividing 8 keep the two-kernel step
     assert _lib.relay_sys_grid(30, 24, 8, 512, 30 * 4096, sms) >= 1
     # no context at all: the system kernel takes every SM
     assert _lib.relay_sys_grid(32, 52, 52, 8192, 0, sms) == sms
-
-
-def test_unified_workspace_contract():
-    """grid 0 sizes the unified step's workspace; non-decode batches or
-    groups not dividing 8 are refused (ContractError)."""
-    from paper_2402_14808_b200.errors import ContractError
-    assert _lib.relay_workspace_bytes(32, 52, 52, 512, 0, 32, 1, 128, 148) > 256
-    with pytest.raises(ContractError):
-        _lib.relay_workspace_bytes(64, 52, 52, 512, 0, 32, 2, 128, 148)   # 2 rows per request
-    with pytest.raises(ContractError):
-        _lib.relay_workspace_bytes(8, 24, 8, 512, 0, 8, 3, 128, 148)      # g = 3
 
 
 def test_plan_tile_sizes_and_aligned_split():
