@@ -89,6 +89,29 @@ __device__ __forceinline__ void chunk_cp_async(uint8_t* slot, const __nv_bfloat1
   }
 }
 
+// The common case of the chunk copy: 16 valid rows, 256 B apart (a paged
+// block's rows of one head, the [blocks][heads][block][128] layout): every
+// address is a base register plus an immediate, no predicates.
+__device__ __forceinline__ void cp_async_16_full(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(gsrc))
+               : "memory");
+}
+__device__ __forceinline__ void chunk_cp_async_full(uint8_t* slot, const __nv_bfloat16* kb,
+                                                    const __nv_bfloat16* vb, int lane) {
+  const int row0 = lane >> 4, c16 = lane & 15;
+  const int cx = c16 ^ row0;
+  uint8_t* d = slot + row0 * kRowBytes;
+  const char* ks = reinterpret_cast<const char*>(kb) + row0 * kRowBytes + c16 * 16;
+  const char* vs = reinterpret_cast<const char*>(vb) + row0 * kRowBytes + c16 * 16;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t off = i * 2 * kRowBytes + ((cx ^ ((2 * i) & 6)) << 4);
+    cp_async_16_full(d + off, ks + i * 2 * kRowBytes);
+    cp_async_16_full(d + kChunk * kRowBytes + off, vs + i * 2 * kRowBytes);
+  }
+}
+
 // Cold path of the chunk copy (blocks not a multiple of 16 tokens, or other
 // row layouts): per-row addresses through the block table.  Out of line so
 // the hot loop stays small (instruction-cache resident).
@@ -319,10 +342,10 @@ __device__ __forceinline__ RelayParts relay_parts_begin(const rb_sys_plan& SP, i
                                                         const float* part_acc, const float* part_ml,
                                                         int lane) {
   RelayParts P;
-  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
-  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-  const int qt = static_cast<int>(f / SP.nq);
-  P.col = static_cast<int>(f % SP.nq);
+  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+  const int f = row * SP.g + hh % SP.g;
+  const int qt = f / SP.nq;
+  P.col = f % SP.nq;
   const int u = (hh / SP.g) * SP.n_qt + qt;
   P.np = rb_unit_parts(&SP, u);
   P.base = static_cast<long long>(u) * SP.max_parts;
@@ -376,9 +399,9 @@ __device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, l
 // probes with acquire semantics; the answer is broadcast to the warp.
 __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, long long pair,
                                                  const int* ready, int lane, bool block) {
-  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
-  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-  const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+  const int f = row * SP.g + hh % SP.g;
+  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
   if (u >= SP.n_units) return false;  // outside the plan (bad q_start): parked, then dropped
   const int np = rb_unit_parts(&SP, u);
   int ok = 1;
@@ -398,9 +421,9 @@ __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, 
 constexpr int kPollSlots = 8;   // polls up to 256 system units
 __device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int hq, long long pair,
                                                      uint32_t pub) {
-  const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
-  const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-  const int u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+  const int f = row * SP.g + hh % SP.g;
+  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
   const uint32_t bits = __shfl_sync(0xffffffffu, pub, u & 31);
   return u < 32 * kPollSlots && ((bits >> (u >> 5)) & 1);
 }
@@ -433,10 +456,10 @@ __device__ __forceinline__ void relay_fuse_parked8(const rb_sys_plan& SP, int hq
   const int sub = lane & 7;
   int u = 0, col = 0, np = 0;
   if (valid) {
-    const int row = static_cast<int>(pair / hq), hh = static_cast<int>(pair % hq);
-    const long long f = static_cast<long long>(row) * SP.g + hh % SP.g;
-    col = static_cast<int>(f % SP.nq);
-    u = (hh / SP.g) * SP.n_qt + static_cast<int>(f / SP.nq);
+    const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+    const int f = row * SP.g + hh % SP.g;
+    col = f % SP.nq;
+    u = (hh / SP.g) * SP.n_qt + f / SP.nq;
     valid = u < SP.n_units;  // a row outside the plan (bad q_start) is dropped, never awaited
     np = valid ? rb_unit_parts(&SP, u) : 0;
     if (sub == 0 && valid)
@@ -517,6 +540,27 @@ struct CtaSmem {
   static_assert(kBytes <= 113 * 1024, "two context CTAs must fit one SM");
 };
 
+// Diagnostics build only: per-warp event trace of CTAs 0 and 1 (clock64,
+// 256 events per warp) at debug_ts + 6144 * 8, read by
+// profiles/diag_ctx_trace.py.
+struct WarpTrace {
+  unsigned long long* p;
+  int n;
+  __device__ __forceinline__ void init(unsigned long long* dts_ctx, int warp, int lane) {
+    p = nullptr;
+    n = 0;
+    if (RB_DIAG && dts_ctx != nullptr && blockIdx.x < 2 && lane == 0)
+      p = dts_ctx - static_cast<long long>(blockIdx.x) * 8 + 6144 * 8 + (blockIdx.x * 6 + warp) * 512;
+  }
+  __device__ __forceinline__ void ev(int code) {
+    if (RB_DIAG && p != nullptr && n < 256) {
+      p[2 * n] = clock64();
+      p[2 * n + 1] = static_cast<unsigned long long>(code);
+    }
+    ++n;
+  }
+};
+
 // Merge two unnormalised softmax states (O, m log2, l) -- the merge of
 // `relay_fusion` (attention.py:137-157) without the normalisation.
 __device__ __forceinline__ void merge_state(float4& O, float& m, float& l, float4 Ok, float mk, float lk) {
@@ -574,6 +618,8 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     dts[1] = smid();
   }
 
+  WarpTrace tr;
+  tr.init(dts, warp, lane);
   if (warp == 0) {
     // ----------------------------------------------------------- scheduler
     // Software pipeline: publish item j, load item j+1's metadata, claim
@@ -632,9 +678,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       ItemSlot<R>& slot = iq[qs];
       // claim item j+3 and load item j+1 while this one is published
       int p = id2 + G;
+      tr.ev(600000 + item);
       if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
       const Raw nxt = load_raw(id1);
       mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
+      tr.ev(610000 + item);
       if (item >= n_items) {
         if (lane == 0) {
           slot.item = -1;
@@ -702,6 +750,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       cur = nxt;
       id1 = id2;
       id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;
+      tr.ev(620000 + id2);
     }
     if (sched != nullptr && lane == 0) {
       // every scheduler's last claim precedes its arrival here, so the last
@@ -846,7 +895,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       const int mb = mi % kNB;
       const uint32_t mph = static_cast<uint32_t>((mi / kNB) & 1);
       if (dts) d_t = global_timer_ns();
+      tr.ev(700000 + item);
       mbar_wait(&m_full[mb], mph);
+      tr.ev(710000 + item);
       if (dts) {
         const unsigned long long t1 = global_timer_ns();
         d_mfull += t1 - d_t;
@@ -892,6 +943,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         }
       }
       __syncwarp();
+      tr.ev(720000 + item);
       if (lane == 0) mbar_arrive(&m_empty[mb]);
       if (split) {
         // the last split of the item to finish combines every split's
@@ -945,6 +997,17 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   long long iss_roff = 0;
   bool have_iss = false;
   int issued = 0, consumed = 0, iss_sl = 0;
+  // Fast issue mode (paged, blocks of a multiple of 16 tokens whose rows are
+  // 256 B apart, no prefix segment, <= 32 chunks of this worker in the
+  // item): when the cursor enters an item, lane l resolves the K address of
+  // the worker's l-th chunk of it (block-table window or a direct load, all
+  // lanes in parallel); issuing a chunk is then one 64-bit shuffle and 16
+  // immediate-offset copies.  V sits at a fixed distance from K.
+  bool iss_fast = false;
+  const __nv_bfloat16* lane_kaddr = a.ctx.k;
+  const long long vdiff = a.ctx.v - a.ctx.k;
+  const bool fast_ok = a.ctx.block_table != nullptr && a.ctx.block_size % kChunk == 0 &&
+                       a.ctx.stride_tok == RB_HEAD_DIM && n_pre == 0;
 
   // Issue chunks while the ring has room.  The cursor blocks on the item
   // queue only for items <= jc (already published); for later items it
@@ -969,6 +1032,19 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         iss_bte = iq[qs].bt[lane];
         have_iss = true;
         ki = w;
+        iss_fast = fast_ok && iss_item >= 0 && iss_nch <= w + 4 * 32;
+        if (iss_fast) {
+          const int kk = w + 4 * lane;                 // this lane's chunk of the worker
+          const int kc = iss_k0 + min(kk, iss_nch - 1);  // context chunk (n_pre == 0)
+          const int bi = a.ctx.block_size == kChunk ? kc : kc * kChunk / a.ctx.block_size;
+          const int rel = bi - iss_bt0;
+          int blk = __shfl_sync(0xffffffffu, iss_bte, rel & 31);
+          if (rel < 0 || rel >= 32)
+            blk = __ldg(a.ctx.block_table + static_cast<long long>(iss_r) * a.ctx.bt_stride + bi);
+          lane_kaddr = a.ctx.k + static_cast<long long>(blk) * a.ctx.stride_block +
+                       static_cast<long long>(kc * kChunk - bi * a.ctx.block_size) * RB_HEAD_DIM +
+                       static_cast<long long>(iss_h) * a.ctx.stride_head;
+        }
       }
       if (iss_item < 0) return;
       if (ki >= iss_nch) {
@@ -976,8 +1052,22 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         have_iss = false;
         continue;
       }
-      const int k = iss_k0 + ki;
       uint8_t* dst = ring_p + iss_sl * kSlotBytes;
+      if (iss_fast) {
+        const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(__shfl_sync(
+            0xffffffffu, reinterpret_cast<unsigned long long>(lane_kaddr), ki >> 2));
+        const int n = iss_lim - (iss_k0 + ki) * kChunk;
+        if (n >= kChunk)
+          chunk_cp_async_full(dst, kb, kb + vdiff, lane);
+        else
+          chunk_cp_async(dst, kb, kb + vdiff, RB_HEAD_DIM, n, lane);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        ++issued;
+        iss_sl = (iss_sl + 1 == kDepth) ? 0 : iss_sl + 1;
+        ki += kWorkers;
+        continue;
+      }
+      const int k = iss_k0 + ki;
       const __nv_bfloat16 *kb = a.ctx.k, *vb = a.ctx.v;
       long long tok_stride = a.ctx.stride_tok;
       int n;
@@ -996,14 +1086,14 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         if (a.ctx.block_table == nullptr) {
           off = (iss_roff + t0) * a.ctx.stride_tok;
         } else if (a.ctx.block_size % kChunk == 0) {
-          const int bi = t0 / a.ctx.block_size;
+          const int bi = a.ctx.block_size == kChunk ? k - n_pre : t0 / a.ctx.block_size;
           const int v0 = __shfl_sync(0xffffffffu, iss_bte, (bi - iss_bt0) & 31);
           const int blk = (bi - iss_bt0 >= 0 && bi - iss_bt0 < 32)
                               ? v0
                               : __ldg(a.ctx.block_table +
                                       static_cast<long long>(iss_r) * a.ctx.bt_stride + bi);
           off = static_cast<long long>(blk) * a.ctx.stride_block +
-                static_cast<long long>(t0 % a.ctx.block_size) * a.ctx.stride_tok;
+                static_cast<long long>(t0 - bi * a.ctx.block_size) * a.ctx.stride_tok;
         } else {
           off = 0;
           rows_ok = false;
@@ -1013,7 +1103,12 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         vb += off;
         if (!rows_ok) chunk_cp_async_rows(dst, a.ctx, iss_r, t0, iss_h, n, lane);
       }
-      if (rows_ok) chunk_cp_async(dst, kb, vb, tok_stride, n, lane);
+      if (rows_ok) {
+        if (n == kChunk && tok_stride == RB_HEAD_DIM)
+          chunk_cp_async_full(dst, kb, vb, lane);
+        else
+          chunk_cp_async(dst, kb, vb, tok_stride, n, lane);
+      }
       asm volatile("cp.async.commit_group;" ::: "memory");
       ++issued;
       iss_sl = (iss_sl + 1 == kDepth) ? 0 : iss_sl + 1;
@@ -1030,6 +1125,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
   for (int jc = 0;; ++jc) {
     if (dts) d_t = global_timer_ns();
     mbar_wait(&i_full[qs], qph);
+    tr.ev(400000 + jc);
     if (dts) d_ifull += global_timer_ns() - d_t;
     const int item = iq[qs].item;
     const CtxItem<R> it = iq[qs].it;
@@ -1045,7 +1141,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     // lets the issue cursor read this item's slot before it is released.
     int k = w;
     for (bool first = true;; first = false) {
+      tr.ev(100000 + issued);
       try_issue(jc);
+      tr.ev(110000 + issued);
       if (first) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&i_empty[qs]);
@@ -1067,6 +1165,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       else
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();  // every lane's copies of the chunk are visible to the warp
+      tr.ev(210000 + consumed);
       const int kg = it.k0 + k;
       const bool pre = kg < n_pre;
       const int key0 = (pre ? kg : kg - n_pre) * kChunk;
@@ -1077,6 +1176,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
       (void)key0;  // diagnostics variant: the data path alone (wrong results)
 #endif
       __syncwarp();  // every lane's reads precede the refill of this slot
+      tr.ev(300000 + consumed);
       ++consumed;
       con_sl = (con_sl + 1 == kDepth) ? 0 : con_sl + 1;
       k += kWorkers;
@@ -1093,6 +1193,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     float* mml = s_ml + (mb * kWorkers + w) * R * 2;
     cmp.handoff(macc, mml, lane);
     __syncwarp();
+    tr.ev(500000 + mi);
     if (lane == 0) mbar_arrive(&m_full[mb]);
     ++mi;
   }

@@ -135,6 +135,26 @@ struct TileWalker {
   }
 };
 
+// Diagnostics build only: per-role event trace of CTA 0 (clock64, 256 events
+// per warp, 12 warps) at debug_ts + 3072 * 8 (profiles/diag_sys_trace.py).
+struct SysTrace {
+  unsigned long long* p;
+  int n;
+  __device__ __forceinline__ void init(const SysArgs& a, int warp, int lane) {
+    p = nullptr;
+    n = 0;
+    if (RB_DIAG && a.debug_ts != nullptr && blockIdx.x == 0 && lane == 0 && warp < 12)
+      p = a.debug_ts + 3072 * 8 + warp * 512;
+  }
+  __device__ __forceinline__ void ev(int code) {
+    if (RB_DIAG && p != nullptr && n < 256) {
+      p[2 * n] = clock64();
+      p[2 * n + 1] = static_cast<unsigned long long>(code);
+    }
+    ++n;
+  }
+};
+
 template <int NQ>
 __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
@@ -220,6 +240,8 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
   unsigned long long* dtx = dts ? args.debug_ts + 2048 * 8 + blockIdx.x * 8 : nullptr;
   if (dtx && threadIdx.x == 0) dtx[0] = global_timer_ns();
 
+  SysTrace tr;
+  tr.init(args, warp, lane);
   const uint32_t smem_k = smem_u32(smem + L::kOffK);
   const uint32_t smem_v = smem_u32(smem + L::kOffV);
   const uint32_t smem_q = smem_u32(smem + L::kOffQ);
@@ -236,6 +258,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       const int kt = tw.kt, h = tw.h, qt = tw.qt;
       const int st = j % KS;
       mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
+      tr.ev(100000 + j);
       if (lane == 0) {
         uint8_t* dst = smem + L::kOffK + st * L::kTileBytes;
         mbar_arrive_expect_tx(&k_full[st], L::kTileBytes);
@@ -279,6 +302,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const int kt = tw.kt, h = tw.h;
         const int st = j % VS;
         mbar_wait(&v_empty[st], ((j / VS) & 1) ^ 1);
+        tr.ev(200000 + j);
         uint8_t* dst = smem + L::kOffV + st * L::kTileBytes;
         mbar_arrive_expect_tx(&v_full[st], L::kTileBytes);
         tma_load_3d(dst, &tmap_v, &v_full[st], 0, kt * RB_KEY_TILE, h, pol);
@@ -303,8 +327,10 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         if (new_unit) mbar_wait(&q_full[qb], (uq >> 1) & 1);
         const int st = j % KS, sb = j & 1;
         mbar_wait(&k_full[st], (j / KS) & 1);
+        tr.ev(300000 + j);
         if (dtx && j == 0) dtx[3] = global_timer_ns();
         mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+        tr.ev(310000 + j);
         tc_fence_after();
         const uint32_t k_base = smem_k + st * L::kTileBytes;
         const uint32_t q_base = smem_q + qb * L::kQBytes;
@@ -340,7 +366,9 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         // O accumulates over the tiles of a unit; its first tile starts fresh
         const uint32_t acc0 = (i > t_begin && tw.kt != 0) ? 1u : 0u;
         mbar_wait(&v_full[st], (j / VS) & 1);
+        tr.ev(400000 + j);
         mbar_wait(&p_full[pb], (j >> 1) & 1);
+        tr.ev(410000 + j);
         tc_fence_after();
         const uint32_t v_base = smem_v + st * L::kTileBytes;
         const uint32_t p_base = smem_p + pb * L::kQBytes;
@@ -410,6 +438,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const uint32_t ph = (j >> 1) & 1;
         // ---- S tile -> scores (log2 domain)
         mbar_wait(&s_full[gb], ph);
+        tr.ev(500000 + j);
         if (dts && j == 0 && threadIdx.x == L::kRoleWarps * 32) dts[2] = global_timer_ns();
         tc_fence_after();
         float x[H];
@@ -432,6 +461,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         over = __any_sync(0xffffffffu, over);
         if (lane == 0) fl[qd] = over ? 1 : 0;
         named_bar_sync(bar_red, 128);
+        tr.ev(510000 + j);
         const int4 fv = *reinterpret_cast<const int4*>(fl);
         if (fv.x | fv.y | fv.z | fv.w) {
           float tmp[H];
@@ -483,7 +513,9 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
           l_part[c] += x[c];
         }
         // ---- P (bf16) -> smem, K-major SW128 [NQ rows][128 keys]
+        tr.ev(520000 + j);
         mbar_wait(&p_empty[gb], ph ^ 1);
+        tr.ev(530000 + j);
         {
           uint8_t* pdst = smem + L::kOffP + gb * L::kQBytes + pkb;
 #pragma unroll
@@ -496,6 +528,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[gb]);
+        tr.ev(540000 + j);
         if (pend_u >= 0 && (it > ia || it == ib)) {
           // publish the previous unit's part now that its stores have had a
           // tile's time to drain: the fence no longer stalls the group
