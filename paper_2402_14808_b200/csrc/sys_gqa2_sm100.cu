@@ -208,8 +208,10 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     // Order per key tile j: P_0(j).V, Q_0.K(j+1)^T, P_1(j).V, Q_1.K(j+1)^T --
     // each S_i(j+1) right behind the P.V that frees its TMEM, so the softmax
-    // of one query tile overlaps the other tile's MMAs.
-    if (lane == 0) {
+    // of one query tile overlaps the other tile's MMAs.  The whole warp runs
+    // the loop (warp-uniform descriptors, built once and offset by adding to
+    // the start-address field); one elected lane issues each MMA / commit.
+    {
       constexpr uint32_t idesc_qk = make_idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16_f32(128, 128, 0, G2_PV_KMAJOR ? 0 : 1);
       const int n = static_cast<int>(t_end - t_begin);
@@ -227,22 +229,26 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
         tc_fence_after();
         G2_EVT(8, j);
       };
+      // descriptor start-address field = byte address >> 4 (bits [0,14))
+      const uint64_t q_desc0 = make_smem_desc_sw128(smem_q, 16, 1024);
+      const uint64_t k_desc0 = make_smem_desc_sw128(smem_k, 16, 1024);
+      const uint64_t v_desc0 = G2_PV_KMAJOR ? make_smem_desc_sw128(smem_v, 16, 1024)
+                                            : make_smem_desc_sw128(smem_v, kTile / 2, 1024);
       auto issue_s = [&](int j, int sub) {
-        const uint32_t k_base = smem_k + (j % KS) * kTile;
-        const uint32_t q_base = smem_q + sub * kQBytes;
+        const uint64_t kd = k_desc0 + (((j % KS) * kTile) >> 4);
+        const uint64_t qd = q_desc0 + ((sub * kQBytes) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk & 3) * 32;
-          const uint64_t a = make_smem_desc_sw128(q_base + (kk >> 2) * (kRows * 128) + koff, 16, 1024);
-          const uint64_t b = make_smem_desc_sw128(k_base + (kk >> 2) * (kTile / 2) + koff, 16, 1024);
-          if (!G2_NO_MMA) umma_f16_ss(tmem_base + sub * 256, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * (kRows * 128) + (kk & 3) * 32) >> 4;
+          const uint32_t offk = ((kk >> 2) * (kTile / 2) + (kk & 3) * 32) >> 4;
+          if (!G2_NO_MMA) umma_f16_ss_elect(tmem_base + sub * 256, qd + off, kd + offk, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[sub]);
+        umma_commit_elect(&s_full[sub]);
       };
       auto end_k = [&](int j) {
-        umma_commit(&k_empty[j % KS]);
+        umma_commit_elect(&k_empty[j % KS]);
         if (k_last) {
-          umma_commit(q_empty);
+          umma_commit_elect(q_empty);
           ++uq;
         }
       };
@@ -258,7 +264,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
         const int st = j % VS;
         mbar_wait(&v_full[st], (j / VS) & 1);
         G2_EVT(9, j);
-        const uint32_t v_base = smem_v + st * kTile;
+        const uint64_t vd = v_desc0 + ((st * kTile) >> 4);
         for (int sub = 0; sub < kSub; ++sub) {
           mbar_wait(&p_full[sub], static_cast<uint32_t>(j & 1));
           tc_fence_after();
@@ -268,21 +274,18 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
           for (int kk = 0; kk < 8; ++kk) {
             // A = P_i (TMEM, 16 keys = 8 columns); B = V tile, MN-major: 16 keys
             // = two 8-key swizzle atoms, the two 64-wide d halves kTile / 2 apart
-            const uint64_t b =
-                G2_PV_KMAJOR
-                    ? make_smem_desc_sw128(v_base + (kk >> 2) * (kTile / 2) + (kk & 3) * 32, 16, 1024)
-                    : make_smem_desc_sw128(v_base + kk * 2048, kTile / 2, 1024);
+            const uint64_t b = vd + ((G2_PV_KMAJOR ? (kk >> 2) * (kTile / 2) + (kk & 3) * 32 : kk * 2048) >> 4);
             if (G2_PV_SS) {
               const uint64_t a = make_smem_desc_sw128(
                   smem_q + sub * kQBytes + (kk >> 2) * (kRows * 128) + (kk & 3) * 32, 16, 1024);
-              umma_f16_ss(tmem_base + sub * 256 + 128, a, b, idesc_pv, kk > 0 ? 1u : acc0);
+              umma_f16_ss_elect(tmem_base + sub * 256 + 128, a, b, idesc_pv, kk > 0 ? 1u : acc0);
             } else if (!G2_NO_MMA) {
-              umma_f16_ts(tmem_base + sub * 256 + 128, p_tmem + kk * 8, b, idesc_pv,
-                          kk > 0 ? 1u : acc0);
+              umma_f16_ts_elect(tmem_base + sub * 256 + 128, p_tmem + kk * 8, b, idesc_pv,
+                                kk > 0 ? 1u : acc0);
             }
           }
-          umma_commit(&o_full[sub]);
-          if (sub == kSub - 1) umma_commit(&v_empty[st]);
+          umma_commit_elect(&o_full[sub]);
+          if (sub == kSub - 1) umma_commit_elect(&v_empty[st]);
           if (j + 1 < n) {
             if (sub == 0) begin_k(j + 1);
             issue_s(j + 1, sub);
@@ -292,7 +295,6 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
         }
       }
     }
-    __syncwarp();
   } else {
     // ------------------------------------------- softmax / epilogue (sub)
     const int sub = (warp - kSmWarp0) >> 2;
