@@ -10,7 +10,8 @@
    __init__, errors, kernels, numerics, attention, costmodel, kvcache, model,
    _kernels_py (.py) and _kernels_cy (.pyx) -- everything attention.py and
    the toy decoder (model.py, whose `_attend` is the reference caller of the
-   relay path) import.
+   relay path) import -- plus engine and serving, whose scheduler loop drives
+   this package's B200 engine in tests/test_gpu_engine.py.
 
 Run:  python oracle/build.py          (idempotent; skips up-to-date outputs)
 """
@@ -28,7 +29,7 @@ REF_MODULES = [
     ("__init__", ".py"), ("errors", ".py"), ("kernels", ".py"),
     ("numerics", ".py"), ("attention", ".py"), ("costmodel", ".py"),
     ("_kernels_py", ".py"), ("_kernels_cy", ".pyx"), ("kvcache", ".py"),
-    ("model", ".py"),
+    ("model", ".py"), ("engine", ".py"), ("serving", ".py"),
 ]
 
 

@@ -99,6 +99,56 @@ class SystemKvCache:
         return cls([conv(k) for k in keys_shd], [conv(v) for v in values_shd], prompt_id,
                    head_dim=d)
 
+    @classmethod
+    def prefill(cls, q_layers, k_layers, v_layers, base=kernels.ROPE_BASE, prompt_id="system",
+                head_dim=HEAD_DIM, out_dtype=torch.bfloat16):
+        """GPU prefill of the shared system prompt (`prefill_system_cache`,
+        model.py:341-353, with the attention of its prompt phase,
+        model.py:314-316).  Per layer, from the model's projections of the s
+        prompt tokens -- q (s, hq, 128), k / v (s, hkv, 128) bf16 CUDA, not
+        yet rotated:
+
+        * q and k rotated to positions 0..s-1 (rope_rows, model.py:292-293;
+          fp64 angles) and the rotated K with V written straight into this
+          cache's [hkv][s][128] layout, one launch (rb_rope_append with the
+          dense cache as a single s-token block);
+        * the prefill attention -- causal over the prompt, row t sees keys
+          0..t (attention_with_lse(causal=True)) -- by the context kernel
+          reading the new cache in place (ragged mode, split-K over long
+          prompts).
+
+        Returns (cache, [(out, lse) per layer]): out (s, hq, 128) in
+        `out_dtype`, lse (s, hq) fp32 natural log."""
+        if not (len(q_layers) == len(k_layers) == len(v_layers)) or len(k_layers) == 0:
+            raise DimensionError("q / k / v need one entry per layer")
+        keys, values, outs = [], [], []
+        for q, k, v in zip(q_layers, k_layers, v_layers):
+            if q.dim() != 3 or k.dim() != 3 or k.shape != v.shape or q.shape[0] != k.shape[0]:
+                raise DimensionError(f"prefill expects q (s, hq, 128), k / v (s, hkv, 128); got "
+                                     f"{tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+            s, hkv, hq = k.shape[0], k.shape[1], q.shape[1]
+            if s < 1:
+                raise ContractError("system prompt must be non-empty")
+            if hq % hkv != 0:
+                raise DimensionError(f"hq={hq} must be a multiple of hkv={hkv}")
+            dev = k.device
+            kc = torch.empty((hkv, s, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+            vc = torch.empty_like(kc)
+            pos = torch.arange(s, dtype=torch.int64, device=dev)
+            qr = kernels.rope_append(q.to(torch.bfloat16).contiguous(), k.to(torch.bfloat16).contiguous(),
+                                     v.to(torch.bfloat16).contiguous(), pos, pos.to(torch.int32),
+                                     kc.unsqueeze(0), vc.unsqueeze(0), s, base=base)
+            out, lse = kernels.context_attention(
+                qr, torch.tensor([0, s], dtype=torch.int32, device=dev), kc, vc,
+                torch.tensor([s], dtype=torch.int32, device=dev), max_rows=s * (hq // hkv), hkv=hkv,
+                req_offset=torch.zeros(1, dtype=torch.int64, device=dev),
+                strides=(0, kc.stride(1), kc.stride(0)), causal=True, scale=head_dim ** -0.5,
+                out_fp32=out_dtype == torch.float32, max_ctx_len=s)
+            keys.append(kc)
+            values.append(vc)
+            outs.append((out if out.dtype == out_dtype else out.to(out_dtype), lse))
+        return cls(keys, values, prompt_id, head_dim=head_dim), outs
+
     # ---- the reference's on-disk format (RELAYKV, kvcache.py:19-20, 66-100):
     # magic b"RELAYKV\0", little-endian uint32 version (1), layers, s, h, d,
     # bits; then per layer the K tensor and the V tensor, (s, h, d) row-major

@@ -1,0 +1,117 @@
+"""the reference's serving loop driving the B200 engine.
+
+`paper_2402_14808_b200.engine.B200AttentionEngine` has the stepping surface
+of the reference's engines (`relayserve/engine.py:88-271`); the UNMODIFIED
+reference scheduler (`relayserve/serving.py:173-266`, compiled into
+oracle/_ref) drives it with its default cost function `wallclock_cost`
+(engine.py:83-85), which then advances the simulated clock by the measured
+device time of each step's append + attention kernels.  Checked here:
+
+* the batch job completes with the reference's bookkeeping (every request
+  to its generation cap, the batch sizes the scheduler may pick, admission
+  within the pool);
+* a prompt step and a decode step of the engine equal the float64 oracle on
+  the engine's own caches (positions, slots, block table, q_start wired
+  right), in relay and in baseline mode;
+* relay vs baseline at a long shared prompt: the relay run finishes the same
+  work in less simulated time (the paper's Fig. 7 ordering), and both runs'
+  per-step device times are recorded (RB_PARITY_LOG).
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import assert_close, log_parity
+
+pytestmark = pytest.mark.gpu
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+
+
+@pytest.fixture(scope="module")
+def serving():
+    if not os.path.isdir(os.path.join(REF, "relayserve")):
+        pytest.skip("oracle/_ref not built (python oracle/build.py)")
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import relayserve.serving as srv
+    return srv
+
+
+def _check_step_vs_oracle(oracle, eng, requests, ms, tag):
+    """The engine's last step (last layer) against the float64 oracle on the
+    engine's own caches."""
+    layer = eng.config.layers - 1
+    q = eng.last_q.float().cpu().numpy().astype(np.float64)
+    out, lse = eng.last_output
+    out = out.float().cpu().numpy()
+    lse = lse.float().cpu().numpy()
+    g = eng.config.heads // eng.config.kv_heads
+    sk = eng.sys_cache.keys[layer].float().cpu().numpy().transpose(1, 0, 2).astype(np.float64)
+    sv = eng.sys_cache.values[layer].float().cpu().numpy().transpose(1, 0, 2).astype(np.float64)
+    row = 0
+    for req, m in zip(requests, ms):
+        kr, vr = eng.ctx_cache.gather(req.id, layer)
+        kr = oracle.expand_kv(kr.float().cpu().numpy().astype(np.float64), g)
+        vr = oracle.expand_kv(vr.float().cpu().numpy().astype(np.float64), g)
+        qr = q[row:row + m][None]
+        if eng.mode == "relay":
+            ref_o, ref_l = oracle.relay_attention(qr, oracle.expand_kv(sk, g), oracle.expand_kv(sv, g),
+                                                  [kr], [vr], return_lse=True)
+        else:
+            kk = np.concatenate([oracle.expand_kv(sk, g), kr])
+            vv = np.concatenate([oracle.expand_kv(sv, g), vr])
+            res = oracle.attention_with_lse(qr, kk[None], vv[None], causal=True)
+            ref_o, ref_l = res.output, res.lse
+        assert_close(out[row:row + m], ref_o[0], f"engine {tag} {req.id}")
+        assert_close(lse[row:row + m], ref_l[0], f"engine {tag} lse {req.id}", lse=True)
+        row += m
+
+
+@pytest.mark.parametrize("mode", ["relay", "baseline"])
+def test_engine_steps_vs_oracle(serving, oracle, mode):
+    from paper_2402_14808_b200.engine import B200AttentionEngine
+    eng = B200AttentionEngine(mode, 200, 256, layers=2, heads=8, kv_heads=2, out_dtype=torch.float32,
+                              seed=3)
+    reqs = serving.synth_workload(u_len=5, gen_len=4, n=3, id_prefix=mode)
+    reqs[1].user_tokens = reqs[1].user_tokens[:2]   # ragged prompts
+    for r in reqs:
+        eng.start_request(r)
+    res = eng.prompt_step(reqs)
+    assert res.kind == "prompt" and res.wall_s > 0 and set(res.tokens) == {r.id for r in reqs}
+    _check_step_vs_oracle(oracle, eng, reqs, [r.user_len for r in reqs], f"{mode} prompt")
+    for _ in range(3):
+        res = eng.decode_step(reqs)
+    _check_step_vs_oracle(oracle, eng, reqs, [1] * len(reqs), f"{mode} decode")
+    assert [eng.ctx_cache.length(r.id) for r in reqs] == [r.user_len + 3 for r in reqs]
+    for r in reqs:
+        eng.finish_request(r)
+    assert eng.reserved_blocks == 0 and eng.free_blocks == eng.total_blocks
+
+
+@pytest.mark.parametrize("s", [512, 2048, 8192])
+def test_reference_scheduler_drives_b200_engine(serving, s):
+    """run_batch_job (serving.py:243-255) on the B200 engine, relay vs
+    baseline (same pool, 24 requests of 32 prompt + 16 generated tokens):
+    same work, relay finishes in less simulated time -- the paper's Fig. 7
+    ordering, here with measured B200 attention step times."""
+    from paper_2402_14808_b200.engine import B200AttentionEngine
+    results = {}
+    for mode in ("relay", "baseline"):
+        eng = B200AttentionEngine(mode, s, 2048, layers=4, heads=8, seed=1)
+        reqs = serving.synth_workload(u_len=32, gen_len=16, n=24, id_prefix=mode)
+        cfg = serving.SchedulerConfig()
+        m = serving.run_batch_job(reqs, mode, eng, cfg)
+        assert m.finished_requests == len(reqs)
+        assert all(r.tokens_emitted == r.max_gen for r in reqs)
+        assert set(m.batch_size_hist) <= set(cfg.allowed_batch_sizes)
+        assert eng.reserved_blocks == 0 and eng.free_blocks == eng.total_blocks
+        results[mode] = m
+        log_parity(f"engine run_batch_job {mode} s={s}", kind="engine", s=s, mode=mode,
+                   total_time_s=m.total_time_s, tokens_per_s=m.throughput_tokens_per_s,
+                   batch_hist=m.batch_size_hist)
+    assert results["relay"].total_time_s < results["baseline"].total_time_s

@@ -2,6 +2,7 @@
 head sharding, cost model, block pool (no GPU)."""
 
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -263,3 +264,25 @@ def test_costmodel_matches_reference_module(tmp_path):
     ref.emit_speedup_curves(tmp_path / "ref.csv")
     costmodel.emit_speedup_curves(tmp_path / "ours.csv")
     assert (tmp_path / "ref.csv").read_text() == (tmp_path / "ours.csv").read_text()
+
+
+def test_engine_traffic_convention_matches_reference():
+    """The B200 engine's per-step attention element count is the reference
+    engine's (relayserve/engine.py:43-53, compiled into oracle/_ref)."""
+    ref_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "relayserve")):
+        pytest.skip("oracle/_ref not built")
+    import sys
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import relayserve.engine as ref_engine
+    from paper_2402_14808_b200.engine import attention_step_elements
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        b = int(rng.integers(1, 9))
+        new = [int(x) for x in rng.integers(1, 40, b)]
+        lens = [n + int(x) for n, x in zip(new, rng.integers(0, 500, b))]
+        s, d = int(rng.integers(1, 5000)), int(rng.integers(1, 1024))
+        for mode in ("relay", "baseline"):
+            assert attention_step_elements(mode, s, new, lens, d) == \
+                ref_engine.attention_step_elements(mode, s, new, lens, d)
