@@ -439,7 +439,10 @@ struct CtxCfg {
   static constexpr int kDepth = R >= 8 ? 2 : 3;    // chunks in flight per worker
   static constexpr int kNB = R == 1 ? 3 : R == 2 ? 2 : R == 4 ? 1 : 2;  // merge buffers
 };
-constexpr int kIQ = 3;                         // item queue depth (claim-ahead bound)
+#ifndef RB_CTX_IQ
+#define RB_CTX_IQ 3
+#endif
+constexpr int kIQ = RB_CTX_IQ;                         // item queue depth (claim-ahead bound)
 constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l

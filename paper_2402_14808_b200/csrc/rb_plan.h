@@ -144,7 +144,16 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, sms);
   const double sys_bytes = (double)p.n_qt * hkv * (double)s * 512.0;
   const double ctx_bytes = (double)ctx_tokens * hkv * 512.0;
-  int g = (int)(sms * sys_bytes / (sys_bytes + RB_RELAY_RATE_RATIO * ctx_bytes) + 0.5);
+  // the context kernel streams long per-request contexts faster per SM than
+  // short ones (each (request, head) item pays a fixed latency chain): the
+  // rate ratio falls from RB_RELAY_RATE_RATIO at <= 8 chunks of 16 tokens per
+  // item to ~0.94 at >= 32 (C3, c ~ U[64, 768]: best split measured 36 CTAs
+  // vs 29 with the flat ratio, 125 -> 108 us per layer; profiles/r02)
+  const double avg_chunks = n_rows > 0 ? (double)ctx_tokens / n_rows / 16.0 : 0.0;
+  double lf = (avg_chunks - 8.0) / 24.0;
+  lf = lf < 0.0 ? 0.0 : (lf > 1.0 ? 1.0 : lf);
+  const double ratio = RB_RELAY_RATE_RATIO / (1.0 + 0.39 * lf);
+  int g = (int)(sms * sys_bytes / (sys_bytes + ratio * ctx_bytes) + 0.5);
   if (p.nq == 256 && p.n_units <= sms) {
     // the 256-row GQA kernel is tensor-bound: balance measured time, not
     // bytes -- RB_GQA2_TILE_US per key tile per CTA against the context

@@ -290,10 +290,12 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
       // Start streaming V only once this CTA's first K tile and its query
       // rows have landed: at launch every SM fires its rings at once, and the
       // first Q.K^T must not queue behind four V tiles per SM.
+#ifndef RB_SYS_V_EARLY
       if (t_begin < t_end) {
         mbar_wait(&k_full[0], 0);
         mbar_wait(&q_full[0], 0);  // Q rows must not queue behind the V burst either
       }
+#endif
       int j = 0;
       TileWalker tw;
       tw.start(P, blockIdx.x, t_begin);
