@@ -42,6 +42,16 @@ METRICS = [
     "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_selected_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
+    # tcgen05 evidence: UTCHMMA instructions (the hmma subpipe counts
+    # HMMA/UTCHMMA/UTCQMMA/UTCOMMA), tensor-memory activity, shared-memory
+    # wavefronts feeding the tensor core, and the SM clock the kernel ran at
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.sum",
+    "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum",
+    "sm__cycles_elapsed.avg.per_second",
 ]
 SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "us": 1e-6, "ns": 1e-9,
          "ms": 1e-3, "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9}
@@ -51,7 +61,9 @@ def read(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units = rows[0], rows[1]
+    # triage metrics carry a section prefix ("TPC.TriageCompute.<metric>")
+    hdr = [h.split("TriageCompute.", 1)[1] if "TriageCompute." in h else h for h in rows[0]]
+    units = rows[1]
     res = []
     for vals in rows[2:]:
         rec = {"kernel": vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else ""}
