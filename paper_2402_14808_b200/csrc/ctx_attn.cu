@@ -201,7 +201,7 @@ struct SwapCompute {
   __device__ __forceinline__ void chunk(const uint8_t* slot_p, int key0, bool pre, int /*max_lim*/,
                                         bool mask, const CtxArgs& a, int lane) {
     const uint32_t slot = smem_u32(slot_p);
-    const int g = lane >> 2, t = lane & 3, j = lane >> 3, r8 = lane & 7;
+    const int g = lane >> 2, j = lane >> 3, r8 = lane & 7;
     // ---- S^T = K Q^T: two accumulators (even / odd k-steps) for ILP
     float sa[4], sb[4];
     {
@@ -539,7 +539,9 @@ struct CtaSmem {
   static constexpr int kOffItems = (kOffML + kNB * kWorkers * R * 8 + 15) & ~15;  // [kIQ] ItemSlot
   static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
   static constexpr int kOffDefer = kOffBar + (3 * kIQ + 2 * kNB) * 8;  // [1 + kMaxDefer] int
-  static constexpr int kBytes = kOffDefer + (1 + kMaxDefer) * 4;
+  // [R][kAccStride] f32: rows of a split combine (merger only)
+  static constexpr int kOffComb = (kOffDefer + (1 + kMaxDefer) * 4 + 15) & ~15;
+  static constexpr int kBytes = kOffComb + R * kAccStride * 4;
   static_assert(kBytes <= 113 * 1024, "two context CTAs must fit one SM");
 };
 
@@ -563,21 +565,6 @@ struct WarpTrace {
     ++n;
   }
 };
-
-// Merge two unnormalised softmax states (O, m log2, l) -- the merge of
-// `relay_fusion` (attention.py:137-157) without the normalisation.
-__device__ __forceinline__ void merge_state(float4& O, float& m, float& l, float4 Ok, float mk, float lk) {
-  const float mn = fmaxf(m, mk);
-  if (mn == -INFINITY) return;
-  const float so = (m == -INFINITY) ? 0.f : fast_exp2(m - mn);
-  const float sk = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mn);
-  l = l * so + lk * sk;
-  O.x = O.x * so + Ok.x * sk;
-  O.y = O.y * so + Ok.y * sk;
-  O.z = O.z * so + Ok.z * sk;
-  O.w = O.w * so + Ok.w * sk;
-  m = mn;
-}
 
 template <int R>
 __global__ void __launch_bounds__(kCtxThreadsPC, 2)
@@ -959,20 +946,70 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           __threadfence();
-#pragma unroll 1
-          for (int i = 0; i < nrow; ++i) {
-            const long long oidx = row_oidx(i);
-            const float* src = a.split_part + oidx * nslots * kPartStride;
-            float4 O = __ldcg(reinterpret_cast<const float4*>(src + d0));
-            float2 ml = __ldcg(reinterpret_cast<const float2*>(src + 128));
-            float M = ml.x, Ls = ml.y;
-            for (int k = 1; k < it.nsplit; ++k) {
-              const float* sk = src + k * kPartStride;
-              const float4 Ok = __ldcg(reinterpret_cast<const float4*>(sk + d0));
-              const float2 mlk = __ldcg(reinterpret_cast<const float2*>(sk + 128));
-              merge_state(O, M, Ls, Ok, mlk.x, mlk.y);
+          // The R rows combine in parallel: lane group rg = lane / LPR owns
+          // row rg, lane li of the group dims [li DPL, (li + 1) DPL).  Per
+          // row: the reference max over the splits (the group's lanes take
+          // every LPR-th split), then O and l as exp2-weighted sums in split
+          // order with KB partials' loads in flight -- deterministic (fixed
+          // order and grouping) and no longer one L2 round trip per split
+          // per row (b = 2, c = 32k: ~37 splits x 4 rows).
+          {
+            constexpr int LPR = 32 / R, DPL = RB_HEAD_DIM / LPR, NV = DPL / 4;
+            constexpr int KB = R >= 8 ? 1 : 8 / R;
+            float* comb = reinterpret_cast<float*>(smem + SM::kOffComb);
+            const int rg = lane / LPR, li = lane % LPR;
+            const bool rv = rg < nrow;
+            const float* src = a.split_part + row_oidx(rv ? rg : 0) * nslots * kPartStride;
+            float mloc = -INFINITY;
+            for (int k = li; k < it.nsplit; k += LPR) mloc = fmaxf(mloc, __ldcg(src + k * kPartStride + 128));
+#pragma unroll
+            for (int off = LPR / 2; off > 0; off >>= 1)
+              mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
+            const float M = mloc;
+            float4 acc[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            float Ls = 0.f;
+            for (int k0 = 0; k0 < it.nsplit; k0 += KB) {
+              float4 Ok[KB][NV];
+              float2 mlk[KB];
+#pragma unroll
+              for (int kk = 0; kk < KB; ++kk) {
+                const float* sk = src + min(k0 + kk, it.nsplit - 1) * kPartStride;
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  Ok[kk][v] = __ldcg(reinterpret_cast<const float4*>(sk + li * DPL + 4 * v));
+                mlk[kk] = __ldcg(reinterpret_cast<const float2*>(sk + 128));
+              }
+#pragma unroll
+              for (int kk = 0; kk < KB; ++kk) {
+                if (k0 + kk >= it.nsplit) break;
+                const float w = (mlk[kk].x == -INFINITY) ? 0.f : fast_exp2(mlk[kk].x - M);
+                Ls = fmaf(mlk[kk].y, w, Ls);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                  acc[v].x = fmaf(Ok[kk][v].x, w, acc[v].x);
+                  acc[v].y = fmaf(Ok[kk][v].y, w, acc[v].y);
+                  acc[v].z = fmaf(Ok[kk][v].z, w, acc[v].z);
+                  acc[v].w = fmaf(Ok[kk][v].w, w, acc[v].w);
+                }
+              }
             }
-            finish(O, M, Ls, oidx, false, pp);
+            if (rv) {
+#pragma unroll
+              for (int v = 0; v < NV; ++v)
+                *reinterpret_cast<float4*>(comb + rg * kAccStride + li * DPL + 4 * v) = acc[v];
+              if (li == 0) {
+                comb[rg * kAccStride + 128] = M;
+                comb[rg * kAccStride + 129] = Ls;
+              }
+            }
+            __syncwarp();
+#pragma unroll 1
+            for (int i = 0; i < nrow; ++i) {
+              const float4 O = *reinterpret_cast<const float4*>(comb + i * kAccStride + d0);
+              finish(O, comb[i * kAccStride + 128], comb[i * kAccStride + 129], row_oidx(i), false, pp);
+            }
           }
           __syncwarp();
           if (lane == 0) a.split_cnt[it.grp] = 0;  // rearm for the next launch

@@ -3,7 +3,7 @@ scheduler claims / publications, worker issue / data-ready / compute / item
 start / handoff, merger waits.  Prints each warp's events with the time since
 the CTA's first event.
 
-    python profiles/diag_ctx_trace.py [s] [phases] [cta]
+    python profiles/diag_ctx_trace.py [s] [phases] [cta] [b hq hkv c]
 """
 import os
 import sys
@@ -25,9 +25,9 @@ def main():
     s = int(sys.argv[1]) if len(sys.argv) > 1 else 512
     phases = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     cta = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-    b, h, c = 32, 52, 128
+    b, h, hkv, c = (int(x) for x in sys.argv[4:8]) if len(sys.argv) > 7 else (32, 52, 52, 128)
     dev = torch.device("cuda", 0)
-    q, sc, paged, bt, cl = bench.build_workload(torch, b, h, h, s, [c] * b, list(range(h)), dev)
+    q, sc, paged, bt, cl = bench.build_workload(torch, b, h, hkv, s, [c] * b, list(range(hkv)), dev)
     flush = bench.make_flush(torch, dev)
     step = RelayDecodeStep(sc, paged, bt, cl, h)
     ts = torch.zeros((8192, 8), dtype=torch.int64, device=dev)
@@ -59,7 +59,7 @@ def main():
                 continue
             line.append(f"{(clk - t0) / GHZ / 1e3:5.2f}:{NAMES.get(code // 10000, '?')}{code % 10000}")
         print(f"--- CTA {cta} {role} ({len(line)} events)")
-        for i in range(0, len(line), 8):
+        for i in range(0, min(len(line), int(os.environ.get("MAXEV", "96"))), 8):
             print("   " + "  ".join(line[i:i + 8]))
 
 

@@ -56,7 +56,8 @@ def run(s, phases=3, b=32, h=52, c=128, hkv=None):
         e0.record()
         kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=h // hkv, hkv=hkv, sys_layout="hsd",
                                 block_table=bt, block_size=16, strides=pst, grid=grid,
-                                phases=phases)
+                                phases=phases,
+                                max_ctx_len=c if os.environ.get("DIAG_SPLIT") else 0)
         e1.record()
         torch.cuda.synchronize()
     _lib.load_diag().rb_debug_set_timestamps(None)
