@@ -150,14 +150,9 @@ int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, i
  * System-kernel CTA count for rb_relay_attention's grid_cap: the two kernels
  * run concurrently, the system kernel on a share of the SMs proportional to
  * its HBM bytes (ctx_tokens = total context tokens of the batch), the
- * context kernel on the rest and on every SM the system kernel releases.
- * 0 selects the unified step for a decode batch (one row per request, GQA
- * group dividing 8) whose shared prefix is short next to its contexts: no
- * system kernel; the context kernel takes the prefix as items of 8 query
- * rows (several requests) x a range of 16-key chunks, claimed with the
- * context items, and every (request, head) combines its system and context
- * partials in a fixed slot order.  rb_relay_workspace_bytes and
- * rb_relay_attention accept grid_cap = 0 for that mode (phase 1 is a no-op).
+ * context kernel on the rest and on every SM the system kernel releases
+ * (the share follows the two kernels' measured per-SM streaming rates and
+ * the context length per request).  Always >= 1.
  */
 int rb_relay_sys_grid(int n_rows, int hq, int hkv, int s, long long ctx_tokens, int sm_count,
                       int* grid);
