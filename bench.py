@@ -441,10 +441,12 @@ def run_b200(args):
         return res
 
     def e2e_stats(q, relay, bt):
-        """Public-API decode step with host buffers: one H2D of this step's
-        q / new-token k / v from pinned memory, paged append, relay step, D2H
-        of the output -- all inside the events (RelayDecodeStep.host_step_graph,
-        a CUDA graph of exactly that; `step_host` is the eager equivalent)."""
+        """Public-API decode step with host buffers: this step's q / new-token
+        k / v cross from pinned memory, are appended and attended, and the
+        output crosses back -- all inside the events (RelayDecodeStep.
+        host_step_graph: one CUDA graph of the zero-copy step, whose kernels
+        read the inputs from / write the output to pinned host memory;
+        `step_host` is the eager copy-based equivalent)."""
         nh = q.shape[1]
         g = torch.Generator().manual_seed(99)
         qkv_h = torch.randn((3, B, nh, D), generator=g).to(torch.bfloat16).pin_memory()
@@ -615,9 +617,12 @@ def run_b200(args):
                      "algorithmic_bytes_per_launch": step_bytes_local},
         "e2e": {"value": e2e_ms * 1e3, "unit": "µs/step", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],
-                "path": "RelayDecodeStep.host_step_graph (CUDA graph): pinned H2D of [q|k_new|v_new] "
-                        "-> rb_kv_append -> rb_relay_attention (system || context, fused in-kernel) -> D2H out",
-                "eager_us": e2e_eager_ms * 1e3, "launches_per_step": 3},
+                "path": "RelayDecodeStep.host_step_graph (CUDA graph, zero-copy): rb_relay_attention "
+                        "reads q and the new tokens' K/V from the pinned host buffer, appends K/V "
+                        "inside the context kernel, runs system || context with the fusion in-kernel "
+                        "and writes the output rows into pinned host memory",
+                "eager_us": e2e_eager_ms * 1e3, "eager_path": "step_host: H2D copies, rb_kv_append, "
+                "the relay step, D2H copy", "launches_per_step": 2},
         "gpu_launches": 2 * args.steps,
         "relay_vs_naive_max_abs": head["relay_vs_naive_max_abs"],
         "sys_plan": head["plan"],

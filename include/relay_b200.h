@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 2
+#define RB_ABI_VERSION 3
 
 enum {
   RB_OK = 0,
@@ -138,6 +138,12 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * header holds the context kernel's work counters), so one buffer serves
  * every step on a stream.  max_ctx_len: an upper bound of ctx_lens (e.g. the
  * block table's width x block_size) for the context split-K.
+ * k_new, v_new, slot_mapping (all NULL, or all set; paged layout only): the
+ * fused append -- the step's new tokens' K / V rows, [n_rows][hkv][128] bf16
+ * in q's row order (device or pinned host memory), are written into the
+ * paged pool at slot_mapping[row] (as rb_kv_append would) by the context
+ * item that streams them, before its workers read them; ctx_lens already
+ * count the new tokens.  One launch pair then covers append + attention.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
  * (2 | 4: the context kernel of a step whose system kernel was launched by an
  * earlier phase-1 call, e.g. with stream work in between; the units are
@@ -164,7 +170,8 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        const long long* req_offset, long long stride_block, long long stride_tok,
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
                        void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
-                       size_t workspace_bytes, int phases, void* stream);
+                       size_t workspace_bytes, int phases, const void* k_new, const void* v_new,
+                       const int* slot_mapping, void* stream);
 
 /*
  * Standalone relay fusion (attention.py:137-157) over n_vec vectors of d

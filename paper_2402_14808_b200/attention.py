@@ -435,7 +435,7 @@ class RelayDecodeStep:
         # next full step must start from rearmed counters
         self._system_pending = False
 
-    def _launch(self, q, phases):
+    def _launch(self, q, phases, out=None, k_new=None, v_new=None, slot_mapping=None):
         if q.dim() != 3 or tuple(q.shape) != (self.b, self.hq, HEAD_DIM):
             raise DimensionError(f"q must be ({self.b}, {self.hq}, {HEAD_DIM}), got {tuple(q.shape)}")
         if self._system_pending and phases & 1:
@@ -446,8 +446,9 @@ class RelayDecodeStep:
             self.paged.k_pool[self.layer], self.paged.v_pool[self.layer], self.ctx_lens,
             max_rows=self.hq // self.hkv, hkv=self.hkv, sys_layout="hsd",
             block_table=self.block_table, block_size=self.paged.block_size,
-            strides=self.paged.strides(), grid=self.grid, out=self.out, lse_out=self.lse,
-            ws=self.ws, phases=phases, scale=self.scale, max_ctx_len=self.max_ctx_len)
+            strides=self.paged.strides(), grid=self.grid, out=self.out if out is None else out,
+            lse_out=self.lse, ws=self.ws, phases=phases, scale=self.scale,
+            max_ctx_len=self.max_ctx_len, k_new=k_new, v_new=v_new, slot_mapping=slot_mapping)
 
     def system(self, q):
         """Only the system kernel of the step (profiling)."""
@@ -458,8 +459,12 @@ class RelayDecodeStep:
         partials of the last `system` call)."""
         return self._launch(q, 2)
 
-    def __call__(self, q):
-        return self._launch(q, 3)
+    def __call__(self, q, k_new=None, v_new=None, slot_mapping=None):
+        """The relay step.  With k_new / v_new (b, hkv, 128) and slot_mapping
+        (int32, b): the new tokens' K / V are appended to the paged cache at
+        those slots inside the same launch (the context kernel writes them
+        before reading them; ctx_lens must already count them)."""
+        return self._launch(q, 3, k_new=k_new, v_new=v_new, slot_mapping=slot_mapping)
 
     def step_host(self, q_host, k_new_host, v_new_host, slot_mapping, out_host):
         """End-to-end decode step from host buffers (pinned for async copies):
@@ -479,20 +484,36 @@ class RelayDecodeStep:
         out_host.copy_(out, non_blocking=True)
         return out_host
 
-    def host_step_graph(self, qkv_host, slot_mapping, out_host):
+    def host_step_graph(self, qkv_host, slot_mapping, out_host, zero_copy=True):
         """CUDA-graph version of `step_host` for a serving loop.
 
         qkv_host: pinned bf16 (3, b, h, 128) holding this step's q, k_new,
         v_new; out_host: pinned bf16 (b, hq, 128).  Returns a callable that
-        replays the step on the current stream: one H2D of the inputs, the
-        paged append of the new tokens, the relay step, the D2H of the output.
-        Refill `qkv_host` between calls.
+        replays the step on the current stream: the host -> device transfer
+        of the inputs, the paged append of the new tokens, the relay step and
+        the device -> host transfer of the output.  Refill `qkv_host` between
+        calls.
+
+        zero_copy (default): no staging copies and no separate append -- the
+        two attention kernels read the queries, and the context kernel the
+        new K / V (which it appends to the pool before streaming them),
+        straight from the pinned host buffer over the host link (UVA); its
+        fused epilogue writes the output rows straight into `out_host`.  The
+        bytes crossing the link are the same as with copies.  False: one H2D
+        copy, the append kernel, the step, one D2H copy (`step_host`'s order).
         """
         dev = self.out.device
         qkv_dev = torch.empty(qkv_host.shape, dtype=torch.bfloat16, device=dev)
         main = torch.cuda.current_stream(dev)
 
         def body():
+            if zero_copy:
+                # one launch pair: queries and new K / V read from the pinned
+                # buffer, the append fused into the context kernel, the
+                # output written into out_host
+                self._launch(qkv_host[0], 3, out=out_host, k_new=qkv_host[1], v_new=qkv_host[2],
+                             slot_mapping=slot_mapping)
+                return
             # one H2D of [q|k_new|v_new], the paged append, then the relay step
             # (system + context kernels run concurrently; the append is the
             # system kernel's PDL primary, so its prologue overlaps it)

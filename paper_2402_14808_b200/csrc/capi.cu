@@ -305,6 +305,8 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = nullptr;  // static item order
+  a.k_new = a.v_new = nullptr;
+  a.slot_mapping = nullptr;
   int st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, workspace, workspace_bytes);
   if (st != RB_OK) return st;
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
@@ -356,8 +358,15 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        const long long* req_offset, long long stride_block, long long stride_tok,
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
                        void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
-                       size_t workspace_bytes, int phases, void* stream) {
+                       size_t workspace_bytes, int phases, const void* k_new, const void* v_new,
+                       const int* slot_mapping, void* stream) {
   if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
+  if ((k_new == nullptr) != (v_new == nullptr) || (k_new != nullptr) != (slot_mapping != nullptr))
+    return fail(RB_ERR_CONTRACT, "k_new, v_new and slot_mapping go together");
+  if (k_new != nullptr && block_table == nullptr)
+    return fail(RB_ERR_CONTRACT, "the fused append needs the paged layout (block_table)");
+  if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15)
+    return fail(RB_ERR_CONTRACT, "k_new / v_new rows must be 16-byte aligned");
   size_t need = 0;
   const int sms = device_sms();
   int st = rb_relay_workspace_bytes(n_rows, hq, hkv, s, grid_cap, b, max_rows, max_ctx_len, sms,
@@ -435,6 +444,9 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.scale_log2 = scale * rb::kLog2e;
   a.debug_ts = g_debug_ts ? g_debug_ts + kCtxTsOffset : nullptr;
   a.sched = header;  // workspace header: dynamic item counters
+  a.k_new = static_cast<const __nv_bfloat16*>(k_new);
+  a.v_new = static_cast<const __nv_bfloat16*>(v_new);
+  a.slot_mapping = slot_mapping;
   {
     // (the context split-K plan covers the context chunks only)
     const size_t split_off = 256 + cnt + cpart + ml + ((acc_b + 255) & ~(size_t)255);

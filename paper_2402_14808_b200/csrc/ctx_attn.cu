@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
     reinterpret_cast<int*>(smem + SM::kOffDefer)[0] = 0;
     for (int i = 0; i < kIQ; ++i) {
       mbar_init(&i_meta[i], 1);
-      mbar_init(&i_full[i], 1);
+      mbar_init(&i_full[i], 32);   // every scheduler lane: cp.async arrive (query rows)
       mbar_init(&i_empty[i], kWorkers + 1);  // workers + merger
     }
     for (int i = 0; i < kNB; ++i) {
@@ -677,8 +677,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         if (lane == 0) {
           slot.item = -1;
           mbar_arrive(&i_meta[qs]);
-          mbar_arrive(&i_full[qs]);
         }
+        __syncwarp();
+        mbar_arrive(&i_full[qs]);
         break;
       }
       CtxItem<R> it;
@@ -724,19 +725,43 @@ __global__ void __launch_bounds__(kCtxThreadsPC, 2)
         slot.item = item;
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&i_meta[qs]);
-        mbar_arrive_expect_tx(&i_full[qs], nvalid * kRowBytes);
+      if (a.k_new != nullptr && it.n_chunks > 0 && it.m_r > 0) {
+        // fused append: the item whose chunk range covers the request's new
+        // tokens (context positions c_r - m_r .. c_r - 1) writes their K / V
+        // rows of head h into the pool first; the i_meta arrive below
+        // releases the stores to the CTA's workers (items of other row tiles
+        // covering the same tokens write identical bytes)
+        const int first_new = n_pre + (it.c_r - it.m_r) / kChunk;
+        const int last_new = n_pre + (it.c_r - 1) / kChunk;
+        if (it.k0 <= last_new && first_new < it.k0 + it.n_chunks) {
+          for (int e = lane; e < it.m_r * 32; e += 32) {
+            const int row = it.row0 + (e >> 5), c16 = e & 15;
+            const bool is_v = (e & 16) != 0;
+            const long long src = (static_cast<long long>(row) * a.hkv + it.h) * RB_HEAD_DIM + c16 * 8;
+            const uint4 val = *reinterpret_cast<const uint4*>((is_v ? a.v_new : a.k_new) + src);
+            const int slot = __ldg(a.slot_mapping + row);
+            const int bs = a.ctx.block_size;
+            const long long dst = static_cast<long long>(slot / bs) * a.ctx.stride_block +
+                                  static_cast<long long>(slot % bs) * a.ctx.stride_tok +
+                                  static_cast<long long>(it.h) * a.ctx.stride_head + c16 * 8;
+            *reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(is_v ? a.ctx.v : a.ctx.k) + dst) = val;
+          }
+          __syncwarp();
+        }
       }
+      if (lane == 0) mbar_arrive(&i_meta[qs]);
       __syncwarp();
-      // query rows of the item: one 256-byte bulk copy per row
-      if (lane < nvalid) {
-        const int li = rbase + lane;
+      // query rows of the item: 16-byte cp.async by all lanes (the LSU path
+      // also reads queries straight from pinned host memory, the zero-copy
+      // e2e step), then every lane arrives on i_full once its copies land
+      for (int c = lane; c < nvalid * 16; c += 32) {
+        const int li = rbase + (c >> 4);
         const int t = li / a.g, jj = li % a.g;
         const __nv_bfloat16* qp = a.q + static_cast<long long>(it.row0 + t) * a.q_row_stride +
-                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride;
-        bulk_copy_g2s(smem + SM::kOffQ + (qs * R + lane) * kRowBytes, qp, kRowBytes, &i_full[qs]);
+                                  static_cast<long long>(it.h * a.g + jj) * a.q_head_stride + (c & 15) * 8;
+        cp_async_16(smem + SM::kOffQ + (qs * R + (c >> 4)) * kRowBytes + (c & 15) * 16, qp, 16u);
       }
+      cp_async_mbar_arrive(&i_full[qs]);
       cur = nxt;
       id1 = id2;
       id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;

@@ -70,6 +70,13 @@ struct CtxArgs {
   int split_chunks, n_split;
   float* split_part;             // [n_rows * hq][n_split][132] f32 partials (O, m log2, l)
   int* split_cnt;                // [b * hkv * n_z] zeroed counters, rearmed by the last split
+  // optional fused append (relay step): the step's new tokens' K / V rows,
+  // [n_rows][hkv][128] in q's row order (device or pinned host memory), are
+  // written into the paged pool at slot_mapping[row] by the context item
+  // that streams them, before its workers read them.  Null: no append.
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  const int* slot_mapping;
 };
 
 #ifdef __CUDACC__

@@ -55,9 +55,14 @@ def workspace(nbytes: int, device, stream_key: int, kind: str = "sys", layout=No
     return ent[0]
 
 
-def _check_bf16(name, t):
-    if t.dtype != torch.bfloat16 or not t.is_cuda:
-        raise ContractError(f"{name}: expected a CUDA bfloat16 tensor, got {t.dtype} on {t.device}")
+def _check_bf16(name, t, host_ok=False):
+    """bf16 with a contiguous head dim, on the GPU -- or, where `host_ok`
+    (the step's inputs / output of the zero-copy e2e path), in pinned host
+    memory, which the kernels address directly (UVA)."""
+    on_dev = t.is_cuda or (host_ok and t.device.type == "cpu" and t.is_pinned())
+    if t.dtype != torch.bfloat16 or not on_dev:
+        where = "CUDA or pinned host" if host_ok else "CUDA"
+        raise ContractError(f"{name}: expected a {where} bfloat16 tensor, got {t.dtype} on {t.device}")
     if t.stride(-1) != 1:
         raise ContractError(f"{name}: head_dim must be the contiguous dimension")
 
@@ -184,28 +189,45 @@ def context_attention(q, q_start, k, v, ctx_lens, *, max_rows, hkv,
 def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
                     sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
                     strides=None, scale=None, grid=None, out=None, lse_out=None,
-                    out_fp32=False, ws=None, phases=3, max_ctx_len=0):
+                    out_fp32=False, ws=None, phases=3, max_ctx_len=0, k_new=None, v_new=None,
+                    slot_mapping=None):
     """The fused relay step (rb_relay_attention): system kernel (stream-K
     partials, no merge) + context kernel whose epilogue merges the system
     partials with the context state.  Returns (out, lse).  max_ctx_len: an
     upper bound of ctx_lens (0: unknown) for the context split-K; `ws` must
-    then hold rb_relay_workspace_bytes(..., max_ctx_len, sm_count) bytes."""
-    _check_bf16("q", q)
+    then hold rb_relay_workspace_bytes(..., max_ctx_len, sm_count) bytes.
+    k_new / v_new (n_rows, hkv, 128) bf16 + slot_mapping int32 (n_rows,):
+    the fused append of the step's new tokens (paged layout; the tensors may
+    be pinned host memory); ctx_lens must already count them."""
+    # q (and out) may live in pinned host memory (zero-copy e2e step); the
+    # caches, indices and workspace are on the device
+    _check_bf16("q", q, host_ok=True)
     for name, t in (("sys_k", sys_k), ("sys_v", sys_v), ("k", k), ("v", v)):
         _check_bf16(name, t)
-        if t.device != q.device:
-            raise ContractError(f"{name} is on {t.device}, q on {q.device}")
-    _check_index("q_start", q_start, q.device)
-    _check_index("ctx_lens", ctx_lens, q.device)
+        if t.device != sys_k.device:
+            raise ContractError(f"{name} is on {t.device}, sys_k on {sys_k.device}")
+    _check_index("q_start", q_start, sys_k.device)
+    _check_index("ctx_lens", ctx_lens, sys_k.device)
     for name, t in (("block_table", block_table), ("req_offset", req_offset)):
         if t is not None:
-            _check_index(name, t, q.device)
+            _check_index(name, t, sys_k.device)
     n_rows, hq, d = q.shape
     if d != HEAD_DIM:
         raise DimensionError(f"head_dim must be {HEAD_DIM}, got {d}")
     if q_start.numel() != ctx_lens.numel() + 1:
         raise DimensionError(f"q_start needs b + 1 = {ctx_lens.numel() + 1} offsets, "
                              f"got {q_start.numel()}")
+    if (k_new is None) != (v_new is None) or (k_new is None) != (slot_mapping is None):
+        raise ContractError("k_new, v_new and slot_mapping go together")
+    if k_new is not None:
+        for name, t in (("k_new", k_new), ("v_new", v_new)):
+            _check_bf16(name, t, host_ok=True)
+            if not t.is_contiguous() or tuple(t.shape) != (q.shape[0], hkv, HEAD_DIM):
+                raise DimensionError(f"{name} must be contiguous ({q.shape[0]}, {hkv}, {HEAD_DIM})")
+        _check_index("slot_mapping", slot_mapping, sys_k.device)
+    for name, t in (("out", out), ("lse_out", lse_out)):
+        if t is not None and not (t.is_cuda or (t.device.type == "cpu" and t.is_pinned())):
+            raise ContractError(f"{name}: expected a CUDA or pinned host tensor")
     if sys_k.shape != sys_v.shape or k.shape != v.shape:
         raise DimensionError("K and V shapes differ")
     if sys_layout == "hsd":
@@ -214,7 +236,7 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
     else:
         s, _, _ = sys_k.shape
         s_tok, s_head = sys_k.stride(0), sys_k.stride(1)
-    dev = q.device
+    dev = sys_k.device
     b = ctx_lens.numel()
     if out is None:
         out = torch.empty((n_rows, hq, HEAD_DIM),
@@ -237,7 +259,8 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
         v.data_ptr(), _ptr(block_table), bt_stride, block_size, _ptr(req_offset), sb, stok, sh,
         ctx_lens.data_ptr(), float(scale), grid, out.data_ptr(),
         1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), int(max_ctx_len),
-        ws.data_ptr(), ws.numel(), phases, stream), "rb_relay_attention")
+        ws.data_ptr(), ws.numel(), phases, _ptr(k_new), _ptr(v_new), _ptr(slot_mapping), stream),
+        "rb_relay_attention")
     return out, lse_out
 
 
@@ -257,13 +280,15 @@ def relay_fusion_fp32(o_sys, lse_sys, o_ctx, lse_ctx, out=None, lse_out=None):
 
 
 def kv_append(k_new, v_new, slot_mapping, k_pool, v_pool, block_size):
-    """Scatter (n_tok, hkv, 128) new rows into a [num_blocks][hkv][bs][128] pool."""
-    _check_bf16("k_new", k_new)
+    """Scatter (n_tok, hkv, 128) new rows into a [num_blocks][hkv][bs][128] pool.
+    k_new / v_new may be pinned host tensors (read directly by the kernel)."""
+    _check_bf16("k_new", k_new, host_ok=True)
+    _check_bf16("v_new", v_new, host_ok=True)
     n_tok, hkv, d = k_new.shape
     _lib.check(_lib.load().rb_kv_append(
         k_new.data_ptr(), v_new.data_ptr(), slot_mapping.data_ptr(), n_tok, k_pool.data_ptr(),
         v_pool.data_ptr(), hkv, d, block_size, k_pool.stride(0), k_pool.stride(2),
-        k_pool.stride(1), _stream(k_new.device)), "rb_kv_append")
+        k_pool.stride(1), _stream(k_pool.device)), "rb_kv_append")
 
 
 ROPE_BASE = 10000.0  # numerics.ROPE_BASE / model.py:292

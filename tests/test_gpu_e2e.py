@@ -41,13 +41,56 @@ def test_host_step_equals_device_step(oracle, b, hq, hkv, s, lens):
     torch.cuda.synchronize()
     assert torch.equal(out_e, ref.cpu()), "step_host differs from the device path"
     out_g = torch.zeros((b, hq, 128), dtype=torch.bfloat16).pin_memory()
-    # host_step_graph takes one (3, b, h, 128) buffer: h = hq = hkv only
+    # host_step_graph takes one (3, b, h, 128) buffer: h = hq = hkv only;
+    # both the zero-copy graph (kernels read / write pinned host memory) and
+    # the staged-copy graph
     if hq == hkv:
         qkv_eq = torch.stack([qkv_h[0], k_new, v_new]).pin_memory()
-        replay = step.host_step_graph(qkv_eq, slots, out_g)
-        replay()
-        torch.cuda.synchronize()
-        assert torch.equal(out_g, ref.cpu()), "host_step_graph differs from the device path"
+        for zc in (True, False):
+            out_g.zero_()
+            replay = step.host_step_graph(qkv_eq, slots, out_g, zero_copy=zc)
+            replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out_g, ref.cpu()), f"host_step_graph(zero_copy={zc}) differs"
     pairs = [(r, h) for r in range(b) for h in sorted({0, hkv - 1})]
     check_sampled_pairs(oracle, out_e.cuda().float(), step.lse, qkv_h[0].cuda(), sys_cache, paged, 0,
                         pairs, hq // hkv, f"e2e host step b={b} g={hq // hkv}")
+
+
+@pytest.mark.parametrize("hq,hkv,bs", [(8, 8, 16), (16, 4, 32), (8, 2, 8)])
+def test_fused_append_equals_separate_append(oracle, hq, hkv, bs):
+    """rb_relay_attention with k_new / v_new / slot_mapping (the append fused
+    into the context kernel) == rb_kv_append followed by the step, bitwise,
+    with the new tokens landing at their slots; new K / V read from device
+    memory and from pinned host memory."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    lens = [20, 1, 47, 16, 33]
+    b = len(lens)
+    q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, 300, lens, seed=hq + bs, block_size=bs)
+    btc = bt.cpu()
+    slots = torch.tensor([int(btc[r, (c - 1) // bs]) * bs + (c - 1) % bs for r, c in enumerate(lens)],
+                         dtype=torch.int32, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    k_new = torch.randn((b, hkv, 128), generator=g, device="cuda").to(torch.bfloat16)
+    v_new = torch.randn((b, hkv, 128), generator=g, device="cuda").to(torch.bfloat16)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq, out_dtype=torch.float32)
+    paged.append_slots(0, k_new, v_new, slots)
+    ref = [t.clone() for t in step(q)]
+    kpool, vpool = paged.k_pool.clone(), paged.v_pool.clone()
+    for src in ("device", "host"):
+        paged.k_pool.normal_()   # poison: the fused path must write the new rows itself
+        paged.v_pool.copy_(vpool)
+        paged.k_pool.copy_(kpool)
+        for r, c in enumerate(lens):     # clear the new tokens' slots
+            blk, off = int(btc[r, (c - 1) // bs]), (c - 1) % bs
+            paged.k_pool[0, blk, :, off] = 0
+            paged.v_pool[0, blk, :, off] = 0
+        kn = k_new if src == "device" else k_new.cpu().pin_memory()
+        vn = v_new if src == "device" else v_new.cpu().pin_memory()
+        got = step(q, k_new=kn, v_new=vn, slot_mapping=slots)
+        torch.cuda.synchronize()
+        assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1]), f"fused append ({src})"
+        assert torch.equal(paged.k_pool, kpool) and torch.equal(paged.v_pool, vpool), f"pool ({src})"
+    pairs = [(r, h) for r in range(b) for h in sorted({0, hkv - 1})]
+    check_sampled_pairs(oracle, ref[0], ref[1], q, sys_cache, paged, 0, pairs, hq // hkv,
+                        f"fused append hq={hq} hkv={hkv} bs={bs}")
