@@ -435,8 +435,14 @@ constexpr int kWorkers = 4;
 // merge buffers (their items are long, the merger keeps up with one or two)
 // and R = 8 a 2-deep ring.
 template <int R>
+#ifndef RB_CTX_MINB
+#define RB_CTX_MINB 2   /* resident CTAs per SM the register budget is sized for */
+#endif
+#ifndef RB_CTX_DEPTH1
+#define RB_CTX_DEPTH1 3
+#endif
 struct CtxCfg {
-  static constexpr int kDepth = R >= 8 ? 2 : 3;    // chunks in flight per worker
+  static constexpr int kDepth = R >= 8 ? 2 : (R == 1 ? RB_CTX_DEPTH1 : 3);    // chunks in flight per worker
   static constexpr int kNB = R == 1 ? 3 : R == 2 ? 2 : R == 4 ? 1 : 2;  // merge buffers
 };
 #ifndef RB_CTX_IQ
@@ -567,7 +573,7 @@ struct WarpTrace {
 };
 
 template <int R>
-__global__ void __launch_bounds__(kCtxThreadsPC, 2)
+__global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
   using SM = CtaSmem<R>;
   constexpr int kDepth = SM::kDepth, kNB = SM::kNB;
