@@ -277,6 +277,111 @@ struct SwapCompute {
       }
     }
   }
+  // Two chunks (32 keys) in one pass: the four Q.K^T chains are
+  // independent, the column max / lazy-rescale vote runs once over 32 keys,
+  // and the P.V MMAs of both chunks accumulate back to back -- the latency
+  // chain of one chunk now covers two (the per-chunk math was ~35% of a
+  // worker's per-item time at C2, profiles/diag_ctx_trace.py).
+  __device__ __forceinline__ void chunk2(const uint8_t* slot_a, const uint8_t* slot_b, int key0a,
+                                         int key0b, bool pre_a, bool pre_b, bool mask_a, bool mask_b,
+                                         const CtxArgs& a, int lane) {
+    const uint32_t sla = smem_u32(slot_a), slb = smem_u32(slot_b);
+    const int g = lane >> 2, j = lane >> 3, r8 = lane & 7;
+    float sa0[4], sa1[4], sb0[4], sb1[4];
+    {
+      const int key = r8 + 8 * (j & 1);
+      const uint32_t ka_addr = sla + key * kRowBytes, kb_addr = slb + key * kRowBytes;
+      uint32_t ka[4], kb[4];
+      ldsm_x4(ka, ka_addr + (((0 + (j >> 1)) ^ (key & 7)) << 4));
+      ldsm_x4(kb, kb_addr + (((0 + (j >> 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816_zero(sa0, ka, qb[0][0], qb[0][1]);
+      mma_bf16_16816_zero(sb0, kb, qb[0][0], qb[0][1]);
+      ldsm_x4(ka, ka_addr + (((2 + (j >> 1)) ^ (key & 7)) << 4));
+      ldsm_x4(kb, kb_addr + (((2 + (j >> 1)) ^ (key & 7)) << 4));
+      mma_bf16_16816_zero(sa1, ka, qb[1][0], qb[1][1]);
+      mma_bf16_16816_zero(sb1, kb, qb[1][0], qb[1][1]);
+#pragma unroll
+      for (int ks = 2; ks < 8; ks += 2) {
+        ldsm_x4(ka, ka_addr + (((2 * ks + (j >> 1)) ^ (key & 7)) << 4));
+        ldsm_x4(kb, kb_addr + (((2 * ks + (j >> 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(sa0, ka, qb[ks][0], qb[ks][1]);
+        mma_bf16_16816(sb0, kb, qb[ks][0], qb[ks][1]);
+        ldsm_x4(ka, ka_addr + (((2 * ks + 2 + (j >> 1)) ^ (key & 7)) << 4));
+        ldsm_x4(kb, kb_addr + (((2 * ks + 2 + (j >> 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(sa1, ka, qb[ks + 1][0], qb[ks + 1][1]);
+        mma_bf16_16816(sb1, kb, qb[ks + 1][0], qb[ks + 1][1]);
+      }
+    }
+    float s[8];  // [0..3]: chunk a (keys g, g+8; columns 2t, 2t+1), [4..7]: chunk b
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s[e] = (sa0[e] + sa1[e]) * a.scale_log2;
+      s[4 + e] = (sb0[e] + sb1[e]) * a.scale_log2;
+    }
+    if (mask_a) {
+      const int b0 = pre_a ? a.s_prefix : lim0, b1 = pre_a ? a.s_prefix : lim1;
+      if (key0a + g >= b0) s[0] = -INFINITY;
+      if (key0a + g >= b1) s[1] = -INFINITY;
+      if (key0a + g + 8 >= b0) s[2] = -INFINITY;
+      if (key0a + g + 8 >= b1) s[3] = -INFINITY;
+    }
+    if (mask_b) {
+      const int b0 = pre_b ? a.s_prefix : lim0, b1 = pre_b ? a.s_prefix : lim1;
+      if (key0b + g >= b0) s[4] = -INFINITY;
+      if (key0b + g >= b1) s[5] = -INFINITY;
+      if (key0b + g + 8 >= b0) s[6] = -INFINITY;
+      if (key0b + g + 8 >= b1) s[7] = -INFINITY;
+    }
+    float cm[2] = {fmaxf(fmaxf(s[0], s[2]), fmaxf(s[4], s[6])), fmaxf(fmaxf(s[1], s[3]), fmaxf(s[5], s[7]))};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 4));
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 8));
+      cm[c] = fmaxf(cm[c], __shfl_xor_sync(0xffffffffu, cm[c], 16));
+    }
+    const bool up0 = cm[0] > m0 + kCtxTau, up1 = cm[1] > m1 + kCtxTau;
+    if (__any_sync(0xffffffffu, up0 || up1)) {
+      const float al0 = up0 ? ((m0 == -INFINITY) ? 0.f : fast_exp2(m0 - cm[0])) : 1.f;
+      const float al1 = up1 ? ((m1 == -INFINITY) ? 0.f : fast_exp2(m1 - cm[1])) : 1.f;
+      if (up0) m0 = cm[0];
+      if (up1) m1 = cm[1];
+      l0 *= al0;
+      l1 *= al1;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= al0;
+        o[mt][1] *= al1;
+        o[mt][2] *= al0;
+        o[mt][3] *= al1;
+      }
+    }
+    const float r0 = (m0 == -INFINITY) ? 0.f : m0, r1 = (m1 == -INFINITY) ? 0.f : m1;
+    float p[8];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      p[e] = fast_exp2(s[e] - r0);
+      p[e + 1] = fast_exp2(s[e + 1] - r1);
+    }
+    const uint32_t pa0 = movmatrix_trans(pack_bf16x2(p[0], p[1]));
+    const uint32_t pa1 = movmatrix_trans(pack_bf16x2(p[2], p[3]));
+    const uint32_t pb0 = movmatrix_trans(pack_bf16x2(p[4], p[5]));
+    const uint32_t pb1 = movmatrix_trans(pack_bf16x2(p[6], p[7]));
+    l0 += (p[0] + p[2]) + (p[4] + p[6]);
+    l1 += (p[1] + p[3]) + (p[5] + p[7]);
+    {
+      const int key = r8 + 8 * (j >> 1);
+      const uint32_t va_addr = sla + kChunk * kRowBytes + key * kRowBytes;
+      const uint32_t vb_addr = slb + kChunk * kRowBytes + key * kRowBytes;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t va[4], vb[4];
+        ldsm_x4_trans(va, va_addr + (((2 * mt + (j & 1)) ^ (key & 7)) << 4));
+        ldsm_x4_trans(vb, vb_addr + (((2 * mt + (j & 1)) ^ (key & 7)) << 4));
+        mma_bf16_16816(o[mt], va, pa0, pa1);
+        mma_bf16_16816(o[mt], vb, pb0, pb1);
+      }
+    }
+  }
   // reduce the row sums over the key lanes, then write rows < R of this
   // worker's state: macc [R][kAccStride] (unnormalised O), mml [R][2]
   __device__ __forceinline__ void handoff(float* macc, float* mml, int lane) {
@@ -435,6 +540,9 @@ constexpr int kWorkers = 4;
 // merge buffers (their items are long, the merger keeps up with one or two)
 // and R = 8 a 2-deep ring.
 template <int R>
+#ifndef RB_CTX_PAIRS
+#define RB_CTX_PAIRS 0   /* 1: a worker's two next chunks in one softmax pass (SwapCompute::chunk2); measured neutral */
+#endif
 #ifndef RB_CTX_MINB
 #define RB_CTX_MINB 2   /* resident CTAs per SM the register budget is sized for */
 #endif
@@ -1226,6 +1334,30 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         cmp.init();
       }
       if (k >= it.n_chunks) break;
+#if RB_CTX_PAIRS
+      if (k + kWorkers < it.n_chunks && issued - consumed >= 2) {
+        // two of this worker's chunks (rings slots con_sl, con_sl + 1) in one pass
+        const int newer2 = issued - consumed - 2;
+        if (kDepth >= 3 && newer2 >= 1)
+          asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        const int kga = it.k0 + k, kgb = kga + kWorkers;
+        const bool pa = kga < n_pre, pb = kgb < n_pre;
+        const int k0a = (pa ? kga : kga - n_pre) * kChunk, k0b = (pb ? kgb : kgb - n_pre) * kChunk;
+        const bool ma = k0a + kChunk > (pa ? a.s_prefix : ctx_nomask);
+        const bool mbk = k0b + kChunk > (pb ? a.s_prefix : ctx_nomask);
+        const int sl2 = (con_sl + 1 == kDepth) ? 0 : con_sl + 1;
+        cmp.chunk2(ring_p + con_sl * kSlotBytes, ring_p + sl2 * kSlotBytes, k0a, k0b, pa, pb, ma, mbk,
+                   a, lane);
+        __syncwarp();
+        consumed += 2;
+        con_sl = (sl2 + 1 == kDepth) ? 0 : sl2 + 1;
+        k += 2 * kWorkers;
+        continue;
+      }
+#endif
       // chunk `consumed` is this warp's commit group number `consumed`; the
       // groups committed after it may stay in flight
       const int newer = issued - consumed - 1;
