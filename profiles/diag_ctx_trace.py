@@ -31,15 +31,19 @@ def main():
     flush = bench.make_flush(torch, dev)
     step = RelayDecodeStep(sc, paged, bt, cl, h)
     ts = torch.zeros((8192, 8), dtype=torch.int64, device=dev)
+    # RB_LIB: a diagnostics variant (built with -DRB_DIAG=1) runs the kernels
+    # and takes the timestamp buffer itself
+    diag = _lib.load_diag() if not os.environ.get("RB_LIB") else _lib.load()
+    diag.rb_debug_set_timestamps.argtypes = [__import__("ctypes").c_void_p]
     for it in range(4):
         if phases == 2:
             step.system(q)
         flush()
         ts.zero_()
-        _lib.load_diag().rb_debug_set_timestamps(ts.data_ptr() if it == 3 else None)
+        diag.rb_debug_set_timestamps(ts.data_ptr() if it == 3 else None)
         step._launch(q, phases)
         torch.cuda.synchronize()
-    _lib.load_diag().rb_debug_set_timestamps(None)
+    diag.rb_debug_set_timestamps(None)
     t = ts.cpu().reshape(-1)
     base = 7168 * 8 + cta * 6 * 512
     evs = []
