@@ -415,17 +415,11 @@ class RelayDecodeStep:
             # concurrent split: system CTAs by their share of the step's HBM bytes
             grid = _lib.relay_sys_grid(self.b, hq, self.hkv, sys_cache.system_len,
                                        int(ctx_lens.sum().item()), kernels.sm_count(dev))
-        if grid < 1:
-            raise ContractError(f"grid must be >= 1 system CTAs, got {grid}")
-        self.grid = grid
-        self.plan, _ = _lib.sys_plan(self.b, hq, self.hkv, sys_cache.system_len, self.grid)
         # the block table's capacity bounds every context it can address, so
         # the split-K plan stays valid while the contexts grow into it
         self.max_ctx_len = block_table.shape[1] * paged_cache.block_size
-        need = _lib.relay_workspace_bytes(self.b, hq, self.hkv, sys_cache.system_len, self.grid,
-                                          self.b, hq // self.hkv, self.max_ctx_len,
-                                          kernels.sm_count(dev))
-        self.ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=dev)
+        self.ws = None
+        self._set_grid(grid)
         self.out = torch.empty((self.b, hq, HEAD_DIM), dtype=out_dtype, device=dev) if out is None else out
         self.lse = torch.empty((self.b, hq), dtype=torch.float32, device=dev) if lse is None else lse
         if tuple(self.out.shape) != (self.b, hq, HEAD_DIM) or tuple(self.lse.shape) != (self.b, hq):
@@ -434,6 +428,37 @@ class RelayDecodeStep:
         # a system-only launch (profiling) leaves its units published; the
         # next full step must start from rearmed counters
         self._system_pending = False
+
+    def _set_grid(self, grid):
+        from . import _lib
+        if grid < 1:
+            raise ContractError(f"grid must be >= 1 system CTAs, got {grid}")
+        dev = self.block_table.device
+        self.grid = grid
+        self.plan, _ = _lib.sys_plan(self.b, self.hq, self.hkv, self.sys_cache.system_len, grid)
+        need = max(256, _lib.relay_workspace_bytes(self.b, self.hq, self.hkv,
+                                                   self.sys_cache.system_len, grid, self.b,
+                                                   self.hq // self.hkv, self.max_ctx_len,
+                                                   kernels.sm_count(dev)))
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+        else:
+            self.ws.zero_()   # the counters / partial layout follow the plan
+        self._system_pending = False
+
+    def resplit(self, ctx_tokens):
+        """Recompute the SM split of the two kernels for the batch's current
+        total context length (the split set at construction goes stale as a
+        serving loop's contexts grow; the host knows the lengths, so no
+        device read is needed).  Returns True when the split changed (a CUDA
+        graph captured before must then be re-captured)."""
+        from . import _lib
+        grid = _lib.relay_sys_grid(self.b, self.hq, self.hkv, self.sys_cache.system_len,
+                                   int(ctx_tokens), kernels.sm_count(self.block_table.device))
+        if grid == self.grid:
+            return False
+        self._set_grid(grid)
+        return True
 
     def _launch(self, q, phases, out=None, k_new=None, v_new=None, slot_mapping=None):
         if q.dim() != 3 or tuple(q.shape) != (self.b, self.hq, HEAD_DIM):

@@ -94,3 +94,25 @@ def test_fused_append_equals_separate_append(oracle, hq, hkv, bs):
     pairs = [(r, h) for r in range(b) for h in sorted({0, hkv - 1})]
     check_sampled_pairs(oracle, ref[0], ref[1], q, sys_cache, paged, 0, pairs, hq // hkv,
                         f"fused append hq={hq} hkv={hkv} bs={bs}")
+
+
+def test_resplit_follows_growing_contexts(oracle):
+    """RelayDecodeStep.resplit: the SM split recomputed for the batch's
+    current context length (a serving loop's contexts grow); the step stays
+    correct under the new split."""
+    from paper_2402_14808_b200 import _lib, kernels
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    lens = [64] * 16
+    q, sys_cache, paged, bt, cl = synth_paged_problem(16, 8, 8, 4096, lens, seed=9)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, 8, out_dtype=torch.float32)
+    g0 = step.grid
+    big = 16 * 60000   # as if the contexts had grown to 60k tokens each
+    changed = step.resplit(big)
+    assert changed == (step.grid != g0)
+    assert step.grid == _lib.relay_sys_grid(16, 8, 8, 4096, big, kernels.sm_count())
+    assert step.grid < g0          # longer contexts: fewer system CTAs
+    assert not step.resplit(big)   # unchanged split: nothing to do
+    out, lse = step(q)
+    torch.cuda.synchronize()
+    check_sampled_pairs(oracle, out, lse, q, sys_cache, paged, 0, [(r, 0) for r in range(16)], 1,
+                        "relay step after resplit")
