@@ -397,6 +397,28 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return f2_from(r);
 }
 
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(r);
+}
+// 2^a for a pair on the FMA pipe instead of MUFU (a <= 127; clamped at
+// -126 so the exponent field never wraps: masked scores give ~1e-38, not 0): a = j + f with j = rint(a) from the 1.5 * 2^23 rounding constant,
+// f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (relative error 7.5e-5,
+// coefficients fitted to the relative error), 2^j added to the exponent bits.
+__device__ __forceinline__ float2 exp2_poly2(float2 a) {
+  a.x = fmaxf(a.x, -126.f);
+  a.y = fmaxf(a.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(a, magic);
+  const float2 f = fsub2(a, fsub2(t, magic));
+  float2 p = ffma2(f, make_float2(0.0551716611f, 0.0551716611f), make_float2(0.242611155f, 0.242611155f));
+  p = ffma2(p, f, make_float2(0.693260968f, 0.693260968f));
+  p = ffma2(p, f, make_float2(0.999928057f, 0.999928057f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

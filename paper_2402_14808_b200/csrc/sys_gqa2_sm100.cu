@@ -60,6 +60,14 @@ constexpr int KS = G2_KS, VS = G2_VS;
 #ifndef G2_PV_SS
 #define G2_PV_SS 0
 #endif
+// G2_POLY=n > 0: one score pair in every n takes exp2 on the FMA pipe
+// (exp2_poly2) instead of MUFU.EX2 (0: all on MUFU).  Measured per-tile
+// period (C4 shape, CTA 0): n=0 3364 cycles, 2: 3432, 3: 3053, 4: 2989,
+// 6: 3095, 8: 3056 -- one in four relieves the MUFU without loading the FMA
+// pipe past it
+#ifndef G2_POLY
+#define G2_POLY 4
+#endif
 constexpr int kQBytes = kRows * 256;       // one query tile: [2 kblocks][128 rows][128 B]
 constexpr int kOffK = 0;
 constexpr int kOffV = kOffK + KS * kTile;
@@ -336,6 +344,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
           for (int e = 0; e < 32; ++e) x[c * 32 + e] = v[e];
         }
         tmem_wait_ld();
+        if (r == 0) G2_EVT(10 + 4 * sub, j);
         const int valid = min(RB_KEY_TILE, P.s - kt * RB_KEY_TILE);
         if (valid < RB_KEY_TILE) {
           // the prefix's last, partial tile only: masked keys get p = 0
@@ -350,6 +359,8 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
           for (int e = 0; e < 4; ++e) m4[e] = fmaxf(m4[e], x[c + e]);
         }
         const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * args.scale_log2;
+        if (RB_DIAG && evt) asm volatile("" ::"f"(mx));
+        if (r == 0) G2_EVT(11 + 4 * sub, j);
         const bool move = mx > m_run + kTau;
         const float m_new = move ? mx : m_run;
         const float al = (!move || m_run == -INFINITY) ? (move ? 0.f : 1.f) : fast_exp2(m_run - m_new);
@@ -365,7 +376,15 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const float2 a2 = ffma2(make_float2(x[c * 32 + e], x[c * 32 + e + 1]), sl2, nmu2);
-            const float p0 = fast_exp2(a2.x), p1 = fast_exp2(a2.y);
+            float p0, p1;
+            if (G2_POLY > 0 && (e >> 1) % (G2_POLY > 0 ? G2_POLY : 1) == G2_POLY - 1) {
+              const float2 pp = exp2_poly2(a2);
+              p0 = pp.x;
+              p1 = pp.y;
+            } else {
+              p0 = fast_exp2(a2.x);
+              p1 = fast_exp2(a2.y);
+            }
             if (e & 2)
               l2b = fadd2(l2b, make_float2(p0, p1));
             else
@@ -374,6 +393,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
           }
           tmem_st16_u32(s_addr + c * 16, pk);
         }
+        if (r == 0) G2_EVT(12 + 4 * sub, j);
         l_run = l_run * al + (l2a.x + l2a.y) + (l2b.x + l2b.y);
         m_run = m_new;
         if (__any_sync(0xffffffffu, move) && t > 0) {
@@ -392,6 +412,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
           }
         }
         tmem_wait_st();
+        if (r == 0) G2_EVT(13 + 4 * sub, j);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sub]);

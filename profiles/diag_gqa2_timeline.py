@@ -32,7 +32,7 @@ def main():
         kernels.system_attention(q, k, v, kv_layout="hsd")
         torch.cuda.synchronize()
     lib.rb_debug_set_timestamps(None)
-    t = ts[6144 * 8:6144 * 8 + 1280].view(10, 128).cpu()
+    t = ts[6144 * 8:6144 * 8 + 18 * 128].view(18, 128).cpu()
     t0 = int(t[t != 0].min())
     print("tile " + " ".join(f"{n:>13s}" for n in NAMES))
     for j in range(0, int(os.environ.get("ROWS", "14"))):
@@ -48,6 +48,22 @@ def main():
     x = [int(t[0, j + 1]) - int(t[1, j]) for j in range(8, 100) if t[0, j + 1] and t[1, j]]
     if x:
         print(f"wg0 P done -> next S ready median {statistics.median(x)}")
+    # softmax phases of warp 0 of each warpgroup (diagnostics events 10-17)
+    for sub in range(2):
+        marks = [2 * sub, 10 + 4 * sub, 11 + 4 * sub, 12 + 4 * sub, 13 + 4 * sub, 2 * sub + 1]
+        names = ["S.ld", "max", "exp+st", "wait.st", "arrive"]
+        parts = []
+        for a, bb, n in zip(marks, marks[1:], names):
+            x = [int(t[bb, j]) - int(t[a, j]) for j in range(8, 100) if t[a, j] and t[bb, j]]
+            if x:
+                parts.append(f"{n} {statistics.median(x):.0f}")
+        print(f"wg{sub} softmax phases (cycles): " + ", ".join(parts))
+    x = [int(t[6, j]) - int(t[3, j]) for j in range(8, 100) if t[6, j] and t[3, j]]
+    if x:
+        print(f"wg1 warp0 P done -> MMA sees P1 median {statistics.median(x)}")
+    x = [int(t[4, j]) - int(t[1, j]) for j in range(8, 100) if t[4, j] and t[1, j]]
+    if x:
+        print(f"wg0 warp0 P done -> MMA sees P0 median {statistics.median(x)}")
 
 
 if __name__ == "__main__":

@@ -1,7 +1,7 @@
 // Microbenchmark: tcgen05.mma issue rate of a CTA pair (cta_group::2,
 // M = 256 across the two SMs of a cluster) against the single-CTA M = 128
-// instruction (profiles/microbench_umma.cu: ~87 cycles per N <= 128 MMA when
-// issued warp-wide with elect.sync, i.e. above the 64-cycle floor).  One
+// instruction, and the single-CTA rate for N = 32 / 64 / 128 / 256 issued
+// warp-wide with elect.sync.  One
 // cluster of 2 CTAs per SM pair, the leader's elected lane issues `iters`
 // K = 16 MMAs back to back, then commits; cycles per MMA and per-SM MAC rate.
 //
@@ -160,6 +160,8 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d_out;
   cudaMalloc(&d_out, 256 * sizeof(unsigned long long));
+  run<32, false>(sms, d_out);
+  run<64, false>(sms, d_out);
   run<128, false>(sms, d_out);
   run<256, false>(sms, d_out);
   run<64, true>(sms, d_out);
