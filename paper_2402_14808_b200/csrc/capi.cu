@@ -26,8 +26,8 @@
 #include "rb_args.cuh"
 
 namespace rb {
-cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
-                                    cudaStream_t);
+cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                                    const SysArgs&, cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
 int ctx_resident_ctas(int sms);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
@@ -150,6 +150,34 @@ static int make_kv_map(CUtensorMap* map, const void* base, int s, int hkv, long 
   return RB_OK;
 }
 
+// Query tiles of the 256-row GQA kernel by TMA: [n_rows][hq][128] bf16 as a 3-D
+// map (d, head, row) with a (64, g, 128 / g) box = one 128-row K-major SW128
+// half tile of KV head h.  Only for q in device memory (TMA does not read
+// pinned host memory -- the zero-copy step keeps the cp.async loader) and g
+// dividing 128; otherwise a.q_tma stays 0.
+static void maybe_q_map(CUtensorMap* map, rb::SysArgs* a, const void* q, int n_rows, int hq,
+                        int hkv) {
+  a->q_tma = 0;
+  std::memset(map, 0, sizeof(*map));
+  const int g = hq / hkv;
+  if (a->plan.nq != 256 || 128 % g != 0) return;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, q) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return;
+  }
+  auto enc = get_encode();
+  if (!enc) return;
+  cuuint64_t dims[3] = {RB_HEAD_DIM, (cuuint64_t)hq, (cuuint64_t)n_rows};
+  cuuint64_t strides[2] = {(cuuint64_t)(a->q_head_stride * 2), (cuuint64_t)(a->q_row_stride * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+    a->q_tma = 1;
+}
+
 // ------------------------------------------------------ system attention
 int rb_system_attention(const void* q, long long q_row_stride, long long q_head_stride,
                         int n_rows, int hq, int hkv, int d, const void* sys_k, const void* sys_v,
@@ -185,12 +213,13 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
   a.part_acc = reinterpret_cast<float*>(ws + cnt + ml);
   a.debug_ts = g_debug_ts;
   a.defer_merge = 0;
-  CUtensorMap tk, tv;
+  CUtensorMap tk, tv, tq;
   st = make_kv_map(&tk, sys_k, s, hkv, kv_stride_tok, kv_stride_head);
   if (st != RB_OK) return st;
   st = make_kv_map(&tv, sys_v, s, hkv, kv_stride_tok, kv_stride_head);
   if (st != RB_OK) return st;
-  return cuda_status(rb::launch_system_attention(tk, tv, a, static_cast<cudaStream_t>(stream)),
+  maybe_q_map(&tq, &a, q, n_rows, hq, hkv);
+  return cuda_status(rb::launch_system_attention(tk, tv, tq, a, static_cast<cudaStream_t>(stream)),
                      "system attention launch");
 }
 
@@ -398,13 +427,14 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   sa.part_acc = reinterpret_cast<float*>(ws + 256 + cnt + cpart + ml);
   sa.debug_ts = g_debug_ts;
   sa.defer_merge = 1;
-  CUtensorMap tk, tv;
+  CUtensorMap tk, tv, tq;
   st = make_kv_map(&tk, sys_k, s, hkv, sys_stride_tok, sys_stride_head);
   if (st != RB_OK) return st;
   st = make_kv_map(&tv, sys_v, s, hkv, sys_stride_tok, sys_stride_head);
   if (st != RB_OK) return st;
+  maybe_q_map(&tq, &sa, q, n_rows, hq, hkv);
   if (phases & 1) {
-    st = cuda_status(rb::launch_system_attention(tk, tv, sa, cs), "system attention launch");
+    st = cuda_status(rb::launch_system_attention(tk, tv, tq, sa, cs), "system attention launch");
     if (st != RB_OK) return st;
   }
   if (b < 1 || !(phases & 2)) return RB_OK;

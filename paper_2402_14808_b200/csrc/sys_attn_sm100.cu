@@ -732,16 +732,16 @@ static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, cons
 
 cudaError_t launch_system_attention_gqa(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
                                         cudaStream_t);
-cudaError_t launch_system_attention_gqa2(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
-                                         cudaStream_t);
+cudaError_t launch_system_attention_gqa2(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                                         const SysArgs&, cudaStream_t);
 
 cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
-                                    const SysArgs& a, cudaStream_t stream) {
+                                    const CUtensorMap& tq, const SysArgs& a, cudaStream_t stream) {
   switch (a.plan.nq) {
     case 16: return launch_sys<16>(tk, tv, a, stream);
     case 32: return launch_sys<32>(tk, tv, a, stream);
     case 128: return launch_system_attention_gqa(tk, tv, a, stream);
-    case 256: return launch_system_attention_gqa2(tk, tv, a, stream);
+    case 256: return launch_system_attention_gqa2(tk, tv, tq, a, stream);
     default: return cudaErrorInvalidValue;
   }
 }

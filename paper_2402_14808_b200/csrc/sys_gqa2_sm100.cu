@@ -68,6 +68,10 @@ constexpr int KS = G2_KS, VS = G2_VS;
 #ifndef G2_POLY
 #define G2_POLY 4
 #endif
+// G2_NO_QTMA=1 (diagnostics variant): query tiles always by the cp.async loader
+#ifndef G2_NO_QTMA
+#define G2_NO_QTMA 0
+#endif
 constexpr int kQBytes = kRows * 256;       // one query tile: [2 kblocks][128 rows][128 B]
 constexpr int kOffK = 0;
 constexpr int kOffV = kOffK + KS * kTile;
@@ -100,7 +104,8 @@ struct Walk {
 
 __global__ void __launch_bounds__(g2::kThreads, 1)
     sys_gqa2_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
-                          const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
+                          const __grid_constant__ CUtensorMap tmap_v,
+                          const __grid_constant__ CUtensorMap tmap_q, const SysArgs args) {
   using namespace g2;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -126,7 +131,9 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
   unsigned long long* evt =
       (RB_DIAG && args.debug_ts && blockIdx.x == 0) ? args.debug_ts + 6144 * 8 : nullptr;
   // per-CTA %globaltimer stamps (same slots as the other system kernels):
-  // [0] entry, [1] smid, [2] first S ready (WG0), [7] exit
+  // [0] entry, [1] smid, [2] first S ready (WG0), [3] last unit's epilogue
+  // start, [4] its part / row written, [5] its merge done (merging CTA), [6]
+  // first unit's query rows in smem, [7] exit
   unsigned long long* dts = (RB_DIAG && args.debug_ts) ? args.debug_ts + blockIdx.x * 8 : nullptr;
   if (dts && threadIdx.x == 0) {
     dts[0] = global_timer_ns();
@@ -145,6 +152,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
     if ((smem_u32(smem) & 1023) != 0) __trap();
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
+    if (args.q_tma) tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -204,11 +212,28 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
       const int h = u / P.n_qt, qt = u % P.n_qt;
       mbar_wait(q_empty, (uq & 1) ^ 1);
       uint8_t* qdst = smem + kOffQ;
-      load_unit_q<kRows, kUnitRows>(qdst, args, h, qt * kUnitRows, lane);
-      cp_async_wait_all();
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
+      if (args.q_tma && !G2_NO_QTMA) {
+        // 4 boxes of (64 d, g heads, 128 / g requests): rows f = request * g
+        // + member in the K-major SW128 order the MMA reads; rows past
+        // rows_per_head are requests past n_rows, zero-filled by the TMA
+        if (lane == 0) {
+          mbar_arrive_expect_tx(q_full, kSub * kQBytes);
+#pragma unroll
+          for (int sb = 0; sb < kSub; ++sb)
+#pragma unroll
+            for (int kb = 0; kb < 2; ++kb)
+              tma_load_3d(qdst + sb * kQBytes + kb * (kRows * 128), &tmap_q, q_full, kb * 64, h * P.g,
+                          (qt * kUnitRows + sb * kRows) / P.g, l2_policy_evict_first());
+        }
+        __syncwarp();
+      } else {
+        load_unit_q<kRows, kUnitRows>(qdst, args, h, qt * kUnitRows, lane);
+        cp_async_wait_all();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(q_full);
+      }
+      if (dts && lane == 0 && uq == 0) dts[6] = global_timer_ns();
       ++uq;
       i = P.rr ? (i / P.tpu + 1) * P.tpu : min(t_end, (i / P.tpu + 1) * P.tpu);
     }
@@ -422,6 +447,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
       const int jl = j - 1;
       mbar_wait(&o_full[sub], static_cast<uint32_t>(jl & 1));
       tc_fence_after();
+      if (dts && r == 0 && sub == 0) dts[3] = global_timer_ns();
       const int h = u / P.n_qt, qt = u % P.n_qt;
       const int f = qt * kUnitRows + ur;
       const bool row_ok = f < P.rows_per_head;
@@ -457,6 +483,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
       } else if (row_ok) {
         args.lse_sys[o_idx] = (m_run + __log2f(l_run)) * kLn2;
       }
+      if (dts && r == 0 && sub == 0) dts[4] = global_timer_ns();
       if (args.defer_merge) {
         if (args.counters != nullptr) {
           named_bar_sync(bar_id, bar_n);  // every row's part written
@@ -517,6 +544,7 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
             }
           }
           if (row_ok) args.lse_sys[o_idx] = (M + __log2f(Ls)) * kLn2;
+          if (dts && r == 0 && sub == 0) dts[5] = global_timer_ns();
         }
         named_bar_sync(bar_id, bar_n);  // misc[2] reads done before the next unit
       }
@@ -534,13 +562,14 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
 }
 
 cudaError_t launch_system_attention_gqa2(const CUtensorMap& tk, const CUtensorMap& tv,
-                                         const SysArgs& a, cudaStream_t stream) {
+                                         const CUtensorMap& tq, const SysArgs& a,
+                                         cudaStream_t stream) {
   static_assert(g2::kBytes <= 232448, "GQA2 system kernel shared memory over the 227 KB limit");
   cudaError_t e = cudaFuncSetAttribute(sys_gqa2_sm100_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, g2::kBytes);
   if (e != cudaSuccess) return e;
   e = launch_pdl(sys_gqa2_sm100_kernel, dim3(a.plan.grid), dim3(g2::kThreads), g2::kBytes, stream,
-                 tk, tv, a);
+                 tk, tv, tq, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
