@@ -28,6 +28,7 @@
 namespace rb {
 cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                                     const SysArgs&, cudaStream_t);
+cudaError_t launch_sys_merge_parts(const SysArgs&, cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
 int ctx_resident_ctas(int sms);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
@@ -212,15 +213,21 @@ int rb_system_attention(const void* q, long long q_row_stride, long long q_head_
   a.part_ml = reinterpret_cast<float*>(ws + cnt);
   a.part_acc = reinterpret_cast<float*>(ws + cnt + ml);
   a.debug_ts = g_debug_ts;
-  a.defer_merge = 0;
+  // split units: every part to its slot, then one merge launch over all
+  // (unit, row) pairs (the in-kernel last-CTA merge serialised a unit's rows
+  // on one SM: 60-90 us at C4 shapes)
+  a.defer_merge = a.plan.max_parts > 1 ? 1 : 0;
+  a.counters = nullptr;
   CUtensorMap tk, tv, tq;
   st = make_kv_map(&tk, sys_k, s, hkv, kv_stride_tok, kv_stride_head);
   if (st != RB_OK) return st;
   st = make_kv_map(&tv, sys_v, s, hkv, kv_stride_tok, kv_stride_head);
   if (st != RB_OK) return st;
   maybe_q_map(&tq, &a, q, n_rows, hq, hkv);
-  return cuda_status(rb::launch_system_attention(tk, tv, tq, a, static_cast<cudaStream_t>(stream)),
-                     "system attention launch");
+  cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  st = cuda_status(rb::launch_system_attention(tk, tv, tq, a, cs), "system attention launch");
+  if (st != RB_OK || !a.defer_merge) return st;
+  return cuda_status(rb::launch_sys_merge_parts(a, cs), "system part merge launch");
 }
 
 // ----------------------------------------------------- context attention

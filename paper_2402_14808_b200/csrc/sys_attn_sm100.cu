@@ -735,6 +735,77 @@ cudaError_t launch_system_attention_gqa(const CUtensorMap&, const CUtensorMap&, 
 cudaError_t launch_system_attention_gqa2(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                                          const SysArgs&, cudaStream_t);
 
+// Standalone system attention with split units: every CTA wrote its part of
+// a unit (defer_merge); one warp per (unit, row) merges the unit's parts in
+// slot order -- max of the parts' m, weights exp2(m_k - M), O and l as
+// weighted sums in slot order (deterministic) -- normalises and writes o_sys
+// / lse_sys.  Spread over the whole GPU instead of one CTA per unit.
+__global__ void __launch_bounds__(256) sys_merge_parts_kernel(const SysArgs args) {
+  const rb_sys_plan& P = args.plan;
+  const int lane = threadIdx.x & 31;
+  const long long pr = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  pdl_wait_primary();
+  if (pr >= static_cast<long long>(P.n_units) * P.nq) return;
+  const int u = static_cast<int>(pr / P.nq), ur = static_cast<int>(pr % P.nq);
+  const int h = u / P.n_qt, qt = u % P.n_qt;
+  const int f = qt * P.nq + ur;
+  if (f >= P.rows_per_head) return;
+  const long long o_idx = static_cast<long long>(f / P.g) * P.hq + h * P.g + f % P.g;
+  const int np = rb_unit_parts(&P, u);
+  const long long base = static_cast<long long>(u) * P.max_parts;
+  float M = -INFINITY;
+  for (int k = lane; k < np; k += 32) M = fmaxf(M, __ldcg(args.part_ml + (base + k) * 2 * P.nq + ur));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+  float L = 0.f;
+  for (int k0 = 0; k0 < np; k0 += 32) {
+    // lane j holds part k0 + j's weight and l; the O rows stream 8 at a time
+    float wj = 0.f, lj = 0.f;
+    if (k0 + lane < np) {
+      const float* ml = args.part_ml + (base + k0 + lane) * 2 * P.nq;
+      const float mk = __ldcg(ml + ur);
+      lj = __ldcg(ml + P.nq + ur);
+      wj = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
+    }
+    const int nk = min(32, np - k0);
+    for (int kb = 0; kb < nk; kb += 8) {
+      float4 a8[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = k0 + min(kb + kk, nk - 1);
+        a8[kk] = __ldcg(reinterpret_cast<const float4*>(args.part_acc + ((base + k) * P.nq + ur) * RB_HEAD_DIM) + lane);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const float w = __shfl_sync(0xffffffffu, wj, min(kb + kk, 31));
+        const float l = __shfl_sync(0xffffffffu, lj, min(kb + kk, 31));
+        if (kb + kk < nk) {
+          L = fmaf(l, w, L);
+          O.x = fmaf(a8[kk].x, w, O.x);
+          O.y = fmaf(a8[kk].y, w, O.y);
+          O.z = fmaf(a8[kk].z, w, O.z);
+          O.w = fmaf(a8[kk].w, w, O.w);
+        }
+      }
+    }
+  }
+  const float inv = 1.f / L;
+  reinterpret_cast<float4*>(args.o_sys + o_idx * RB_HEAD_DIM)[lane] =
+      make_float4(O.x * inv, O.y * inv, O.z * inv, O.w * inv);
+  if (lane == 0) args.lse_sys[o_idx] = (M + __log2f(L)) * kLn2;
+}
+
+cudaError_t launch_sys_merge_parts(const SysArgs& a, cudaStream_t stream) {
+  const long long pairs = static_cast<long long>(a.plan.n_units) * a.plan.nq;
+  const long long blocks = (pairs + 7) / 8;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  cudaError_t e = launch_pdl(sys_merge_parts_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0,
+                             stream, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
                                     const CUtensorMap& tq, const SysArgs& a, cudaStream_t stream) {
   switch (a.plan.nq) {
