@@ -608,81 +608,9 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
                 args.lse_sys[o_idx] = (m_run[c] + __log2f(lrow[c])) * kLn2;
             }
           }
-        } else {
-          const int slot = blockIdx.x - owner0;
-          const long long pbase = static_cast<long long>(u) * P.max_parts + slot;
-          float* pacc = args.part_acc + pbase * NQ * RB_HEAD_DIM;
-          float* pml = args.part_ml + pbase * 2 * NQ;
-#pragma unroll
-          for (int c = 0; c < H; ++c) {
-            const int col = col0 + c;
-            pacc[col * RB_HEAD_DIM + dcol] = acc[c];
-            if (qd == 0 && lane == 0) {
-              pml[col] = m_run[c];
-              pml[NQ + col] = lrow[c];
-            }
-          }
-          named_bar_sync(bar_grp, L::NCW * 32);
-          if (cw == 0 && lane == 0) {
-            __threadfence();
-            const int prev = atomicAdd(&args.counters[u], 1);
-            const int last = (prev == nparts - 1);
-            if (last) atomicExch(&args.counters[u], 0);
-            misc[2] = last;
-          }
-          named_bar_sync(bar_grp, L::NCW * 32);
-          if (misc[2]) {
-            // last CTA of unit u: merge the slots in slot order (deterministic
-            // whoever merges); per slot all H columns' loads are in flight.
-            __threadfence();
-            const float* uacc =
-                args.part_acc + static_cast<long long>(u) * P.max_parts * NQ * RB_HEAD_DIM;
-            const float* uml = args.part_ml + static_cast<long long>(u) * P.max_parts * 2 * NQ;
-            // running merge state reuses m_run / lrow / acc (own slot is re-read
-            // from global like every other slot)
-            float* M = m_run;
-            float* Ls = lrow;
-            float* Os = acc;
-#pragma unroll
-            for (int c = 0; c < H; ++c) {
-              M[c] = -INFINITY;
-              Ls[c] = 0.f;
-              Os[c] = 0.f;
-            }
-            for (int k = 0; k < nparts; ++k) {
-#pragma unroll
-              for (int c0 = 0; c0 < H; c0 += 8) {
-                float mk[8], lk[8], ak[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                  mk[c] = __ldcg(uml + k * 2 * NQ + col0 + c0 + c);
-                  lk[c] = __ldcg(uml + k * 2 * NQ + NQ + col0 + c0 + c);
-                  ak[c] = __ldcg(uacc + (static_cast<long long>(k) * NQ + col0 + c0 + c) *
-                                            RB_HEAD_DIM + dcol);
-                }
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                  const float mn = fmaxf(M[c0 + c], mk[c]);
-                  const float so = (M[c0 + c] == -INFINITY) ? 0.f : fast_exp2(M[c0 + c] - mn);
-                  const float sk = fast_exp2(mk[c] - mn);
-                  Ls[c0 + c] = Ls[c0 + c] * so + lk[c] * sk;
-                  Os[c0 + c] = Os[c0 + c] * so + ak[c] * sk;
-                  M[c0 + c] = mn;
-                }
-              }
-            }
-#pragma unroll
-            for (int c = 0; c < H; ++c) {
-              const int f = qt * NQ + col0 + c;
-              if (f < P.rows_per_head) {
-                const int row = f / P.g, hh = h * P.g + f % P.g;
-                const long long o_idx = static_cast<long long>(row) * P.hq + hh;
-                args.o_sys[o_idx * RB_HEAD_DIM + dcol] = Os[c] / Ls[c];
-                if (qd == 0 && lane == 0) args.lse_sys[o_idx] = (M[c] + __log2f(Ls[c])) * kLn2;
-              }
-            }
-          }
         }
+        // (split units always defer: rb_system_attention merges their parts in
+        // a separate launch, sys_merge_parts_kernel)
       }
       if (dts) {
         d_e3 += global_timer_ns() - d_t0;

@@ -473,53 +473,9 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
           named_bar_sync(1, 128);  // every row's part written
           pend_u = u;
         }
-      } else if (nparts > 1) {
-        named_bar_sync(1, 128);
-        if (warp == kSmWarp0 && lane == 0) {
-          __threadfence();
-          const int prev = atomicAdd(&args.counters[u], 1);
-          const int last = (prev == nparts - 1);
-          if (last) atomicExch(&args.counters[u], 0);
-          misc[2] = last;
-        }
-        named_bar_sync(1, 128);
-        if (misc[2]) {
-          // last CTA of unit u: merge the slots in slot order (deterministic)
-          __threadfence();
-          const long long ubase = static_cast<long long>(u) * P.max_parts;
-          float M = -INFINITY, Ls = 0.f;
-          float O[128];
-#pragma unroll
-          for (int e = 0; e < 128; ++e) O[e] = 0.f;
-          for (int k = 0; k < nparts; ++k) {
-            const float mk = __ldcg(args.part_ml + (ubase + k) * 2 * kRows + r);
-            const float lk = __ldcg(args.part_ml + (ubase + k) * 2 * kRows + kRows + r);
-            const float mn = fmaxf(M, mk);
-            const float so = (M == -INFINITY) ? 0.f : fast_exp2(M - mn);
-            const float sk = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mn);
-            Ls = Ls * so + lk * sk;
-            const float* src = args.part_acc + ((ubase + k) * kRows + r) * RB_HEAD_DIM;
-#pragma unroll
-            for (int e = 0; e < 128; e += 4) {
-              const float4 a4 = __ldcg(reinterpret_cast<const float4*>(src + e));
-              O[e] = O[e] * so + a4.x * sk;
-              O[e + 1] = O[e + 1] * so + a4.y * sk;
-              O[e + 2] = O[e + 2] * so + a4.z * sk;
-              O[e + 3] = O[e + 3] * so + a4.w * sk;
-            }
-            M = mn;
-          }
-          if (row_ok) {
-            const float iv = 1.f / Ls;
-#pragma unroll
-            for (int e = 0; e < 128; e += 4)
-              *reinterpret_cast<float4*>(args.o_sys + o_idx * RB_HEAD_DIM + e) =
-                  make_float4(O[e] * iv, O[e + 1] * iv, O[e + 2] * iv, O[e + 3] * iv);
-            args.lse_sys[o_idx] = (M + __log2f(Ls)) * kLn2;
-          }
-        }
-        named_bar_sync(1, 128);  // misc[2] reads done before the next unit
       }
+      // (split units always defer: rb_system_attention merges their parts in
+      // a separate launch, sys_merge_parts_kernel)
       i = unit_end;
     }
     if (pend_u >= 0 && warp == kSmWarp0 && lane == 0) {
