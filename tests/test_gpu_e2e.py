@@ -116,3 +116,27 @@ def test_resplit_follows_growing_contexts(oracle):
     torch.cuda.synchronize()
     check_sampled_pairs(oracle, out, lse, q, sys_cache, paged, 0, [(r, 0) for r in range(16)], 1,
                         "relay step after resplit")
+
+
+@pytest.mark.parametrize("b,hq,hkv,s", [(64, 32, 8, 300), (40, 64, 8, 520)])
+def test_gqa2_query_loaders_agree(oracle, b, hq, hkv, s):
+    """The 256-row GQA system kernel loads its query tiles by TMA when q is in
+    device memory and with cp.async when q is pinned host memory (the
+    zero-copy step): both must give the same step bitwise, and the oracle's
+    result on sampled pairs (b=40, g=8: a partial last unit, rows past the
+    batch zero-filled by either loader)."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    lens = [1 + (7 * r) % 90 for r in range(b)]
+    q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, seed=b + s)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq)
+    assert step.plan["nq"] == 256, step.plan
+    ref = step(q)[0].clone()
+    lse_ref = step.lse.clone()
+    qh = q.cpu().pin_memory()
+    step._launch(qh, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(step.out, ref), "host-q (cp.async) and device-q (TMA) steps differ"
+    assert torch.equal(step.lse, lse_ref)
+    pairs = [(r, h) for r in (0, b // 2, b - 1) for h in (0, hkv - 1)]
+    check_sampled_pairs(oracle, ref.float(), lse_ref, q, sys_cache, paged, 0, pairs, hq // hkv,
+                        f"gqa2 loaders b={b} g={hq // hkv}")
