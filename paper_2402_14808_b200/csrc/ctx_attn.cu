@@ -425,10 +425,20 @@ using CtxCompute = SwapCompute<R>;
 // system parts per batch of loads in flight in the relay fusion (C4 split
 // units have 6 parts: batch 8 = one round trip per row; C4 step 110.6 ->
 // 105.2 us against batch 4)
+#ifndef RB_RELAY_GROUPED
+#define RB_RELAY_GROUPED 1
+#endif
 #ifndef RB_RELAY_BATCH
 #define RB_RELAY_BATCH 8
 #endif
 constexpr int kRB = RB_RELAY_BATCH;  // system parts per batch of loads in flight
+// One step of the slot-order part fold, o * so + a * sk, with the rounding
+// spelled out so every fusion path (per row, grouped rows, parked rows)
+// gives the same bits whichever of them a row takes.
+__device__ __forceinline__ float relay_fold(float o, float so, float a, float sk) {
+  return __fmaf_rn(o, so, __fmul_rn(a, sk));
+}
+
 struct RelayParts {
   long long base;
   int np, col;
@@ -478,11 +488,11 @@ __device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayPa
       const float mn = fmaxf(mt, P.mk[kk]);
       const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
       const float sk = fast_exp2(P.mk[kk] - mn);
-      lt = lt * so + P.lk[kk] * sk;
-      O.x = O.x * so + P.ak[kk].x * sk;
-      O.y = O.y * so + P.ak[kk].y * sk;
-      O.z = O.z * so + P.ak[kk].z * sk;
-      O.w = O.w * so + P.ak[kk].w * sk;
+      lt = relay_fold(lt, so, P.lk[kk], sk);
+      O.x = relay_fold(O.x, so, P.ak[kk].x, sk);
+      O.y = relay_fold(O.y, so, P.ak[kk].y, sk);
+      O.z = relay_fold(O.z, so, P.ak[kk].z, sk);
+      O.w = relay_fold(O.w, so, P.ak[kk].w, sk);
       mt = mn;
     }
   }
@@ -505,6 +515,102 @@ __device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, l
                                                 float* lse_out, int lane) {
   RelayParts P = relay_parts_begin(SP, hq, pair, part_acc, part_ml, lane);
   relay_fuse_finish(SP, P, pair, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
+}
+
+// Relay fusion of all R rows of an item at once, when they share one published
+// system unit (a row's unit: its KV head and query tile; an item's rows are
+// consecutive flattened rows).  Lane group rg = lane / LPR owns row rg, lane
+// li of the group head dims [li DPL, (li + 1) DPL): the row's context state
+// is combined from the workers' merge buffers, then the unit's parts are
+// folded in slot order with KB parts' loads in flight -- one L2 round trip
+// per KB parts for the whole item instead of one per row (R = 8 at C5: the
+// per-row fusion made the merger the bottleneck once the system units were
+// published).  Same arithmetic per element as relay_fuse_finish.
+template <int R>
+__device__ __forceinline__ void relay_fuse_rows(const rb_sys_plan& SP, int hq, long long pair,
+                                                const float* bacc, const float* bml,
+                                                const float* part_acc, const float* part_ml,
+                                                void* out, int out_fp32, float* lse_out, int lane) {
+  constexpr int LPR = 32 / R, DPL = RB_HEAD_DIM / LPR, NV = DPL / 4;
+  constexpr int KB = R >= 8 ? 2 : 8 / R;
+  const int rg = lane / LPR, li = lane % LPR;
+  float M = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) M = fmaxf(M, bml[(k * R + rg) * 2]);
+  float Ls = 0.f;
+  float4 O[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) O[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (M != -INFINITY) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float mk = bml[(k * R + rg) * 2];
+      const float wt = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
+      Ls = fmaf(bml[(k * R + rg) * 2 + 1], wt, Ls);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const float4 av = *reinterpret_cast<const float4*>(bacc + (k * R + rg) * kAccStride + li * DPL + 4 * v);
+        O[v].x = fmaf(av.x, wt, O[v].x);
+        O[v].y = fmaf(av.y, wt, O[v].y);
+        O[v].z = fmaf(av.z, wt, O[v].z);
+        O[v].w = fmaf(av.w, wt, O[v].w);
+      }
+    }
+  }
+  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+  const int f = row * SP.g + hh % SP.g;
+  const int col = f % SP.nq;
+  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
+  const int np = rb_unit_parts(&SP, u);
+  const long long base = static_cast<long long>(u) * SP.max_parts;
+  float mt = M, lt = Ls;
+  for (int k0 = 0; k0 < np; k0 += KB) {
+    float mk[KB], lk[KB];
+    float4 ak[KB][NV];
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      const int k = min(k0 + kk, np - 1);
+      const float* pml = part_ml + (base + k) * 2 * SP.nq;
+      mk[kk] = __ldcg(pml + col);
+      lk[kk] = __ldcg(pml + SP.nq + col);
+      const float* pa = part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + li * DPL;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) ak[kk][v] = __ldcg(reinterpret_cast<const float4*>(pa + 4 * v));
+    }
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      if (k0 + kk >= np) break;
+      const float mn = fmaxf(mt, mk[kk]);
+      const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+      const float sk = fast_exp2(mk[kk] - mn);
+      lt = relay_fold(lt, so, lk[kk], sk);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        O[v].x = relay_fold(O[v].x, so, ak[kk][v].x, sk);
+        O[v].y = relay_fold(O[v].y, so, ak[kk][v].y, sk);
+        O[v].z = relay_fold(O[v].z, so, ak[kk][v].z, sk);
+        O[v].w = relay_fold(O[v].w, so, ak[kk][v].w, sk);
+      }
+      mt = mn;
+    }
+  }
+  const float inv = 1.f / lt;
+  if (out_fp32) {
+    float* o = reinterpret_cast<float*>(out) + pair * 128 + li * DPL;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      reinterpret_cast<float4*>(o)[v] = make_float4(O[v].x * inv, O[v].y * inv, O[v].z * inv, O[v].w * inv);
+  } else {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + pair * 128 + li * DPL;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      uint2 pk;
+      pk.x = pack_bf16x2(O[v].x * inv, O[v].y * inv);
+      pk.y = pack_bf16x2(O[v].z * inv, O[v].w * inv);
+      reinterpret_cast<uint2*>(o)[v] = pk;
+    }
+  }
+  if (lse_out != nullptr && li == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
 }
 
 // Is the system unit of `pair` published (all its parts written)?  Lane 0
@@ -531,6 +637,11 @@ __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, 
 // Published-unit bitmask of the merger's background poll: lane l holds bit
 // k for unit l + 32 k (k < kPollSlots); warp-uniform call.
 constexpr int kPollSlots = 8;   // polls up to 256 system units
+__device__ __forceinline__ int relay_unit_of(const rb_sys_plan& SP, int hq, long long pair) {
+  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
+  const int f = row * SP.g + hh % SP.g;
+  return (hh / SP.g) * SP.n_qt + f / SP.nq;
+}
 __device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int hq, long long pair,
                                                      uint32_t pub) {
   const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
@@ -557,9 +668,10 @@ template <int R>
 #define RB_CTX_DEPTH1 3
 #endif
 // chunks in flight per worker for 4- and 8-row items (C4 / C5 GQA shapes):
-// measured C4 step 110.3 us at depth 3, 104.8 at 2, 136 at 1; C5 640.5 at
-// depth 2, 631 at 1 -- fewer context bytes in flight leave HBM to the
-// concurrent system kernel without starving the context side
+// measured C4 step 110.3 us at depth 3, 104.8 at 2, 136 at 1; C5 with the
+// grouped relay fusion 625 us at depth 2, 659 at 1 -- fewer context bytes
+// in flight leave HBM to the concurrent system kernel, too few starve the
+// context side
 #ifndef RB_CTX_DEPTH4
 #define RB_CTX_DEPTH4 2
 #endif
@@ -567,11 +679,23 @@ template <int R>
 #define RB_CTX_NB4 1
 #endif
 #ifndef RB_CTX_DEPTH8
-#define RB_CTX_DEPTH8 1
+#define RB_CTX_DEPTH8 2
 #endif
 struct CtxCfg {
   static constexpr int kDepth = R >= 8 ? RB_CTX_DEPTH8 : (R == 1 ? RB_CTX_DEPTH1 : R == 4 ? RB_CTX_DEPTH4 : 3);  // chunks in flight per worker
   static constexpr int kNB = R == 1 ? 3 : R == 2 ? 2 : R == 4 ? RB_CTX_NB4 : 2;  // merge buffers
+  // relay rows a CTA can park while their system unit is unpublished; when
+  // the list is full the merger blocks on the unit.  At C5 every unit is
+  // published only when the system kernel ends (~470 us), so the context
+  // CTAs beside it block after ~8 items -- and that measured faster than
+  // letting them run on (1022 / 4094 slots: C5 625 -> 659 us with depth 2;
+  // the extra context traffic slows the tensor-bound system kernel more
+  // than it saves, and their parked rows make a 20 us end-phase tail)
+#ifdef RB_CTX_MAXDEFER
+  static constexpr int kMaxDefer = RB_CTX_MAXDEFER;
+#else
+  static constexpr int kMaxDefer = 62;
+#endif
 };
 #ifndef RB_CTX_IQ
 #define RB_CTX_IQ 3
@@ -580,7 +704,6 @@ constexpr int kIQ = RB_CTX_IQ;                         // item queue depth (clai
 constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
-constexpr int kMaxDefer = 62;                  // relay rows per CTA awaiting their system unit
 
 // Relay fusion of a parked pair (the end phase): 8 lanes per pair, lane
 // sub = lane & 7 owning head dims [16 sub, 16 sub + 16), so one warp fuses
@@ -622,13 +745,13 @@ __device__ __forceinline__ void relay_fuse_parked8(const rb_sys_plan& SP, int hq
     const float mn = fmaxf(mt, mk);
     const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
     const float sk = fast_exp2(mk - mn);
-    lt = lt * so + lk * sk;
+    lt = relay_fold(lt, so, lk, sk);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      O[v].x = O[v].x * so + ak[v].x * sk;
-      O[v].y = O[v].y * so + ak[v].y * sk;
-      O[v].z = O[v].z * so + ak[v].z * sk;
-      O[v].w = O[v].w * so + ak[v].w * sk;
+      O[v].x = relay_fold(O[v].x, so, ak[v].x, sk);
+      O[v].y = relay_fold(O[v].y, so, ak[v].y, sk);
+      O[v].z = relay_fold(O[v].z, so, ak[v].z, sk);
+      O[v].w = relay_fold(O[v].w, so, ak[v].w, sk);
     }
     mt = mn;
   }
@@ -672,6 +795,7 @@ struct CtaSmem {
   static constexpr int kOffML = kOffAcc + kNB * kWorkers * R * kAccStride * 4;  // [kNB][kWorkers][R][2]
   static constexpr int kOffItems = (kOffML + kNB * kWorkers * R * 8 + 15) & ~15;  // [kIQ] ItemSlot
   static constexpr int kOffBar = (kOffItems + kIQ * static_cast<int>(sizeof(ItemSlot<R>)) + 7) & ~7;
+  static constexpr int kMaxDefer = CtxCfg<R>::kMaxDefer;
   static constexpr int kOffDefer = kOffBar + (3 * kIQ + 2 * kNB) * 8;  // [1 + kMaxDefer] int
   // [R][kAccStride] f32: rows of a split combine (merger only)
   static constexpr int kOffComb = (kOffDefer + (1 + kMaxDefer) * 4 + 15) & ~15;
@@ -943,7 +1067,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     // the last step of a (row, head): relay fusion / park, or output
     auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts& pp) {
       if (a.ctx_part != nullptr) {
-        const bool full = defer[0] >= kMaxDefer;
+        const bool full = defer[0] >= SM::kMaxDefer;
         if (use_pre) {
           relay_fuse_finish(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
                             a.out_fp32, a.lse_out, lane);
@@ -1062,8 +1186,18 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         const int t = li / a.g, jj = li % a.g;
         return static_cast<long long>(it.row0 + t) * a.hq + it.h * a.g + jj;
       };
+      // all rows of the item in one published system unit: grouped fusion
+      bool grouped = false;
+      if (RB_RELAY_GROUPED && R > 1 && !split && poll && nrow == R) {
+        const long long o0 = row_oidx(0), o1 = row_oidx(R - 1);
+        grouped = relay_unit_of(a.sys_plan, a.hq, o0) == relay_unit_of(a.sys_plan, a.hq, o1) &&
+                  relay_unit_published(a.sys_plan, a.hq, o0, pub);
+      }
+      if (grouped)
+        relay_fuse_rows<R>(a.sys_plan, a.hq, row_oidx(lane / (32 / R)), bacc, bml, a.sys_part_acc,
+                           a.sys_part_ml, a.out, a.out_fp32, a.lse_out, lane);
 #pragma unroll 1
-      for (int i = 0; i < nrow; ++i) {
+      for (int i = 0; i < (grouped ? 0 : nrow); ++i) {
         const long long oidx = row_oidx(i);
         float M = -INFINITY;
 #pragma unroll

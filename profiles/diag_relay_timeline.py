@@ -124,6 +124,20 @@ def run(s, phases=3, b=32, h=52, c=128, hkv=None):
                 print(f"  ctx {n:20s} {q([float(v) / 1e3 for v in wst[:, i].tolist()])}")
             print(f"  ctx w0 chunks        {q([float(v) for v in wst[:, 4].tolist()])}")
             print(f"  ctx w0 waits w/ 1 in flight {q([float(v) for v in wst[:, 3].tolist()])}")
+        # early (started beside the system kernel) vs late context CTAs
+        accf = t[4096:4096 + 1024]
+        ctx_idx = [i for i in range(1024) if int(t[1024 + i, 0]) != 0]
+        if len(ctx_idx) and int(accf[:, 6].max()) != 0:
+            early = [i for i in ctx_idx if us(t[1024 + i, 0]) < 50.0]
+            late = [i for i in ctx_idx if us(t[1024 + i, 0]) >= 50.0]
+            for name, grp in (("early", early), ("late", late)):
+                if not grp:
+                    continue
+                ep = [us(accf[i, 6]) for i in grp if int(accf[i, 6])]
+                dn = [us(t[1024 + i, 6]) for i in grp if int(t[1024 + i, 6])]
+                nd = [float(accf[i, 7]) for i in grp]
+                print(f"  ctx {name} CTAs {len(grp)}: end-phase start {q(ep) if ep else '-'}")
+                print(f"  ctx {name} done {q(dn) if dn else '-'}; deferred {q(nd)}")
         durs = [(int(r[7]) - int(r[0])) / 1e3 for r in ctx_t]
         print(f"  ctx CTA duration p50 {statistics.median(durs):.1f} max {max(durs):.1f}")
 
