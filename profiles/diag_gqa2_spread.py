@@ -52,6 +52,10 @@ def main():
     d = [(int(r[5]) - int(r[4])) / 1e3 for r in rows if int(r[5]) and int(r[4])]
     if d:
         print(f"merge duration p50 {statistics.median(d):.1f} max {max(d):.1f} us")
+    d = sorted((int(r[3]) - int(r[2])) / 1e3 for r in rows if int(r[3]) and int(r[2]))
+    if d:
+        print(f"first S -> last epilogue p10 {d[len(d) // 10]:.1f} p50 {statistics.median(d):.1f} "
+              f"max {d[-1]:.1f} us (key-tile loop of the CTA's range)")
     d = [(int(r[4]) - int(r[3])) / 1e3 for r in rows if int(r[4]) and int(r[3])]
     if d:
         print(f"part write p50 {statistics.median(d):.1f} max {max(d):.1f} us")
