@@ -735,25 +735,38 @@ __device__ __forceinline__ void relay_fuse_parked8(const rb_sys_plan& SP, int hq
   const float2 ml = __ldcg(reinterpret_cast<const float2*>(cp + 128));
   float mt = ml.x, lt = ml.y;
   const long long base = static_cast<long long>(u) * SP.max_parts;
-  for (int k = 0; k < np; ++k) {  // the first part's loads fly with the context part's
-    const float* pml = part_ml + (base + k) * 2 * SP.nq;
-    const float mk = __ldcg(pml + col), lk = __ldcg(pml + SP.nq + col);
-    const float* pa = part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0;
-    float4 ak[4];
+  // parts in batches of 4 with all their loads in flight (the first batch's
+  // with the context part's): C4's 6-part units took 6 dependent round trips
+  constexpr int KB = 4;
+  for (int k0 = 0; k0 < np; k0 += KB) {
+    float mk[KB], lk[KB];
+    float4 ak[KB][4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) ak[v] = __ldcg(reinterpret_cast<const float4*>(pa + 4 * v));
-    const float mn = fmaxf(mt, mk);
-    const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
-    const float sk = fast_exp2(mk - mn);
-    lt = relay_fold(lt, so, lk, sk);
+    for (int kk = 0; kk < KB; ++kk) {
+      const int k = min(k0 + kk, np - 1);
+      const float* pml = part_ml + (base + k) * 2 * SP.nq;
+      mk[kk] = __ldcg(pml + col);
+      lk[kk] = __ldcg(pml + SP.nq + col);
+      const float* pa = part_acc + ((base + k) * SP.nq + col) * RB_HEAD_DIM + d0;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      O[v].x = relay_fold(O[v].x, so, ak[v].x, sk);
-      O[v].y = relay_fold(O[v].y, so, ak[v].y, sk);
-      O[v].z = relay_fold(O[v].z, so, ak[v].z, sk);
-      O[v].w = relay_fold(O[v].w, so, ak[v].w, sk);
+      for (int v = 0; v < 4; ++v) ak[kk][v] = __ldcg(reinterpret_cast<const float4*>(pa + 4 * v));
     }
-    mt = mn;
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      if (k0 + kk >= np) break;
+      const float mn = fmaxf(mt, mk[kk]);
+      const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+      const float sk = fast_exp2(mk[kk] - mn);
+      lt = relay_fold(lt, so, lk[kk], sk);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        O[v].x = relay_fold(O[v].x, so, ak[kk][v].x, sk);
+        O[v].y = relay_fold(O[v].y, so, ak[kk][v].y, sk);
+        O[v].z = relay_fold(O[v].z, so, ak[kk][v].z, sk);
+        O[v].w = relay_fold(O[v].w, so, ak[kk][v].w, sk);
+      }
+      mt = mn;
+    }
   }
   const float inv = 1.f / lt;
   if (out_fp32) {
