@@ -144,6 +144,10 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * paged pool at slot_mapping[row] (as rb_kv_append would) by the context
  * item that streams them, before its workers read them; ctx_lens already
  * count the new tokens.  One launch pair then covers append + attention.
+ * q and out may be pinned host memory (the zero-copy step): host queries are
+ * first copied into a staging region of the workspace by one small kernel
+ * (both kernels then read device memory; the system kernel's K/V prefetch
+ * overlaps the copy), and output rows are written to host memory directly.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
  * (2 | 4: the context kernel of a step whose system kernel was launched by an
  * earlier phase-1 call, e.g. with stream work in between; the units are

@@ -29,6 +29,8 @@ namespace rb {
 cudaError_t launch_system_attention(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                                     const SysArgs&, cudaStream_t);
 cudaError_t launch_sys_merge_parts(const SysArgs&, cudaStream_t);
+cudaError_t launch_q_stage(const __nv_bfloat16*, long long, long long, int, int, __nv_bfloat16*, int,
+                           cudaStream_t);
 cudaError_t launch_context_attention(const CtxArgs&, int, cudaStream_t);
 int ctx_resident_ctas(int sms);
 cudaError_t launch_relay_fusion(const float*, const float*, const float*, const float*, float*,
@@ -361,6 +363,20 @@ static void relay_ws_layout(const rb_sys_plan& p, size_t* cnt_bytes, size_t* cpa
   *acc_bytes = (size_t)p.n_units * p.max_parts * p.nq * RB_HEAD_DIM * sizeof(float);
 }
 
+// staging copy of the queries when the caller passes them in host memory
+static size_t q_stage_bytes(int n_rows, int hq) {
+  return ((size_t)n_rows * hq * RB_HEAD_DIM * 2 + 255) & ~(size_t)255;
+}
+
+static bool is_host_memory(const void* p) {
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
 int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, int b,
                              int max_rows, int max_ctx_len, int sm_count, size_t* bytes) {
   long long f[8];
@@ -374,7 +390,7 @@ int rb_relay_workspace_bytes(int n_rows, int hq, int hkv, int s, int grid_cap, i
   int L, ns;
   ctx_split_plan(b, hkv, max_rows, 0, max_ctx_len, sm_count, &L, &ns);
   const size_t split = (size_t)rb_ctx_split_bytes(b, n_rows, hq, hkv, max_rows, ns);
-  *bytes = 256 + cnt + cpart + ml + ((acc + 255) & ~(size_t)255) + split;
+  *bytes = 256 + cnt + cpart + ml + ((acc + 255) & ~(size_t)255) + q_stage_bytes(n_rows, hq) + split;
   return RB_OK;
 }
 
@@ -416,17 +432,31 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
       (reinterpret_cast<uintptr_t>(q) & 15))
     return fail(RB_ERR_CONTRACT, "q rows must be 16-byte aligned");
   cudaStream_t cs = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
   rb::SysArgs sa;
   rb_make_sys_plan(&sa.plan, n_rows, hq, hkv, s, grid_cap);
+  size_t cnt, cpart, ml, acc_b;
+  relay_ws_layout(sa.plan, &cnt, &cpart, &ml, &acc_b);
+  const size_t q_off = 256 + cnt + cpart + ml + ((acc_b + 255) & ~(size_t)255);
+  const size_t split_off = q_off + q_stage_bytes(n_rows, hq);
+  if ((phases & 1) && is_host_memory(q)) {
+    // queries in pinned host memory (the zero-copy step): staged once into
+    // the workspace; both kernels read the device copy
+    __nv_bfloat16* qd = reinterpret_cast<__nv_bfloat16*>(ws + q_off);
+    st = cuda_status(rb::launch_q_stage(static_cast<const __nv_bfloat16*>(q), q_row_stride,
+                                        q_head_stride, n_rows, hq, qd, sms, cs),
+                     "query staging launch");
+    if (st != RB_OK) return st;
+    q = qd;
+    q_row_stride = (long long)hq * RB_HEAD_DIM;
+    q_head_stride = RB_HEAD_DIM;
+  }
   sa.q = static_cast<const __nv_bfloat16*>(q);
   sa.q_row_stride = q_row_stride;
   sa.q_head_stride = q_head_stride;
   sa.scale_log2 = scale * rb::kLog2e;
   sa.o_sys = nullptr;
   sa.lse_sys = nullptr;
-  uint8_t* ws = static_cast<uint8_t*>(workspace);
-  size_t cnt, cpart, ml, acc_b;
-  relay_ws_layout(sa.plan, &cnt, &cpart, &ml, &acc_b);
   int* header = reinterpret_cast<int*>(ws);
   float* ctx_part = reinterpret_cast<float*>(ws + 256 + cnt);
   sa.counters = reinterpret_cast<int*>(ws + 256);
@@ -486,7 +516,6 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.slot_mapping = slot_mapping;
   {
     // (the context split-K plan covers the context chunks only)
-    const size_t split_off = 256 + cnt + cpart + ml + ((acc_b + 255) & ~(size_t)255);
     st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, ws + split_off, workspace_bytes - split_off);
     if (st != RB_OK) return st;
   }

@@ -1701,6 +1701,41 @@ __global__ void kv_append_kernel(const __nv_bfloat16* __restrict__ k_new,
     *reinterpret_cast<uint4*>(k_pool + dst) = *reinterpret_cast<const uint4*>(k_new + src);
 }
 
+// Zero-copy relay step with the queries in pinned host memory: one pass
+// copies them into device memory ([rows][hq][128], 16 B per thread per
+// iteration, as many loads in flight as the SMs hold) before the system and
+// context kernels read them -- both kernels used to read the host rows
+// themselves, the system kernel once per stream-K part of a unit, so ~1.5 MB
+// crossed PCIe for 0.43 MB of queries at C2.  The system kernel launches as a
+// PDL dependent at once and prefetches its K/V tiles; its query loader waits
+// for this grid.
+__global__ void __launch_bounds__(256) q_stage_kernel(const __nv_bfloat16* __restrict__ q,
+                                                      long long row_stride, long long head_stride,
+                                                      int n_rows, int hq,
+                                                      __nv_bfloat16* __restrict__ dst) {
+  pdl_launch_dependents();
+  const long long chunks = static_cast<long long>(n_rows) * hq * 16;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < chunks; i += 256LL * gridDim.x) {
+    const int c = static_cast<int>(i & 15);
+    const long long rh = i >> 4;
+    const int row = static_cast<int>(rh / hq), h = static_cast<int>(rh % hq);
+    reinterpret_cast<uint4*>(dst)[i] =
+        *reinterpret_cast<const uint4*>(q + row * row_stride + h * head_stride + c * 8);
+  }
+}
+
+cudaError_t launch_q_stage(const __nv_bfloat16* q, long long row_stride, long long head_stride,
+                           int n_rows, int hq, __nv_bfloat16* dst, int sms, cudaStream_t stream) {
+  const long long chunks = static_cast<long long>(n_rows) * hq * 16;
+  if (chunks == 0) return cudaSuccess;
+  const long long want = (chunks + 255) / 256;
+  const int grid = static_cast<int>(want < 4LL * sms ? want : 4LL * sms);
+  cudaError_t e = launch_pdl(q_stage_kernel, dim3(grid), dim3(256), 0, stream, q, row_stride, head_stride,
+                             n_rows, hq, dst);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_kv_append(const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                              const int* slots, __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
                              int n_tok, int hkv, int block_size, long long stride_block,
