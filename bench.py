@@ -618,11 +618,13 @@ def run_b200(args):
         "e2e": {"value": e2e_ms * 1e3, "unit": "µs/step", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],
                 "path": "RelayDecodeStep.host_step_graph (CUDA graph, zero-copy): rb_relay_attention "
-                        "reads q and the new tokens' K/V from the pinned host buffer, appends K/V "
-                        "inside the context kernel, runs system || context with the fusion in-kernel "
-                        "and writes the output rows into pinned host memory",
+                        "stages q from the pinned host buffer into device memory (q_stage_kernel, "
+                        "PDL-overlapped with the system kernel's K/V prefetch), reads the new tokens' "
+                        "K/V from pinned memory and appends them inside the context kernel, runs "
+                        "system || context with the fusion in-kernel and writes the output rows into "
+                        "pinned host memory",
                 "eager_us": e2e_eager_ms * 1e3, "eager_path": "step_host: H2D copies, rb_kv_append, "
-                "the relay step, D2H copy", "launches_per_step": 2},
+                "the relay step, D2H copy", "launches_per_step": 3},
         "gpu_launches": 2 * args.steps,
         "relay_vs_naive_max_abs": head["relay_vs_naive_max_abs"],
         "sys_plan": head["plan"],
