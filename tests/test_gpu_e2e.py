@@ -118,13 +118,13 @@ def test_resplit_follows_growing_contexts(oracle):
                         "relay step after resplit")
 
 
-@pytest.mark.parametrize("b,hq,hkv,s", [(64, 32, 8, 300), (40, 64, 8, 520)])
+@pytest.mark.parametrize("b,hq,hkv,s", [(64, 32, 8, 300), (40, 64, 8, 520), (48, 48, 8, 260)])
 def test_gqa2_query_loaders_agree(oracle, b, hq, hkv, s):
-    """The 256-row GQA system kernel loads its query tiles by TMA when q is in
-    device memory and with cp.async when q is pinned host memory (the
-    zero-copy step): both must give the same step bitwise, and the oracle's
-    result on sampled pairs (b=40, g=8: a partial last unit, rows past the
-    batch zero-filled by either loader)."""
+    """Query rows of the 256-row GQA system kernel: by TMA from device memory
+    (g divides 128), by the cp.async loader otherwise (g = 6 here), and from
+    pinned host memory through the step's staging copy.  Host and device q
+    must give the same step bitwise, and the oracle's result on sampled
+    pairs (b=40, g=8: a partial last unit, rows past the batch zero-filled)."""
     from paper_2402_14808_b200.attention import RelayDecodeStep
     lens = [1 + (7 * r) % 90 for r in range(b)]
     q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, seed=b + s)
