@@ -502,62 +502,9 @@ __global__ void __launch_bounds__(g2::kThreads, 1)
             atomicAdd(&args.counters[u], 1);
           }
         }
-      } else if (nparts > 1) {
-        named_bar_sync(bar_id, bar_n);
-        if (warp == kSmWarp0 && lane == 0) {
-          __threadfence();
-          const int prev = atomicAdd(&args.counters[u], 1);
-          const int last = (prev == nparts - 1);
-          if (last) atomicExch(&args.counters[u], 0);
-          misc[2] = last;
-        }
-        named_bar_sync(bar_id, bar_n);
-        if (misc[2]) {
-          // last CTA of unit u: merge the slots in slot order (deterministic),
-          // 32 head dims at a time
-          __threadfence();
-          const long long ubase = static_cast<long long>(u) * P.max_parts;
-          float M = -INFINITY, Ls = 0.f;
-          for (int k = 0; k < nparts; ++k) {
-            const float mk = __ldcg(args.part_ml + (ubase + k) * 2 * kUnitRows + ur);
-            const float lk = __ldcg(args.part_ml + (ubase + k) * 2 * kUnitRows + kUnitRows + ur);
-            const float mn = fmaxf(M, mk);
-            const float so = (M == -INFINITY) ? 0.f : fast_exp2(M - mn);
-            const float sk = (mk == -INFINITY) ? 0.f : fast_exp2(mk - mn);
-            Ls = Ls * so + lk * sk;
-            M = mn;
-          }
-          const float iv = 1.f / Ls;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            float O[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) O[e] = 0.f;
-            for (int k = 0; k < nparts; ++k) {
-              const float mk = __ldcg(args.part_ml + (ubase + k) * 2 * kUnitRows + ur);
-              const float sk = (mk == -INFINITY) ? 0.f : fast_exp2(mk - M);
-              const float* src = args.part_acc + ((ubase + k) * kUnitRows + ur) * RB_HEAD_DIM + c * 32;
-#pragma unroll
-              for (int e = 0; e < 32; e += 4) {
-                const float4 a4 = __ldcg(reinterpret_cast<const float4*>(src + e));
-                O[e] = fmaf(a4.x, sk, O[e]);
-                O[e + 1] = fmaf(a4.y, sk, O[e + 1]);
-                O[e + 2] = fmaf(a4.z, sk, O[e + 2]);
-                O[e + 3] = fmaf(a4.w, sk, O[e + 3]);
-              }
-            }
-            if (row_ok) {
-#pragma unroll
-              for (int e = 0; e < 32; e += 4)
-                *reinterpret_cast<float4*>(args.o_sys + o_idx * RB_HEAD_DIM + c * 32 + e) =
-                    make_float4(O[e] * iv, O[e + 1] * iv, O[e + 2] * iv, O[e + 3] * iv);
-            }
-          }
-          if (row_ok) args.lse_sys[o_idx] = (M + __log2f(Ls)) * kLn2;
-          if (dts && r == 0 && sub == 0) dts[5] = global_timer_ns();
-        }
-        named_bar_sync(bar_id, bar_n);  // misc[2] reads done before the next unit
       }
+      // (split units always defer: rb_system_attention merges their parts in
+      // a separate launch, sys_merge_parts_kernel)
       i = unit_end;
     }
   }
