@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define RB_ABI_VERSION 3
+#define RB_ABI_VERSION 4
 
 enum {
   RB_OK = 0,
@@ -148,6 +148,11 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * first copied into a staging region of the workspace by one small kernel
  * (both kernels then read device memory; the system kernel's K/V prefetch
  * overlaps the copy), and output rows are written to host memory directly.
+ * req_order (optional, int32 [b], a permutation of 0..b-1): the order in which
+ * the context kernel claims the requests' work -- longest context first
+ * keeps the last claims short when the contexts vary (each CTA claims a few
+ * items ahead, and a long queued item at the end is a tail).  Results do not
+ * depend on it.
  * phases: 3 = the full step; 1 / 2 launch only the system / context kernel
  * (2 | 4: the context kernel of a step whose system kernel was launched by an
  * earlier phase-1 call, e.g. with stream work in between; the units are
@@ -175,7 +180,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
                        void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
                        size_t workspace_bytes, int phases, const void* k_new, const void* v_new,
-                       const int* slot_mapping, void* stream);
+                       const int* slot_mapping, const int* req_order, void* stream);
 
 /*
  * Standalone relay fusion (attention.py:137-157) over n_vec vectors of d

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("RB_LIB") or (
     DIAG_LIB_PATH if os.environ.get("RB_DIAG") == "1" else os.path.join(_HERE, "librelay_b200.so"))
 
 RB_OK, RB_ERR_DIMENSION, RB_ERR_CONTRACT, RB_ERR_CUDA = 0, 1, 2, 3
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # every symbol include/relay_b200.h declares
 EXPORTS = (
@@ -90,7 +90,7 @@ def _bind(path):
         vp, vp, i32, i64, i64,                            # sys_k .. sys_stride_head
         vp, vp, vp, i32, i32, vp, i64, i64, i64, vp,      # k .. ctx_lens
         f32, i32, vp, i32, vp, i32, vp, ctypes.c_size_t, i32,   # scale .. phases
-        vp, vp, vp, vp]                                   # k_new, v_new, slot_mapping, stream
+        vp, vp, vp, vp, vp]                               # k_new, v_new, slot_mapping, req_order, stream
     lib.rb_relay_fusion.argtypes = [vp, vp, vp, vp, vp, vp, i64, i32, vp]
     lib.rb_kv_append.argtypes = [vp, vp, vp, i32, vp, vp, i32, i32, i32, i64, i64, i64, vp]
     lib.rb_rope_rows.argtypes = [vp, vp, vp, i64, i32, ctypes.c_double, vp]

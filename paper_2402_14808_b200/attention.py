@@ -428,6 +428,20 @@ class RelayDecodeStep:
         # a system-only launch (profiling) leaves its units published; the
         # next full step must start from rearmed counters
         self._system_pending = False
+        # claim order of the requests' context work: longest first when the
+        # lengths differ (each context CTA claims a few items ahead, and a long
+        # item queued at the end of the pool is a tail); None when uniform
+        self.req_order = None
+        if self.b > 1 and int(ctx_lens.max().item()) != int(ctx_lens.min().item()):
+            self.req_order = torch.empty(self.b, dtype=torch.int32, device=dev)
+            self.reorder()
+
+    def reorder(self):
+        """Recompute the context claim order from the current ctx_lens (in
+        place, so a captured CUDA graph keeps using it; device-side, no sync).
+        Results never depend on the order."""
+        if self.req_order is not None:
+            self.req_order.copy_(torch.argsort(self.ctx_lens, descending=True, stable=True))
 
     def _set_grid(self, grid):
         from . import _lib
@@ -455,6 +469,7 @@ class RelayDecodeStep:
         from . import _lib
         grid = _lib.relay_sys_grid(self.b, self.hq, self.hkv, self.sys_cache.system_len,
                                    int(ctx_tokens), kernels.sm_count(self.block_table.device))
+        self.reorder()
         if grid == self.grid:
             return False
         self._set_grid(grid)
@@ -473,7 +488,8 @@ class RelayDecodeStep:
             block_table=self.block_table, block_size=self.paged.block_size,
             strides=self.paged.strides(), grid=self.grid, out=self.out if out is None else out,
             lse_out=self.lse, ws=self.ws, phases=phases, scale=self.scale,
-            max_ctx_len=self.max_ctx_len, k_new=k_new, v_new=v_new, slot_mapping=slot_mapping)
+            max_ctx_len=self.max_ctx_len, k_new=k_new, v_new=v_new, slot_mapping=slot_mapping,
+            req_order=self.req_order)
 
     def system(self, q):
         """Only the system kernel of the step (profiling)."""

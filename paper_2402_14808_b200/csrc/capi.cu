@@ -345,6 +345,7 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
   a.sched = nullptr;  // static item order
   a.k_new = a.v_new = nullptr;
   a.slot_mapping = nullptr;
+  a.req_order = nullptr;
   int st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, workspace, workspace_bytes);
   if (st != RB_OK) return st;
   return cuda_status(rb::launch_context_attention(a, max_rows, static_cast<cudaStream_t>(stream)),
@@ -411,7 +412,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
                        long long stride_head, const int* ctx_lens, float scale, int grid_cap,
                        void* out, int out_fp32, float* lse_out, int max_ctx_len, void* workspace,
                        size_t workspace_bytes, int phases, const void* k_new, const void* v_new,
-                       const int* slot_mapping, void* stream) {
+                       const int* slot_mapping, const int* req_order, void* stream) {
   if (d != RB_HEAD_DIM) return fail(RB_ERR_DIMENSION, "head_dim %d unsupported (kernels are d=128)", d);
   if ((k_new == nullptr) != (v_new == nullptr) || (k_new != nullptr) != (slot_mapping != nullptr))
     return fail(RB_ERR_CONTRACT, "k_new, v_new and slot_mapping go together");
@@ -514,6 +515,7 @@ int rb_relay_attention(const void* q, long long q_row_stride, long long q_head_s
   a.k_new = static_cast<const __nv_bfloat16*>(k_new);
   a.v_new = static_cast<const __nv_bfloat16*>(v_new);
   a.slot_mapping = slot_mapping;
+  a.req_order = req_order;
   {
     // (the context split-K plan covers the context chunks only)
     st = ctx_split_args(a, n_rows, max_rows, max_ctx_len, ws + split_off, workspace_bytes - split_off);

@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       w.qs0 = w.qs1 = w.clen = w.bte = w.bt0 = 0;
       w.roff = 0;
       if (item < n_items) {
-        const int r = item / per_req;
+        const int r = a.req_order != nullptr ? __ldg(a.req_order + item / per_req) : item / per_req;
         const int sp = item % n_split;
         w.qs0 = __ldg(a.q_start + r);
         w.qs1 = __ldg(a.q_start + r + 1);
@@ -963,6 +963,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         it.z = grp % n_z;
         it.h = (grp / n_z) % a.hkv;
         it.r = grp / (n_z * a.hkv);
+        if (a.req_order != nullptr) it.r = __ldg(a.req_order + it.r);
         it.row0 = cur.qs0;
         it.m_r = cur.qs1 - cur.qs0;
         it.nrows = it.m_r * a.g;

@@ -79,6 +79,10 @@ struct CtxArgs {
   const __nv_bfloat16* k_new;
   const __nv_bfloat16* v_new;
   const int* slot_mapping;
+  // optional claim order of the requests (a permutation of 0..b-1, e.g. the
+  // longest context first): items are claimed in this order, so the last
+  // claims -- the ones whose queued items make a CTA's tail -- are short
+  const int* req_order;
 };
 
 #ifdef __CUDACC__

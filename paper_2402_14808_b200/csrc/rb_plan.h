@@ -181,6 +181,40 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
     g = (k < 1 ? 1 : k) * p.n_units;
     return g;
   }
+  {
+    // Round-robin plans (several query tiles per KV head, whole units per
+    // CTA) can only take n_units / waves CTAs: rounding the byte balance to
+    // one of them leaves the two kernels unbalanced.  Pick the wave count
+    // with the shortest estimated step instead: the system kernel takes
+    // waves x tpu key tiles per CTA; the context kernel streams on the other
+    // SMs meanwhile and on all of them after.  (C3, c ~ U[64, 768], with the
+    // context claimed longest first: 32 CTAs (2 waves) 3223 us per 32-layer
+    // stack, 64 CTAs (1 wave) 3064 us; profiles/diag_c3_stack.py)
+    rb_sys_plan pg;
+    rb_make_sys_plan(&pg, n_rows, hq, hkv, s, g < 1 ? 1 : g);
+    if (pg.rr) {
+      const double rc = RB_CTX_SM_GBS * 1e3;  // context bytes per us per SM
+      const double rs = ratio * rc;           // system bytes per us per SM
+      const double tile_bytes = RB_KEY_TILE * 512.0;
+      double best = 1e300;
+      int bg = pg.grid;
+      for (int w = 1; w <= 8 && w <= p.n_units; ++w) {
+        const int gw = (p.n_units + w - 1) / w;
+        if (gw >= sms) continue;
+        rb_sys_plan pw;
+        rb_make_sys_plan(&pw, n_rows, hq, hkv, s, gw);
+        if (!pw.rr || pw.grid != gw) continue;
+        const double t_sys = (double)w * p.tpu * tile_bytes / rs;
+        const double done = (double)(sms - gw) * rc * t_sys;
+        const double t = done >= ctx_bytes ? t_sys : t_sys + (ctx_bytes - done) / (sms * rc);
+        if (t < best) {
+          best = t;
+          bg = gw;
+        }
+      }
+      g = bg;
+    }
+  }
   // latency floor: with few key tiles per CTA the system kernel is bound by
   // its per-CTA pipeline (prologue + ~1.5 us per tile), not by bytes; the
   // measured optimum at s <= 2k keeps ~20% of the SMs on it

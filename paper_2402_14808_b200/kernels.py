@@ -190,7 +190,7 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
                     sys_layout="hsd", block_table=None, block_size=0, req_offset=None,
                     strides=None, scale=None, grid=None, out=None, lse_out=None,
                     out_fp32=False, ws=None, phases=3, max_ctx_len=0, k_new=None, v_new=None,
-                    slot_mapping=None):
+                    slot_mapping=None, req_order=None):
     """The fused relay step (rb_relay_attention): system kernel (stream-K
     partials, no merge) + context kernel whose epilogue merges the system
     partials with the context state.  Returns (out, lse).  max_ctx_len: an
@@ -198,7 +198,10 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
     then hold rb_relay_workspace_bytes(..., max_ctx_len, sm_count) bytes.
     k_new / v_new (n_rows, hkv, 128) bf16 + slot_mapping int32 (n_rows,):
     the fused append of the step's new tokens (paged layout; the tensors may
-    be pinned host memory); ctx_lens must already count them."""
+    be pinned host memory); ctx_lens must already count them.  req_order
+    (int32 (b,), a permutation of the requests, optional): the order the
+    context kernel claims their work in (longest context first balances
+    varied lengths); the results do not depend on it."""
     # q (and out) may live in pinned host memory (zero-copy e2e step); the
     # caches, indices and workspace are on the device
     _check_bf16("q", q, host_ok=True)
@@ -225,6 +228,10 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
             if not t.is_contiguous() or tuple(t.shape) != (q.shape[0], hkv, HEAD_DIM):
                 raise DimensionError(f"{name} must be contiguous ({q.shape[0]}, {hkv}, {HEAD_DIM})")
         _check_index("slot_mapping", slot_mapping, sys_k.device)
+    if req_order is not None:
+        _check_index("req_order", req_order, sys_k.device)
+        if req_order.numel() != ctx_lens.numel():
+            raise DimensionError(f"req_order needs b = {ctx_lens.numel()} entries, got {req_order.numel()}")
     for name, t in (("out", out), ("lse_out", lse_out)):
         if t is not None and not (t.is_cuda or (t.device.type == "cpu" and t.is_pinned())):
             raise ContractError(f"{name}: expected a CUDA or pinned host tensor")
@@ -259,7 +266,8 @@ def relay_attention(q, q_start, sys_k, sys_v, k, v, ctx_lens, *, max_rows, hkv,
         v.data_ptr(), _ptr(block_table), bt_stride, block_size, _ptr(req_offset), sb, stok, sh,
         ctx_lens.data_ptr(), float(scale), grid, out.data_ptr(),
         1 if out.dtype == torch.float32 else 0, lse_out.data_ptr(), int(max_ctx_len),
-        ws.data_ptr(), ws.numel(), phases, _ptr(k_new), _ptr(v_new), _ptr(slot_mapping), stream),
+        ws.data_ptr(), ws.numel(), phases, _ptr(k_new), _ptr(v_new), _ptr(slot_mapping),
+        _ptr(req_order), stream),
         "rb_relay_attention")
     return out, lse_out
 

@@ -43,7 +43,16 @@ def run(s, phases=3, b=32, h=52, c=128, hkv=None):
     if os.environ.get("DIAG_SEQBT"):
         bt = torch.arange(b * nblk, device=dev, dtype=torch.int32).reshape(b, nblk)
     cl = torch.full((b,), c, dtype=torch.int32, device=dev)
+    if os.environ.get("DIAG_CLENS_U"):
+        # C3-style context lengths ~ U[lo, hi] (seeded), in a c-token block table
+        lo, hi = (int(x) for x in os.environ["DIAG_CLENS_U"].split(","))
+        import numpy as np
+        lens = np.random.default_rng(1002).integers(lo, hi + 1, size=b)
+        cl = torch.tensor(lens, dtype=torch.int32, device=dev)
     qs = torch.arange(b + 1, dtype=torch.int32, device=dev)
+    # DIAG_ORDER=1: claim the context work longest request first (RelayDecodeStep's req_order)
+    order = (torch.argsort(cl, descending=True, stable=True).to(torch.int32)
+             if os.environ.get("DIAG_ORDER") else None)
     ts = torch.zeros((8192, 8), dtype=torch.int64, device=dev)
     import bench
     flush_fn = bench.make_flush(torch, dev)
@@ -56,7 +65,7 @@ def run(s, phases=3, b=32, h=52, c=128, hkv=None):
         e0.record()
         kernels.relay_attention(qq, qs, k, v, pk, pv, cl, max_rows=h // hkv, hkv=hkv, sys_layout="hsd",
                                 block_table=bt, block_size=16, strides=pst, grid=grid,
-                                phases=phases,
+                                phases=phases, req_order=order,
                                 max_ctx_len=c if os.environ.get("DIAG_SPLIT") else 0)
         e1.record()
         torch.cuda.synchronize()

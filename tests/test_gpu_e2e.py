@@ -140,3 +140,26 @@ def test_gqa2_query_loaders_agree(oracle, b, hq, hkv, s):
     pairs = [(r, h) for r in (0, b // 2, b - 1) for h in (0, hkv - 1)]
     check_sampled_pairs(oracle, ref.float(), lse_ref, q, sys_cache, paged, 0, pairs, hq // hkv,
                         f"gqa2 loaders b={b} g={hq // hkv}")
+
+
+@pytest.mark.parametrize("b,hq,hkv,s", [(24, 8, 8, 300), (16, 32, 8, 700)])
+def test_claim_order_does_not_change_results(oracle, b, hq, hkv, s):
+    """RelayDecodeStep claims the context work longest request first when
+    the lengths differ (req_order); the step must be bitwise the same as in
+    request order, and equal the oracle."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    lens = [1 + (37 * r) % 300 for r in range(b)]
+    q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, seed=b * 3 + s)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq)
+    assert step.req_order is not None
+    order = step.req_order.cpu().tolist()
+    assert sorted(order) == list(range(b))
+    assert all(lens[order[i]] >= lens[order[i + 1]] for i in range(b - 1))
+    out_o = step(q)[0].clone()
+    lse_o = step.lse.clone()
+    step.req_order = None
+    out_n = step(q)[0].clone()
+    assert torch.equal(out_o, out_n) and torch.equal(lse_o, step.lse)
+    pairs = [(r, h) for r in (0, b // 2, b - 1) for h in (0, hkv - 1)]
+    check_sampled_pairs(oracle, out_o.float(), lse_o, q, sys_cache, paged, 0, pairs, hq // hkv,
+                        f"claim order b={b} g={hq // hkv}")
