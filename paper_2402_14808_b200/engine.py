@@ -168,6 +168,9 @@ class B200AttentionEngine:
         out = torch.empty((n, hq, HEAD_DIM), dtype=self.out_dtype, device=dev)
         lse = torch.empty((n, hq), dtype=torch.float32, device=dev)
         pool = self.ctx_cache
+        # context work claimed longest request first (RelayDecodeStep's req_order)
+        order = torch.argsort(ctx_lens, descending=True, stable=True).to(torch.int32) \
+            if self.mode == "relay" and n > 1 else None
         e0, e1 = self._ev
         e0.record()
         for layer in range(L):
@@ -179,7 +182,7 @@ class B200AttentionEngine:
                     qr, q_start, sk, sv, pool.k_pool[layer], pool.v_pool[layer], ctx_lens,
                     max_rows=max_rows, hkv=hkv, sys_layout="hsd", block_table=bt,
                     block_size=pool.block_size, strides=pool.strides(), scale=self.sys_cache.scale,
-                    grid=grid, out=out, lse_out=lse, max_ctx_len=max_ctx_len)
+                    grid=grid, out=out, lse_out=lse, max_ctx_len=max_ctx_len, req_order=order)
             else:
                 kernels.context_attention(
                     qr, q_start, pool.k_pool[layer], pool.v_pool[layer], ctx_lens,
