@@ -270,6 +270,12 @@ static int ctx_split_args(rb::CtxArgs& a, int n_rows, int max_rows, int max_ctx_
   a.n_split = 1;
   a.split_part = nullptr;
   a.split_cnt = nullptr;
+  // items of >= 16 chunks (context bound, or the split length below): the
+  // context scheduler claims them one at a time (rb_args.cuh claim_lazy)
+#ifndef RB_CLAIM_LAZY
+#define RB_CLAIM_LAZY 1
+#endif
+  a.claim_lazy = RB_CLAIM_LAZY && (max_ctx_len + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK >= 16 ? 1 : 0;
   if (ws == nullptr) return RB_OK;
   int L, ns;
   ctx_split_plan(a.b, a.hkv, max_rows, a.s_prefix, max_ctx_len, device_sms(), &L, &ns);
@@ -280,6 +286,7 @@ static int ctx_split_args(rb::CtxArgs& a, int n_rows, int max_rows, int max_ctx_
   const size_t part = ((size_t)n_rows * a.hq * ns * 132 * 4 + 255) & ~(size_t)255;
   a.split_chunks = L;
   a.n_split = ns;
+  a.claim_lazy = RB_CLAIM_LAZY && L >= 16 ? 1 : 0;
   a.split_part = static_cast<float*>(ws);
   a.split_cnt = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part);
   return RB_OK;

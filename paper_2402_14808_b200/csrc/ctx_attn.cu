@@ -923,10 +923,16 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       return w;
     };
     const int G = static_cast<int>(gridDim.x);
+    // Long items (a.claim_lazy): claim one item at a time, the next only
+    // once the one before the current is done, so a CTA never holds more
+    // than two unfinished items -- claiming three ahead let the CTAs that
+    // started early hoard the pool's last long items (C4: their tail ran
+    // ~10 us past the others').
+    const bool lazy = a.claim_lazy != 0 && sched != nullptr;
     int id0 = blockIdx.x, id1 = blockIdx.x + G, id2 = blockIdx.x + 2 * G;
     if (sched != nullptr) {
       int base = 0;
-      if (lane == 0) base = atomicAdd(sched, 3);
+      if (lane == 0) base = atomicAdd(sched, lazy ? 1 : 3);
       base = __shfl_sync(0xffffffffu, base, 0);
       id0 = base;
       id1 = base + 1;
@@ -940,8 +946,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       // claim item j+3 and load item j+1 while this one is published
       int p = id2 + G;
       tr.ev(600000 + item);
-      if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
-      const Raw nxt = load_raw(id1);
+      Raw nxt;
+      if (!lazy) {
+        if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
+        nxt = load_raw(id1);
+      }
       mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
       tr.ev(610000 + item);
       if (item >= n_items) {
@@ -1034,6 +1043,16 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         cp_async_16(smem + SM::kOffQ + (qs * R + (c >> 4)) * kRowBytes + (c & 15) * 16, qp, 16u);
       }
       cp_async_mbar_arrive(&i_full[qs]);
+      if (lazy) {
+        // the next item once item j-1 is done (its slot released)
+        if (j >= 1) mbar_wait(&i_empty[(j - 1) % kIQ], static_cast<uint32_t>(((j - 1) / kIQ) & 1));
+        int pn = 0;
+        if (lane == 0) pn = atomicAdd(sched, 1);
+        pn = __shfl_sync(0xffffffffu, pn, 0);
+        tr.ev(620000 + pn);
+        cur = load_raw(pn);
+        continue;
+      }
       cur = nxt;
       id1 = id2;
       id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;

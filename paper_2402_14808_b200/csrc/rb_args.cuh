@@ -83,6 +83,9 @@ struct CtxArgs {
   // longest context first): items are claimed in this order, so the last
   // claims -- the ones whose queued items make a CTA's tail -- are short
   const int* req_order;
+  // 1: the items are long (>= 16 chunks): claim one item at a time instead of
+  // three ahead (set by the host from the context-length bound)
+  int claim_lazy;
 };
 
 #ifdef __CUDACC__
