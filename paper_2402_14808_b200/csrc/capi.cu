@@ -275,7 +275,10 @@ static int ctx_split_args(rb::CtxArgs& a, int n_rows, int max_rows, int max_ctx_
 #ifndef RB_CLAIM_LAZY
 #define RB_CLAIM_LAZY 1
 #endif
-  a.claim_lazy = RB_CLAIM_LAZY && (max_ctx_len + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK >= 16 ? 1 : 0;
+#ifndef RB_CLAIM_LAZY_MIN
+#define RB_CLAIM_LAZY_MIN 16
+#endif
+  a.claim_lazy = RB_CLAIM_LAZY && (max_ctx_len + RB_CTX_CHUNK - 1) / RB_CTX_CHUNK >= RB_CLAIM_LAZY_MIN ? 1 : 0;
   if (ws == nullptr) return RB_OK;
   int L, ns;
   ctx_split_plan(a.b, a.hkv, max_rows, a.s_prefix, max_ctx_len, device_sms(), &L, &ns);
@@ -286,7 +289,7 @@ static int ctx_split_args(rb::CtxArgs& a, int n_rows, int max_rows, int max_ctx_
   const size_t part = ((size_t)n_rows * a.hq * ns * 132 * 4 + 255) & ~(size_t)255;
   a.split_chunks = L;
   a.n_split = ns;
-  a.claim_lazy = RB_CLAIM_LAZY && L >= 16 ? 1 : 0;
+  a.claim_lazy = RB_CLAIM_LAZY && L >= RB_CLAIM_LAZY_MIN ? 1 : 0;
   a.split_part = static_cast<float*>(ws);
   a.split_cnt = reinterpret_cast<int*>(static_cast<uint8_t*>(ws) + part);
   return RB_OK;

@@ -700,7 +700,10 @@ struct CtxCfg {
 #ifndef RB_CTX_IQ
 #define RB_CTX_IQ 3
 #endif
-constexpr int kIQ = RB_CTX_IQ;                         // item queue depth (claim-ahead bound)
+constexpr int kIQ = RB_CTX_IQ;
+#ifndef RB_CLAIM_LAZY
+#define RB_CLAIM_LAZY 1
+#endif                         // item queue depth (claim-ahead bound)
 constexpr int kCtxThreadsPC = 32 * (2 + kWorkers);  // scheduler + workers + merger
 constexpr int kMergerWarp = 1 + kWorkers;
 constexpr int kPartStride = 132;               // floats per relay context partial: O[128], m, l
@@ -1638,10 +1641,14 @@ static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStre
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R>, kCtxThreadsPC, smem);
   if (e != cudaSuccess) return e;
   const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
+  // fewer than three items per CTA: claiming three at once would leave most
+  // CTAs without work (C1: 128 items, 43 CTAs busy) -- claim one at a time
+  CtxArgs la = a;
+  if (RB_CLAIM_LAZY && n_items < 3 * grid) la.claim_lazy = 1;
   // PDL: the relay step's context kernel starts as soon as the system kernel
   // has triggered (it runs on the SMs the system kernel leaves free); the
   // other modes wait for their predecessor before the first output write.
-  e = launch_pdl(ctx_cta_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, a, n_items, n_z);
+  e = launch_pdl(ctx_cta_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, la, n_items, n_z);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
