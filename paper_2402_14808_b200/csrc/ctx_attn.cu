@@ -840,7 +840,7 @@ struct WarpTrace {
   }
 };
 
-template <int R>
+template <int R, bool LAZY>
 __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
   using SM = CtaSmem<R>;
@@ -931,7 +931,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     // than two unfinished items -- claiming three ahead let the CTAs that
     // started early hoard the pool's last long items (C4: their tail ran
     // ~10 us past the others').
-    const bool lazy = a.claim_lazy != 0 && sched != nullptr;
+    // (a compile-time variant: the lazy loop's code in every kernel cost the
+    // short-item decode steps ~2 us -- instruction footprint)
+    const bool lazy = LAZY && sched != nullptr;
     int id0 = blockIdx.x, id1 = blockIdx.x + G, id2 = blockIdx.x + 2 * G;
     if (sched != nullptr) {
       int base = 0;
@@ -941,30 +943,9 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       id1 = base + 1;
       id2 = base + 2;
     }
-    Raw cur = load_raw(id0);
-    for (int j = 0;; ++j) {
-      const int item = cur.item;
-      const int qs = j % kIQ;
+    // publish item `item` (metadata `cur`) into queue slot qs (the slot is free)
+    auto publish = [&](const Raw& cur, int item, int qs) {
       ItemSlot<R>& slot = iq[qs];
-      // claim item j+3 and load item j+1 while this one is published
-      int p = id2 + G;
-      tr.ev(600000 + item);
-      Raw nxt;
-      if (!lazy) {
-        if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
-        nxt = load_raw(id1);
-      }
-      mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
-      tr.ev(610000 + item);
-      if (item >= n_items) {
-        if (lane == 0) {
-          slot.item = -1;
-          mbar_arrive(&i_meta[qs]);
-        }
-        __syncwarp();
-        mbar_arrive(&i_full[qs]);
-        break;
-      }
       CtxItem<R> it;
       it.bt0 = cur.bt0;
       it.roff = cur.roff;
@@ -1046,20 +1027,56 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         cp_async_16(smem + SM::kOffQ + (qs * R + (c >> 4)) * kRowBytes + (c & 15) * 16, qp, 16u);
       }
       cp_async_mbar_arrive(&i_full[qs]);
-      if (lazy) {
-        // the next item once item j-1 is done (its slot released)
+    };
+    auto publish_end = [&](int qs) {
+      ItemSlot<R>& slot = iq[qs];
+      if (lane == 0) {
+        slot.item = -1;
+        mbar_arrive(&i_meta[qs]);
+      }
+      __syncwarp();
+      mbar_arrive(&i_full[qs]);
+    };
+    if (lazy) {
+      // at most two unfinished items: claim item j+1 once item j-1 is done
+      Raw cur = load_raw(id0);
+      for (int j = 0;; ++j) {
+        const int qs = j % kIQ;
+        mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
+        if (cur.item >= n_items) {
+          publish_end(qs);
+          break;
+        }
+        publish(cur, cur.item, qs);
         if (j >= 1) mbar_wait(&i_empty[(j - 1) % kIQ], static_cast<uint32_t>(((j - 1) / kIQ) & 1));
         int pn = 0;
         if (lane == 0) pn = atomicAdd(sched, 1);
         pn = __shfl_sync(0xffffffffu, pn, 0);
         tr.ev(620000 + pn);
         cur = load_raw(pn);
-        continue;
       }
-      cur = nxt;
-      id1 = id2;
-      id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;
-      tr.ev(620000 + id2);
+    } else {
+      Raw cur = load_raw(id0);
+      for (int j = 0;; ++j) {
+        const int item = cur.item;
+        const int qs = j % kIQ;
+        // claim item j+3 and load item j+1 while this one is published
+        int p = id2 + G;
+        tr.ev(600000 + item);
+        if (sched != nullptr && lane == 0) p = atomicAdd(sched, 1);
+        const Raw nxt = load_raw(id1);
+        mbar_wait(&i_empty[qs], ((j / kIQ) & 1) ^ 1);
+        tr.ev(610000 + item);
+        if (item >= n_items) {
+          publish_end(qs);
+          break;
+        }
+        publish(cur, item, qs);
+        cur = nxt;
+        id1 = id2;
+        id2 = (sched != nullptr) ? __shfl_sync(0xffffffffu, p, 0) : p;
+        tr.ev(620000 + id2);
+      }
     }
     if (sched != nullptr && lane == 0) {
       // every scheduler's last claim precedes its arrival here, so the last
@@ -1636,9 +1653,11 @@ static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStre
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int smem = CtaSmem<R>::kBytes;
-  cudaError_t e = cudaFuncSetAttribute(ctx_cta_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(ctx_cta_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R>, kCtxThreadsPC, smem);
+  e = cudaFuncSetAttribute(ctx_cta_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctx_cta_kernel<R, false>, kCtxThreadsPC, smem);
   if (e != cudaSuccess) return e;
   const int grid = max(1, min(n_items, sms * max(per_sm, 1)));
   // fewer than three items per CTA: claiming three at once would leave most
@@ -1648,7 +1667,9 @@ static cudaError_t launch_ctx_r(const CtxArgs& a, int n_items, int n_z, cudaStre
   // PDL: the relay step's context kernel starts as soon as the system kernel
   // has triggered (it runs on the SMs the system kernel leaves free); the
   // other modes wait for their predecessor before the first output write.
-  e = launch_pdl(ctx_cta_kernel<R>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, la, n_items, n_z);
+  e = la.claim_lazy
+          ? launch_pdl(ctx_cta_kernel<R, true>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, la, n_items, n_z)
+          : launch_pdl(ctx_cta_kernel<R, false>, dim3(grid), dim3(kCtxThreadsPC), smem, stream, la, n_items, n_z);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
