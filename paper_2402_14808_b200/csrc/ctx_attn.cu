@@ -118,11 +118,13 @@ __device__ __forceinline__ void chunk_cp_async_full(uint8_t* slot, const __nv_bf
 __device__ __noinline__ void chunk_cp_async_rows(uint8_t* dst, KvView kv, int r, int t0, int h, int n,
                                                  int lane) {
   const int row0 = lane >> 4, c16 = lane & 15;
+  // (not unrolled: this path is cold and ctx_row divides by the block size)
+#pragma unroll 1
   for (int i = 0; i < 8; ++i) {
     const int row = row0 + 2 * i;
     const bool ok = row < n;
     const __nv_bfloat16* ks = ok ? ctx_row(kv, kv.k, r, t0 + row, h) : kv.k;
-    const __nv_bfloat16* vs = ok ? ctx_row(kv, kv.v, r, t0 + row, h) : kv.v;
+    const __nv_bfloat16* vs = ok ? kv.v + (ks - kv.k) : kv.v;
     const uint32_t so = slot_off(row, c16);
     cp_async_16(dst + so, ks + c16 * 8, ok ? 16u : 0u);
     cp_async_16(dst + kChunk * kRowBytes + so, vs + c16 * 8, ok ? 16u : 0u);
@@ -439,19 +441,21 @@ __device__ __forceinline__ float relay_fold(float o, float so, float a, float sk
   return __fmaf_rn(o, so, __fmul_rn(a, sk));
 }
 
+template <int B>
 struct RelayParts {
   long long base;
   int np, col;
-  float mk[kRB], lk[kRB];
-  float4 ak[kRB];
+  float mk[B], lk[B];
+  float4 ak[B];
 };
 
+template <int B>
 __device__ __forceinline__ void relay_parts_load(const rb_sys_plan& SP, const float* part_acc,
                                                  const float* part_ml, long long base, int np,
                                                  int col, int k0, int lane, float* mk, float* lk,
                                                  float4* ak) {
 #pragma unroll
-  for (int kk = 0; kk < kRB; ++kk) {
+  for (int kk = 0; kk < B; ++kk) {
     const int k = min(k0 + kk, np - 1);
     const float* pml = part_ml + (base + k) * 2 * SP.nq;
     mk[kk] = __ldcg(pml + col);
@@ -460,10 +464,11 @@ __device__ __forceinline__ void relay_parts_load(const rb_sys_plan& SP, const fl
   }
 }
 
-__device__ __forceinline__ RelayParts relay_parts_begin(const rb_sys_plan& SP, int hq, long long pair,
-                                                        const float* part_acc, const float* part_ml,
-                                                        int lane) {
-  RelayParts P;
+template <int B>
+__device__ __forceinline__ RelayParts<B> relay_parts_begin(const rb_sys_plan& SP, int hq, long long pair,
+                                                           const float* part_acc, const float* part_ml,
+                                                           int lane) {
+  RelayParts<B> P;
   const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
   const int f = row * SP.g + hh % SP.g;
   const int qt = f / SP.nq;
@@ -471,19 +476,20 @@ __device__ __forceinline__ RelayParts relay_parts_begin(const rb_sys_plan& SP, i
   const int u = (hh / SP.g) * SP.n_qt + qt;
   P.np = rb_unit_parts(&SP, u);
   P.base = static_cast<long long>(u) * SP.max_parts;
-  relay_parts_load(SP, part_acc, part_ml, P.base, P.np, P.col, 0, lane, P.mk, P.lk, P.ak);
+  relay_parts_load<B>(SP, part_acc, part_ml, P.base, P.np, P.col, 0, lane, P.mk, P.lk, P.ak);
   return P;
 }
 
-__device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayParts& P, long long pair,
+template <int B>
+__device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayParts<B>& P, long long pair,
                                                   const float* part_acc, const float* part_ml,
                                                   float4 O, float mt, float lt, void* out, int out_fp32,
                                                   float* lse_out, int lane) {
   const int d0 = lane * 4;
-  for (int k0 = 0; k0 < P.np; k0 += kRB) {
-    if (k0 > 0) relay_parts_load(SP, part_acc, part_ml, P.base, P.np, P.col, k0, lane, P.mk, P.lk, P.ak);
+  for (int k0 = 0; k0 < P.np; k0 += B) {
+    if (k0 > 0) relay_parts_load<B>(SP, part_acc, part_ml, P.base, P.np, P.col, k0, lane, P.mk, P.lk, P.ak);
 #pragma unroll
-    for (int kk = 0; kk < kRB; ++kk) {
+    for (int kk = 0; kk < B; ++kk) {
       if (k0 + kk >= P.np) break;
       const float mn = fmaxf(mt, P.mk[kk]);
       const float so = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
@@ -509,12 +515,13 @@ __device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayPa
   if (lse_out != nullptr && lane == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
 }
 
+template <int B>
 __device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, long long pair,
                                                 const float* part_acc, const float* part_ml,
                                                 float4 O, float mt, float lt, void* out, int out_fp32,
                                                 float* lse_out, int lane) {
-  RelayParts P = relay_parts_begin(SP, hq, pair, part_acc, part_ml, lane);
-  relay_fuse_finish(SP, P, pair, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
+  RelayParts<B> P = relay_parts_begin<B>(SP, hq, pair, part_acc, part_ml, lane);
+  relay_fuse_finish<B>(SP, P, pair, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
 }
 
 // Relay fusion of all R rows of an item at once, when they share one published
@@ -845,6 +852,10 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     ctx_cta_kernel(const CtxArgs a, int n_items, int n_z) {
   using SM = CtaSmem<R>;
   constexpr int kDepth = SM::kDepth, kNB = SM::kNB;
+  // relay fusion: system parts per batch of loads (C4's 6-part units with
+  // 4-row items want 8; the 1-2-row items of C2 / C3 see <= 4 parts, and the
+  // smaller batch keeps the merger's per-item code short)
+  constexpr int kRBr = R >= 4 ? kRB : (kRB < 4 ? kRB : 4);
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_pre = (a.s_prefix + kChunk - 1) / kChunk;
@@ -1118,16 +1129,16 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     const int d0 = lane * 4;
     int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
     // the last step of a (row, head): relay fusion / park, or output
-    auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts& pp) {
+    auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts<kRBr>& pp) {
       if (a.ctx_part != nullptr) {
         const bool full = defer[0] >= SM::kMaxDefer;
         if (use_pre) {
-          relay_fuse_finish(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
+          relay_fuse_finish<kRBr>(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
                             a.out_fp32, a.lse_out, lane);
         } else if (poll ? (relay_unit_published(a.sys_plan, a.hq, oidx, pub) ||
                            (full && relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, true)))
                         : relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
-          relay_fuse_pair(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
+          relay_fuse_pair<kRBr>(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
                           a.out_fp32, a.lse_out, lane);
         } else {
           float* dst = a.ctx_part + oidx * kPartStride;
@@ -1194,7 +1205,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       // relay: if row 0's system unit is already published, issue its
       // parts' loads now so they land while the workers finish the item
       bool pre = false;
-      RelayParts pp;
+      RelayParts<kRBr> pp;
       if (poll) {
         // fold in the previous poll, then issue the next one
 #pragma unroll
@@ -1210,7 +1221,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
                              it.h * a.g + (it.z * R) % a.g;
         pre = poll ? relay_unit_published(a.sys_plan, a.hq, o0, pub)
                    : relay_unit_ready(a.sys_plan, a.hq, o0, a.sys_ready, lane, false);
-        if (pre) pp = relay_parts_begin(a.sys_plan, a.hq, o0, a.sys_part_acc, a.sys_part_ml, lane);
+        if (pre) pp = relay_parts_begin<kRBr>(a.sys_plan, a.hq, o0, a.sys_part_acc, a.sys_part_ml, lane);
       }
       if (!waited && a.ctx_part == nullptr) {
         // before the first output write / o_sys read: the previous grid (a
