@@ -96,7 +96,17 @@ int rb_sys_plan_query(int n_rows, int hq, int hkv, int s, int grid_cap, long lon
                 "relay attention requires a non-empty system segment; use the baseline path "
                 "when there is no shared prefix");
   rb_sys_plan p;
+  {
+    // the stream-K index math is 32-bit (rb_plan.h): bound total x grid
+    const long long total = (long long)hkv * ((long long)n_rows * (hq / hkv) + 15) / 16 *
+                            (((long long)s + RB_KEY_TILE - 1) / RB_KEY_TILE);
+    if (total * (grid_cap < 1 ? 1 : grid_cap) > RB_PLAN_MAX_PRODUCT || (long long)n_rows * hq > 0x7fffffffLL)
+      return fail(RB_ERR_DIMENSION, "problem too large for one stream-K plan (%d rows x %d heads, s=%d)",
+                  n_rows, hq, s);
+  }
   rb_make_sys_plan(&p, n_rows, hq, hkv, s, grid_cap);
+  if ((long long)p.total * p.grid > RB_PLAN_MAX_PRODUCT)
+    return fail(RB_ERR_DIMENSION, "problem too large for one stream-K plan");
   if (fields) {
     fields[0] = p.nq;
     fields[1] = p.n_qt;

@@ -39,12 +39,19 @@ typedef struct {
   int rr;             // 1: whole units dealt round-robin (CTA c: units c, c+grid, ...)
 } rb_sys_plan;
 
+// The stream-K index math runs in 32-bit unsigned arithmetic: plans keep
+// total * grid < 2^32 (RB_PLAN_MAX_PRODUCT; rb_sys_plan_query rejects larger
+// ones -- e.g. 64 units x 8192 key tiles x 148 CTAs is 7.8e7).  The 64-bit
+// divisions it replaces were ~1400 instructions of the context kernel's code
+// (inlined at every relay site), whose per-item path is sensitive to its
+// instruction footprint.
+#define RB_PLAN_MAX_PRODUCT 4294967295LL
 RB_HD long long rb_cta_begin(const rb_sys_plan* p, int c) {
-  return (long long)c * p->total / p->grid;
+  return (long long)(((unsigned)c * (unsigned)p->total) / (unsigned)p->grid);
 }
 // CTA owning global tile x (stream-K mode).
 RB_HD int rb_tile_owner(const rb_sys_plan* p, long long x) {
-  return (int)(((x + 1) * (long long)p->grid - 1) / p->total);
+  return (int)(((unsigned)(x + 1) * (unsigned)p->grid - 1u) / (unsigned)p->total);
 }
 RB_HD int rb_unit_parts(const rb_sys_plan* p, int u) {
   if (p->rr) return 1;
@@ -67,7 +74,7 @@ RB_HD void rb_cta_range(const rb_sys_plan* p, int c, long long* b, long long* e)
 }
 // Unit of tile i of CTA c (i from rb_cta_range).
 RB_HD int rb_tile_unit(const rb_sys_plan* p, int c, long long i) {
-  return p->rr ? c + (int)(i / p->tpu) * p->grid : (int)(i / p->tpu);
+  return p->rr ? c + (int)((unsigned)i / (unsigned)p->tpu) * p->grid : (int)((unsigned)i / (unsigned)p->tpu);
 }
 // First CTA holding a part of unit u (its part slot is 0).
 RB_HD int rb_unit_owner0(const rb_sys_plan* p, int u) {
