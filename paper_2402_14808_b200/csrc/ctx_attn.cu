@@ -464,16 +464,21 @@ __device__ __forceinline__ void relay_parts_load(const rb_sys_plan& SP, const fl
   }
 }
 
+// A (row, head) pair of the relay step: output index, its system unit and
+// its row within the unit (from the item geometry, no runtime divisions by
+// hq / nq -- they were a few hundred instructions on the merger's per-row path)
+struct RowRef {
+  long long oidx;
+  int u, col;
+};
+
 template <int B>
-__device__ __forceinline__ RelayParts<B> relay_parts_begin(const rb_sys_plan& SP, int hq, long long pair,
+__device__ __forceinline__ RelayParts<B> relay_parts_begin(const rb_sys_plan& SP, const RowRef& rr,
                                                            const float* part_acc, const float* part_ml,
                                                            int lane) {
   RelayParts<B> P;
-  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
-  const int f = row * SP.g + hh % SP.g;
-  const int qt = f / SP.nq;
-  P.col = f % SP.nq;
-  const int u = (hh / SP.g) * SP.n_qt + qt;
+  P.col = rr.col;
+  const int u = rr.u;
   P.np = rb_unit_parts(&SP, u);
   P.base = static_cast<long long>(u) * SP.max_parts;
   relay_parts_load<B>(SP, part_acc, part_ml, P.base, P.np, P.col, 0, lane, P.mk, P.lk, P.ak);
@@ -516,12 +521,12 @@ __device__ __forceinline__ void relay_fuse_finish(const rb_sys_plan& SP, RelayPa
 }
 
 template <int B>
-__device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, int hq, long long pair,
+__device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, const RowRef& rr,
                                                 const float* part_acc, const float* part_ml,
                                                 float4 O, float mt, float lt, void* out, int out_fp32,
                                                 float* lse_out, int lane) {
-  RelayParts<B> P = relay_parts_begin<B>(SP, hq, pair, part_acc, part_ml, lane);
-  relay_fuse_finish<B>(SP, P, pair, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
+  RelayParts<B> P = relay_parts_begin<B>(SP, rr, part_acc, part_ml, lane);
+  relay_fuse_finish<B>(SP, P, rr.oidx, part_acc, part_ml, O, mt, lt, out, out_fp32, lse_out, lane);
 }
 
 // Relay fusion of all R rows of an item at once, when they share one published
@@ -620,13 +625,10 @@ __device__ __forceinline__ void relay_fuse_rows(const rb_sys_plan& SP, int hq, l
   if (lse_out != nullptr && li == 0) lse_out[pair] = (mt + __log2f(lt)) * kLn2;
 }
 
-// Is the system unit of `pair` published (all its parts written)?  Lane 0
-// probes with acquire semantics; the answer is broadcast to the warp.
-__device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int hq, long long pair,
-                                                 const int* ready, int lane, bool block) {
-  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
-  const int f = row * SP.g + hh % SP.g;
-  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
+// Is system unit u published (all its parts written)?  Lane 0 probes with
+// acquire semantics; the answer is broadcast to the warp.
+__device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int u, const int* ready, int lane,
+                                                 bool block) {
   if (u >= SP.n_units) return false;  // outside the plan (bad q_start): parked, then dropped
   const int np = rb_unit_parts(&SP, u);
   int ok = 1;
@@ -649,11 +651,7 @@ __device__ __forceinline__ int relay_unit_of(const rb_sys_plan& SP, int hq, long
   const int f = row * SP.g + hh % SP.g;
   return (hh / SP.g) * SP.n_qt + f / SP.nq;
 }
-__device__ __forceinline__ bool relay_unit_published(const rb_sys_plan& SP, int hq, long long pair,
-                                                     uint32_t pub) {
-  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
-  const int f = row * SP.g + hh % SP.g;
-  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
+__device__ __forceinline__ bool relay_unit_published(int u, uint32_t pub) {
   const uint32_t bits = __shfl_sync(0xffffffffu, pub, u & 31);
   return u < 32 * kPollSlots && ((bits >> (u >> 5)) & 1);
 }
@@ -1128,17 +1126,31 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
     }
     const int d0 = lane * 4;
     int* defer = reinterpret_cast<int*>(smem + SM::kOffDefer);
+    // (row, head) pair of item row li (rows of an item: request row0 + li / g,
+    // group member li % g); system units are power-of-two row tiles
+    const int nq_sh = __ffs(a.sys_plan.nq) - 1;
+    auto item_row_ref = [&](const CtxItem<R>& itm, int li) -> RowRef {
+      const int t = a.g == 1 ? li : li / a.g, jj = li - t * a.g;
+      const int row = itm.row0 + t;
+      const int f = row * a.g + jj;
+      RowRef rr;
+      rr.oidx = static_cast<long long>(row) * a.hq + itm.h * a.g + jj;
+      rr.u = itm.h * a.sys_plan.n_qt + (f >> nq_sh);
+      rr.col = f & (a.sys_plan.nq - 1);
+      return rr;
+    };
     // the last step of a (row, head): relay fusion / park, or output
-    auto finish = [&](float4 O, float M, float Ls, long long oidx, bool use_pre, RelayParts<kRBr>& pp) {
+    auto finish = [&](float4 O, float M, float Ls, const RowRef& rr, bool use_pre, RelayParts<kRBr>& pp) {
+      const long long oidx = rr.oidx;
       if (a.ctx_part != nullptr) {
         const bool full = defer[0] >= SM::kMaxDefer;
         if (use_pre) {
           relay_fuse_finish<kRBr>(a.sys_plan, pp, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
                             a.out_fp32, a.lse_out, lane);
-        } else if (poll ? (relay_unit_published(a.sys_plan, a.hq, oidx, pub) ||
-                           (full && relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, true)))
-                        : relay_unit_ready(a.sys_plan, a.hq, oidx, a.sys_ready, lane, full)) {
-          relay_fuse_pair<kRBr>(a.sys_plan, a.hq, oidx, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
+        } else if (poll ? (relay_unit_published(rr.u, pub) ||
+                           (full && relay_unit_ready(a.sys_plan, rr.u, a.sys_ready, lane, true)))
+                        : relay_unit_ready(a.sys_plan, rr.u, a.sys_ready, lane, full)) {
+          relay_fuse_pair<kRBr>(a.sys_plan, rr, a.sys_part_acc, a.sys_part_ml, O, M, Ls, a.out,
                           a.out_fp32, a.lse_out, lane);
         } else {
           float* dst = a.ctx_part + oidx * kPartStride;
@@ -1217,11 +1229,10 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
           if (np[k] != 0x7fffffff && !((pub >> k) & 1)) pv[k] = ld_acquire_gpu(a.sys_ready + lane + 32 * k);
       }
       if (a.ctx_part != nullptr && !split && it.z * R < it.nrows) {
-        const long long o0 = static_cast<long long>(it.row0 + (it.z * R) / a.g) * a.hq +
-                             it.h * a.g + (it.z * R) % a.g;
-        pre = poll ? relay_unit_published(a.sys_plan, a.hq, o0, pub)
-                   : relay_unit_ready(a.sys_plan, a.hq, o0, a.sys_ready, lane, false);
-        if (pre) pp = relay_parts_begin<kRBr>(a.sys_plan, a.hq, o0, a.sys_part_acc, a.sys_part_ml, lane);
+        const RowRef r0 = item_row_ref(it, it.z * R);
+        pre = poll ? relay_unit_published(r0.u, pub)
+                   : relay_unit_ready(a.sys_plan, r0.u, a.sys_ready, lane, false);
+        if (pre) pp = relay_parts_begin<kRBr>(a.sys_plan, r0, a.sys_part_acc, a.sys_part_ml, lane);
       }
       if (!waited && a.ctx_part == nullptr) {
         // before the first output write / o_sys read: the previous grid (a
@@ -1255,7 +1266,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       if (RB_RELAY_GROUPED && R > 1 && !split && poll && nrow == R) {
         const long long o0 = row_oidx(0), o1 = row_oidx(R - 1);
         grouped = relay_unit_of(a.sys_plan, a.hq, o0) == relay_unit_of(a.sys_plan, a.hq, o1) &&
-                  relay_unit_published(a.sys_plan, a.hq, o0, pub);
+                  relay_unit_published(relay_unit_of(a.sys_plan, a.hq, o0), pub);
       }
       if (grouped)
         relay_fuse_rows<R>(a.sys_plan, a.hq, row_oidx(lane / (32 / R)), bacc, bml, a.sys_part_acc,
@@ -1286,7 +1297,7 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
           __stcg(reinterpret_cast<float4*>(dst + d0), O);
           if (lane == 0) __stcg(reinterpret_cast<float2*>(dst + 128), make_float2(M, Ls));
         } else {
-          finish(O, M, Ls, oidx, i == 0 && pre, pp);
+          finish(O, M, Ls, item_row_ref(it, rbase + i), i == 0 && pre, pp);
         }
       }
       __syncwarp();
@@ -1365,7 +1376,8 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
 #pragma unroll 1
             for (int i = 0; i < nrow; ++i) {
               const float4 O = *reinterpret_cast<const float4*>(comb + i * kAccStride + d0);
-              finish(O, comb[i * kAccStride + 128], comb[i * kAccStride + 129], row_oidx(i), false, pp);
+              finish(O, comb[i * kAccStride + 128], comb[i * kAccStride + 129], item_row_ref(it, rbase + i), false,
+                     pp);
             }
           }
           __syncwarp();
