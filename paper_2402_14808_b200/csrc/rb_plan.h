@@ -37,6 +37,7 @@ typedef struct {
   int grid;           // CTAs launched
   int max_parts;      // max partial slots over all units
   int rr;             // 1: whole units dealt round-robin (CTA c: units c, c+grid, ...)
+  unsigned long long total_magic;  // ceil(2^64 / total) (0 when total == 1): owner by multiply-high
 } rb_sys_plan;
 
 // The stream-K index math runs in 32-bit unsigned arithmetic: plans keep
@@ -49,9 +50,17 @@ typedef struct {
 RB_HD long long rb_cta_begin(const rb_sys_plan* p, int c) {
   return (long long)(((unsigned)c * (unsigned)p->total) / (unsigned)p->grid);
 }
-// CTA owning global tile x (stream-K mode).
+// CTA owning global tile x (stream-K mode): floor(((x + 1) grid - 1) / total)
+// -- on the device as a multiply-high by ceil(2^64 / total), exact for
+// numerators below 2^32 (the relay sites inline it several times; a 32-bit
+// division is ~20 instructions, this is ~4)
 RB_HD int rb_tile_owner(const rb_sys_plan* p, long long x) {
-  return (int)(((unsigned)(x + 1) * (unsigned)p->grid - 1u) / (unsigned)p->total);
+  const unsigned n = (unsigned)(x + 1) * (unsigned)p->grid - 1u;
+#ifdef __CUDA_ARCH__
+  return p->total_magic ? (int)__umul64hi((unsigned long long)n, p->total_magic) : (int)n;
+#else
+  return (int)(n / (unsigned)p->total);
+#endif
 }
 RB_HD int rb_unit_parts(const rb_sys_plan* p, int u) {
   if (p->rr) return 1;
@@ -104,6 +113,7 @@ RB_HD void rb_make_sys_plan(rb_sys_plan* p, int n_rows, int hq, int hkv, int s,
   p->tpu = (s + RB_KEY_TILE - 1) / RB_KEY_TILE;
   p->n_units = hkv * p->n_qt;
   p->total = (long long)p->n_units * p->tpu;
+  p->total_magic = p->total > 1 ? ~0ULL / (unsigned long long)p->total + 1ULL : 0ULL;
   long long gcap = grid_cap < 1 ? 1 : grid_cap;
   // Several query tiles per KV head (large GQA batches): deal whole units
   // round-robin, so the CTAs working on a head's query tiles at the same
