@@ -669,8 +669,10 @@ template <int R>
 #ifndef RB_CTX_MINB
 #define RB_CTX_MINB 2   /* resident CTAs per SM the register budget is sized for */
 #endif
+// 1-row items (C2 / C3 decode): 2 chunks in flight per worker -- with the
+// smaller kernel, C2 s=2048 47.0 -> 45.1 us, s=1024 40.9 -> 38.9 us against 3
 #ifndef RB_CTX_DEPTH1
-#define RB_CTX_DEPTH1 3
+#define RB_CTX_DEPTH1 2
 #endif
 // chunks in flight per worker for 4- and 8-row items (C4 / C5 GQA shapes):
 // measured C4 step 110.3 us at depth 3, 104.8 at 2, 136 at 1; C5 with the
