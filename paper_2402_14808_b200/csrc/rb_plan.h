@@ -171,6 +171,15 @@ RB_HD int rb_relay_split(int n_rows, int hq, int hkv, int s, long long ctx_token
   lf = lf < 0.0 ? 0.0 : (lf > 1.0 ? 1.0 : lf);
   const double ratio = RB_RELAY_RATE_RATIO / (1.0 + 0.39 * lf);
   int g = (int)(sms * sys_bytes / (sys_bytes + ratio * ctx_bytes) + 0.5);
+  // 8-24 key tiles per system CTA: its fixed per-CTA cost (first S,
+  // epilogues) weighs on its rate, so it gets a larger share (C2 s = 2048:
+  // 41 -> 48 CTAs, 45.1 -> 43.0 us measured by profiles/sweep_split.py;
+  // s = 4096 and up keep the byte balance; below 8 tiles per CTA -- C1 --
+  // more CTAs measured no better)
+  if (g > 0 && (double)p.total / g < 24.0 && (double)p.total / g >= 8.0) {
+    const double r2 = 0.8 * ratio;
+    g = (int)(sms * sys_bytes / (sys_bytes + r2 * ctx_bytes) + 0.5);
+  }
   if (p.nq == 256 && p.n_units <= sms) {
     // the 256-row GQA kernel is tensor-bound: balance measured time, not
     // bytes -- RB_GQA2_TILE_US per key tile per CTA against the context
