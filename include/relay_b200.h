@@ -148,7 +148,8 @@ int rb_context_attention(const void* q, long long q_row_stride, long long q_head
  * first copied into a staging region of the workspace by one small kernel
  * (both kernels then read device memory; the system kernel's K/V prefetch
  * overlaps the copy), and output rows are written to host memory directly.
- * req_order (optional, int32 [b], a permutation of 0..b-1): the order in which
+ * req_order (optional, int32 [b], a permutation of 0..b-1; an entry out of range falls
+ * back to its own position): the order in which
  * the context kernel claims the requests' work -- longest context first
  * keeps the last claims short when the contexts vary (each CTA claims a few
  * items ahead, and a long queued item at the end is a tail).  Results do not

@@ -917,7 +917,13 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       w.qs0 = w.qs1 = w.clen = w.bte = w.bt0 = 0;
       w.roff = 0;
       if (item < n_items) {
-        const int r = a.req_order != nullptr ? __ldg(a.req_order + item / per_req) : item / per_req;
+        int r = item / per_req;
+        if (a.req_order != nullptr) {
+          // a permutation of the requests (an out-of-range entry falls back to
+          // the position itself: never an out-of-bounds read)
+          const int ro = __ldg(a.req_order + r);
+          r = static_cast<unsigned>(ro) < static_cast<unsigned>(a.b) ? ro : r;
+        }
         const int sp = item % n_split;
         w.qs0 = __ldg(a.q_start + r);
         w.qs1 = __ldg(a.q_start + r + 1);
@@ -967,7 +973,10 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
         it.z = grp % n_z;
         it.h = (grp / n_z) % a.hkv;
         it.r = grp / (n_z * a.hkv);
-        if (a.req_order != nullptr) it.r = __ldg(a.req_order + it.r);
+        if (a.req_order != nullptr) {
+          const int ro = __ldg(a.req_order + it.r);
+          it.r = static_cast<unsigned>(ro) < static_cast<unsigned>(a.b) ? ro : it.r;
+        }
         it.row0 = cur.qs0;
         it.m_r = cur.qs1 - cur.qs0;
         it.nrows = it.m_r * a.g;
