@@ -52,3 +52,25 @@ def test_error_mapping_without_gpu():
         _lib.sys_plan(4, 2, 2, 0, 148)          # empty system segment
     with pytest.raises(DimensionError):
         _lib.sys_plan(4, 3, 2, 16, 148)         # hq not a multiple of hkv
+
+
+def test_plan_size_bound_and_owner_math():
+    """The stream-K index math is 32-bit (rb_plan.h: total x grid < 2^32,
+    larger plans rejected) and the device finds a tile's owner by a
+    multiply-high with ceil(2^64 / total): restated here and checked against
+    the exact division over the edge cases of the bound."""
+    import pytest
+    from paper_2402_14808_b200 import _lib
+    from paper_2402_14808_b200.errors import DimensionError
+    with pytest.raises(DimensionError):
+        _lib.sys_plan(4096, 64, 64, 1 << 22, 148)   # 64 heads x 4.2M keys x 148 CTAs
+    fields, _ = _lib.sys_plan(256, 64, 8, 65536, 148)
+    assert fields["total"] * fields["grid"] < 1 << 32
+    for total in (2, 3, 7, 127, 4096, 32768, 33554431, (1 << 32) // 148):
+        magic = (2 ** 64 - 1) // total + 1
+        for grid in (1, 90, 148):
+            for x in (0, 1, total // 3, total - 2, total - 1):
+                n = (x + 1) * grid - 1
+                if n >= 1 << 32:
+                    continue
+                assert (n * magic) >> 64 == n // total, (total, grid, x)
