@@ -539,7 +539,7 @@ __device__ __forceinline__ void relay_fuse_pair(const rb_sys_plan& SP, const Row
 // per-row fusion made the merger the bottleneck once the system units were
 // published).  Same arithmetic per element as relay_fuse_finish.
 template <int R>
-__device__ __forceinline__ void relay_fuse_rows(const rb_sys_plan& SP, int hq, long long pair,
+__device__ __forceinline__ void relay_fuse_rows(const rb_sys_plan& SP, const RowRef& rr,
                                                 const float* bacc, const float* bml,
                                                 const float* part_acc, const float* part_ml,
                                                 void* out, int out_fp32, float* lse_out, int lane) {
@@ -569,10 +569,8 @@ __device__ __forceinline__ void relay_fuse_rows(const rb_sys_plan& SP, int hq, l
       }
     }
   }
-  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
-  const int f = row * SP.g + hh % SP.g;
-  const int col = f % SP.nq;
-  const int u = (hh / SP.g) * SP.n_qt + f / SP.nq;
+  const long long pair = rr.oidx;
+  const int col = rr.col, u = rr.u;
   const int np = rb_unit_parts(&SP, u);
   const long long base = static_cast<long long>(u) * SP.max_parts;
   float mt = M, lt = Ls;
@@ -646,11 +644,6 @@ __device__ __forceinline__ bool relay_unit_ready(const rb_sys_plan& SP, int u, c
 // Published-unit bitmask of the merger's background poll: lane l holds bit
 // k for unit l + 32 k (k < kPollSlots); warp-uniform call.
 constexpr int kPollSlots = 8;   // polls up to 256 system units
-__device__ __forceinline__ int relay_unit_of(const rb_sys_plan& SP, int hq, long long pair) {
-  const int row = static_cast<int>(pair) / hq, hh = static_cast<int>(pair) % hq;
-  const int f = row * SP.g + hh % SP.g;
-  return (hh / SP.g) * SP.n_qt + f / SP.nq;
-}
 __device__ __forceinline__ bool relay_unit_published(int u, uint32_t pub) {
   const uint32_t bits = __shfl_sync(0xffffffffu, pub, u & 31);
   return u < 32 * kPollSlots && ((bits >> (u >> 5)) & 1);
@@ -1275,12 +1268,11 @@ __global__ void __launch_bounds__(kCtxThreadsPC, RB_CTX_MINB)
       // all rows of the item in one published system unit: grouped fusion
       bool grouped = false;
       if (RB_RELAY_GROUPED && R > 1 && !split && poll && nrow == R) {
-        const long long o0 = row_oidx(0), o1 = row_oidx(R - 1);
-        grouped = relay_unit_of(a.sys_plan, a.hq, o0) == relay_unit_of(a.sys_plan, a.hq, o1) &&
-                  relay_unit_published(relay_unit_of(a.sys_plan, a.hq, o0), pub);
+        const int u0 = item_row_ref(it, rbase).u;
+        grouped = u0 == item_row_ref(it, rbase + R - 1).u && relay_unit_published(u0, pub);
       }
       if (grouped)
-        relay_fuse_rows<R>(a.sys_plan, a.hq, row_oidx(lane / (32 / R)), bacc, bml, a.sys_part_acc,
+        relay_fuse_rows<R>(a.sys_plan, item_row_ref(it, rbase + lane / (32 / R)), bacc, bml, a.sys_part_acc,
                            a.sys_part_ml, a.out, a.out_fp32, a.lse_out, lane);
 #pragma unroll 1
       for (int i = 0; i < (grouped ? 0 : nrow); ++i) {
