@@ -173,7 +173,10 @@ static void maybe_q_map(CUtensorMap* map, rb::SysArgs* a, const void* q, int n_r
   a->q_tma = 0;
   std::memset(map, 0, sizeof(*map));
   const int g = hq / hkv;
-  if (a->plan.nq != 256 || 128 % g != 0) return;
+  // query tile rows per TMA box pair: the 256-row kernel loads two 128-row
+  // tiles, the swap-AB kernels one nq-row tile; the 128-row kernel has no map
+  const int tile_rows = a->plan.nq == 256 ? 128 : a->plan.nq;
+  if (a->plan.nq == 128 || tile_rows % g != 0) return;
   cudaPointerAttributes attr;
   if (cudaPointerGetAttributes(&attr, q) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
     cudaGetLastError();
@@ -183,7 +186,7 @@ static void maybe_q_map(CUtensorMap* map, rb::SysArgs* a, const void* q, int n_r
   if (!enc) return;
   cuuint64_t dims[3] = {RB_HEAD_DIM, (cuuint64_t)hq, (cuuint64_t)n_rows};
   cuuint64_t strides[2] = {(cuuint64_t)(a->q_head_stride * 2), (cuuint64_t)(a->q_row_stride * 2)};
-  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(128 / g)};
+  cuuint32_t box[3] = {64, (cuuint32_t)g, (cuuint32_t)(tile_rows / g)};
   cuuint32_t estr[3] = {1, 1, 1};
   if (enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -158,7 +158,8 @@ struct SysTrace {
 template <int NQ>
 __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     sys_attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
-                          const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
+                          const __grid_constant__ CUtensorMap tmap_v,
+                          const __grid_constant__ CUtensorMap tmap_q, const SysArgs args) {
   using L = SysCfg<NQ>;
   constexpr int H = L::H;
   constexpr int KS = L::KS, VS = L::VS;
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
     if ((smem_u32(smem) & 1023) != 0) __trap();  // SW128 tiles need 1 KB alignment
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
+    if (args.q_tma) tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -273,12 +275,24 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
         const int qb = uq & 1;
         mbar_wait(&q_empty[qb], ((uq >> 1) & 1) ^ 1);
         uint8_t* qdst = smem + L::kOffQ + qb * L::kQBytes;
-        // all of the tile's 16-byte chunks in flight at once (zero-fill past the rows)
-        load_unit_q<NQ, NQ>(qdst, args, h, qt * NQ, lane);
-        cp_async_wait_all();
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&q_full[qb]);
+        if (args.q_tma) {
+          // q in device memory, g | NQ: two TMA boxes of (64 d, g heads, NQ / g
+          // requests) = the unit's K-major SW128 tile (rows past the batch
+          // zero-filled)
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&q_full[qb], L::kQBytes);
+            tma_load_3d(qdst, &tmap_q, &q_full[qb], 0, h * P.g, qt * NQ / P.g, pol);
+            tma_load_3d(qdst + NQ * 128, &tmap_q, &q_full[qb], 64, h * P.g, qt * NQ / P.g, pol);
+          }
+          __syncwarp();
+        } else {
+          // all of the tile's 16-byte chunks in flight at once (zero-fill past the rows)
+          load_unit_q<NQ, NQ>(qdst, args, h, qt * NQ, lane);
+          cp_async_wait_all();
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&q_full[qb]);
+        }
         if (dtx && lane == 0 && uq == 0) dtx[2] = global_timer_ns();
         ++uq;
       }
@@ -645,15 +659,15 @@ __global__ void __launch_bounds__(SysCfg<NQ>::kThreads, 1)
 // ------------------------------------------------------------------- host
 
 template <int NQ>
-static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, const SysArgs& a,
-                              cudaStream_t stream) {
+static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tq,
+                              const SysArgs& a, cudaStream_t stream) {
   using L = SysCfg<NQ>;
   static_assert(L::kBytes <= 232448, "system kernel shared memory over the 227 KB limit");
   static_assert(L::kThreads <= 1024, "too many warps");
   auto kern = sys_attn_sm100_kernel<NQ>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, dim3(a.plan.grid), dim3(L::kThreads), L::kBytes, stream, tk, tv, a);
+  e = launch_pdl(kern, dim3(a.plan.grid), dim3(L::kThreads), L::kBytes, stream, tk, tv, tq, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -737,8 +751,8 @@ cudaError_t launch_sys_merge_parts(const SysArgs& a, cudaStream_t stream) {
 cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv,
                                     const CUtensorMap& tq, const SysArgs& a, cudaStream_t stream) {
   switch (a.plan.nq) {
-    case 16: return launch_sys<16>(tk, tv, a, stream);
-    case 32: return launch_sys<32>(tk, tv, a, stream);
+    case 16: return launch_sys<16>(tk, tv, tq, a, stream);
+    case 32: return launch_sys<32>(tk, tv, tq, a, stream);
     case 128: return launch_system_attention_gqa(tk, tv, a, stream);
     case 256: return launch_system_attention_gqa2(tk, tv, tq, a, stream);
     default: return cudaErrorInvalidValue;
