@@ -163,3 +163,23 @@ def test_claim_order_does_not_change_results(oracle, b, hq, hkv, s):
     pairs = [(r, h) for r in (0, b // 2, b - 1) for h in (0, hkv - 1)]
     check_sampled_pairs(oracle, out_o.float(), lse_o, q, sys_cache, paged, 0, pairs, hq // hkv,
                         f"claim order b={b} g={hq // hkv}")
+
+
+@pytest.mark.parametrize("b,hq,hkv,s", [(8, 12, 4, 300), (6, 32, 8, 700)])
+def test_swap_ab_query_loaders(oracle, b, hq, hkv, s):
+    """Query rows of the swap-AB system kernels: by TMA when g divides the
+    unit's rows (g = 4 here), by the cp.async loader otherwise (g = 3); the
+    step equals the oracle either way and host q (staged) equals device q."""
+    from paper_2402_14808_b200.attention import RelayDecodeStep
+    lens = [1 + (11 * r) % 70 for r in range(b)]
+    q, sys_cache, paged, bt, cl = synth_paged_problem(b, hq, hkv, s, lens, seed=b + s + hq)
+    step = RelayDecodeStep(sys_cache, paged, bt, cl, hq)
+    assert step.plan["nq"] in (16, 32), step.plan
+    ref = step(q)[0].clone()
+    lse_ref = step.lse.clone()
+    step._launch(q.cpu().pin_memory(), 3)
+    torch.cuda.synchronize()
+    assert torch.equal(step.out, ref) and torch.equal(step.lse, lse_ref)
+    pairs = [(r, h) for r in (0, b - 1) for h in (0, hkv - 1)]
+    check_sampled_pairs(oracle, ref.float(), lse_ref, q, sys_cache, paged, 0, pairs, hq // hkv,
+                        f"swap-AB loaders b={b} g={hq // hkv}")
