@@ -174,9 +174,9 @@ static void maybe_q_map(CUtensorMap* map, rb::SysArgs* a, const void* q, int n_r
   std::memset(map, 0, sizeof(*map));
   const int g = hq / hkv;
   // query tile rows per TMA box pair: the 256-row kernel loads two 128-row
-  // tiles, the swap-AB kernels one nq-row tile; the 128-row kernel has no map
+  // tiles, the others one nq-row tile
   const int tile_rows = a->plan.nq == 256 ? 128 : a->plan.nq;
-  if (a->plan.nq == 128 || tile_rows % g != 0) return;
+  if (tile_rows % g != 0) return;
   cudaPointerAttributes attr;
   if (cudaPointerGetAttributes(&attr, q) != cudaSuccess || attr.type != cudaMemoryTypeDevice) {
     cudaGetLastError();

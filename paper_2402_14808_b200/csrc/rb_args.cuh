@@ -19,8 +19,8 @@ struct SysArgs {
   int* counters;           // int  [n_units], zero between launches
   unsigned long long* debug_ts;  // optional per-CTA %globaltimer stamps [grid][8]
   int defer_merge;         // 1: write every unit part to its slot, no merge, no o_sys
-  int q_tma;               // 1: the 256-row kernel loads query tiles with TMA (tmap_q):
-                           //    q in device memory, g divides 128
+  int q_tma;               // 1: the system kernels load query tiles with TMA (tmap_q):
+                           //    q in device memory, g divides the tile rows
 };
 
 struct KvView {

@@ -672,8 +672,8 @@ static cudaError_t launch_sys(const CUtensorMap& tk, const CUtensorMap& tv, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_system_attention_gqa(const CUtensorMap&, const CUtensorMap&, const SysArgs&,
-                                        cudaStream_t);
+cudaError_t launch_system_attention_gqa(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
+                                        const SysArgs&, cudaStream_t);
 cudaError_t launch_system_attention_gqa2(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&,
                                          const SysArgs&, cudaStream_t);
 
@@ -753,7 +753,7 @@ cudaError_t launch_system_attention(const CUtensorMap& tk, const CUtensorMap& tv
   switch (a.plan.nq) {
     case 16: return launch_sys<16>(tk, tv, tq, a, stream);
     case 32: return launch_sys<32>(tk, tv, tq, a, stream);
-    case 128: return launch_system_attention_gqa(tk, tv, a, stream);
+    case 128: return launch_system_attention_gqa(tk, tv, tq, a, stream);
     case 256: return launch_system_attention_gqa2(tk, tv, tq, a, stream);
     default: return cudaErrorInvalidValue;
   }

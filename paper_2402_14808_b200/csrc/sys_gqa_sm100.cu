@@ -77,7 +77,8 @@ struct Walk {
 
 __global__ void __launch_bounds__(gqa::kThreads, 1)
     sys_gqa_sm100_kernel(const __grid_constant__ CUtensorMap tmap_k,
-                         const __grid_constant__ CUtensorMap tmap_v, const SysArgs args) {
+                         const __grid_constant__ CUtensorMap tmap_v,
+                         const __grid_constant__ CUtensorMap tmap_q, const SysArgs args) {
   using namespace gqa;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
     if ((smem_u32(smem) & 1023) != 0) __trap();
     tma_prefetch_desc(&tmap_k);
     tma_prefetch_desc(&tmap_v);
+    if (args.q_tma) tma_prefetch_desc(&tmap_q);
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -161,11 +163,21 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
         // the unit's 128 query rows (zero past the last row), K-major SW128
         mbar_wait(q_empty, (uq & 1) ^ 1);
         uint8_t* qdst = smem + kOffQ;
-        load_unit_q<kRows, kRows>(qdst, args, h, qt * kRows, lane);
-        cp_async_wait_all();
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(q_full);
+        if (args.q_tma) {
+          // q in device memory, g | 128: two (64 d, g heads, 128 / g requests) boxes
+          if (lane == 0) {
+            mbar_arrive_expect_tx(q_full, kRows * 256);
+            tma_load_3d(qdst, &tmap_q, q_full, 0, h * P.g, qt * kRows / P.g, pol);
+            tma_load_3d(qdst + kRows * 128, &tmap_q, q_full, 64, h * P.g, qt * kRows / P.g, pol);
+          }
+          __syncwarp();
+        } else {
+          load_unit_q<kRows, kRows>(qdst, args, h, qt * kRows, lane);
+          cp_async_wait_all();
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(q_full);
+        }
         ++uq;
       }
     }
@@ -496,13 +508,13 @@ __global__ void __launch_bounds__(gqa::kThreads, 1)
 }
 
 cudaError_t launch_system_attention_gqa(const CUtensorMap& tk, const CUtensorMap& tv,
-                                        const SysArgs& a, cudaStream_t stream) {
+                                        const CUtensorMap& tq, const SysArgs& a, cudaStream_t stream) {
   static_assert(gqa::kBytes <= 232448, "GQA system kernel shared memory over the 227 KB limit");
   cudaError_t e = cudaFuncSetAttribute(sys_gqa_sm100_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, gqa::kBytes);
   if (e != cudaSuccess) return e;
   e = launch_pdl(sys_gqa_sm100_kernel, dim3(a.plan.grid), dim3(gqa::kThreads), gqa::kBytes, stream,
-                 tk, tv, a);
+                 tk, tv, tq, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
